@@ -1,0 +1,222 @@
+/*
+ * gh.h — C ABI of the B200-native Glinthawk two-tier decode path.
+ *
+ * The reference (`tierplan`, /root/reference/proj) has no decode code; its only coupling to
+ * the kernels is (a) the model-shape contract, (b) per-prompt KV sizing, (c) the inter-tier
+ * message byte counts and (d) the per-stage kernel-latency CSV.  Every entry point below cites
+ * the reference symbol it implements or the paper operation it executes (P = PAPER.md).
+ *
+ * Conventions
+ *  - Plain C types only: no torch, no C++ types.  `stream` arguments are `cudaStream_t`
+ *    passed as `void*` (NULL = legacy default stream).  All device pointers are raw.
+ *  - Status codes, never exceptions.  0..3 mirror the reference CLI exit codes
+ *    (proj/include/tierplan/commands.hpp:14-17): OK / internal / validation / feasibility.
+ *    gh_last_error() returns a thread-local message for the last failing call.
+ *  - Ownership: the library owns weights and the KV arena; the caller owns token / position /
+ *    slot arrays, activations and message buffers.  Hot calls never allocate device memory.
+ *  - Threading: a handle is used by one host thread at a time; device work is asynchronous on
+ *    the given stream.  Accounting calls are pure functions (reference S:105-106).
+ *  - Storage dtype = spec.dtype_bytes (4 = fp32, 2 = bf16); compute is fp32 (P:514:
+ *    "Kernel computations run at FP32, while kernel results are stored in the model's native
+ *    data type").
+ *
+ * Message layouts (row-major, token-major, storage dtype; byte counts = PayloadModel,
+ * proj/src/netmodel.cpp:18-24):
+ *    fwd  (Tier-1 -> Tier-2) per token: [ x (D) | q (D) | k (D_kv) | v (D_kv) ]
+ *    bwd  (Tier-2 -> Tier-1) per token: [ x (D) | attn (D) ]
+ *    pp   (Tier-1 -> Tier-1) per token: [ x (D) ]
+ */
+#ifndef GH_GH_H
+#define GH_GH_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define GH_ABI_VERSION 1
+
+typedef enum {
+  GH_OK = 0,
+  GH_EINTERNAL = 1,     /* commands.hpp:14-17 exit 1 */
+  GH_EINVAL = 2,        /* ValidationError, errors.hpp:18-22, exit 2 */
+  GH_EINFEASIBLE = 3,   /* FeasibilityError, errors.hpp:24-32, exit 3 (e.g. KV slots exhausted) */
+  GH_ECUDA = 4,         /* CUDA runtime / driver error (or no device) */
+  GH_ENCCL = 5,         /* NCCL error or NCCL library unavailable */
+  GH_EUNSUPPORTED = 6   /* shape/dtype the kernels do not implement */
+} gh_status;
+
+/* First nine fields = TransformerSpec (proj/include/tierplan/model.hpp:14-28), vocab_size 0 =
+ * absent.  rope_theta / norm_eps are the sidecar hyper-parameters the reference JSON rejects
+ * (model.cpp:92-100) and that the paper leaves to the Llama-2 defaults. */
+typedef struct gh_model_spec {
+  uint64_t n_layers;     /* N    */
+  uint64_t d_model;      /* D    */
+  uint64_t d_kv;         /* D_kv */
+  uint64_t d_hidden;     /* D_h  */
+  uint64_t n_heads;      /* H    */
+  uint64_t n_kv_heads;   /* H_kv */
+  uint64_t max_seq_len;  /* S    */
+  uint64_t dtype_bytes;  /* 4 = fp32, 2 = bf16 */
+  uint64_t vocab_size;   /* V    */
+  float rope_theta;
+  float norm_eps;
+} gh_model_spec;
+
+/* StageKind (proj/include/tierplan/profiles.hpp:13) */
+typedef enum { GH_STAGE_NONATTENTION = 0, GH_STAGE_ATTENTION = 1, GH_STAGE_CLASSIFIER = 2 } gh_stage;
+
+typedef struct gh_tier1 gh_tier1;
+typedef struct gh_tier2 gh_tier2;
+typedef struct gh_engine gh_engine;
+typedef struct gh_comm gh_comm;
+
+/* ------------------------------------------------------------------ misc */
+int gh_abi_version(void);
+const char* gh_last_error(void);
+const char* gh_status_name(gh_status s);
+/* Number of CUDA devices visible (0 on a GPU-less host; never fails). */
+int gh_device_count(void);
+
+/* ------------------------------------------------------------------ accounting (host only)
+ * Bit-identical restatements of the reference's contract functions; tests compare each one
+ * against the reference library compiled from /root/reference (oracle/_ref). */
+gh_status gh_spec_validate(const gh_model_spec* spec);                     /* model.cpp:12-38 */
+gh_status gh_kv_bytes_per_prompt(const gh_model_spec* spec, uint64_t seq_len,
+                                 uint64_t* out);                           /* model.cpp:40-46 */
+gh_status gh_nonattention_footprint(const gh_model_spec* spec, uint64_t batch,
+                                    uint64_t* mem_accesses, uint64_t* flops); /* model.cpp:48-56 */
+gh_status gh_attention_footprint(const gh_model_spec* spec, uint64_t batch, uint64_t seq_len,
+                                 uint64_t* mem_accesses, uint64_t* flops); /* model.cpp:58-67 */
+gh_status gh_weights_bytes(const gh_model_spec* spec, uint64_t* out);    /* model.cpp:69-77 */
+/* out[0] = tier1_to_tier2_per_token, out[1] = tier2_to_tier1_per_token,
+ * out[2] = intra_tier1_per_token (netmodel.cpp:18-24) */
+gh_status gh_payload_bytes(const gh_model_spec* spec, uint64_t out[3]);
+gh_status gh_layer_spans(uint64_t n_layers, uint64_t nodes, uint64_t* spans_out); /* optimizer.cpp:116-123 */
+gh_status gh_node_weight_bytes(const gh_model_spec* spec, uint64_t tier1_nodes,
+                               uint64_t* bytes_out);                       /* optimizer.cpp:125-136 */
+gh_status gh_two_tier_context_slots(const gh_model_spec* spec, uint64_t tier1_nodes,
+                                    uint64_t tier2_per_tier1, uint64_t tier2_memory_per_node,
+                                    uint64_t seq_len, uint64_t* out);      /* optimizer.cpp:175-192 */
+/* Rounded sqrt(2) grid (profiles.cpp:232-245).  Writes at most `cap` entries, *n = full count. */
+gh_status gh_batch_grid(uint64_t max_batch, uint64_t* out, uint64_t cap, uint64_t* n);
+/* Throughput identity B_total*IF/mean(TBT) (des.cpp:298-310); gen_ts in ns. */
+gh_status gh_throughput_from(const int64_t* gen_ts_ns, uint64_t n, uint64_t batch_total,
+                             uint64_t inflight, double* tokens_per_s);
+
+/* ------------------------------------------------------------------ kernel-latency boundary
+ * Writes rows of `device,stage,seq_len,batch_size,latency_us` (profiles.hpp:66-69,
+ * parse_profile profiles.cpp:168-224).  mode "w" writes the header first, "a" appends rows.
+ * Rejects non-positive latency and a stage name outside {nonattention,attention,classifier}. */
+gh_status gh_profile_write_csv(const char* path, const char* mode, const char* device,
+                               gh_stage stage, uint64_t seq_len, const uint64_t* batches,
+                               const double* latency_us, uint64_t n);
+
+/* ------------------------------------------------------------------ Tier-1 (weights; F1, F3, classifier)
+ * Owns layers [layer_begin, layer_end) (a layer_spans block), the embedding when
+ * layer_begin == 0 and the final norm + classifier when layer_end == n_layers.  Weights are
+ * generated on the device from `weight_seed`.
+ * max_batch bounds B for every call (scratch is sized at create time). */
+gh_status gh_tier1_create(const gh_model_spec* spec, int device, uint32_t layer_begin,
+                          uint32_t layer_end, uint64_t weight_seed, uint32_t max_batch,
+                          gh_tier1** out);
+gh_status gh_tier1_destroy(gh_tier1* t1);
+/* x[b,:] = E[tok[b],:]   (tok: device int32 [B]; x: device [B, D]) */
+gh_status gh_tier1_embed(gh_tier1* t1, uint32_t B, const int32_t* tok, void* x, void* stream);
+/* F1: RMSNorm -> x*[Wq|Wk|Wv] -> RoPE(pos) -> msg_fwd [x|q|k|v]  (pos: device int32 [B]) */
+gh_status gh_tier1_pre(gh_tier1* t1, uint32_t layer, uint32_t B, const void* x,
+                       const int32_t* pos, void* msg_fwd, void* stream);
+/* F3: h = attn*Wo + x; x_next = h + W2(silu(W1 rms(h)) * W3 rms(h)).  msg_bwd [x|attn]. */
+gh_status gh_tier1_post(gh_tier1* t1, uint32_t layer, uint32_t B, const void* msg_bwd,
+                        void* x_next, void* stream);
+/* Classifier: RMSNorm -> x*Wcls^T -> greedy argmax (lowest index on ties).
+ * logits (optional, device fp32 [B, V]); next_tok device int32 [B]. */
+gh_status gh_tier1_classify(gh_tier1* t1, uint32_t B, const void* x, float* logits,
+                            int32_t* next_tok, void* stream);
+
+/* ------------------------------------------------------------------ Tier-2 (KV context; F2)
+ * KV arena for layers [layer_begin, layer_end) and n_slots prompts at max_seq_len:
+ * n_slots * 2 * dtype * S * D_kv * span bytes (<= two_tier_context_slots). */
+gh_status gh_tier2_create(const gh_model_spec* spec, int device, uint32_t layer_begin,
+                          uint32_t layer_end, uint32_t n_slots, gh_tier2** out);
+gh_status gh_tier2_destroy(gh_tier2* t2);
+/* F2: append (k,v) of msg_fwd at pos[b] into slot[b], attend over positions
+ * 0..pos[b] with the new key included, write msg_bwd [x|attn].
+ * slot: device uint32 [B]; pos: device int32 [B].  Returns GH_EINFEASIBLE (checked on the
+ * host only when check_host != 0 via gh_tier2_check) for slot >= n_slots or pos >= S. */
+gh_status gh_tier2_attend(gh_tier2* t2, uint32_t layer, uint32_t B, const uint32_t* slot,
+                          const int32_t* pos, const void* msg_fwd, void* msg_bwd, void* stream);
+/* Host-side admission check of a batch (slot < n_slots, 0 <= pos < S). */
+gh_status gh_tier2_check(const gh_tier2* t2, uint32_t B, const uint32_t* slot_host,
+                         const int32_t* pos_host);
+/* Fill positions [0, n_positions) of the given slots (all layers) with synthetic N(0,1)-like
+ * values from `seed` (benchmark pre-fill; content does not change the cost). */
+gh_status gh_tier2_fill_synthetic(gh_tier2* t2, uint64_t seed, uint32_t n_slots_to_fill,
+                                  uint32_t n_positions, void* stream);
+/* Copy one (layer, slot, kv, head) block of positions [0, n) to host (tests). */
+gh_status gh_tier2_read_kv(gh_tier2* t2, uint32_t layer, uint32_t slot, uint32_t kv,
+                           uint32_t head, uint32_t n, void* host_out);
+uint64_t gh_tier2_arena_bytes(const gh_tier2* t2);
+
+/* ------------------------------------------------------------------ NCCL transport
+ * One communicator per process (one process per GPU).  `unique_id` is the 128-byte
+ * ncclUniqueId produced by gh_comm_unique_id on rank 0 and distributed by the caller. */
+gh_status gh_comm_unique_id(uint8_t out[128]);
+gh_status gh_comm_create(const uint8_t unique_id[128], int nranks, int rank, int device,
+                         gh_comm** out);
+/* n_comms communicators at once (ids: n_comms * 128 bytes); the engine's tier split uses one
+ * communicator per in-flight batch so that batches never wait on each other's transfers. */
+gh_status gh_comm_create_n(const uint8_t* unique_ids, int n_comms, int nranks, int rank,
+                           int device, gh_comm** out);
+gh_status gh_comm_destroy(gh_comm* c);
+
+/* ------------------------------------------------------------------ Engine: one decode step
+ * Role of this process:
+ *   - colocated (world 1): Tier-1 for all layers + Tier-2 for all layers on one GPU;
+ *   - tier split (world n >= 2): rank 0 = Tier-1 (all layers, embedding, classifier),
+ *     ranks 1..n-1 = Tier-2 each holding the KV of its prompt shard for all layers.
+ * A step decodes one token for each of the B prompts of every in-flight batch. */
+typedef struct gh_engine_config {
+  gh_model_spec spec;
+  int device;
+  uint64_t weight_seed;
+  uint32_t batch;          /* prompts per in-flight batch (whole Tier-1 batch B*K') */
+  uint32_t inflight;       /* IF in-flight batches (>=1); each has its own slots */
+  uint32_t n_slots;        /* Tier-2 slots on this GPU (0 = exactly what the shard needs) */
+  int use_graph;           /* capture the step in a CUDA graph (colocated only) */
+} gh_engine_config;
+
+gh_status gh_engine_create(const gh_engine_config* cfg, gh_comm* comm, gh_engine** out);
+gh_status gh_engine_destroy(gh_engine* e);
+/* Rank role: 0 = colocated, 1 = tier1, 2 = tier2 */
+int gh_engine_role(const gh_engine* e);
+/* Device-resident step for in-flight batch `ib`: tokens/pos/slots are device arrays owned by
+ * the engine (see gh_engine_io).  next_tok is written on device. */
+gh_status gh_engine_step_device(gh_engine* e, uint32_t ib, void* stream);
+/* End-to-end step through host buffers: copies tok_host/pos_host (pinned or pageable) to the
+ * device, runs the step, copies next tokens (and optionally logits [B,V] fp32) back.
+ * Synchronous on `stream` when it returns.  Tier-2 ranks pass NULLs. */
+gh_status gh_engine_step_host(gh_engine* e, uint32_t ib, const int32_t* tok_host,
+                              const int32_t* pos_host, int32_t* next_host, float* logits_host,
+                              void* stream);
+/* Full step over all in-flight batches, pipelined across batches (tier split) or sequential
+ * (colocated).  Device-resident inputs (engine io buffers). */
+gh_status gh_engine_step_all(gh_engine* e, void* stream);
+/* Device pointers of in-flight batch ib: tok [B] int32, pos [B] int32, slot [B] uint32,
+ * next [B] int32.  Any may be NULL. */
+gh_status gh_engine_io(gh_engine* e, uint32_t ib, int32_t** tok, int32_t** pos,
+                       uint32_t** slot, int32_t** next);
+/* Device-side batch-state update for batch ib: tok <- next, pos += pos_increment (pos_increment
+ * 0 keeps the context length fixed, the steady-state benchmark mode). Tier-1 / colocated only. */
+gh_status gh_engine_advance(gh_engine* e, uint32_t ib, int pos_increment, void* stream);
+gh_tier1* gh_engine_tier1(gh_engine* e);
+gh_tier2* gh_engine_tier2(gh_engine* e);
+/* Launch count of this library's kernels since the last reset (device work accounting). */
+uint64_t gh_kernel_launches(int reset);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* GH_GH_H */

@@ -1,0 +1,272 @@
+// attention.cuh — Tier-2 batched decode attention F2 for sm_100a.
+//
+// One work unit = (prompt b, query head h).  The KV arena is head-major so that the cached
+// keys (and values) of one (slot, kv head) are one contiguous [S_max, d_h] block:
+//
+//   arena[layer][slot][kv ∈ {K, V}][kv_head][position][d_h]         (storage dtype)
+//
+// A persistent CTA per SM walks its units; warp 0 is a TMA producer that streams K and V tiles
+// of TPOS positions with 1-D bulk copies (cp.async.bulk, SASS UBLKCP) into a STAGES-deep
+// shared-memory ring guarded by mbarriers; warps 1..W are consumers that compute scores with
+// 16-byte shared loads and warp-shuffle reductions, run an online (running-max) softmax per
+// warp, and accumulate P·V in fp32 registers.  The W partial states are merged through shared
+// memory at the end of each unit.  The new token's key/value come straight from the Tier-1
+// message (fwd [x|q|k|v]) and are appended to the arena by the same kernel (fused append), so
+// there is no ordering hazard between the append and the bulk loads (which only cover cached
+// positions 0..pos-1).  Output = bwd message [x|attn].
+#pragma once
+#include "common.cuh"
+#include "params.hpp"
+
+namespace gh {
+
+template <typename T, int DH>
+struct AttnCfg {
+  static constexpr int kVec = 16 / sizeof(T);          // elements per 16-byte chunk
+  static constexpr int kChunks = DH / kVec;            // 16-byte chunks per row
+  static constexpr int kLpp = (kChunks % 8 == 0) ? 8 : (kChunks % 4 == 0) ? 4 : (kChunks % 2 == 0) ? 2 : 1;
+  static constexpr int kCpl = kChunks / kLpp;          // chunks per lane
+  static constexpr int kPg = 32 / kLpp;                // positions per warp pass
+  static constexpr int kW = 8;                         // consumer warps
+  static constexpr int kTpos = (kW * kPg > 64) ? kW * kPg : 64;  // positions per stage
+  static constexpr int kPasses = kTpos / (kW * kPg);
+  static constexpr int kTileBytes = kTpos * DH * (int)sizeof(T);
+  static constexpr int kStages = (196608 / (2 * kTileBytes)) > 6 ? 6 : (196608 / (2 * kTileBytes));
+  static constexpr int kThreads = 32 * (1 + kW);
+  static constexpr int kEl = kCpl * kVec;              // elements per lane
+  static constexpr int kCombOffset = kStages * 2 * kTileBytes;
+  static constexpr int kCombBytes = kW * (DH + 2) * 4;
+  static constexpr int kBarOffset = kCombOffset + ((kCombBytes + 127) / 128) * 128;
+  static constexpr int kSmem = kBarOffset + 2 * kStages * 8 + 16;
+  static_assert(kChunks * kVec == DH, "d_head must be a multiple of 16 bytes");
+};
+
+// 16-byte chunk -> kVec floats
+template <typename T> GH_DEV void chunk_to_f32(const uint4& c, float* f);
+template <> GH_DEV void chunk_to_f32<float>(const uint4& c, float* f) {
+  f[0] = __uint_as_float(c.x); f[1] = __uint_as_float(c.y);
+  f[2] = __uint_as_float(c.z); f[3] = __uint_as_float(c.w);
+}
+template <> GH_DEV void chunk_to_f32<bf16_t>(const uint4& c, float* f) {
+  const uint32_t w[4] = {c.x, c.y, c.z, c.w};
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    f[2 * i] = __uint_as_float(w[i] << 16);
+    f[2 * i + 1] = __uint_as_float(w[i] & 0xffff0000u);
+  }
+}
+
+template <typename T, int DH>
+__global__ void __launch_bounds__(AttnCfg<T, DH>::kThreads, 1)
+    attn_decode_kernel(const AttnArgs a) {
+  using C = AttnCfg<T, DH>;
+  extern __shared__ __align__(128) uint8_t smem[];
+  uint64_t* full = (uint64_t*)(smem + C::kBarOffset);
+  uint64_t* empty = full + C::kStages;
+  float* comb = (float*)(smem + C::kCombOffset);
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const int n_units = a.B * a.H;
+  const int group = a.H / a.Hkv;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < C::kStages; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], C::kW); }
+    fence_barrier_init();
+  }
+  __syncthreads();
+
+  const T* fwd = (const T*)a.msg_fwd;
+  T* bwd = (T*)a.msg_bwd;
+  T* arena = (T*)a.arena;
+  const long ld_fwd = 2L * a.D + 2L * a.Dkv;
+  const long ld_bwd = 2L * a.D;
+
+  if (warp == 0) {
+    // ------------------------------------------------ producer
+    if (elect_one()) {
+      const uint64_t pol = policy_evict_first();
+      uint32_t it = 0;
+      for (int u = blockIdx.x; u < n_units; u += gridDim.x) {
+        const int b = u / a.H, h = u % a.H, kvh = h / group;
+        const int L = a.pos[b];
+        const T* kbase = arena + (long)a.slot[b] * a.slot_stride + (long)kvh * a.head_stride;
+        const T* vbase = kbase + a.kv_stride;
+        for (int p0 = 0; p0 < L; p0 += C::kTpos, ++it) {
+          const int s = it % C::kStages;
+          const uint32_t ph = (it / C::kStages) & 1;
+          mbar_wait(&empty[s], ph ^ 1);
+          const int np = min(C::kTpos, L - p0);
+          const uint32_t bytes = (uint32_t)np * DH * sizeof(T);
+          uint8_t* sk = smem + s * 2 * C::kTileBytes;
+          mbar_arrive_expect_tx(&full[s], 2 * bytes);
+          bulk_g2s(sk, kbase + (long)p0 * DH, bytes, &full[s], pol);
+          bulk_g2s(sk + C::kTileBytes, vbase + (long)p0 * DH, bytes, &full[s], pol);
+        }
+      }
+    }
+    return;
+  }
+
+  // -------------------------------------------------- consumers
+  const int cw = warp - 1;
+  const int grp = lane / C::kLpp;
+  const int sub = lane % C::kLpp;
+  uint32_t it = 0;
+
+  for (int u = blockIdx.x; u < n_units; u += gridDim.x) {
+    const int b = u / a.H, h = u % a.H, kvh = h / group;
+    const int L = a.pos[b];
+    const T* qrow = fwd + (long)b * ld_fwd + a.D + (long)h * DH;
+
+    float q[C::kEl], o[C::kEl];
+#pragma unroll
+    for (int j = 0; j < C::kCpl; ++j) {
+      uint4 c = *(const uint4*)(qrow + (sub + j * C::kLpp) * C::kVec);
+      chunk_to_f32<T>(c, q + j * C::kVec);
+    }
+#pragma unroll
+    for (int e = 0; e < C::kEl; ++e) { q[e] *= a.scale_log2; o[e] = 0.f; }
+    float m = -INFINITY;  // warp-uniform running max (log2 domain)
+    float l = 0.f;        // per-group partial sum
+
+    if (cw == 0) {
+      // new token: score from the message, append k/v to the arena (group 0 lanes)
+      const T* krow = fwd + (long)b * ld_fwd + 2L * a.D + (long)kvh * DH;
+      const T* vrow = krow + a.Dkv;
+      T* kdst = arena + (long)a.slot[b] * a.slot_stride + (long)kvh * a.head_stride + (long)L * DH;
+      T* vdst = kdst + a.kv_stride;
+      float part = 0.f;
+      float vf[C::kEl];
+#pragma unroll
+      for (int j = 0; j < C::kCpl; ++j) {
+        const int off = (sub + j * C::kLpp) * C::kVec;
+        uint4 kc = *(const uint4*)(krow + off);
+        uint4 vc = *(const uint4*)(vrow + off);
+        if (grp == 0 && (h % group) == 0) {  // one writer per kv head
+          *(uint4*)(kdst + off) = kc;
+          *(uint4*)(vdst + off) = vc;
+        }
+        float kf[C::kVec];
+        chunk_to_f32<T>(kc, kf);
+        chunk_to_f32<T>(vc, vf + j * C::kVec);
+#pragma unroll
+        for (int e = 0; e < C::kVec; ++e) part = fmaf(q[j * C::kVec + e], kf[e], part);
+      }
+#pragma unroll
+      for (int o2 = C::kLpp / 2; o2 > 0; o2 >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o2);
+      m = part;  // identical in every group; only group 0 keeps mass
+      if (grp == 0) {
+        l = 1.f;
+#pragma unroll
+        for (int e = 0; e < C::kEl; ++e) o[e] = vf[e];
+      }
+    }
+
+    for (int p0 = 0; p0 < L; p0 += C::kTpos, ++it) {
+      const int s = it % C::kStages;
+      const uint32_t ph = (it / C::kStages) & 1;
+      const int np = min(C::kTpos, L - p0);
+      mbar_wait(&full[s], ph);
+      const T* sk = (const T*)(smem + s * 2 * C::kTileBytes);
+      const T* sv = (const T*)(smem + s * 2 * C::kTileBytes + C::kTileBytes);
+
+      float sc[C::kPasses];
+      float mx = -INFINITY;
+#pragma unroll
+      for (int ps = 0; ps < C::kPasses; ++ps) {
+        const int r = ps * C::kW * C::kPg + cw * C::kPg + grp;
+        float part = 0.f;
+        if (r < np) {
+#pragma unroll
+          for (int j = 0; j < C::kCpl; ++j) {
+            uint4 kc = *(const uint4*)(sk + r * DH + (sub + j * C::kLpp) * C::kVec);
+            float kf[C::kVec];
+            chunk_to_f32<T>(kc, kf);
+#pragma unroll
+            for (int e = 0; e < C::kVec; ++e) part = fmaf(q[j * C::kVec + e], kf[e], part);
+          }
+        }
+#pragma unroll
+        for (int o2 = C::kLpp / 2; o2 > 0; o2 >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o2);
+        sc[ps] = (r < np) ? part : -INFINITY;
+        mx = fmaxf(mx, sc[ps]);
+      }
+#pragma unroll
+      for (int o2 = C::kLpp; o2 < 32; o2 <<= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o2));
+      if (mx != -INFINITY) {
+        const float mn = fmaxf(m, mx);
+        const float corr = (m == -INFINITY) ? 0.f : exp2f(m - mn);
+        l *= corr;
+#pragma unroll
+        for (int e = 0; e < C::kEl; ++e) o[e] *= corr;
+#pragma unroll
+        for (int ps = 0; ps < C::kPasses; ++ps) {
+          const int r = ps * C::kW * C::kPg + cw * C::kPg + grp;
+          if (r < np) {
+            const float p = exp2f(sc[ps] - mn);
+            l += p;
+#pragma unroll
+            for (int j = 0; j < C::kCpl; ++j) {
+              uint4 vc = *(const uint4*)(sv + r * DH + (sub + j * C::kLpp) * C::kVec);
+              float vf[C::kVec];
+              chunk_to_f32<T>(vc, vf);
+#pragma unroll
+              for (int e = 0; e < C::kVec; ++e) o[j * C::kVec + e] = fmaf(p, vf[e], o[j * C::kVec + e]);
+            }
+          }
+        }
+        m = mn;
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[s]);
+    }
+
+    // merge the groups of this warp (m is warp-uniform)
+#pragma unroll
+    for (int o2 = C::kLpp; o2 < 32; o2 <<= 1) {
+      l += __shfl_xor_sync(0xffffffffu, l, o2);
+#pragma unroll
+      for (int e = 0; e < C::kEl; ++e) o[e] += __shfl_xor_sync(0xffffffffu, o[e], o2);
+    }
+    float* cwbuf = comb + cw * (DH + 2);
+    if (grp == 0) {
+#pragma unroll
+      for (int j = 0; j < C::kCpl; ++j)
+#pragma unroll
+        for (int e = 0; e < C::kVec; ++e) cwbuf[(sub + j * C::kLpp) * C::kVec + e] = o[j * C::kVec + e];
+    }
+    if (lane == 0) { cwbuf[DH] = m; cwbuf[DH + 1] = l; }
+    asm volatile("bar.sync 1, %0;\n" ::"r"(C::kW * 32) : "memory");
+    {
+      const int t = threadIdx.x - 32;
+      float M = -INFINITY;
+#pragma unroll
+      for (int w = 0; w < C::kW; ++w) M = fmaxf(M, comb[w * (DH + 2) + DH]);
+      float den = 0.f;
+      float f[C::kW];
+#pragma unroll
+      for (int w = 0; w < C::kW; ++w) {
+        const float mw = comb[w * (DH + 2) + DH];
+        f[w] = (mw == -INFINITY) ? 0.f : exp2f(mw - M);
+        den += comb[w * (DH + 2) + DH + 1] * f[w];
+      }
+      const float inv = 1.f / den;
+      T* orow = bwd + (long)b * ld_bwd + a.D + (long)h * DH;
+      for (int d = t; d < DH; d += C::kW * 32) {
+        float acc = 0.f;
+#pragma unroll
+        for (int w = 0; w < C::kW; ++w) acc += comb[w * (DH + 2) + d] * f[w];
+        St<T>::store(orow, d, acc * inv);
+      }
+      if (h == 0) {  // pass the residual stream through: bwd.x = fwd.x
+        const uint4* xs = (const uint4*)(fwd + (long)b * ld_fwd);
+        uint4* xd = (uint4*)(bwd + (long)b * ld_bwd);
+        for (int i = t; i < a.D / C::kVec; i += C::kW * 32) xd[i] = xs[i];
+      }
+    }
+    asm volatile("bar.sync 1, %0;\n" ::"r"(C::kW * 32) : "memory");
+  }
+}
+
+}  // namespace gh

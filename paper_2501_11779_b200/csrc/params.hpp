@@ -1,0 +1,52 @@
+// params.hpp — plain-old-data launch parameters shared by host code and the sm_100a kernels.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace gh {
+
+enum EpiKind : int {
+  EPI_STORE = 0,         // out[b, n] = acc
+  EPI_STORE_RESID = 1,   // out[b, n] = acc + resid[b, n]
+  EPI_QKV_ROPE = 2,      // msg_fwd[b, D + n] = rope(acc) for q/k rows, acc for v rows
+  EPI_SWIGLU = 3,        // rows interleaved (gate_f, up_f): out[b, f] = silu(gate) * up
+  EPI_LOGITS_ARGMAX = 4  // logits[b, n] = acc (optional); per-tile (max, argmax) over n
+};
+
+struct EpiParams {
+  int kind;
+  void* out;            // output base (storage type T_out: bf16 except logits fp32)
+  long ldo;             // output row stride (elements)
+  const void* resid;    // residual base (same storage type as out)
+  long ldr;
+  const float2* rope;   // [max_seq][d_head/2] (cos, sin)
+  const int* pos;       // [B]
+  int d_head;
+  int rope_rows;        // leading output rows (q and k) that receive RoPE
+  float* logits;        // [B][ldl] fp32 (optional)
+  long ldl;
+  float2* part;         // [n_tiles][Bt] (max value, argmax index as float bits)
+};
+
+struct GemmShape {
+  int N, K, Bt;         // weight rows, reduction length, batch
+  int ks;               // K splits (>= 1)
+  int kb_total;         // ceil(K / 64)
+  float* ws;            // split workspace (ks > 1)
+  int* tickets;         // per output tile counters (ks > 1), zero between launches
+};
+
+struct AttnArgs {
+  const void* msg_fwd;  // [B][2D + 2Dkv]
+  void* msg_bwd;        // [B][2D]
+  void* arena;          // layer base
+  const uint32_t* slot; // [B]
+  const int* pos;       // [B]  (cached positions before the new token)
+  long slot_stride;     // elements per slot (= 2 * Hkv * S * DH)
+  long kv_stride;       // elements between K and V blocks (= Hkv * S * DH)
+  long head_stride;     // elements per kv head (= S * DH)
+  int B, H, Hkv, D, Dkv;
+  float scale_log2;     // log2(e) / sqrt(DH)
+};
+
+}  // namespace gh

@@ -1,0 +1,853 @@
+// runtime.cpp — Tier-1 / Tier-2 stage objects, the NCCL transport and the decode engine
+// behind the C ABI (include/gh/gh.h).
+//
+// Stage taxonomy follows the reference (proj/include/tierplan/profiles.hpp:13):
+//   nonattention = gh_tier1_pre (F1) + gh_tier1_post (F3)      on the weight-holding GPU
+//   attention    = gh_tier2_attend (F2)                         on the KV-holding GPU
+//   classifier   = gh_tier1_classify
+// Messages between the stages use the PayloadModel byte layout (netmodel.cpp:18-24).
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <dlfcn.h>
+#include <nccl.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <map>
+#include <memory>
+#include <mutex>
+#include <string>
+#include <tuple>
+#include <vector>
+
+#include "params.hpp"
+#include "common.cuh"
+#include "gh/gh.h"
+#include "internal.hpp"
+#include "kernels.hpp"
+
+namespace gh {
+
+static thread_local std::string g_last_error;
+void set_error(const std::string& msg) { g_last_error = msg; }
+
+// ---------------------------------------------------------------- derived shape
+struct Shape {
+  gh_model_spec s{};
+  int N = 0, D = 0, Dkv = 0, Dh = 0, H = 0, Hkv = 0, S = 0, V = 0, dh = 0, db = 0;
+  static gh_status from(const gh_model_spec* spec, Shape* out) {
+    GH_TRY(gh_spec_validate(spec));
+    Shape x;
+    x.s = *spec;
+    x.N = (int)spec->n_layers; x.D = (int)spec->d_model; x.Dkv = (int)spec->d_kv;
+    x.Dh = (int)spec->d_hidden; x.H = (int)spec->n_heads; x.Hkv = (int)spec->n_kv_heads;
+    x.S = (int)spec->max_seq_len; x.V = (int)spec->vocab_size; x.db = (int)spec->dtype_bytes;
+    x.dh = x.D / x.H;
+    if (x.db != 2 && x.db != 4) return fail(GH_EUNSUPPORTED, "kernels implement dtype_bytes 2 (bf16) and 4 (fp32)");
+    if (x.Dkv / x.Hkv != x.dh) return fail(GH_EUNSUPPORTED, "query and kv head dims differ (d_model/n_heads != d_kv/n_kv_heads)");
+    if (x.H % x.Hkv != 0) return fail(GH_EUNSUPPORTED, "n_heads must be a multiple of n_kv_heads");
+    if (!attention_supported(x.db, x.dh)) return fail(GH_EUNSUPPORTED, "head dim must be 48, 64 or 128");
+    if (x.dh % 2) return fail(GH_EUNSUPPORTED, "RoPE needs an even head dim");
+    if ((x.D * x.db) % 16 || (x.Dkv * x.db) % 16) return fail(GH_EUNSUPPORTED, "rows must be 16-byte multiples");
+    *out = x;
+    return GH_OK;
+  }
+  long ld_fwd() const { return 2L * D + 2L * Dkv; }
+  long ld_bwd() const { return 2L * D; }
+};
+
+struct DevMem {
+  void* p = nullptr;
+  ~DevMem() { if (p) cudaFree(p); }
+};
+
+static gh_status dev_alloc(std::vector<std::unique_ptr<DevMem>>& pool, size_t bytes, void** out) {
+  auto m = std::make_unique<DevMem>();
+  if (bytes == 0) bytes = 16;
+  cudaError_t e = cudaMalloc(&m->p, bytes);
+  if (e != cudaSuccess)
+    return fail(e == cudaErrorMemoryAllocation ? GH_EINFEASIBLE : GH_ECUDA,
+                "cudaMalloc(" + std::to_string(bytes) + "): " + cudaGetErrorString(e));
+  *out = m->p;
+  pool.push_back(std::move(m));
+  return GH_OK;
+}
+
+// cache of tensor maps over activation buffers: key (ptr, rows, cols, ld, box)
+struct TmapCache {
+  std::map<std::tuple<const void*, uint64_t, uint64_t, uint64_t, uint32_t>, CUtensorMap> m;
+  gh_status get(const void* p, uint64_t rows, uint64_t cols, uint64_t ld, uint32_t box, CUtensorMap** out) {
+    auto key = std::make_tuple(p, rows, cols, ld, box);
+    auto it = m.find(key);
+    if (it == m.end()) {
+      CUtensorMap t;
+      cudaError_t e = make_tmap_bf16(&t, p, rows, cols, ld, box);
+      if (e != cudaSuccess) return fail(GH_ECUDA, "cuTensorMapEncodeTiled failed (activation)");
+      it = m.emplace(key, t).first;
+    }
+    *out = &it->second;
+    return GH_OK;
+  }
+};
+
+}  // namespace gh
+
+using namespace gh;
+
+// ================================================================== Tier-1
+struct gh_tier1 {
+  Shape sh;
+  int device = 0;
+  uint32_t l0 = 0, l1 = 0, max_batch = 0;
+  std::vector<std::unique_ptr<DevMem>> mem;
+  struct Layer {
+    Weight qkv, o, w13, w2;
+    CUtensorMap tm_qkv, tm_o, tm_13, tm_2;
+    void* attn_norm = nullptr;
+    void* ffn_norm = nullptr;
+  };
+  std::vector<Layer> layers;
+  bool has_embed = false, has_cls = false;
+  Weight embed, cls;
+  CUtensorMap tm_cls;
+  void* final_norm = nullptr;
+  float2* rope = nullptr;
+  void *xn = nullptr, *h = nullptr, *hn = nullptr, *g = nullptr;
+  float2* part = nullptr;
+  GemmScratch gsc;
+  TmapCache tmaps;
+  std::map<std::tuple<int, int, int>, GemmPlan> plans;
+
+  const GemmPlan& plan(int N, int K, int B) {
+    auto key = std::make_tuple(N, K, B);
+    auto it = plans.find(key);
+    if (it == plans.end()) it = plans.emplace(key, plan_gemm(N, K, B)).first;
+    return it->second;
+  }
+  // X: [B, K] with row stride ldx
+  gh_status gemm(const Weight& W, const CUtensorMap* tmW, const void* X, long ldx, int B,
+                 const EpiParams& ep, cudaStream_t st) {
+    const GemmPlan& p = plan(W.N, W.K, B);
+    CUtensorMap* tmX = nullptr;
+    if (sh.db == 2) GH_TRY(tmaps.get(X, (uint64_t)B, (uint64_t)W.K, (uint64_t)ldx, (uint32_t)p.BN, &tmX));
+    GH_CUDA(launch_gemm(W, tmW, X, ldx, tmX, B, p, ep, gsc, st));
+    return GH_OK;
+  }
+};
+
+static EpiParams epi_default() {
+  EpiParams e;
+  memset(&e, 0, sizeof(e));
+  return e;
+}
+
+static gh_status init_weight(gh_tier1* t, Weight* w, int N, int K, CUtensorMap* tm) {
+  w->N = N; w->K = K; w->dtype_bytes = t->sh.db;
+  GH_TRY(dev_alloc(t->mem, (size_t)N * K * t->sh.db, &w->ptr));
+  if (tm && t->sh.db == 2) {
+    cudaError_t e = make_tmap_bf16(tm, w->ptr, (uint64_t)N, (uint64_t)K, (uint64_t)K, 128);
+    if (e != cudaSuccess) return fail(GH_ECUDA, "cuTensorMapEncodeTiled failed (weights)");
+  }
+  return GH_OK;
+}
+
+extern "C" {
+
+int gh_abi_version(void) { return GH_ABI_VERSION; }
+const char* gh_last_error(void) { return g_last_error.c_str(); }
+const char* gh_status_name(gh_status s) {
+  switch (s) {
+    case GH_OK: return "GH_OK";
+    case GH_EINTERNAL: return "GH_EINTERNAL";
+    case GH_EINVAL: return "GH_EINVAL";
+    case GH_EINFEASIBLE: return "GH_EINFEASIBLE";
+    case GH_ECUDA: return "GH_ECUDA";
+    case GH_ENCCL: return "GH_ENCCL";
+    case GH_EUNSUPPORTED: return "GH_EUNSUPPORTED";
+  }
+  return "GH_UNKNOWN";
+}
+int gh_device_count(void) {
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess) { cudaGetLastError(); return 0; }
+  return n;
+}
+uint64_t gh_kernel_launches(int reset) {
+  uint64_t v = launch_counter();
+  if (reset) launch_counter() = 0;
+  return v;
+}
+
+gh_status gh_tier1_create(const gh_model_spec* spec, int device, uint32_t layer_begin,
+                          uint32_t layer_end, uint64_t seed, uint32_t max_batch, gh_tier1** out) {
+  if (!out) return fail(GH_EINVAL, "out is null");
+  *out = nullptr;
+  Shape sh;
+  GH_TRY(Shape::from(spec, &sh));
+  if (layer_begin >= layer_end || layer_end > (uint32_t)sh.N) return fail(GH_EINVAL, "bad layer range");
+  if (max_batch == 0) return fail(GH_EINVAL, "max_batch must be >= 1");
+  if (sh.V == 0) return fail(GH_EINVAL, "vocab_size required for Tier-1");
+  if (gh_device_count() <= device) return fail(GH_ECUDA, "no CUDA device " + std::to_string(device));
+  GH_CUDA(cudaSetDevice(device));
+  GH_CUDA(configure_kernels());
+  auto t = std::make_unique<gh_tier1>();
+  t->sh = sh; t->device = device; t->l0 = layer_begin; t->l1 = layer_end; t->max_batch = max_batch;
+  const int D = sh.D, Dkv = sh.Dkv, Dh = sh.Dh, V = sh.V, db = sh.db;
+  cudaStream_t st = 0;
+  t->layers.resize(layer_end - layer_begin);
+  for (uint32_t l = layer_begin; l < layer_end; ++l) {
+    auto& L = t->layers[l - layer_begin];
+    GH_TRY(init_weight(t.get(), &L.qkv, D + 2 * Dkv, D, &L.tm_qkv));
+    GH_TRY(init_weight(t.get(), &L.o, D, D, &L.tm_o));
+    GH_TRY(init_weight(t.get(), &L.w13, 2 * Dh, D, &L.tm_13));
+    GH_TRY(init_weight(t.get(), &L.w2, D, Dh, &L.tm_2));
+    const double sD = 1.0 / std::sqrt((double)D), sH = 1.0 / std::sqrt((double)Dh);
+    char* q = (char*)L.qkv.ptr;
+    GH_CUDA(launch_init_matrix(db, q, seed, tid_layer(l, kWq), D, D, sD, st));
+    GH_CUDA(launch_init_matrix(db, q + (size_t)D * D * db, seed, tid_layer(l, kWk), Dkv, D, sD, st));
+    GH_CUDA(launch_init_matrix(db, q + (size_t)(D + Dkv) * D * db, seed, tid_layer(l, kWv), Dkv, D, sD, st));
+    GH_CUDA(launch_init_matrix(db, L.o.ptr, seed, tid_layer(l, kWo), D, D, sD, st));
+    GH_CUDA(launch_init_interleaved(db, L.w13.ptr, seed, tid_layer(l, kW1), tid_layer(l, kW3), Dh, D, sD, st));
+    GH_CUDA(launch_init_matrix(db, L.w2.ptr, seed, tid_layer(l, kW2), D, Dh, sH, st));
+    GH_TRY(dev_alloc(t->mem, (size_t)D * db, &L.attn_norm));
+    GH_TRY(dev_alloc(t->mem, (size_t)D * db, &L.ffn_norm));
+    GH_CUDA(launch_fill_const(db, L.attn_norm, D, 1.0f, st));
+    GH_CUDA(launch_fill_const(db, L.ffn_norm, D, 1.0f, st));
+  }
+  t->has_embed = layer_begin == 0;
+  t->has_cls = layer_end == (uint32_t)sh.N;
+  if (t->has_embed) {
+    GH_TRY(init_weight(t.get(), &t->embed, V, D, nullptr));
+    GH_CUDA(launch_init_matrix(db, t->embed.ptr, seed, kTidEmbed, V, D, 1.0, st));
+  }
+  if (t->has_cls) {
+    GH_TRY(init_weight(t.get(), &t->cls, V, D, &t->tm_cls));
+    GH_CUDA(launch_init_matrix(db, t->cls.ptr, seed, kTidCls, V, D, 1.0 / std::sqrt((double)D), st));
+    GH_TRY(dev_alloc(t->mem, (size_t)D * db, &t->final_norm));
+    GH_CUDA(launch_fill_const(db, t->final_norm, D, 1.0f, st));
+  }
+  // RoPE table (cos, sin) computed in double on the host: [S][dh/2]
+  {
+    const int half = sh.dh / 2;
+    std::vector<float2> tab((size_t)sh.S * half);
+    for (int p = 0; p < sh.S; ++p)
+      for (int i = 0; i < half; ++i) {
+        const double freq = std::pow((double)spec->rope_theta, -2.0 * i / (double)sh.dh);
+        const double a = (double)p * freq;
+        tab[(size_t)p * half + i] = make_float2((float)std::cos(a), (float)std::sin(a));
+      }
+    void* r;
+    GH_TRY(dev_alloc(t->mem, tab.size() * sizeof(float2), &r));
+    GH_CUDA(cudaMemcpy(r, tab.data(), tab.size() * sizeof(float2), cudaMemcpyHostToDevice));
+    t->rope = (float2*)r;
+  }
+  // scratch
+  const size_t B = max_batch;
+  GH_TRY(dev_alloc(t->mem, B * D * db, &t->xn));
+  GH_TRY(dev_alloc(t->mem, B * D * db, &t->h));
+  GH_TRY(dev_alloc(t->mem, B * D * db, &t->hn));
+  GH_TRY(dev_alloc(t->mem, B * Dh * db, &t->g));
+  {
+    void* p;
+    const size_t n_tiles = (V + 127) / 128;
+    GH_TRY(dev_alloc(t->mem, n_tiles * B * sizeof(float2), &p));
+    t->part = (float2*)p;
+  }
+  size_t ws = 0, tk = 0;
+  const int NK[5][2] = {{D + 2 * Dkv, D}, {D, D}, {2 * Dh, D}, {D, Dh}, {V, D}};
+  for (uint32_t b = 1; b <= max_batch; ++b)
+    for (auto& nk : NK) {
+      GemmPlan p = plan_gemm(nk[0], nk[1], (int)b);
+      ws = std::max(ws, p.ws_floats);
+      tk = std::max(tk, p.tickets);
+    }
+  if (db == 2) {
+    void* p;
+    t->gsc.ws_floats = ws;
+    GH_TRY(dev_alloc(t->mem, std::max<size_t>(ws, 4) * sizeof(float), &p));
+    t->gsc.ws = (float*)p;
+    t->gsc.n_tickets = tk;
+    GH_TRY(dev_alloc(t->mem, std::max<size_t>(tk, 1) * sizeof(int), &p));
+    t->gsc.tickets = (int*)p;
+    GH_CUDA(cudaMemset(p, 0, std::max<size_t>(tk, 1) * sizeof(int)));
+  } else {
+    void* p;
+    const size_t n = B * (size_t)std::max({D + 2 * Dkv, 2 * Dh, V, D});
+    GH_TRY(dev_alloc(t->mem, n * sizeof(float), &p));
+    t->gsc.stage = (float*)p;
+    t->gsc.stage_floats = n;
+  }
+  GH_CUDA(cudaDeviceSynchronize());
+  *out = t.release();
+  return GH_OK;
+}
+
+gh_status gh_tier1_destroy(gh_tier1* t) {
+  if (t) { cudaSetDevice(t->device); cudaDeviceSynchronize(); delete t; }
+  return GH_OK;
+}
+
+gh_status gh_tier1_embed(gh_tier1* t, uint32_t B, const int32_t* tok, void* x, void* stream) {
+  if (!t || !tok || !x) return fail(GH_EINVAL, "null argument");
+  if (!t->has_embed) return fail(GH_EINVAL, "this Tier-1 span does not own the embedding");
+  if (B > t->max_batch) return fail(GH_EINVAL, "B exceeds max_batch");
+  GH_CUDA(launch_embed(t->sh.db, t->embed.ptr, tok, x, (int)B, t->sh.D, t->sh.V, (cudaStream_t)stream));
+  return GH_OK;
+}
+
+gh_status gh_tier1_pre(gh_tier1* t, uint32_t layer, uint32_t B, const void* x, const int32_t* pos,
+                       void* msg_fwd, void* stream) {
+  if (!t || !x || !pos || !msg_fwd) return fail(GH_EINVAL, "null argument");
+  if (layer < t->l0 || layer >= t->l1) return fail(GH_EINVAL, "layer not owned by this Tier-1");
+  if (B > t->max_batch) return fail(GH_EINVAL, "B exceeds max_batch");
+  if (B == 0) return GH_OK;
+  cudaStream_t st = (cudaStream_t)stream;
+  const Shape& s = t->sh;
+  auto& L = t->layers[layer - t->l0];
+  // RMSNorm(x) -> xn ; x copied into the message's x slot
+  GH_CUDA(launch_rmsnorm(s.db, x, s.D, L.attn_norm, t->xn, s.D, msg_fwd, s.ld_fwd(), (int)B, s.D,
+                         s.s.norm_eps, st));
+  EpiParams ep = epi_default();
+  ep.kind = EPI_QKV_ROPE;
+  ep.out = (char*)msg_fwd + (size_t)s.D * s.db;
+  ep.ldo = s.ld_fwd();
+  ep.rope = t->rope;
+  ep.pos = pos;
+  ep.d_head = s.dh;
+  ep.rope_rows = s.D + s.Dkv;
+  return t->gemm(L.qkv, &L.tm_qkv, t->xn, s.D, (int)B, ep, st);
+}
+
+gh_status gh_tier1_post(gh_tier1* t, uint32_t layer, uint32_t B, const void* msg_bwd, void* x_next,
+                        void* stream) {
+  if (!t || !msg_bwd || !x_next) return fail(GH_EINVAL, "null argument");
+  if (layer < t->l0 || layer >= t->l1) return fail(GH_EINVAL, "layer not owned by this Tier-1");
+  if (B > t->max_batch) return fail(GH_EINVAL, "B exceeds max_batch");
+  if (B == 0) return GH_OK;
+  cudaStream_t st = (cudaStream_t)stream;
+  const Shape& s = t->sh;
+  auto& L = t->layers[layer - t->l0];
+  // h = attn Wo^T + x
+  EpiParams ep = epi_default();
+  ep.kind = EPI_STORE_RESID;
+  ep.out = t->h; ep.ldo = s.D;
+  ep.resid = msg_bwd; ep.ldr = s.ld_bwd();
+  GH_TRY(t->gemm(L.o, &L.tm_o, (const char*)msg_bwd + (size_t)s.D * s.db, s.ld_bwd(), (int)B, ep, st));
+  // hn = RMSNorm(h)
+  GH_CUDA(launch_rmsnorm(s.db, t->h, s.D, L.ffn_norm, t->hn, s.D, nullptr, 0, (int)B, s.D, s.s.norm_eps, st));
+  // g = silu(hn W1^T) * (hn W3^T)
+  ep = epi_default();
+  ep.kind = EPI_SWIGLU;
+  ep.out = t->g; ep.ldo = s.Dh;
+  GH_TRY(t->gemm(L.w13, &L.tm_13, t->hn, s.D, (int)B, ep, st));
+  // x_next = g W2^T + h
+  ep = epi_default();
+  ep.kind = EPI_STORE_RESID;
+  ep.out = x_next; ep.ldo = s.D;
+  ep.resid = t->h; ep.ldr = s.D;
+  return t->gemm(L.w2, &L.tm_2, t->g, s.Dh, (int)B, ep, st);
+}
+
+gh_status gh_tier1_classify(gh_tier1* t, uint32_t B, const void* x, float* logits, int32_t* next,
+                            void* stream) {
+  if (!t || !x || !next) return fail(GH_EINVAL, "null argument");
+  if (!t->has_cls) return fail(GH_EINVAL, "this Tier-1 span does not own the classifier");
+  if (B > t->max_batch) return fail(GH_EINVAL, "B exceeds max_batch");
+  if (B == 0) return GH_OK;
+  cudaStream_t st = (cudaStream_t)stream;
+  const Shape& s = t->sh;
+  GH_CUDA(launch_rmsnorm(s.db, x, s.D, t->final_norm, t->xn, s.D, nullptr, 0, (int)B, s.D, s.s.norm_eps, st));
+  EpiParams ep = epi_default();
+  ep.kind = EPI_LOGITS_ARGMAX;
+  ep.logits = logits; ep.ldl = s.V;
+  ep.part = t->part;
+  GH_TRY(t->gemm(t->cls, &t->tm_cls, t->xn, s.D, (int)B, ep, st));
+  if (s.db == 2) {
+    GH_CUDA(launch_argmax_final(t->part, (s.V + 127) / 128, (int)B, next, st));
+  } else {
+    GH_CUDA(launch_argmax_rows(logits ? logits : t->gsc.stage, (int)B, s.V, next, st));
+  }
+  return GH_OK;
+}
+
+}  // extern "C"
+
+// ================================================================== Tier-2
+struct gh_tier2 {
+  Shape sh;
+  int device = 0;
+  uint32_t l0 = 0, l1 = 0, n_slots = 0;
+  std::vector<std::unique_ptr<DevMem>> mem;
+  void* arena = nullptr;
+  size_t arena_bytes = 0;
+  long slot_stride() const { return 2L * sh.Hkv * sh.S * sh.dh; }
+  long layer_stride() const { return (long)n_slots * slot_stride(); }
+};
+
+extern "C" {
+
+gh_status gh_tier2_create(const gh_model_spec* spec, int device, uint32_t layer_begin,
+                          uint32_t layer_end, uint32_t n_slots, gh_tier2** out) {
+  if (!out) return fail(GH_EINVAL, "out is null");
+  *out = nullptr;
+  Shape sh;
+  GH_TRY(Shape::from(spec, &sh));
+  if (layer_begin >= layer_end || layer_end > (uint32_t)sh.N) return fail(GH_EINVAL, "bad layer range");
+  if (n_slots == 0) return fail(GH_EINVAL, "n_slots must be >= 1");
+  if (gh_device_count() <= device) return fail(GH_ECUDA, "no CUDA device " + std::to_string(device));
+  GH_CUDA(cudaSetDevice(device));
+  GH_CUDA(configure_kernels());
+  auto t = std::make_unique<gh_tier2>();
+  t->sh = sh; t->device = device; t->l0 = layer_begin; t->l1 = layer_end; t->n_slots = n_slots;
+  t->arena_bytes = (size_t)(layer_end - layer_begin) * (size_t)t->layer_stride() * sh.db;
+  size_t free_b = 0, total_b = 0;
+  GH_CUDA(cudaMemGetInfo(&free_b, &total_b));
+  if (t->arena_bytes > free_b)
+    return fail(GH_EINFEASIBLE, "KV arena of " + std::to_string(t->arena_bytes) +
+                                    " bytes exceeds free device memory (binding constraint: memory)");
+  GH_TRY(dev_alloc(t->mem, t->arena_bytes, &t->arena));
+  *out = t.release();
+  return GH_OK;
+}
+
+gh_status gh_tier2_destroy(gh_tier2* t) {
+  if (t) { cudaSetDevice(t->device); cudaDeviceSynchronize(); delete t; }
+  return GH_OK;
+}
+
+uint64_t gh_tier2_arena_bytes(const gh_tier2* t) { return t ? t->arena_bytes : 0; }
+
+gh_status gh_tier2_check(const gh_tier2* t, uint32_t B, const uint32_t* slot, const int32_t* pos) {
+  if (!t || (B && (!slot || !pos))) return fail(GH_EINVAL, "null argument");
+  for (uint32_t b = 0; b < B; ++b) {
+    if (slot[b] >= t->n_slots)
+      return fail(GH_EINFEASIBLE, "slot " + std::to_string(slot[b]) + " >= n_slots " + std::to_string(t->n_slots) +
+                                      " (binding constraint: memory)");
+    if (pos[b] < 0 || pos[b] >= t->sh.S)
+      return fail(GH_EINFEASIBLE, "position " + std::to_string(pos[b]) + " outside [0, max_seq_len)");
+  }
+  return GH_OK;
+}
+
+gh_status gh_tier2_attend(gh_tier2* t, uint32_t layer, uint32_t B, const uint32_t* slot, const int32_t* pos,
+                          const void* msg_fwd, void* msg_bwd, void* stream) {
+  if (!t || !slot || !pos || !msg_fwd || !msg_bwd) return fail(GH_EINVAL, "null argument");
+  if (layer < t->l0 || layer >= t->l1) return fail(GH_EINVAL, "layer not owned by this Tier-2");
+  if (B == 0) return GH_OK;
+  const Shape& s = t->sh;
+  AttnArgs a;
+  a.msg_fwd = msg_fwd;
+  a.msg_bwd = msg_bwd;
+  a.arena = (char*)t->arena + (size_t)(layer - t->l0) * t->layer_stride() * s.db;
+  a.slot = slot;
+  a.pos = pos;
+  a.slot_stride = t->slot_stride();
+  a.kv_stride = (long)s.Hkv * s.S * s.dh;
+  a.head_stride = (long)s.S * s.dh;
+  a.B = (int)B; a.H = s.H; a.Hkv = s.Hkv; a.D = s.D; a.Dkv = s.Dkv;
+  a.scale_log2 = (float)(1.4426950408889634 / std::sqrt((double)s.dh));
+  GH_CUDA(launch_attention(s.db, s.dh, a, (cudaStream_t)stream));
+  return GH_OK;
+}
+
+gh_status gh_tier2_fill_synthetic(gh_tier2* t, uint64_t seed, uint32_t n_fill, uint32_t npos, void* stream) {
+  if (!t) return fail(GH_EINVAL, "null argument");
+  if (n_fill > t->n_slots || npos > (uint32_t)t->sh.S) return fail(GH_EINVAL, "fill exceeds arena");
+  GH_CUDA(launch_fill_kv(t->sh.db, t->arena, seed, (int)t->l0, (int)t->l1, (int)n_fill, (int)t->n_slots,
+                         t->sh.Hkv, t->sh.S, t->sh.dh, (int)npos, (cudaStream_t)stream));
+  return GH_OK;
+}
+
+gh_status gh_tier2_read_kv(gh_tier2* t, uint32_t layer, uint32_t slot, uint32_t kv, uint32_t head,
+                           uint32_t n, void* host_out) {
+  if (!t || !host_out) return fail(GH_EINVAL, "null argument");
+  if (layer < t->l0 || layer >= t->l1 || slot >= t->n_slots || kv > 1 || head >= (uint32_t)t->sh.Hkv ||
+      n > (uint32_t)t->sh.S)
+    return fail(GH_EINVAL, "read_kv out of range");
+  const Shape& s = t->sh;
+  const size_t off = (size_t)(layer - t->l0) * t->layer_stride() + (size_t)slot * t->slot_stride() +
+                     (size_t)kv * s.Hkv * s.S * s.dh + (size_t)head * s.S * s.dh;
+  GH_CUDA(cudaMemcpy(host_out, (char*)t->arena + off * s.db, (size_t)n * s.dh * s.db, cudaMemcpyDeviceToHost));
+  return GH_OK;
+}
+
+}  // extern "C"
+
+// ================================================================== NCCL transport (dlopen)
+namespace {
+struct NcclApi {
+  bool ok = false;
+  std::string why;
+  ncclResult_t (*GetUniqueId)(ncclUniqueId*) = nullptr;
+  ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+  ncclResult_t (*Send)(const void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*Recv)(void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*GroupStart)() = nullptr;
+  ncclResult_t (*GroupEnd)() = nullptr;
+  const char* (*GetErrorString)(ncclResult_t) = nullptr;
+};
+NcclApi& nccl() {
+  static NcclApi api;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) { api.why = std::string("dlopen libnccl.so.2 failed: ") + dlerror(); return; }
+#define GH_SYM(name) api.name = (decltype(api.name))dlsym(h, "nccl" #name); if (!api.name) { api.why = "missing nccl" #name; return; }
+    GH_SYM(GetUniqueId) GH_SYM(CommInitRank) GH_SYM(CommDestroy) GH_SYM(Send) GH_SYM(Recv)
+    GH_SYM(GroupStart) GH_SYM(GroupEnd) GH_SYM(GetErrorString)
+#undef GH_SYM
+    api.ok = true;
+  });
+  return api;
+}
+}  // namespace
+
+#define GH_NCCL(call)                                                                          \
+  do {                                                                                         \
+    ncclResult_t r_ = (call);                                                                  \
+    if (r_ != ncclSuccess) return fail(GH_ENCCL, std::string(#call) + ": " + nccl().GetErrorString(r_)); \
+  } while (0)
+
+struct gh_comm {
+  int nranks = 0, rank = 0, device = 0;
+  std::vector<ncclComm_t> comms;  // one communicator per in-flight batch
+};
+
+extern "C" {
+
+gh_status gh_comm_unique_id(uint8_t out[128]) {
+  if (!out) return fail(GH_EINVAL, "null argument");
+  if (!nccl().ok) return fail(GH_ENCCL, nccl().why);
+  ncclUniqueId id;
+  GH_NCCL(nccl().GetUniqueId(&id));
+  static_assert(sizeof(id) == 128, "ncclUniqueId size");
+  memcpy(out, &id, 128);
+  return GH_OK;
+}
+
+gh_status gh_comm_create_n(const uint8_t* ids, int n_comms, int nranks, int rank, int device, gh_comm** out) {
+  if (!ids || !out || n_comms < 1) return fail(GH_EINVAL, "bad argument");
+  if (!nccl().ok) return fail(GH_ENCCL, nccl().why);
+  GH_CUDA(cudaSetDevice(device));
+  auto c = std::make_unique<gh_comm>();
+  c->nranks = nranks; c->rank = rank; c->device = device;
+  for (int i = 0; i < n_comms; ++i) {
+    ncclUniqueId id;
+    memcpy(&id, ids + 128 * i, 128);
+    ncclComm_t comm;
+    GH_NCCL(nccl().CommInitRank(&comm, nranks, id, rank));
+    c->comms.push_back(comm);
+  }
+  *out = c.release();
+  return GH_OK;
+}
+
+gh_status gh_comm_create(const uint8_t unique_id[128], int nranks, int rank, int device, gh_comm** out) {
+  return gh_comm_create_n(unique_id, 1, nranks, rank, device, out);
+}
+
+gh_status gh_comm_destroy(gh_comm* c) {
+  if (c) {
+    for (auto cm : c->comms) nccl().CommDestroy(cm);
+    delete c;
+  }
+  return GH_OK;
+}
+
+}  // extern "C"
+
+// ================================================================== Engine
+// colocated: Tier-1 + Tier-2 on this GPU.  Tier split: rank 0 = Tier-1, ranks 1.. = Tier-2.
+struct gh_engine {
+  gh_engine_config cfg{};
+  Shape sh;
+  int role = 0;  // 0 colocated, 1 tier1, 2 tier2
+  gh_comm* comm = nullptr;
+  int kp = 0;    // K' = number of Tier-2 ranks (split mode)
+  gh_tier1* t1 = nullptr;
+  gh_tier2* t2 = nullptr;
+  std::vector<std::unique_ptr<DevMem>> mem;
+  struct Batch {
+    int32_t *tok = nullptr, *pos = nullptr, *next = nullptr;
+    uint32_t* slot = nullptr;
+    void *x0 = nullptr, *x1 = nullptr, *fwd = nullptr, *bwd = nullptr;
+    float* logits = nullptr;
+    cudaStream_t stream = nullptr;
+    cudaEvent_t done = nullptr;
+    cudaGraphExec_t graph = nullptr;
+  };
+  std::vector<Batch> batches;
+  std::vector<int> shard_off, shard_cnt;  // split mode: per Tier-2 rank
+  int my_cnt = 0;                         // tier2: prompts of my shard per batch
+  cudaEvent_t fork = nullptr;
+  ~gh_engine() {
+    for (auto& b : batches) {
+      if (b.graph) cudaGraphExecDestroy(b.graph);
+      if (b.stream) cudaStreamDestroy(b.stream);
+      if (b.done) cudaEventDestroy(b.done);
+    }
+    if (fork) cudaEventDestroy(fork);
+    gh_tier1_destroy(t1);
+    gh_tier2_destroy(t2);
+  }
+  int rows() const { return role == 2 ? my_cnt : (int)cfg.batch; }
+};
+
+static gh_status engine_layer_loop_colocated(gh_engine* e, gh_engine::Batch& b, bool want_logits, cudaStream_t st) {
+  const Shape& s = e->sh;
+  const uint32_t B = e->cfg.batch;
+  GH_TRY(gh_tier1_embed(e->t1, B, b.tok, b.x0, st));
+  void* x = b.x0;
+  void* xn = b.x1;
+  for (int l = 0; l < s.N; ++l) {
+    GH_TRY(gh_tier1_pre(e->t1, l, B, x, b.pos, b.fwd, st));
+    GH_TRY(gh_tier2_attend(e->t2, l, B, b.slot, b.pos, b.fwd, b.bwd, st));
+    GH_TRY(gh_tier1_post(e->t1, l, B, b.bwd, xn, st));
+    std::swap(x, xn);
+  }
+  GH_TRY(gh_tier1_classify(e->t1, B, x, want_logits ? b.logits : nullptr, b.next, st));
+  return GH_OK;
+}
+
+extern "C" {
+
+gh_status gh_engine_create(const gh_engine_config* cfg, gh_comm* comm, gh_engine** out) {
+  if (!cfg || !out) return fail(GH_EINVAL, "null argument");
+  *out = nullptr;
+  auto e = std::make_unique<gh_engine>();
+  e->cfg = *cfg;
+  GH_TRY(Shape::from(&cfg->spec, &e->sh));
+  if (cfg->batch == 0 || cfg->inflight == 0) return fail(GH_EINVAL, "batch and inflight must be >= 1");
+  if (gh_device_count() <= cfg->device) return fail(GH_ECUDA, "no CUDA device " + std::to_string(cfg->device));
+  GH_CUDA(cudaSetDevice(cfg->device));
+  const Shape& s = e->sh;
+  e->comm = comm;
+  const int world = comm ? comm->nranks : 1;
+  const int rank = comm ? comm->rank : 0;
+  if (world == 1) {
+    e->role = 0;
+  } else {
+    if ((int)comm->comms.size() < (int)cfg->inflight)
+      return fail(GH_EINVAL, "tier split needs one communicator per in-flight batch");
+    e->role = rank == 0 ? 1 : 2;
+    e->kp = world - 1;
+    if ((int)cfg->batch < e->kp) return fail(GH_EINVAL, "batch smaller than the number of Tier-2 ranks");
+    int off = 0;
+    for (int j = 0; j < e->kp; ++j) {  // balanced shards differing by at most one (analytic.cpp:119)
+      const int c = (int)cfg->batch / e->kp + (j < (int)cfg->batch % e->kp ? 1 : 0);
+      e->shard_off.push_back(off);
+      e->shard_cnt.push_back(c);
+      off += c;
+    }
+    if (e->role == 2) e->my_cnt = e->shard_cnt[rank - 1];
+  }
+  const int R = e->rows();
+  if (e->role != 2)
+    GH_TRY(gh_tier1_create(&cfg->spec, cfg->device, 0, s.N, cfg->weight_seed, cfg->batch, &e->t1));
+  if (e->role != 1) {
+    uint32_t need = (uint32_t)R * cfg->inflight;
+    uint32_t n_slots = cfg->n_slots ? cfg->n_slots : need;
+    if (n_slots < need) return fail(GH_EINFEASIBLE, "n_slots smaller than batch * inflight (binding constraint: memory)");
+    GH_TRY(gh_tier2_create(&cfg->spec, cfg->device, 0, s.N, n_slots, &e->t2));
+  }
+  GH_CUDA(cudaEventCreateWithFlags(&e->fork, cudaEventDisableTiming));
+  e->batches.resize(cfg->inflight);
+  for (uint32_t ib = 0; ib < cfg->inflight; ++ib) {
+    auto& b = e->batches[ib];
+    void* p;
+    GH_TRY(dev_alloc(e->mem, (size_t)R * 4, &p)); b.tok = (int32_t*)p;
+    GH_TRY(dev_alloc(e->mem, (size_t)R * 4, &p)); b.pos = (int32_t*)p;
+    GH_TRY(dev_alloc(e->mem, (size_t)R * 4, &p)); b.next = (int32_t*)p;
+    GH_TRY(dev_alloc(e->mem, (size_t)R * 4, &p)); b.slot = (uint32_t*)p;
+    GH_TRY(dev_alloc(e->mem, (size_t)R * s.D * s.db, &b.x0));
+    GH_TRY(dev_alloc(e->mem, (size_t)R * s.D * s.db, &b.x1));
+    GH_TRY(dev_alloc(e->mem, (size_t)R * s.ld_fwd() * s.db, &b.fwd));
+    GH_TRY(dev_alloc(e->mem, (size_t)R * s.ld_bwd() * s.db, &b.bwd));
+    if (e->role != 2) { GH_TRY(dev_alloc(e->mem, (size_t)R * s.V * 4, &p)); b.logits = (float*)p; }
+    std::vector<uint32_t> slots(R);
+    for (int i = 0; i < R; ++i) slots[i] = ib * R + i;
+    GH_CUDA(cudaMemcpy(b.slot, slots.data(), R * 4, cudaMemcpyHostToDevice));
+    GH_CUDA(cudaMemset(b.tok, 0, R * 4));
+    GH_CUDA(cudaMemset(b.pos, 0, R * 4));
+    GH_CUDA(cudaMemset(b.next, 0, R * 4));
+    GH_CUDA(cudaStreamCreateWithFlags(&b.stream, cudaStreamNonBlocking));
+    GH_CUDA(cudaEventCreateWithFlags(&b.done, cudaEventDisableTiming));
+  }
+  GH_CUDA(cudaDeviceSynchronize());
+  *out = e.release();
+  return GH_OK;
+}
+
+gh_status gh_engine_destroy(gh_engine* e) {
+  delete e;
+  return GH_OK;
+}
+
+int gh_engine_role(const gh_engine* e) { return e ? e->role : -1; }
+gh_tier1* gh_engine_tier1(gh_engine* e) { return e ? e->t1 : nullptr; }
+
+gh_status gh_engine_advance(gh_engine* e, uint32_t ib, int inc, void* stream) {
+  if (!e || ib >= e->batches.size()) return fail(GH_EINVAL, "bad engine / batch index");
+  if (e->role == 2) return fail(GH_EINVAL, "Tier-2 ranks hold no token state");
+  auto& b = e->batches[ib];
+  GH_CUDA(launch_advance(b.tok, b.next, b.pos, (int)e->cfg.batch, inc, (cudaStream_t)stream));
+  return GH_OK;
+}
+gh_tier2* gh_engine_tier2(gh_engine* e) { return e ? e->t2 : nullptr; }
+
+gh_status gh_engine_io(gh_engine* e, uint32_t ib, int32_t** tok, int32_t** pos, uint32_t** slot, int32_t** next) {
+  if (!e || ib >= e->batches.size()) return fail(GH_EINVAL, "bad engine / batch index");
+  auto& b = e->batches[ib];
+  if (tok) *tok = b.tok;
+  if (pos) *pos = b.pos;
+  if (slot) *slot = b.slot;
+  if (next) *next = b.next;
+  return GH_OK;
+}
+
+// --- tier-split body for one in-flight batch, issued on the batch stream.
+// Tier-1:  for each layer: F1 -> send shards [x|q|k|v] -> recv shards [x|attn] -> F3
+// Tier-2:  for each layer: recv shard -> F2 -> send shard
+static gh_status split_begin(gh_engine* e, gh_engine::Batch& b, ncclComm_t comm, cudaStream_t st) {
+  auto& api = nccl();
+  if (e->role == 1) {
+    // step header: positions of each shard (Dispatcher batch state)
+    GH_NCCL(api.GroupStart());
+    for (int j = 0; j < e->kp; ++j)
+      GH_NCCL(api.Send(b.pos + e->shard_off[j], e->shard_cnt[j], ncclInt32, j + 1, comm, st));
+    GH_NCCL(api.GroupEnd());
+    GH_TRY(gh_tier1_embed(e->t1, e->cfg.batch, b.tok, b.x0, st));
+  } else {
+    GH_NCCL(api.Recv(b.pos, e->my_cnt, ncclInt32, 0, comm, st));
+  }
+  return GH_OK;
+}
+
+static gh_status split_layer(gh_engine* e, gh_engine::Batch& b, ncclComm_t comm, int l, void** x, void** xn,
+                             cudaStream_t st) {
+  auto& api = nccl();
+  const Shape& s = e->sh;
+  const size_t fwd_row = (size_t)s.ld_fwd() * s.db, bwd_row = (size_t)s.ld_bwd() * s.db;
+  if (e->role == 1) {
+    GH_TRY(gh_tier1_pre(e->t1, l, e->cfg.batch, *x, b.pos, b.fwd, st));
+    GH_NCCL(api.GroupStart());
+    for (int j = 0; j < e->kp; ++j)
+      GH_NCCL(api.Send((char*)b.fwd + e->shard_off[j] * fwd_row, e->shard_cnt[j] * fwd_row, ncclUint8, j + 1, comm, st));
+    GH_NCCL(api.GroupEnd());
+    GH_NCCL(api.GroupStart());
+    for (int j = 0; j < e->kp; ++j)
+      GH_NCCL(api.Recv((char*)b.bwd + e->shard_off[j] * bwd_row, e->shard_cnt[j] * bwd_row, ncclUint8, j + 1, comm, st));
+    GH_NCCL(api.GroupEnd());
+    GH_TRY(gh_tier1_post(e->t1, l, e->cfg.batch, b.bwd, *xn, st));
+    std::swap(*x, *xn);
+  } else {
+    GH_NCCL(api.Recv(b.fwd, e->my_cnt * fwd_row, ncclUint8, 0, comm, st));
+    GH_TRY(gh_tier2_attend(e->t2, l, e->my_cnt, b.slot, b.pos, b.fwd, b.bwd, st));
+    GH_NCCL(api.Send(b.bwd, e->my_cnt * bwd_row, ncclUint8, 0, comm, st));
+  }
+  return GH_OK;
+}
+
+gh_status gh_engine_step_device(gh_engine* e, uint32_t ib, void* stream) {
+  if (!e || ib >= e->batches.size()) return fail(GH_EINVAL, "bad engine / batch index");
+  auto& b = e->batches[ib];
+  cudaStream_t st = (cudaStream_t)stream;
+  GH_CUDA(cudaSetDevice(e->cfg.device));
+  if (e->role == 0) {
+    if (e->cfg.use_graph) {
+      if (!b.graph) {
+        cudaStream_t cs;
+        GH_CUDA(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
+        GH_CUDA(cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal));
+        gh_status r = engine_layer_loop_colocated(e, b, false, cs);
+        cudaGraph_t g = nullptr;
+        cudaError_t ce = cudaStreamEndCapture(cs, &g);
+        cudaStreamDestroy(cs);
+        if (r != GH_OK) { if (g) cudaGraphDestroy(g); return r; }
+        GH_CUDA(ce);
+        cudaError_t ie = cudaGraphInstantiate(&b.graph, g, 0);
+        cudaGraphDestroy(g);
+        GH_CUDA(ie);
+      }
+      GH_CUDA(cudaGraphLaunch(b.graph, st));
+      return GH_OK;
+    }
+    return engine_layer_loop_colocated(e, b, false, st);
+  }
+  ncclComm_t comm = e->comm->comms[ib];
+  GH_TRY(split_begin(e, b, comm, st));
+  void* x = b.x0;
+  void* xn = b.x1;
+  for (int l = 0; l < e->sh.N; ++l) GH_TRY(split_layer(e, b, comm, l, &x, &xn, st));
+  if (e->role == 1) GH_TRY(gh_tier1_classify(e->t1, e->cfg.batch, x, nullptr, b.next, st));
+  return GH_OK;
+}
+
+// All in-flight batches; in split mode the batches are interleaved layer by layer on their own
+// streams so that Tier-1 compute of one batch overlaps Tier-2 attention of another.
+gh_status gh_engine_step_all(gh_engine* e, void* stream) {
+  if (!e) return fail(GH_EINVAL, "null engine");
+  cudaStream_t st = (cudaStream_t)stream;
+  GH_CUDA(cudaSetDevice(e->cfg.device));
+  const int nb = (int)e->batches.size();
+  if (e->role == 0 || nb == 1) {
+    for (int ib = 0; ib < nb; ++ib) GH_TRY(gh_engine_step_device(e, ib, stream));
+    return GH_OK;
+  }
+  GH_CUDA(cudaEventRecord(e->fork, st));
+  std::vector<void*> x(nb), xn(nb);
+  for (int ib = 0; ib < nb; ++ib) {
+    auto& b = e->batches[ib];
+    GH_CUDA(cudaStreamWaitEvent(b.stream, e->fork, 0));
+    GH_TRY(split_begin(e, b, e->comm->comms[ib], b.stream));
+    x[ib] = b.x0; xn[ib] = b.x1;
+  }
+  for (int l = 0; l < e->sh.N; ++l)
+    for (int ib = 0; ib < nb; ++ib)
+      GH_TRY(split_layer(e, e->batches[ib], e->comm->comms[ib], l, &x[ib], &xn[ib], e->batches[ib].stream));
+  for (int ib = 0; ib < nb; ++ib) {
+    auto& b = e->batches[ib];
+    if (e->role == 1) GH_TRY(gh_tier1_classify(e->t1, e->cfg.batch, x[ib], nullptr, b.next, b.stream));
+    GH_CUDA(cudaEventRecord(b.done, b.stream));
+    GH_CUDA(cudaStreamWaitEvent(st, b.done, 0));
+  }
+  return GH_OK;
+}
+
+gh_status gh_engine_step_host(gh_engine* e, uint32_t ib, const int32_t* tok_host, const int32_t* pos_host,
+                              int32_t* next_host, float* logits_host, void* stream) {
+  if (!e || ib >= e->batches.size()) return fail(GH_EINVAL, "bad engine / batch index");
+  auto& b = e->batches[ib];
+  cudaStream_t st = (cudaStream_t)stream;
+  GH_CUDA(cudaSetDevice(e->cfg.device));
+  const int R = e->rows();
+  if (e->role != 2) {
+    if (!tok_host || !pos_host || !next_host) return fail(GH_EINVAL, "host token/pos/next buffers required");
+    GH_CUDA(cudaMemcpyAsync(b.tok, tok_host, (size_t)R * 4, cudaMemcpyHostToDevice, st));
+    GH_CUDA(cudaMemcpyAsync(b.pos, pos_host, (size_t)R * 4, cudaMemcpyHostToDevice, st));
+  }
+  if (logits_host && e->role == 0) {
+    GH_TRY(engine_layer_loop_colocated(e, b, true, st));
+  } else if (logits_host && e->role == 1) {
+    ncclComm_t comm = e->comm->comms[ib];
+    GH_TRY(split_begin(e, b, comm, st));
+    void* x = b.x0;
+    void* xn = b.x1;
+    for (int l = 0; l < e->sh.N; ++l) GH_TRY(split_layer(e, b, comm, l, &x, &xn, st));
+    GH_TRY(gh_tier1_classify(e->t1, e->cfg.batch, x, b.logits, b.next, st));
+  } else {
+    GH_TRY(gh_engine_step_device(e, ib, stream));
+  }
+  if (e->role != 2) {
+    GH_CUDA(cudaMemcpyAsync(next_host, b.next, (size_t)R * 4, cudaMemcpyDeviceToHost, st));
+    if (logits_host)
+      GH_CUDA(cudaMemcpyAsync(logits_host, b.logits, (size_t)R * e->sh.V * 4, cudaMemcpyDeviceToHost, st));
+  }
+  GH_CUDA(cudaStreamSynchronize(st));
+  return GH_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,225 @@
+"""Host-side mirror of the two-tier stage interface (Glinthawk compute kernels).
+
+Stage taxonomy and names follow the reference (proj/include/tierplan/profiles.hpp:13):
+``nonattention`` = Tier-1 F1 (``pre``) + F3 (``post``), ``attention`` = Tier-2 F2 (``attend``),
+``classifier`` = Tier-1 ``classify``.  Every method is a thin call through the C ABI; device
+buffers are torch tensors (plumbing only) passed by address, streams are torch CUDA streams.
+"""
+from __future__ import annotations
+
+import ctypes as C
+
+import numpy as np
+
+from . import _lib as L
+from .spec import ModelSpec
+
+
+def _stream(stream) -> int | None:
+    if stream is None:
+        import torch
+        return torch.cuda.current_stream().cuda_stream
+    return stream if isinstance(stream, int) else stream.cuda_stream
+
+
+def _torch_dtype(spec: ModelSpec):
+    import torch
+    return {4: torch.float32, 2: torch.bfloat16}[spec.dtype_bytes]
+
+
+class Tier1:
+    """Weight-holding stage for layers [layer_begin, layer_end) (a layer_spans block)."""
+
+    def __init__(self, spec: ModelSpec, device: int = 0, layer_begin: int = 0,
+                 layer_end: int | None = None, weight_seed: int = 1234, max_batch: int = 64):
+        self.spec = spec
+        self.layer_begin, self.layer_end = layer_begin, spec.n_layers if layer_end is None else layer_end
+        h = C.c_void_p()
+        L.check(L.lib().gh_tier1_create(C.byref(spec.c()), device, self.layer_begin, self.layer_end,
+                                        weight_seed, max_batch, C.byref(h)))
+        self.h = h
+
+    def close(self):
+        if getattr(self, "h", None):
+            L.lib().gh_tier1_destroy(self.h)
+            self.h = None
+
+    __del__ = close
+
+    def embed(self, tok, x, stream=None):
+        L.check(L.lib().gh_tier1_embed(self.h, tok.shape[0], L.ptr(tok), L.ptr(x), _stream(stream)))
+
+    def pre(self, layer: int, x, pos, msg_fwd, stream=None):
+        """F1 -> fwd message [x|q|k|v]"""
+        L.check(L.lib().gh_tier1_pre(self.h, layer, x.shape[0], L.ptr(x), L.ptr(pos), L.ptr(msg_fwd),
+                                     _stream(stream)))
+
+    def post(self, layer: int, msg_bwd, x_next, stream=None):
+        """F3 from bwd message [x|attn]"""
+        L.check(L.lib().gh_tier1_post(self.h, layer, msg_bwd.shape[0], L.ptr(msg_bwd), L.ptr(x_next),
+                                      _stream(stream)))
+
+    def classify(self, x, next_tok, logits=None, stream=None):
+        L.check(L.lib().gh_tier1_classify(self.h, x.shape[0], L.ptr(x), L.ptr(logits), L.ptr(next_tok),
+                                          _stream(stream)))
+
+
+class Tier2:
+    """KV-context stage: n_slots prompt slots for layers [layer_begin, layer_end)."""
+
+    def __init__(self, spec: ModelSpec, n_slots: int, device: int = 0, layer_begin: int = 0,
+                 layer_end: int | None = None):
+        self.spec = spec
+        self.n_slots = n_slots
+        self.layer_begin, self.layer_end = layer_begin, spec.n_layers if layer_end is None else layer_end
+        h = C.c_void_p()
+        L.check(L.lib().gh_tier2_create(C.byref(spec.c()), device, self.layer_begin, self.layer_end,
+                                        n_slots, C.byref(h)))
+        self.h = h
+
+    def close(self):
+        if getattr(self, "h", None):
+            L.lib().gh_tier2_destroy(self.h)
+            self.h = None
+
+    __del__ = close
+
+    @property
+    def arena_bytes(self) -> int:
+        return L.lib().gh_tier2_arena_bytes(self.h)
+
+    def check(self, slot: np.ndarray, pos: np.ndarray):
+        s = np.ascontiguousarray(slot, dtype=np.uint32)
+        p = np.ascontiguousarray(pos, dtype=np.int32)
+        L.check(L.lib().gh_tier2_check(self.h, len(s), s.ctypes.data_as(C.POINTER(C.c_uint32)),
+                                       p.ctypes.data_as(C.POINTER(C.c_int32))))
+
+    def attend(self, layer: int, slot, pos, msg_fwd, msg_bwd, stream=None):
+        """F2: append + attention"""
+        L.check(L.lib().gh_tier2_attend(self.h, layer, msg_fwd.shape[0], L.ptr(slot), L.ptr(pos),
+                                        L.ptr(msg_fwd), L.ptr(msg_bwd), _stream(stream)))
+
+    def fill_synthetic(self, seed: int, n_slots: int, n_positions: int, stream=None):
+        L.check(L.lib().gh_tier2_fill_synthetic(self.h, seed, n_slots, n_positions, _stream(stream)))
+
+    def read_kv(self, layer: int, slot: int, kv: int, head: int, n: int) -> np.ndarray:
+        out = np.empty((n, self.spec.d_head), dtype=np.float32 if self.spec.dtype_bytes == 4 else np.uint16)
+        L.check(L.lib().gh_tier2_read_kv(self.h, layer, slot, kv, head, n, out.ctypes.data))
+        return out
+
+
+def message_buffers(spec: ModelSpec, B: int, device: int = 0):
+    """(x, msg_fwd, msg_bwd) device buffers with the PayloadModel layouts."""
+    import torch
+    dt = _torch_dtype(spec)
+    dev = torch.device("cuda", device)
+    x = torch.zeros(B, spec.d_model, dtype=dt, device=dev)
+    fwd = torch.zeros(B, 2 * spec.d_model + 2 * spec.d_kv, dtype=dt, device=dev)
+    bwd = torch.zeros(B, 2 * spec.d_model, dtype=dt, device=dev)
+    return x, fwd, bwd
+
+
+class Comm:
+    """NCCL transport (one communicator per in-flight batch); ids from rank 0."""
+
+    @staticmethod
+    def unique_ids(n: int) -> bytes:
+        out = b""
+        for _ in range(n):
+            buf = (C.c_uint8 * 128)()
+            L.check(L.lib().gh_comm_unique_id(buf))
+            out += bytes(buf)
+        return out
+
+    def __init__(self, ids: bytes, nranks: int, rank: int, device: int):
+        n = len(ids) // 128
+        buf = (C.c_uint8 * len(ids)).from_buffer_copy(ids)
+        h = C.c_void_p()
+        L.check(L.lib().gh_comm_create_n(buf, n, nranks, rank, device, C.byref(h)))
+        self.h, self.nranks, self.rank = h, nranks, rank
+
+    def close(self):
+        if getattr(self, "h", None):
+            L.lib().gh_comm_destroy(self.h)
+            self.h = None
+
+
+class Engine:
+    """One decode step over all layers: colocated (1 GPU) or tier split (rank 0 Tier-1,
+    ranks 1.. Tier-2, NCCL send/recv of the PayloadModel messages every layer)."""
+
+    ROLES = {0: "colocated", 1: "tier1", 2: "tier2"}
+
+    def __init__(self, spec: ModelSpec, batch: int, inflight: int = 1, device: int = 0,
+                 weight_seed: int = 1234, n_slots: int = 0, use_graph: bool = True,
+                 comm: Comm | None = None):
+        self.spec, self.batch, self.inflight = spec, batch, inflight
+        cfg = L.GhEngineConfig(spec.c(), device, weight_seed, batch, inflight, n_slots, int(use_graph))
+        h = C.c_void_p()
+        L.check(L.lib().gh_engine_create(C.byref(cfg), comm.h if comm else None, C.byref(h)))
+        self.h = h
+        self.comm = comm
+        self.role = self.ROLES[L.lib().gh_engine_role(h)]
+        self._pinned = {}
+
+    def close(self):
+        if getattr(self, "h", None):
+            L.lib().gh_engine_destroy(self.h)
+            self.h = None
+
+    __del__ = close
+
+    @property
+    def tier2(self) -> int:
+        return L.lib().gh_engine_tier2(self.h)
+
+    def step_host(self, tok: np.ndarray | None, pos: np.ndarray | None, want_logits=False, ib=0,
+                  stream=None):
+        """End-to-end step through host buffers; returns (next_tokens, logits or None)."""
+        if self.role == "tier2":
+            L.check(L.lib().gh_engine_step_host(self.h, ib, None, None, None, None, _stream(stream)))
+            return None, None
+        t = np.ascontiguousarray(tok, dtype=np.int32)
+        p = np.ascontiguousarray(pos, dtype=np.int32)
+        nxt = np.empty(self.batch, dtype=np.int32)
+        lg = np.empty((self.batch, self.spec.vocab_size), dtype=np.float32) if want_logits else None
+        L.check(L.lib().gh_engine_step_host(self.h, ib, t.ctypes.data, p.ctypes.data, nxt.ctypes.data,
+                                            None if lg is None else lg.ctypes.data, _stream(stream)))
+        return nxt, lg
+
+    def step_device(self, ib=0, stream=None):
+        L.check(L.lib().gh_engine_step_device(self.h, ib, _stream(stream)))
+
+    def step_all(self, stream=None):
+        L.check(L.lib().gh_engine_step_all(self.h, _stream(stream)))
+
+    def advance(self, ib=0, pos_increment=0, stream=None):
+        L.check(L.lib().gh_engine_advance(self.h, ib, pos_increment, _stream(stream)))
+
+
+class Dispatcher:
+    """Greedy decode driver over an Engine (Dispatcher): prompt i of the batch owns
+    context slot i; prompt tokens are fed one per step (the dispatcher does not distinguish
+    input and output tokens) and generation continues greedily."""
+
+    def __init__(self, engine: Engine):
+        self.engine = engine
+
+    def generate(self, prompts: np.ndarray, max_new: int, want_logits=False):
+        prompts = np.asarray(prompts, dtype=np.int32)
+        B, plen = prompts.shape
+        assert B == self.engine.batch
+        tok = prompts[:, 0].copy()
+        out, logits = [], []
+        for t in range(plen - 1 + max_new):
+            pos = np.full(B, t, dtype=np.int32)
+            nxt, lg = self.engine.step_host(tok, pos, want_logits=want_logits)
+            if t + 1 < plen:
+                tok = prompts[:, t + 1].copy()
+            else:
+                out.append(nxt.copy())
+                if want_logits:
+                    logits.append(lg)
+                tok = nxt
+        gen = np.stack(out, axis=1) if out else np.zeros((B, 0), np.int32)
+        return gen, (np.stack(logits, axis=1) if want_logits else None)
