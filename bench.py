@@ -1,0 +1,418 @@
+#!/usr/bin/env python
+"""Decode-throughput benchmark of the B200 two-tier decode path (BASELINE.json metric).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config C2|C3]
+
+N = 1: config C2 (Llama-2-7B shape, batch 64, context 512, both tiers colocated on one B200).
+N > 1 (torchrun, one process per GPU): config C3 tier split — rank 0 = Tier-1 (weights),
+ranks 1..N-1 = Tier-2 (KV shards by prompt), NCCL send/recv of the PayloadModel messages every
+layer, IF = 2 in-flight batches; batch = the capacity-admitted batch (two_tier_context_slots).
+
+A step = one decode token for every prompt of every in-flight batch, all layers + classifier +
+greedy argmax, at a fixed context (each step appends at position ctx-1 and attends over ctx
+positions; KV pre-filled with synthetic values).  Inputs (13.5 GB weights + KV) are far larger
+than the 126 MB L2, so no L2 flush is needed between steps.
+
+--impl reference times the reference-side CPU implementation of the path (the oracle port,
+oracle/oracle.c, all host threads) on a bounded sample of the same workload.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+GiB = 1 << 30
+
+
+def peaks():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        return d["hbm_gbs"], d["bf16_tflops"], "measured"
+    return 6650.0, 1590.0, "fallback"
+
+
+# ------------------------------------------------------------------ clocks sampler
+class Clocks:
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except OSError:
+            self.proc = None
+        return self
+
+    def __exit__(self, *a):
+        self.lines = []
+        if self.proc:
+            self.proc.terminate()
+            try:
+                out, _ = self.proc.communicate(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+                out, _ = self.proc.communicate()
+            self.lines = [ln for ln in out.splitlines() if ln.strip()]
+
+    def summary(self):
+        sm, mx, reasons = [], 0.0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in getattr(self, "lines", []):
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 6:
+                continue
+            try:
+                sm.append(float(f[0]))
+                mx = max(mx, float(f[1]))
+            except ValueError:
+                continue
+            for n, v in zip(names, f[2:6]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx or None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ------------------------------------------------------------------ CPU baseline (oracle)
+def cpu_sample(spec, B, ctx, threads=0):
+    """Time the oracle on a bounded sample: embed + 2 layers + classifier of the same shape at
+    batch B and context ctx; extrapolate to all layers.  Returns (tokens/s, sample text, cores)."""
+    from oracle import Oracle, olib
+    sub = spec.with_(n_layers=2)
+    t_setup = time.time()
+    ora = Oracle(sub, n_slots=B, threads=threads)
+    ora.fill_synthetic(99, B, ctx - 1)
+    setup_s = time.time() - t_setup
+    rng = np.random.default_rng(5678)
+    tok = rng.integers(0, spec.vocab_size, size=B).astype(np.int32)
+    pos = np.full(B, ctx - 1, np.int32)
+    slot = np.arange(B, dtype=np.uint32)
+    x, fwd, bwd = ora.buffers(B)
+    x2 = np.zeros_like(x)
+    t0 = time.perf_counter()
+    ora.embed(tok, x)
+    t_emb = time.perf_counter() - t0
+    t_layers = []
+    for layer in range(2):
+        t0 = time.perf_counter()
+        ora.pre(layer, x, pos, fwd)
+        ora.attend(layer, slot, pos, fwd, bwd)
+        ora.post(layer, bwd, x2)
+        t_layers.append(time.perf_counter() - t0)
+        x, x2 = x2, x
+    t0 = time.perf_counter()
+    ora.classify(x, want_logits=False)
+    t_cls = time.perf_counter() - t0
+    ora.close()
+    t_step = t_emb + spec.n_layers * statistics.mean(t_layers) + t_cls
+    cores = olib().or_max_threads()
+    sample = (f"oracle.c fp32 on {cores} threads: embed + 2 of {spec.n_layers} layers + classifier at batch {B}, "
+              f"ctx {ctx}; per-layer {statistics.mean(t_layers) * 1e3:.1f} ms x {spec.n_layers} + classifier "
+              f"{t_cls * 1e3:.1f} ms = {t_step:.2f} s/step (setup {setup_s:.1f} s untimed)")
+    return B / t_step, sample, cores, t_step
+
+
+# ------------------------------------------------------------------ configs
+def workload(args, world):
+    import paper_2501_11779_b200 as gh
+    cfg = args.config or ("C2" if world == 1 else "C3")
+    c = gh.CONFIGS[cfg]
+    spec, ctx = c["spec"], c["ctx"]
+    if world == 1:
+        return dict(name=cfg, spec=spec, ctx=ctx, batch=c["batch"], requested=c["batch"], inflight=1,
+                    shard=c["batch"], kp=0)
+    kp = world - 1
+    mem = 179 * GiB
+    slots = gh.two_tier_context_slots(spec, 1, kp, mem, ctx)  # optimizer.cpp:175-192
+    inflight = 2
+    per_gpu = slots // kp
+    shard = min(per_gpu // inflight, c["batch"] // (kp * inflight) or 1)
+    return dict(name=cfg, spec=spec, ctx=ctx, batch=shard * kp, requested=c["batch"], inflight=inflight,
+                shard=shard, kp=kp, admitted_slots=slots)
+
+
+def attention_bytes(spec, B, ctx):
+    """SURVEY.md §8d algorithmic bytes of one attention launch (one layer):
+    dtype*(2*D_kv*sum_b S_b + 2*B*D_kv + 2*B*D), S_b = ctx (cached ctx-1 + the new token)."""
+    db = spec.dtype_bytes
+    return db * (2 * spec.d_kv * B * ctx + 2 * B * spec.d_kv + 2 * B * spec.d_model)
+
+
+def gemm_layer_bytes(spec, B):
+    """weights of one layer + activations in/out of the four GEMMs (model.cpp:53 weight term)"""
+    D, Dkv, Dh, db = spec.d_model, spec.d_kv, spec.d_hidden, spec.dtype_bytes
+    w = D * (2 * D + 3 * Dh + 2 * Dkv)
+    act = B * (D + (D + 2 * Dkv)) + B * (D + D + D) + B * (D + Dh) + B * (Dh + D + D)
+    return db * (w + act)
+
+
+# ------------------------------------------------------------------ our arm, 1 GPU
+def run_colocated(args, wl):
+    import torch
+    import paper_2501_11779_b200 as gh
+    from paper_2501_11779_b200 import _lib as L
+    from paper_2501_11779_b200.stages import Engine, Tier1, Tier2, message_buffers
+
+    spec, B, ctx = wl["spec"], wl["batch"], wl["ctx"]
+    torch.cuda.set_device(0)
+    stream = torch.cuda.Stream()
+    eng = Engine(spec, batch=B, use_graph=True)
+    lib = gh.lib()
+    L.check(lib.gh_tier2_fill_synthetic(eng.tier2, 99, B, ctx - 1, None))
+    rng = np.random.default_rng(5678)
+    tok = rng.integers(0, spec.vocab_size, size=B).astype(np.int32)
+    pos = np.full(B, ctx - 1, np.int32)
+    torch.cuda.synchronize()
+    n0 = lib.gh_kernel_launches(0)
+    eng.step_host(tok, pos)                       # sets device tok/pos; captures the CUDA graph
+    per_step_launches = lib.gh_kernel_launches(0) - n0 + 1   # captured kernels + advance
+    for _ in range(args.warmup):
+        eng.step_device(stream=stream)
+        eng.advance(pos_increment=0, stream=stream)
+    stream.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with Clocks(0) as clk:
+        torch.cuda.synchronize()
+        e0.record(stream)
+        for _ in range(args.steps):
+            eng.step_device(stream=stream)
+            eng.advance(pos_increment=0, stream=stream)
+        e1.record(stream)
+        torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / args.steps
+    value = B / (ms / 1e3)
+
+    # e2e through the public API: host tokens/pos in, next tokens out, every step
+    nxt = tok
+    t0 = time.perf_counter()
+    for _ in range(max(2, args.steps // 2)):
+        nxt, _ = eng.step_host(nxt, pos, stream=stream)
+    e2e_ms = (time.perf_counter() - t0) * 1e3 / max(2, args.steps // 2)
+
+    # dominant kernel: attention of one layer, timed alone with CUDA events on its stream
+    eng.close()
+    del eng
+    torch.cuda.empty_cache()
+    t2 = Tier2(spec.with_(n_layers=1), n_slots=B)
+    t2.fill_synthetic(99, B, ctx - 1)
+    x, fwd, bwd = message_buffers(spec, B)
+    fwd.normal_()
+    pos_d = torch.full((B,), ctx - 1, dtype=torch.int32, device="cuda")
+    slot_d = torch.arange(B, dtype=torch.int32, device="cuda")
+    with torch.cuda.stream(stream):
+        for _ in range(3):
+            t2.attend(0, slot_d, pos_d, fwd, bwd, stream=stream)
+        a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        reps = 20
+        a0.record(stream)
+        for _ in range(reps):
+            t2.attend(0, slot_d, pos_d, fwd, bwd, stream=stream)
+        a1.record(stream)
+    stream.synchronize()
+    attn_ms = a0.elapsed_time(a1) / reps
+    t2.close()
+    # Tier-1 nonattention of one layer (pre + post), for the GEMM roofline
+    t1 = Tier1(spec.with_(n_layers=1), max_batch=B)
+    with torch.cuda.stream(stream):
+        for _ in range(3):
+            t1.pre(0, x, pos_d, fwd, stream=stream)
+            t1.post(0, bwd, x, stream=stream)
+        g0, g1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        g0.record(stream)
+        for _ in range(reps):
+            t1.pre(0, x, pos_d, fwd, stream=stream)
+            t1.post(0, bwd, x, stream=stream)
+        g1.record(stream)
+    stream.synchronize()
+    na_ms = g0.elapsed_time(g1) / reps
+    t1.close()
+    return dict(ms=ms, value=value, e2e_ms=e2e_ms, launches=per_step_launches * args.steps,
+                attn_ms=attn_ms, na_ms=na_ms, clocks=clk.summary())
+
+
+# ------------------------------------------------------------------ our arm, tier split
+def run_split(args, wl, rank, world):
+    import torch
+    import torch.distributed as dist
+    import paper_2501_11779_b200 as gh
+    from paper_2501_11779_b200 import _lib as L
+    from paper_2501_11779_b200.stages import Comm, Engine
+
+    spec, ctx, IF = wl["spec"], wl["ctx"], wl["inflight"]
+    dev = int(os.environ.get("LOCAL_RANK", rank))
+    torch.cuda.set_device(dev)
+    obj = [Comm.unique_ids(IF) if rank == 0 else None]
+    dist.broadcast_object_list(obj, src=0)
+    comm = Comm(obj[0], world, rank, dev)
+    eng = Engine(spec, batch=wl["batch"], inflight=IF, device=dev, use_graph=False, comm=comm)
+    lib = gh.lib()
+    stream = torch.cuda.Stream()
+    if eng.role == "tier2":
+        L.check(lib.gh_tier2_fill_synthetic(eng.tier2, 99, wl["shard"] * IF, ctx - 1, None))
+    rng = np.random.default_rng(5678)
+    tok = rng.integers(0, spec.vocab_size, size=wl["batch"]).astype(np.int32)
+    pos = np.full(wl["batch"], ctx - 1, np.int32)
+    torch.cuda.synchronize()
+    for ib in range(IF):
+        eng.step_host(tok, pos, ib=ib)
+    dist.barrier()
+    n0 = lib.gh_kernel_launches(0)
+    for _ in range(args.warmup):
+        eng.step_all(stream=stream)
+        if eng.role == "tier1":
+            for ib in range(IF):
+                eng.advance(ib, 0, stream=stream)
+    stream.synchronize()
+    per_step = (lib.gh_kernel_launches(0) - n0) / max(args.warmup, 1)
+    dist.barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with Clocks(dev) as clk:
+        torch.cuda.synchronize()
+        dist.barrier()
+        e0.record(stream)
+        for _ in range(args.steps):
+            eng.step_all(stream=stream)
+            if eng.role == "tier1":
+                for ib in range(IF):
+                    eng.advance(ib, 0, stream=stream)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        dist.barrier()
+    ms_local = e0.elapsed_time(e1) / args.steps
+    t = torch.tensor([ms_local], dtype=torch.float64)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms = float(t.item())
+    launches = torch.tensor([per_step * args.steps], dtype=torch.float64)
+    dist.all_reduce(launches, op=dist.ReduceOp.SUM)
+    # e2e: host tokens in / next tokens out on Tier-1 every step (in-flight batch 0..IF-1)
+    dist.barrier()
+    t0 = time.perf_counter()
+    nsteps = max(2, args.steps // 2)
+    nxt = tok
+    for _ in range(nsteps):
+        for ib in range(IF):
+            r, _ = eng.step_host(nxt if eng.role == "tier1" else None, pos if eng.role == "tier1" else None, ib=ib)
+            if r is not None:
+                nxt = r
+    e2e_ms = torch.tensor([(time.perf_counter() - t0) * 1e3 / nsteps], dtype=torch.float64)
+    dist.all_reduce(e2e_ms, op=dist.ReduceOp.MAX)
+    eng.close()
+    comm.close()
+    total = wl["batch"] * IF
+    return dict(ms=ms, value=total / (ms / 1e3), e2e_ms=float(e2e_ms.item()), launches=int(launches.item()),
+                clocks=clk.summary(), total=total)
+
+
+# ------------------------------------------------------------------ main
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default=None, choices=[None, "C2", "C3"])
+    ap.add_argument("--cpu-threads", type=int, default=0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    wl = workload(args, max(world, args.gpus if world == 1 else world))
+    spec = wl["spec"]
+    hbm, tf, peak_kind = peaks()
+    metric = "decode tokens/s (Llama-2-7B shape, 2-tier split)"
+    cfg = {"workload": f"{wl['name']}: {spec.name} shape random-init, context {wl['ctx']}, "
+                       + ("both tiers colocated on 1 GPU" if wl["kp"] == 0 else
+                          f"Tier-1 on 1 GPU + Tier-2 KV sharded by prompt over {wl['kp']} GPUs, IF={wl['inflight']}"),
+           "batch": wl["batch"] * wl["inflight"], "requested_batch": wl["requested"], "ctx": wl["ctx"],
+           "inflight": wl["inflight"], "dtype_storage": "bf16", "l2": "inputs larger than L2 (no flush)"}
+    if "admitted_slots" in wl:
+        cfg["admitted_slots"] = wl["admitted_slots"]
+
+    if args.impl == "reference":
+        if world > 1 and rank != 0:
+            return
+        B = wl["batch"] if wl["kp"] == 0 else min(wl["batch"], 64)
+        vals = []
+        samples = []
+        for _ in range(max(1, min(args.steps, 3))):
+            v, sample, cores, _ = cpu_sample(spec, B, wl["ctx"], args.cpu_threads)
+            vals.append(v)
+            samples.append(sample)
+        v = statistics.mean(vals)
+        print(json.dumps({
+            "impl": "reference", "metric": metric, "value": v, "unit": "tokens/s", "n_gpus": 0,
+            "steps": len(vals), "warmup": 0, "ms_per_step": B / v * 1e3, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic", "config": cfg,
+            "cpu_baseline": {"value": v, "unit": "tokens/s", "cores": cores, "kind": "port",
+                             "sample": samples[-1]},
+            "e2e": {"value": v, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+            "note": "reference has no decode implementation (SURVEY.md §0.2); the CPU arm is the oracle port "
+                    "of the paper's CPU Tier-2 path (P:514, OpenMP)"}))
+        return
+
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("gloo")
+        res = run_split(args, wl, rank, world)
+        if rank != 0:
+            dist.destroy_process_group()
+            return
+    else:
+        res = run_colocated(args, wl)
+
+    out = {"metric": metric, "value": res["value"], "unit": "tokens/s", "n_gpus": max(world, 1),
+           "steps": args.steps, "warmup": args.warmup, "ms_per_step": res["ms"], "higher_is_better": True,
+           "scaling": "weak", "vs_baseline": None, "dtype": "bf16", "data": "synthetic", "config": cfg}
+    B_step = wl["batch"] * wl["inflight"]
+    out["e2e"] = {"value": B_step / (res["e2e_ms"] / 1e3), "unit": "tokens/s",
+                  "h2d_bytes_per_step": B_step * 8, "d2h_bytes_per_step": B_step * 4}
+    out["gpu_launches"] = int(res["launches"])
+    out["clocks"] = res["clocks"]
+    if world == 1:
+        ab = attention_bytes(spec, wl["batch"], wl["ctx"])
+        ach = ab / (res["attn_ms"] / 1e3) / 1e9
+        out["roofline"] = {"bound": "hbm", "kernel": "attn_decode_kernel (Tier-2 F2, one layer)",
+                           "achieved": ach, "peak": hbm, "unit": "GB/s", "frac": ach / hbm,
+                           "peak_kind": peak_kind, "traffic": None, "algorithmic_bytes": ab,
+                           "duration_us": res["attn_ms"] * 1e3, "frac_of_8TBs": ach / 8000.0}
+        gb = gemm_layer_bytes(spec, wl["batch"])
+        gach = gb / (res["na_ms"] / 1e3) / 1e9
+        out["roofline_nonattention"] = {"bound": "hbm", "kernels": "Tier-1 F1+F3 of one layer (rmsnorm x2 + 4 "
+                                        "tcgen05 GEMMs)", "achieved": gach, "peak": hbm, "unit": "GB/s",
+                                        "frac": gach / hbm, "duration_us": res["na_ms"] * 1e3,
+                                        "algorithmic_bytes": gb}
+        step_bytes = spec.n_layers * (ab + gb) + spec.dtype_bytes * 2 * spec.vocab_size * spec.d_model // 2
+        out["step_roofline"] = {"bytes_per_step": step_bytes, "ideal_ms": step_bytes / (hbm * 1e9) * 1e3,
+                                "frac": step_bytes / (hbm * 1e9) / (res["ms"] / 1e3)}
+    if not args.no_cpu_baseline and rank == 0:
+        B = wl["batch"] if wl["kp"] == 0 else min(wl["batch"], 64)
+        v, sample, cores, _ = cpu_sample(spec, B, wl["ctx"], args.cpu_threads)
+        out["cpu_baseline"] = {"value": v, "unit": "tokens/s", "cores": cores, "kind": "port", "sample": sample}
+    print(json.dumps(out))
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

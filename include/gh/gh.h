@@ -216,6 +216,13 @@ gh_tier2* gh_engine_tier2(gh_engine* e);
 /* Launch count of this library's kernels since the last reset (device work accounting). */
 uint64_t gh_kernel_launches(int reset);
 
+/* ------------------------------------------------------------------ diagnostics
+ * Microbenchmark of the Tier-1 tcgen05 GEMM on device 0: Y[B,N] = X[B,K] W[N,K]^T (bf16) with
+ * the plain-store epilogue.  flags = GEMM_DBG_* bits (1 no MMA, 2 no activation loads, 4 no L2
+ * cache hints, 8 no epilogue); stages / grid 0 = the production choice (grid = persistent CTAs).  Returns the mean device
+ * time per launch over `reps` launches (CUDA events) in *us. */
+gh_status gh_debug_gemm_bench(int N, int K, int B, int flags, int stages, int grid, int reps, float* us);
+
 #ifdef __cplusplus
 }
 #endif

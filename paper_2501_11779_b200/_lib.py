@@ -114,6 +114,7 @@ PROTOTYPES = {
     "gh_engine_tier1": (vp, [vp]),
     "gh_engine_tier2": (vp, [vp]),
     "gh_kernel_launches": (u64, [C.c_int]),
+    "gh_debug_gemm_bench": (st, [C.c_int] * 7 + [P(C.c_float)]),
 }
 
 _lib = None

@@ -56,6 +56,21 @@ template <> GH_DEV void chunk_to_f32<bf16_t>(const uint4& c, float* f) {
   }
 }
 
+// out = f * g * s packed back into a 16-byte chunk of the storage type
+template <typename T> GH_DEV void pack_f32(const float* f, const float* g, float s, uint4& o);
+template <> GH_DEV void pack_f32<float>(const float* f, const float* g, float s, uint4& o) {
+  o.x = __float_as_uint(f[0] * s * g[0]); o.y = __float_as_uint(f[1] * s * g[1]);
+  o.z = __float_as_uint(f[2] * s * g[2]); o.w = __float_as_uint(f[3] * s * g[3]);
+}
+template <> GH_DEV void pack_f32<bf16_t>(const float* f, const float* g, float s, uint4& o) {
+  uint32_t w[4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+    w[i] = (uint32_t)f32_to_bf16(f[2 * i] * s * g[2 * i]) |
+           ((uint32_t)f32_to_bf16(f[2 * i + 1] * s * g[2 * i + 1]) << 16);
+  o = make_uint4(w[0], w[1], w[2], w[3]);
+}
+
 template <typename T, int DH>
 __global__ void __launch_bounds__(AttnCfg<T, DH>::kThreads, 1)
     attn_decode_kernel(const AttnArgs a) {

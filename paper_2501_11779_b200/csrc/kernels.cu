@@ -28,27 +28,29 @@ uint64_t& launch_counter() {
 static float ih_k(double std_) { return (float)(1.7320508075688772 * std_ / 16777216.0); }
 
 template <typename T>
-__global__ void init_matrix_kernel(T* dst, uint64_t base, uint64_t n, float k) {
-  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
-       i += (uint64_t)gridDim.x * blockDim.x)
-    St<T>::store(dst, i, randn_scaled(base, i, k));
-}
-template <>
-__global__ void init_matrix_kernel<float>(float* dst, uint64_t base, uint64_t n, float k) {
-  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
-       i += (uint64_t)gridDim.x * blockDim.x)
-    dst[i] = randn_scaled(base, i, k);
-}
-
-template <typename T>
-__global__ void init_interleaved_kernel(T* dst, uint64_t base_even, uint64_t base_odd,
-                                        uint64_t pairs, uint64_t cols, float k) {
-  const uint64_t n = 2 * pairs * cols;
-  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
+__global__ void init_weight_kernel(T* dst, uint64_t n_phys, int N, int K, int KB, int tiled, RowSegs sg) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n_phys;
        i += (uint64_t)gridDim.x * blockDim.x) {
-    const uint64_t r = i / cols, c = i % cols;
-    const uint64_t logical = (r >> 1) * cols + c;
-    St<T>::store(dst, i, randn_scaled((r & 1) ? base_odd : base_even, logical, k));
+    int n, k;
+    if (tiled) {
+      const uint64_t tile = i >> 13, w = i & 8191;
+      n = (int)((tile / KB) * 128 + (w >> 6));
+      k = (int)((tile % KB) * 64 + (w & 63));
+    } else {
+      n = (int)(i / K);
+      k = (int)(i % K);
+    }
+    float v = 0.f;
+    if (n < N && k < K) {
+      int seg, r;
+      if (sg.interleave2) { seg = n & 1; r = n >> 1; }
+      else {
+        seg = 0; r = n;
+        while (seg + 1 < sg.n && r >= sg.rows[seg]) { r -= sg.rows[seg]; ++seg; }
+      }
+      v = randn_scaled(sg.base[seg], (uint64_t)r * K + k, sg.k[seg]);
+    }
+    St<T>::store(dst, i, v);
   }
 }
 
@@ -87,26 +89,26 @@ static int grid_for(uint64_t n) {
   return (int)std::min<uint64_t>(g, (uint64_t)kNumSMs * 32);
 }
 
-cudaError_t launch_init_matrix(int db, void* dst, uint64_t seed, uint64_t tid, uint64_t rows,
-                               uint64_t cols, double std_, cudaStream_t st) {
-  const uint64_t n = rows * cols;
-  const uint64_t base = tensor_base(seed, tid);
-  GH_COUNT_LAUNCH();
-  if (db == 4) init_matrix_kernel<float><<<grid_for(n), 256, 0, st>>>((float*)dst, base, n, ih_k(std_));
-  else init_matrix_kernel<bf16_t><<<grid_for(n), 256, 0, st>>>((bf16_t*)dst, base, n, ih_k(std_));
-  return cudaGetLastError();
+RowSegs make_segs(uint64_t seed, int n, const uint64_t* tids, const int* rows, const double* stds,
+                  bool interleave2) {
+  RowSegs sg{};
+  sg.n = n;
+  sg.interleave2 = interleave2 ? 1 : 0;
+  for (int i = 0; i < n; ++i) {
+    sg.base[i] = tensor_base(seed, tids[i]);
+    sg.rows[i] = rows[i];
+    sg.k[i] = ih_k(stds[i]);
+  }
+  return sg;
 }
 
-cudaError_t launch_init_interleaved(int db, void* dst, uint64_t seed, uint64_t tid_even,
-                                    uint64_t tid_odd, uint64_t pairs, uint64_t cols, double std_,
-                                    cudaStream_t st) {
-  const uint64_t n = 2 * pairs * cols;
-  const uint64_t be = tensor_base(seed, tid_even), bo = tensor_base(seed, tid_odd);
+cudaError_t launch_init_weight(const Weight& W, const RowSegs& sg, cudaStream_t st) {
+  const uint64_t n = W.elems();
   GH_COUNT_LAUNCH();
-  if (db == 4)
-    init_interleaved_kernel<float><<<grid_for(n), 256, 0, st>>>((float*)dst, be, bo, pairs, cols, ih_k(std_));
+  if (W.dtype_bytes == 4)
+    init_weight_kernel<float><<<grid_for(n), 256, 0, st>>>((float*)W.ptr, n, W.N, W.K, W.kb(), W.tiled, sg);
   else
-    init_interleaved_kernel<bf16_t><<<grid_for(n), 256, 0, st>>>((bf16_t*)dst, be, bo, pairs, cols, ih_k(std_));
+    init_weight_kernel<bf16_t><<<grid_for(n), 256, 0, st>>>((bf16_t*)W.ptr, n, W.N, W.K, W.kb(), W.tiled, sg);
   return cudaGetLastError();
 }
 
@@ -133,33 +135,49 @@ cudaError_t launch_fill_kv(int db, void* arena, uint64_t seed, int l0, int l1, i
 
 // ====================================================================== rmsnorm / embed
 // y = x * rsqrt(mean(x^2) + eps) * w  (one CTA per row; fp32 math, storage-dtype result).
+// 16-byte vector loads, the row stays in registers between the reduction and the scaling.
 // Optionally copies the input row to copy_out (the x slot of the fwd message).
-template <typename T>
-__global__ void rmsnorm_kernel(const T* x, long ldx, const T* w, T* y, long ldy, T* copy_out,
-                               long ldc, int D, float eps) {
+template <typename T, int kMaxVec>
+__global__ void __launch_bounds__(128) rmsnorm_kernel(const T* x, long ldx, const T* w, T* y, long ldy,
+                                                      T* copy_out, long ldc, int D, float eps) {
+  constexpr int kV = 16 / sizeof(T);
   const int b = blockIdx.x;
-  const T* xr = x + (long)b * ldx;
-  __shared__ float red[32];
+  const int nv = D / kV;
+  const uint4* xr = (const uint4*)(x + (long)b * ldx);
+  __shared__ float red[4];
+  uint4 buf[kMaxVec];
   float ss = 0.f;
-  for (int i = threadIdx.x; i < D; i += blockDim.x) {
-    const float v = St<T>::load(xr, i);
-    ss = fmaf(v, v, ss);
+#pragma unroll
+  for (int j = 0; j < kMaxVec; ++j) {
+    const int i = threadIdx.x + j * 128;
+    if (i < nv) {
+      buf[j] = xr[i];
+      float f[kV];
+      chunk_to_f32<T>(buf[j], f);
+#pragma unroll
+      for (int e = 0; e < kV; ++e) ss = fmaf(f[e], f[e], ss);
+    }
   }
   ss = warp_sum(ss);
   if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = ss;
   __syncthreads();
-  if (threadIdx.x < 32) {
-    float t = threadIdx.x < (blockDim.x >> 5) ? red[threadIdx.x] : 0.f;
-    t = warp_sum(t);
-    if (threadIdx.x == 0) red[0] = t;
-  }
-  __syncthreads();
-  const float inv = 1.0f / sqrtf(red[0] / (float)D + eps);
-  T* yr = y + (long)b * ldy;
-  for (int i = threadIdx.x; i < D; i += blockDim.x) {
-    const float v = St<T>::load(xr, i);
-    St<T>::store(yr, i, v * inv * St<T>::load(w, i));
-    if (copy_out) copy_out[(long)b * ldc + i] = xr[i];
+  const float tot = (red[0] + red[1]) + (red[2] + red[3]);
+  const float inv = 1.0f / sqrtf(tot / (float)D + eps);
+  const uint4* wr = (const uint4*)w;
+  uint4* yr = (uint4*)(y + (long)b * ldy);
+  uint4* cr = copy_out ? (uint4*)(copy_out + (long)b * ldc) : nullptr;
+#pragma unroll
+  for (int j = 0; j < kMaxVec; ++j) {
+    const int i = threadIdx.x + j * 128;
+    if (i < nv) {
+      float f[kV], g[kV];
+      chunk_to_f32<T>(buf[j], f);
+      chunk_to_f32<T>(wr[i], g);
+      uint4 o;
+      pack_f32<T>(f, g, inv, o);
+      yr[i] = o;
+      if (cr) cr[i] = buf[j];
+    }
   }
 }
 
@@ -167,12 +185,17 @@ cudaError_t launch_rmsnorm(int db, const void* x, long ldx, const void* w, void*
                            void* copy_out, long ldc, int B, int D, float eps, cudaStream_t st) {
   if (B <= 0) return cudaSuccess;
   GH_COUNT_LAUNCH();
+  const int nv = D * db / 16;
+  if (nv > 128 * 16 || (D * db) % 16) return cudaErrorInvalidValue;
   if (db == 4)
-    rmsnorm_kernel<float><<<B, 256, 0, st>>>((const float*)x, ldx, (const float*)w, (float*)y, ldy,
-                                             (float*)copy_out, ldc, D, eps);
+    rmsnorm_kernel<float, 16><<<B, 128, 0, st>>>((const float*)x, ldx, (const float*)w, (float*)y, ldy,
+                                                 (float*)copy_out, ldc, D, eps);
+  else if (nv <= 128 * 4)
+    rmsnorm_kernel<bf16_t, 4><<<B, 128, 0, st>>>((const bf16_t*)x, ldx, (const bf16_t*)w, (bf16_t*)y, ldy,
+                                                 (bf16_t*)copy_out, ldc, D, eps);
   else
-    rmsnorm_kernel<bf16_t><<<B, 256, 0, st>>>((const bf16_t*)x, ldx, (const bf16_t*)w, (bf16_t*)y, ldy,
-                                              (bf16_t*)copy_out, ldc, D, eps);
+    rmsnorm_kernel<bf16_t, 16><<<B, 128, 0, st>>>((const bf16_t*)x, ldx, (const bf16_t*)w, (bf16_t*)y, ldy,
+                                                  (bf16_t*)copy_out, ldc, D, eps);
   return cudaGetLastError();
 }
 
@@ -314,62 +337,43 @@ cudaError_t make_tmap_bf16(CUtensorMap* out, const void* base, uint64_t rows, ui
 }
 
 static const int kBNs[] = {16, 32, 48, 64, 96, 128, 192, 256};
-static int ctas_per_sm(int BN) { return BN <= 96 ? 2 : 1; }
+static int stages_override = 0;  // diagnostics
 
 GemmPlan plan_gemm(int N, int K, int Bt) {
   GemmPlan p;
-  int bt_cap = std::min(Bt, 256);
+  const int bt_cap = std::min(Bt, 256);
   p.BN = 256;
   for (int bn : kBNs) if (bn >= bt_cap) { p.BN = bn; break; }
   p.b_tiles = (Bt + p.BN - 1) / p.BN;
   p.n_tiles = (N + kBlockM - 1) / kBlockM;
-  const int kb_total = (K + kBlockK - 1) / kBlockK;
-  const int tiles = p.n_tiles * p.b_tiles;
-  const int slots = kNumSMs * ctas_per_sm(p.BN);
-  // time model (arbitrary units): streaming time of the busiest SM + split fix-up reads
-  const double tile_bytes = (double)kBlockM * K * 2 + (double)p.BN * K * 2;
-  const double partial = (double)kBlockM * p.BN * 4;
-  double best = 1e300;
-  int best_ks = 1;
-  const int ks_max = std::max(1, std::min(16, kb_total / 4));
-  for (int ks = 1; ks <= ks_max; ++ks) {
-    const int ctas = tiles * ks;
-    const int waves = (ctas + slots - 1) / slots;
-    const int per_sm = std::min(ctas_per_sm(p.BN), (ctas + kNumSMs - 1) / kNumSMs);
-    const double stream = waves * (tile_bytes / ks) * per_sm / 44.0;  // ns @ 44 GB/s per SM
-    const double fix = ks > 1 ? (ks * partial) / 100.0 + 1500.0 : 0.0;  // ns
-    const double t = stream + fix;
-    if (t < best * 0.97) { best = t; best_ks = ks; }
-  }
-  p.ks = best_ks;
-  if (p.ks > 1) {
-    p.ws_floats = (size_t)tiles * p.ks * kBlockM * p.BN;
-    p.tickets = (size_t)tiles;
-  }
+  const long KB = (K + kBlockK - 1) / kBlockK;
+  const long T = (long)p.n_tiles * p.b_tiles * KB;
+  p.grid = (int)std::min<long>(kNumSMs, T);
+  // a tile of KB iterations spans at most ceil(KB * G / T) + 1 CTAs
+  p.max_pieces = (int)((KB * p.grid + T - 1) / T) + 1;
+  p.ws_floats = (size_t)p.n_tiles * p.b_tiles * p.max_pieces * kBlockM * p.BN;
+  p.tickets = (size_t)p.n_tiles * p.b_tiles;
   return p;
 }
 
-// pipeline depth per batch tile: <= ~113 KB (2 CTAs / SM) for BN <= 96, else ~200 KB
-template <int BN> struct TcStages {
-  static constexpr int value = (BN == 16) ? 6 : (BN == 32 || BN == 48) ? 5
-                             : (BN == 64 || BN == 96) ? 4 : (BN == 128) ? 6 : (BN == 192) ? 5 : 4;
-};
 template <int BN>
 static cudaError_t configure_tc() {
-  constexpr int S = TcStages<BN>::value;
-  return cudaFuncSetAttribute(gemm_tc_kernel<BN, S>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                              GemmSmem<BN, S>::kTotal);
+  return cudaFuncSetAttribute(gemm_tc_kernel<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
 }
 template <int BN>
-static cudaError_t launch_tc(const CUtensorMap* tmW, const CUtensorMap* tmX, const GemmShape& gs,
+static cudaError_t launch_tc(const CUtensorMap* tmW, const CUtensorMap* tmX, GemmShape gs,
                              const GemmPlan& p, const EpiParams& ep, cudaStream_t st) {
-  constexpr int S = TcStages<BN>::value;
-  using L = GemmSmem<BN, S>;
-  dim3 grid(p.n_tiles, p.b_tiles, p.ks);
+  using L = GemmSmem<BN>;
+  const int smax = L::max_stages(227 * 1024);
+  gs.stages = std::max(2, std::min(smax, stages_override ? stages_override : smax));
+  const int smem = L::bytes(gs.stages);
+  if (smem > 227 * 1024) return cudaErrorInvalidValue;
   GH_COUNT_LAUNCH();
-  gemm_tc_kernel<BN, S><<<grid, kGemmThreads, L::kTotal, st>>>(*tmW, *tmX, gs, ep);
+  gemm_tc_kernel<BN><<<p.grid, kGemmThreads, smem, st>>>(*tmW, *tmX, gs, ep);
   return cudaGetLastError();
 }
+
+void gemm_debug_set(int stages) { stages_override = stages; }
 
 cudaError_t launch_gemm(const Weight& W, const CUtensorMap* tmW, const void* X, long ldx,
                         const CUtensorMap* tmX, int Bt, const GemmPlan& p, const EpiParams& ep,
@@ -391,10 +395,13 @@ cudaError_t launch_gemm(const Weight& W, const CUtensorMap* tmW, const void* X, 
     return cudaGetLastError();
   }
   GemmShape gs;
-  gs.N = W.N; gs.K = W.K; gs.Bt = Bt; gs.ks = p.ks;
+  gs.N = W.N; gs.K = W.K; gs.Bt = Bt;
+  gs.n_tiles = p.n_tiles; gs.b_tiles = p.b_tiles;
   gs.kb_total = (W.K + kBlockK - 1) / kBlockK;
+  gs.max_pieces = p.max_pieces;
   gs.ws = sc.ws; gs.tickets = sc.tickets;
-  if (p.ks > 1 && (p.ws_floats > sc.ws_floats || p.tickets > sc.n_tickets)) return cudaErrorInvalidValue;
+  gs.flags = sc.debug_flags;
+  if (p.ws_floats > sc.ws_floats || p.tickets > sc.n_tickets) return cudaErrorInvalidValue;
   switch (p.BN) {
     case 16: return launch_tc<16>(tmW, tmX, gs, p, ep, st);
     case 32: return launch_tc<32>(tmW, tmX, gs, p, ep, st);
@@ -411,8 +418,11 @@ cudaError_t launch_gemm(const Weight& W, const CUtensorMap* tmW, const void* X, 
 // ====================================================================== attention dispatch
 template <typename T, int DH>
 static cudaError_t configure_attn() {
-  return cudaFuncSetAttribute(attn_decode_kernel<T, DH>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                              AttnCfg<T, DH>::kSmem);
+  cudaError_t e = cudaFuncSetAttribute(attn_decode_kernel<T, DH>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       AttnCfg<T, DH>::kSmem);
+  if (e != cudaSuccess) return e;
+  return cudaFuncSetAttribute(attn_decode_kernel<T, DH>, cudaFuncAttributePreferredSharedMemoryCarveout,
+                              (int)cudaSharedmemCarveoutMaxShared);
 }
 template <typename T, int DH>
 static cudaError_t launch_attn_t(const AttnArgs& a, cudaStream_t st) {

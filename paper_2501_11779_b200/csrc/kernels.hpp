@@ -8,20 +8,40 @@ namespace gh {
 
 struct EpiParams;
 
-// Dense weight matrix W[N, K] (row-major, K contiguous) in device memory.
+// Dense weight matrix W[N, K] in device memory.
+//  row-major (K contiguous) for fp32 storage;
+//  "tile-contiguous" for bf16 (tcgen05 operand): W is cut into 128 x 64 tiles (rows x K), tile
+//  (nt, kb) is one contiguous 16 KB block at ((nt * KB + kb) * 128 + r) * 64 + c, zero padded to
+//  N_pad = ceil(N/128)*128 and KB = ceil(K/64).  Every TMA box of the GEMM mainloop is therefore
+//  one contiguous 16 KB burst of HBM instead of 128 segments of 128 B strided by K.
 struct Weight {
   void* ptr = nullptr;
   int N = 0, K = 0;
   int dtype_bytes = 2;
+  bool tiled = false;
+  int n_pad() const { return (N + 127) / 128 * 128; }
+  int kb() const { return (K + 63) / 64; }
+  size_t elems() const { return tiled ? (size_t)n_pad() * kb() * 64 : (size_t)N * K; }
 };
 
-// Per-GEMM launch plan (split-K factor, batch tile) chosen on the host.
+// Logical source rows of a weight: up to 3 stacked synthetic tensors (e.g. Wq|Wk|Wv), or two
+// row-interleaved tensors (W1/W3: physical row 2f = gate f, 2f+1 = up f).
+struct RowSegs {
+  uint64_t base[3];   // tensor_base(seed, tid) per segment
+  int rows[3];        // logical rows per segment (stacked mode)
+  float k[3];         // sqrt(3) * std / 2^24 per segment
+  int n = 1;
+  int interleave2 = 0;
+};
+
+// Per-GEMM launch plan chosen on the host: batch tile and persistent stream-K grid.
 struct GemmPlan {
-  int BN = 0;       // batch tile (16..256)
-  int ks = 1;       // K splits
-  int n_tiles = 0;  // ceil(N / 128)
+  int BN = 0;         // batch tile (16..256)
+  int n_tiles = 0;    // ceil(N / 128)
   int b_tiles = 0;
-  size_t ws_floats = 0;   // split workspace
+  int grid = 0;       // persistent CTAs (<= 148)
+  int max_pieces = 1;
+  size_t ws_floats = 0;   // stream-K partial workspace
   size_t tickets = 0;
 };
 GemmPlan plan_gemm(int N, int K, int Bt);
@@ -31,7 +51,9 @@ struct GemmScratch {
   float* ws = nullptr;     size_t ws_floats = 0;
   int* tickets = nullptr;  size_t n_tickets = 0;
   float* stage = nullptr;  size_t stage_floats = 0;  // SIMT path fp32 result [Bt][N]
+  int debug_flags = 0;                                // GEMM_DBG_* (diagnostics only)
 };
+void gemm_debug_set(int stages);  // 0 = production pipeline depth
 
 // Encode a 2-D bf16 tensor map over a row-major [rows, cols] matrix with row stride ld
 // (elements), box {64, box_rows}, 128-byte swizzle.
@@ -63,11 +85,10 @@ bool attention_supported(int dtype_bytes, int d_head);
 // Logical matrix [rows, cols] of tensor `tid` with std `std_`; `row_map` selects which logical
 // row lands in physical row r: logical = r for map 0, interleave (r even -> gate r/2 of tidA,
 // r odd -> up r/2 of tidB) for map 1.
-cudaError_t launch_init_matrix(int dtype_bytes, void* dst, uint64_t seed, uint64_t tid,
-                               uint64_t rows, uint64_t cols, double std_, cudaStream_t st);
-cudaError_t launch_init_interleaved(int dtype_bytes, void* dst, uint64_t seed, uint64_t tid_even,
-                                    uint64_t tid_odd, uint64_t pairs, uint64_t cols, double std_,
-                                    cudaStream_t st);
+RowSegs make_segs(uint64_t seed, int n, const uint64_t* tids, const int* rows, const double* stds,
+                  bool interleave2);
+// Generate W (logical [N, K] from `segs`) in W's layout (row-major or tile-contiguous).
+cudaError_t launch_init_weight(const Weight& W, const RowSegs& segs, cudaStream_t st);
 cudaError_t launch_fill_const(int dtype_bytes, void* dst, uint64_t n, float v, cudaStream_t st);
 // Fill positions [0, npos) of K and V blocks of `n_slots` slots for layers [l0, l1).
 cudaError_t launch_fill_kv(int dtype_bytes, void* arena, uint64_t seed, int l0, int l1,

@@ -30,11 +30,15 @@ struct EpiParams {
 
 struct GemmShape {
   int N, K, Bt;         // weight rows, reduction length, batch
-  int ks;               // K splits (>= 1)
-  int kb_total;         // ceil(K / 64)
-  float* ws;            // split workspace (ks > 1)
-  int* tickets;         // per output tile counters (ks > 1), zero between launches
+  int n_tiles, b_tiles; // 128-row weight tiles x BN-column batch tiles
+  int kb_total;         // KB = ceil(K / 64)
+  int max_pieces;       // upper bound of CTAs sharing one tile (workspace slots per tile)
+  float* ws;            // stream-K partial workspace [tiles][max_pieces][128 x BN]
+  int* tickets;         // per tile arrival counters, zero between launches
+  int stages;           // TMA -> MMA pipeline depth (shared-memory ring)
+  int flags;            // diagnostics (GEMM_DBG_*), 0 in production
 };
+enum GemmDbg : int { GEMM_DBG_NO_MMA = 1, GEMM_DBG_NO_X = 2, GEMM_DBG_NO_HINT = 4, GEMM_DBG_NO_EPI = 8 };
 
 struct AttnArgs {
   const void* msg_fwd;  // [B][2D + 2Dkv]

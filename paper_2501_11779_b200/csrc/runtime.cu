@@ -142,13 +142,17 @@ static EpiParams epi_default() {
   return e;
 }
 
-static gh_status init_weight(gh_tier1* t, Weight* w, int N, int K, CUtensorMap* tm) {
+// tm != nullptr: a tcgen05 GEMM operand -> tile-contiguous layout for bf16 (kernels.hpp Weight)
+static gh_status init_weight(gh_tier1* t, Weight* w, int N, int K, CUtensorMap* tm, const RowSegs& segs) {
   w->N = N; w->K = K; w->dtype_bytes = t->sh.db;
-  GH_TRY(dev_alloc(t->mem, (size_t)N * K * t->sh.db, &w->ptr));
-  if (tm && t->sh.db == 2) {
-    cudaError_t e = make_tmap_bf16(tm, w->ptr, (uint64_t)N, (uint64_t)K, (uint64_t)K, 128);
+  w->tiled = tm != nullptr && t->sh.db == 2;
+  GH_TRY(dev_alloc(t->mem, w->elems() * t->sh.db, &w->ptr));
+  if (w->tiled) {
+    const uint64_t rows = (uint64_t)w->n_pad() * w->kb();
+    cudaError_t e = make_tmap_bf16(tm, w->ptr, rows, 64, 64, 128);
     if (e != cudaSuccess) return fail(GH_ECUDA, "cuTensorMapEncodeTiled failed (weights)");
   }
+  GH_CUDA(launch_init_weight(*w, segs, 0));
   return GH_OK;
 }
 
@@ -198,18 +202,27 @@ gh_status gh_tier1_create(const gh_model_spec* spec, int device, uint32_t layer_
   t->layers.resize(layer_end - layer_begin);
   for (uint32_t l = layer_begin; l < layer_end; ++l) {
     auto& L = t->layers[l - layer_begin];
-    GH_TRY(init_weight(t.get(), &L.qkv, D + 2 * Dkv, D, &L.tm_qkv));
-    GH_TRY(init_weight(t.get(), &L.o, D, D, &L.tm_o));
-    GH_TRY(init_weight(t.get(), &L.w13, 2 * Dh, D, &L.tm_13));
-    GH_TRY(init_weight(t.get(), &L.w2, D, Dh, &L.tm_2));
     const double sD = 1.0 / std::sqrt((double)D), sH = 1.0 / std::sqrt((double)Dh);
-    char* q = (char*)L.qkv.ptr;
-    GH_CUDA(launch_init_matrix(db, q, seed, tid_layer(l, kWq), D, D, sD, st));
-    GH_CUDA(launch_init_matrix(db, q + (size_t)D * D * db, seed, tid_layer(l, kWk), Dkv, D, sD, st));
-    GH_CUDA(launch_init_matrix(db, q + (size_t)(D + Dkv) * D * db, seed, tid_layer(l, kWv), Dkv, D, sD, st));
-    GH_CUDA(launch_init_matrix(db, L.o.ptr, seed, tid_layer(l, kWo), D, D, sD, st));
-    GH_CUDA(launch_init_interleaved(db, L.w13.ptr, seed, tid_layer(l, kW1), tid_layer(l, kW3), Dh, D, sD, st));
-    GH_CUDA(launch_init_matrix(db, L.w2.ptr, seed, tid_layer(l, kW2), D, Dh, sH, st));
+    {
+      const uint64_t tq[3] = {tid_layer(l, kWq), tid_layer(l, kWk), tid_layer(l, kWv)};
+      const int rq[3] = {D, Dkv, Dkv};
+      const double sq[3] = {sD, sD, sD};
+      GH_TRY(init_weight(t.get(), &L.qkv, D + 2 * Dkv, D, &L.tm_qkv, make_segs(seed, 3, tq, rq, sq, false)));
+    }
+    {
+      const uint64_t to = tid_layer(l, kWo); const int ro = D; const double so = sD;
+      GH_TRY(init_weight(t.get(), &L.o, D, D, &L.tm_o, make_segs(seed, 1, &to, &ro, &so, false)));
+    }
+    {
+      const uint64_t t13[2] = {tid_layer(l, kW1), tid_layer(l, kW3)};
+      const int r13[2] = {Dh, Dh};
+      const double s13[2] = {sD, sD};
+      GH_TRY(init_weight(t.get(), &L.w13, 2 * Dh, D, &L.tm_13, make_segs(seed, 2, t13, r13, s13, true)));
+    }
+    {
+      const uint64_t t2 = tid_layer(l, kW2); const int r2 = D; const double s2 = sH;
+      GH_TRY(init_weight(t.get(), &L.w2, D, Dh, &L.tm_2, make_segs(seed, 1, &t2, &r2, &s2, false)));
+    }
     GH_TRY(dev_alloc(t->mem, (size_t)D * db, &L.attn_norm));
     GH_TRY(dev_alloc(t->mem, (size_t)D * db, &L.ffn_norm));
     GH_CUDA(launch_fill_const(db, L.attn_norm, D, 1.0f, st));
@@ -218,12 +231,12 @@ gh_status gh_tier1_create(const gh_model_spec* spec, int device, uint32_t layer_
   t->has_embed = layer_begin == 0;
   t->has_cls = layer_end == (uint32_t)sh.N;
   if (t->has_embed) {
-    GH_TRY(init_weight(t.get(), &t->embed, V, D, nullptr));
-    GH_CUDA(launch_init_matrix(db, t->embed.ptr, seed, kTidEmbed, V, D, 1.0, st));
+    const uint64_t te = kTidEmbed; const int re = V; const double se = 1.0;
+    GH_TRY(init_weight(t.get(), &t->embed, V, D, nullptr, make_segs(seed, 1, &te, &re, &se, false)));
   }
   if (t->has_cls) {
-    GH_TRY(init_weight(t.get(), &t->cls, V, D, &t->tm_cls));
-    GH_CUDA(launch_init_matrix(db, t->cls.ptr, seed, kTidCls, V, D, 1.0 / std::sqrt((double)D), st));
+    const uint64_t tc = kTidCls; const int rc = V; const double sc = 1.0 / std::sqrt((double)D);
+    GH_TRY(init_weight(t.get(), &t->cls, V, D, &t->tm_cls, make_segs(seed, 1, &tc, &rc, &sc, false)));
     GH_TRY(dev_alloc(t->mem, (size_t)D * db, &t->final_norm));
     GH_CUDA(launch_fill_const(db, t->final_norm, D, 1.0f, st));
   }
@@ -851,3 +864,54 @@ gh_status gh_engine_step_host(gh_engine* e, uint32_t ib, const int32_t* tok_host
 }
 
 }  // extern "C"
+
+extern "C" gh_status gh_debug_gemm_bench(int N, int K, int B, int flags, int stages, int ks, int reps, float* us) {
+  if (!us || N <= 0 || K <= 0 || B <= 0 || reps <= 0) return fail(GH_EINVAL, "bad argument");
+  if (gh_device_count() == 0) return fail(GH_ECUDA, "no CUDA device");
+  GH_CUDA(cudaSetDevice(0));
+  GH_CUDA(configure_kernels());
+  std::vector<std::unique_ptr<DevMem>> mem;
+  Weight W;
+  W.N = N; W.K = K; W.dtype_bytes = 2; W.tiled = true;
+  GH_TRY(dev_alloc(mem, W.elems() * 2, &W.ptr));
+  const uint64_t tid = 7; const int rows = N; const double sd = 0.02;
+  GH_CUDA(launch_init_weight(W, make_segs(1, 1, &tid, &rows, &sd, false), 0));
+  CUtensorMap tmW, tmX;
+  GH_CUDA(make_tmap_bf16(&tmW, W.ptr, (uint64_t)W.n_pad() * W.kb(), 64, 64, 128));
+  void *X, *Y;
+  GH_TRY(dev_alloc(mem, (size_t)B * K * 2, &X));
+  GH_TRY(dev_alloc(mem, (size_t)B * N * 2, &Y));
+  GH_CUDA(cudaMemset(X, 0, (size_t)B * K * 2));
+  GemmPlan p = plan_gemm(N, K, B);
+  if (ks > 0) {  // diagnostics: override the persistent grid size
+    const long T = (long)p.n_tiles * p.b_tiles * ((K + 63) / 64);
+    p.grid = (int)std::min<long>(ks, T);
+    p.max_pieces = (int)((((K + 63) / 64) * (long)p.grid + T - 1) / T) + 1;
+    p.ws_floats = (size_t)p.n_tiles * p.b_tiles * p.max_pieces * 128 * p.BN;
+  }
+  GH_CUDA(make_tmap_bf16(&tmX, X, (uint64_t)B, (uint64_t)K, (uint64_t)K, (uint32_t)p.BN));
+  GemmScratch sc;
+  void* q;
+  sc.ws_floats = std::max<size_t>(p.ws_floats, 4);
+  GH_TRY(dev_alloc(mem, sc.ws_floats * 4, &q)); sc.ws = (float*)q;
+  sc.n_tickets = std::max<size_t>(p.tickets, 1);
+  GH_TRY(dev_alloc(mem, sc.n_tickets * 4, &q)); sc.tickets = (int*)q;
+  GH_CUDA(cudaMemset(q, 0, sc.n_tickets * 4));
+  sc.debug_flags = flags;
+  EpiParams ep = epi_default();
+  ep.kind = EPI_STORE; ep.out = Y; ep.ldo = N;
+  gemm_debug_set(stages);
+  cudaEvent_t e0, e1;
+  GH_CUDA(cudaEventCreate(&e0)); GH_CUDA(cudaEventCreate(&e1));
+  for (int i = 0; i < 3; ++i) GH_CUDA(launch_gemm(W, &tmW, X, K, &tmX, B, p, ep, sc, 0));
+  GH_CUDA(cudaEventRecord(e0, 0));
+  for (int i = 0; i < reps; ++i) GH_CUDA(launch_gemm(W, &tmW, X, K, &tmX, B, p, ep, sc, 0));
+  GH_CUDA(cudaEventRecord(e1, 0));
+  GH_CUDA(cudaEventSynchronize(e1));
+  float ms = 0;
+  GH_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+  cudaEventDestroy(e0); cudaEventDestroy(e1);
+  gemm_debug_set(0);
+  *us = ms * 1000.f / reps;
+  return GH_OK;
+}

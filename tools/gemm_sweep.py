@@ -1,0 +1,30 @@
+"""Sweep the tcgen05 GEMM mainloop (diagnostics): python tools/gemm_sweep.py"""
+import ctypes as C
+import sys
+from pathlib import Path
+
+sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
+import paper_2501_11779_b200 as gh  # noqa: E402
+from paper_2501_11779_b200 import _lib as L  # noqa: E402
+
+lib = gh.lib()
+
+
+def bench(N, K, B, flags=0, stages=0, grid=0, reps=20):
+    us = C.c_float()
+    L.check(lib.gh_debug_gemm_bench(N, K, B, flags, stages, grid, reps, C.byref(us)))
+    return us.value
+
+
+shapes = {"qkv": (12288, 4096), "o": (4096, 4096), "w13": (22016, 4096), "w2": (4096, 11008), "lm": (32000, 4096)}
+B = int(sys.argv[1]) if len(sys.argv) > 1 else 64
+for name, (N, K) in shapes.items():
+    wb = N * K * 2
+    base = bench(N, K, B)
+    row = [f"{name:4s} N={N:6d} K={K:6d} prod {base:7.1f}us {wb / base / 1e3:6.0f}GB/s"]
+    for label, kw in [("noMMA", dict(flags=1)), ("noX", dict(flags=2)), ("noHint", dict(flags=4)),
+                      ("noEpi", dict(flags=8)), ("noMMA+noEpi", dict(flags=9)), ("st4", dict(stages=4)),
+                      ("st6", dict(stages=6)), ("g132", dict(grid=132)), ("g74", dict(grid=74))]:
+        t = bench(N, K, B, **kw)
+        row.append(f"{label} {t:6.1f}")
+    print(" | ".join(row), flush=True)
