@@ -219,9 +219,16 @@ uint64_t gh_kernel_launches(int reset);
 /* ------------------------------------------------------------------ diagnostics
  * Microbenchmark of the Tier-1 tcgen05 GEMM on device 0: Y[B,N] = X[B,K] W[N,K]^T (bf16) with
  * the plain-store epilogue.  flags = GEMM_DBG_* bits (1 no MMA, 2 no activation loads, 4 no L2
- * cache hints, 8 no epilogue); stages / grid 0 = the production choice (grid = persistent CTAs).  Returns the mean device
+ * cache hints, 8 no epilogue); stages / cluster 0 = the production choice (cluster = CTAs per
+ * thread-block cluster = K splits per tile, 1/2/4/8).  Returns the mean device
  * time per launch over `reps` launches (CUDA events) in *us. */
-gh_status gh_debug_gemm_bench(int N, int K, int B, int flags, int stages, int grid, int reps, float* us);
+gh_status gh_debug_gemm_bench(int N, int K, int B, int flags, int stages, int cluster, int reps, float* us);
+/* Same, rotating over `copies` weight buffers (copies * N*K*2 bytes > L2 defeats L2 reuse) and,
+ * when trace != NULL, recording 16 globaltimer stamps per CTA of the last launch into trace
+ * (ns; 0 start, 1 weights prefetched, 2 after griddepcontrol.wait, 3 first stage landed,
+ * 4 last MMA issued, 5 epilogue done, 6 exit, 7.. epilogue phases of the last tile). */
+gh_status gh_debug_gemm_trace(int N, int K, int B, int copies, int reps, float* us,
+                              unsigned long long* trace, int trace_cap);
 
 #ifdef __cplusplus
 }

@@ -115,6 +115,7 @@ PROTOTYPES = {
     "gh_engine_tier2": (vp, [vp]),
     "gh_kernel_launches": (u64, [C.c_int]),
     "gh_debug_gemm_bench": (st, [C.c_int] * 7 + [P(C.c_float)]),
+    "gh_debug_gemm_trace": (st, [C.c_int] * 5 + [P(C.c_float), P(C.c_uint64), C.c_int]),
 }
 
 _lib = None

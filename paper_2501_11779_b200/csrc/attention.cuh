@@ -90,6 +90,8 @@ __global__ void __launch_bounds__(AttnCfg<T, DH>::kThreads, 1)
     fence_barrier_init();
   }
   __syncthreads();
+  griddep_launch_dependents();
+  griddep_wait();  // the fwd message (and the arena of the previous step) are now visible
 
   const T* fwd = (const T*)a.msg_fwd;
   T* bwd = (T*)a.msg_bwd;

@@ -74,6 +74,11 @@ GH_HD uint64_t tid_kv(uint64_t layer, uint64_t slot, uint64_t kv) {
 }
 
 // ------------------------------------------------------------------ misc device helpers
+GH_DEV unsigned long long globaltimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
 GH_DEV uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
 GH_DEV int lane_id() { return threadIdx.x & 31; }
 GH_DEV int warp_id() { return threadIdx.x >> 5; }
@@ -94,6 +99,15 @@ GH_DEV bool elect_one() {
       : "=r"(pred));
   return pred != 0;
 }
+
+// ------------------------------------------------------------------ programmatic dependent launch
+// Every decode-path kernel is launched with programmatic stream serialization: it lets its
+// dependents launch as soon as all of its CTAs have started (griddep_launch_dependents), and
+// waits for its predecessor's completion + memory visibility (griddep_wait) only before it reads
+// data the predecessor produced (weights and its own prologue overlap the predecessor's tail).
+// Both are no-ops when the kernel was launched without the attribute.
+GH_DEV void griddep_wait() { asm volatile("griddepcontrol.wait;\n" ::: "memory"); }
+GH_DEV void griddep_launch_dependents() { asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory"); }
 
 // ------------------------------------------------------------------ mbarrier
 GH_DEV void mbar_init(uint64_t* bar, uint32_t count) {
@@ -118,6 +132,47 @@ GH_DEV void mbar_wait(uint64_t* bar, uint32_t parity) {
       "@!P1 bra WAIT_%=;\n\t}\n" ::"r"(addr),
       "r"(parity)
       : "memory");
+}
+
+// ------------------------------------------------------------------ thread-block clusters / DSMEM
+GH_DEV uint32_t cluster_ctarank() { uint32_t r; asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r)); return r; }
+GH_DEV uint32_t cluster_nctarank() { uint32_t r; asm volatile("mov.u32 %0, %%cluster_nctarank;" : "=r"(r)); return r; }
+GH_DEV uint32_t cluster_id_x() { uint32_t r; asm volatile("mov.u32 %0, %%clusterid.x;" : "=r"(r)); return r; }
+GH_DEV uint32_t cluster_count_x() { uint32_t r; asm volatile("mov.u32 %0, %%nclusterid.x;" : "=r"(r)); return r; }
+// shared::cta address -> shared::cluster address of the same variable in CTA `rank`
+GH_DEV uint32_t mapa_shared(uint32_t saddr, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(saddr), "r"(rank));
+  return r;
+}
+// (volatile keeps it after the preceding mbarrier wait; no memory clobber so that a batch of
+// these loads can be issued back to back before their results are consumed)
+GH_DEV float4 ld_dsmem_f4(uint32_t caddr) {
+  float4 v;
+  asm volatile("ld.shared::cluster.v4.f32 {%0, %1, %2, %3}, [%4];"
+               : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(caddr));
+  return v;
+}
+// arrive (release, cluster scope) on an mbarrier that lives in another CTA of the cluster
+GH_DEV void mbar_arrive_cluster(uint32_t caddr) {
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(caddr) : "memory");
+}
+GH_DEV void mbar_wait_cluster(uint64_t* bar, uint32_t parity) {
+  uint32_t addr = smem_u32(bar);
+  asm volatile(
+      "{\n\t.reg .pred P1;\n"
+      "WAITC_%=:\n\t"
+      "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 P1, [%0], %1;\n\t"
+      "@!P1 bra WAITC_%=;\n\t}\n" ::"r"(addr),
+      "r"(parity)
+      : "memory");
+}
+GH_DEV void mbar_arrive_cluster_relaxed(uint32_t caddr) {
+  asm volatile("mbarrier.arrive.relaxed.cluster.shared::cluster.b64 _, [%0];" ::"r"(caddr) : "memory");
+}
+GH_DEV void fence_acq_rel_cluster() { asm volatile("fence.acq_rel.cluster;" ::: "memory"); }
+GH_DEV void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
 }
 
 // ------------------------------------------------------------------ bulk / tensor copies (TMA)

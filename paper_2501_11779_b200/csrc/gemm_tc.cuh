@@ -10,13 +10,17 @@
 // fp32 accumulator in TMEM; four epilogue warps drain TMEM with tcgen05.ld and apply the fused
 // epilogue (residual add, RoPE + message packing, SwiGLU, logits + partial argmax).
 //
-// Scheduling is persistent stream-K: the linearised (tile, k-block) iteration space is cut into
-// gridDim.x equal contiguous ranges, one per CTA (one CTA per SM), so every SM streams the same
-// number of weight bytes.  A CTA's range is a sequence of "segments" (a k-range of one tile).
-// The accumulator is double-buffered in TMEM so the epilogue of segment j overlaps the TMA/MMA
-// mainloop of segment j+1.  A tile cut across CTAs ("pieces") is combined deterministically:
-// each piece writes its fp32 partial to a workspace, the last piece to arrive (atomic ticket)
-// sums all pieces in piece order and runs the epilogue — no CTA ever waits for another.
+// Scheduling is persistent "cluster split-K": the grid is a set of thread-block clusters of C
+// CTAs (C in {1, 2, 4, 8}, chosen per GEMM shape on the host); cluster c processes output tiles
+// c, c + n_clusters, ... and CTA rank r of the cluster computes k-blocks [r*KB/C, (r+1)*KB/C) of
+// every tile it visits, so weights are streamed by up to all 148 SMs even when the GEMM has
+// fewer output tiles than SMs.  The accumulator is double-buffered in TMEM so the epilogue of
+// tile j overlaps the TMA/MMA mainloop of tile j+1.  The C fp32 partials of a tile are combined
+// through distributed shared memory: every CTA publishes its partial into its own shared
+// memory, signals its peers with remote mbarrier arrivals, then reduces a 128/C-row slice of the
+// tile by reading all C partials in rank order (deterministic) and runs the epilogue on that
+// slice with direct, coalesced global stores.  Clusters are gang-scheduled, so waiting on peers
+// can never deadlock, and no global workspace or atomics are involved.
 //
 // Warp roles (192 threads): warp 0 = TMA producer, warp 1 = TMEM allocator + MMA issuer,
 // warps 2..5 = epilogue (warp w drains TMEM lanes 32*(w%4) .. +31).
@@ -40,25 +44,6 @@ struct EpiSmem {
   static constexpr int kPos = 2 * kEpiCols * 256;
   static constexpr int kRed = kPos + kEpiCols * 4;
   static constexpr int kBytes = kRed + 512;
-};
-
-template <int BN>
-struct GemmSmem {
-  static constexpr int kABytes = kBlockM * kBlockK * 2;  // 16 KB
-  static constexpr int kBBytes = BN * kBlockK * 2;
-  static constexpr int kStageBytes = kABytes + kBBytes;
-  static constexpr int kMaxStages = 16;
-  static constexpr uint32_t kAccCols = BN < 32 ? 32 : BN;  // one accumulator buffer
-  static constexpr uint32_t kTmemCols = 2 * kAccCols <= 64 ? 64 : 2 * kAccCols <= 128 ? 128
-                                      : 2 * kAccCols <= 256 ? 256 : 512;
-  static constexpr int kBarBytes = (2 * kMaxStages + 4) * 8 + 16;
-  GH_HD static int epi_offset(int stages) { return stages * kStageBytes; }
-  GH_HD static int bar_offset(int stages) { return stages * kStageBytes + EpiSmem::kBytes; }
-  GH_HD static int bytes(int stages) { return bar_offset(stages) + kBarBytes + 1024; }
-  static int max_stages(int budget) {
-    int s = (budget - EpiSmem::kBytes - kBarBytes - 1024) / kStageBytes;
-    return s > kMaxStages ? kMaxStages : s;
-  }
 };
 
 GH_DEV float silu_f(float g) { return g / (1.0f + __expf(-g)); }
@@ -237,15 +222,173 @@ GH_DEV void epi_group_end(const EpiParams& ep, const GemmShape& gs, int n0, int 
     tile_copy<false>(ot, 128, out + (long)g0 * ep.ldo + n0, ep.ldo, rows, 128, min(128, gs.N - n0));
 }
 
-// ------------------------------------------------------------------ stream-K schedule
-// Iteration space: tiles x KB, tile t = tile_n * b_tiles + tile_b (batch tiles of one weight
-// tile are adjacent, so they stream the same weights close in time and share them in L2).
-struct StreamK {
-  long T;         // total iterations
-  int KB, G;
-  GH_HD long begin(int c) const { return (long)c * T / G; }
-  GH_HD int cta_of(long it) const { return (int)(((it + 1) * (long)G - 1) / T); }
+// ------------------------------------------------------------------ cluster split-K epilogue
+// Slice epilogue (BN <= 64): thread t of the 128 epilogue threads owns batch column
+// b = t / (128/BN) and a run of En = BN/C consecutive weight rows n of the CTA's slice; it has
+// the fully reduced fp32 values in `v` and writes its outputs directly (row-major [b][n]).
+template <int En>
+GH_DEV void store_run_bf16(uint16_t* dst, const float* v) {
+  if ((((uintptr_t)dst) & 15) == 0 && En % 8 == 0) {
+#pragma unroll
+    for (int e = 0; e < En; e += 8) {
+      uint4 o;
+      o.x = (uint32_t)f32_to_bf16(v[e]) | ((uint32_t)f32_to_bf16(v[e + 1]) << 16);
+      o.y = (uint32_t)f32_to_bf16(v[e + 2]) | ((uint32_t)f32_to_bf16(v[e + 3]) << 16);
+      o.z = (uint32_t)f32_to_bf16(v[e + 4]) | ((uint32_t)f32_to_bf16(v[e + 5]) << 16);
+      o.w = (uint32_t)f32_to_bf16(v[e + 6]) | ((uint32_t)f32_to_bf16(v[e + 7]) << 16);
+      *(uint4*)(dst + e) = o;
+    }
+  } else {
+#pragma unroll
+    for (int e = 0; e < En; ++e) dst[e] = f32_to_bf16(v[e]);
+  }
+}
+
+template <int BN, int En>
+GH_DEV void epi_slice(const EpiParams& ep, const GemmShape& gs, int n, int b, float (&v)[En], int slice) {
+  const bool col_ok = b < gs.Bt;
+  const bool full = n + En <= gs.N;
+  switch (ep.kind) {
+    case EPI_STORE:
+    case EPI_STORE_RESID: {
+      if (!col_ok) return;
+      if (ep.kind == EPI_STORE_RESID) {
+        const uint16_t* rp = (const uint16_t*)ep.resid + (long)b * ep.ldr + n;
+        if (full && En % 8 == 0 && ((uintptr_t)rp & 15) == 0) {
+          uint4 rr[En / 8 > 0 ? En / 8 : 1];
+#pragma unroll
+          for (int e = 0; e < En / 8; ++e) rr[e] = __ldg((const uint4*)rp + e);
+#pragma unroll
+          for (int e = 0; e < En / 8; ++e) {
+            const uint32_t w[4] = {rr[e].x, rr[e].y, rr[e].z, rr[e].w};
+#pragma unroll
+            for (int h = 0; h < 4; ++h) {
+              v[8 * e + 2 * h] += __uint_as_float(w[h] << 16);
+              v[8 * e + 2 * h + 1] += __uint_as_float(w[h] & 0xffff0000u);
+            }
+          }
+        } else {
+#pragma unroll
+          for (int e = 0; e < En; ++e) v[e] += (full || n + e < gs.N) ? bf16_to_f32(rp[e]) : 0.f;
+        }
+      }
+      uint16_t* op = (uint16_t*)ep.out + (long)b * ep.ldo + n;
+      if (full) store_run_bf16<En>(op, v);
+      else
+        for (int e = 0; e < En && n + e < gs.N; ++e) op[e] = f32_to_bf16(v[e]);
+      return;
+    }
+    case EPI_QKV_ROPE: {
+      if (!col_ok) return;
+      if (n < ep.rope_rows) {
+        const float2* cs = ep.rope + (long)ep.pos[b] * (ep.d_head >> 1) + ((n % ep.d_head) >> 1);
+#pragma unroll
+        for (int e = 0; e < En; e += 2) {
+          const float2 c = cs[e >> 1];
+          const float a = v[e], o = v[e + 1];
+          // pair (a, o) = (even, odd): even' = a cos - o sin, odd' = a sin + o cos
+          v[e] = a * c.x - o * c.y;
+          v[e + 1] = a * c.y + o * c.x;
+        }
+      }
+      uint16_t* op = (uint16_t*)ep.out + (long)b * ep.ldo + n;
+      if (full) store_run_bf16<En>(op, v);
+      else
+        for (int e = 0; e < En && n + e < gs.N; ++e) op[e] = f32_to_bf16(v[e]);
+      return;
+    }
+    case EPI_SWIGLU: {
+      if (!col_ok) return;
+      float h[En / 2];
+#pragma unroll
+      for (int e = 0; e < En / 2; ++e) h[e] = silu_f(v[2 * e]) * v[2 * e + 1];
+      uint16_t* op = (uint16_t*)ep.out + (long)b * ep.ldo + (n >> 1);
+      if (full) store_run_bf16<En / 2>(op, h);
+      else
+        for (int e = 0; e < En / 2 && n + 2 * e < gs.N; ++e) op[e] = f32_to_bf16(h[e]);
+      return;
+    }
+    default: {
+      // EPI_LOGITS_ARGMAX: logits (optional) and (max, argmax) over the slice per column b
+      float best = -INFINITY;
+      int bi = 0x7fffffff;
+#pragma unroll
+      for (int e = 0; e < En; ++e)
+        if (n + e < gs.N && (v[e] > best || (v[e] == best && n + e < bi))) { best = v[e]; bi = n + e; }
+      if (ep.logits && col_ok) {
+        float* lp = ep.logits + (long)b * ep.ldl + n;
+        for (int e = 0; e < En && n + e < gs.N; ++e) lp[e] = v[e];
+      }
+      // reduce over the 128/BN threads that share column b (adjacent lanes)
+      constexpr int kRuns = 128 / BN;
+#pragma unroll
+      for (int o = 1; o < kRuns; o <<= 1) {
+        const float ov = __shfl_xor_sync(0xffffffffu, best, o);
+        const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+        if (ov > best || (ov == best && oi < bi)) { best = ov; bi = oi; }
+      }
+      if (col_ok && ((threadIdx.x - 64) % kRuns) == 0)
+        ep.part[(long)slice * gs.Bt + b] = make_float2(best, __int_as_float(bi));
+      return;
+    }
+  }
+}
+
+template <int BN>
+struct GemmSmem {
+  static constexpr int kABytes = kBlockM * kBlockK * 2;  // 16 KB
+  static constexpr int kBBytes = BN * kBlockK * 2;
+  static constexpr int kStageBytes = kABytes + kBBytes;
+  static constexpr int kMaxStages = 16;
+  static constexpr bool kSplit = BN <= 64;                 // cluster split-K capable
+  // BN <= 64: fp32 partial tile [BN][128] published to the cluster; BN > 64: staging tiles
+  static constexpr int kEpiBytes = kSplit ? BN * 128 * 4 : EpiSmem::kBytes;
+  static constexpr uint32_t kAccCols = BN < 32 ? 32 : BN;  // one accumulator buffer
+  static constexpr uint32_t kTmemCols = 2 * kAccCols <= 64 ? 64 : 2 * kAccCols <= 128 ? 128
+                                      : 2 * kAccCols <= 256 ? 256 : 512;
+  static constexpr int kBarBytes = (2 * kMaxStages + 8) * 8 + 16;
+  GH_HD static int epi_offset(int stages) { return stages * kStageBytes; }
+  GH_HD static int bar_offset(int stages) { return stages * kStageBytes + kEpiBytes; }
+  GH_HD static int bytes(int stages) { return bar_offset(stages) + kBarBytes + 1024; }
+  static int max_stages(int budget) {
+    int s = (budget - kEpiBytes - kBarBytes - 1024) / kStageBytes;
+    return s > kMaxStages ? kMaxStages : s;
+  }
 };
+
+template <int BN, int C>
+GH_DEV void reduce_and_store(const EpiParams& ep, const GemmShape& gs, uint32_t red_saddr, int r, int n0,
+                             int b0, int tile_n, uint32_t consumed_saddr, unsigned long long* tr) {
+  // thread -> (column b, run of En rows inside this CTA's slice of 128/C rows)
+  constexpr int En = BN / C;
+  constexpr int kRuns = 128 / BN;
+  const int t = threadIdx.x - 64;
+  const int b = t / kRuns;
+  const int nl = r * (128 / C) + (t % kRuns) * En;
+  // issue every remote load first (one DSMEM round trip), then sum in rank order (deterministic)
+  float4 q[C][En / 4];
+#pragma unroll
+  for (int p = 0; p < C; ++p) {
+    const uint32_t src = mapa_shared(red_saddr, p) + (uint32_t)(b * 128 + nl) * 4;
+#pragma unroll
+    for (int e = 0; e < En / 4; ++e) q[p][e] = ld_dsmem_f4(src + e * 16);
+  }
+  float v[En];
+#pragma unroll
+  for (int e = 0; e < En / 4; ++e) {
+    float4 a = q[0][e];
+#pragma unroll
+    for (int p = 1; p < C; ++p) { a.x += q[p][e].x; a.y += q[p][e].y; a.z += q[p][e].z; a.w += q[p][e].w; }
+    v[4 * e] = a.x; v[4 * e + 1] = a.y; v[4 * e + 2] = a.z; v[4 * e + 3] = a.w;
+  }
+  // every remote value is in registers: tell the peers their partial buffers are free again
+  if (tr) tr[15] = globaltimer();
+  epi_bar();
+  if (threadIdx.x == 64)
+    for (int p = 0; p < C; ++p) mbar_arrive_cluster_relaxed(mapa_shared(consumed_saddr, p));
+  // all peers may reuse their partial buffer once everyone has read: caller signals
+  epi_slice<BN, En>(ep, gs, n0 + nl, b0 + b, v, tile_n * C + r);
+}
 
 template <int BN>
 __global__ void __launch_bounds__(kGemmThreads, 1)
@@ -260,41 +403,71 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   uint64_t* empty = full + L::kMaxStages;
   uint64_t* tfull = empty + L::kMaxStages;   // [2] accumulator ready
   uint64_t* tempty = tfull + 2;              // [2] accumulator drained
-  uint32_t* tmem_slot = (uint32_t*)(tempty + 2);
-  int* flag_smem = (int*)(tmem_slot + 1);
+  uint64_t* ready = tempty + 2;              // all C partials of the tile published (count C)
+  uint64_t* consumed = ready + 1;            // all C peers finished reading my partial (count C)
+  uint32_t* tmem_slot = (uint32_t*)(consumed + 1);
 
   const int warp = threadIdx.x >> 5;
   const int KB = gs.kb_total;
-  const StreamK sk{(long)gs.n_tiles * gs.b_tiles * KB, KB, (int)gridDim.x};
-  const long it_begin = sk.begin(blockIdx.x), it_end = sk.begin(blockIdx.x + 1);
+  const int C = (int)cluster_nctarank();
+  const int rank = (int)cluster_ctarank();
+  const int cid = (int)cluster_id_x(), ncl = (int)cluster_count_x();
+  const int n_tiles_total = gs.n_tiles * gs.b_tiles;
+  const int kbA = rank * KB / C, kbB = (rank + 1) * KB / C;  // this CTA's k-range of every tile
+  const int nkb = kbB - kbA;
+  const int my_tiles = cid < n_tiles_total ? (n_tiles_total - 1 - cid) / ncl + 1 : 0;
+  unsigned long long* trace = gs.trace ? gs.trace + blockIdx.x * 16 : nullptr;
+  if (trace && threadIdx.x == 0) trace[0] = globaltimer();
 
   if (threadIdx.x == 0) {
     prefetch_tmap(&tmW);
     prefetch_tmap(&tmX);
     for (int s = 0; s < S; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
     for (int a = 0; a < 2; ++a) { mbar_init(&tfull[a], 1); mbar_init(&tempty[a], 4); }
+    mbar_init(ready, C);      // one arrival per CTA of the cluster
+    mbar_init(consumed, C);
     fence_barrier_init();
   }
   if (warp == 1) tmem_alloc<L::kTmemCols>(tmem_slot);
   tc_fence_before();
-  __syncthreads();
+  if (C > 1) cluster_sync_all();  // peers' barriers are initialised before any remote arrive
+  else __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  griddep_launch_dependents();
 
   if (warp == 0) {
-    // ---------------- TMA producer: every k-block of every segment, one continuous ring
+    // ---------------- TMA producer: k-blocks [kbA, kbB) of each of this cluster's tiles
     if (elect_one()) {
       const bool hint = !(gs.flags & GEMM_DBG_NO_HINT);
       const bool load_x = !(gs.flags & GEMM_DBG_NO_X);
       const uint64_t pol_w = hint ? policy_evict_first() : 0;  // weights stream through once
       const uint64_t pol_x = hint ? policy_evict_last() : 0;   // activations are re-read by every tile
-      int i = 0;
-      for (long it = it_begin; it < it_end; ++it, ++i) {
-        const int tile = (int)(it / KB), kb = (int)(it % KB);
+      const int total = my_tiles * nkb;
+      const int pre = min(S, total);
+      // Weights do not depend on the previous kernel: the first S stages of weights are requested
+      // before griddepcontrol.wait (overlapping the predecessor's tail), activations after it.
+      for (int i = 0; i < pre; ++i) {
+        const int tile = cid + (i / nkb) * ncl, kb = kbA + i % nkb;
+        mbar_arrive_expect_tx(&full[i], load_x ? L::kStageBytes : L::kABytes);
+        uint8_t* sa = smem + i * L::kStageBytes;
+        if (hint) tma_load_2d(sa, &tmW, 0, ((tile / gs.b_tiles) * KB + kb) * kBlockM, &full[i], pol_w);
+        else tma_load_2d_nohint(sa, &tmW, 0, ((tile / gs.b_tiles) * KB + kb) * kBlockM, &full[i]);
+      }
+      if (trace) trace[1] = globaltimer();
+      griddep_wait();
+      if (trace) trace[2] = globaltimer();
+      for (int i = 0; i < pre && load_x; ++i) {
+        const int tile = cid + (i / nkb) * ncl, kb = kbA + i % nkb;
+        uint8_t* sb = smem + i * L::kStageBytes + L::kABytes;
+        if (hint) tma_load_2d(sb, &tmX, kb * kBlockK, (tile % gs.b_tiles) * BN, &full[i], pol_x);
+        else tma_load_2d_nohint(sb, &tmX, kb * kBlockK, (tile % gs.b_tiles) * BN, &full[i]);
+      }
+      for (int i = pre; i < total; ++i) {
+        const int tile = cid + (i / nkb) * ncl, kb = kbA + i % nkb;
         const int tile_n = tile / gs.b_tiles, tile_b = tile % gs.b_tiles;
         const int s = i % S;
-        const uint32_t ph = (i / S) & 1;
-        mbar_wait(&empty[s], ph ^ 1);
+        mbar_wait(&empty[s], ((i / S) & 1) ^ 1);
         uint8_t* sa = smem + s * L::kStageBytes;
         uint8_t* sb = sa + L::kABytes;
         mbar_arrive_expect_tx(&full[s], load_x ? L::kStageBytes : L::kABytes);
@@ -309,63 +482,62 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       }
     }
   } else if (warp == 1) {
-    // ---------------- MMA issuer: one accumulator buffer per segment, alternating
+    // ---------------- MMA issuer: one accumulator buffer per tile, alternating
     const uint32_t idesc = umma_idesc_bf16(kBlockM, BN);
     const bool no_mma = gs.flags & GEMM_DBG_NO_MMA;
-    int i = 0, j = 0;
-    for (long it = it_begin; it < it_end; ++j) {
-      const int kb0 = (int)(it % KB);
-      const int kb1 = (int)min((long)KB, kb0 + (it_end - it));
+    int i = 0;
+    for (int j = 0; j < my_tiles; ++j) {
+      if (trace && j == 0 && elect_one()) { mbar_wait(&full[0], 0); trace[3] = globaltimer(); }
+      __syncwarp();
       const int acc = j & 1;
       mbar_wait(&tempty[acc], ((j >> 1) & 1) ^ 1);
       tc_fence_after();
       const uint32_t d_tmem = tmem_base + acc * L::kAccCols;
-      for (int kb = kb0; kb < kb1; ++kb, ++i) {
+      for (int k = 0; k < nkb; ++k, ++i) {
         const int s = i % S;
         mbar_wait(&full[s], (i / S) & 1);
         tc_fence_after();
         if (elect_one()) {
           if (no_mma) {
             mbar_arrive(&empty[s]);
-            if (kb == kb1 - 1) mbar_arrive(&tfull[acc]);
+            if (k == nkb - 1) mbar_arrive(&tfull[acc]);
           } else {
             const uint32_t sa = smem_u32(smem + s * L::kStageBytes);
             const uint64_t da = umma_desc_sw128(sa);
             const uint64_t db = umma_desc_sw128(sa + L::kABytes);
 #pragma unroll
-            for (int k = 0; k < kBlockK / 16; ++k)
+            for (int kk = 0; kk < kBlockK / 16; ++kk)
               // +32 bytes along K inside the 128-byte swizzle atom = +2 in the >>4 address field
-              umma_bf16(d_tmem, da + (uint64_t)(k * 2), db + (uint64_t)(k * 2), idesc,
-                        (kb > kb0 || k > 0) ? 1u : 0u);
+              umma_bf16(d_tmem, da + (uint64_t)(kk * 2), db + (uint64_t)(kk * 2), idesc,
+                        (k > 0 || kk > 0) ? 1u : 0u);
             umma_commit(&empty[s]);
-            if (kb == kb1 - 1) umma_commit(&tfull[acc]);
+            if (k == nkb - 1) umma_commit(&tfull[acc]);
           }
         }
         __syncwarp();
       }
-      it += kb1 - kb0;
     }
+    if (trace && elect_one()) trace[4] = globaltimer();
   } else {
     // ---------------- epilogue warps 2..5
     const int q = warp & 3;  // TMEM lane quarter this warp may access
     const int row = q * 32 + (threadIdx.x & 31);
-    int j = 0;
-    for (long it = it_begin; it < it_end; ++j) {
-      const int tile = (int)(it / KB);
-      const int kb0 = (int)(it % KB);
-      const int kb1 = (int)min((long)KB, kb0 + (it_end - it));
-      it += kb1 - kb0;
+    const bool skip = gs.flags & GEMM_DBG_NO_EPI;
+    griddep_wait();          // residual / positions belong to earlier kernels
+    const uint32_t red_saddr = smem_u32(esm);
+    float* red = (float*)esm;
+    for (int j = 0; j < my_tiles; ++j) {
+      const int tile = cid + j * ncl;
       const int tile_n = tile / gs.b_tiles, tile_b = tile % gs.b_tiles;
       const int n0 = tile_n * kBlockM, b0 = tile_b * BN;
       const int acc = j & 1;
       const uint32_t taddr = tmem_base + ((uint32_t)(q * 32) << 16) + acc * L::kAccCols;
       mbar_wait(&tfull[acc], (j >> 1) & 1);
       tc_fence_after();
-      const bool whole = kb0 == 0 && kb1 == KB;
-      const bool skip = gs.flags & GEMM_DBG_NO_EPI;
-
-      if (whole && BN <= 64) {
-        // drain the accumulator into registers, release TMEM, then run the epilogue
+      const bool tr = trace && threadIdx.x == 64 && j == my_tiles - 1;
+      if (tr) trace[7] = globaltimer();
+      if constexpr (L::kSplit) {
+        // drain TMEM, release it to the MMA warp, publish the partial to the cluster
         float v[BN];
 #pragma unroll
         for (int c0 = 0; c0 < BN; c0 += 16) {
@@ -378,15 +550,38 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         tc_fence_before();
         __syncwarp();
         if ((threadIdx.x & 31) == 0) mbar_arrive(&tempty[acc]);
-        if (!skip) {
-          epi_group_begin(ep, gs, n0, b0, esm);
+        if (tr) trace[8] = globaltimer();
+        if (j > 0) mbar_wait_cluster(consumed, (j - 1) & 1);  // peers done reading tile j-1
+        if (tr) trace[9] = globaltimer();
 #pragma unroll
-          for (int c0 = 0; c0 < BN; c0 += 16)
-            if (b0 + c0 < gs.Bt) epi_chunk(ep, gs, row, n0, b0, b0 + c0, v + c0, esm, tile_n);
-          epi_group_end(ep, gs, n0, b0, esm);
+        for (int c = 0; c < BN; ++c) red[c * 128 + row] = v[c];
+        epi_bar();  // the four warps' partial writes happen before thread 64's cluster fence
+        if (threadIdx.x == 64) {
+          fence_acq_rel_cluster();
+          for (int p = 0; p < C; ++p) mbar_arrive_cluster_relaxed(mapa_shared(smem_u32(ready), p));
         }
-      } else if (whole) {
-        // wide batch tile: epilogue straight from TMEM, 64-column groups
+        if (tr) trace[10] = globaltimer();
+        mbar_wait_cluster(ready, j & 1);  // every peer's partial of this tile is visible
+        if (tr) trace[11] = globaltimer();
+        if (!skip) {
+          switch (C) {
+            case 1: reduce_and_store<BN, 1>(ep, gs, red_saddr, rank, n0, b0, tile_n, smem_u32(consumed), tr ? trace : nullptr); break;
+            case 2: reduce_and_store<BN, 2>(ep, gs, red_saddr, rank, n0, b0, tile_n, smem_u32(consumed), tr ? trace : nullptr); break;
+            case 4: reduce_and_store<BN, 4>(ep, gs, red_saddr, rank, n0, b0, tile_n, smem_u32(consumed), tr ? trace : nullptr); break;
+            case 8:
+              if constexpr (BN >= 32) reduce_and_store<BN, 8>(ep, gs, red_saddr, rank, n0, b0, tile_n, smem_u32(consumed), tr ? trace : nullptr);
+              break;
+          }
+        }
+        if (tr) trace[12] = globaltimer();
+        if (skip) {
+          epi_bar();
+          if (threadIdx.x == 64)
+            for (int p = 0; p < C; ++p) mbar_arrive_cluster_relaxed(mapa_shared(smem_u32(consumed), p));
+        }
+        if (tr) trace[13] = globaltimer();
+      } else {
+        // wide batch tile (C == 1): epilogue straight from TMEM in 64-column staged groups
         if (!skip) {
           for (int g = 0; g < BN && b0 + g < gs.Bt; g += kEpiCols) {
             epi_group_begin(ep, gs, n0, b0 + g, esm);
@@ -405,64 +600,16 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         tc_fence_before();
         __syncwarp();
         if ((threadIdx.x & 31) == 0) mbar_arrive(&tempty[acc]);
-      } else {
-        // a piece of a tile shared with other CTAs: publish the fp32 partial, take a ticket;
-        // the last piece to arrive sums all pieces in piece order and runs the epilogue.
-        const int c_first = sk.cta_of((long)tile * KB), c_last = sk.cta_of((long)tile * KB + KB - 1);
-        const int n_pieces = c_last - c_first + 1;
-        const int piece = blockIdx.x - c_first;
-        float* wst = gs.ws + (long)tile * gs.max_pieces * kBlockM * BN;
-        for (int c0 = 0; c0 < BN; c0 += 16) {
-          uint32_t r[16];
-          tmem_ld16(taddr + c0, r);
-          tmem_ld_wait();
-          float4* dst = (float4*)(wst + ((long)piece * (BN / 16) + c0 / 16) * kBlockM * 16 + row * 16);
-#pragma unroll
-          for (int e = 0; e < 4; ++e)
-            __stcg(dst + e, make_float4(__uint_as_float(r[4 * e]), __uint_as_float(r[4 * e + 1]),
-                                        __uint_as_float(r[4 * e + 2]), __uint_as_float(r[4 * e + 3])));
-        }
-        tc_fence_before();
-        __syncwarp();
-        if ((threadIdx.x & 31) == 0) mbar_arrive(&tempty[acc]);
-        __threadfence();
-        epi_bar();
-        if (threadIdx.x == 64) {
-          const int t = atomicAdd(&gs.tickets[tile], 1);
-          *flag_smem = (t == n_pieces - 1);
-          if (t == n_pieces - 1) gs.tickets[tile] = 0;  // reset for the next launch
-        }
-        epi_bar();
-        if (*flag_smem && !skip) {
-          __threadfence();
-          for (int g = 0; g < BN && b0 + g < gs.Bt; g += kEpiCols) {
-            epi_group_begin(ep, gs, n0, b0 + g, esm);
-            for (int c = g; c < g + kEpiCols && b0 + c < gs.Bt; c += 16) {
-              float v[16];
-#pragma unroll
-              for (int e = 0; e < 16; ++e) v[e] = 0.f;
-              for (int p = 0; p < n_pieces; ++p) {
-                const float4* src =
-                    (const float4*)(wst + ((long)p * (BN / 16) + c / 16) * kBlockM * 16 + row * 16);
-                float4 t4[4];
-#pragma unroll
-                for (int e = 0; e < 4; ++e) t4[e] = __ldcg(src + e);
-#pragma unroll
-                for (int e = 0; e < 4; ++e) {
-                  v[4 * e] += t4[e].x; v[4 * e + 1] += t4[e].y; v[4 * e + 2] += t4[e].z; v[4 * e + 3] += t4[e].w;
-                }
-              }
-              epi_chunk(ep, gs, row, n0, b0 + g, b0 + c, v, esm, tile_n);
-            }
-            epi_group_end(ep, gs, n0, b0 + g, esm);
-          }
-        }
       }
     }
+    if (L::kSplit && my_tiles > 0) mbar_wait_cluster(consumed, (my_tiles - 1) & 1);  // peers done with my smem
+    if (trace && threadIdx.x == 64) trace[14] = globaltimer();
   }
+  if (trace && threadIdx.x == 64) trace[5] = globaltimer();
   tc_fence_before();
   __syncthreads();
   if (warp == 1) tmem_free<L::kTmemCols>(tmem_base);
+  if (trace && threadIdx.x == 0) trace[6] = globaltimer();
 }
 
 }  // namespace gh

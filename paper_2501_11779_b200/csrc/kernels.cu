@@ -9,6 +9,8 @@
 #include <cudaTypedefs.h>
 #include <math.h>
 #include <algorithm>
+#include <cstdlib>
+#include <map>
 #include <mutex>
 
 #include "attention.cuh"
@@ -23,6 +25,25 @@ uint64_t& launch_counter() {
   return n;
 }
 #define GH_COUNT_LAUNCH() (++launch_counter())
+
+// launch with programmatic stream serialization (PDL), see common.cuh
+template <typename... KArgs, typename... Args>
+static cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                              Args... args) {
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  static const bool pdl = getenv("GH_NO_PDL") == nullptr;  // diagnostics A/B switch
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl ? 1 : 0;
+  GH_COUNT_LAUNCH();
+  return cudaLaunchKernelEx(&cfg, kernel, static_cast<KArgs>(args)...);
+}
 
 // ====================================================================== init / fill
 static float ih_k(double std_) { return (float)(1.7320508075688772 * std_ / 16777216.0); }
@@ -144,6 +165,8 @@ __global__ void __launch_bounds__(128) rmsnorm_kernel(const T* x, long ldx, cons
   const int b = blockIdx.x;
   const int nv = D / kV;
   const uint4* xr = (const uint4*)(x + (long)b * ldx);
+  griddep_launch_dependents();
+  griddep_wait();
   __shared__ float red[4];
   uint4 buf[kMaxVec];
   float ss = 0.f;
@@ -184,23 +207,22 @@ __global__ void __launch_bounds__(128) rmsnorm_kernel(const T* x, long ldx, cons
 cudaError_t launch_rmsnorm(int db, const void* x, long ldx, const void* w, void* y, long ldy,
                            void* copy_out, long ldc, int B, int D, float eps, cudaStream_t st) {
   if (B <= 0) return cudaSuccess;
-  GH_COUNT_LAUNCH();
   const int nv = D * db / 16;
   if (nv > 128 * 16 || (D * db) % 16) return cudaErrorInvalidValue;
   if (db == 4)
-    rmsnorm_kernel<float, 16><<<B, 128, 0, st>>>((const float*)x, ldx, (const float*)w, (float*)y, ldy,
-                                                 (float*)copy_out, ldc, D, eps);
-  else if (nv <= 128 * 4)
-    rmsnorm_kernel<bf16_t, 4><<<B, 128, 0, st>>>((const bf16_t*)x, ldx, (const bf16_t*)w, (bf16_t*)y, ldy,
-                                                 (bf16_t*)copy_out, ldc, D, eps);
-  else
-    rmsnorm_kernel<bf16_t, 16><<<B, 128, 0, st>>>((const bf16_t*)x, ldx, (const bf16_t*)w, (bf16_t*)y, ldy,
-                                                  (bf16_t*)copy_out, ldc, D, eps);
-  return cudaGetLastError();
+    return launch_pdl(rmsnorm_kernel<float, 16>, B, 128, 0, st, (const float*)x, ldx, (const float*)w,
+                      (float*)y, ldy, (float*)copy_out, ldc, D, eps);
+  if (nv <= 128 * 4)
+    return launch_pdl(rmsnorm_kernel<bf16_t, 4>, B, 128, 0, st, (const bf16_t*)x, ldx, (const bf16_t*)w,
+                      (bf16_t*)y, ldy, (bf16_t*)copy_out, ldc, D, eps);
+  return launch_pdl(rmsnorm_kernel<bf16_t, 16>, B, 128, 0, st, (const bf16_t*)x, ldx, (const bf16_t*)w,
+                    (bf16_t*)y, ldy, (bf16_t*)copy_out, ldc, D, eps);
 }
 
 __global__ void embed_kernel(const uint4* table, const int32_t* tok, uint4* x, int row_vecs, int V) {
   const int b = blockIdx.x;
+  griddep_launch_dependents();
+  griddep_wait();
   int t = tok[b];
   t = t < 0 ? 0 : (t >= V ? V - 1 : t);
   const uint4* src = table + (long)t * row_vecs;
@@ -211,9 +233,7 @@ __global__ void embed_kernel(const uint4* table, const int32_t* tok, uint4* x, i
 cudaError_t launch_embed(int db, const void* table, const int32_t* tok, void* x, int B, int D,
                          int V, cudaStream_t st) {
   if (B <= 0) return cudaSuccess;
-  GH_COUNT_LAUNCH();
-  embed_kernel<<<B, 128, 0, st>>>((const uint4*)table, tok, (uint4*)x, D * db / 16, V);
-  return cudaGetLastError();
+  return launch_pdl(embed_kernel, B, 128, 0, st, (const uint4*)table, tok, (uint4*)x, D * db / 16, V);
 }
 
 // ====================================================================== argmax
@@ -222,6 +242,8 @@ GH_DEV void argmax_merge(float& v, int& i, float ov, int oi) {
 }
 __global__ void argmax_final_kernel(const float2* part, int n_tiles, int B, int32_t* next) {
   const int b = blockIdx.x;
+  griddep_launch_dependents();
+  griddep_wait();
   float v = -INFINITY; int idx = 0x7fffffff;
   for (int t = threadIdx.x; t < n_tiles; t += blockDim.x) {
     const float2 p = part[(long)t * B + b];
@@ -240,6 +262,8 @@ __global__ void argmax_final_kernel(const float2* part, int n_tiles, int B, int3
 }
 __global__ void argmax_rows_kernel(const float* logits, int V, int32_t* next) {
   const int b = blockIdx.x;
+  griddep_launch_dependents();
+  griddep_wait();
   const float* r = logits + (long)b * V;
   float v = -INFINITY; int idx = 0x7fffffff;
   for (int i = threadIdx.x; i < V; i += blockDim.x) argmax_merge(v, idx, r[i], i);
@@ -255,26 +279,22 @@ __global__ void argmax_rows_kernel(const float* logits, int V, int32_t* next) {
   }
 }
 cudaError_t launch_argmax_final(const float2* part, int n_tiles, int B, int32_t* next, cudaStream_t st) {
-  GH_COUNT_LAUNCH();
-  argmax_final_kernel<<<B, 256, 0, st>>>(part, n_tiles, B, next);
-  return cudaGetLastError();
+  return launch_pdl(argmax_final_kernel, B, 256, 0, st, part, n_tiles, B, next);
 }
 cudaError_t launch_argmax_rows(const float* logits, int B, int V, int32_t* next, cudaStream_t st) {
-  GH_COUNT_LAUNCH();
-  argmax_rows_kernel<<<B, 256, 0, st>>>(logits, V, next);
-  return cudaGetLastError();
+  return launch_pdl(argmax_rows_kernel, B, 256, 0, st, logits, V, next);
 }
 
 // ====================================================================== batch state
 __global__ void advance_kernel(int32_t* tok, const int32_t* next, int32_t* pos, int n, int inc) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  griddep_launch_dependents();
+  griddep_wait();
   if (i < n) { tok[i] = next[i]; pos[i] += inc; }
 }
 cudaError_t launch_advance(int32_t* tok, const int32_t* next, int32_t* pos, int n, int inc, cudaStream_t st) {
   if (n <= 0) return cudaSuccess;
-  GH_COUNT_LAUNCH();
-  advance_kernel<<<(n + 255) / 256, 256, 0, st>>>(tok, next, pos, n, inc);
-  return cudaGetLastError();
+  return launch_pdl(advance_kernel, (n + 255) / 256, 256, 0, st, tok, next, pos, n, inc);
 }
 
 // ====================================================================== SIMT GEMM (fp32 storage)
@@ -336,9 +356,55 @@ cudaError_t make_tmap_bf16(CUtensorMap* out, const void* base, uint64_t rows, ui
   return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorInvalidValue;
 }
 
-static const int kBNs[] = {16, 32, 48, 64, 96, 128, 192, 256};
+static const int kBNs[] = {16, 32, 64, 128, 256};
 static int stages_override = 0;  // diagnostics
+static int cluster_override = 0;  // diagnostics
 
+template <int BN>
+static int tc_stages() {
+  using L = GemmSmem<BN>;
+  const int smax = L::max_stages(227 * 1024);
+  return std::max(2, std::min(smax, stages_override ? stages_override : smax));
+}
+
+// co-resident clusters of C CTAs for the BN instantiation (cudaOccupancyMaxActiveClusters)
+template <int BN>
+static int max_clusters(int C) {
+  static std::map<int, int> cache;
+  auto it = cache.find(C);
+  if (it != cache.end()) return it->second;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(C * (kNumSMs / C));
+  cfg.blockDim = dim3(kGemmThreads);
+  cfg.dynamicSmemBytes = GemmSmem<BN>::bytes(tc_stages<BN>());
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = C;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  int n = 0;
+  if (cudaOccupancyMaxActiveClusters(&n, gemm_tc_kernel<BN>, &cfg) != cudaSuccess || n <= 0) {
+    cudaGetLastError();
+    n = kNumSMs / C;
+  }
+  cache[C] = n;
+  return n;
+}
+
+static int max_clusters_bn(int BN, int C) {
+  switch (BN) {
+    case 16: return max_clusters<16>(C);
+    case 32: return max_clusters<32>(C);
+    case 64: return max_clusters<64>(C);
+    case 128: return max_clusters<128>(C);
+    default: return max_clusters<256>(C);
+  }
+}
+
+// Choose the cluster size C minimising the k-blocks on the critical path of one CTA:
+// rounds(C) * (ceil(KB / C) + reduction overhead), rounds = ceil(tiles / co-resident clusters).
 GemmPlan plan_gemm(int N, int K, int Bt) {
   GemmPlan p;
   const int bt_cap = std::min(Bt, 256);
@@ -346,13 +412,17 @@ GemmPlan plan_gemm(int N, int K, int Bt) {
   for (int bn : kBNs) if (bn >= bt_cap) { p.BN = bn; break; }
   p.b_tiles = (Bt + p.BN - 1) / p.BN;
   p.n_tiles = (N + kBlockM - 1) / kBlockM;
-  const long KB = (K + kBlockK - 1) / kBlockK;
-  const long T = (long)p.n_tiles * p.b_tiles * KB;
-  p.grid = (int)std::min<long>(kNumSMs, T);
-  // a tile of KB iterations spans at most ceil(KB * G / T) + 1 CTAs
-  p.max_pieces = (int)((KB * p.grid + T - 1) / T) + 1;
-  p.ws_floats = (size_t)p.n_tiles * p.b_tiles * p.max_pieces * kBlockM * p.BN;
-  p.tickets = (size_t)p.n_tiles * p.b_tiles;
+  const int KB = (K + kBlockK - 1) / kBlockK;
+  const int tiles = p.n_tiles * p.b_tiles;
+  double best = 1e30;
+  for (int C : {1, 2, 4, 8}) {
+    if (C > 1 && (p.BN > 64 || p.BN / C < 4 || C > KB)) continue;
+    if (cluster_override && C != cluster_override) continue;
+    const int ncl = std::min(tiles, max_clusters_bn(p.BN, C));
+    const int rounds = (tiles + ncl - 1) / ncl;
+    const double cost = rounds * ((KB + C - 1) / C + (C > 1 ? 1.0 : 0.0));
+    if (cost < best - 1e-9) { best = cost; p.C = C; p.n_clusters = ncl; }
+  }
   return p;
 }
 
@@ -364,15 +434,29 @@ template <int BN>
 static cudaError_t launch_tc(const CUtensorMap* tmW, const CUtensorMap* tmX, GemmShape gs,
                              const GemmPlan& p, const EpiParams& ep, cudaStream_t st) {
   using L = GemmSmem<BN>;
-  const int smax = L::max_stages(227 * 1024);
-  gs.stages = std::max(2, std::min(smax, stages_override ? stages_override : smax));
+  gs.stages = tc_stages<BN>();
   const int smem = L::bytes(gs.stages);
   if (smem > 227 * 1024) return cudaErrorInvalidValue;
+  static const bool pdl = getenv("GH_NO_PDL") == nullptr;
+  cudaLaunchAttribute attr[2];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = p.C;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[1].val.programmaticStreamSerializationAllowed = 1;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(p.n_clusters * p.C);
+  cfg.blockDim = dim3(kGemmThreads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl ? 2 : 1;
   GH_COUNT_LAUNCH();
-  gemm_tc_kernel<BN><<<p.grid, kGemmThreads, smem, st>>>(*tmW, *tmX, gs, ep);
-  return cudaGetLastError();
+  return cudaLaunchKernelEx(&cfg, gemm_tc_kernel<BN>, *tmW, *tmX, gs, ep);
 }
 
+void gemm_debug_cluster(int C) { cluster_override = C; }
 void gemm_debug_set(int stages) { stages_override = stages; }
 
 cudaError_t launch_gemm(const Weight& W, const CUtensorMap* tmW, const void* X, long ldx,
@@ -398,18 +482,13 @@ cudaError_t launch_gemm(const Weight& W, const CUtensorMap* tmW, const void* X, 
   gs.N = W.N; gs.K = W.K; gs.Bt = Bt;
   gs.n_tiles = p.n_tiles; gs.b_tiles = p.b_tiles;
   gs.kb_total = (W.K + kBlockK - 1) / kBlockK;
-  gs.max_pieces = p.max_pieces;
-  gs.ws = sc.ws; gs.tickets = sc.tickets;
   gs.flags = sc.debug_flags;
-  if (p.ws_floats > sc.ws_floats || p.tickets > sc.n_tickets) return cudaErrorInvalidValue;
+  gs.trace = sc.trace;
   switch (p.BN) {
     case 16: return launch_tc<16>(tmW, tmX, gs, p, ep, st);
     case 32: return launch_tc<32>(tmW, tmX, gs, p, ep, st);
-    case 48: return launch_tc<48>(tmW, tmX, gs, p, ep, st);
     case 64: return launch_tc<64>(tmW, tmX, gs, p, ep, st);
-    case 96: return launch_tc<96>(tmW, tmX, gs, p, ep, st);
     case 128: return launch_tc<128>(tmW, tmX, gs, p, ep, st);
-    case 192: return launch_tc<192>(tmW, tmX, gs, p, ep, st);
     case 256: return launch_tc<256>(tmW, tmX, gs, p, ep, st);
   }
   return cudaErrorInvalidValue;
@@ -430,9 +509,7 @@ static cudaError_t launch_attn_t(const AttnArgs& a, cudaStream_t st) {
   const int units = a.B * a.H;
   if (units <= 0) return cudaSuccess;
   const int grid = std::min(units, kNumSMs);
-  GH_COUNT_LAUNCH();
-  attn_decode_kernel<T, DH><<<grid, C::kThreads, C::kSmem, st>>>(a);
-  return cudaGetLastError();
+  return launch_pdl(attn_decode_kernel<T, DH>, grid, C::kThreads, C::kSmem, st, a);
 }
 
 bool attention_supported(int db, int dh) {
@@ -459,8 +536,8 @@ cudaError_t launch_attention(int db, int dh, const AttnArgs& a, cudaStream_t st)
 cudaError_t configure_kernels() {
   cudaError_t e = cudaSuccess;
   auto chk = [&](cudaError_t r) { if (e == cudaSuccess) e = r; };
-  chk(configure_tc<16>()); chk(configure_tc<32>()); chk(configure_tc<48>()); chk(configure_tc<64>());
-  chk(configure_tc<96>()); chk(configure_tc<128>()); chk(configure_tc<192>()); chk(configure_tc<256>());
+  chk(configure_tc<16>()); chk(configure_tc<32>()); chk(configure_tc<64>());
+  chk(configure_tc<128>()); chk(configure_tc<256>());
   chk(configure_attn<bf16_t, 48>()); chk(configure_attn<bf16_t, 64>()); chk(configure_attn<bf16_t, 128>());
   chk(configure_attn<float, 48>()); chk(configure_attn<float, 64>()); chk(configure_attn<float, 128>());
   return e;

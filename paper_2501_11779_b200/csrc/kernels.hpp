@@ -34,26 +34,25 @@ struct RowSegs {
   int interleave2 = 0;
 };
 
-// Per-GEMM launch plan chosen on the host: batch tile and persistent stream-K grid.
+// Per-GEMM launch plan chosen on the host: batch tile and persistent cluster split-K grid.
 struct GemmPlan {
-  int BN = 0;         // batch tile (16..256)
+  int BN = 0;         // batch tile (16, 32, 64, 128, 256)
   int n_tiles = 0;    // ceil(N / 128)
   int b_tiles = 0;
-  int grid = 0;       // persistent CTAs (<= 148)
-  int max_pieces = 1;
-  size_t ws_floats = 0;   // stream-K partial workspace
-  size_t tickets = 0;
+  int C = 1;          // CTAs per cluster = K splits of every tile (1, 2, 4, 8)
+  int n_clusters = 0; // persistent clusters (<= co-resident clusters)
+  int slices() const { return n_tiles * C; }  // argmax partials per batch column
 };
 GemmPlan plan_gemm(int N, int K, int Bt);
 
-// Scratch shared by every GEMM of a tier (split workspace, tickets, SIMT staging).
+// Scratch shared by every GEMM of a tier (SIMT staging, diagnostics).
 struct GemmScratch {
-  float* ws = nullptr;     size_t ws_floats = 0;
-  int* tickets = nullptr;  size_t n_tickets = 0;
   float* stage = nullptr;  size_t stage_floats = 0;  // SIMT path fp32 result [Bt][N]
   int debug_flags = 0;                                // GEMM_DBG_* (diagnostics only)
+  unsigned long long* trace = nullptr;                // per-CTA timestamps (diagnostics only)
 };
 void gemm_debug_set(int stages);  // 0 = production pipeline depth
+void gemm_debug_cluster(int C);   // 0 = production cluster-size choice
 
 // Encode a 2-D bf16 tensor map over a row-major [rows, cols] matrix with row stride ld
 // (elements), box {64, box_rows}, 128-byte swizzle.

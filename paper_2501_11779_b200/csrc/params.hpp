@@ -25,18 +25,16 @@ struct EpiParams {
   int rope_rows;        // leading output rows (q and k) that receive RoPE
   float* logits;        // [B][ldl] fp32 (optional)
   long ldl;
-  float2* part;         // [n_tiles][Bt] (max value, argmax index as float bits)
+  float2* part;         // [n_tiles * C][Bt] (max value, argmax index as float bits); C = cluster size
 };
 
 struct GemmShape {
   int N, K, Bt;         // weight rows, reduction length, batch
   int n_tiles, b_tiles; // 128-row weight tiles x BN-column batch tiles
   int kb_total;         // KB = ceil(K / 64)
-  int max_pieces;       // upper bound of CTAs sharing one tile (workspace slots per tile)
-  float* ws;            // stream-K partial workspace [tiles][max_pieces][128 x BN]
-  int* tickets;         // per tile arrival counters, zero between launches
   int stages;           // TMA -> MMA pipeline depth (shared-memory ring)
   int flags;            // diagnostics (GEMM_DBG_*), 0 in production
+  unsigned long long* trace;  // diagnostics: per-CTA globaltimer stamps [grid][8] (nullptr = off)
 };
 enum GemmDbg : int { GEMM_DBG_NO_MMA = 1, GEMM_DBG_NO_X = 2, GEMM_DBG_NO_HINT = 4, GEMM_DBG_NO_EPI = 8 };
 

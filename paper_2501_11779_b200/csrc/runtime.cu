@@ -263,28 +263,11 @@ gh_status gh_tier1_create(const gh_model_spec* spec, int device, uint32_t layer_
   GH_TRY(dev_alloc(t->mem, B * Dh * db, &t->g));
   {
     void* p;
-    const size_t n_tiles = (V + 127) / 128;
-    GH_TRY(dev_alloc(t->mem, n_tiles * B * sizeof(float2), &p));
+    const size_t n_slices = (size_t)(V + 127) / 128 * 8;  // tiles x max cluster size
+    GH_TRY(dev_alloc(t->mem, n_slices * B * sizeof(float2), &p));
     t->part = (float2*)p;
   }
-  size_t ws = 0, tk = 0;
-  const int NK[5][2] = {{D + 2 * Dkv, D}, {D, D}, {2 * Dh, D}, {D, Dh}, {V, D}};
-  for (uint32_t b = 1; b <= max_batch; ++b)
-    for (auto& nk : NK) {
-      GemmPlan p = plan_gemm(nk[0], nk[1], (int)b);
-      ws = std::max(ws, p.ws_floats);
-      tk = std::max(tk, p.tickets);
-    }
-  if (db == 2) {
-    void* p;
-    t->gsc.ws_floats = ws;
-    GH_TRY(dev_alloc(t->mem, std::max<size_t>(ws, 4) * sizeof(float), &p));
-    t->gsc.ws = (float*)p;
-    t->gsc.n_tickets = tk;
-    GH_TRY(dev_alloc(t->mem, std::max<size_t>(tk, 1) * sizeof(int), &p));
-    t->gsc.tickets = (int*)p;
-    GH_CUDA(cudaMemset(p, 0, std::max<size_t>(tk, 1) * sizeof(int)));
-  } else {
+  if (db == 4) {
     void* p;
     const size_t n = B * (size_t)std::max({D + 2 * Dkv, 2 * Dh, V, D});
     GH_TRY(dev_alloc(t->mem, n * sizeof(float), &p));
@@ -377,7 +360,7 @@ gh_status gh_tier1_classify(gh_tier1* t, uint32_t B, const void* x, float* logit
   ep.part = t->part;
   GH_TRY(t->gemm(t->cls, &t->tm_cls, t->xn, s.D, (int)B, ep, st));
   if (s.db == 2) {
-    GH_CUDA(launch_argmax_final(t->part, (s.V + 127) / 128, (int)B, next, st));
+    GH_CUDA(launch_argmax_final(t->part, t->plan(s.V, s.D, (int)B).slices(), (int)B, next, st));
   } else {
     GH_CUDA(launch_argmax_rows(logits ? logits : t->gsc.stage, (int)B, s.V, next, st));
   }
@@ -882,21 +865,11 @@ extern "C" gh_status gh_debug_gemm_bench(int N, int K, int B, int flags, int sta
   GH_TRY(dev_alloc(mem, (size_t)B * K * 2, &X));
   GH_TRY(dev_alloc(mem, (size_t)B * N * 2, &Y));
   GH_CUDA(cudaMemset(X, 0, (size_t)B * K * 2));
+  gemm_debug_cluster(ks);  // diagnostics: force the cluster size (0 = production choice)
   GemmPlan p = plan_gemm(N, K, B);
-  if (ks > 0) {  // diagnostics: override the persistent grid size
-    const long T = (long)p.n_tiles * p.b_tiles * ((K + 63) / 64);
-    p.grid = (int)std::min<long>(ks, T);
-    p.max_pieces = (int)((((K + 63) / 64) * (long)p.grid + T - 1) / T) + 1;
-    p.ws_floats = (size_t)p.n_tiles * p.b_tiles * p.max_pieces * 128 * p.BN;
-  }
+  gemm_debug_cluster(0);
   GH_CUDA(make_tmap_bf16(&tmX, X, (uint64_t)B, (uint64_t)K, (uint64_t)K, (uint32_t)p.BN));
   GemmScratch sc;
-  void* q;
-  sc.ws_floats = std::max<size_t>(p.ws_floats, 4);
-  GH_TRY(dev_alloc(mem, sc.ws_floats * 4, &q)); sc.ws = (float*)q;
-  sc.n_tickets = std::max<size_t>(p.tickets, 1);
-  GH_TRY(dev_alloc(mem, sc.n_tickets * 4, &q)); sc.tickets = (int*)q;
-  GH_CUDA(cudaMemset(q, 0, sc.n_tickets * 4));
   sc.debug_flags = flags;
   EpiParams ep = epi_default();
   ep.kind = EPI_STORE; ep.out = Y; ep.ldo = N;
@@ -913,5 +886,60 @@ extern "C" gh_status gh_debug_gemm_bench(int N, int K, int B, int flags, int sta
   cudaEventDestroy(e0); cudaEventDestroy(e1);
   gemm_debug_set(0);
   *us = ms * 1000.f / reps;
+  return GH_OK;
+}
+
+extern "C" gh_status gh_debug_gemm_trace(int N, int K, int B, int copies, int reps, float* us,
+                                         unsigned long long* trace, int trace_cap) {
+  if (!us || N <= 0 || K <= 0 || B <= 0 || reps <= 0 || copies <= 0) return fail(GH_EINVAL, "bad argument");
+  if (gh_device_count() == 0) return fail(GH_ECUDA, "no CUDA device");
+  const int dbg_flags = reps / 1000;  // diagnostics: flags packed above the repetition count
+  reps %= 1000;
+  GH_CUDA(cudaSetDevice(0));
+  GH_CUDA(configure_kernels());
+  std::vector<std::unique_ptr<DevMem>> mem;
+  std::vector<Weight> Ws(copies);
+  std::vector<CUtensorMap> tms(copies);
+  for (int c = 0; c < copies; ++c) {
+    Weight& W = Ws[c];
+    W.N = N; W.K = K; W.dtype_bytes = 2; W.tiled = true;
+    GH_TRY(dev_alloc(mem, W.elems() * 2, &W.ptr));
+    const uint64_t tid = 7 + c; const int rows = N; const double sd = 0.02;
+    GH_CUDA(launch_init_weight(W, make_segs(1, 1, &tid, &rows, &sd, false), 0));
+    GH_CUDA(make_tmap_bf16(&tms[c], W.ptr, (uint64_t)W.n_pad() * W.kb(), 64, 64, 128));
+  }
+  void *X, *Y;
+  GH_TRY(dev_alloc(mem, (size_t)B * K * 2, &X));
+  GH_TRY(dev_alloc(mem, (size_t)B * N * 2, &Y));
+  GH_CUDA(cudaMemset(X, 0, (size_t)B * K * 2));
+  GemmPlan p = plan_gemm(N, K, B);
+  CUtensorMap tmX;
+  GH_CUDA(make_tmap_bf16(&tmX, X, (uint64_t)B, (uint64_t)K, (uint64_t)K, (uint32_t)p.BN));
+  GemmScratch sc;
+  void* q;
+  sc.debug_flags = dbg_flags;
+  unsigned long long* dtrace = nullptr;
+  if (trace) {
+    GH_TRY(dev_alloc(mem, (size_t)p.n_clusters * p.C * 128, &q));
+    dtrace = (unsigned long long*)q;
+    GH_CUDA(cudaMemset(q, 0, (size_t)p.n_clusters * p.C * 128));
+  }
+  EpiParams ep = epi_default();
+  ep.kind = EPI_STORE; ep.out = Y; ep.ldo = N;
+  cudaEvent_t e0, e1;
+  GH_CUDA(cudaEventCreate(&e0)); GH_CUDA(cudaEventCreate(&e1));
+  for (int i = 0; i < copies; ++i) GH_CUDA(launch_gemm(Ws[i], &tms[i], X, K, &tmX, B, p, ep, sc, 0));
+  GH_CUDA(cudaEventRecord(e0, 0));
+  for (int i = 0; i < reps; ++i) {
+    if (i == reps - 1) sc.trace = dtrace;
+    GH_CUDA(launch_gemm(Ws[i % copies], &tms[i % copies], X, K, &tmX, B, p, ep, sc, 0));
+  }
+  GH_CUDA(cudaEventRecord(e1, 0));
+  GH_CUDA(cudaEventSynchronize(e1));
+  float ms = 0;
+  GH_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+  cudaEventDestroy(e0); cudaEventDestroy(e1);
+  *us = ms * 1000.f / reps;
+  if (trace) GH_CUDA(cudaMemcpy(trace, dtrace, (size_t)std::min(p.n_clusters * p.C, trace_cap / 16) * 128, cudaMemcpyDeviceToHost));
   return GH_OK;
 }

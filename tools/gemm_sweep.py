@@ -10,9 +10,9 @@ from paper_2501_11779_b200 import _lib as L  # noqa: E402
 lib = gh.lib()
 
 
-def bench(N, K, B, flags=0, stages=0, grid=0, reps=20):
+def bench(N, K, B, flags=0, stages=0, cluster=0, reps=20):
     us = C.c_float()
-    L.check(lib.gh_debug_gemm_bench(N, K, B, flags, stages, grid, reps, C.byref(us)))
+    L.check(lib.gh_debug_gemm_bench(N, K, B, flags, stages, cluster, reps, C.byref(us)))
     return us.value
 
 
@@ -24,7 +24,8 @@ for name, (N, K) in shapes.items():
     row = [f"{name:4s} N={N:6d} K={K:6d} prod {base:7.1f}us {wb / base / 1e3:6.0f}GB/s"]
     for label, kw in [("noMMA", dict(flags=1)), ("noX", dict(flags=2)), ("noHint", dict(flags=4)),
                       ("noEpi", dict(flags=8)), ("noMMA+noEpi", dict(flags=9)), ("st4", dict(stages=4)),
-                      ("st6", dict(stages=6)), ("g132", dict(grid=132)), ("g74", dict(grid=74))]:
+                      ("st6", dict(stages=6)), ("c1", dict(cluster=1)), ("c2", dict(cluster=2)),
+                      ("c4", dict(cluster=4)), ("c8", dict(cluster=8))]:
         t = bench(N, K, B, **kw)
         row.append(f"{label} {t:6.1f}")
     print(" | ".join(row), flush=True)
