@@ -102,6 +102,9 @@ gh_status gh_two_tier_context_slots(const gh_model_spec* spec, uint64_t tier1_no
                                     uint64_t seq_len, uint64_t* out);      /* optimizer.cpp:175-192 */
 /* Rounded sqrt(2) grid (profiles.cpp:232-245).  Writes at most `cap` entries, *n = full count. */
 gh_status gh_batch_grid(uint64_t max_batch, uint64_t* out, uint64_t cap, uint64_t* n);
+/* Tier split of a Tier-1 batch over K' Tier-2 ranks: balanced shards differing by at most one
+ * prompt (analytic.cpp:119), lower ranks first; off/cnt arrays of length kp. */
+gh_status gh_shard_plan(uint64_t batch, uint64_t kp, uint64_t* off, uint64_t* cnt);
 /* Throughput identity B_total*IF/mean(TBT) (des.cpp:298-310); gen_ts in ns. */
 gh_status gh_throughput_from(const int64_t* gen_ts_ns, uint64_t n, uint64_t batch_total,
                              uint64_t inflight, double* tokens_per_s);

@@ -7,11 +7,11 @@ from ._lib import (CudaError, FeasibilityError, GhError, NcclError, UnsupportedE
                    lib)
 from .spec import (CONFIGS, LLAMA2_7B, LLAMA2_13B, LLAMA2_70B, TINY, ModelSpec, attention_footprint,
                    batch_grid, kv_bytes_per_prompt, layer_spans, node_weight_bytes, nonattention_footprint,
-                   payload, throughput_from, two_tier_context_slots, weights_bytes)
+                   payload, shard_plan, throughput_from, two_tier_context_slots, weights_bytes)
 
 __all__ = [
     "CONFIGS", "LLAMA2_7B", "LLAMA2_13B", "LLAMA2_70B", "TINY", "ModelSpec", "attention_footprint",
     "batch_grid", "kv_bytes_per_prompt", "layer_spans", "node_weight_bytes", "nonattention_footprint",
-    "payload", "throughput_from", "two_tier_context_slots", "weights_bytes", "GhError", "ValidationError",
+    "payload", "shard_plan", "throughput_from", "two_tier_context_slots", "weights_bytes", "GhError", "ValidationError",
     "FeasibilityError", "CudaError", "NcclError", "UnsupportedError", "lib",
 ]

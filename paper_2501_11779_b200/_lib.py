@@ -84,6 +84,7 @@ PROTOTYPES = {
     "gh_two_tier_context_slots": (st, [P(GhSpec), u64, u64, u64, u64, P(u64)]),
     "gh_batch_grid": (st, [u64, P(u64), u64, P(u64)]),
     "gh_throughput_from": (st, [P(i64), u64, u64, u64, P(C.c_double)]),
+    "gh_shard_plan": (st, [u64, u64, P(u64), P(u64)]),
     "gh_profile_write_csv": (st, [C.c_char_p, C.c_char_p, C.c_char_p, C.c_int, u64, P(u64),
                                   P(C.c_double), u64]),
     "gh_tier1_create": (st, [P(GhSpec), C.c_int, u32, u32, u64, u32, P(vp)]),

@@ -141,6 +141,19 @@ gh_status gh_batch_grid(uint64_t max_batch, uint64_t* out, uint64_t cap, uint64_
   return GH_OK;
 }
 
+// Balanced shards (analytic.cpp:119): batch / kp each, the remainder to the low ranks
+gh_status gh_shard_plan(uint64_t batch, uint64_t kp, uint64_t* off, uint64_t* cnt) {
+  if (!off || !cnt) return fail(GH_EINVAL, "null argument");
+  if (kp == 0 || batch < kp) return fail(GH_EINVAL, "shard_plan: need 1 <= kp <= batch");
+  uint64_t o = 0;
+  for (uint64_t j = 0; j < kp; ++j) {
+    cnt[j] = batch / kp + (j < batch % kp ? 1 : 0);
+    off[j] = o;
+    o += cnt[j];
+  }
+  return GH_OK;
+}
+
 // throughput_from (des.cpp:298-310)
 gh_status gh_throughput_from(const int64_t* ts, uint64_t n, uint64_t batch_total,
                              uint64_t inflight, double* tps) {

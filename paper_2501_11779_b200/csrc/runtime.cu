@@ -631,12 +631,11 @@ gh_status gh_engine_create(const gh_engine_config* cfg, gh_comm* comm, gh_engine
     e->role = rank == 0 ? 1 : 2;
     e->kp = world - 1;
     if ((int)cfg->batch < e->kp) return fail(GH_EINVAL, "batch smaller than the number of Tier-2 ranks");
-    int off = 0;
-    for (int j = 0; j < e->kp; ++j) {  // balanced shards differing by at most one (analytic.cpp:119)
-      const int c = (int)cfg->batch / e->kp + (j < (int)cfg->batch % e->kp ? 1 : 0);
-      e->shard_off.push_back(off);
-      e->shard_cnt.push_back(c);
-      off += c;
+    std::vector<uint64_t> off(e->kp), cnt(e->kp);  // balanced shards (analytic.cpp:119)
+    GH_TRY(gh_shard_plan(cfg->batch, e->kp, off.data(), cnt.data()));
+    for (int j = 0; j < e->kp; ++j) {
+      e->shard_off.push_back((int)off[j]);
+      e->shard_cnt.push_back((int)cnt[j]);
     }
     if (e->role == 2) e->my_cnt = e->shard_cnt[rank - 1];
   }

@@ -166,3 +166,11 @@ def throughput_from(gen_ts_ns, batch_total: int, inflight: int) -> float:
     o = C.c_double(0)
     L.check(L.lib().gh_throughput_from(ts, len(gen_ts_ns), batch_total, inflight, C.byref(o)))
     return o.value
+
+
+def shard_plan(batch: int, kp: int):
+    """(offsets, counts) of the K' Tier-2 shards of a Tier-1 batch (analytic.cpp:119)."""
+    off = (C.c_uint64 * max(kp, 1))()
+    cnt = (C.c_uint64 * max(kp, 1))()
+    L.check(L.lib().gh_shard_plan(batch, kp, off, cnt))
+    return list(off), list(cnt)

@@ -1,0 +1,93 @@
+"""NCCL tier split on real GPUs (needs >= 2 GPUs; skipped otherwise): rank 0 = Tier-1, ranks
+1.. = Tier-2 holding the KV of their prompt shard.  Tokens and logits must be identical to the
+colocated engine (same kernels, same batch -> same arithmetic)."""
+import os
+import socket
+
+import numpy as np
+import pytest
+
+import paper_2501_11779_b200 as gh
+
+pytestmark = pytest.mark.gpu
+
+SPEC = gh.ModelSpec("split-gpu", 3, 512, 512, 1024, 4, 4, 64, 2, 1500)
+B, STEPS = 13, 6
+
+
+def n_gpus():
+    try:
+        return gh.lib().gh_device_count()
+    except Exception:
+        return 0
+
+
+def prompts():
+    return np.random.default_rng(9).integers(0, SPEC.vocab_size, size=(B, 3), dtype=np.int32)
+
+
+def run_engine(eng, ib_count=1):
+    """Greedy decode of `prompts()` on in-flight batch 0 (and a second identical batch when
+    ib_count == 2, decoded through gh_engine_step_all)."""
+    p = prompts()
+    tok = p[:, 0].copy()
+    toks, logits = [], []
+    for t in range(p.shape[1] - 1 + STEPS):
+        pos = np.full(B, t, np.int32)
+        nxt, lg = eng.step_host(tok, pos, want_logits=True)
+        if eng.role == "tier2":
+            continue
+        if t + 1 < p.shape[1]:
+            tok = p[:, t + 1].copy()
+        else:
+            toks.append(nxt)
+            logits.append(lg)
+            tok = nxt
+    return (np.stack(toks, 1), np.stack(logits, 1)) if toks else (None, None)
+
+
+def worker(rank, world, port, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    import torch
+    import torch.distributed as dist
+    from paper_2501_11779_b200.stages import Comm, Engine
+    torch.cuda.set_device(rank)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    obj = [Comm.unique_ids(1) if rank == 0 else None]
+    dist.broadcast_object_list(obj, src=0)
+    comm = Comm(obj[0], world, rank, rank)
+    eng = Engine(SPEC, batch=B, device=rank, use_graph=False, comm=comm)
+    toks, lg = run_engine(eng)
+    eng.close()
+    comm.close()
+    if rank == 0:
+        q.put((toks, lg))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.skipif(n_gpus() < 2, reason="needs >= 2 GPUs")
+@pytest.mark.parametrize("world", [2, 3])
+def test_nccl_tier_split_matches_colocated(world):
+    if n_gpus() < world:
+        pytest.skip(f"needs {world} GPUs")
+    import torch.multiprocessing as mp
+    from paper_2501_11779_b200.stages import Engine
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    toks, lg = q.get(timeout=600)
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    ref = Engine(SPEC, batch=B, use_graph=False)
+    rtoks, rlg = run_engine(ref)
+    ref.close()
+    assert np.array_equal(toks, rtoks)
+    assert np.array_equal(lg, rlg)

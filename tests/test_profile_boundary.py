@@ -1,0 +1,65 @@
+"""The kernel-latency CSV emitted through the C ABI (gh_profile_write_csv) is consumed by the
+reference's own parser (profiles.cpp:168-224) with no warnings, and latency queries through the
+reference (profiles.cpp:93-129) return the emitted values."""
+import ctypes as C
+
+import pytest
+
+import paper_2501_11779_b200 as gh
+from paper_2501_11779_b200 import _lib as L
+from paper_2501_11779_b200.profiles import write_profile
+from oracle import Ref, ref_available
+
+needs_ref = pytest.mark.skipif(not ref_available(), reason="oracle/_ref not built (no /root/reference)")
+
+
+def synthetic_rows():
+    grid = gh.batch_grid(1024)
+    na = {b: 40.0 + 0.09 * b for b in grid}                 # monotone non-attention
+    at = {b: 1.5 + 0.65 * b for b in grid}                  # linear attention
+    return grid, na, at
+
+
+def test_write_rejects_bad_rows(tmp_path):
+    p = tmp_path / "x.csv"
+    with pytest.raises(gh.ValidationError):
+        write_profile(p, "b200", [("nonattention", 1, 4, 0.0)])
+    with pytest.raises(gh.ValidationError):
+        write_profile(p, "b,200", [("nonattention", 1, 4, 1.0)])
+    with pytest.raises(gh.ValidationError):
+        write_profile(p, "b200", [("nonattention", 1, 0, 1.0)])
+
+
+def test_header_and_rows(tmp_path):
+    p = tmp_path / "x.csv"
+    write_profile(p, "b200", [("nonattention", 2048, 4, 12.5), ("attention", 2048, 4, 3.25)])
+    lines = p.read_text().splitlines()
+    assert lines[0] == "device,stage,seq_len,batch_size,latency_us"
+    assert lines[1] == "b200,nonattention,2048,4,12.5000"
+
+
+@needs_ref
+def test_reference_parser_accepts_emitted_csv(tmp_path):
+    grid, na, at = synthetic_rows()
+    rows = [("nonattention", 2048, b, na[b]) for b in grid] + [("attention", 2048, b, at[b]) for b in grid]
+    p = tmp_path / "b200.csv"
+    write_profile(p, "b200-sxm", rows)
+    rc, warnings = Ref.profile_check(p)
+    assert rc == 0, Ref.err()
+    assert warnings == 0
+    for b in grid:
+        rc, ns = Ref.profile_latency(p, 0, b)
+        assert rc == 0 and ns == round(na[b] * 1000)
+        rc, ns = Ref.profile_latency(p, 1, b, 2048)
+        assert rc == 0 and ns == round(at[b] * 1000)
+    # interpolation between emitted grid points (profiles.cpp:118-128)
+    rc, ns = Ref.profile_latency(p, 1, 5)
+    assert rc == 0 and abs(ns - round((at[4] + at[6]) / 2 * 1000)) <= 1
+
+
+@needs_ref
+def test_reference_parser_rejects_duplicates(tmp_path):
+    p = tmp_path / "dup.csv"
+    write_profile(p, "b200", [("attention", 512, 4, 1.0), ("attention", 512, 4, 2.0)])
+    rc, _ = Ref.profile_check(p)
+    assert rc == 2
