@@ -4,9 +4,11 @@
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config C2|C3]
 
 N = 1: config C2 (Llama-2-7B shape, batch 64, context 512, both tiers colocated on one B200).
-N > 1 (torchrun, one process per GPU): config C3 tier split — rank 0 = Tier-1 (weights),
-ranks 1..N-1 = Tier-2 (KV shards by prompt), NCCL send/recv of the PayloadModel messages every
-layer, IF = 2 in-flight batches; batch = the capacity-admitted batch (two_tier_context_slots).
+N > 1 (torchrun, one process per GPU): tier split of the same prompt shape — rank 0 = Tier-1
+(weights), ranks 1..N-1 = Tier-2 (KV shards by prompt), NCCL send/recv of the PayloadModel
+messages every layer, IF = 2 in-flight batches of 64 prompts per Tier-2 GPU each (weak scaling:
+fixed work per Tier-2 GPU).  --config C3: context 2048 at the capacity-admitted batch
+(two_tier_context_slots at 179 GiB per GPU; the requested 1024 does not fit).
 
 A step = one decode token for every prompt of every in-flight batch, all layers + classifier +
 greedy argmax, at a fixed context (each step appends at position ctx-1 and attends over ctx
@@ -133,13 +135,17 @@ def cpu_sample(spec, B, ctx, threads=0):
 # ------------------------------------------------------------------ configs
 def workload(args, world):
     import paper_2501_11779_b200 as gh
-    cfg = args.config or ("C2" if world == 1 else "C3")
+    cfg = args.config or "C2"
     c = gh.CONFIGS[cfg]
     spec, ctx = c["spec"], c["ctx"]
     if world == 1:
         return dict(name=cfg, spec=spec, ctx=ctx, batch=c["batch"], requested=c["batch"], inflight=1,
                     shard=c["batch"], kp=0)
     kp = world - 1
+    if cfg == "C2":  # weak scaling of the N=1 workload: 64 prompts per Tier-2 GPU per in-flight batch
+        return dict(name="C2-split", spec=spec, ctx=ctx, batch=c["batch"] * kp, requested=c["batch"] * kp * 2,
+                    inflight=2, shard=c["batch"], kp=kp,
+                    admitted_slots=gh.two_tier_context_slots(spec, 1, kp, 179 * GiB, ctx))
     mem = 179 * GiB
     slots = gh.two_tier_context_slots(spec, 1, kp, mem, ctx)  # optimizer.cpp:175-192
     inflight = 2
@@ -259,7 +265,7 @@ def run_split(args, wl, rank, world):
     spec, ctx, IF = wl["spec"], wl["ctx"], wl["inflight"]
     dev = int(os.environ.get("LOCAL_RANK", rank))
     torch.cuda.set_device(dev)
-    obj = [Comm.unique_ids(IF) if rank == 0 else None]
+    obj = [Comm.unique_ids(1) if rank == 0 else None]
     dist.broadcast_object_list(obj, src=0)
     comm = Comm(obj[0], world, rank, dev)
     eng = Engine(spec, batch=wl["batch"], inflight=IF, device=dev, use_graph=False, comm=comm)
@@ -302,16 +308,18 @@ def run_split(args, wl, rank, world):
     ms = float(t.item())
     launches = torch.tensor([per_step * args.steps], dtype=torch.float64)
     dist.all_reduce(launches, op=dist.ReduceOp.SUM)
-    # e2e: host tokens in / next tokens out on Tier-1 every step (in-flight batch 0..IF-1)
+    # e2e: the same pipelined step through the host API: tokens/positions of every in-flight
+    # batch copied in, next tokens copied out, every step
     dist.barrier()
     t0 = time.perf_counter()
     nsteps = max(2, args.steps // 2)
-    nxt = tok
+    toks = np.tile(tok, (IF, 1))
+    poss = np.tile(pos, (IF, 1))
     for _ in range(nsteps):
-        for ib in range(IF):
-            r, _ = eng.step_host(nxt if eng.role == "tier1" else None, pos if eng.role == "tier1" else None, ib=ib)
-            if r is not None:
-                nxt = r
+        r = eng.step_all_host(toks if eng.role == "tier1" else None, poss if eng.role == "tier1" else None,
+                              stream=stream)
+        if r is not None:
+            toks = r
     e2e_ms = torch.tensor([(time.perf_counter() - t0) * 1e3 / nsteps], dtype=torch.float64)
     dist.all_reduce(e2e_ms, op=dist.ReduceOp.MAX)
     eng.close()

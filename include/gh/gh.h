@@ -207,6 +207,11 @@ gh_status gh_engine_step_host(gh_engine* e, uint32_t ib, const int32_t* tok_host
 /* Full step over all in-flight batches, pipelined across batches (tier split) or sequential
  * (colocated).  Device-resident inputs (engine io buffers). */
 gh_status gh_engine_step_all(gh_engine* e, void* stream);
+/* End-to-end variant of gh_engine_step_all: copies every in-flight batch's tokens and positions
+ * from host ([inflight][batch] int32 each, row per batch), runs the pipelined step and copies
+ * the next tokens back ([inflight][batch]).  Synchronous.  Tier-2 ranks pass NULLs. */
+gh_status gh_engine_step_all_host(gh_engine* e, const int32_t* tok_host, const int32_t* pos_host,
+                                  int32_t* next_host, void* stream);
 /* Device pointers of in-flight batch ib: tok [B] int32, pos [B] int32, slot [B] uint32,
  * next [B] int32.  Any may be NULL. */
 gh_status gh_engine_io(gh_engine* e, uint32_t ib, int32_t** tok, int32_t** pos,
@@ -214,6 +219,8 @@ gh_status gh_engine_io(gh_engine* e, uint32_t ib, int32_t** tok, int32_t** pos,
 /* Device-side batch-state update for batch ib: tok <- next, pos += pos_increment (pos_increment
  * 0 keeps the context length fixed, the steady-state benchmark mode). Tier-1 / colocated only. */
 gh_status gh_engine_advance(gh_engine* e, uint32_t ib, int pos_increment, void* stream);
+/* Copy the next tokens of in-flight batch ib to host (synchronous; Tier-1 / colocated only). */
+gh_status gh_engine_read_next(gh_engine* e, uint32_t ib, int32_t* next_host);
 gh_tier1* gh_engine_tier1(gh_engine* e);
 gh_tier2* gh_engine_tier2(gh_engine* e);
 /* Launch count of this library's kernels since the last reset (device work accounting). */

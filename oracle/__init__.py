@@ -238,7 +238,7 @@ def rlib() -> C.CDLL:
             "ref_throughput_from": (C.c_int, [P(C.c_int64), u64, u64, u64, P(C.c_double)]),
             "ref_profile_check": (C.c_int, [C.c_char_p, P(C.c_int)]),
             "ref_profile_latency": (C.c_int, [C.c_char_p, C.c_int, u64, u64, P(C.c_int64)]),
-            "ref_cmd_simulate": (C.c_int, [C.c_char_p] * 4 + [u64, u64, u64, u64, C.c_char_p, u64]),
+            "ref_cmd_simulate": (C.c_int, [C.c_char_p] * 4 + [u64, u64, u64, u64, u64, C.c_char_p, u64]),
         }
         for n, (r, a) in sig.items():
             f = getattr(L, n)
@@ -322,8 +322,8 @@ class Ref:
         return rlib().ref_profile_latency(str(path).encode(), stage, batch, seq, C.byref(o)), o.value
 
     @staticmethod
-    def simulate(model, cluster, t1, t2, k1, k2, batch, seq=0):
+    def simulate(model, cluster, t1, t2, k1, k2, batch, seq=0, inflight=0):
         buf = C.create_string_buffer(1 << 20)
         rc = rlib().ref_cmd_simulate(*(str(p).encode() for p in (model, cluster, t1, t2)), k1, k2, batch, seq,
-                                     buf, 1 << 20)
+                                     inflight, buf, 1 << 20)
         return rc, buf.value.decode()

@@ -115,7 +115,8 @@ int ref_profile_latency(const char* path, int stage, uint64_t batch, uint64_t se
 }
 // Run a reference command in-process (commands.hpp:90-93); writes stdout into `out`.
 int ref_cmd_simulate(const char* model, const char* cluster, const char* t1_profile, const char* t2_profile,
-                     uint64_t k1, uint64_t k2, uint64_t batch, uint64_t seq, char* out, uint64_t cap) {
+                     uint64_t k1, uint64_t k2, uint64_t batch, uint64_t seq, uint64_t inflight, char* out,
+                     uint64_t cap) {
   std::ostringstream os, es;
   SimulateArgs a;
   a.model_path = model;
@@ -125,6 +126,7 @@ int ref_cmd_simulate(const char* model, const char* cluster, const char* t1_prof
   a.tier2_per_tier1 = k2;
   a.batch = batch;
   if (seq) a.seq_len = seq;
+  if (inflight) a.inflight_override = inflight;
   int rc = cmd_simulate(a, os, es);
   std::string s = os.str() + es.str();
   if (out && cap) { strncpy(out, s.c_str(), cap - 1); out[cap - 1] = 0; }

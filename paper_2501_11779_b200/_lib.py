@@ -110,8 +110,10 @@ PROTOTYPES = {
     "gh_engine_step_device": (st, [vp, u32, vp]),
     "gh_engine_step_host": (st, [vp, u32, vp, vp, vp, vp, vp]),
     "gh_engine_step_all": (st, [vp, vp]),
+    "gh_engine_step_all_host": (st, [vp, vp, vp, vp, vp]),
     "gh_engine_io": (st, [vp, u32, P(vp), P(vp), P(vp), P(vp)]),
     "gh_engine_advance": (st, [vp, u32, C.c_int, vp]),
+    "gh_engine_read_next": (st, [vp, u32, vp]),
     "gh_engine_tier1": (vp, [vp]),
     "gh_engine_tier2": (vp, [vp]),
     "gh_kernel_launches": (u64, [C.c_int]),

@@ -626,8 +626,6 @@ gh_status gh_engine_create(const gh_engine_config* cfg, gh_comm* comm, gh_engine
   if (world == 1) {
     e->role = 0;
   } else {
-    if ((int)comm->comms.size() < (int)cfg->inflight)
-      return fail(GH_EINVAL, "tier split needs one communicator per in-flight batch");
     e->role = rank == 0 ? 1 : 2;
     e->kp = world - 1;
     if ((int)cfg->batch < e->kp) return fail(GH_EINVAL, "batch smaller than the number of Tier-2 ranks");
@@ -683,6 +681,15 @@ gh_status gh_engine_destroy(gh_engine* e) {
 
 int gh_engine_role(const gh_engine* e) { return e ? e->role : -1; }
 gh_tier1* gh_engine_tier1(gh_engine* e) { return e ? e->t1 : nullptr; }
+
+gh_status gh_engine_read_next(gh_engine* e, uint32_t ib, int32_t* next_host) {
+  if (!e || ib >= e->batches.size() || !next_host) return fail(GH_EINVAL, "bad argument");
+  if (e->role == 2) return fail(GH_EINVAL, "Tier-2 ranks hold no token state");
+  GH_CUDA(cudaSetDevice(e->cfg.device));
+  GH_CUDA(cudaDeviceSynchronize());
+  GH_CUDA(cudaMemcpy(next_host, e->batches[ib].next, (size_t)e->cfg.batch * 4, cudaMemcpyDeviceToHost));
+  return GH_OK;
+}
 
 gh_status gh_engine_advance(gh_engine* e, uint32_t ib, int inc, void* stream) {
   if (!e || ib >= e->batches.size()) return fail(GH_EINVAL, "bad engine / batch index");
@@ -772,7 +779,7 @@ gh_status gh_engine_step_device(gh_engine* e, uint32_t ib, void* stream) {
     }
     return engine_layer_loop_colocated(e, b, false, st);
   }
-  ncclComm_t comm = e->comm->comms[ib];
+  ncclComm_t comm = e->comm->comms[0];
   GH_TRY(split_begin(e, b, comm, st));
   void* x = b.x0;
   void* xn = b.x1;
@@ -783,32 +790,132 @@ gh_status gh_engine_step_device(gh_engine* e, uint32_t ib, void* stream) {
 
 // All in-flight batches; in split mode the batches are interleaved layer by layer on their own
 // streams so that Tier-1 compute of one batch overlaps Tier-2 attention of another.
+// ---- tier split, all in-flight batches, one stream per rank, software-pipelined.
+// Tier-1 issue order: embed_b, pre_b(0) for every batch b, then for each layer l and batch b:
+//   [group: pending sends + recv_b(l)] -> post_b(l) -> pre_b(l+1) (its send becomes pending)
+// Tier-2: [group: positions + recv_0(0)] -> for each (l, b): attend_b(l) -> [group: send_b(l) +
+// recv of the next (batch, layer)].  Every send is grouped with the recv the issuing rank needs
+// next, so the rendezvous of both directions progresses together (no deadlock), and while
+// Tier-2 attends batch b Tier-1 runs F3 / F1 of the other batches.  A single stream means no
+// NCCL kernel ever spins next to a persistent GEMM / attention grid on the same GPU.
+static gh_status t1_group(gh_engine* e, ncclComm_t comm, cudaStream_t st, std::vector<int>& pending_send,
+                          int recv_ib, bool pos_header) {
+  auto& api = nccl();
+  const Shape& s = e->sh;
+  const size_t fwd_row = (size_t)s.ld_fwd() * s.db, bwd_row = (size_t)s.ld_bwd() * s.db;
+  GH_NCCL(api.GroupStart());
+  if (pos_header)
+    for (auto& b : e->batches)
+      for (int j = 0; j < e->kp; ++j)
+        GH_NCCL(api.Send(b.pos + e->shard_off[j], e->shard_cnt[j], ncclInt32, j + 1, comm, st));
+  for (int ib : pending_send) {
+    auto& b = e->batches[ib];
+    for (int j = 0; j < e->kp; ++j)
+      GH_NCCL(api.Send((char*)b.fwd + e->shard_off[j] * fwd_row, e->shard_cnt[j] * fwd_row, ncclUint8, j + 1,
+                       comm, st));
+  }
+  if (recv_ib >= 0) {
+    auto& b = e->batches[recv_ib];
+    for (int j = 0; j < e->kp; ++j)
+      GH_NCCL(api.Recv((char*)b.bwd + e->shard_off[j] * bwd_row, e->shard_cnt[j] * bwd_row, ncclUint8, j + 1,
+                       comm, st));
+  }
+  GH_NCCL(api.GroupEnd());
+  pending_send.clear();
+  return GH_OK;
+}
+
+static gh_status t2_group(gh_engine* e, ncclComm_t comm, cudaStream_t st, int send_ib, int recv_ib,
+                          bool pos_header) {
+  auto& api = nccl();
+  const Shape& s = e->sh;
+  const size_t fwd_row = (size_t)s.ld_fwd() * s.db, bwd_row = (size_t)s.ld_bwd() * s.db;
+  GH_NCCL(api.GroupStart());
+  if (pos_header)
+    for (auto& b : e->batches) GH_NCCL(api.Recv(b.pos, e->my_cnt, ncclInt32, 0, comm, st));
+  if (send_ib >= 0) GH_NCCL(api.Send(e->batches[send_ib].bwd, e->my_cnt * bwd_row, ncclUint8, 0, comm, st));
+  if (recv_ib >= 0) GH_NCCL(api.Recv(e->batches[recv_ib].fwd, e->my_cnt * fwd_row, ncclUint8, 0, comm, st));
+  GH_NCCL(api.GroupEnd());
+  return GH_OK;
+}
+
+static gh_status split_step_pipelined(gh_engine* e, cudaStream_t st) {
+  const int nb = (int)e->batches.size();
+  const int N = e->sh.N;
+  ncclComm_t comm = e->comm->comms[0];
+  if (e->role == 1) {
+    std::vector<void*> x(nb), xn(nb);
+    std::vector<int> pending;
+    bool header = true;
+    for (int ib = 0; ib < nb; ++ib) {
+      auto& b = e->batches[ib];
+      x[ib] = b.x0; xn[ib] = b.x1;
+      GH_TRY(gh_tier1_embed(e->t1, e->cfg.batch, b.tok, b.x0, st));
+      GH_TRY(gh_tier1_pre(e->t1, 0, e->cfg.batch, x[ib], b.pos, b.fwd, st));
+      pending.push_back(ib);
+      if (ib < nb - 1) {  // let Tier-2 start on batch ib while batch ib+1 is prepared
+        GH_TRY(t1_group(e, comm, st, pending, -1, header));
+        header = false;
+      }
+    }
+    for (int l = 0; l < N; ++l)
+      for (int ib = 0; ib < nb; ++ib) {
+        auto& b = e->batches[ib];
+        GH_TRY(t1_group(e, comm, st, pending, ib, header));
+        header = false;
+        GH_TRY(gh_tier1_post(e->t1, l, e->cfg.batch, b.bwd, xn[ib], st));
+        std::swap(x[ib], xn[ib]);
+        if (l + 1 < N) {
+          GH_TRY(gh_tier1_pre(e->t1, l + 1, e->cfg.batch, x[ib], b.pos, b.fwd, st));
+          pending.push_back(ib);
+        } else {
+          GH_TRY(gh_tier1_classify(e->t1, e->cfg.batch, x[ib], nullptr, b.next, st));
+        }
+      }
+    if (!pending.empty()) GH_TRY(t1_group(e, comm, st, pending, -1, false));
+  } else {
+    GH_TRY(t2_group(e, comm, st, -1, 0, true));
+    for (int l = 0; l < N; ++l)
+      for (int ib = 0; ib < nb; ++ib) {
+        auto& b = e->batches[ib];
+        GH_TRY(gh_tier2_attend(e->t2, l, e->my_cnt, b.slot, b.pos, b.fwd, b.bwd, st));
+        const bool last = (l == N - 1 && ib == nb - 1);
+        GH_TRY(t2_group(e, comm, st, ib, last ? -1 : (ib + 1) % nb, false));
+      }
+  }
+  return GH_OK;
+}
+
 gh_status gh_engine_step_all(gh_engine* e, void* stream) {
   if (!e) return fail(GH_EINVAL, "null engine");
   cudaStream_t st = (cudaStream_t)stream;
   GH_CUDA(cudaSetDevice(e->cfg.device));
   const int nb = (int)e->batches.size();
-  if (e->role == 0 || nb == 1) {
+  if (e->role == 0) {
     for (int ib = 0; ib < nb; ++ib) GH_TRY(gh_engine_step_device(e, ib, stream));
     return GH_OK;
   }
-  GH_CUDA(cudaEventRecord(e->fork, st));
-  std::vector<void*> x(nb), xn(nb);
-  for (int ib = 0; ib < nb; ++ib) {
-    auto& b = e->batches[ib];
-    GH_CUDA(cudaStreamWaitEvent(b.stream, e->fork, 0));
-    GH_TRY(split_begin(e, b, e->comm->comms[ib], b.stream));
-    x[ib] = b.x0; xn[ib] = b.x1;
+  return split_step_pipelined(e, st);
+}
+
+gh_status gh_engine_step_all_host(gh_engine* e, const int32_t* tok_host, const int32_t* pos_host,
+                                  int32_t* next_host, void* stream) {
+  if (!e) return fail(GH_EINVAL, "null engine");
+  cudaStream_t st = (cudaStream_t)stream;
+  GH_CUDA(cudaSetDevice(e->cfg.device));
+  const size_t R = e->cfg.batch;
+  if (e->role != 2) {
+    if (!tok_host || !pos_host || !next_host) return fail(GH_EINVAL, "host token/pos/next buffers required");
+    for (size_t ib = 0; ib < e->batches.size(); ++ib) {
+      GH_CUDA(cudaMemcpyAsync(e->batches[ib].tok, tok_host + ib * R, R * 4, cudaMemcpyHostToDevice, st));
+      GH_CUDA(cudaMemcpyAsync(e->batches[ib].pos, pos_host + ib * R, R * 4, cudaMemcpyHostToDevice, st));
+    }
   }
-  for (int l = 0; l < e->sh.N; ++l)
-    for (int ib = 0; ib < nb; ++ib)
-      GH_TRY(split_layer(e, e->batches[ib], e->comm->comms[ib], l, &x[ib], &xn[ib], e->batches[ib].stream));
-  for (int ib = 0; ib < nb; ++ib) {
-    auto& b = e->batches[ib];
-    if (e->role == 1) GH_TRY(gh_tier1_classify(e->t1, e->cfg.batch, x[ib], nullptr, b.next, b.stream));
-    GH_CUDA(cudaEventRecord(b.done, b.stream));
-    GH_CUDA(cudaStreamWaitEvent(st, b.done, 0));
-  }
+  GH_TRY(gh_engine_step_all(e, stream));
+  if (e->role != 2)
+    for (size_t ib = 0; ib < e->batches.size(); ++ib)
+      GH_CUDA(cudaMemcpyAsync(next_host + ib * R, e->batches[ib].next, R * 4, cudaMemcpyDeviceToHost, st));
+  GH_CUDA(cudaStreamSynchronize(st));
   return GH_OK;
 }
 
@@ -827,7 +934,7 @@ gh_status gh_engine_step_host(gh_engine* e, uint32_t ib, const int32_t* tok_host
   if (logits_host && e->role == 0) {
     GH_TRY(engine_layer_loop_colocated(e, b, true, st));
   } else if (logits_host && e->role == 1) {
-    ncclComm_t comm = e->comm->comms[ib];
+    ncclComm_t comm = e->comm->comms[0];
     GH_TRY(split_begin(e, b, comm, st));
     void* x = b.x0;
     void* xn = b.x1;

@@ -187,11 +187,29 @@ class Engine:
                                             None if lg is None else lg.ctypes.data, _stream(stream)))
         return nxt, lg
 
+    def step_all_host(self, tok: np.ndarray | None, pos: np.ndarray | None, stream=None):
+        """End-to-end pipelined step over all in-flight batches: tok/pos [inflight, batch] int32
+        host arrays in, next tokens [inflight, batch] out (Tier-2 ranks pass None)."""
+        if self.role == "tier2":
+            L.check(L.lib().gh_engine_step_all_host(self.h, None, None, None, _stream(stream)))
+            return None
+        t = np.ascontiguousarray(tok, dtype=np.int32).reshape(self.inflight, self.batch)
+        p = np.ascontiguousarray(pos, dtype=np.int32).reshape(self.inflight, self.batch)
+        nxt = np.empty((self.inflight, self.batch), dtype=np.int32)
+        L.check(L.lib().gh_engine_step_all_host(self.h, t.ctypes.data, p.ctypes.data, nxt.ctypes.data,
+                                                _stream(stream)))
+        return nxt
+
     def step_device(self, ib=0, stream=None):
         L.check(L.lib().gh_engine_step_device(self.h, ib, _stream(stream)))
 
     def step_all(self, stream=None):
         L.check(L.lib().gh_engine_step_all(self.h, _stream(stream)))
+
+    def read_next(self, ib=0) -> np.ndarray:
+        out = np.empty(self.batch, dtype=np.int32)
+        L.check(L.lib().gh_engine_read_next(self.h, ib, out.ctypes.data))
+        return out
 
     def advance(self, ib=0, pos_increment=0, stream=None):
         L.check(L.lib().gh_engine_advance(self.h, ib, pos_increment, _stream(stream)))

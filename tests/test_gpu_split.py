@@ -91,3 +91,64 @@ def test_nccl_tier_split_matches_colocated(world):
     ref.close()
     assert np.array_equal(toks, rtoks)
     assert np.array_equal(lg, rlg)
+
+
+def worker_all(rank, world, port, q, IF):
+    """step_all (pipelined, all in-flight batches) + advance for STEPS steps."""
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    import torch
+    import torch.distributed as dist
+    from paper_2501_11779_b200.stages import Comm, Engine
+    torch.cuda.set_device(rank)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    comm = None
+    if world > 1:
+        obj = [Comm.unique_ids(1) if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        comm = Comm(obj[0], world, rank, rank)
+    out = run_all(Engine(SPEC, batch=B, inflight=IF, device=rank, use_graph=False, comm=comm), IF)
+    if rank == 0:
+        q.put(out)
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def run_all(eng, IF):
+    p = prompts()
+    for ib in range(IF):  # step 0 through the host path sets tokens/positions of every batch
+        eng.step_host(np.roll(p[:, 0], ib) if eng.role != "tier2" else None,
+                      np.zeros(B, np.int32) if eng.role != "tier2" else None, ib=ib)
+    seq = []
+    for _ in range(STEPS):
+        if eng.role != "tier2":
+            for ib in range(IF):
+                eng.advance(ib, 1)
+        eng.step_all()
+        if eng.role != "tier2":
+            seq.append(np.stack([eng.read_next(ib) for ib in range(IF)]))
+    eng.close()
+    return np.stack(seq) if seq else None
+
+
+@pytest.mark.skipif(n_gpus() < 2, reason="needs >= 2 GPUs")
+@pytest.mark.parametrize("world,IF", [(2, 2), (3, 2), (2, 3)])
+def test_pipelined_step_all_matches_colocated(world, IF):
+    if n_gpus() < world:
+        pytest.skip(f"needs {world} GPUs")
+    import torch.multiprocessing as mp
+    from paper_2501_11779_b200.stages import Engine
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=worker_all, args=(r, world, port, q, IF)) for r in range(world)]
+    for p in procs:
+        p.start()
+    got = q.get(timeout=600)
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    ref = run_all(Engine(SPEC, batch=B, inflight=IF, use_graph=False), IF)
+    assert np.array_equal(got, ref)
