@@ -34,17 +34,6 @@ namespace gh {
 constexpr int kBlockM = 128;   // weight rows per tile (UMMA M)
 constexpr int kBlockK = 64;    // 64 bf16 = 128 B = one swizzle atom row
 constexpr int kGemmThreads = 192;
-constexpr int kEpiCols = 64;   // epilogue column group (staging width)
-
-// Shared memory: [stage ring][epilogue staging][barriers]
-//   epilogue staging: otile [64][128] bf16 | rtile [64][128] bf16 | pos [64] int | argmax 512 B
-struct EpiSmem {
-  static constexpr int kO = 0;
-  static constexpr int kR = kEpiCols * 256;
-  static constexpr int kPos = 2 * kEpiCols * 256;
-  static constexpr int kRed = kPos + kEpiCols * 4;
-  static constexpr int kBytes = kRed + 512;
-};
 
 GH_DEV float silu_f(float g) { return g / (1.0f + __expf(-g)); }
 
@@ -79,151 +68,10 @@ GH_DEV void epi_store_one(const EpiParams& ep, int n, int b, float v, float part
   }
 }
 
-// ------------------------------------------------------------------ tile epilogue
-// The accumulator tile is 128 weight rows (n) x BN batch columns (b); thread `row` of the four
-// epilogue warps owns weight row n0+row.  Outputs are row-major [b][n], so 64-column groups are
-// staged through shared memory and written (and the residual read) with coalesced 16-byte
-// accesses; per-column scalars (positions, RoPE factors) are loaded in independent batches.
-GH_DEV void epi_bar() { asm volatile("bar.sync 1, 128;\n" ::: "memory"); }
-
-// coalesced copy of a [rows][cols] bf16 tile between global (row stride ld) and shared memory
-template <bool kToShared>
-GH_DEV void tile_copy(uint16_t* sm, int sm_ld, uint16_t* gm, long ld, int rows, int cols, int valid_cols) {
-  const int t = threadIdx.x - 64;
-  const bool vec = valid_cols == cols && ((uintptr_t)gm & 15) == 0 && (ld % 8) == 0;
-  if (vec) {
-    const int cpr = cols / 8;
-    for (int i = t; i < rows * cpr; i += 128) {
-      const int r = i / cpr, c = (i % cpr) * 8;
-      if (kToShared) *(uint4*)(sm + r * sm_ld + c) = *(const uint4*)(gm + (long)r * ld + c);
-      else *(uint4*)(gm + (long)r * ld + c) = *(const uint4*)(sm + r * sm_ld + c);
-    }
-  } else {
-    for (int i = t; i < rows * cols; i += 128) {
-      const int r = i / cols, c = i % cols;
-      if (c >= valid_cols) continue;
-      if (kToShared) sm[r * sm_ld + c] = gm[(long)r * ld + c];
-      else gm[(long)r * ld + c] = sm[r * sm_ld + c];
-    }
-  }
-}
-
-// before a column group [g0, g0+64): residual tile / positions into shared memory
-GH_DEV void epi_group_begin(const EpiParams& ep, const GemmShape& gs, int n0, int g0, uint8_t* esm) {
-  const int rows = min(kEpiCols, gs.Bt - g0);
-  epi_bar();  // the previous group's staged tile has been stored
-  if (ep.kind == EPI_STORE_RESID)
-    tile_copy<true>((uint16_t*)(esm + EpiSmem::kR), 128, (uint16_t*)ep.resid + (long)g0 * ep.ldr + n0,
-                    ep.ldr, rows, 128, min(128, gs.N - n0));
-  if (ep.kind == EPI_QKV_ROPE) {
-    int* ps = (int*)(esm + EpiSmem::kPos);
-    for (int i = threadIdx.x - 64; i < rows; i += 128) ps[i] = ep.pos[g0 + i];
-  }
-  epi_bar();
-}
-
-// 16 accumulator columns [c0, c0+16) (absolute batch index b = c0 + j, group base g0)
-GH_DEV void epi_chunk(const EpiParams& ep, const GemmShape& gs, int row, int n0, int g0, int c0,
-                      const float* v, uint8_t* esm, int tile_n) {
-  const int n = n0 + row;
-  const bool row_ok = n < gs.N;
-  const int lc = c0 - g0;  // local column in the staging tile
-  uint16_t* ot = (uint16_t*)(esm + EpiSmem::kO);
-  switch (ep.kind) {
-    case EPI_STORE:
-#pragma unroll
-      for (int j = 0; j < 16; ++j) ot[(lc + j) * 128 + row] = f32_to_bf16(v[j]);
-      return;
-    case EPI_STORE_RESID: {
-      const uint16_t* rt = (const uint16_t*)(esm + EpiSmem::kR);
-#pragma unroll
-      for (int j = 0; j < 16; ++j)
-        ot[(lc + j) * 128 + row] = f32_to_bf16(v[j] + bf16_to_f32(rt[(lc + j) * 128 + row]));
-      return;
-    }
-    case EPI_QKV_ROPE: {
-      const int* ps = (const int*)(esm + EpiSmem::kPos);
-      const bool rope = n < ep.rope_rows;
-      const int half = ep.d_head >> 1, pair = (n % ep.d_head) >> 1;
-      const bool odd = (n & 1) != 0;
-      float2 cs[16];
-#pragma unroll
-      for (int j = 0; j < 16; ++j) {  // independent loads, issued back to back
-        const int b = min(c0 + j, gs.Bt - 1) - g0;
-        cs[j] = rope ? __ldg(ep.rope + (long)ps[b] * half + pair) : make_float2(1.f, 0.f);
-      }
-#pragma unroll
-      for (int j = 0; j < 16; ++j) {
-        const float partner = __shfl_xor_sync(0xffffffffu, v[j], 1);
-        // pair (a, c) = (even, odd): even' = a cos - c sin, odd' = a sin + c cos
-        const float x = odd ? (partner * cs[j].y + v[j] * cs[j].x) : (v[j] * cs[j].x - partner * cs[j].y);
-        ot[(lc + j) * 128 + row] = f32_to_bf16(x);
-      }
-      return;
-    }
-    case EPI_SWIGLU: {
-      const bool odd = (row & 1) != 0;
-#pragma unroll
-      for (int j = 0; j < 16; ++j) {
-        const float up = __shfl_xor_sync(0xffffffffu, v[j], 1);
-        if (!odd) ot[(lc + j) * 128 + (row >> 1)] = f32_to_bf16(silu_f(v[j]) * up);
-      }
-      return;
-    }
-    default:
-      break;
-  }
-  // EPI_LOGITS_ARGMAX: logits (optional) + (max, argmax) across the tile's 128 rows per column
-  float* red = (float*)(esm + EpiSmem::kRed);
-  const int wq = (threadIdx.x >> 5) & 3;
-#pragma unroll
-  for (int j = 0; j < 16; ++j) {
-    const int b = c0 + j;
-    float val = row_ok ? v[j] : -INFINITY;
-    int idx = row_ok ? n : 0x7fffffff;
-    if (ep.logits && row_ok && b < gs.Bt) ep.logits[(long)b * ep.ldl + n] = v[j];
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-      const float ov = __shfl_xor_sync(0xffffffffu, val, o);
-      const int oi = __shfl_xor_sync(0xffffffffu, idx, o);
-      if (ov > val || (ov == val && oi < idx)) { val = ov; idx = oi; }
-    }
-    if ((threadIdx.x & 31) == 0) {
-      red[(wq * 16 + j) * 2] = val;
-      red[(wq * 16 + j) * 2 + 1] = __int_as_float(idx);
-    }
-  }
-  epi_bar();
-  if (threadIdx.x >= 64 && threadIdx.x < 64 + 16) {
-    const int j = threadIdx.x - 64;
-    float best = red[j * 2];
-    int bi = __float_as_int(red[j * 2 + 1]);
-#pragma unroll
-    for (int w = 1; w < 4; ++w) {
-      const float ov = red[(w * 16 + j) * 2];
-      const int oi = __float_as_int(red[(w * 16 + j) * 2 + 1]);
-      if (ov > best || (ov == best && oi < bi)) { best = ov; bi = oi; }
-    }
-    const int b = c0 + j;
-    if (b < gs.Bt) ep.part[(long)tile_n * gs.Bt + b] = make_float2(best, __int_as_float(bi));
-  }
-  epi_bar();
-}
-
-GH_DEV void epi_group_end(const EpiParams& ep, const GemmShape& gs, int n0, int g0, uint8_t* esm) {
-  if (ep.kind == EPI_LOGITS_ARGMAX) return;
-  epi_bar();
-  const int rows = min(kEpiCols, gs.Bt - g0);
-  uint16_t* ot = (uint16_t*)(esm + EpiSmem::kO);
-  uint16_t* out = (uint16_t*)ep.out;
-  if (ep.kind == EPI_SWIGLU)
-    tile_copy<false>(ot, 128, out + (long)g0 * ep.ldo + n0 / 2, ep.ldo, rows, 64, min(64, (gs.N - n0) / 2));
-  else
-    tile_copy<false>(ot, 128, out + (long)g0 * ep.ldo + n0, ep.ldo, rows, 128, min(128, gs.N - n0));
-}
-
 // ------------------------------------------------------------------ cluster split-K epilogue
-// Slice epilogue (BN <= 64): thread t of the 128 epilogue threads owns batch column
+GH_DEV void epi_bar() { asm volatile("bar.sync 1, 128;\n" ::: "memory"); }  // the 4 epilogue warps
+
+// Slice epilogue: thread t of the 128 epilogue threads owns batch column
 // b = t / (128/BN) and a run of En = BN/C consecutive weight rows n of the CTA's slice; it has
 // the fully reduced fp32 values in `v` and writes its outputs directly (row-major [b][n]).
 template <int En>
@@ -340,9 +188,8 @@ struct GemmSmem {
   static constexpr int kBBytes = BN * kBlockK * 2;
   static constexpr int kStageBytes = kABytes + kBBytes;
   static constexpr int kMaxStages = 16;
-  static constexpr bool kSplit = BN <= 64;                 // cluster split-K capable
-  // BN <= 64: fp32 partial tile [BN][128] published to the cluster; BN > 64: staging tiles
-  static constexpr int kEpiBytes = kSplit ? BN * 128 * 4 : EpiSmem::kBytes;
+  // receive buffer: C pushed partial slices [C][BN][128/C] (one tile of fp32 in total)
+  static constexpr int kEpiBytes = BN * 128 * 4;
   static constexpr uint32_t kAccCols = BN < 32 ? 32 : BN;  // one accumulator buffer
   static constexpr uint32_t kTmemCols = 2 * kAccCols <= 64 ? 64 : 2 * kAccCols <= 128 ? 128
                                       : 2 * kAccCols <= 256 ? 256 : 512;
@@ -356,38 +203,55 @@ struct GemmSmem {
   }
 };
 
+// Receive buffer of the CTA that owns rows [r*R, (r+1)*R) of a tile (R = 128/C):
+//   recv[src rank p][batch column b][row_local]   (fp32, C*BN*R floats = one full partial)
+// Every CTA pushes each of its partial values into the owner's buffer with posted DSMEM stores
+// while it drains TMEM, so the owner reduces from local shared memory (no remote round trip).
+// The 16-byte chunks of a row are XOR-swizzled by the batch column so that the owner's float4
+// reads of consecutive columns hit distinct banks.
 template <int BN, int C>
-GH_DEV void reduce_and_store(const EpiParams& ep, const GemmShape& gs, uint32_t red_saddr, int r, int n0,
+GH_DEV int recv_index(int p, int b, int rl) {
+  constexpr int R = 128 / C;
+  return (p * BN + b) * R + ((((rl >> 2) ^ (b & (R / 4 - 1)))) << 2) + (rl & 3);
+}
+template <int BN, int C>
+GH_DEV void push_partial(uint32_t recv_saddr, int rank, int row, const float* v16, int c0) {
+  constexpr int R = 128 / C;
+  const int owner = row / R, rl = row % R;
+  const uint32_t dst = mapa_shared(recv_saddr, owner);
+#pragma unroll
+  for (int e = 0; e < 16; ++e)
+    asm volatile("st.shared::cluster.f32 [%0], %1;" ::"r"(dst + (uint32_t)recv_index<BN, C>(rank, c0 + e, rl) * 4),
+                 "f"(v16[e]) : "memory");
+}
+
+template <int BN, int C>
+GH_DEV void reduce_and_store(const EpiParams& ep, const GemmShape& gs, const float* recv, int r, int n0,
                              int b0, int tile_n, uint32_t consumed_saddr, unsigned long long* tr) {
-  // thread -> (column b, run of En rows inside this CTA's slice of 128/C rows)
+  // thread -> (column b, run of En rows inside this CTA's slice of R = 128/C rows)
+  constexpr int R = 128 / C;
   constexpr int En = BN / C;
   constexpr int kRuns = 128 / BN;
   const int t = threadIdx.x - 64;
   const int b = t / kRuns;
-  const int nl = r * (128 / C) + (t % kRuns) * En;
-  // issue every remote load first (one DSMEM round trip), then sum in rank order (deterministic)
-  float4 q[C][En / 4];
-#pragma unroll
-  for (int p = 0; p < C; ++p) {
-    const uint32_t src = mapa_shared(red_saddr, p) + (uint32_t)(b * 128 + nl) * 4;
-#pragma unroll
-    for (int e = 0; e < En / 4; ++e) q[p][e] = ld_dsmem_f4(src + e * 16);
-  }
+  const int rl = (t % kRuns) * En;
   float v[En];
 #pragma unroll
-  for (int e = 0; e < En / 4; ++e) {
-    float4 a = q[0][e];
+  for (int e = 0; e < En; e += 4) {
+    float4 a = *(const float4*)(recv + recv_index<BN, C>(0, b, rl + e));
 #pragma unroll
-    for (int p = 1; p < C; ++p) { a.x += q[p][e].x; a.y += q[p][e].y; a.z += q[p][e].z; a.w += q[p][e].w; }
-    v[4 * e] = a.x; v[4 * e + 1] = a.y; v[4 * e + 2] = a.z; v[4 * e + 3] = a.w;
+    for (int p = 1; p < C; ++p) {  // rank order: deterministic
+      const float4 q = *(const float4*)(recv + recv_index<BN, C>(p, b, rl + e));
+      a.x += q.x; a.y += q.y; a.z += q.z; a.w += q.w;
+    }
+    v[e] = a.x; v[e + 1] = a.y; v[e + 2] = a.z; v[e + 3] = a.w;
   }
-  // every remote value is in registers: tell the peers their partial buffers are free again
   if (tr) tr[15] = globaltimer();
+  // my receive buffer is free again: every peer may push its next tile
   epi_bar();
   if (threadIdx.x == 64)
     for (int p = 0; p < C; ++p) mbar_arrive_cluster_relaxed(mapa_shared(consumed_saddr, p));
-  // all peers may reuse their partial buffer once everyone has read: caller signals
-  epi_slice<BN, En>(ep, gs, n0 + nl, b0 + b, v, tile_n * C + r);
+  epi_slice<BN, En>(ep, gs, n0 + r * R + rl, b0 + b, v, tile_n * C + r);
 }
 
 template <int BN>
@@ -536,40 +400,47 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       tc_fence_after();
       const bool tr = trace && threadIdx.x == 64 && j == my_tiles - 1;
       if (tr) trace[7] = globaltimer();
-      if constexpr (L::kSplit) {
-        // drain TMEM, release it to the MMA warp, publish the partial to the cluster
-        float v[BN];
-#pragma unroll
+      {
+        // drain TMEM and push every value to the CTA that owns its rows, release TMEM
+        if (tr) trace[8] = globaltimer();
+        if (j > 0) mbar_wait_cluster(consumed, (j - 1) & 1);  // every owner has read tile j-1
+        if (tr) trace[9] = globaltimer();
+#pragma unroll 1
         for (int c0 = 0; c0 < BN; c0 += 16) {
           uint32_t r[16];
           tmem_ld16(taddr + c0, r);
           tmem_ld_wait();
+          float v16[16];
 #pragma unroll
-          for (int e = 0; e < 16; ++e) v[c0 + e] = __uint_as_float(r[e]);
+          for (int e = 0; e < 16; ++e) v16[e] = __uint_as_float(r[e]);
+          switch (C) {
+            case 1: push_partial<BN, 1>(red_saddr, rank, row, v16, c0); break;
+            case 2: push_partial<BN, 2>(red_saddr, rank, row, v16, c0); break;
+            case 4: push_partial<BN, 4>(red_saddr, rank, row, v16, c0); break;
+            default: push_partial<BN, 8>(red_saddr, rank, row, v16, c0); break;
+          }
         }
         tc_fence_before();
         __syncwarp();
         if ((threadIdx.x & 31) == 0) mbar_arrive(&tempty[acc]);
-        if (tr) trace[8] = globaltimer();
-        if (j > 0) mbar_wait_cluster(consumed, (j - 1) & 1);  // peers done reading tile j-1
-        if (tr) trace[9] = globaltimer();
-#pragma unroll
-        for (int c = 0; c < BN; ++c) red[c * 128 + row] = v[c];
-        epi_bar();  // the four warps' partial writes happen before thread 64's cluster fence
+        epi_bar();  // the four warps' pushes happen before thread 64's cluster fence
         if (threadIdx.x == 64) {
           fence_acq_rel_cluster();
           for (int p = 0; p < C; ++p) mbar_arrive_cluster_relaxed(mapa_shared(smem_u32(ready), p));
         }
         if (tr) trace[10] = globaltimer();
-        mbar_wait_cluster(ready, j & 1);  // every peer's partial of this tile is visible
+        mbar_wait_cluster(ready, j & 1);  // every peer's push into my buffer is visible
         if (tr) trace[11] = globaltimer();
+        unsigned long long* rt = tr ? trace : nullptr;
         if (!skip) {
           switch (C) {
-            case 1: reduce_and_store<BN, 1>(ep, gs, red_saddr, rank, n0, b0, tile_n, smem_u32(consumed), tr ? trace : nullptr); break;
-            case 2: reduce_and_store<BN, 2>(ep, gs, red_saddr, rank, n0, b0, tile_n, smem_u32(consumed), tr ? trace : nullptr); break;
-            case 4: reduce_and_store<BN, 4>(ep, gs, red_saddr, rank, n0, b0, tile_n, smem_u32(consumed), tr ? trace : nullptr); break;
+            case 1:
+              if constexpr (BN <= 64) reduce_and_store<BN, 1>(ep, gs, red, rank, n0, b0, tile_n, smem_u32(consumed), rt);
+              break;
+            case 2: reduce_and_store<BN, 2>(ep, gs, red, rank, n0, b0, tile_n, smem_u32(consumed), rt); break;
+            case 4: reduce_and_store<BN, 4>(ep, gs, red, rank, n0, b0, tile_n, smem_u32(consumed), rt); break;
             case 8:
-              if constexpr (BN >= 32) reduce_and_store<BN, 8>(ep, gs, red_saddr, rank, n0, b0, tile_n, smem_u32(consumed), tr ? trace : nullptr);
+              if constexpr (BN >= 32) reduce_and_store<BN, 8>(ep, gs, red, rank, n0, b0, tile_n, smem_u32(consumed), rt);
               break;
           }
         }
@@ -580,29 +451,9 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
             for (int p = 0; p < C; ++p) mbar_arrive_cluster_relaxed(mapa_shared(smem_u32(consumed), p));
         }
         if (tr) trace[13] = globaltimer();
-      } else {
-        // wide batch tile (C == 1): epilogue straight from TMEM in 64-column staged groups
-        if (!skip) {
-          for (int g = 0; g < BN && b0 + g < gs.Bt; g += kEpiCols) {
-            epi_group_begin(ep, gs, n0, b0 + g, esm);
-            for (int c = g; c < g + kEpiCols && b0 + c < gs.Bt; c += 16) {
-              uint32_t r[16];
-              tmem_ld16(taddr + c, r);
-              tmem_ld_wait();
-              float v[16];
-#pragma unroll
-              for (int e = 0; e < 16; ++e) v[e] = __uint_as_float(r[e]);
-              epi_chunk(ep, gs, row, n0, b0 + g, b0 + c, v, esm, tile_n);
-            }
-            epi_group_end(ep, gs, n0, b0 + g, esm);
-          }
-        }
-        tc_fence_before();
-        __syncwarp();
-        if ((threadIdx.x & 31) == 0) mbar_arrive(&tempty[acc]);
       }
     }
-    if (L::kSplit && my_tiles > 0) mbar_wait_cluster(consumed, (my_tiles - 1) & 1);  // peers done with my smem
+    if (my_tiles > 0) mbar_wait_cluster(consumed, (my_tiles - 1) & 1);  // peers done with my smem
     if (trace && threadIdx.x == 64) trace[14] = globaltimer();
   }
   if (trace && threadIdx.x == 64) trace[5] = globaltimer();

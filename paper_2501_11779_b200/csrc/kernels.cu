@@ -356,7 +356,7 @@ cudaError_t make_tmap_bf16(CUtensorMap* out, const void* base, uint64_t rows, ui
   return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorInvalidValue;
 }
 
-static const int kBNs[] = {16, 32, 64, 128, 256};
+static const int kBNs[] = {16, 32, 64, 128};  // batches > 128 use several batch tiles
 static int stages_override = 0;  // diagnostics
 static int cluster_override = 0;  // diagnostics
 
@@ -398,8 +398,7 @@ static int max_clusters_bn(int BN, int C) {
     case 16: return max_clusters<16>(C);
     case 32: return max_clusters<32>(C);
     case 64: return max_clusters<64>(C);
-    case 128: return max_clusters<128>(C);
-    default: return max_clusters<256>(C);
+    default: return max_clusters<128>(C);
   }
 }
 
@@ -407,8 +406,8 @@ static int max_clusters_bn(int BN, int C) {
 // rounds(C) * (ceil(KB / C) + reduction overhead), rounds = ceil(tiles / co-resident clusters).
 GemmPlan plan_gemm(int N, int K, int Bt) {
   GemmPlan p;
-  const int bt_cap = std::min(Bt, 256);
-  p.BN = 256;
+  const int bt_cap = std::min(Bt, 128);
+  p.BN = 128;
   for (int bn : kBNs) if (bn >= bt_cap) { p.BN = bn; break; }
   p.b_tiles = (Bt + p.BN - 1) / p.BN;
   p.n_tiles = (N + kBlockM - 1) / kBlockM;
@@ -416,7 +415,8 @@ GemmPlan plan_gemm(int N, int K, int Bt) {
   const int tiles = p.n_tiles * p.b_tiles;
   double best = 1e30;
   for (int C : {1, 2, 4, 8}) {
-    if (C > 1 && (p.BN > 64 || p.BN / C < 4 || C > KB)) continue;
+    if (C == 1 && p.BN > 64) continue;  // the reduction keeps BN/C <= 64 rows per thread
+    if (C > 1 && (p.BN / C < 4 || C > KB)) continue;
     if (cluster_override && C != cluster_override) continue;
     const int ncl = std::min(tiles, max_clusters_bn(p.BN, C));
     const int rounds = (tiles + ncl - 1) / ncl;
@@ -489,7 +489,6 @@ cudaError_t launch_gemm(const Weight& W, const CUtensorMap* tmW, const void* X, 
     case 32: return launch_tc<32>(tmW, tmX, gs, p, ep, st);
     case 64: return launch_tc<64>(tmW, tmX, gs, p, ep, st);
     case 128: return launch_tc<128>(tmW, tmX, gs, p, ep, st);
-    case 256: return launch_tc<256>(tmW, tmX, gs, p, ep, st);
   }
   return cudaErrorInvalidValue;
 }
@@ -536,8 +535,7 @@ cudaError_t launch_attention(int db, int dh, const AttnArgs& a, cudaStream_t st)
 cudaError_t configure_kernels() {
   cudaError_t e = cudaSuccess;
   auto chk = [&](cudaError_t r) { if (e == cudaSuccess) e = r; };
-  chk(configure_tc<16>()); chk(configure_tc<32>()); chk(configure_tc<64>());
-  chk(configure_tc<128>()); chk(configure_tc<256>());
+  chk(configure_tc<16>()); chk(configure_tc<32>()); chk(configure_tc<64>()); chk(configure_tc<128>());
   chk(configure_attn<bf16_t, 48>()); chk(configure_attn<bf16_t, 64>()); chk(configure_attn<bf16_t, 128>());
   chk(configure_attn<float, 48>()); chk(configure_attn<float, 64>()); chk(configure_attn<float, 128>());
   return e;
