@@ -20,23 +20,28 @@
 
 namespace gh {
 
-template <typename T, int DH>
+template <typename T, int DH, int W = 8>
 struct AttnCfg {
   static constexpr int kVec = 16 / sizeof(T);          // elements per 16-byte chunk
   static constexpr int kChunks = DH / kVec;            // 16-byte chunks per row
   static constexpr int kLpp = (kChunks % 8 == 0) ? 8 : (kChunks % 4 == 0) ? 4 : (kChunks % 2 == 0) ? 2 : 1;
   static constexpr int kCpl = kChunks / kLpp;          // chunks per lane
   static constexpr int kPg = 32 / kLpp;                // positions per warp pass
-  static constexpr int kW = 8;                         // consumer warps
+  static constexpr int kW = W;                         // consumer warps
   static constexpr int kTpos = (kW * kPg > 64) ? kW * kPg : 64;  // positions per stage
   static constexpr int kPasses = kTpos / (kW * kPg);
   static constexpr int kTileBytes = kTpos * DH * (int)sizeof(T);
-  static constexpr int kStages = (196608 / (2 * kTileBytes)) > 6 ? 6 : (196608 / (2 * kTileBytes));
+  // per-stage header (first stage of a unit): q, new k, new v (bulk-copied) + {L, b, h}
+  static constexpr int kHdrBytes = 3 * DH * (int)sizeof(T) + 16;
+  static constexpr int kStageBytes = ((2 * kTileBytes + kHdrBytes + 127) / 128) * 128;
+  static constexpr int kStages = (196608 / kStageBytes) > 6 ? 6 : (196608 / kStageBytes);
   static constexpr int kThreads = 32 * (1 + kW);
   static constexpr int kEl = kCpl * kVec;              // elements per lane
-  static constexpr int kCombOffset = kStages * 2 * kTileBytes;
-  static constexpr int kCombBytes = kW * (DH + 2) * 4;
-  static constexpr int kBarOffset = kCombOffset + ((kCombBytes + 127) / 128) * 128;
+  static constexpr int kNB = 4;                        // combine buffers (units in flight)
+  static constexpr int kCombOffset = kStages * kStageBytes;
+  static constexpr int kCombBytes = kNB * kW * (DH + 2) * 4;
+  static constexpr int kCtlOffset = kCombOffset + ((kCombBytes + 127) / 128) * 128;  // 2*kNB ints
+  static constexpr int kBarOffset = kCtlOffset + 128;
   static constexpr int kSmem = kBarOffset + 2 * kStages * 8 + 16;
   static_assert(kChunks * kVec == DH, "d_head must be a multiple of 16 bytes");
 };
@@ -71,14 +76,16 @@ template <> GH_DEV void pack_f32<bf16_t>(const float* f, const float* g, float s
   o = make_uint4(w[0], w[1], w[2], w[3]);
 }
 
-template <typename T, int DH>
-__global__ void __launch_bounds__(AttnCfg<T, DH>::kThreads, 1)
+template <typename T, int DH, int W>
+__global__ void __launch_bounds__(AttnCfg<T, DH, W>::kThreads, 1)
     attn_decode_kernel(const AttnArgs a) {
-  using C = AttnCfg<T, DH>;
+  using C = AttnCfg<T, DH, W>;
   extern __shared__ __align__(128) uint8_t smem[];
   uint64_t* full = (uint64_t*)(smem + C::kBarOffset);
   uint64_t* empty = full + C::kStages;
   float* comb = (float*)(smem + C::kCombOffset);
+  int* comb_cnt = (int*)(smem + C::kCtlOffset);       // [kNB] warps that published unit i
+  volatile int* comb_seq = comb_cnt + C::kNB;          // [kNB] units combined from this buffer
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -87,6 +94,7 @@ __global__ void __launch_bounds__(AttnCfg<T, DH>::kThreads, 1)
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < C::kStages; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], C::kW); }
+    for (int i = 0; i < C::kNB; ++i) { comb_cnt[i] = 0; comb_seq[i] = 0; }
     fence_barrier_init();
   }
   __syncthreads();
@@ -104,22 +112,43 @@ __global__ void __launch_bounds__(AttnCfg<T, DH>::kThreads, 1)
     if (elect_one()) {
       const uint64_t pol = policy_evict_first();
       uint32_t it = 0;
-      for (int u = blockIdx.x; u < n_units; u += gridDim.x) {
+      int u = blockIdx.x;
+      int L = 0, sl = 0;
+      if (u < n_units) { L = a.pos[u / a.H]; sl = (int)a.slot[u / a.H]; }
+      for (; u < n_units; u += gridDim.x) {
         const int b = u / a.H, h = u % a.H, kvh = h / group;
-        const int L = a.pos[b];
-        const T* kbase = arena + (long)a.slot[b] * a.slot_stride + (long)kvh * a.head_stride;
+        // next unit's position / slot, one unit ahead (hides the dependent global loads)
+        const int un = u + gridDim.x;
+        int Ln = 0, sln = 0;
+        if (un < n_units) { Ln = a.pos[un / a.H]; sln = (int)a.slot[un / a.H]; }
+        const T* kbase = arena + (long)sl * a.slot_stride + (long)kvh * a.head_stride;
         const T* vbase = kbase + a.kv_stride;
-        for (int p0 = 0; p0 < L; p0 += C::kTpos, ++it) {
+        const int nch = L > 0 ? (L + C::kTpos - 1) / C::kTpos : 1;
+        for (int c = 0; c < nch; ++c, ++it) {
           const int s = it % C::kStages;
-          const uint32_t ph = (it / C::kStages) & 1;
-          mbar_wait(&empty[s], ph ^ 1);
-          const int np = min(C::kTpos, L - p0);
+          mbar_wait(&empty[s], ((it / C::kStages) & 1) ^ 1);
+          const int np = max(0, min(C::kTpos, L - c * C::kTpos));
           const uint32_t bytes = (uint32_t)np * DH * sizeof(T);
-          uint8_t* sk = smem + s * 2 * C::kTileBytes;
-          mbar_arrive_expect_tx(&full[s], 2 * bytes);
-          bulk_g2s(sk, kbase + (long)p0 * DH, bytes, &full[s], pol);
-          bulk_g2s(sk + C::kTileBytes, vbase + (long)p0 * DH, bytes, &full[s], pol);
+          uint8_t* sk = smem + s * C::kStageBytes;
+          uint8_t* hdr = sk + 2 * C::kTileBytes;
+          if (c == 0) {  // unit header: metadata (plain store, released by the arrive) + q/k/v copies
+            int* meta = (int*)(hdr + 3 * DH * sizeof(T));
+            meta[0] = L; meta[1] = b; meta[2] = h;
+          }
+          mbar_arrive_expect_tx(&full[s], 2 * bytes + (c == 0 ? 3 * DH * (uint32_t)sizeof(T) : 0u));
+          if (np > 0) {
+            bulk_g2s(sk, kbase + (long)c * C::kTpos * DH, bytes, &full[s], pol);
+            bulk_g2s(sk + C::kTileBytes, vbase + (long)c * C::kTpos * DH, bytes, &full[s], pol);
+          }
+          if (c == 0) {
+            const T* row = fwd + (long)b * ld_fwd;
+            bulk_g2s(hdr, row + a.D + (long)h * DH, DH * sizeof(T), &full[s], pol);
+            bulk_g2s(hdr + DH * sizeof(T), row + 2L * a.D + (long)kvh * DH, DH * sizeof(T), &full[s], pol);
+            bulk_g2s(hdr + 2 * DH * sizeof(T), row + 2L * a.D + a.Dkv + (long)kvh * DH, DH * sizeof(T), &full[s], pol);
+          }
         }
+        L = Ln;
+        sl = sln;
       }
     }
     return;
@@ -131,15 +160,23 @@ __global__ void __launch_bounds__(AttnCfg<T, DH>::kThreads, 1)
   const int sub = lane % C::kLpp;
   uint32_t it = 0;
 
-  for (int u = blockIdx.x; u < n_units; u += gridDim.x) {
-    const int b = u / a.H, h = u % a.H, kvh = h / group;
-    const int L = a.pos[b];
-    const T* qrow = fwd + (long)b * ld_fwd + a.D + (long)h * DH;
+  int ui = 0;
+  for (int u = blockIdx.x; u < n_units; u += gridDim.x, ++ui) {
+    // unit header (first stage of the unit)
+    const int s0 = it % C::kStages;
+    mbar_wait(&full[s0], (it / C::kStages) & 1);
+    const uint8_t* hdr = smem + s0 * C::kStageBytes + 2 * C::kTileBytes;
+    const T* hq = (const T*)hdr;
+    const T* hk = hq + DH;
+    const T* hv = hk + DH;
+    const int* meta = (const int*)(hdr + 3 * DH * sizeof(T));
+    const int L = meta[0], b = meta[1], h = meta[2], kvh = h / group;
+    const int nch = L > 0 ? (L + C::kTpos - 1) / C::kTpos : 1;
 
     float q[C::kEl], o[C::kEl];
 #pragma unroll
     for (int j = 0; j < C::kCpl; ++j) {
-      uint4 c = *(const uint4*)(qrow + (sub + j * C::kLpp) * C::kVec);
+      uint4 c = *(const uint4*)(hq + (sub + j * C::kLpp) * C::kVec);
       chunk_to_f32<T>(c, q + j * C::kVec);
     }
 #pragma unroll
@@ -148,9 +185,7 @@ __global__ void __launch_bounds__(AttnCfg<T, DH>::kThreads, 1)
     float l = 0.f;        // per-group partial sum
 
     if (cw == 0) {
-      // new token: score from the message, append k/v to the arena (group 0 lanes)
-      const T* krow = fwd + (long)b * ld_fwd + 2L * a.D + (long)kvh * DH;
-      const T* vrow = krow + a.Dkv;
+      // new token: score from the header, append k/v to the arena (group 0 lanes)
       T* kdst = arena + (long)a.slot[b] * a.slot_stride + (long)kvh * a.head_stride + (long)L * DH;
       T* vdst = kdst + a.kv_stride;
       float part = 0.f;
@@ -158,8 +193,8 @@ __global__ void __launch_bounds__(AttnCfg<T, DH>::kThreads, 1)
 #pragma unroll
       for (int j = 0; j < C::kCpl; ++j) {
         const int off = (sub + j * C::kLpp) * C::kVec;
-        uint4 kc = *(const uint4*)(krow + off);
-        uint4 vc = *(const uint4*)(vrow + off);
+        uint4 kc = *(const uint4*)(hk + off);
+        uint4 vc = *(const uint4*)(hv + off);
         if (grp == 0 && (h % group) == 0) {  // one writer per kv head
           *(uint4*)(kdst + off) = kc;
           *(uint4*)(vdst + off) = vc;
@@ -180,13 +215,17 @@ __global__ void __launch_bounds__(AttnCfg<T, DH>::kThreads, 1)
       }
     }
 
-    for (int p0 = 0; p0 < L; p0 += C::kTpos, ++it) {
+    for (int c = 0; c < nch; ++c, ++it) {
       const int s = it % C::kStages;
-      const uint32_t ph = (it / C::kStages) & 1;
-      const int np = min(C::kTpos, L - p0);
-      mbar_wait(&full[s], ph);
-      const T* sk = (const T*)(smem + s * 2 * C::kTileBytes);
-      const T* sv = (const T*)(smem + s * 2 * C::kTileBytes + C::kTileBytes);
+      const int np = max(0, min(C::kTpos, L - c * C::kTpos));
+      if (c > 0) mbar_wait(&full[s], (it / C::kStages) & 1);
+      if (a.flags & 1) {  // diagnostics: streaming only
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[s]);
+        continue;
+      }
+      const T* sk = (const T*)(smem + s * C::kStageBytes);
+      const T* sv = (const T*)(smem + s * C::kStageBytes + C::kTileBytes);
 
       float sc[C::kPasses];
       float mx = -INFINITY;
@@ -195,14 +234,18 @@ __global__ void __launch_bounds__(AttnCfg<T, DH>::kThreads, 1)
         const int r = ps * C::kW * C::kPg + cw * C::kPg + grp;
         float part = 0.f;
         if (r < np) {
+          uint4 kc[C::kCpl];
+#pragma unroll
+          for (int j = 0; j < C::kCpl; ++j) kc[j] = *(const uint4*)(sk + r * DH + (sub + j * C::kLpp) * C::kVec);
+          float pp[4] = {0.f, 0.f, 0.f, 0.f};  // four independent FMA chains
 #pragma unroll
           for (int j = 0; j < C::kCpl; ++j) {
-            uint4 kc = *(const uint4*)(sk + r * DH + (sub + j * C::kLpp) * C::kVec);
             float kf[C::kVec];
-            chunk_to_f32<T>(kc, kf);
+            chunk_to_f32<T>(kc[j], kf);
 #pragma unroll
-            for (int e = 0; e < C::kVec; ++e) part = fmaf(q[j * C::kVec + e], kf[e], part);
+            for (int e = 0; e < C::kVec; ++e) pp[e & 3] = fmaf(q[j * C::kVec + e], kf[e], pp[e & 3]);
           }
+          part = (pp[0] + pp[1]) + (pp[2] + pp[3]);
         }
 #pragma unroll
         for (int o2 = C::kLpp / 2; o2 > 0; o2 >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o2);
@@ -238,6 +281,7 @@ __global__ void __launch_bounds__(AttnCfg<T, DH>::kThreads, 1)
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[s]);
     }
+    if (a.flags & 1) continue;
 
     // merge the groups of this warp (m is warp-uniform)
 #pragma unroll
@@ -246,7 +290,12 @@ __global__ void __launch_bounds__(AttnCfg<T, DH>::kThreads, 1)
 #pragma unroll
       for (int e = 0; e < C::kEl; ++e) o[e] += __shfl_xor_sync(0xffffffffu, o[e], o2);
     }
-    float* cwbuf = comb + cw * (DH + 2);
+    // publish this warp's state to combine buffer ui % kNB; the last warp to publish merges the
+    // kW states and writes the output (no CTA barrier: the other warps move on to the next unit)
+    const int cb = ui % C::kNB;
+    while (comb_seq[cb] != ui / C::kNB) { }  // the merge of unit ui - kNB has left this buffer
+    float* cbuf = comb + cb * C::kW * (DH + 2);
+    float* cwbuf = cbuf + cw * (DH + 2);
     if (grp == 0) {
 #pragma unroll
       for (int j = 0; j < C::kCpl; ++j)
@@ -254,35 +303,46 @@ __global__ void __launch_bounds__(AttnCfg<T, DH>::kThreads, 1)
         for (int e = 0; e < C::kVec; ++e) cwbuf[(sub + j * C::kLpp) * C::kVec + e] = o[j * C::kVec + e];
     }
     if (lane == 0) { cwbuf[DH] = m; cwbuf[DH + 1] = l; }
-    asm volatile("bar.sync 1, %0;\n" ::"r"(C::kW * 32) : "memory");
-    {
-      const int t = threadIdx.x - 32;
+    __syncwarp();
+    int last = 0;
+    if (lane == 0) {
+      __threadfence_block();
+      last = atomicAdd(&comb_cnt[cb], 1) == C::kW - 1;
+    }
+    last = __shfl_sync(0xffffffffu, last, 0);
+    if (last) {
+      __threadfence_block();
       float M = -INFINITY;
 #pragma unroll
-      for (int w = 0; w < C::kW; ++w) M = fmaxf(M, comb[w * (DH + 2) + DH]);
+      for (int w = 0; w < C::kW; ++w) M = fmaxf(M, cbuf[w * (DH + 2) + DH]);
       float den = 0.f;
       float f[C::kW];
 #pragma unroll
       for (int w = 0; w < C::kW; ++w) {
-        const float mw = comb[w * (DH + 2) + DH];
+        const float mw = cbuf[w * (DH + 2) + DH];
         f[w] = (mw == -INFINITY) ? 0.f : exp2f(mw - M);
-        den += comb[w * (DH + 2) + DH + 1] * f[w];
+        den += cbuf[w * (DH + 2) + DH + 1] * f[w];
       }
       const float inv = 1.f / den;
       T* orow = bwd + (long)b * ld_bwd + a.D + (long)h * DH;
-      for (int d = t; d < DH; d += C::kW * 32) {
+      for (int d = lane; d < DH; d += 32) {
         float acc = 0.f;
 #pragma unroll
-        for (int w = 0; w < C::kW; ++w) acc += comb[w * (DH + 2) + d] * f[w];
+        for (int w = 0; w < C::kW; ++w) acc += cbuf[w * (DH + 2) + d] * f[w];
         St<T>::store(orow, d, acc * inv);
       }
       if (h == 0) {  // pass the residual stream through: bwd.x = fwd.x
         const uint4* xs = (const uint4*)(fwd + (long)b * ld_fwd);
         uint4* xd = (uint4*)(bwd + (long)b * ld_bwd);
-        for (int i = t; i < a.D / C::kVec; i += C::kW * 32) xd[i] = xs[i];
+        for (int i = lane; i < a.D / C::kVec; i += 32) xd[i] = xs[i];
+      }
+      __syncwarp();
+      if (lane == 0) {
+        comb_cnt[cb] = 0;
+        __threadfence_block();
+        comb_seq[cb] = ui / C::kNB + 1;
       }
     }
-    asm volatile("bar.sync 1, %0;\n" ::"r"(C::kW * 32) : "memory");
   }
 }
 

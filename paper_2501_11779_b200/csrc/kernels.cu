@@ -494,21 +494,34 @@ cudaError_t launch_gemm(const Weight& W, const CUtensorMap* tmW, const void* X, 
 }
 
 // ====================================================================== attention dispatch
-template <typename T, int DH>
-static cudaError_t configure_attn() {
-  cudaError_t e = cudaFuncSetAttribute(attn_decode_kernel<T, DH>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       AttnCfg<T, DH>::kSmem);
+template <typename T, int DH, int W>
+static cudaError_t configure_attn_w() {
+  cudaError_t e = cudaFuncSetAttribute(attn_decode_kernel<T, DH, W>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       AttnCfg<T, DH, W>::kSmem);
   if (e != cudaSuccess) return e;
-  return cudaFuncSetAttribute(attn_decode_kernel<T, DH>, cudaFuncAttributePreferredSharedMemoryCarveout,
+  return cudaFuncSetAttribute(attn_decode_kernel<T, DH, W>, cudaFuncAttributePreferredSharedMemoryCarveout,
                               (int)cudaSharedmemCarveoutMaxShared);
 }
 template <typename T, int DH>
-static cudaError_t launch_attn_t(const AttnArgs& a, cudaStream_t st) {
-  using C = AttnCfg<T, DH>;
+static cudaError_t configure_attn() {
+  cudaError_t e = configure_attn_w<T, DH, 8>();
+  return e != cudaSuccess ? e : configure_attn_w<T, DH, 16>();
+}
+static int attn_warps() {  // consumer warps per CTA (diagnostics override GH_ATTN_WARPS)
+  static const int w = getenv("GH_ATTN_WARPS") ? atoi(getenv("GH_ATTN_WARPS")) : 8;
+  return w;
+}
+template <typename T, int DH, int W>
+static cudaError_t launch_attn_w(const AttnArgs& a, cudaStream_t st) {
+  using C = AttnCfg<T, DH, W>;
   const int units = a.B * a.H;
   if (units <= 0) return cudaSuccess;
   const int grid = std::min(units, kNumSMs);
-  return launch_pdl(attn_decode_kernel<T, DH>, grid, C::kThreads, C::kSmem, st, a);
+  return launch_pdl(attn_decode_kernel<T, DH, W>, grid, C::kThreads, C::kSmem, st, a);
+}
+template <typename T, int DH>
+static cudaError_t launch_attn_t(const AttnArgs& a, cudaStream_t st) {
+  return attn_warps() == 16 ? launch_attn_w<T, DH, 16>(a, st) : launch_attn_w<T, DH, 8>(a, st);
 }
 
 bool attention_supported(int db, int dh) {

@@ -49,6 +49,7 @@ struct AttnArgs {
   long head_stride;     // elements per kv head (= S * DH)
   int B, H, Hkv, D, Dkv;
   float scale_log2;     // log2(e) / sqrt(DH)
+  int flags;            // diagnostics: 1 = consumers release stages without computing
 };
 
 }  // namespace gh

@@ -13,6 +13,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <memory>
@@ -443,6 +444,8 @@ gh_status gh_tier2_attend(gh_tier2* t, uint32_t layer, uint32_t B, const uint32_
   a.head_stride = (long)s.S * s.dh;
   a.B = (int)B; a.H = s.H; a.Hkv = s.Hkv; a.D = s.D; a.Dkv = s.Dkv;
   a.scale_log2 = (float)(1.4426950408889634 / std::sqrt((double)s.dh));
+  static const int attn_flags = getenv("GH_ATTN_FLAGS") ? atoi(getenv("GH_ATTN_FLAGS")) : 0;  // diagnostics
+  a.flags = attn_flags;
   GH_CUDA(launch_attention(s.db, s.dh, a, (cudaStream_t)stream));
   return GH_OK;
 }

@@ -40,7 +40,7 @@ class Tier1:
         self.h = h
 
     def close(self):
-        if getattr(self, "h", None):
+        if getattr(self, "h", None) and L is not None and L.lib is not None:
             L.lib().gh_tier1_destroy(self.h)
             self.h = None
 
@@ -78,7 +78,7 @@ class Tier2:
         self.h = h
 
     def close(self):
-        if getattr(self, "h", None):
+        if getattr(self, "h", None) and L is not None and L.lib is not None:
             L.lib().gh_tier2_destroy(self.h)
             self.h = None
 
@@ -163,7 +163,7 @@ class Engine:
         self._pinned = {}
 
     def close(self):
-        if getattr(self, "h", None):
+        if getattr(self, "h", None) and L is not None and L.lib is not None:
             L.lib().gh_engine_destroy(self.h)
             self.h = None
 

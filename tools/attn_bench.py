@@ -1,0 +1,33 @@
+"""Time the Tier-2 attention kernel alone (CUDA events, KV >> L2) at a batch / context."""
+import sys
+from pathlib import Path
+
+import torch
+
+sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
+import paper_2501_11779_b200 as gh  # noqa: E402
+from paper_2501_11779_b200.stages import Tier2, message_buffers  # noqa: E402
+
+B = int(sys.argv[1]) if len(sys.argv) > 1 else 64
+ctx = int(sys.argv[2]) if len(sys.argv) > 2 else 512
+layers = 4  # rotate layers so the KV of one launch is never L2-resident from the previous
+spec = gh.LLAMA2_7B.with_(n_layers=layers, max_seq_len=ctx)
+t2 = Tier2(spec, n_slots=B)
+t2.fill_synthetic(99, B, ctx - 1)
+x, fwd, bwd = message_buffers(spec, B)
+fwd.normal_()
+pos = torch.full((B,), ctx - 1, dtype=torch.int32, device="cuda")
+slot = torch.arange(B, dtype=torch.int32, device="cuda")
+for i in range(8):
+    t2.attend(i % layers, slot, pos, fwd, bwd)
+e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+reps = 40
+e0.record()
+for i in range(reps):
+    t2.attend(i % layers, slot, pos, fwd, bwd)
+e1.record()
+torch.cuda.synchronize()
+us = e0.elapsed_time(e1) * 1e3 / reps
+byts = 2 * (2 * spec.d_kv * B * ctx + 2 * B * spec.d_kv + 2 * B * spec.d_model)
+print(f"B={B} ctx={ctx}: {us:.1f} us  {byts / us / 1e3:.0f} GB/s")
+t2.close()
