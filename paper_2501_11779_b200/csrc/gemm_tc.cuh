@@ -92,10 +92,45 @@ GH_DEV void store_run_bf16(uint16_t* dst, const float* v) {
   }
 }
 
+constexpr int kMaxInvCols = 256;  // batch columns whose fused-RMSNorm scale is kept in smem (larger: unfused)
+
+// 1/rms of every batch column of the GEMM input, from the producer's per-slice sums of squares
+// (summed in slice order: deterministic).  Run once per CTA by the epilogue warps.
+GH_DEV void compute_inv_rms(const EpiParams& ep, const GemmShape& gs, float* inv) {
+  for (int b = threadIdx.x - 64; b < gs.Bt; b += 128) {
+    float ss = 0.f;
+    for (int s = 0; s < ep.ss_in_slices; ++s) ss += __ldg(ep.ss_in + (long)s * gs.Bt + b);
+    inv[b] = 1.0f / sqrtf(ss / (float)ep.ss_dim + ep.ss_eps);
+  }
+}
+
 template <int BN, int En>
-GH_DEV void epi_slice(const EpiParams& ep, const GemmShape& gs, int n, int b, float (&v)[En], int slice) {
+GH_DEV void epi_slice(const EpiParams& ep, const GemmShape& gs, int n, int b, float (&v)[En], int slice,
+                      const float* inv) {
   const bool col_ok = b < gs.Bt;
   const bool full = n + En <= gs.N;
+  if (ep.ss_in && col_ok) {  // fused RMSNorm of the GEMM input
+    const float sc = inv[b];
+#pragma unroll
+    for (int e = 0; e < En; ++e) v[e] *= sc;
+  }
+  if (ep.ss_out) {  // sums of squares of the rounded outputs, reduced over the slice's threads
+    constexpr int kRuns = 128 / BN;
+    float sq = 0.f;
+    if (col_ok && ep.kind == EPI_STORE_RESID) {
+      const uint16_t* rp = (const uint16_t*)ep.resid + (long)b * ep.ldr + n;
+#pragma unroll
+      for (int e = 0; e < En; ++e) {
+        if (full || n + e < gs.N) {
+          const float y = bf16_to_f32(f32_to_bf16(v[e] + bf16_to_f32(rp[e])));
+          sq = fmaf(y, y, sq);
+        }
+      }
+    }
+#pragma unroll
+    for (int o = 1; o < kRuns; o <<= 1) sq += __shfl_xor_sync(0xffffffffu, sq, o);
+    if (col_ok && ((threadIdx.x - 64) % kRuns) == 0) ep.ss_out[(long)slice * gs.Bt + b] = sq;
+  }
   switch (ep.kind) {
     case EPI_STORE:
     case EPI_STORE_RESID: {
@@ -128,6 +163,16 @@ GH_DEV void epi_slice(const EpiParams& ep, const GemmShape& gs, int n, int b, fl
     }
     case EPI_QKV_ROPE: {
       if (!col_ok) return;
+      if (ep.xcopy_src && n < ep.xcopy_rows) {  // x into the message's x slot (fused RMSNorm path)
+        const uint16_t* xs = (const uint16_t*)ep.xcopy_src + (long)b * ep.xcopy_ld + n;
+        uint16_t* xd = (uint16_t*)ep.out + (long)b * ep.ldo + n - ep.xcopy_rows;
+        if (En % 8 == 0 && n + En <= ep.xcopy_rows && ((uintptr_t)xs & 15) == 0 && ((uintptr_t)xd & 15) == 0) {
+#pragma unroll
+          for (int e = 0; e < En; e += 8) *(uint4*)(xd + e) = __ldg((const uint4*)(xs + e));
+        } else {
+          for (int e = 0; e < En && n + e < ep.xcopy_rows; ++e) xd[e] = xs[e];
+        }
+      }
       if (n < ep.rope_rows) {
         const float2* cs = ep.rope + (long)ep.pos[b] * (ep.d_head >> 1) + ((n % ep.d_head) >> 1);
 #pragma unroll
@@ -193,7 +238,7 @@ struct GemmSmem {
   static constexpr uint32_t kAccCols = BN < 32 ? 32 : BN;  // one accumulator buffer
   static constexpr uint32_t kTmemCols = 2 * kAccCols <= 64 ? 64 : 2 * kAccCols <= 128 ? 128
                                       : 2 * kAccCols <= 256 ? 256 : 512;
-  static constexpr int kBarBytes = (2 * kMaxStages + 8) * 8 + 16;
+  static constexpr int kBarBytes = (2 * kMaxStages + 8) * 8 + 16 + kMaxInvCols * 4;
   GH_HD static int epi_offset(int stages) { return stages * kStageBytes; }
   GH_HD static int bar_offset(int stages) { return stages * kStageBytes + kEpiBytes; }
   GH_HD static int bytes(int stages) { return bar_offset(stages) + kBarBytes + 1024; }
@@ -227,7 +272,8 @@ GH_DEV void push_partial(uint32_t recv_saddr, int rank, int row, const float* v1
 
 template <int BN, int C>
 GH_DEV void reduce_and_store(const EpiParams& ep, const GemmShape& gs, const float* recv, int r, int n0,
-                             int b0, int tile_n, uint32_t consumed_saddr, unsigned long long* tr) {
+                             int b0, int tile_n, uint32_t consumed_saddr, unsigned long long* tr,
+                             const float* inv) {
   // thread -> (column b, run of En rows inside this CTA's slice of R = 128/C rows)
   constexpr int R = 128 / C;
   constexpr int En = BN / C;
@@ -251,7 +297,7 @@ GH_DEV void reduce_and_store(const EpiParams& ep, const GemmShape& gs, const flo
   epi_bar();
   if (threadIdx.x == 64)
     for (int p = 0; p < C; ++p) mbar_arrive_cluster_relaxed(mapa_shared(consumed_saddr, p));
-  epi_slice<BN, En>(ep, gs, n0 + r * R + rl, b0 + b, v, tile_n * C + r);
+  epi_slice<BN, En>(ep, gs, n0 + r * R + rl, b0 + b, v, tile_n * C + r, inv);
 }
 
 template <int BN>
@@ -270,6 +316,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   uint64_t* ready = tempty + 2;              // all C partials of the tile published (count C)
   uint64_t* consumed = ready + 1;            // all C peers finished reading my partial (count C)
   uint32_t* tmem_slot = (uint32_t*)(consumed + 1);
+  float* inv_smem = (float*)(consumed + 4);  // [kMaxInvCols] fused-RMSNorm scales
 
   const int warp = threadIdx.x >> 5;
   const int KB = gs.kb_total;
@@ -388,6 +435,10 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     const int row = q * 32 + (threadIdx.x & 31);
     const bool skip = gs.flags & GEMM_DBG_NO_EPI;
     griddep_wait();          // residual / positions belong to earlier kernels
+    if (ep.ss_in) {          // overlaps the mainloop: the epilogue warps are idle until tile 0
+      compute_inv_rms(ep, gs, inv_smem);
+      epi_bar();
+    }
     const uint32_t red_saddr = smem_u32(esm);
     float* red = (float*)esm;
     for (int j = 0; j < my_tiles; ++j) {
@@ -435,12 +486,12 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         if (!skip) {
           switch (C) {
             case 1:
-              if constexpr (BN <= 64) reduce_and_store<BN, 1>(ep, gs, red, rank, n0, b0, tile_n, smem_u32(consumed), rt);
+              if constexpr (BN <= 64) reduce_and_store<BN, 1>(ep, gs, red, rank, n0, b0, tile_n, smem_u32(consumed), rt, inv_smem);
               break;
-            case 2: reduce_and_store<BN, 2>(ep, gs, red, rank, n0, b0, tile_n, smem_u32(consumed), rt); break;
-            case 4: reduce_and_store<BN, 4>(ep, gs, red, rank, n0, b0, tile_n, smem_u32(consumed), rt); break;
+            case 2: reduce_and_store<BN, 2>(ep, gs, red, rank, n0, b0, tile_n, smem_u32(consumed), rt, inv_smem); break;
+            case 4: reduce_and_store<BN, 4>(ep, gs, red, rank, n0, b0, tile_n, smem_u32(consumed), rt, inv_smem); break;
             case 8:
-              if constexpr (BN >= 32) reduce_and_store<BN, 8>(ep, gs, red, rank, n0, b0, tile_n, smem_u32(consumed), rt);
+              if constexpr (BN >= 32) reduce_and_store<BN, 8>(ep, gs, red, rank, n0, b0, tile_n, smem_u32(consumed), rt, inv_smem);
               break;
           }
         }

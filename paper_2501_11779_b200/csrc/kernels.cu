@@ -219,7 +219,9 @@ cudaError_t launch_rmsnorm(int db, const void* x, long ldx, const void* w, void*
                     (bf16_t*)y, ldy, (bf16_t*)copy_out, ldc, D, eps);
 }
 
-__global__ void embed_kernel(const uint4* table, const int32_t* tok, uint4* x, int row_vecs, int V) {
+// x[b] = E[tok[b]]; optionally ss[b] = sum of squares of the row (fused RMSNorm of layer 0)
+template <typename T>
+__global__ void embed_kernel(const uint4* table, const int32_t* tok, uint4* x, int row_vecs, int V, float* ss) {
   const int b = blockIdx.x;
   griddep_launch_dependents();
   griddep_wait();
@@ -227,13 +229,30 @@ __global__ void embed_kernel(const uint4* table, const int32_t* tok, uint4* x, i
   t = t < 0 ? 0 : (t >= V ? V - 1 : t);
   const uint4* src = table + (long)t * row_vecs;
   uint4* dst = x + (long)b * row_vecs;
-  for (int i = threadIdx.x; i < row_vecs; i += blockDim.x) dst[i] = src[i];
+  float sq = 0.f;
+  for (int i = threadIdx.x; i < row_vecs; i += blockDim.x) {
+    const uint4 c = src[i];
+    dst[i] = c;
+    float f[16 / sizeof(T)];
+    chunk_to_f32<T>(c, f);
+#pragma unroll
+    for (int e = 0; e < (int)(16 / sizeof(T)); ++e) sq = fmaf(f[e], f[e], sq);
+  }
+  if (ss) {
+    __shared__ float red[4];
+    sq = warp_sum(sq);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = sq;
+    __syncthreads();
+    if (threadIdx.x == 0) ss[b] = (red[0] + red[1]) + (red[2] + red[3]);
+  }
 }
 
-cudaError_t launch_embed(int db, const void* table, const int32_t* tok, void* x, int B, int D,
-                         int V, cudaStream_t st) {
+cudaError_t launch_embed(int db, const void* table, const int32_t* tok, void* x, int B, int D, int V, float* ss,
+                         cudaStream_t st) {
   if (B <= 0) return cudaSuccess;
-  return launch_pdl(embed_kernel, B, 128, 0, st, (const uint4*)table, tok, (uint4*)x, D * db / 16, V);
+  if (db == 4)
+    return launch_pdl(embed_kernel<float>, B, 128, 0, st, (const uint4*)table, tok, (uint4*)x, D * db / 16, V, ss);
+  return launch_pdl(embed_kernel<bf16_t>, B, 128, 0, st, (const uint4*)table, tok, (uint4*)x, D * db / 16, V, ss);
 }
 
 // ====================================================================== argmax

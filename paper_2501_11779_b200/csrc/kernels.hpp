@@ -70,7 +70,7 @@ cudaError_t launch_rmsnorm(int dtype_bytes, const void* x, long ldx, const void*
                            long ldy, void* copy_out, long ldc, int B, int D, float eps,
                            cudaStream_t st);
 cudaError_t launch_embed(int dtype_bytes, const void* table, const int32_t* tok, void* x, int B,
-                         int D, int V, cudaStream_t st);
+                         int D, int V, float* ss, cudaStream_t st);
 cudaError_t launch_argmax_final(const float2* part, int n_tiles, int B, int32_t* next_tok,
                                 cudaStream_t st);
 cudaError_t launch_argmax_rows(const float* logits, int B, int V, int32_t* next_tok,

@@ -26,6 +26,20 @@ struct EpiParams {
   float* logits;        // [B][ldl] fp32 (optional)
   long ldl;
   float2* part;         // [n_tiles * C][Bt] (max value, argmax index as float bits); C = cluster size
+  // fused RMSNorm (bf16 tcgen05 path): the GEMM input X is the raw activation; column b of the
+  // accumulator is scaled by 1/sqrt(sum_s ss_in[s][b] / ss_dim + ss_eps) (norm weight folded
+  // into W).  ss_in holds per-slice sums of squares written by the producer of X.
+  const float* ss_in;   // [ss_in_slices][Bt] or nullptr
+  int ss_in_slices;
+  int ss_dim;
+  float ss_eps;
+  // per-slice sums of squares of the rounded outputs of this GEMM (STORE_RESID) for the next
+  // fused norm: ss_out[n_tile * C + r][Bt]; nullptr = none
+  float* ss_out;
+  // QKV_ROPE: copy x[b][n] (row stride xcopy_ld) into the fwd message x slot for n < xcopy_rows
+  const void* xcopy_src;
+  long xcopy_ld;
+  int xcopy_rows;
 };
 
 struct GemmShape {

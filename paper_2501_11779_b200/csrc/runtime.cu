@@ -24,6 +24,7 @@
 
 #include "params.hpp"
 #include "common.cuh"
+#include "gemm_tc.cuh"
 #include "gh/gh.h"
 #include "internal.hpp"
 #include "kernels.hpp"
@@ -115,6 +116,7 @@ struct gh_tier1 {
   void* final_norm = nullptr;
   float2* rope = nullptr;
   void *xn = nullptr, *h = nullptr, *hn = nullptr, *g = nullptr;
+  float* ss_h = nullptr;  // per-slice sums of squares of h (fused FFN RMSNorm)
   float2* part = nullptr;
   GemmScratch gsc;
   TmapCache tmaps;
@@ -264,6 +266,11 @@ gh_status gh_tier1_create(const gh_model_spec* spec, int device, uint32_t layer_
   GH_TRY(dev_alloc(t->mem, B * Dh * db, &t->g));
   {
     void* p;
+    GH_TRY(dev_alloc(t->mem, (size_t)(D + 127) / 128 * 8 * B * sizeof(float), &p));  // tiles x max C
+    t->ss_h = (float*)p;
+  }
+  {
+    void* p;
     const size_t n_slices = (size_t)(V + 127) / 128 * 8;  // tiles x max cluster size
     GH_TRY(dev_alloc(t->mem, n_slices * B * sizeof(float2), &p));
     t->part = (float2*)p;
@@ -285,26 +292,36 @@ gh_status gh_tier1_destroy(gh_tier1* t) {
   return GH_OK;
 }
 
-gh_status gh_tier1_embed(gh_tier1* t, uint32_t B, const int32_t* tok, void* x, void* stream) {
+}  // extern "C"
+
+// ---- Tier-1 stage implementations.  `SsRef` describes per-slice sums of squares of an
+// activation buffer emitted by its producer (embedding / W2 epilogue) so that the consumer GEMM
+// applies RMSNorm in its epilogue (bf16 path) instead of a separate normalisation kernel.  The
+// public ABI entry points pass none (they normalise explicitly and are correct for any input);
+// the engine, which owns the activation buffers, threads the sums of squares through.
+namespace gh {
+struct SsRef {
+  const float* ss = nullptr;
+  int slices = 0;
+};
+}  // namespace gh
+
+static gh_status t1_embed(gh_tier1* t, uint32_t B, const int32_t* tok, void* x, float* ss_out, cudaStream_t st) {
   if (!t || !tok || !x) return fail(GH_EINVAL, "null argument");
   if (!t->has_embed) return fail(GH_EINVAL, "this Tier-1 span does not own the embedding");
   if (B > t->max_batch) return fail(GH_EINVAL, "B exceeds max_batch");
-  GH_CUDA(launch_embed(t->sh.db, t->embed.ptr, tok, x, (int)B, t->sh.D, t->sh.V, (cudaStream_t)stream));
+  GH_CUDA(launch_embed(t->sh.db, t->embed.ptr, tok, x, (int)B, t->sh.D, t->sh.V, t->sh.db == 2 ? ss_out : nullptr, st));
   return GH_OK;
 }
 
-gh_status gh_tier1_pre(gh_tier1* t, uint32_t layer, uint32_t B, const void* x, const int32_t* pos,
-                       void* msg_fwd, void* stream) {
+static gh_status t1_pre(gh_tier1* t, uint32_t layer, uint32_t B, const void* x, SsRef ss, const int32_t* pos,
+                        void* msg_fwd, cudaStream_t st) {
   if (!t || !x || !pos || !msg_fwd) return fail(GH_EINVAL, "null argument");
   if (layer < t->l0 || layer >= t->l1) return fail(GH_EINVAL, "layer not owned by this Tier-1");
   if (B > t->max_batch) return fail(GH_EINVAL, "B exceeds max_batch");
   if (B == 0) return GH_OK;
-  cudaStream_t st = (cudaStream_t)stream;
   const Shape& s = t->sh;
   auto& L = t->layers[layer - t->l0];
-  // RMSNorm(x) -> xn ; x copied into the message's x slot
-  GH_CUDA(launch_rmsnorm(s.db, x, s.D, L.attn_norm, t->xn, s.D, msg_fwd, s.ld_fwd(), (int)B, s.D,
-                         s.s.norm_eps, st));
   EpiParams ep = epi_default();
   ep.kind = EPI_QKV_ROPE;
   ep.out = (char*)msg_fwd + (size_t)s.D * s.db;
@@ -313,59 +330,102 @@ gh_status gh_tier1_pre(gh_tier1* t, uint32_t layer, uint32_t B, const void* x, c
   ep.pos = pos;
   ep.d_head = s.dh;
   ep.rope_rows = s.D + s.Dkv;
+  if (s.db == 2 && ss.ss && B <= (uint32_t)kMaxInvCols) {
+    // fused: QKV on the raw x, RMSNorm scale in the epilogue, x copied into the message there
+    ep.ss_in = ss.ss; ep.ss_in_slices = ss.slices; ep.ss_dim = s.D; ep.ss_eps = s.s.norm_eps;
+    ep.xcopy_src = x; ep.xcopy_ld = s.D; ep.xcopy_rows = s.D;
+    return t->gemm(L.qkv, &L.tm_qkv, x, s.D, (int)B, ep, st);
+  }
+  // RMSNorm(x) -> xn ; x copied into the message's x slot
+  GH_CUDA(launch_rmsnorm(s.db, x, s.D, L.attn_norm, t->xn, s.D, msg_fwd, s.ld_fwd(), (int)B, s.D,
+                         s.s.norm_eps, st));
   return t->gemm(L.qkv, &L.tm_qkv, t->xn, s.D, (int)B, ep, st);
 }
 
-gh_status gh_tier1_post(gh_tier1* t, uint32_t layer, uint32_t B, const void* msg_bwd, void* x_next,
-                        void* stream) {
+static gh_status t1_post(gh_tier1* t, uint32_t layer, uint32_t B, const void* msg_bwd, void* x_next, float* ss_next,
+                         int* ss_next_slices, cudaStream_t st) {
   if (!t || !msg_bwd || !x_next) return fail(GH_EINVAL, "null argument");
   if (layer < t->l0 || layer >= t->l1) return fail(GH_EINVAL, "layer not owned by this Tier-1");
   if (B > t->max_batch) return fail(GH_EINVAL, "B exceeds max_batch");
   if (B == 0) return GH_OK;
-  cudaStream_t st = (cudaStream_t)stream;
   const Shape& s = t->sh;
   auto& L = t->layers[layer - t->l0];
-  // h = attn Wo^T + x
+  const bool fused = s.db == 2 && B <= (uint32_t)kMaxInvCols;
+  // h = attn Wo^T + x   (+ per-slice sums of squares of h for the fused FFN norm)
   EpiParams ep = epi_default();
   ep.kind = EPI_STORE_RESID;
   ep.out = t->h; ep.ldo = s.D;
   ep.resid = msg_bwd; ep.ldr = s.ld_bwd();
+  if (fused) ep.ss_out = t->ss_h;
   GH_TRY(t->gemm(L.o, &L.tm_o, (const char*)msg_bwd + (size_t)s.D * s.db, s.ld_bwd(), (int)B, ep, st));
-  // hn = RMSNorm(h)
-  GH_CUDA(launch_rmsnorm(s.db, t->h, s.D, L.ffn_norm, t->hn, s.D, nullptr, 0, (int)B, s.D, s.s.norm_eps, st));
-  // g = silu(hn W1^T) * (hn W3^T)
+  // g = silu(rms(h) W1^T) * (rms(h) W3^T)
+  const void* ffn_in = t->h;
   ep = epi_default();
   ep.kind = EPI_SWIGLU;
   ep.out = t->g; ep.ldo = s.Dh;
-  GH_TRY(t->gemm(L.w13, &L.tm_13, t->hn, s.D, (int)B, ep, st));
-  // x_next = g W2^T + h
+  if (fused) {
+    ep.ss_in = t->ss_h; ep.ss_in_slices = t->plan(s.D, s.D, (int)B).slices(); ep.ss_dim = s.D;
+    ep.ss_eps = s.s.norm_eps;
+  } else {
+    GH_CUDA(launch_rmsnorm(s.db, t->h, s.D, L.ffn_norm, t->hn, s.D, nullptr, 0, (int)B, s.D, s.s.norm_eps, st));
+    ffn_in = t->hn;
+  }
+  GH_TRY(t->gemm(L.w13, &L.tm_13, ffn_in, s.D, (int)B, ep, st));
+  // x_next = g W2^T + h   (+ sums of squares of x_next for the next fused norm)
   ep = epi_default();
   ep.kind = EPI_STORE_RESID;
   ep.out = x_next; ep.ldo = s.D;
   ep.resid = t->h; ep.ldr = s.D;
+  if (fused && ss_next) {
+    ep.ss_out = ss_next;
+    if (ss_next_slices) *ss_next_slices = t->plan(s.D, s.Dh, (int)B).slices();
+  }
   return t->gemm(L.w2, &L.tm_2, t->g, s.Dh, (int)B, ep, st);
 }
 
-gh_status gh_tier1_classify(gh_tier1* t, uint32_t B, const void* x, float* logits, int32_t* next,
-                            void* stream) {
+static gh_status t1_classify(gh_tier1* t, uint32_t B, const void* x, SsRef ss, float* logits, int32_t* next,
+                             cudaStream_t st) {
   if (!t || !x || !next) return fail(GH_EINVAL, "null argument");
   if (!t->has_cls) return fail(GH_EINVAL, "this Tier-1 span does not own the classifier");
   if (B > t->max_batch) return fail(GH_EINVAL, "B exceeds max_batch");
   if (B == 0) return GH_OK;
-  cudaStream_t st = (cudaStream_t)stream;
   const Shape& s = t->sh;
-  GH_CUDA(launch_rmsnorm(s.db, x, s.D, t->final_norm, t->xn, s.D, nullptr, 0, (int)B, s.D, s.s.norm_eps, st));
   EpiParams ep = epi_default();
   ep.kind = EPI_LOGITS_ARGMAX;
   ep.logits = logits; ep.ldl = s.V;
   ep.part = t->part;
-  GH_TRY(t->gemm(t->cls, &t->tm_cls, t->xn, s.D, (int)B, ep, st));
+  const void* in = x;
+  if (s.db == 2 && ss.ss && B <= (uint32_t)kMaxInvCols) {
+    ep.ss_in = ss.ss; ep.ss_in_slices = ss.slices; ep.ss_dim = s.D; ep.ss_eps = s.s.norm_eps;
+  } else {
+    GH_CUDA(launch_rmsnorm(s.db, x, s.D, t->final_norm, t->xn, s.D, nullptr, 0, (int)B, s.D, s.s.norm_eps, st));
+    in = t->xn;
+  }
+  GH_TRY(t->gemm(t->cls, &t->tm_cls, in, s.D, (int)B, ep, st));
   if (s.db == 2) {
     GH_CUDA(launch_argmax_final(t->part, t->plan(s.V, s.D, (int)B).slices(), (int)B, next, st));
   } else {
     GH_CUDA(launch_argmax_rows(logits ? logits : t->gsc.stage, (int)B, s.V, next, st));
   }
   return GH_OK;
+}
+
+extern "C" {
+
+gh_status gh_tier1_embed(gh_tier1* t, uint32_t B, const int32_t* tok, void* x, void* stream) {
+  return t1_embed(t, B, tok, x, nullptr, (cudaStream_t)stream);
+}
+gh_status gh_tier1_pre(gh_tier1* t, uint32_t layer, uint32_t B, const void* x, const int32_t* pos,
+                       void* msg_fwd, void* stream) {
+  return t1_pre(t, layer, B, x, SsRef{}, pos, msg_fwd, (cudaStream_t)stream);
+}
+gh_status gh_tier1_post(gh_tier1* t, uint32_t layer, uint32_t B, const void* msg_bwd, void* x_next,
+                        void* stream) {
+  return t1_post(t, layer, B, msg_bwd, x_next, nullptr, nullptr, (cudaStream_t)stream);
+}
+gh_status gh_tier1_classify(gh_tier1* t, uint32_t B, const void* x, float* logits, int32_t* next,
+                            void* stream) {
+  return t1_classify(t, B, x, SsRef{}, logits, next, (cudaStream_t)stream);
 }
 
 }  // extern "C"
@@ -573,6 +633,11 @@ struct gh_engine {
     int32_t *tok = nullptr, *pos = nullptr, *next = nullptr;
     uint32_t* slot = nullptr;
     void *x0 = nullptr, *x1 = nullptr, *fwd = nullptr, *bwd = nullptr;
+    float *ss0 = nullptr, *ss1 = nullptr;  // per-slice sums of squares of x0 / x1 (fused RMSNorm)
+    int ss_slices[2] = {0, 0};
+    int cur = 0;                           // which of x0 / x1 holds the current activation
+    void* x(int i) const { return i ? x1 : x0; }
+    float* ss(int i) const { return i ? ss1 : ss0; }
     float* logits = nullptr;
     cudaStream_t stream = nullptr;
     cudaEvent_t done = nullptr;
@@ -595,20 +660,36 @@ struct gh_engine {
   int rows() const { return role == 2 ? my_cnt : (int)cfg.batch; }
 };
 
+// Tier-1 stage calls on an in-flight batch's activation ping-pong (x0 / x1) with the sums of
+// squares of the current activation threaded from its producer to its consumer (fused RMSNorm).
+static gh_status act_embed(gh_engine* e, gh_engine::Batch& b, cudaStream_t st) {
+  b.cur = 0;
+  b.ss_slices[0] = 1;
+  return t1_embed(e->t1, e->cfg.batch, b.tok, b.x0, b.ss0, st);
+}
+static gh_status act_pre(gh_engine* e, gh_engine::Batch& b, int l, cudaStream_t st) {
+  return t1_pre(e->t1, l, e->cfg.batch, b.x(b.cur), SsRef{b.ss(b.cur), b.ss_slices[b.cur]}, b.pos, b.fwd, st);
+}
+static gh_status act_post(gh_engine* e, gh_engine::Batch& b, int l, cudaStream_t st) {
+  const int nx = b.cur ^ 1;
+  GH_TRY(t1_post(e->t1, l, e->cfg.batch, b.bwd, b.x(nx), b.ss(nx), &b.ss_slices[nx], st));
+  b.cur = nx;
+  return GH_OK;
+}
+static gh_status act_classify(gh_engine* e, gh_engine::Batch& b, float* logits, cudaStream_t st) {
+  return t1_classify(e->t1, e->cfg.batch, b.x(b.cur), SsRef{b.ss(b.cur), b.ss_slices[b.cur]}, logits, b.next, st);
+}
+
 static gh_status engine_layer_loop_colocated(gh_engine* e, gh_engine::Batch& b, bool want_logits, cudaStream_t st) {
   const Shape& s = e->sh;
   const uint32_t B = e->cfg.batch;
-  GH_TRY(gh_tier1_embed(e->t1, B, b.tok, b.x0, st));
-  void* x = b.x0;
-  void* xn = b.x1;
+  GH_TRY(act_embed(e, b, st));
   for (int l = 0; l < s.N; ++l) {
-    GH_TRY(gh_tier1_pre(e->t1, l, B, x, b.pos, b.fwd, st));
+    GH_TRY(act_pre(e, b, l, st));
     GH_TRY(gh_tier2_attend(e->t2, l, B, b.slot, b.pos, b.fwd, b.bwd, st));
-    GH_TRY(gh_tier1_post(e->t1, l, B, b.bwd, xn, st));
-    std::swap(x, xn);
+    GH_TRY(act_post(e, b, l, st));
   }
-  GH_TRY(gh_tier1_classify(e->t1, B, x, want_logits ? b.logits : nullptr, b.next, st));
-  return GH_OK;
+  return act_classify(e, b, want_logits ? b.logits : nullptr, st);
 }
 
 extern "C" {
@@ -662,6 +743,11 @@ gh_status gh_engine_create(const gh_engine_config* cfg, gh_comm* comm, gh_engine
     GH_TRY(dev_alloc(e->mem, (size_t)R * s.D * s.db, &b.x1));
     GH_TRY(dev_alloc(e->mem, (size_t)R * s.ld_fwd() * s.db, &b.fwd));
     GH_TRY(dev_alloc(e->mem, (size_t)R * s.ld_bwd() * s.db, &b.bwd));
+    {
+      const size_t nss = (size_t)(s.D + 127) / 128 * 8 * R;  // W2 output tiles x max cluster size
+      GH_TRY(dev_alloc(e->mem, nss * sizeof(float), &p)); b.ss0 = (float*)p;
+      GH_TRY(dev_alloc(e->mem, nss * sizeof(float), &p)); b.ss1 = (float*)p;
+    }
     if (e->role != 2) { GH_TRY(dev_alloc(e->mem, (size_t)R * s.V * 4, &p)); b.logits = (float*)p; }
     std::vector<uint32_t> slots(R);
     for (int i = 0; i < R; ++i) slots[i] = ib * R + i;
@@ -724,20 +810,19 @@ static gh_status split_begin(gh_engine* e, gh_engine::Batch& b, ncclComm_t comm,
     for (int j = 0; j < e->kp; ++j)
       GH_NCCL(api.Send(b.pos + e->shard_off[j], e->shard_cnt[j], ncclInt32, j + 1, comm, st));
     GH_NCCL(api.GroupEnd());
-    GH_TRY(gh_tier1_embed(e->t1, e->cfg.batch, b.tok, b.x0, st));
+    GH_TRY(act_embed(e, b, st));
   } else {
     GH_NCCL(api.Recv(b.pos, e->my_cnt, ncclInt32, 0, comm, st));
   }
   return GH_OK;
 }
 
-static gh_status split_layer(gh_engine* e, gh_engine::Batch& b, ncclComm_t comm, int l, void** x, void** xn,
-                             cudaStream_t st) {
+static gh_status split_layer(gh_engine* e, gh_engine::Batch& b, ncclComm_t comm, int l, cudaStream_t st) {
   auto& api = nccl();
   const Shape& s = e->sh;
   const size_t fwd_row = (size_t)s.ld_fwd() * s.db, bwd_row = (size_t)s.ld_bwd() * s.db;
   if (e->role == 1) {
-    GH_TRY(gh_tier1_pre(e->t1, l, e->cfg.batch, *x, b.pos, b.fwd, st));
+    GH_TRY(act_pre(e, b, l, st));
     GH_NCCL(api.GroupStart());
     for (int j = 0; j < e->kp; ++j)
       GH_NCCL(api.Send((char*)b.fwd + e->shard_off[j] * fwd_row, e->shard_cnt[j] * fwd_row, ncclUint8, j + 1, comm, st));
@@ -746,8 +831,7 @@ static gh_status split_layer(gh_engine* e, gh_engine::Batch& b, ncclComm_t comm,
     for (int j = 0; j < e->kp; ++j)
       GH_NCCL(api.Recv((char*)b.bwd + e->shard_off[j] * bwd_row, e->shard_cnt[j] * bwd_row, ncclUint8, j + 1, comm, st));
     GH_NCCL(api.GroupEnd());
-    GH_TRY(gh_tier1_post(e->t1, l, e->cfg.batch, b.bwd, *xn, st));
-    std::swap(*x, *xn);
+    GH_TRY(act_post(e, b, l, st));
   } else {
     GH_NCCL(api.Recv(b.fwd, e->my_cnt * fwd_row, ncclUint8, 0, comm, st));
     GH_TRY(gh_tier2_attend(e->t2, l, e->my_cnt, b.slot, b.pos, b.fwd, b.bwd, st));
@@ -784,10 +868,8 @@ gh_status gh_engine_step_device(gh_engine* e, uint32_t ib, void* stream) {
   }
   ncclComm_t comm = e->comm->comms[0];
   GH_TRY(split_begin(e, b, comm, st));
-  void* x = b.x0;
-  void* xn = b.x1;
-  for (int l = 0; l < e->sh.N; ++l) GH_TRY(split_layer(e, b, comm, l, &x, &xn, st));
-  if (e->role == 1) GH_TRY(gh_tier1_classify(e->t1, e->cfg.batch, x, nullptr, b.next, st));
+  for (int l = 0; l < e->sh.N; ++l) GH_TRY(split_layer(e, b, comm, l, st));
+  if (e->role == 1) GH_TRY(act_classify(e, b, nullptr, st));
   return GH_OK;
 }
 
@@ -847,14 +929,12 @@ static gh_status split_step_pipelined(gh_engine* e, cudaStream_t st) {
   const int N = e->sh.N;
   ncclComm_t comm = e->comm->comms[0];
   if (e->role == 1) {
-    std::vector<void*> x(nb), xn(nb);
     std::vector<int> pending;
     bool header = true;
     for (int ib = 0; ib < nb; ++ib) {
       auto& b = e->batches[ib];
-      x[ib] = b.x0; xn[ib] = b.x1;
-      GH_TRY(gh_tier1_embed(e->t1, e->cfg.batch, b.tok, b.x0, st));
-      GH_TRY(gh_tier1_pre(e->t1, 0, e->cfg.batch, x[ib], b.pos, b.fwd, st));
+      GH_TRY(act_embed(e, b, st));
+      GH_TRY(act_pre(e, b, 0, st));
       pending.push_back(ib);
       if (ib < nb - 1) {  // let Tier-2 start on batch ib while batch ib+1 is prepared
         GH_TRY(t1_group(e, comm, st, pending, -1, header));
@@ -866,13 +946,12 @@ static gh_status split_step_pipelined(gh_engine* e, cudaStream_t st) {
         auto& b = e->batches[ib];
         GH_TRY(t1_group(e, comm, st, pending, ib, header));
         header = false;
-        GH_TRY(gh_tier1_post(e->t1, l, e->cfg.batch, b.bwd, xn[ib], st));
-        std::swap(x[ib], xn[ib]);
+        GH_TRY(act_post(e, b, l, st));
         if (l + 1 < N) {
-          GH_TRY(gh_tier1_pre(e->t1, l + 1, e->cfg.batch, x[ib], b.pos, b.fwd, st));
+          GH_TRY(act_pre(e, b, l + 1, st));
           pending.push_back(ib);
         } else {
-          GH_TRY(gh_tier1_classify(e->t1, e->cfg.batch, x[ib], nullptr, b.next, st));
+          GH_TRY(act_classify(e, b, nullptr, st));
         }
       }
     if (!pending.empty()) GH_TRY(t1_group(e, comm, st, pending, -1, false));
@@ -939,10 +1018,8 @@ gh_status gh_engine_step_host(gh_engine* e, uint32_t ib, const int32_t* tok_host
   } else if (logits_host && e->role == 1) {
     ncclComm_t comm = e->comm->comms[0];
     GH_TRY(split_begin(e, b, comm, st));
-    void* x = b.x0;
-    void* xn = b.x1;
-    for (int l = 0; l < e->sh.N; ++l) GH_TRY(split_layer(e, b, comm, l, &x, &xn, st));
-    GH_TRY(gh_tier1_classify(e->t1, e->cfg.batch, x, b.logits, b.next, st));
+    for (int l = 0; l < e->sh.N; ++l) GH_TRY(split_layer(e, b, comm, l, st));
+    GH_TRY(act_classify(e, b, b.logits, st));
   } else {
     GH_TRY(gh_engine_step_device(e, ib, stream));
   }
