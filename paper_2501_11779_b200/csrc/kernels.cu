@@ -9,6 +9,7 @@
 #include <cudaTypedefs.h>
 #include <math.h>
 #include <algorithm>
+#include <cstdio>
 #include <cstdlib>
 #include <map>
 #include <mutex>
@@ -433,7 +434,9 @@ GemmPlan plan_gemm(int N, int K, int Bt) {
   const int KB = (K + kBlockK - 1) / kBlockK;
   const int tiles = p.n_tiles * p.b_tiles;
   double best = 1e30;
-  for (int C : {1, 2, 4, 8}) {
+  // C = 8 (clusters of 8 CTAs) is excluded: only ~16 such clusters fit (GPC packing) and it
+  // measured 2-3x slower than C <= 4 for every decode shape (tools/gemm_sweep.py).
+  for (int C : {1, 2, 4}) {
     if (C == 1 && p.BN > 64) continue;  // the reduction keeps BN/C <= 64 rows per thread
     if (C > 1 && (p.BN / C < 4 || C > KB)) continue;
     if (cluster_override && C != cluster_override) continue;
@@ -442,6 +445,10 @@ GemmPlan plan_gemm(int N, int K, int Bt) {
     const double cost = rounds * ((KB + C - 1) / C + (C > 1 ? 1.0 : 0.0));
     if (cost < best - 1e-9) { best = cost; p.C = C; p.n_clusters = ncl; }
   }
+  static const bool verbose = getenv("GH_GEMM_VERBOSE") != nullptr;  // diagnostics
+  if (verbose)
+    fprintf(stderr, "[gh] gemm N=%d K=%d B=%d: BN=%d b_tiles=%d C=%d clusters=%d (max %d)\n", N, K, Bt, p.BN,
+            p.b_tiles, p.C, p.n_clusters, max_clusters_bn(p.BN, p.C));
   return p;
 }
 
