@@ -155,6 +155,21 @@ def workload(args, world):
                 shard=shard, kp=kp, admitted_slots=slots)
 
 
+def ncu_traffic(kernel_prefix):
+    """DRAM bytes per launch (read + write) of a kernel from the committed ncu --set full capture
+    (profiles/*_ncu_full_metrics.csv, newest round first), or None."""
+    import csv
+    for p in sorted((ROOT / "profiles").glob("r*_ncu_full_metrics.csv"), reverse=True):
+        with open(p) as f:
+            for row in csv.DictReader(f):
+                if kernel_prefix in row.get("Kernel Name", ""):
+                    try:
+                        return (float(row["dram__bytes_read.sum"]) + float(row["dram__bytes_write.sum"])) * 1e6
+                    except (KeyError, ValueError):
+                        return None
+    return None
+
+
 def attention_bytes(spec, B, ctx):
     """SURVEY.md §8d algorithmic bytes of one attention launch (one layer):
     dtype*(2*D_kv*sum_b S_b + 2*B*D_kv + 2*B*D), S_b = ctx (cached ctx-1 + the new token)."""
@@ -401,7 +416,9 @@ def main():
         ach = ab / (res["attn_ms"] / 1e3) / 1e9
         out["roofline"] = {"bound": "hbm", "kernel": "attn_decode_kernel (Tier-2 F2, one layer)",
                            "achieved": ach, "peak": hbm, "unit": "GB/s", "frac": ach / hbm,
-                           "peak_kind": peak_kind, "traffic": None, "algorithmic_bytes": ab,
+                           "peak_kind": peak_kind, "traffic": ncu_traffic("attn_decode_kernel"),
+                           "traffic_source": "profiles/*_ncu_full_metrics.csv (dram read+write per launch)",
+                           "algorithmic_bytes": ab,
                            "duration_us": res["attn_ms"] * 1e3, "frac_of_8TBs": ach / 8000.0}
         gb = gemm_layer_bytes(spec, wl["batch"])
         gach = gb / (res["na_ms"] / 1e3) / 1e9
