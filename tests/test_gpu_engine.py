@@ -66,6 +66,10 @@ def test_c1_graph_matches_eager(need_gpu):
 @pytest.mark.parametrize("spec,B,steps", [
     (gh.ModelSpec("e2e-bf16", 3, 512, 512, 1024, 4, 4, 128, 2, 2000), 20, 10),
     (gh.ModelSpec("e2e-gqa", 2, 1024, 256, 1536, 16, 4, 128, 2, 1000), 9, 6),
+    # B > 256: several 128-column batch tiles and the unfused-RMSNorm fallback of the Tier-1 path
+    (gh.ModelSpec("e2e-wide", 2, 512, 512, 1024, 4, 4, 64, 2, 700), 300, 3),
+    # 128 < B <= 256: two batch tiles with the fused RMSNorm
+    (gh.ModelSpec("e2e-b192", 2, 512, 512, 1024, 4, 4, 64, 2, 700), 192, 3),
 ])
 def test_bf16_engine_teacher_forced(need_gpu, spec, B, steps):
     """bf16 storage: per step, the GPU's argmax equals the oracle's wherever the oracle's top-2
