@@ -245,6 +245,49 @@ GH_DEV void umma_commit(uint64_t* bar) {
           smem_u32(bar))
       : "memory");
 }
+// ---- CTA-pair (cta_group::2) variants: the two CTAs of a cluster pair share one M = 256 MMA.
+// Both CTAs' allocator warps allocate together (same column count, same smem slot offset).
+template <uint32_t kCols>
+GH_DEV void tmem_alloc_pair(uint32_t* smem_dst) {
+  asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(smem_u32(smem_dst)),
+               "n"(kCols));
+  asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;\n");
+}
+template <uint32_t kCols>
+GH_DEV void tmem_free_pair(uint32_t taddr) {
+  asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;\n" ::"r"(taddr), "n"(kCols));
+}
+// Issued by the leader CTA only: A rows 0..127 / B rows 0..N/2-1 come from the leader's shared
+// memory, A rows 128..255 / B rows N/2..N-1 from the peer's at the same offsets; D rows 0..127
+// land in the leader's TMEM and rows 128..255 in the peer's.
+GH_DEV void umma_bf16_pair(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc, uint32_t idesc,
+                           uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(d_tmem),
+      "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate));
+}
+// Arrive on the mbarrier at the same offset in every CTA of `mask` once the leader's previously
+// issued pair MMAs complete.
+GH_DEV void umma_commit_pair(uint64_t* bar, uint16_t mask) {
+  asm volatile(
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;\n" ::"r"(
+          smem_u32(bar)),
+      "h"(mask)
+      : "memory");
+}
+// TMA into this CTA's shared memory whose completion is signalled on the LEADER's mbarrier
+// (`leader_bar` is a shared::cluster address, see mapa_shared).
+GH_DEV void tma_load_2d_pair(void* smem_dst, const void* tmap, int c0, int c1, uint32_t leader_bar,
+                             uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+      " [%0], [%1, {%2, %3}], [%4], %5;\n" ::"r"(smem_u32(smem_dst)),
+      "l"(tmap), "r"(c0), "r"(c1), "r"(leader_bar), "l"(policy)
+      : "memory");
+}
+
 // 32 lanes x 32b, 16 consecutive columns per thread
 GH_DEV void tmem_ld16(uint32_t taddr, uint32_t (&r)[16]) {
   asm volatile(

@@ -158,7 +158,9 @@ GH_DEV void epi_slice(const EpiParams& ep, const GemmShape& gs, int n, int b, fl
       uint16_t* op = (uint16_t*)ep.out + (long)b * ep.ldo + n;
       if (full) store_run_bf16<En>(op, v);
       else
-        for (int e = 0; e < En && n + e < gs.N; ++e) op[e] = f32_to_bf16(v[e]);
+#pragma unroll
+        for (int e = 0; e < En; ++e)
+          if (n + e < gs.N) op[e] = f32_to_bf16(v[e]);
       return;
     }
     case EPI_QKV_ROPE: {
@@ -187,7 +189,9 @@ GH_DEV void epi_slice(const EpiParams& ep, const GemmShape& gs, int n, int b, fl
       uint16_t* op = (uint16_t*)ep.out + (long)b * ep.ldo + n;
       if (full) store_run_bf16<En>(op, v);
       else
-        for (int e = 0; e < En && n + e < gs.N; ++e) op[e] = f32_to_bf16(v[e]);
+#pragma unroll
+        for (int e = 0; e < En; ++e)
+          if (n + e < gs.N) op[e] = f32_to_bf16(v[e]);
       return;
     }
     case EPI_SWIGLU: {
@@ -198,7 +202,9 @@ GH_DEV void epi_slice(const EpiParams& ep, const GemmShape& gs, int n, int b, fl
       uint16_t* op = (uint16_t*)ep.out + (long)b * ep.ldo + (n >> 1);
       if (full) store_run_bf16<En / 2>(op, h);
       else
-        for (int e = 0; e < En / 2 && n + 2 * e < gs.N; ++e) op[e] = f32_to_bf16(h[e]);
+#pragma unroll
+        for (int e = 0; e < En / 2; ++e)
+          if (n + 2 * e < gs.N) op[e] = f32_to_bf16(h[e]);
       return;
     }
     default: {
@@ -210,7 +216,9 @@ GH_DEV void epi_slice(const EpiParams& ep, const GemmShape& gs, int n, int b, fl
         if (n + e < gs.N && (v[e] > best || (v[e] == best && n + e < bi))) { best = v[e]; bi = n + e; }
       if (ep.logits && col_ok) {
         float* lp = ep.logits + (long)b * ep.ldl + n;
-        for (int e = 0; e < En && n + e < gs.N; ++e) lp[e] = v[e];
+#pragma unroll
+        for (int e = 0; e < En; ++e)
+          if (n + e < gs.N) lp[e] = v[e];
       }
       // reduce over the 128/BN threads that share column b (adjacent lanes)
       constexpr int kRuns = 128 / BN;

@@ -16,6 +16,7 @@
 
 #include "attention.cuh"
 #include "common.cuh"
+#include "gemm_pair.cuh"
 #include "gemm_tc.cuh"
 #include "kernels.hpp"
 
@@ -422,8 +423,68 @@ static int max_clusters_bn(int BN, int C) {
   }
 }
 
+static int pair_override = 0;  // diagnostics: 1 = split-K only, 2 = pair whenever possible
+
+static int pair_stages(int BN) { return std::max(2, PairSmem::max_stages(BN, 227 * 1024)); }
+
+// co-resident CTA pairs of the pair kernel (cudaOccupancyMaxActiveClusters, largest tile)
+static int max_pairs() {
+  static int n = -1;
+  if (n >= 0) return n;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(kNumSMs);
+  cfg.blockDim = dim3(kGemmThreads);
+  cfg.dynamicSmemBytes = PairSmem::bytes(kPairMaxBN, pair_stages(kPairMaxBN));
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = 2;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  if (cudaOccupancyMaxActiveClusters(&n, gemm_pair_kernel, &cfg) != cudaSuccess || n <= 0) {
+    cudaGetLastError();
+    n = kNumSMs / 2;
+  }
+  return n;
+}
+
+// Per-k-block cycles of one CTA, bounded by the L2->SM operand stream (~57 B/clk/SM measured
+// with the MMA disabled, tools/gemm_sweep.py) or by the tensor core (4096 bf16 MAC/clk/SM).
+static double kblock_clk(double bytes_per_sm, double mma_clk) {
+  return std::max(bytes_per_sm / 57.0, mma_clk) + 40.0;
+}
+
+// Pair plan for a large batch: the batch split into b_tiles tiles of BN (multiple of 32, <= 256)
+// columns minimising rounds * KB * kblock_clk (wave quantisation against per-tile L2 traffic).
+static GemmPlan plan_pair(int N, int KB, int Bt, double* cost_out) {
+  GemmPlan best;
+  double best_cost = 1e30;
+  const int n_tiles = (N + 2 * kBlockM - 1) / (2 * kBlockM);
+  const int npairs = max_pairs();
+  int last_bn = 0;
+  for (int bt = (Bt + kPairMaxBN - 1) / kPairMaxBN; bt <= (Bt + 31) / 32; ++bt) {
+    const int BN = ((Bt + bt - 1) / bt + 31) / 32 * 32;
+    if (BN == last_bn) continue;
+    last_bn = BN;
+    const int b_tiles = (Bt + BN - 1) / BN;
+    const int tiles = n_tiles * b_tiles;
+    const int np = std::min(tiles, npairs);
+    const int rounds = (tiles + np - 1) / np;
+    const double cost = (double)rounds * KB * kblock_clk(16384.0 + BN * 64.0, 2.0 * BN);
+    if (cost < best_cost - 1e-9) {
+      best_cost = cost;
+      best.pair = true; best.BN = BN; best.b_tiles = b_tiles; best.n_tiles = n_tiles;
+      best.C = 2; best.n_clusters = np;
+    }
+  }
+  *cost_out = best_cost;
+  return best;
+}
+
 // Choose the cluster size C minimising the k-blocks on the critical path of one CTA:
 // rounds(C) * (ceil(KB / C) + reduction overhead), rounds = ceil(tiles / co-resident clusters).
+// Batches above 128 columns also consider the pair kernel (always used above 256).
 GemmPlan plan_gemm(int N, int K, int Bt) {
   GemmPlan p;
   const int bt_cap = std::min(Bt, 128);
@@ -445,10 +506,16 @@ GemmPlan plan_gemm(int N, int K, int Bt) {
     const double cost = rounds * ((KB + C - 1) / C + (C > 1 ? 1.0 : 0.0));
     if (cost < best - 1e-9) { best = cost; p.C = C; p.n_clusters = ncl; }
   }
+  if ((Bt > 128 && pair_override != 1) || pair_override == 2 || Bt > 256) {
+    double pc = 0;
+    GemmPlan pp = plan_pair(N, KB, Bt, &pc);
+    const double sc = best * kblock_clk(16384.0 + p.BN * 128.0, 2.0 * p.BN);
+    if (Bt > 256 || pair_override == 2 || pc < sc) p = pp;
+  }
   static const bool verbose = getenv("GH_GEMM_VERBOSE") != nullptr;  // diagnostics
   if (verbose)
-    fprintf(stderr, "[gh] gemm N=%d K=%d B=%d: BN=%d b_tiles=%d C=%d clusters=%d (max %d)\n", N, K, Bt, p.BN,
-            p.b_tiles, p.C, p.n_clusters, max_clusters_bn(p.BN, p.C));
+    fprintf(stderr, "[gh] gemm N=%d K=%d B=%d: %s BN=%d b_tiles=%d n_tiles=%d C=%d clusters=%d\n", N, K, Bt,
+            p.pair ? "pair" : "split-K", p.BN, p.b_tiles, p.n_tiles, p.C, p.n_clusters);
   return p;
 }
 
@@ -482,7 +549,34 @@ static cudaError_t launch_tc(const CUtensorMap* tmW, const CUtensorMap* tmX, Gem
   return cudaLaunchKernelEx(&cfg, gemm_tc_kernel<BN>, *tmW, *tmX, gs, ep);
 }
 
+static cudaError_t launch_pair(const CUtensorMap* tmW, const CUtensorMap* tmX, GemmShape gs, const GemmPlan& p,
+                               const EpiParams& ep, cudaStream_t st) {
+  gs.BN = p.BN;
+  gs.stages = pair_stages(p.BN);
+  const int smem = PairSmem::bytes(p.BN, gs.stages);
+  if (smem > 227 * 1024 || p.BN % 32 || p.BN > kPairMaxBN) return cudaErrorInvalidValue;
+  if (ep.ss_in && gs.Bt > kPairMaxInvCols) return cudaErrorInvalidValue;
+  static const bool pdl = getenv("GH_NO_PDL") == nullptr;
+  cudaLaunchAttribute attr[2];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = 2;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[1].val.programmaticStreamSerializationAllowed = 1;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(2 * p.n_clusters);
+  cfg.blockDim = dim3(kGemmThreads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl ? 2 : 1;
+  GH_COUNT_LAUNCH();
+  return cudaLaunchKernelEx(&cfg, gemm_pair_kernel, *tmW, *tmX, gs, ep);
+}
+
 void gemm_debug_cluster(int C) { cluster_override = C; }
+void gemm_debug_pair(int mode) { pair_override = mode; }
 void gemm_debug_set(int stages) { stages_override = stages; }
 
 cudaError_t launch_gemm(const Weight& W, const CUtensorMap* tmW, const void* X, long ldx,
@@ -510,6 +604,9 @@ cudaError_t launch_gemm(const Weight& W, const CUtensorMap* tmW, const void* X, 
   gs.kb_total = (W.K + kBlockK - 1) / kBlockK;
   gs.flags = sc.debug_flags;
   gs.trace = sc.trace;
+  gs.BN = p.BN;
+  if (p.pair) return launch_pair(tmW, tmX, gs, p, ep, st);
+  if (ep.ss_in && Bt > kMaxInvCols) return cudaErrorInvalidValue;
   switch (p.BN) {
     case 16: return launch_tc<16>(tmW, tmX, gs, p, ep, st);
     case 32: return launch_tc<32>(tmW, tmX, gs, p, ep, st);
@@ -575,6 +672,7 @@ cudaError_t configure_kernels() {
   cudaError_t e = cudaSuccess;
   auto chk = [&](cudaError_t r) { if (e == cudaSuccess) e = r; };
   chk(configure_tc<16>()); chk(configure_tc<32>()); chk(configure_tc<64>()); chk(configure_tc<128>());
+  chk(cudaFuncSetAttribute(gemm_pair_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
   chk(configure_attn<bf16_t, 48>()); chk(configure_attn<bf16_t, 64>()); chk(configure_attn<bf16_t, 128>());
   chk(configure_attn<float, 48>()); chk(configure_attn<float, 64>()); chk(configure_attn<float, 128>());
   return e;

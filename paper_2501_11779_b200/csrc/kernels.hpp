@@ -35,14 +35,21 @@ struct RowSegs {
 };
 
 // Per-GEMM launch plan chosen on the host: batch tile and persistent cluster split-K grid.
+//  split-K kernel (gemm_tc.cuh): 128-row tiles, clusters of C CTAs split K;
+//  pair kernel (gemm_pair.cuh, large batches): 256-row tiles on CTA pairs (C = 2), no K split.
 struct GemmPlan {
-  int BN = 0;         // batch tile (16, 32, 64, 128, 256)
-  int n_tiles = 0;    // ceil(N / 128)
+  bool pair = false;
+  int BN = 0;         // batch tile (split-K: 16, 32, 64, 128; pair: multiple of 32 up to 256)
+  int n_tiles = 0;    // ceil(N / 128), pair: ceil(N / 256)
   int b_tiles = 0;
-  int C = 1;          // CTAs per cluster = K splits of every tile (1, 2, 4, 8)
+  int C = 1;          // CTAs per cluster (split-K: K splits 1, 2, 4; pair: 2)
   int n_clusters = 0; // persistent clusters (<= co-resident clusters)
-  int slices() const { return n_tiles * C; }  // argmax partials per batch column
+  int slices() const { return n_tiles * C; }  // 128-row (or 128/C-row) output slices: argmax / norm partials
+  int x_box_rows() const { return pair ? BN / 2 : BN; }  // activation rows per TMA box
 };
+// Largest batch whose RMSNorm can be fused into the consuming GEMM's epilogue (the planner
+// uses the pair kernel, whose scale table holds 1024 columns, for every batch above 256).
+constexpr int kFusedNormMaxBatch = 1024;
 GemmPlan plan_gemm(int N, int K, int Bt);
 
 // Scratch shared by every GEMM of a tier (SIMT staging, diagnostics).
@@ -53,6 +60,7 @@ struct GemmScratch {
 };
 void gemm_debug_set(int stages);  // 0 = production pipeline depth
 void gemm_debug_cluster(int C);   // 0 = production cluster-size choice
+void gemm_debug_pair(int mode);   // 0 = planner's choice, 1 = force split-K (B <= 256), 2 = force pair
 
 // Encode a 2-D bf16 tensor map over a row-major [rows, cols] matrix with row stride ld
 // (elements), box {64, box_rows}, 128-byte swizzle.

@@ -47,6 +47,7 @@ struct GemmShape {
   int n_tiles, b_tiles; // 128-row weight tiles x BN-column batch tiles
   int kb_total;         // KB = ceil(K / 64)
   int stages;           // TMA -> MMA pipeline depth (shared-memory ring)
+  int BN;               // pair kernel: batch columns per tile (multiple of 32, <= 256)
   int flags;            // diagnostics (GEMM_DBG_*), 0 in production
   unsigned long long* trace;  // diagnostics: per-CTA globaltimer stamps [grid][8] (nullptr = off)
 };

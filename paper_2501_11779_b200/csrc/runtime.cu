@@ -133,7 +133,7 @@ struct gh_tier1 {
                  const EpiParams& ep, cudaStream_t st) {
     const GemmPlan& p = plan(W.N, W.K, B);
     CUtensorMap* tmX = nullptr;
-    if (sh.db == 2) GH_TRY(tmaps.get(X, (uint64_t)B, (uint64_t)W.K, (uint64_t)ldx, (uint32_t)p.BN, &tmX));
+    if (sh.db == 2) GH_TRY(tmaps.get(X, (uint64_t)B, (uint64_t)W.K, (uint64_t)ldx, (uint32_t)p.x_box_rows(), &tmX));
     GH_CUDA(launch_gemm(W, tmW, X, ldx, tmX, B, p, ep, gsc, st));
     return GH_OK;
   }
@@ -330,7 +330,7 @@ static gh_status t1_pre(gh_tier1* t, uint32_t layer, uint32_t B, const void* x, 
   ep.pos = pos;
   ep.d_head = s.dh;
   ep.rope_rows = s.D + s.Dkv;
-  if (s.db == 2 && ss.ss && B <= (uint32_t)kMaxInvCols) {
+  if (s.db == 2 && ss.ss && B <= (uint32_t)kFusedNormMaxBatch) {
     // fused: QKV on the raw x, RMSNorm scale in the epilogue, x copied into the message there
     ep.ss_in = ss.ss; ep.ss_in_slices = ss.slices; ep.ss_dim = s.D; ep.ss_eps = s.s.norm_eps;
     ep.xcopy_src = x; ep.xcopy_ld = s.D; ep.xcopy_rows = s.D;
@@ -350,7 +350,7 @@ static gh_status t1_post(gh_tier1* t, uint32_t layer, uint32_t B, const void* ms
   if (B == 0) return GH_OK;
   const Shape& s = t->sh;
   auto& L = t->layers[layer - t->l0];
-  const bool fused = s.db == 2 && B <= (uint32_t)kMaxInvCols;
+  const bool fused = s.db == 2 && B <= (uint32_t)kFusedNormMaxBatch;
   // h = attn Wo^T + x   (+ per-slice sums of squares of h for the fused FFN norm)
   EpiParams ep = epi_default();
   ep.kind = EPI_STORE_RESID;
@@ -395,7 +395,7 @@ static gh_status t1_classify(gh_tier1* t, uint32_t B, const void* x, SsRef ss, f
   ep.logits = logits; ep.ldl = s.V;
   ep.part = t->part;
   const void* in = x;
-  if (s.db == 2 && ss.ss && B <= (uint32_t)kMaxInvCols) {
+  if (s.db == 2 && ss.ss && B <= (uint32_t)kFusedNormMaxBatch) {
     ep.ss_in = ss.ss; ep.ss_in_slices = ss.slices; ep.ss_dim = s.D; ep.ss_eps = s.s.norm_eps;
   } else {
     GH_CUDA(launch_rmsnorm(s.db, x, s.D, t->final_norm, t->xn, s.D, nullptr, 0, (int)B, s.D, s.s.norm_eps, st));
@@ -1051,10 +1051,13 @@ extern "C" gh_status gh_debug_gemm_bench(int N, int K, int B, int flags, int sta
   GH_TRY(dev_alloc(mem, (size_t)B * K * 2, &X));
   GH_TRY(dev_alloc(mem, (size_t)B * N * 2, &Y));
   GH_CUDA(cudaMemset(X, 0, (size_t)B * K * 2));
-  gemm_debug_cluster(ks);  // diagnostics: force the cluster size (0 = production choice)
+  // diagnostics: ks > 0 forces the split-K cluster size, -1 forces split-K, -2 the pair kernel
+  if (ks >= 0) gemm_debug_cluster(ks);
+  else gemm_debug_pair(-ks);
   GemmPlan p = plan_gemm(N, K, B);
   gemm_debug_cluster(0);
-  GH_CUDA(make_tmap_bf16(&tmX, X, (uint64_t)B, (uint64_t)K, (uint64_t)K, (uint32_t)p.BN));
+  gemm_debug_pair(0);
+  GH_CUDA(make_tmap_bf16(&tmX, X, (uint64_t)B, (uint64_t)K, (uint64_t)K, (uint32_t)p.x_box_rows()));
   GemmScratch sc;
   sc.debug_flags = flags;
   EpiParams ep = epi_default();
@@ -1100,7 +1103,7 @@ extern "C" gh_status gh_debug_gemm_trace(int N, int K, int B, int copies, int re
   GH_CUDA(cudaMemset(X, 0, (size_t)B * K * 2));
   GemmPlan p = plan_gemm(N, K, B);
   CUtensorMap tmX;
-  GH_CUDA(make_tmap_bf16(&tmX, X, (uint64_t)B, (uint64_t)K, (uint64_t)K, (uint32_t)p.BN));
+  GH_CUDA(make_tmap_bf16(&tmX, X, (uint64_t)B, (uint64_t)K, (uint64_t)K, (uint32_t)p.x_box_rows()));
   GemmScratch sc;
   void* q;
   sc.debug_flags = dbg_flags;
