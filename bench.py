@@ -283,7 +283,9 @@ def run_split(args, wl, rank, world):
     obj = [Comm.unique_ids(1) if rank == 0 else None]
     dist.broadcast_object_list(obj, src=0)
     comm = Comm(obj[0], world, rank, dev)
-    eng = Engine(spec, batch=wl["batch"], inflight=IF, device=dev, use_graph=False, comm=comm)
+    eng = Engine(spec, batch=wl["batch"], inflight=IF, device=dev, use_graph=False, comm=comm,
+                 transport=args.transport)
+    transport = eng.transport
     lib = gh.lib()
     stream = torch.cuda.Stream()
     if eng.role == "tier2":
@@ -341,7 +343,7 @@ def run_split(args, wl, rank, world):
     comm.close()
     total = wl["batch"] * IF
     return dict(ms=ms, value=total / (ms / 1e3), e2e_ms=float(e2e_ms.item()), launches=int(launches.item()),
-                clocks=clk.summary(), total=total)
+                clocks=clk.summary(), total=total, transport=transport)
 
 
 # ------------------------------------------------------------------ main
@@ -354,6 +356,8 @@ def main():
     ap.add_argument("--config", default=None, choices=[None, "C2", "C3"])
     ap.add_argument("--cpu-threads", type=int, default=0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--transport", default="auto", choices=["auto", "nccl", "peer"],
+                    help="tier-split message transport (peer: copy engines + IPC flags; nccl: send/recv)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
 
@@ -397,6 +401,7 @@ def main():
         import torch.distributed as dist
         dist.init_process_group("gloo")
         res = run_split(args, wl, rank, world)
+        cfg["transport"] = res["transport"]
         if rank != 0:
             dist.destroy_process_group()
             return

@@ -189,7 +189,18 @@ typedef struct gh_engine_config {
   uint32_t inflight;       /* IF in-flight batches (>=1); each has its own slots */
   uint32_t n_slots;        /* Tier-2 slots on this GPU (0 = exactly what the shard needs) */
   int use_graph;           /* capture the step in a CUDA graph (colocated only) */
+  int transport;           /* tier split, pipelined step (gh_engine_step_all*): GH_TRANSPORT_* */
 } gh_engine_config;
+
+/* Inter-tier message transport of the pipelined tier-split step.
+ *  AUTO: PEER when every rank can map every peer buffer (CUDA IPC over NVLink), else NCCL.
+ *  NCCL: grouped ncclSend/ncclRecv on the compute stream.
+ *  PEER: copy-engine writes into the receiving GPU's message buffers + sequence-number flags
+ *        (cuStreamWriteValue32 / cuStreamWaitValue32); no SM time is spent on transfers.
+ * The per-batch entry points (gh_engine_step_device / step_host) always use NCCL. */
+enum { GH_TRANSPORT_AUTO = 0, GH_TRANSPORT_NCCL = 1, GH_TRANSPORT_PEER = 2 };
+/* Transport in use (split roles), -1 when colocated. */
+int gh_engine_transport(const gh_engine* e);
 
 gh_status gh_engine_create(const gh_engine_config* cfg, gh_comm* comm, gh_engine** out);
 gh_status gh_engine_destroy(gh_engine* e);

@@ -60,7 +60,8 @@ class GhSpec(C.Structure):
 class GhEngineConfig(C.Structure):
     _fields_ = [("spec", GhSpec), ("device", C.c_int), ("weight_seed", C.c_uint64),
                 ("batch", C.c_uint32), ("inflight", C.c_uint32), ("n_slots", C.c_uint32),
-                ("use_graph", C.c_int)]
+                ("use_graph", C.c_int),
+                ("transport", C.c_int)]
 
 
 u64, u32, i32, i64, vp = C.c_uint64, C.c_uint32, C.c_int32, C.c_int64, C.c_void_p
@@ -107,6 +108,7 @@ PROTOTYPES = {
     "gh_engine_create": (st, [P(GhEngineConfig), vp, P(vp)]),
     "gh_engine_destroy": (st, [vp]),
     "gh_engine_role": (C.c_int, [vp]),
+    "gh_engine_transport": (C.c_int, [vp]),
     "gh_engine_step_device": (st, [vp, u32, vp]),
     "gh_engine_step_host": (st, [vp, u32, vp, vp, vp, vp, vp]),
     "gh_engine_step_all": (st, [vp, vp]),

@@ -31,8 +31,9 @@ struct AttnCfg {
   static constexpr int kTpos = (kW * kPg > 64) ? kW * kPg : 64;  // positions per stage
   static constexpr int kPasses = kTpos / (kW * kPg);
   static constexpr int kTileBytes = kTpos * DH * (int)sizeof(T);
-  // per-stage header (first stage of a unit): q, new k, new v (bulk-copied) + {L, b, h}
-  static constexpr int kHdrBytes = 3 * DH * (int)sizeof(T) + 16;
+  // per-stage header (first stage of a unit): q, new k, new v and the unit's d_h-slice of the
+  // residual x (bulk-copied from the fwd message) + {L, b, h, slot}
+  static constexpr int kHdrBytes = 4 * DH * (int)sizeof(T) + 16;
   static constexpr int kStageBytes = ((2 * kTileBytes + kHdrBytes + 127) / 128) * 128;
   static constexpr int kStages = (196608 / kStageBytes) > 6 ? 6 : (196608 / kStageBytes);
   static constexpr int kThreads = 32 * (1 + kW);
@@ -131,11 +132,11 @@ __global__ void __launch_bounds__(AttnCfg<T, DH, W>::kThreads, 1)
           const uint32_t bytes = (uint32_t)np * DH * sizeof(T);
           uint8_t* sk = smem + s * C::kStageBytes;
           uint8_t* hdr = sk + 2 * C::kTileBytes;
-          if (c == 0) {  // unit header: metadata (plain store, released by the arrive) + q/k/v copies
-            int* meta = (int*)(hdr + 3 * DH * sizeof(T));
-            meta[0] = L; meta[1] = b; meta[2] = h;
+          if (c == 0) {  // unit header: metadata (plain store, released by the arrive) + q/k/v/x copies
+            int* meta = (int*)(hdr + 4 * DH * sizeof(T));
+            meta[0] = L; meta[1] = b; meta[2] = h; meta[3] = sl;
           }
-          mbar_arrive_expect_tx(&full[s], 2 * bytes + (c == 0 ? 3 * DH * (uint32_t)sizeof(T) : 0u));
+          mbar_arrive_expect_tx(&full[s], 2 * bytes + (c == 0 ? 4 * DH * (uint32_t)sizeof(T) : 0u));
           if (np > 0) {
             bulk_g2s(sk, kbase + (long)c * C::kTpos * DH, bytes, &full[s], pol);
             bulk_g2s(sk + C::kTileBytes, vbase + (long)c * C::kTpos * DH, bytes, &full[s], pol);
@@ -145,11 +146,13 @@ __global__ void __launch_bounds__(AttnCfg<T, DH, W>::kThreads, 1)
             bulk_g2s(hdr, row + a.D + (long)h * DH, DH * sizeof(T), &full[s], pol);
             bulk_g2s(hdr + DH * sizeof(T), row + 2L * a.D + (long)kvh * DH, DH * sizeof(T), &full[s], pol);
             bulk_g2s(hdr + 2 * DH * sizeof(T), row + 2L * a.D + a.Dkv + (long)kvh * DH, DH * sizeof(T), &full[s], pol);
+            bulk_g2s(hdr + 3 * DH * sizeof(T), row + (long)h * DH, DH * sizeof(T), &full[s], pol);
           }
         }
         L = Ln;
         sl = sln;
       }
+      prefetch_l2_share(a.pf, a.pf_bytes, blockIdx.x, gridDim.x);
     }
     return;
   }
@@ -169,8 +172,8 @@ __global__ void __launch_bounds__(AttnCfg<T, DH, W>::kThreads, 1)
     const T* hq = (const T*)hdr;
     const T* hk = hq + DH;
     const T* hv = hk + DH;
-    const int* meta = (const int*)(hdr + 3 * DH * sizeof(T));
-    const int L = meta[0], b = meta[1], h = meta[2], kvh = h / group;
+    const int* meta = (const int*)(hdr + 4 * DH * sizeof(T));
+    const int L = meta[0], b = meta[1], h = meta[2], kvh = h / group, slot = meta[3];
     const int nch = L > 0 ? (L + C::kTpos - 1) / C::kTpos : 1;
 
     float q[C::kEl], o[C::kEl];
@@ -186,7 +189,7 @@ __global__ void __launch_bounds__(AttnCfg<T, DH, W>::kThreads, 1)
 
     if (cw == 0) {
       // new token: score from the header, append k/v to the arena (group 0 lanes)
-      T* kdst = arena + (long)a.slot[b] * a.slot_stride + (long)kvh * a.head_stride + (long)L * DH;
+      T* kdst = arena + (long)slot * a.slot_stride + (long)kvh * a.head_stride + (long)L * DH;
       T* vdst = kdst + a.kv_stride;
       float part = 0.f;
       float vf[C::kEl];
@@ -213,6 +216,12 @@ __global__ void __launch_bounds__(AttnCfg<T, DH, W>::kThreads, 1)
 #pragma unroll
         for (int e = 0; e < C::kEl; ++e) o[e] = vf[e];
       }
+    }
+
+    if (cw == (C::kW > 1 ? 1 : 0) && lane < C::kChunks) {
+      // pass the residual stream through, one d_h slice per unit: bwd.x[h*DH .. +DH) = fwd.x[...]
+      const uint4* xs = (const uint4*)(hk + 2 * DH);
+      *((uint4*)(bwd + (long)b * ld_bwd + (long)h * DH) + lane) = xs[lane];
     }
 
     for (int c = 0; c < nch; ++c, ++it) {
@@ -330,11 +339,6 @@ __global__ void __launch_bounds__(AttnCfg<T, DH, W>::kThreads, 1)
 #pragma unroll
         for (int w = 0; w < C::kW; ++w) acc += cbuf[w * (DH + 2) + d] * f[w];
         St<T>::store(orow, d, acc * inv);
-      }
-      if (h == 0) {  // pass the residual stream through: bwd.x = fwd.x
-        const uint4* xs = (const uint4*)(fwd + (long)b * ld_fwd);
-        uint4* xd = (uint4*)(bwd + (long)b * ld_bwd);
-        for (int i = lane; i < a.D / C::kVec; i += 32) xd[i] = xs[i];
       }
       __syncwarp();
       if (lane == 0) {

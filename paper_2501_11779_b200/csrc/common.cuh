@@ -211,6 +211,17 @@ GH_DEV void tma_load_2d_nohint(void* smem_dst, const void* tmap, int c0, int c1,
       "l"(tmap), "r"(c0), "r"(c1), "r"(smem_u32(bar))
       : "memory");
 }
+// Bulk L2 prefetch (no completion tracking): part `part` of `nparts` equal shares of [base, +bytes).
+GH_DEV void prefetch_l2_share(const void* base, unsigned long long bytes, int part, int nparts) {
+  if (!base || bytes == 0) return;
+  const unsigned long long share = ((bytes + nparts - 1) / nparts + 4095) & ~4095ull;
+  const unsigned long long lo = share * part;
+  const unsigned long long hi = lo + share < bytes ? lo + share : bytes;
+  for (unsigned long long o = lo; o < hi; o += 32768) {
+    const uint32_t n = (uint32_t)((hi - o < 32768 ? hi - o : 32768) & ~15ull);
+    if (n) asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"((const char*)base + o), "r"(n) : "memory");
+  }
+}
 GH_DEV void prefetch_tmap(const void* tmap) {
   asm volatile("prefetch.tensormap [%0];\n" ::"l"(tmap) : "memory");
 }

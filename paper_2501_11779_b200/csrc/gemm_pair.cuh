@@ -127,6 +127,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         tma_load_2d_pair(sa, &tmW, 0, w_row(i), full0 + s * 8, pol_w);
         tma_load_2d_pair(sa + L::kABytes, &tmX, (i % KB) * kBlockK, x_row(i), full0 + s * 8, pol_x);
       }
+      prefetch_l2_share(gs.pf, gs.pf_bytes, blockIdx.x, gridDim.x);
     }
   } else if (warp == 1) {
     // ---------------- MMA issuer (leader only): one accumulator buffer per tile, alternating

@@ -399,6 +399,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
           if (load_x) tma_load_2d_nohint(sb, &tmX, kb * kBlockK, tile_b * BN, &full[s]);
         }
       }
+      prefetch_l2_share(gs.pf, gs.pf_bytes, blockIdx.x, gridDim.x);
     }
   } else if (warp == 1) {
     // ---------------- MMA issuer: one accumulator buffer per tile, alternating

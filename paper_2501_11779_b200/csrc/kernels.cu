@@ -581,7 +581,7 @@ void gemm_debug_set(int stages) { stages_override = stages; }
 
 cudaError_t launch_gemm(const Weight& W, const CUtensorMap* tmW, const void* X, long ldx,
                         const CUtensorMap* tmX, int Bt, const GemmPlan& p, const EpiParams& ep,
-                        const GemmScratch& sc, cudaStream_t st) {
+                        const GemmScratch& sc, cudaStream_t st, const void* pf, size_t pf_bytes) {
   if (Bt <= 0) return cudaSuccess;
   if (W.dtype_bytes == 4) {
     // fp32 storage: CUDA-core GEMM into fp32 staging, then the scalar epilogue
@@ -605,6 +605,8 @@ cudaError_t launch_gemm(const Weight& W, const CUtensorMap* tmW, const void* X, 
   gs.flags = sc.debug_flags;
   gs.trace = sc.trace;
   gs.BN = p.BN;
+  gs.pf = pf;
+  gs.pf_bytes = pf ? pf_bytes : 0;
   if (p.pair) return launch_pair(tmW, tmX, gs, p, ep, st);
   if (ep.ss_in && Bt > kMaxInvCols) return cudaErrorInvalidValue;
   switch (p.BN) {

@@ -50,6 +50,10 @@ struct GemmShape {
   int BN;               // pair kernel: batch columns per tile (multiple of 32, <= 256)
   int flags;            // diagnostics (GEMM_DBG_*), 0 in production
   unsigned long long* trace;  // diagnostics: per-CTA globaltimer stamps [grid][8] (nullptr = off)
+  // L2 prefetch of the NEXT kernel's leading weight bytes, issued by each CTA's producer once
+  // its own loads are all in flight (fills the HBM idle time of this kernel's tail)
+  const void* pf;
+  unsigned long long pf_bytes;
 };
 enum GemmDbg : int { GEMM_DBG_NO_MMA = 1, GEMM_DBG_NO_X = 2, GEMM_DBG_NO_HINT = 4, GEMM_DBG_NO_EPI = 8 };
 
@@ -65,6 +69,8 @@ struct AttnArgs {
   int B, H, Hkv, D, Dkv;
   float scale_log2;     // log2(e) / sqrt(DH)
   int flags;            // diagnostics: 1 = consumers release stages without computing
+  const void* pf;       // L2 prefetch of the next kernel's leading weight bytes (see GemmShape)
+  unsigned long long pf_bytes;
 };
 
 }  // namespace gh

@@ -129,13 +129,20 @@ struct gh_tier1 {
     return it->second;
   }
   // X: [B, K] with row stride ldx
+  // `next`: the weight the following Tier-1 kernel streams; its leading bytes are prefetched into
+  // L2 during this GEMM's tail (gemm_tc.cuh, GemmShape::pf)
   gh_status gemm(const Weight& W, const CUtensorMap* tmW, const void* X, long ldx, int B,
-                 const EpiParams& ep, cudaStream_t st) {
+                 const EpiParams& ep, cudaStream_t st, const Weight* next = nullptr) {
     const GemmPlan& p = plan(W.N, W.K, B);
     CUtensorMap* tmX = nullptr;
     if (sh.db == 2) GH_TRY(tmaps.get(X, (uint64_t)B, (uint64_t)W.K, (uint64_t)ldx, (uint32_t)p.x_box_rows(), &tmX));
-    GH_CUDA(launch_gemm(W, tmW, X, ldx, tmX, B, p, ep, gsc, st));
+    GH_CUDA(launch_gemm(W, tmW, X, ldx, tmX, B, p, ep, gsc, st, next ? next->ptr : nullptr, prefetch_bytes(next)));
     return GH_OK;
+  }
+  static size_t prefetch_bytes(const Weight* w) {
+    static const size_t cap = (size_t)(getenv("GH_PF_MB") ? atof(getenv("GH_PF_MB")) : 16.0) * (1 << 20);
+    if (!w || !w->ptr || w->dtype_bytes != 2) return 0;
+    return std::min(cap, w->elems() * 2);
   }
 };
 
@@ -294,6 +301,9 @@ gh_status gh_tier1_destroy(gh_tier1* t) {
 
 }  // extern "C"
 
+static gh_status t2_attend(gh_tier2* t, uint32_t layer, uint32_t B, const uint32_t* slot, const int32_t* pos,
+                           const void* msg_fwd, void* msg_bwd, void* stream, const void* pf, size_t pf_bytes);
+
 // ---- Tier-1 stage implementations.  `SsRef` describes per-slice sums of squares of an
 // activation buffer emitted by its producer (embedding / W2 epilogue) so that the consumer GEMM
 // applies RMSNorm in its epilogue (bf16 path) instead of a separate normalisation kernel.  The
@@ -357,7 +367,7 @@ static gh_status t1_post(gh_tier1* t, uint32_t layer, uint32_t B, const void* ms
   ep.out = t->h; ep.ldo = s.D;
   ep.resid = msg_bwd; ep.ldr = s.ld_bwd();
   if (fused) ep.ss_out = t->ss_h;
-  GH_TRY(t->gemm(L.o, &L.tm_o, (const char*)msg_bwd + (size_t)s.D * s.db, s.ld_bwd(), (int)B, ep, st));
+  GH_TRY(t->gemm(L.o, &L.tm_o, (const char*)msg_bwd + (size_t)s.D * s.db, s.ld_bwd(), (int)B, ep, st, &L.w13));
   // g = silu(rms(h) W1^T) * (rms(h) W3^T)
   const void* ffn_in = t->h;
   ep = epi_default();
@@ -370,7 +380,7 @@ static gh_status t1_post(gh_tier1* t, uint32_t layer, uint32_t B, const void* ms
     GH_CUDA(launch_rmsnorm(s.db, t->h, s.D, L.ffn_norm, t->hn, s.D, nullptr, 0, (int)B, s.D, s.s.norm_eps, st));
     ffn_in = t->hn;
   }
-  GH_TRY(t->gemm(L.w13, &L.tm_13, ffn_in, s.D, (int)B, ep, st));
+  GH_TRY(t->gemm(L.w13, &L.tm_13, ffn_in, s.D, (int)B, ep, st, &L.w2));
   // x_next = g W2^T + h   (+ sums of squares of x_next for the next fused norm)
   ep = epi_default();
   ep.kind = EPI_STORE_RESID;
@@ -380,7 +390,8 @@ static gh_status t1_post(gh_tier1* t, uint32_t layer, uint32_t B, const void* ms
     ep.ss_out = ss_next;
     if (ss_next_slices) *ss_next_slices = t->plan(s.D, s.Dh, (int)B).slices();
   }
-  return t->gemm(L.w2, &L.tm_2, t->g, s.Dh, (int)B, ep, st);
+  const Weight* next = layer + 1 < t->l1 ? &t->layers[layer + 1 - t->l0].qkv : (t->has_cls ? &t->cls : nullptr);
+  return t->gemm(L.w2, &L.tm_2, t->g, s.Dh, (int)B, ep, st, next);
 }
 
 static gh_status t1_classify(gh_tier1* t, uint32_t B, const void* x, SsRef ss, float* logits, int32_t* next,
@@ -401,7 +412,7 @@ static gh_status t1_classify(gh_tier1* t, uint32_t B, const void* x, SsRef ss, f
     GH_CUDA(launch_rmsnorm(s.db, x, s.D, t->final_norm, t->xn, s.D, nullptr, 0, (int)B, s.D, s.s.norm_eps, st));
     in = t->xn;
   }
-  GH_TRY(t->gemm(t->cls, &t->tm_cls, in, s.D, (int)B, ep, st));
+  GH_TRY(t->gemm(t->cls, &t->tm_cls, in, s.D, (int)B, ep, st, t->l1 > t->l0 ? &t->layers[0].qkv : nullptr));
   if (s.db == 2) {
     GH_CUDA(launch_argmax_final(t->part, t->plan(s.V, s.D, (int)B).slices(), (int)B, next, st));
   } else {
@@ -489,6 +500,14 @@ gh_status gh_tier2_check(const gh_tier2* t, uint32_t B, const uint32_t* slot, co
 
 gh_status gh_tier2_attend(gh_tier2* t, uint32_t layer, uint32_t B, const uint32_t* slot, const int32_t* pos,
                           const void* msg_fwd, void* msg_bwd, void* stream) {
+  return t2_attend(t, layer, B, slot, pos, msg_fwd, msg_bwd, stream, nullptr, 0);
+}
+}  // extern "C"
+
+// `pf`: leading bytes of the weight Tier-1 streams next on this GPU (colocated engine), prefetched
+// into L2 during the attention kernel's tail
+static gh_status t2_attend(gh_tier2* t, uint32_t layer, uint32_t B, const uint32_t* slot, const int32_t* pos,
+                           const void* msg_fwd, void* msg_bwd, void* stream, const void* pf, size_t pf_bytes) {
   if (!t || !slot || !pos || !msg_fwd || !msg_bwd) return fail(GH_EINVAL, "null argument");
   if (layer < t->l0 || layer >= t->l1) return fail(GH_EINVAL, "layer not owned by this Tier-2");
   if (B == 0) return GH_OK;
@@ -506,9 +525,13 @@ gh_status gh_tier2_attend(gh_tier2* t, uint32_t layer, uint32_t B, const uint32_
   a.scale_log2 = (float)(1.4426950408889634 / std::sqrt((double)s.dh));
   static const int attn_flags = getenv("GH_ATTN_FLAGS") ? atoi(getenv("GH_ATTN_FLAGS")) : 0;  // diagnostics
   a.flags = attn_flags;
+  a.pf = pf;
+  a.pf_bytes = pf ? pf_bytes : 0;
   GH_CUDA(launch_attention(s.db, s.dh, a, (cudaStream_t)stream));
   return GH_OK;
 }
+
+extern "C" {
 
 gh_status gh_tier2_fill_synthetic(gh_tier2* t, uint64_t seed, uint32_t n_fill, uint32_t npos, void* stream) {
   if (!t) return fail(GH_EINVAL, "null argument");
@@ -545,6 +568,8 @@ struct NcclApi {
   ncclResult_t (*Recv)(void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
   ncclResult_t (*GroupStart)() = nullptr;
   ncclResult_t (*GroupEnd)() = nullptr;
+  ncclResult_t (*AllGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*AllReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t, cudaStream_t) = nullptr;
   const char* (*GetErrorString)(ncclResult_t) = nullptr;
 };
 NcclApi& nccl() {
@@ -556,7 +581,7 @@ NcclApi& nccl() {
     if (!h) { api.why = std::string("dlopen libnccl.so.2 failed: ") + dlerror(); return; }
 #define GH_SYM(name) api.name = (decltype(api.name))dlsym(h, "nccl" #name); if (!api.name) { api.why = "missing nccl" #name; return; }
     GH_SYM(GetUniqueId) GH_SYM(CommInitRank) GH_SYM(CommDestroy) GH_SYM(Send) GH_SYM(Recv)
-    GH_SYM(GroupStart) GH_SYM(GroupEnd) GH_SYM(GetErrorString)
+    GH_SYM(GroupStart) GH_SYM(GroupEnd) GH_SYM(AllGather) GH_SYM(AllReduce) GH_SYM(GetErrorString)
 #undef GH_SYM
     api.ok = true;
   });
@@ -647,7 +672,26 @@ struct gh_engine {
   std::vector<int> shard_off, shard_cnt;  // split mode: per Tier-2 rank
   int my_cnt = 0;                         // tier2: prompts of my shard per batch
   cudaEvent_t fork = nullptr;
+  // Peer transport (split mode, pipelined step): messages are written straight into the
+  // receiving GPU's buffers over NVLink by copy engines (CUDA IPC mappings of the peer's
+  // cudaMalloc buffers), and completion is a sequence number written into the receiver's flag
+  // word after the copy (cuStreamWriteValue32) and awaited by the receiver's compute stream
+  // (cuStreamWaitValue32) -- no SM time and no NCCL kernel on either side.
+  struct Peer {
+    bool on = false;
+    uint32_t* flags = nullptr;                // mine: tier1 [IF][K'] bwd arrivals, tier2 [IF] fwd arrivals
+    std::vector<std::vector<void*>> fwd, pos; // tier1: [j][ib] Tier-2 rank j's fwd / pos buffers
+    std::vector<uint32_t*> rflags;            // tier1: [j] Tier-2 rank j's flags; tier2: [0] Tier-1's
+    std::vector<void*> bwd;                   // tier2: [ib] Tier-1's bwd buffers
+    std::vector<cudaStream_t> cs;             // copy streams (tier1: one per Tier-2 rank; tier2: one)
+    std::vector<cudaEvent_t> ev;              // per batch: message produced on the compute stream
+    std::vector<uint32_t> seq;                // per batch: messages exchanged so far (both directions)
+    std::vector<void*> opened;                // IPC mappings
+  } peer;
   ~gh_engine() {
+    for (void* p : peer.opened) cudaIpcCloseMemHandle(p);
+    for (auto s : peer.cs) cudaStreamDestroy(s);
+    for (auto v : peer.ev) cudaEventDestroy(v);
     for (auto& b : batches) {
       if (b.graph) cudaGraphExecDestroy(b.graph);
       if (b.stream) cudaStreamDestroy(b.stream);
@@ -680,13 +724,16 @@ static gh_status act_classify(gh_engine* e, gh_engine::Batch& b, float* logits, 
   return t1_classify(e->t1, e->cfg.batch, b.x(b.cur), SsRef{b.ss(b.cur), b.ss_slices[b.cur]}, logits, b.next, st);
 }
 
+extern "C" { static gh_status peer_setup(gh_engine* e); }
+
 static gh_status engine_layer_loop_colocated(gh_engine* e, gh_engine::Batch& b, bool want_logits, cudaStream_t st) {
   const Shape& s = e->sh;
   const uint32_t B = e->cfg.batch;
   GH_TRY(act_embed(e, b, st));
   for (int l = 0; l < s.N; ++l) {
     GH_TRY(act_pre(e, b, l, st));
-    GH_TRY(gh_tier2_attend(e->t2, l, B, b.slot, b.pos, b.fwd, b.bwd, st));
+    const Weight& wo = e->t1->layers[l].o;
+    GH_TRY(t2_attend(e->t2, l, B, b.slot, b.pos, b.fwd, b.bwd, st, wo.ptr, gh_tier1::prefetch_bytes(&wo)));
     GH_TRY(act_post(e, b, l, st));
   }
   return act_classify(e, b, want_logits ? b.logits : nullptr, st);
@@ -759,8 +806,16 @@ gh_status gh_engine_create(const gh_engine_config* cfg, gh_comm* comm, gh_engine
     GH_CUDA(cudaEventCreateWithFlags(&b.done, cudaEventDisableTiming));
   }
   GH_CUDA(cudaDeviceSynchronize());
+  if (e->role != 0 && cfg->transport != GH_TRANSPORT_NCCL) GH_TRY(peer_setup(e.get()));
+  if (cfg->transport == GH_TRANSPORT_PEER && e->role != 0 && !e->peer.on)
+    return fail(GH_EUNSUPPORTED, "peer transport requested but not available on every rank");
   *out = e.release();
   return GH_OK;
+}
+
+int gh_engine_transport(const gh_engine* e) {
+  if (!e || e->role == 0) return -1;
+  return e->peer.on ? GH_TRANSPORT_PEER : GH_TRANSPORT_NCCL;
 }
 
 gh_status gh_engine_destroy(gh_engine* e) {
@@ -924,7 +979,189 @@ static gh_status t2_group(gh_engine* e, ncclComm_t comm, cudaStream_t st, int se
   return GH_OK;
 }
 
+// ---- peer transport (see gh_engine::Peer)
+namespace {
+typedef CUresult (*PFN_streamValue32)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
+struct MemOps {
+  PFN_streamValue32 wait = nullptr, write = nullptr;
+};
+MemOps& memops() {
+  static MemOps m;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuStreamWaitValue32", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      m.wait = (PFN_streamValue32)p;
+    if (cudaGetDriverEntryPoint("cuStreamWriteValue32", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      m.write = (PFN_streamValue32)p;
+  });
+  return m;
+}
+}  // namespace
+
+#define GH_CU(call)                                                                           \
+  do {                                                                                        \
+    CUresult r_ = (call);                                                                     \
+    if (r_ != CUDA_SUCCESS) return fail(GH_ECUDA, std::string(#call) + " failed: " + std::to_string((int)r_)); \
+  } while (0)
+
+// Collective over all ranks of the engine's communicator: export this rank's receive buffers as
+// CUDA IPC handles, all-gather them, map the peers' buffers.  The transport is enabled only if
+// every rank mapped every buffer it needs (all-reduce min of the outcome), so all ranks agree.
+static gh_status peer_setup(gh_engine* e) {
+  auto& api = nccl();
+  auto& P = e->peer;
+  const int IF = (int)e->batches.size(), kp = e->kp, world = kp + 1, rank = e->comm->rank;
+  const int nslot = 1 + 3 * IF;
+  ncclComm_t comm = e->comm->comms[0];
+  void* p;
+  GH_TRY(dev_alloc(e->mem, (size_t)IF * std::max(kp, 1) * 4, &p));
+  P.flags = (uint32_t*)p;
+  GH_CUDA(cudaMemset(P.flags, 0, (size_t)IF * std::max(kp, 1) * 4));
+  std::vector<cudaIpcMemHandle_t> mine(nslot);
+  memset(mine.data(), 0, nslot * sizeof(cudaIpcMemHandle_t));
+  int ok = memops().wait && memops().write;
+  auto get = [&](int i, void* ptr) { if (cudaIpcGetMemHandle(&mine[i], ptr) != cudaSuccess) { cudaGetLastError(); ok = 0; } };
+  get(0, P.flags);
+  for (int ib = 0; ib < IF; ++ib) {
+    auto& b = e->batches[ib];
+    if (e->role == 2) { get(1 + ib, b.fwd); get(1 + IF + ib, b.pos); }
+    else get(1 + 2 * IF + ib, b.bwd);
+  }
+  const size_t rec = nslot * sizeof(cudaIpcMemHandle_t);
+  void *dmine, *dall, *dok;
+  GH_TRY(dev_alloc(e->mem, rec, &dmine));
+  GH_TRY(dev_alloc(e->mem, rec * world, &dall));
+  GH_TRY(dev_alloc(e->mem, 4, &dok));
+  cudaStream_t st;
+  GH_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+  GH_CUDA(cudaMemcpy(dmine, mine.data(), rec, cudaMemcpyHostToDevice));
+  GH_NCCL(api.AllGather(dmine, dall, rec, ncclUint8, comm, st));
+  GH_CUDA(cudaStreamSynchronize(st));
+  std::vector<cudaIpcMemHandle_t> all((size_t)nslot * world);
+  GH_CUDA(cudaMemcpy(all.data(), dall, rec * world, cudaMemcpyDeviceToHost));
+  auto open = [&](int r, int i) -> void* {
+    void* q = nullptr;
+    if (!ok) return nullptr;
+    if (cudaIpcOpenMemHandle(&q, all[(size_t)r * nslot + i], cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) {
+      cudaGetLastError();
+      ok = 0;
+      return nullptr;
+    }
+    P.opened.push_back(q);
+    return q;
+  };
+  if (e->role == 1) {
+    P.fwd.assign(kp, std::vector<void*>(IF, nullptr));
+    P.pos.assign(kp, std::vector<void*>(IF, nullptr));
+    for (int j = 0; j < kp; ++j) {
+      P.rflags.push_back((uint32_t*)open(j + 1, 0));
+      for (int ib = 0; ib < IF; ++ib) { P.fwd[j][ib] = open(j + 1, 1 + ib); P.pos[j][ib] = open(j + 1, 1 + IF + ib); }
+    }
+  } else {
+    P.rflags.push_back((uint32_t*)open(0, 0));
+    for (int ib = 0; ib < IF; ++ib) P.bwd.push_back(open(0, 1 + 2 * IF + ib));
+  }
+  (void)rank;
+  GH_CUDA(cudaMemcpy(dok, &ok, 4, cudaMemcpyHostToDevice));
+  GH_NCCL(api.AllReduce(dok, dok, 1, ncclInt32, ncclMin, comm, st));
+  GH_CUDA(cudaStreamSynchronize(st));
+  GH_CUDA(cudaMemcpy(&ok, dok, 4, cudaMemcpyDeviceToHost));
+  cudaStreamDestroy(st);
+  if (!ok) {
+    for (void* q : P.opened) cudaIpcCloseMemHandle(q);
+    P.opened.clear();
+    return GH_OK;  // NCCL send/recv transport
+  }
+  const int ncs = e->role == 1 ? kp : 1;
+  for (int j = 0; j < ncs; ++j) {
+    cudaStream_t c;
+    GH_CUDA(cudaStreamCreateWithFlags(&c, cudaStreamNonBlocking));
+    P.cs.push_back(c);
+  }
+  for (int ib = 0; ib < IF; ++ib) {
+    cudaEvent_t v;
+    GH_CUDA(cudaEventCreateWithFlags(&v, cudaEventDisableTiming));
+    P.ev.push_back(v);
+  }
+  P.seq.assign(IF, 0);
+  P.on = true;
+  return GH_OK;
+}
+
+// Tier-1: copy batch ib's fwd message shards (and, at the first layer of a step, its positions)
+// into every Tier-2 rank's buffers, then publish the sequence number in that rank's flag word.
+static gh_status peer_send_fwd(gh_engine* e, int ib, bool with_pos, cudaStream_t st) {
+  auto& P = e->peer;
+  auto& b = e->batches[ib];
+  const size_t fwd_row = (size_t)e->sh.ld_fwd() * e->sh.db;
+  const uint32_t sq = ++P.seq[ib];
+  GH_CUDA(cudaEventRecord(P.ev[ib], st));
+  for (int j = 0; j < e->kp; ++j) {
+    cudaStream_t c = P.cs[j];
+    GH_CUDA(cudaStreamWaitEvent(c, P.ev[ib], 0));
+    if (with_pos)
+      GH_CUDA(cudaMemcpyAsync(P.pos[j][ib], b.pos + e->shard_off[j], (size_t)e->shard_cnt[j] * 4, cudaMemcpyDeviceToDevice, c));
+    GH_CUDA(cudaMemcpyAsync(P.fwd[j][ib], (char*)b.fwd + e->shard_off[j] * fwd_row, e->shard_cnt[j] * fwd_row,
+                            cudaMemcpyDeviceToDevice, c));
+    GH_CU(memops().write((CUstream)c, (CUdeviceptr)(P.rflags[j] + ib), sq, CU_STREAM_WRITE_VALUE_DEFAULT));
+  }
+  return GH_OK;
+}
+
+static gh_status split_step_peer(gh_engine* e, cudaStream_t st) {
+  auto& P = e->peer;
+  // diagnostics: GH_SPLIT_NOWAIT=1 drops the flag waits (wrong results; isolates compute time)
+  static const bool nowait = getenv("GH_SPLIT_NOWAIT") != nullptr;
+  const int nb = (int)e->batches.size();
+  const int N = e->sh.N;
+  if (e->role == 1) {
+    for (int ib = 0; ib < nb; ++ib) {
+      auto& b = e->batches[ib];
+      GH_TRY(act_embed(e, b, st));
+      GH_TRY(act_pre(e, b, 0, st));
+      GH_TRY(peer_send_fwd(e, ib, true, st));
+    }
+    for (int l = 0; l < N; ++l)
+      for (int ib = 0; ib < nb; ++ib) {
+        auto& b = e->batches[ib];
+        for (int j = 0; j < e->kp && !nowait; ++j)  // every shard of the attention output has landed
+          GH_CU(memops().wait((CUstream)st, (CUdeviceptr)(P.flags + ib * e->kp + j), P.seq[ib],
+                              CU_STREAM_WAIT_VALUE_GEQ));
+        GH_TRY(act_post(e, b, l, st));
+        if (l + 1 < N) {
+          GH_TRY(act_pre(e, b, l + 1, st));
+          GH_TRY(peer_send_fwd(e, ib, false, st));
+        } else {
+          GH_TRY(act_classify(e, b, nullptr, st));
+        }
+      }
+  } else {
+    const size_t bwd_row = (size_t)e->sh.ld_bwd() * e->sh.db;
+    const int me = e->comm->rank - 1;
+    for (int l = 0; l < N; ++l)
+      for (int ib = 0; ib < nb; ++ib) {
+        auto& b = e->batches[ib];
+        const uint32_t sq = ++P.seq[ib];
+        if (!nowait) GH_CU(memops().wait((CUstream)st, (CUdeviceptr)(P.flags + ib), sq, CU_STREAM_WAIT_VALUE_GEQ));
+        GH_TRY(gh_tier2_attend(e->t2, l, e->my_cnt, b.slot, b.pos, b.fwd, b.bwd, st));
+        GH_CUDA(cudaEventRecord(P.ev[ib], st));
+        cudaStream_t c = P.cs[0];
+        GH_CUDA(cudaStreamWaitEvent(c, P.ev[ib], 0));
+        GH_CUDA(cudaMemcpyAsync((char*)P.bwd[ib] + e->shard_off[me] * bwd_row, b.bwd, e->my_cnt * bwd_row,
+                                cudaMemcpyDeviceToDevice, c));
+        GH_CU(memops().write((CUstream)c, (CUdeviceptr)(P.rflags[0] + ib * e->kp + me), sq,
+                             CU_STREAM_WRITE_VALUE_DEFAULT));
+      }
+  }
+  return GH_OK;
+}
+
 static gh_status split_step_pipelined(gh_engine* e, cudaStream_t st) {
+  if (e->peer.on) return split_step_peer(e, st);
   const int nb = (int)e->batches.size();
   const int N = e->sh.N;
   ncclComm_t comm = e->comm->comms[0];

@@ -146,15 +146,17 @@ class Comm:
 
 class Engine:
     """One decode step over all layers: colocated (1 GPU) or tier split (rank 0 Tier-1,
-    ranks 1.. Tier-2, NCCL send/recv of the PayloadModel messages every layer)."""
+    ranks 1.. Tier-2, PayloadModel messages every layer over peer copies or NCCL send/recv)."""
 
     ROLES = {0: "colocated", 1: "tier1", 2: "tier2"}
+    TRANSPORTS = {"auto": 0, "nccl": 1, "peer": 2}
 
     def __init__(self, spec: ModelSpec, batch: int, inflight: int = 1, device: int = 0,
                  weight_seed: int = 1234, n_slots: int = 0, use_graph: bool = True,
-                 comm: Comm | None = None):
+                 comm: Comm | None = None, transport: str = "auto"):
         self.spec, self.batch, self.inflight = spec, batch, inflight
-        cfg = L.GhEngineConfig(spec.c(), device, weight_seed, batch, inflight, n_slots, int(use_graph))
+        cfg = L.GhEngineConfig(spec.c(), device, weight_seed, batch, inflight, n_slots, int(use_graph),
+                               self.TRANSPORTS[transport])
         h = C.c_void_p()
         L.check(L.lib().gh_engine_create(C.byref(cfg), comm.h if comm else None, C.byref(h)))
         self.h = h
@@ -168,6 +170,12 @@ class Engine:
             self.h = None
 
     __del__ = close
+
+    @property
+    def transport(self) -> str | None:
+        """Inter-tier transport of the pipelined step ("nccl" / "peer"), None when colocated."""
+        t = L.lib().gh_engine_transport(self.h)
+        return {1: "nccl", 2: "peer"}.get(t)
 
     @property
     def tier2(self) -> int:

@@ -93,7 +93,7 @@ def test_nccl_tier_split_matches_colocated(world):
     assert np.array_equal(lg, rlg)
 
 
-def worker_all(rank, world, port, q, IF):
+def worker_all(rank, world, port, q, IF, transport="auto"):
     """step_all (pipelined, all in-flight batches) + advance for STEPS steps."""
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     import torch
@@ -106,9 +106,11 @@ def worker_all(rank, world, port, q, IF):
         obj = [Comm.unique_ids(1) if rank == 0 else None]
         dist.broadcast_object_list(obj, src=0)
         comm = Comm(obj[0], world, rank, rank)
-    out = run_all(Engine(SPEC, batch=B, inflight=IF, device=rank, use_graph=False, comm=comm), IF)
+    eng = Engine(SPEC, batch=B, inflight=IF, device=rank, use_graph=False, comm=comm, transport=transport)
+    used = eng.transport
+    out = run_all(eng, IF)
     if rank == 0:
-        q.put(out)
+        q.put((out, used))
     dist.barrier()
     dist.destroy_process_group()
 
@@ -131,8 +133,11 @@ def run_all(eng, IF):
 
 
 @pytest.mark.skipif(n_gpus() < 2, reason="needs >= 2 GPUs")
+@pytest.mark.parametrize("transport", ["nccl", "peer"])
 @pytest.mark.parametrize("world,IF", [(2, 2), (3, 2), (2, 3)])
-def test_pipelined_step_all_matches_colocated(world, IF):
+def test_pipelined_step_all_matches_colocated(world, IF, transport):
+    """Pipelined step_all over NCCL send/recv and over the peer-copy transport (CUDA IPC +
+    copy engines + stream-ordered flags): tokens identical to the colocated engine."""
     if n_gpus() < world:
         pytest.skip(f"needs {world} GPUs")
     import torch.multiprocessing as mp
@@ -143,10 +148,11 @@ def test_pipelined_step_all_matches_colocated(world, IF):
     s.close()
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
-    procs = [ctx.Process(target=worker_all, args=(r, world, port, q, IF)) for r in range(world)]
+    procs = [ctx.Process(target=worker_all, args=(r, world, port, q, IF, transport)) for r in range(world)]
     for p in procs:
         p.start()
-    got = q.get(timeout=600)
+    got, used = q.get(timeout=600)
+    assert used == transport
     for p in procs:
         p.join(timeout=120)
         assert p.exitcode == 0
