@@ -97,10 +97,14 @@ constexpr int kMaxInvCols = 256;  // batch columns whose fused-RMSNorm scale is 
 // 1/rms of every batch column of the GEMM input, from the producer's per-slice sums of squares
 // (summed in slice order: deterministic).  Run once per CTA by the epilogue warps.
 GH_DEV void compute_inv_rms(const EpiParams& ep, const GemmShape& gs, float* inv) {
-  for (int b = threadIdx.x - 64; b < gs.Bt; b += 128) {
+  const float* __restrict__ ssp = ep.ss_in;
+  const int ns = ep.ss_in_slices, Bt = gs.Bt;
+  const float dim = (float)ep.ss_dim, eps = ep.ss_eps;
+  for (int b = threadIdx.x - 64; b < Bt; b += 128) {
     float ss = 0.f;
-    for (int s = 0; s < ep.ss_in_slices; ++s) ss += __ldg(ep.ss_in + (long)s * gs.Bt + b);
-    inv[b] = 1.0f / sqrtf(ss / (float)ep.ss_dim + ep.ss_eps);
+#pragma unroll 8
+    for (int s = 0; s < ns; ++s) ss += __ldg(ssp + (long)s * Bt + b);  // slice order: deterministic
+    inv[b] = 1.0f / sqrtf(ss / dim + eps);
   }
 }
 

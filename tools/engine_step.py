@@ -9,7 +9,8 @@ from pathlib import Path
 import numpy as np
 import torch
 
-sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
+import os  # noqa: E402
+sys.path.insert(0, os.environ.get("GH_PKG_ROOT") or str(Path(__file__).resolve().parents[1]))
 import paper_2501_11779_b200 as gh  # noqa: E402
 from paper_2501_11779_b200 import _lib as L  # noqa: E402
 from paper_2501_11779_b200.stages import Engine  # noqa: E402
