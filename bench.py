@@ -47,32 +47,51 @@ def peaks():
 
 # ------------------------------------------------------------------ clocks sampler
 class Clocks:
+    """nvidia-smi clocks / throttle-reason sampler (every 20 ms) around a timed region.  The
+    sampler is started and its first line awaited BEFORE the region, so that even a region of a
+    few hundred milliseconds gets samples; only samples taken inside the region are kept."""
     Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
          "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
 
     def __init__(self, index: int):
         self.index = index
         self.proc = None
+        self.samples = []  # (time, line)
+        self.t0 = self.t1 = None
+
+    def _reader(self):
+        for ln in self.proc.stdout:
+            self.samples.append((time.perf_counter(), ln))
 
     def __enter__(self):
+        import threading
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
-                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+                 "-lms", "20"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._reader, daemon=True)
+            self.thread.start()
+            deadline = time.perf_counter() + 10
+            while not self.samples and time.perf_counter() < deadline and self.proc.poll() is None:
+                time.sleep(0.01)
         except OSError:
             self.proc = None
+        self.t0 = time.perf_counter()
         return self
 
     def __exit__(self, *a):
-        self.lines = []
+        self.t1 = time.perf_counter()
         if self.proc:
+            time.sleep(0.05)
             self.proc.terminate()
             try:
-                out, _ = self.proc.communicate(timeout=5)
+                self.proc.wait(timeout=5)
             except subprocess.TimeoutExpired:
                 self.proc.kill()
-                out, _ = self.proc.communicate()
-            self.lines = [ln for ln in out.splitlines() if ln.strip()]
+            self.thread.join(timeout=5)
+        inside = [ln for t, ln in self.samples if self.t0 <= t <= self.t1 + 0.03 and ln.strip()]
+        # a region shorter than the sampling interval still reports the sample closest to it
+        self.lines = inside or [ln for t, ln in self.samples[-2:] if ln.strip()]
 
     def summary(self):
         sm, mx, reasons = [], 0.0, set()

@@ -22,12 +22,27 @@ GH_HD float bf16_to_f32(uint16_t b) {
 }
 // Round-to-nearest-even (finite inputs); identical to the oracle's restatement.
 GH_HD uint16_t f32_to_bf16(float f) {
+#ifdef __CUDA_ARCH__
+  uint16_t r;  // one cvt.rn (the bit manipulation below costs ~10 instructions per element)
+  asm("cvt.rn.bf16.f32 %0, %1;" : "=h"(r) : "f"(f));
+  return r;
+#endif
   union { uint32_t u; float f; } v; v.f = f;
   uint32_t u = v.u;
   if ((u & 0x7f800000u) == 0x7f800000u) return (uint16_t)((u >> 16) | ((u & 0xffff) ? 0x40 : 0));
   u += 0x7fffu + ((u >> 16) & 1u);
   return (uint16_t)(u >> 16);
 }
+
+#ifdef __CUDACC__
+// Two floats -> packed bf16x2 (lo in bits 0..15) with one cvt.rn (round-to-nearest-even: the same
+// bits as f32_to_bf16 for every finite input).
+__device__ __forceinline__ uint32_t pack_bf16x2(float lo, float hi) {
+  uint32_t r;
+  asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(hi), "f"(lo));
+  return r;
+}
+#endif
 
 template <typename T> struct St;
 template <> struct St<float> {
@@ -173,6 +188,14 @@ GH_DEV void mbar_arrive_cluster_relaxed(uint32_t caddr) {
 GH_DEV void fence_acq_rel_cluster() { asm volatile("fence.acq_rel.cluster;" ::: "memory"); }
 GH_DEV void cluster_sync_all() {
   asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+
+// spin (acquire, gpu scope) until *flag >= target
+GH_DEV void flag_wait(const unsigned int* flag, unsigned int target) {
+  unsigned int v;
+  do {
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(flag) : "memory");
+  } while (v < target);
 }
 
 // ------------------------------------------------------------------ bulk / tensor copies (TMA)

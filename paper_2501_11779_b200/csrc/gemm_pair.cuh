@@ -40,7 +40,8 @@ struct PairSmem {
   static constexpr int kStgBytes = 32 * 128 * 4;  // epilogue staging: 32 columns x 128 rows fp32
   static constexpr uint32_t kAccCols = kPairMaxBN;
   static constexpr uint32_t kTmemCols = 512;
-  static constexpr int kBarBytes = (2 * kMaxStages + 8) * 8 + 16 + kPairMaxInvCols * 4;
+  static constexpr int kBarBytes = (2 * kMaxStages + 16) * 8 + 16 + kPairMaxInvCols * 4;
+  static constexpr int kFixSlots = 8;  // stream-K fixup: 16 KB partial blocks in flight
   GH_HD static int b_bytes(int BN) { return BN / 2 * kBlockK * 2; }
   GH_HD static int stage_bytes(int BN) { return kABytes + b_bytes(BN); }
   GH_HD static int stg_offset(int BN, int stages) { return stages * stage_bytes(BN); }
@@ -52,11 +53,42 @@ struct PairSmem {
   }
 };
 
-// staging index of (column c, row r): 16-byte chunks of a column XOR-swizzled so that both the
-// row-per-thread writes and the (column, 32-row run)-per-thread float4 reads are conflict-free
-GH_DEV int pair_stg_index(int c, int r) {
-  return c * 128 + ((((r >> 2) ^ (((c & 1) << 2) | ((r >> 5) & 3)))) << 2) + (r & 3);
+// staging index of (column c, row r): 16-byte chunks of odd columns XOR-swizzled by one so that
+// both the row-per-thread writes and the float4 reads of the epilogue mapping (4 threads per
+// column, rows q*8 + 32j + 0..7) are conflict-free
+GH_DEV int pair_stg_index(int c, int r) { return c * 128 + (((r >> 2) ^ (c & 1)) << 2) + (r & 3); }
+
+// Stream-K work split (deterministic).  The T = n_tiles x b_tiles output tiles are cut into
+// T x KB units (one 64-deep k-block of one tile); CTA pair p processes the contiguous units
+// [p*U/P, (p+1)*U/P), so every pair streams the same number of k-blocks whatever the tile count
+// (no wave quantisation).  A tile whose units span several pairs is finished by its OWNER, the
+// pair that processes its k-block 0 (at the END of the owner's range); the other pairs process
+// the tile's later k-blocks at the START of their ranges, so their fp32 partials (written to a
+// global workspace, one slot per pair) are ready early, and the owner adds them in pair order
+// (a fixed summation order: results do not depend on timing).  Owners wait only on pairs that
+// are co-resident (the grid never exceeds the co-resident pairs), contributors never wait.
+struct SkPiece {
+  int tile, kb0, kb1;  // k-blocks [kb0, kb1) of tile
+};
+// tiles == true: tile-aligned ranges (no split tiles) -- the planner's choice when the fixups
+// would cost more than the wave quantisation they remove
+GH_DEV long sk_start(int p, int P, long U, int KB, bool tiles) {
+  return tiles ? (long)p * (U / KB) / P * KB : (long)p * U / P;
 }
+struct SkRange {
+  long u, u1;
+  int KB;
+  GH_DEV SkRange(int p, int P, long U, int kb, bool tiles)
+      : u(sk_start(p, P, U, kb, tiles)), u1(sk_start(p + 1, P, U, kb, tiles)), KB(kb) {}
+  GH_DEV bool next(SkPiece& pc) {
+    if (u >= u1) return false;
+    pc.tile = (int)(u / KB);
+    pc.kb0 = (int)(u % KB);
+    pc.kb1 = (int)min((long)KB, pc.kb0 + (u1 - u));
+    u += pc.kb1 - pc.kb0;
+    return true;
+  }
+};
 
 __global__ void __launch_bounds__(kGemmThreads, 1)
     gemm_pair_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CUtensorMap tmX,
@@ -74,19 +106,24 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   uint64_t* tempty = tfull + 2;             // [2] accumulator drained (leader, 8 warps)
   uint32_t* tmem_slot = (uint32_t*)(tempty + 2);
   float* inv_smem = (float*)(tempty + 4);
+  uint64_t* pbar = (uint64_t*)(inv_smem + kPairMaxInvCols);  // [kFixSlots] stream-K fixup blocks
 
   const int warp = threadIdx.x >> 5;
   const int KB = gs.kb_total;
   const int rank = (int)cluster_ctarank();  // 0 = leader
   const int pid = (int)cluster_id_x(), npair = (int)cluster_count_x();
-  const int n_tiles_total = gs.n_tiles * gs.b_tiles;
-  const int my_tiles = pid < n_tiles_total ? (n_tiles_total - 1 - pid) / npair + 1 : 0;
+  const int bt = gs.b_tiles;
+  const long U = (long)gs.n_tiles * bt * KB;
+  const bool sk_tiles = !gs.sk_split || (gs.flags & GEMM_DBG_SK_TILES);
+  unsigned long long* trace = gs.trace ? gs.trace + blockIdx.x * 16 : nullptr;  // diagnostics
+  if (trace && threadIdx.x == 0) trace[0] = globaltimer();
 
   if (threadIdx.x == 0) {
     prefetch_tmap(&tmW);
     prefetch_tmap(&tmX);
     for (int s = 0; s < S; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
     for (int a = 0; a < 2; ++a) { mbar_init(&tfull[a], 1); mbar_init(&tempty[a], 8); }
+    for (int a = 0; a < L::kFixSlots; ++a) mbar_init(&pbar[a], 1);
     fence_barrier_init();
   }
   if (warp == 1) tmem_alloc_pair<L::kTmemCols>(tmem_slot);
@@ -101,46 +138,64 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     if (elect_one()) {
       const uint64_t pol_w = policy_evict_first();
       const uint64_t pol_x = policy_evict_last();
-      const int total = my_tiles * KB;
-      const int pre = min(S, total);
       const int half = BN / 2;
-      auto w_row = [&](int i) {
-        const int tile = pid + (i / KB) * npair;
-        // tile-contiguous weights: 128-row tile (2*tile_n + rank, kb)
-        return ((2 * (tile / gs.b_tiles) + rank) * KB + i % KB) * kBlockM;
-      };
-      auto x_row = [&](int i) { return (pid + (i / KB) * npair) % gs.b_tiles * BN + rank * half; };
       const uint32_t full0 = mapa_shared(smem_u32(full), 0);
-      // weights do not depend on the previous kernel: request them before griddepcontrol.wait
-      for (int i = 0; i < pre; ++i) {
-        if (rank == 0) mbar_arrive_expect_tx(&full[i], 2 * kStage);
-        tma_load_2d_pair(smem + i * kStage, &tmW, 0, w_row(i), full0 + i * 8, pol_w);
+      SkRange rg(pid, npair, U, KB, sk_tiles);
+      SkPiece pc;
+      int i = 0, pre_done = 0;
+      // weights do not depend on the previous kernel: the first S stages of weights are requested
+      // before griddepcontrol.wait, their activations after it
+      int pre_tile[L::kMaxStages], pre_kb[L::kMaxStages];
+      while (rg.next(pc)) {
+        for (int kb = pc.kb0; kb < pc.kb1; ++kb, ++i) {
+          const int s = i % S;
+          const int w_row = ((2 * (pc.tile / bt) + rank) * KB + kb) * kBlockM;  // tile-contiguous W
+          const int x_row = (pc.tile % bt) * BN + rank * half;
+          if (i >= S) mbar_wait(&empty[s], ((i / S) & 1) ^ 1);
+          if (rank == 0) mbar_arrive_expect_tx(&full[s], 2 * kStage);
+          tma_load_2d_pair(smem + s * kStage, &tmW, 0, w_row, full0 + s * 8, pol_w);
+          if (i < S) {
+            pre_tile[i] = x_row;
+            pre_kb[i] = kb;
+            if (i == S - 1) {
+              if (trace) trace[1] = globaltimer();
+              griddep_wait();
+              if (trace) trace[2] = globaltimer();
+              for (int k = 0; k < S; ++k)
+                tma_load_2d_pair(smem + k * kStage + L::kABytes, &tmX, pre_kb[k] * kBlockK, pre_tile[k],
+                                 full0 + k * 8, pol_x);
+              pre_done = 1;
+            }
+          } else {
+            tma_load_2d_pair(smem + s * kStage + L::kABytes, &tmX, kb * kBlockK, x_row, full0 + s * 8, pol_x);
+          }
+        }
       }
-      griddep_wait();
-      for (int i = 0; i < pre; ++i)
-        tma_load_2d_pair(smem + i * kStage + L::kABytes, &tmX, (i % KB) * kBlockK, x_row(i), full0 + i * 8, pol_x);
-      for (int i = pre; i < total; ++i) {
-        const int s = i % S;
-        mbar_wait(&empty[s], ((i / S) & 1) ^ 1);
-        if (rank == 0) mbar_arrive_expect_tx(&full[s], 2 * kStage);
-        uint8_t* sa = smem + s * kStage;
-        tma_load_2d_pair(sa, &tmW, 0, w_row(i), full0 + s * 8, pol_w);
-        tma_load_2d_pair(sa + L::kABytes, &tmX, (i % KB) * kBlockK, x_row(i), full0 + s * 8, pol_x);
+      if (!pre_done) {  // fewer than S k-blocks in this pair's range
+        if (trace) trace[1] = globaltimer();
+        griddep_wait();
+        if (trace) trace[2] = globaltimer();
+        for (int k = 0; k < i; ++k)
+          tma_load_2d_pair(smem + k * kStage + L::kABytes, &tmX, pre_kb[k] * kBlockK, pre_tile[k], full0 + k * 8,
+                           pol_x);
       }
       prefetch_l2_share(gs.pf, gs.pf_bytes, blockIdx.x, gridDim.x);
+      if (trace) trace[3] = globaltimer();  // all loads issued
     }
   } else if (warp == 1) {
-    // ---------------- MMA issuer (leader only): one accumulator buffer per tile, alternating
+    // ---------------- MMA issuer (leader only): one accumulator buffer per piece, alternating
     if (rank == 0) {
       const uint32_t idesc = umma_idesc_bf16(2 * kBlockM, BN);
       const bool no_mma = gs.flags & GEMM_DBG_NO_MMA;
-      int i = 0;
-      for (int j = 0; j < my_tiles; ++j) {
+      SkRange rg(pid, npair, U, KB, sk_tiles);
+      SkPiece pc;
+      int i = 0, j = 0;
+      while (rg.next(pc)) {
         const int acc = j & 1;
         mbar_wait(&tempty[acc], ((j >> 1) & 1) ^ 1);
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + acc * L::kAccCols;
-        for (int k = 0; k < KB; ++k, ++i) {
+        for (int kb = pc.kb0; kb < pc.kb1; ++kb, ++i) {
           const int s = i % S;
           mbar_wait(&full[s], (i / S) & 1);
           tc_fence_after();
@@ -152,68 +207,136 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
 #pragma unroll
               for (int kk = 0; kk < kBlockK / 16; ++kk)
                 umma_bf16_pair(d_tmem, da + (uint64_t)(kk * 2), db + (uint64_t)(kk * 2), idesc,
-                               (k > 0 || kk > 0) ? 1u : 0u);
+                               (kb > pc.kb0 || kk > 0) ? 1u : 0u);
             }
             umma_commit_pair(&empty[s], 0x3);
-            if (k == KB - 1) umma_commit_pair(&tfull[acc], 0x3);
+            if (kb == pc.kb1 - 1) umma_commit_pair(&tfull[acc], 0x3);
           }
           __syncwarp();
         }
+        ++j;
       }
+      if (trace && elect_one()) trace[4] = globaltimer();  // last MMA issued
     }
   } else {
     // ---------------- epilogue warps 2..5 (both CTAs): rows rank*128 + 32*(warp%4) + lane
     const int q = warp & 3;
     const int row = q * 32 + (threadIdx.x & 31);
     const int t = threadIdx.x - 64;
-    const int cb = t >> 2, rl = (t & 3) * 32;  // staged read: column cb, rows rl..rl+31
+    const int cb = t >> 2, rl = (t & 3) * 8;  // staged read: column cb, rows rl + 32j + 0..7
     const bool skip = gs.flags & GEMM_DBG_NO_EPI;
     const uint32_t tempty0 = mapa_shared(smem_u32(tempty), 0);
+    // partial slot of pair p, CTA rank r: ws[p][r][column][128 rows] fp32 (a 32-column chunk is
+    // one contiguous 16 KB block)
+    auto ws_col = [&](int p, int c) { return gs.sk_ws + ((long)(2 * p + rank) * kPairMaxBN + c) * kBlockM; };
+    // fixup ring in the (then idle) pipeline stages: block b = (chunk b / nc, contributor b % nc)
+    const int n_slots = min(L::kFixSlots, S * kStage / 16384);
+    uint32_t pphase = 0;  // parity bits of the fixup barriers (one per slot)
     griddep_wait();  // residual / positions / norm statistics belong to earlier kernels
     if (ep.ss_in) {
       compute_inv_rms(ep, gs, inv_smem);
       epi_bar();
     }
-    for (int j = 0; j < my_tiles; ++j) {
-      const int tile = pid + j * npair;
-      const int tile_n = tile / gs.b_tiles, tile_b = tile % gs.b_tiles;
-      const int n0 = (2 * tile_n + rank) * kBlockM, b0 = tile_b * BN;
+    SkRange rg(pid, npair, U, KB, sk_tiles);
+    SkPiece pc;
+    int j = 0;
+    while (rg.next(pc)) {
       const int acc = j & 1;
+      ++j;
+      const int tile_n = pc.tile / bt, tile_b = pc.tile % bt;
+      const int n0 = (2 * tile_n + rank) * kBlockM, b0 = tile_b * BN;
       const uint32_t taddr = tmem_base + ((uint32_t)(q * 32) << 16) + acc * L::kAccCols;
-      mbar_wait(&tfull[acc], (j >> 1) & 1);
+      const bool owner = pc.kb0 == 0;
+      // contributors to an owned tile: the following pairs whose ranges start inside it
+      int c_end = pid + 1;
+      if (owner && pc.kb1 < KB)
+        while (c_end < npair && sk_start(c_end, npair, U, KB, sk_tiles) < (long)(pc.tile + 1) * KB) ++c_end;
+      mbar_wait(&tfull[acc], ((j - 1) >> 1) & 1);
       tc_fence_after();
+      if (trace && t == 0) trace[owner ? 5 : 8] = globaltimer();  // piece accumulated
+      const int nc = owner ? c_end - pid - 1 : 0;  // contributors (only ever on this pair's last piece)
+      const int nblk = nc * (BN / 32);
+      auto issue = [&](int b) {  // bulk-copy fixup block b into its ring slot
+        const int slot = b % n_slots, k = b / nc, c = pid + 1 + b % nc;
+        mbar_arrive_expect_tx(&pbar[slot], 16384);
+        bulk_g2s(smem + slot * 16384, ws_col(c, 32 * k), 16384, &pbar[slot], policy_evict_first());
+      };
+      if (nc > 0) {  // wait for the contributors' partials, start streaming them into shared memory
+        if (t == 0) {
+          for (int c = pid + 1; c < c_end; ++c) flag_wait(gs.sk_flags + 2 * c + rank, 1u);
+          asm volatile("fence.proxy.async.global;" ::: "memory");
+          for (int b = 0; b < min(n_slots, nblk); ++b) issue(b);
+        }
+        if (trace && t == 0) trace[6] = globaltimer();  // partials available
+      }
+      unsigned long long ta = 0, tb = 0, tc = 0, td = 0, tx;
 #pragma unroll 1
       for (int c0 = 0; c0 < BN; c0 += 32) {
+        tx = trace ? globaltimer() : 0;
         uint32_t r0[16], r1[16];
         tmem_ld16(taddr + c0, r0);
         tmem_ld16(taddr + c0 + 16, r1);
         tmem_ld_wait();
+        if (trace) { const unsigned long long n = globaltimer(); ta += n - tx; tx = n; }
         if (c0 + 32 >= BN) {  // accumulator buffer fully read: the leader may reuse it
           tc_fence_before();
           __syncwarp();
-          if ((threadIdx.x & 31) == 0) mbar_arrive_cluster(tempty0 + acc * 8);
+          // relaxed: the TMEM reads are ordered by the tcgen05 fences; a release here would wait
+          // for this thread's earlier global stores
+          if ((threadIdx.x & 31) == 0) mbar_arrive_cluster_relaxed(tempty0 + acc * 8);
         }
-        if (skip) continue;
-#pragma unroll
-        for (int e = 0; e < 16; ++e) {
-          stg[pair_stg_index(e, row)] = __uint_as_float(r0[e]);
-          stg[pair_stg_index(e + 16, row)] = __uint_as_float(r1[e]);
-        }
-        epi_bar();
         float v[32];
 #pragma unroll
-        for (int e = 0; e < 32; e += 4) {
-          const float4 a = *(const float4*)(stg + pair_stg_index(cb, rl + e));
-          v[e] = a.x; v[e + 1] = a.y; v[e + 2] = a.z; v[e + 3] = a.w;
+        for (int e = 0; e < 16; ++e) { v[e] = __uint_as_float(r0[e]); v[e + 16] = __uint_as_float(r1[e]); }
+        if (!owner) {  // contributor: publish the partial (coalesced: a warp writes 32 rows of a column)
+#pragma unroll
+          for (int e = 0; e < 32; ++e) ws_col(pid, c0 + e)[row] = v[e];
+          continue;
         }
-        epi_slice<32, 32>(ep, gs, n0 + rl, b0 + c0 + cb, v, 2 * tile_n + rank, inv_smem);
+        for (int i = 0; i < nc; ++i) {  // contributors in pair order: deterministic
+          const int b = (c0 / 32) * nc + i, slot = b % n_slots;
+          mbar_wait(&pbar[slot], (pphase >> slot) & 1);
+          pphase ^= 1u << slot;
+          const float* blk = (const float*)(smem + slot * 16384);
+#pragma unroll
+          for (int e = 0; e < 32; ++e) v[e] += blk[e * kBlockM + row];
+          epi_bar();  // every thread is done with the slot
+          if (t == 0 && b + n_slots < nblk) issue(b + n_slots);
+        }
+        if (trace) { const unsigned long long n = globaltimer(); tb += n - tx; tx = n; }
+        if (skip) continue;
+#pragma unroll
+        for (int e = 0; e < 32; ++e) stg[pair_stg_index(e, row)] = v[e];
+        epi_bar();
+        float o[32];
+#pragma unroll
+        for (int e = 0; e < 32; e += 4) {
+          const float4 a = *(const float4*)(stg + pair_stg_index(cb, rl + (e >> 3) * 32 + (e & 7)));
+          o[e] = a.x; o[e + 1] = a.y; o[e + 2] = a.z; o[e + 3] = a.w;
+        }
+        if (trace) { const unsigned long long n = globaltimer(); tc += n - tx; tx = n; }
+        epi_slice<32, 32, 32>(ep, gs, n0 + rl, b0 + c0 + cb, o, 2 * tile_n + rank, inv_smem);
         epi_bar();  // staging is reused by the next chunk
+        if (trace) { const unsigned long long n = globaltimer(); td += n - tx; tx = n; }
+      }
+      if (trace && t == 0 && owner) { trace[11] = ta; trace[12] = tb; trace[13] = tc; trace[14] = td; }
+      if (!owner) {  // partial stored: release it to the owner
+        __threadfence();
+        epi_bar();
+        if (trace && t == 0) trace[9] = globaltimer();  // partial published
+        if (t == 0) asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(gs.sk_flags + 2 * pid + rank), "r"(1u) : "memory");
+      } else if (c_end > pid + 1) {  // partials consumed: re-arm the contributors' flags
+        epi_bar();
+        if (t == 0)
+          for (int c = pid + 1; c < c_end; ++c) gs.sk_flags[2 * c + rank] = 0u;
       }
     }
   }
+  if (trace && threadIdx.x == 64) trace[7] = globaltimer();  // epilogue done
   tc_fence_before();
   cluster_sync_all();  // the peer's last remote arrivals and TMEM reads are done
   if (warp == 1) tmem_free_pair<L::kTmemCols>(tmem_base);
+  if (trace && threadIdx.x == 0) trace[10] = globaltimer();
 }
 
 }  // namespace gh

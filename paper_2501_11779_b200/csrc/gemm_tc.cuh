@@ -71,24 +71,26 @@ GH_DEV void epi_store_one(const EpiParams& ep, int n, int b, float v, float part
 // ------------------------------------------------------------------ cluster split-K epilogue
 GH_DEV void epi_bar() { asm volatile("bar.sync 1, 128;\n" ::: "memory"); }  // the 4 epilogue warps
 
-// Slice epilogue: thread t of the 128 epilogue threads owns batch column
-// b = t / (128/BN) and a run of En = BN/C consecutive weight rows n of the CTA's slice; it has
-// the fully reduced fp32 values in `v` and writes its outputs directly (row-major [b][n]).
-template <int En>
+// Slice epilogue: thread t of the 128 epilogue threads owns batch column b and En weight rows n
+// of the output tile, as En/8 chunks of 8 consecutive rows RS rows apart (RS = 8: one run of En
+// consecutive rows).  It has the fully reduced fp32 values in `v` and writes its outputs directly
+// (row-major [b][n]).  RS > 8 lets the threads sharing a column interleave their chunks so that
+// every store instruction of a warp covers whole 32-byte sectors.
+template <int En, int RS>
 GH_DEV void store_run_bf16(uint16_t* dst, const float* v) {
   if ((((uintptr_t)dst) & 15) == 0 && En % 8 == 0) {
 #pragma unroll
     for (int e = 0; e < En; e += 8) {
       uint4 o;
-      o.x = (uint32_t)f32_to_bf16(v[e]) | ((uint32_t)f32_to_bf16(v[e + 1]) << 16);
-      o.y = (uint32_t)f32_to_bf16(v[e + 2]) | ((uint32_t)f32_to_bf16(v[e + 3]) << 16);
-      o.z = (uint32_t)f32_to_bf16(v[e + 4]) | ((uint32_t)f32_to_bf16(v[e + 5]) << 16);
-      o.w = (uint32_t)f32_to_bf16(v[e + 6]) | ((uint32_t)f32_to_bf16(v[e + 7]) << 16);
-      *(uint4*)(dst + e) = o;
+      o.x = pack_bf16x2(v[e], v[e + 1]);
+      o.y = pack_bf16x2(v[e + 2], v[e + 3]);
+      o.z = pack_bf16x2(v[e + 4], v[e + 5]);
+      o.w = pack_bf16x2(v[e + 6], v[e + 7]);
+      *(uint4*)(dst + (e >> 3) * RS) = o;
     }
   } else {
 #pragma unroll
-    for (int e = 0; e < En; ++e) dst[e] = f32_to_bf16(v[e]);
+    for (int e = 0; e < En; ++e) dst[(e >> 3) * RS + (e & 7)] = f32_to_bf16(v[e]);
   }
 }
 
@@ -108,11 +110,13 @@ GH_DEV void compute_inv_rms(const EpiParams& ep, const GemmShape& gs, float* inv
   }
 }
 
-template <int BN, int En>
+template <int BN, int En, int RS = 8>
 GH_DEV void epi_slice(const EpiParams& ep, const GemmShape& gs, int n, int b, float (&v)[En], int slice,
                       const float* inv) {
+  // element e of this thread is output row n + off(e)
+  auto off = [](int e) { return (e >> 3) * RS + (e & 7); };
   const bool col_ok = b < gs.Bt;
-  const bool full = n + En <= gs.N;
+  const bool full = n + off(En - 1) < gs.N;
   if (ep.ss_in && col_ok) {  // fused RMSNorm of the GEMM input
     const float sc = inv[b];
 #pragma unroll
@@ -125,8 +129,8 @@ GH_DEV void epi_slice(const EpiParams& ep, const GemmShape& gs, int n, int b, fl
       const uint16_t* rp = (const uint16_t*)ep.resid + (long)b * ep.ldr + n;
 #pragma unroll
       for (int e = 0; e < En; ++e) {
-        if (full || n + e < gs.N) {
-          const float y = bf16_to_f32(f32_to_bf16(v[e] + bf16_to_f32(rp[e])));
+        if (full || n + off(e) < gs.N) {
+          const float y = bf16_to_f32(f32_to_bf16(v[e] + bf16_to_f32(rp[off(e)])));
           sq = fmaf(y, y, sq);
         }
       }
@@ -134,6 +138,10 @@ GH_DEV void epi_slice(const EpiParams& ep, const GemmShape& gs, int n, int b, fl
 #pragma unroll
     for (int o = 1; o < kRuns; o <<= 1) sq += __shfl_xor_sync(0xffffffffu, sq, o);
     if (col_ok && ((threadIdx.x - 64) % kRuns) == 0) ep.ss_out[(long)slice * gs.Bt + b] = sq;
+  }
+  if (gs.flags & GEMM_DBG_NO_STORE) {  // diagnostics: no output stores
+    if (col_ok && v[0] == 12345.f) ((float*)ep.out)[0] = v[1];
+    return;
   }
   switch (ep.kind) {
     case EPI_STORE:
@@ -144,7 +152,7 @@ GH_DEV void epi_slice(const EpiParams& ep, const GemmShape& gs, int n, int b, fl
         if (full && En % 8 == 0 && ((uintptr_t)rp & 15) == 0) {
           uint4 rr[En / 8 > 0 ? En / 8 : 1];
 #pragma unroll
-          for (int e = 0; e < En / 8; ++e) rr[e] = __ldg((const uint4*)rp + e);
+          for (int e = 0; e < En / 8; ++e) rr[e] = __ldg((const uint4*)(rp + e * RS));
 #pragma unroll
           for (int e = 0; e < En / 8; ++e) {
             const uint32_t w[4] = {rr[e].x, rr[e].y, rr[e].z, rr[e].w};
@@ -156,15 +164,15 @@ GH_DEV void epi_slice(const EpiParams& ep, const GemmShape& gs, int n, int b, fl
           }
         } else {
 #pragma unroll
-          for (int e = 0; e < En; ++e) v[e] += (full || n + e < gs.N) ? bf16_to_f32(rp[e]) : 0.f;
+          for (int e = 0; e < En; ++e) v[e] += (full || n + off(e) < gs.N) ? bf16_to_f32(rp[off(e)]) : 0.f;
         }
       }
       uint16_t* op = (uint16_t*)ep.out + (long)b * ep.ldo + n;
-      if (full) store_run_bf16<En>(op, v);
+      if (full) store_run_bf16<En, RS>(op, v);
       else
 #pragma unroll
         for (int e = 0; e < En; ++e)
-          if (n + e < gs.N) op[e] = f32_to_bf16(v[e]);
+          if (n + off(e) < gs.N) op[off(e)] = f32_to_bf16(v[e]);
       return;
     }
     case EPI_QKV_ROPE: {
@@ -172,18 +180,20 @@ GH_DEV void epi_slice(const EpiParams& ep, const GemmShape& gs, int n, int b, fl
       if (ep.xcopy_src && n < ep.xcopy_rows) {  // x into the message's x slot (fused RMSNorm path)
         const uint16_t* xs = (const uint16_t*)ep.xcopy_src + (long)b * ep.xcopy_ld + n;
         uint16_t* xd = (uint16_t*)ep.out + (long)b * ep.ldo + n - ep.xcopy_rows;
-        if (En % 8 == 0 && n + En <= ep.xcopy_rows && ((uintptr_t)xs & 15) == 0 && ((uintptr_t)xd & 15) == 0) {
+        if (En % 8 == 0 && n + off(En - 1) < ep.xcopy_rows && ((uintptr_t)xs & 15) == 0 && ((uintptr_t)xd & 15) == 0) {
 #pragma unroll
-          for (int e = 0; e < En; e += 8) *(uint4*)(xd + e) = __ldg((const uint4*)(xs + e));
+          for (int e = 0; e < En; e += 8) *(uint4*)(xd + off(e)) = __ldg((const uint4*)(xs + off(e)));
         } else {
-          for (int e = 0; e < En && n + e < ep.xcopy_rows; ++e) xd[e] = xs[e];
+#pragma unroll
+          for (int e = 0; e < En; ++e)
+            if (n + off(e) < ep.xcopy_rows) xd[off(e)] = xs[off(e)];
         }
       }
       if (n < ep.rope_rows) {
-        const float2* cs = ep.rope + (long)ep.pos[b] * (ep.d_head >> 1) + ((n % ep.d_head) >> 1);
+        const float2* cs = ep.rope + (long)ep.pos[b] * (ep.d_head >> 1);
 #pragma unroll
         for (int e = 0; e < En; e += 2) {
-          const float2 c = cs[e >> 1];
+          const float2 c = cs[((n + off(e)) % ep.d_head) >> 1];
           const float a = v[e], o = v[e + 1];
           // pair (a, o) = (even, odd): even' = a cos - o sin, odd' = a sin + o cos
           v[e] = a * c.x - o * c.y;
@@ -191,11 +201,11 @@ GH_DEV void epi_slice(const EpiParams& ep, const GemmShape& gs, int n, int b, fl
         }
       }
       uint16_t* op = (uint16_t*)ep.out + (long)b * ep.ldo + n;
-      if (full) store_run_bf16<En>(op, v);
+      if (full) store_run_bf16<En, RS>(op, v);
       else
 #pragma unroll
         for (int e = 0; e < En; ++e)
-          if (n + e < gs.N) op[e] = f32_to_bf16(v[e]);
+          if (n + off(e) < gs.N) op[off(e)] = f32_to_bf16(v[e]);
       return;
     }
     case EPI_SWIGLU: {
@@ -203,12 +213,21 @@ GH_DEV void epi_slice(const EpiParams& ep, const GemmShape& gs, int n, int b, fl
       float h[En / 2];
 #pragma unroll
       for (int e = 0; e < En / 2; ++e) h[e] = silu_f(v[2 * e]) * v[2 * e + 1];
+      // output element e/2 of chunk j lands at (n + j*RS)/2 + (e%8)/2: chunks of 4, RS/2 apart
       uint16_t* op = (uint16_t*)ep.out + (long)b * ep.ldo + (n >> 1);
-      if (full) store_run_bf16<En / 2>(op, h);
-      else
+      if (full && En % 8 == 0 && (((uintptr_t)op) & 7) == 0) {
+#pragma unroll
+        for (int e = 0; e < En / 2; e += 4) {
+          uint2 o;
+          o.x = pack_bf16x2(h[e], h[e + 1]);
+          o.y = pack_bf16x2(h[e + 2], h[e + 3]);
+          *(uint2*)(op + (e >> 2) * (RS / 2)) = o;
+        }
+      } else {
 #pragma unroll
         for (int e = 0; e < En / 2; ++e)
-          if (n + 2 * e < gs.N) op[e] = f32_to_bf16(h[e]);
+          if (n + off(2 * e) < gs.N) op[off(2 * e) >> 1] = f32_to_bf16(h[e]);
+      }
       return;
     }
     default: {
@@ -216,13 +235,15 @@ GH_DEV void epi_slice(const EpiParams& ep, const GemmShape& gs, int n, int b, fl
       float best = -INFINITY;
       int bi = 0x7fffffff;
 #pragma unroll
-      for (int e = 0; e < En; ++e)
-        if (n + e < gs.N && (v[e] > best || (v[e] == best && n + e < bi))) { best = v[e]; bi = n + e; }
+      for (int e = 0; e < En; ++e) {
+        const int r = n + off(e);
+        if (r < gs.N && (v[e] > best || (v[e] == best && r < bi))) { best = v[e]; bi = r; }
+      }
       if (ep.logits && col_ok) {
         float* lp = ep.logits + (long)b * ep.ldl + n;
 #pragma unroll
         for (int e = 0; e < En; ++e)
-          if (n + e < gs.N) lp[e] = v[e];
+          if (n + off(e) < gs.N) lp[off(e)] = v[e];
       }
       // reduce over the 128/BN threads that share column b (adjacent lanes)
       constexpr int kRuns = 128 / BN;

@@ -455,27 +455,48 @@ static double kblock_clk(double bytes_per_sm, double mma_clk) {
   return std::max(bytes_per_sm / 57.0, mma_clk) + 40.0;
 }
 
-// Pair plan for a large batch: the batch split into b_tiles tiles of BN (multiple of 32, <= 256)
-// columns minimising rounds * KB * kblock_clk (wave quantisation against per-tile L2 traffic).
-static GemmPlan plan_pair(int N, int KB, int Bt, double* cost_out) {
+// Pair plan for a large batch: the batch is cut into b_tiles tiles of BN columns (multiple of 32,
+// <= 256) and the work is spread over the co-resident pairs either tile by tile (contiguous tile
+// ranges) or by stream-K (contiguous k-block ranges, split tiles finished by their owner from the
+// contributors' fp32 partials).  Cost in SM clocks: the per-pair mainloop (kblock_clk per
+// k-block) but never below the weights' HBM streaming time, plus the stream-K fixup (the owner
+// reads every contributor's 128 x BN partial at ~25 B/clk, measured) and the last epilogue.
+static double hbm_floor_clk(int N, int K) { return (double)N * K * 2 / 3300.0; }  // ~6.5 TB/s at 1965 MHz
+static double epi_clk(int BN) { return BN / 32 * 500.0; }
+
+static GemmPlan plan_pair(int N, int K, int Bt, double* cost_out) {
   GemmPlan best;
   double best_cost = 1e30;
+  const int KB = (K + kBlockK - 1) / kBlockK;
   const int n_tiles = (N + 2 * kBlockM - 1) / (2 * kBlockM);
-  const int npairs = max_pairs();
+  const int npairs = std::min(max_pairs(), (int)(kSkWsBytes / (256 * 256 * 4)));
+  const double floor = hbm_floor_clk(N, K);
   int last_bn = 0;
   for (int bt = (Bt + kPairMaxBN - 1) / kPairMaxBN; bt <= (Bt + 31) / 32; ++bt) {
     const int BN = ((Bt + bt - 1) / bt + 31) / 32 * 32;
     if (BN == last_bn) continue;
     last_bn = BN;
     const int b_tiles = (Bt + BN - 1) / BN;
-    const int tiles = n_tiles * b_tiles;
-    const int np = std::min(tiles, npairs);
-    const int rounds = (tiles + np - 1) / np;
-    const double cost = (double)rounds * KB * kblock_clk(16384.0 + BN * 64.0, 2.0 * BN);
-    if (cost < best_cost - 1e-9) {
-      best_cost = cost;
-      best.pair = true; best.BN = BN; best.b_tiles = b_tiles; best.n_tiles = n_tiles;
-      best.C = 2; best.n_clusters = np;
+    const double tkb = kblock_clk(16384.0 + BN * 64.0, 2.0 * BN);
+    for (int split = 0; split < 2; ++split) {
+      const long tiles = (long)n_tiles * b_tiles, units = tiles * KB;
+      double cost;
+      int np;
+      if (!split) {
+        np = (int)std::min<long>(tiles, npairs);
+        cost = std::max((double)((tiles + np - 1) / np) * KB * tkb, floor) + epi_clk(BN);
+      } else {
+        np = (int)std::min<long>(units, npairs);
+        const double per = (double)units / np;
+        const double contrib = per >= KB ? 1.0 : std::ceil(KB / per);  // partials an owner adds
+        const double part = 128.0 * BN * 4;
+        cost = std::max(std::ceil(per) * tkb, floor) + contrib * part / 25.0 + part / 64.0 + epi_clk(BN);
+      }
+      if (cost < best_cost - 1e-9) {
+        best_cost = cost;
+        best.pair = true; best.split = split; best.BN = BN; best.b_tiles = b_tiles; best.n_tiles = n_tiles;
+        best.C = 2; best.n_clusters = np;
+      }
     }
   }
   *cost_out = best_cost;
@@ -508,14 +529,16 @@ GemmPlan plan_gemm(int N, int K, int Bt) {
   }
   if ((Bt > 128 && pair_override != 1) || pair_override == 2 || Bt > 256) {
     double pc = 0;
-    GemmPlan pp = plan_pair(N, KB, Bt, &pc);
-    const double sc = best * kblock_clk(16384.0 + p.BN * 128.0, 2.0 * p.BN);
+    GemmPlan pp = plan_pair(N, K, Bt, &pc);
+    // split-K cluster kernel: critical-path k-blocks, HBM floor, reduction + epilogue tail (~2.6 us)
+    const double sc = std::max(best * kblock_clk(16384.0 + p.BN * 128.0, 2.0 * p.BN), hbm_floor_clk(N, K)) + 5100.0;
     if (Bt > 256 || pair_override == 2 || pc < sc) p = pp;
   }
   static const bool verbose = getenv("GH_GEMM_VERBOSE") != nullptr;  // diagnostics
   if (verbose)
     fprintf(stderr, "[gh] gemm N=%d K=%d B=%d: %s BN=%d b_tiles=%d n_tiles=%d C=%d clusters=%d\n", N, K, Bt,
-            p.pair ? "pair" : "split-K", p.BN, p.b_tiles, p.n_tiles, p.C, p.n_clusters);
+            p.pair ? (p.split ? "pair stream-K" : "pair tiles") : "split-K", p.BN, p.b_tiles, p.n_tiles, p.C,
+            p.n_clusters);
   return p;
 }
 
@@ -607,7 +630,13 @@ cudaError_t launch_gemm(const Weight& W, const CUtensorMap* tmW, const void* X, 
   gs.BN = p.BN;
   gs.pf = pf;
   gs.pf_bytes = pf ? pf_bytes : 0;
-  if (p.pair) return launch_pair(tmW, tmX, gs, p, ep, st);
+  gs.sk_ws = sc.sk_ws;
+  gs.sk_flags = sc.sk_flags;
+  gs.sk_split = p.split ? 1 : 0;
+  if (p.pair) {
+    if (!sc.sk_ws || !sc.sk_flags) return cudaErrorInvalidValue;
+    return launch_pair(tmW, tmX, gs, p, ep, st);
+  }
   if (ep.ss_in && Bt > kMaxInvCols) return cudaErrorInvalidValue;
   switch (p.BN) {
     case 16: return launch_tc<16>(tmW, tmX, gs, p, ep, st);

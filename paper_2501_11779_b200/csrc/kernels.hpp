@@ -39,6 +39,7 @@ struct RowSegs {
 //  pair kernel (gemm_pair.cuh, large batches): 256-row tiles on CTA pairs (C = 2), no K split.
 struct GemmPlan {
   bool pair = false;
+  bool split = false;  // pair kernel: stream-K k-block ranges (else contiguous tile ranges)
   int BN = 0;         // batch tile (split-K: 16, 32, 64, 128; pair: multiple of 32 up to 256)
   int n_tiles = 0;    // ceil(N / 128), pair: ceil(N / 256)
   int b_tiles = 0;
@@ -57,7 +58,10 @@ struct GemmScratch {
   float* stage = nullptr;  size_t stage_floats = 0;  // SIMT path fp32 result [Bt][N]
   int debug_flags = 0;                                // GEMM_DBG_* (diagnostics only)
   unsigned long long* trace = nullptr;                // per-CTA timestamps (diagnostics only)
+  float* sk_ws = nullptr;                             // pair kernel stream-K partials (kSkWsBytes)
+  unsigned int* sk_flags = nullptr;                   // [kNumSMs] zero-initialised
 };
+constexpr size_t kSkWsBytes = (size_t)74 * 256 * 256 * 4;  // co-resident pairs x 256 columns x 256 rows fp32
 void gemm_debug_set(int stages);  // 0 = production pipeline depth
 void gemm_debug_cluster(int C);   // 0 = production cluster-size choice
 void gemm_debug_pair(int mode);   // 0 = planner's choice, 1 = force split-K (B <= 256), 2 = force pair

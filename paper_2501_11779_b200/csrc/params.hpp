@@ -54,8 +54,14 @@ struct GemmShape {
   // its own loads are all in flight (fills the HBM idle time of this kernel's tail)
   const void* pf;
   unsigned long long pf_bytes;
+  // pair kernel, stream-K: fp32 partial workspace [pairs][256 columns][256 rows] and one flag
+  // per (pair, CTA) (zero between launches)
+  float* sk_ws;
+  unsigned int* sk_flags;
+  int sk_split;         // 1: stream-K k-block ranges; 0: contiguous whole-tile ranges
 };
-enum GemmDbg : int { GEMM_DBG_NO_MMA = 1, GEMM_DBG_NO_X = 2, GEMM_DBG_NO_HINT = 4, GEMM_DBG_NO_EPI = 8 };
+enum GemmDbg : int { GEMM_DBG_NO_MMA = 1, GEMM_DBG_NO_X = 2, GEMM_DBG_NO_HINT = 4, GEMM_DBG_NO_EPI = 8, GEMM_DBG_SK_TILES = 16,
+                     GEMM_DBG_NO_STORE = 32 };
 
 struct AttnArgs {
   const void* msg_fwd;  // [B][2D + 2Dkv]

@@ -282,6 +282,14 @@ gh_status gh_tier1_create(const gh_model_spec* spec, int device, uint32_t layer_
     GH_TRY(dev_alloc(t->mem, n_slices * B * sizeof(float2), &p));
     t->part = (float2*)p;
   }
+  if (db == 2 && B > 128) {  // batches the planner may give to the CTA-pair kernel (stream-K)
+    void* p;
+    GH_TRY(dev_alloc(t->mem, kSkWsBytes, &p));
+    t->gsc.sk_ws = (float*)p;
+    GH_TRY(dev_alloc(t->mem, kNumSMs * sizeof(unsigned int), &p));
+    t->gsc.sk_flags = (unsigned int*)p;
+    GH_CUDA(cudaMemset(p, 0, kNumSMs * sizeof(unsigned int)));
+  }
   if (db == 4) {
     void* p;
     const size_t n = B * (size_t)std::max({D + 2 * Dkv, 2 * Dh, V, D});
@@ -1296,6 +1304,14 @@ extern "C" gh_status gh_debug_gemm_bench(int N, int K, int B, int flags, int sta
   gemm_debug_pair(0);
   GH_CUDA(make_tmap_bf16(&tmX, X, (uint64_t)B, (uint64_t)K, (uint64_t)K, (uint32_t)p.x_box_rows()));
   GemmScratch sc;
+  {
+    void* q;
+    GH_TRY(dev_alloc(mem, kSkWsBytes, &q));
+    sc.sk_ws = (float*)q;
+    GH_TRY(dev_alloc(mem, kNumSMs * sizeof(unsigned int), &q));
+    sc.sk_flags = (unsigned int*)q;
+    GH_CUDA(cudaMemset(q, 0, kNumSMs * sizeof(unsigned int)));
+  }
   sc.debug_flags = flags;
   EpiParams ep = epi_default();
   ep.kind = EPI_STORE; ep.out = Y; ep.ldo = N;
@@ -1342,6 +1358,14 @@ extern "C" gh_status gh_debug_gemm_trace(int N, int K, int B, int copies, int re
   CUtensorMap tmX;
   GH_CUDA(make_tmap_bf16(&tmX, X, (uint64_t)B, (uint64_t)K, (uint64_t)K, (uint32_t)p.x_box_rows()));
   GemmScratch sc;
+  {
+    void* q;
+    GH_TRY(dev_alloc(mem, kSkWsBytes, &q));
+    sc.sk_ws = (float*)q;
+    GH_TRY(dev_alloc(mem, kNumSMs * sizeof(unsigned int), &q));
+    sc.sk_flags = (unsigned int*)q;
+    GH_CUDA(cudaMemset(q, 0, kNumSMs * sizeof(unsigned int)));
+  }
   void* q;
   sc.debug_flags = dbg_flags;
   unsigned long long* dtrace = nullptr;
