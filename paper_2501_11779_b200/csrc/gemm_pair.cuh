@@ -40,7 +40,7 @@ struct PairSmem {
   static constexpr int kStgBytes = 32 * 128 * 4;  // epilogue staging: 32 columns x 128 rows fp32
   static constexpr uint32_t kAccCols = kPairMaxBN;
   static constexpr uint32_t kTmemCols = 512;
-  static constexpr int kBarBytes = (2 * kMaxStages + 16) * 8 + 16 + kPairMaxInvCols * 4;
+  static constexpr int kBarBytes = (2 * kMaxStages + 16) * 8 + 16 + kPairMaxInvCols * 8;  // + RoPE positions
   static constexpr int kFixSlots = 8;  // stream-K fixup: 16 KB partial blocks in flight
   GH_HD static int b_bytes(int BN) { return BN / 2 * kBlockK * 2; }
   GH_HD static int stage_bytes(int BN) { return kABytes + b_bytes(BN); }
@@ -107,6 +107,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   uint32_t* tmem_slot = (uint32_t*)(tempty + 2);
   float* inv_smem = (float*)(tempty + 4);
   uint64_t* pbar = (uint64_t*)(inv_smem + kPairMaxInvCols);  // [kFixSlots] stream-K fixup blocks
+  int* pos_smem = (int*)(pbar + L::kFixSlots);                // [kPairMaxInvCols] RoPE positions
 
   const int warp = threadIdx.x >> 5;
   const int KB = gs.kb_total;
@@ -233,10 +234,12 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     const int n_slots = min(L::kFixSlots, S * kStage / 16384);
     uint32_t pphase = 0;  // parity bits of the fixup barriers (one per slot)
     griddep_wait();  // residual / positions / norm statistics belong to earlier kernels
-    if (ep.ss_in) {
-      compute_inv_rms(ep, gs, inv_smem);
-      epi_bar();
-    }
+    // positions of every batch column once (the RoPE table lookups then need no dependent load)
+    const bool pos_cached = ep.kind == EPI_QKV_ROPE && gs.Bt <= kPairMaxInvCols;
+    if (pos_cached)
+      for (int b = t; b < gs.Bt; b += 128) pos_smem[b] = __ldg(ep.pos + b);
+    if (ep.ss_in) compute_inv_rms(ep, gs, inv_smem);
+    if (ep.ss_in || pos_cached) epi_bar();
     SkRange rg(pid, npair, U, KB, sk_tiles);
     SkPiece pc;
     int j = 0;
@@ -315,7 +318,8 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
           o[e] = a.x; o[e + 1] = a.y; o[e + 2] = a.z; o[e + 3] = a.w;
         }
         if (trace) { const unsigned long long n = globaltimer(); tc += n - tx; tx = n; }
-        epi_slice<32, 32, 32>(ep, gs, n0 + rl, b0 + c0 + cb, o, 2 * tile_n + rank, inv_smem);
+        epi_slice<32, 32, 32>(ep, gs, n0 + rl, b0 + c0 + cb, o, 2 * tile_n + rank, inv_smem,
+                              pos_cached ? pos_smem : nullptr);
         epi_bar();  // staging is reused by the next chunk
         if (trace) { const unsigned long long n = globaltimer(); td += n - tx; tx = n; }
       }

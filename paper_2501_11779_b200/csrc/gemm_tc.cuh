@@ -36,6 +36,8 @@ constexpr int kBlockK = 64;    // 64 bf16 = 128 B = one swizzle atom row
 constexpr int kGemmThreads = 192;
 
 GH_DEV float silu_f(float g) { return g / (1.0f + __expf(-g)); }
+// tensor-core epilogues (bf16 storage, tolerance-checked): fast reciprocal instead of IEEE division
+GH_DEV float silu_fast(float g) { return __fdividef(g, 1.0f + __expf(-g)); }
 
 // Scalar epilogue for STORE / STORE_RESID / QKV_ROPE / SWIGLU at output (row n, batch b).
 // `partner` is the accumulator of row n^1 (RoPE pair / interleaved gate-up pair).  Used by the
@@ -112,7 +114,7 @@ GH_DEV void compute_inv_rms(const EpiParams& ep, const GemmShape& gs, float* inv
 
 template <int BN, int En, int RS = 8>
 GH_DEV void epi_slice(const EpiParams& ep, const GemmShape& gs, int n, int b, float (&v)[En], int slice,
-                      const float* inv) {
+                      const float* inv, const int* pos_smem = nullptr) {
   // element e of this thread is output row n + off(e)
   auto off = [](int e) { return (e >> 3) * RS + (e & 7); };
   const bool col_ok = b < gs.Bt;
@@ -190,10 +192,12 @@ GH_DEV void epi_slice(const EpiParams& ep, const GemmShape& gs, int n, int b, fl
         }
       }
       if (n < ep.rope_rows) {
-        const float2* cs = ep.rope + (long)ep.pos[b] * (ep.d_head >> 1);
+        const float2* cs = ep.rope + (long)(pos_smem ? pos_smem[b] : ep.pos[b]) * (ep.d_head >> 1);
+        int hb = 0;  // (row % d_head) / 2 at the start of the current 8-row chunk (a chunk never crosses a head)
 #pragma unroll
         for (int e = 0; e < En; e += 2) {
-          const float2 c = cs[((n + off(e)) % ep.d_head) >> 1];
+          if ((e & 7) == 0) hb = ((n + off(e)) % ep.d_head) >> 1;
+          const float2 c = cs[hb + ((e & 7) >> 1)];
           const float a = v[e], o = v[e + 1];
           // pair (a, o) = (even, odd): even' = a cos - o sin, odd' = a sin + o cos
           v[e] = a * c.x - o * c.y;
@@ -212,7 +216,7 @@ GH_DEV void epi_slice(const EpiParams& ep, const GemmShape& gs, int n, int b, fl
       if (!col_ok) return;
       float h[En / 2];
 #pragma unroll
-      for (int e = 0; e < En / 2; ++e) h[e] = silu_f(v[2 * e]) * v[2 * e + 1];
+      for (int e = 0; e < En / 2; ++e) h[e] = silu_fast(v[2 * e]) * v[2 * e + 1];
       // output element e/2 of chunk j lands at (n + j*RS)/2 + (e%8)/2: chunks of 4, RS/2 apart
       uint16_t* op = (uint16_t*)ep.out + (long)b * ep.ldo + (n >> 1);
       if (full && En % 8 == 0 && (((uintptr_t)op) & 7) == 0) {

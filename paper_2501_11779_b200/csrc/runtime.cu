@@ -282,6 +282,7 @@ gh_status gh_tier1_create(const gh_model_spec* spec, int device, uint32_t layer_
     GH_TRY(dev_alloc(t->mem, n_slices * B * sizeof(float2), &p));
     t->part = (float2*)p;
   }
+  if (getenv("GH_GEMM_DBG")) t->gsc.debug_flags = atoi(getenv("GH_GEMM_DBG"));  // diagnostics (wrong results)
   if (db == 2 && B > 128) {  // batches the planner may give to the CTA-pair kernel (stream-K)
     void* p;
     GH_TRY(dev_alloc(t->mem, kSkWsBytes, &p));
