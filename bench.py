@@ -152,6 +152,44 @@ def cpu_sample(spec, B, ctx, threads=0):
 
 
 # ------------------------------------------------------------------ configs
+def _profile_latency(path: Path, stage: str, batch: int) -> float:
+    """Per-layer latency (us) at `batch` from a reference-format profile CSV: linear interpolation
+    between grid points, clamped below and extrapolated from the top two points above (the
+    reference's KernelProfile::latency, profiles.cpp:93-129)."""
+    pts = []
+    for ln in path.read_text().splitlines()[1:]:
+        f = ln.split(",")
+        if len(f) == 5 and f[1] == stage:
+            pts.append((int(f[3]), float(f[4])))
+    pts.sort()
+    if batch <= pts[0][0]:
+        return pts[0][1]
+    for (b0, l0), (b1, l1) in zip(pts, pts[1:]):
+        if batch <= b1:
+            return l0 + (l1 - l0) * (batch - b0) / (b1 - b0)
+    (b0, l0), (b1, l1) = pts[-2], pts[-1]
+    return l1 + (l1 - l0) * (batch - b1) / (b1 - b0)
+
+
+def if_gh_from_profiles(spec, t1_batch: int, shard: int, ctx: int) -> int:
+    """In-flight batches that keep Tier-1 busy while a batch is at Tier-2: the reference's
+    if_gh = 1 + ceil((t_att + t_roundtrip) / t_noatt) (analytic.cpp:31-39), with t_noatt and
+    t_att from this repo's measured B200 stage profiles (profiles/b200_tier{1,2}_C2.csv) and the
+    round trip of the PayloadModel messages of one shard (netmodel.cpp:18-24) over NVLink at a
+    conservative 400 GB/s plus 2 x 10 us of copy / flag latency.  At least 2."""
+    import math
+    root = Path(__file__).resolve().parent / "profiles"
+    try:
+        t_noatt = _profile_latency(root / "b200_tier1_C2.csv", "nonattention", t1_batch)
+        t_att = _profile_latency(root / "b200_tier2_C2.csv", "attention", shard)
+    except (OSError, IndexError, ValueError):
+        return 2
+    db = spec.dtype_bytes
+    msg = shard * db * ((2 * spec.d_model + 2 * spec.d_kv) + 2 * spec.d_model)
+    t_rt = 20.0 + msg / 400e9 * 1e6
+    return max(2, 1 + math.ceil((t_att + t_rt) / t_noatt))
+
+
 def workload(args, world):
     import paper_2501_11779_b200 as gh
     cfg = args.config or "C2"
@@ -162,8 +200,9 @@ def workload(args, world):
                     shard=c["batch"], kp=0)
     kp = world - 1
     if cfg == "C2":  # weak scaling of the N=1 workload: 64 prompts per Tier-2 GPU per in-flight batch
-        return dict(name="C2-split", spec=spec, ctx=ctx, batch=c["batch"] * kp, requested=c["batch"] * kp * 2,
-                    inflight=2, shard=c["batch"], kp=kp,
+        IF = args.inflight or if_gh_from_profiles(spec, c["batch"] * kp, c["batch"], ctx)
+        return dict(name="C2-split", spec=spec, ctx=ctx, batch=c["batch"] * kp, requested=c["batch"] * kp * IF,
+                    inflight=IF, shard=c["batch"], kp=kp,
                     admitted_slots=gh.two_tier_context_slots(spec, 1, kp, 179 * GiB, ctx))
     mem = 179 * GiB
     slots = gh.two_tier_context_slots(spec, 1, kp, mem, ctx)  # optimizer.cpp:175-192
@@ -182,9 +221,11 @@ def ncu_traffic(kernel_prefix):
         with open(p) as f:
             for row in csv.DictReader(f):
                 if kernel_prefix in row.get("Kernel Name", ""):
+                    rd = next((v for k, v in row.items() if k.startswith("dram__bytes_read.sum")), None)
+                    wr = next((v for k, v in row.items() if k.startswith("dram__bytes_write.sum")), None)
                     try:
-                        return (float(row["dram__bytes_read.sum"]) + float(row["dram__bytes_write.sum"])) * 1e6
-                    except (KeyError, ValueError):
+                        return (float(rd) + float(wr)) * 1e6  # Mbyte
+                    except (TypeError, ValueError):
                         return None
     return None
 
@@ -375,6 +416,8 @@ def main():
     ap.add_argument("--config", default=None, choices=[None, "C2", "C3"])
     ap.add_argument("--cpu-threads", type=int, default=0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--inflight", type=int, default=0,
+                    help="tier split: in-flight batches (0 = if_gh from the stage profiles)")
     ap.add_argument("--transport", default="auto", choices=["auto", "nccl", "peer"],
                     help="tier-split message transport (peer: copy engines + IPC flags; nccl: send/recv)")
     args = ap.parse_args()
