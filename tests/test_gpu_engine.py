@@ -70,6 +70,12 @@ def test_c1_graph_matches_eager(need_gpu):
     (gh.ModelSpec("e2e-wide", 2, 512, 512, 1024, 4, 4, 64, 2, 700), 300, 3),
     # 128 < B <= 256: two batch tiles with the fused RMSNorm
     (gh.ModelSpec("e2e-b192", 2, 512, 512, 1024, 4, 4, 64, 2, 700), 192, 3),
+    # Tier-1 batch of the 8-GPU split (7 x 64): CTA-pair kernel, several batch tiles, stream-K
+    (gh.ModelSpec("e2e-b448", 2, 1024, 1024, 2816, 8, 8, 64, 2, 1000), 448, 2),
+    # SURVEY 8(a) config shapes at full width, 2 layers: C3/C4 13B-class MHA (D 5120, 40 heads)
+    # and C5 70B GQA (D 8192, 64 query / 8 KV heads, FFN 28672)
+    (gh.ModelSpec("c4-13b-shape", 2, 5120, 5120, 13824, 40, 40, 64, 2, 32000), 8, 2),
+    (gh.ModelSpec("c5-70b-shape", 2, 8192, 1024, 28672, 64, 8, 64, 2, 32000), 8, 2),
 ])
 def test_bf16_engine_teacher_forced(need_gpu, spec, B, steps):
     """bf16 storage: per step, the GPU's argmax equals the oracle's wherever the oracle's top-2
