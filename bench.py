@@ -198,11 +198,15 @@ def workload(args, world):
     if world == 1:
         return dict(name=cfg, spec=spec, ctx=ctx, batch=c["batch"], requested=c["batch"], inflight=1,
                     shard=c["batch"], kp=0)
-    kp = world - 1
+    n1 = max(1, args.tier1)
+    if (world - n1) % n1 or world <= n1:
+        raise SystemExit(f"--tier1 {n1}: world size {world} must be tier1 * (1 + K')")
+    kp = (world - n1) // n1  # Tier-2 GPUs per Tier-1 span
     if cfg == "C2":  # weak scaling of the N=1 workload: 64 prompts per Tier-2 GPU per in-flight batch
-        IF = args.inflight or if_gh_from_profiles(spec, c["batch"] * kp, c["batch"], ctx)
-        return dict(name="C2-split", spec=spec, ctx=ctx, batch=c["batch"] * kp, requested=c["batch"] * kp * IF,
-                    inflight=IF, shard=c["batch"], kp=kp,
+        shard = args.shard or c["batch"]
+        IF = args.inflight or if_gh_from_profiles(spec, shard * kp, shard, ctx)
+        return dict(name="C2-split", spec=spec, ctx=ctx, batch=shard * kp, requested=shard * kp * IF,
+                    inflight=IF, shard=shard, kp=kp,
                     admitted_slots=gh.two_tier_context_slots(spec, 1, kp, 179 * GiB, ctx))
     mem = 179 * GiB
     slots = gh.two_tier_context_slots(spec, 1, kp, mem, ctx)  # optimizer.cpp:175-192
@@ -344,7 +348,7 @@ def run_split(args, wl, rank, world):
     dist.broadcast_object_list(obj, src=0)
     comm = Comm(obj[0], world, rank, dev)
     eng = Engine(spec, batch=wl["batch"], inflight=IF, device=dev, use_graph=False, comm=comm,
-                 transport=args.transport)
+                 transport=args.transport, tier1_ranks=max(1, args.tier1))
     transport = eng.transport
     lib = gh.lib()
     stream = torch.cuda.Stream()
@@ -354,8 +358,8 @@ def run_split(args, wl, rank, world):
     tok = rng.integers(0, spec.vocab_size, size=wl["batch"]).astype(np.int32)
     pos = np.full(wl["batch"], ctx - 1, np.int32)
     torch.cuda.synchronize()
-    for ib in range(IF):
-        eng.step_host(tok, pos, ib=ib)
+    t1 = eng.role == "tier1"
+    eng.step_all_host(np.tile(tok, (IF, 1)) if t1 else None, np.tile(pos, (IF, 1)) if t1 else None, stream=stream)
     dist.barrier()
     n0 = lib.gh_kernel_launches(0)
     for _ in range(args.warmup):
@@ -416,6 +420,10 @@ def main():
     ap.add_argument("--config", default=None, choices=[None, "C2", "C3"])
     ap.add_argument("--cpu-threads", type=int, default=0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--tier1", type=int, default=1,
+                    help="tier split: Tier-1 pipeline stages (layer spans, each with its own Tier-2 GPUs)")
+    ap.add_argument("--shard", type=int, default=0,
+                    help="C2 tier split: prompts per Tier-2 GPU per in-flight batch (default 64, the N=1 batch)")
     ap.add_argument("--inflight", type=int, default=0,
                     help="tier split: in-flight batches (0 = if_gh from the stage profiles)")
     ap.add_argument("--transport", default="auto", choices=["auto", "nccl", "peer"],
@@ -431,7 +439,10 @@ def main():
     metric = "decode tokens/s (Llama-2-7B shape, 2-tier split)"
     cfg = {"workload": f"{wl['name']}: {spec.name} shape random-init, context {wl['ctx']}, "
                        + ("both tiers colocated on 1 GPU" if wl["kp"] == 0 else
-                          f"Tier-1 on 1 GPU + Tier-2 KV sharded by prompt over {wl['kp']} GPUs, IF={wl['inflight']}"),
+                          (f"Tier-1 on 1 GPU + Tier-2 KV sharded by prompt over {wl['kp']} GPUs, IF={wl['inflight']}"
+                           if args.tier1 <= 1 else
+                           f"Tier-1 pipelined over {args.tier1} GPUs (layer spans), each span with "
+                           f"{wl['kp']} Tier-2 GPUs holding its layers' KV, IF={wl['inflight']}")),
            "batch": wl["batch"] * wl["inflight"], "requested_batch": wl["requested"], "ctx": wl["ctx"],
            "inflight": wl["inflight"], "dtype_storage": "bf16", "l2": "inputs larger than L2 (no flush)"}
     if "admitted_slots" in wl:
@@ -496,7 +507,7 @@ def main():
         step_bytes = spec.n_layers * (ab + gb) + spec.dtype_bytes * 2 * spec.vocab_size * spec.d_model // 2
         out["step_roofline"] = {"bytes_per_step": step_bytes, "ideal_ms": step_bytes / (hbm * 1e9) * 1e3,
                                 "frac": step_bytes / (hbm * 1e9) / (res["ms"] / 1e3)}
-    if not args.no_cpu_baseline and rank == 0:
+    if not args.no_cpu_baseline and world == 1:  # the CPU baseline is an N = 1 figure (rank 0 only)
         B = wl["batch"] if wl["kp"] == 0 else min(wl["batch"], 64)
         v, sample, cores, _ = cpu_sample(spec, B, wl["ctx"], args.cpu_threads)
         out["cpu_baseline"] = {"value": v, "unit": "tokens/s", "cores": cores, "kind": "port", "sample": sample}

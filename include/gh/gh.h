@@ -190,6 +190,11 @@ typedef struct gh_engine_config {
   uint32_t n_slots;        /* Tier-2 slots on this GPU (0 = exactly what the shard needs) */
   int use_graph;           /* capture the step in a CUDA graph (colocated only) */
   int transport;           /* tier split, pipelined step (gh_engine_step_all*): GH_TRANSPORT_* */
+  uint32_t tier1_ranks;    /* tier split: Tier-1 pipeline stages (0/1 = one Tier-1 rank). With T > 1
+                              ranks 0..T-1 hold contiguous layer spans (layer_spans,
+                              optimizer.cpp:116-123; embedding on the first, classifier on the
+                              last) and ranks T + s*K' + j are the K' Tier-2 ranks dedicated to
+                              span s; world = T * (1 + K').  Peer transport only. */
 } gh_engine_config;
 
 /* Inter-tier message transport of the pipelined tier-split step.

@@ -61,7 +61,8 @@ class GhEngineConfig(C.Structure):
     _fields_ = [("spec", GhSpec), ("device", C.c_int), ("weight_seed", C.c_uint64),
                 ("batch", C.c_uint32), ("inflight", C.c_uint32), ("n_slots", C.c_uint32),
                 ("use_graph", C.c_int),
-                ("transport", C.c_int)]
+                ("transport", C.c_int),
+                ("tier1_ranks", C.c_uint32)]
 
 
 u64, u32, i32, i64, vp = C.c_uint64, C.c_uint32, C.c_int32, C.c_int64, C.c_void_p

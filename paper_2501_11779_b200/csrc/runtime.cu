@@ -659,7 +659,12 @@ struct gh_engine {
   Shape sh;
   int role = 0;  // 0 colocated, 1 tier1, 2 tier2
   gh_comm* comm = nullptr;
-  int kp = 0;    // K' = number of Tier-2 ranks (split mode)
+  int kp = 0;    // K' = number of Tier-2 ranks per Tier-1 span (split mode)
+  int n1 = 1;    // Tier-1 pipeline stages (layer spans)
+  int span = 0;  // this rank's span (tier1 / tier2)
+  int shard = 0; // tier2: this rank's prompt shard within its span
+  int l0 = 0, l1 = 0;  // this rank's layers
+  int t2_rank(int sp, int j) const { return n1 + sp * kp + j; }
   gh_tier1* t1 = nullptr;
   gh_tier2* t2 = nullptr;
   std::vector<std::unique_ptr<DevMem>> mem;
@@ -688,13 +693,22 @@ struct gh_engine {
   // (cuStreamWaitValue32) -- no SM time and no NCCL kernel on either side.
   struct Peer {
     bool on = false;
-    uint32_t* flags = nullptr;                // mine: tier1 [IF][K'] bwd arrivals, tier2 [IF] fwd arrivals
-    std::vector<std::vector<void*>> fwd, pos; // tier1: [j][ib] Tier-2 rank j's fwd / pos buffers
-    std::vector<uint32_t*> rflags;            // tier1: [j] Tier-2 rank j's flags; tier2: [0] Tier-1's
-    std::vector<void*> bwd;                   // tier2: [ib] Tier-1's bwd buffers
-    std::vector<cudaStream_t> cs;             // copy streams (tier1: one per Tier-2 rank; tier2: one)
+    // my flag words, IF x (K' + 3): [ib*K' + j] bwd of Tier-2 shard j arrived (tier1),
+    // [IF*K' + ib] fwd arrived (tier2), [IF*(K'+1) + ib] activation from the previous span
+    // arrived (tier1, span > 0), [IF*(K'+2) + ib] next tokens from the last span arrived (span 0)
+    uint32_t* flags = nullptr;
+    std::vector<std::vector<void*>> fwd, pos; // tier1: [j][ib] its Tier-2 rank j's fwd / pos buffers
+    std::vector<uint32_t*> rflags;            // tier1: [j] its Tier-2 rank j's flags; tier2: [0] its Tier-1's
+    std::vector<void*> bwd;                   // tier2: [ib] its Tier-1's bwd buffers
+    uint32_t* nflags = nullptr;               // tier1 span s < n1-1: span s+1's flags
+    std::vector<void*> nx, nss, npos;         // [ib] span s+1's x0 / ss0 / pos buffers
+    uint32_t* fflags = nullptr;               // last span (n1 > 1): span 0's flags
+    std::vector<void*> fnext;                 // [ib] span 0's next-token buffers
+    std::vector<cudaStream_t> cs;             // copy streams (one per Tier-2 rank, + one to the next span)
     std::vector<cudaEvent_t> ev;              // per batch: message produced on the compute stream
-    std::vector<uint32_t> seq;                // per batch: messages exchanged so far (both directions)
+    std::vector<uint32_t> seq;                // per batch: layer messages exchanged so far (both directions)
+    std::vector<uint32_t> seqxo, seqxi;       // per batch: activations handed to / from the neighbour spans
+    std::vector<uint32_t> seqt;               // per batch: token hand-backs sent (last span) / awaited (span 0)
     std::vector<void*> opened;                // IPC mappings
   } peer;
   ~gh_engine() {
@@ -733,7 +747,10 @@ static gh_status act_classify(gh_engine* e, gh_engine::Batch& b, float* logits, 
   return t1_classify(e->t1, e->cfg.batch, b.x(b.cur), SsRef{b.ss(b.cur), b.ss_slices[b.cur]}, logits, b.next, st);
 }
 
-extern "C" { static gh_status peer_setup(gh_engine* e); }
+extern "C" {
+static gh_status peer_setup(gh_engine* e);
+static gh_status peer_wait_tokens(gh_engine* e, int ib, cudaStream_t st);
+}
 
 static gh_status engine_layer_loop_colocated(gh_engine* e, gh_engine::Batch& b, bool want_logits, cudaStream_t st) {
   const Shape& s = e->sh;
@@ -763,11 +780,25 @@ gh_status gh_engine_create(const gh_engine_config* cfg, gh_comm* comm, gh_engine
   e->comm = comm;
   const int world = comm ? comm->nranks : 1;
   const int rank = comm ? comm->rank : 0;
+  e->l0 = 0;
+  e->l1 = s.N;
   if (world == 1) {
     e->role = 0;
   } else {
-    e->role = rank == 0 ? 1 : 2;
-    e->kp = world - 1;
+    e->n1 = cfg->tier1_ranks > 1 ? (int)cfg->tier1_ranks : 1;
+    if (world <= e->n1 || (world - e->n1) % e->n1)
+      return fail(GH_EINVAL, "world size must be tier1_ranks * (1 + K') with K' >= 1");
+    if (e->n1 > s.N) return fail(GH_EINVAL, "more Tier-1 spans than layers");
+    if (e->n1 > 1 && cfg->transport == GH_TRANSPORT_NCCL)
+      return fail(GH_EUNSUPPORTED, "Tier-1 pipeline stages need the peer transport");
+    e->kp = (world - e->n1) / e->n1;
+    e->role = rank < e->n1 ? 1 : 2;
+    e->span = rank < e->n1 ? rank : (rank - e->n1) / e->kp;
+    e->shard = rank < e->n1 ? 0 : (rank - e->n1) % e->kp;
+    std::vector<uint64_t> spans(e->n1);  // contiguous layer blocks, remainder to low ranks (optimizer.cpp:116-123)
+    GH_TRY(gh_layer_spans((uint64_t)s.N, (uint64_t)e->n1, spans.data()));
+    for (int sp = 0; sp < e->span; ++sp) e->l0 += (int)spans[sp];
+    e->l1 = e->l0 + (int)spans[e->span];
     if ((int)cfg->batch < e->kp) return fail(GH_EINVAL, "batch smaller than the number of Tier-2 ranks");
     std::vector<uint64_t> off(e->kp), cnt(e->kp);  // balanced shards (analytic.cpp:119)
     GH_TRY(gh_shard_plan(cfg->batch, e->kp, off.data(), cnt.data()));
@@ -775,16 +806,17 @@ gh_status gh_engine_create(const gh_engine_config* cfg, gh_comm* comm, gh_engine
       e->shard_off.push_back((int)off[j]);
       e->shard_cnt.push_back((int)cnt[j]);
     }
-    if (e->role == 2) e->my_cnt = e->shard_cnt[rank - 1];
+    if (e->role == 2) e->my_cnt = e->shard_cnt[e->shard];
   }
   const int R = e->rows();
   if (e->role != 2)
-    GH_TRY(gh_tier1_create(&cfg->spec, cfg->device, 0, s.N, cfg->weight_seed, cfg->batch, &e->t1));
+    GH_TRY(gh_tier1_create(&cfg->spec, cfg->device, (uint32_t)e->l0, (uint32_t)e->l1, cfg->weight_seed, cfg->batch,
+                           &e->t1));
   if (e->role != 1) {
     uint32_t need = (uint32_t)R * cfg->inflight;
     uint32_t n_slots = cfg->n_slots ? cfg->n_slots : need;
     if (n_slots < need) return fail(GH_EINFEASIBLE, "n_slots smaller than batch * inflight (binding constraint: memory)");
-    GH_TRY(gh_tier2_create(&cfg->spec, cfg->device, 0, s.N, n_slots, &e->t2));
+    GH_TRY(gh_tier2_create(&cfg->spec, cfg->device, (uint32_t)e->l0, (uint32_t)e->l1, n_slots, &e->t2));
   }
   GH_CUDA(cudaEventCreateWithFlags(&e->fork, cudaEventDisableTiming));
   e->batches.resize(cfg->inflight);
@@ -816,7 +848,7 @@ gh_status gh_engine_create(const gh_engine_config* cfg, gh_comm* comm, gh_engine
   }
   GH_CUDA(cudaDeviceSynchronize());
   if (e->role != 0 && cfg->transport != GH_TRANSPORT_NCCL) GH_TRY(peer_setup(e.get()));
-  if (cfg->transport == GH_TRANSPORT_PEER && e->role != 0 && !e->peer.on)
+  if ((cfg->transport == GH_TRANSPORT_PEER || e->n1 > 1) && e->role != 0 && !e->peer.on)
     return fail(GH_EUNSUPPORTED, "peer transport requested but not available on every rank");
   *out = e.release();
   return GH_OK;
@@ -848,6 +880,9 @@ gh_status gh_engine_advance(gh_engine* e, uint32_t ib, int inc, void* stream) {
   if (!e || ib >= e->batches.size()) return fail(GH_EINVAL, "bad engine / batch index");
   if (e->role == 2) return fail(GH_EINVAL, "Tier-2 ranks hold no token state");
   auto& b = e->batches[ib];
+  if (e->role == 1 && e->span > 0) return GH_OK;  // later spans take tokens / positions from the hand-off
+  GH_CUDA(cudaSetDevice(e->cfg.device));
+  GH_TRY(peer_wait_tokens(e, (int)ib, (cudaStream_t)stream));  // first span: the last span's next tokens
   GH_CUDA(launch_advance(b.tok, b.next, b.pos, (int)e->cfg.batch, inc, (cudaStream_t)stream));
   return GH_OK;
 }
@@ -930,6 +965,7 @@ gh_status gh_engine_step_device(gh_engine* e, uint32_t ib, void* stream) {
     }
     return engine_layer_loop_colocated(e, b, false, st);
   }
+  if (e->n1 > 1) return fail(GH_EUNSUPPORTED, "Tier-1 pipeline stages: use gh_engine_step_all / step_all_host");
   ncclComm_t comm = e->comm->comms[0];
   GH_TRY(split_begin(e, b, comm, st));
   for (int l = 0; l < e->sh.N; ++l) GH_TRY(split_layer(e, b, comm, l, st));
@@ -1020,25 +1056,42 @@ MemOps& memops() {
 // Collective over all ranks of the engine's communicator: export this rank's receive buffers as
 // CUDA IPC handles, all-gather them, map the peers' buffers.  The transport is enabled only if
 // every rank mapped every buffer it needs (all-reduce min of the outcome), so all ranks agree.
+// Exported slots per rank: [flags, fwd x IF, pos x IF, bwd x IF, x0 x IF, ss0 x IF, next x IF].
 static gh_status peer_setup(gh_engine* e) {
   auto& api = nccl();
   auto& P = e->peer;
-  const int IF = (int)e->batches.size(), kp = e->kp, world = kp + 1, rank = e->comm->rank;
-  const int nslot = 1 + 3 * IF;
+  const int IF = (int)e->batches.size(), kp = e->kp, world = e->comm->nranks, rank = e->comm->rank;
+  const int n1 = e->n1;
+  const int nslot = 1 + 6 * IF;
+  auto slot_fwd = [&](int ib) { return 1 + ib; };
+  auto slot_pos = [&](int ib) { return 1 + IF + ib; };
+  auto slot_bwd = [&](int ib) { return 1 + 2 * IF + ib; };
+  auto slot_x0 = [&](int ib) { return 1 + 3 * IF + ib; };
+  auto slot_ss0 = [&](int ib) { return 1 + 4 * IF + ib; };
+  auto slot_next = [&](int ib) { return 1 + 5 * IF + ib; };
   ncclComm_t comm = e->comm->comms[0];
   void* p;
-  GH_TRY(dev_alloc(e->mem, (size_t)IF * std::max(kp, 1) * 4, &p));
+  const size_t nflags = (size_t)IF * (kp + 3);
+  GH_TRY(dev_alloc(e->mem, nflags * 4, &p));
   P.flags = (uint32_t*)p;
-  GH_CUDA(cudaMemset(P.flags, 0, (size_t)IF * std::max(kp, 1) * 4));
+  GH_CUDA(cudaMemset(P.flags, 0, nflags * 4));
   std::vector<cudaIpcMemHandle_t> mine(nslot);
   memset(mine.data(), 0, nslot * sizeof(cudaIpcMemHandle_t));
   int ok = memops().wait && memops().write;
-  auto get = [&](int i, void* ptr) { if (cudaIpcGetMemHandle(&mine[i], ptr) != cudaSuccess) { cudaGetLastError(); ok = 0; } };
+  auto get = [&](int i, void* ptr) {
+    if (ptr && cudaIpcGetMemHandle(&mine[i], ptr) != cudaSuccess) { cudaGetLastError(); ok = 0; }
+  };
   get(0, P.flags);
   for (int ib = 0; ib < IF; ++ib) {
     auto& b = e->batches[ib];
-    if (e->role == 2) { get(1 + ib, b.fwd); get(1 + IF + ib, b.pos); }
-    else get(1 + 2 * IF + ib, b.bwd);
+    get(slot_fwd(ib), b.fwd);
+    get(slot_pos(ib), b.pos);
+    get(slot_bwd(ib), b.bwd);
+    if (e->role == 1) {
+      get(slot_x0(ib), b.x0);
+      if (b.ss0) get(slot_ss0(ib), b.ss0);
+      get(slot_next(ib), b.next);
+    }
   }
   const size_t rec = nslot * sizeof(cudaIpcMemHandle_t);
   void *dmine, *dall, *dok;
@@ -1067,12 +1120,26 @@ static gh_status peer_setup(gh_engine* e) {
     P.fwd.assign(kp, std::vector<void*>(IF, nullptr));
     P.pos.assign(kp, std::vector<void*>(IF, nullptr));
     for (int j = 0; j < kp; ++j) {
-      P.rflags.push_back((uint32_t*)open(j + 1, 0));
-      for (int ib = 0; ib < IF; ++ib) { P.fwd[j][ib] = open(j + 1, 1 + ib); P.pos[j][ib] = open(j + 1, 1 + IF + ib); }
+      const int r = e->t2_rank(e->span, j);
+      P.rflags.push_back((uint32_t*)open(r, 0));
+      for (int ib = 0; ib < IF; ++ib) { P.fwd[j][ib] = open(r, slot_fwd(ib)); P.pos[j][ib] = open(r, slot_pos(ib)); }
+    }
+    if (e->span + 1 < n1) {  // activation hand-off to the next span (the PP message is [x], netmodel.cpp:22)
+      const int r = e->span + 1;
+      P.nflags = (uint32_t*)open(r, 0);
+      for (int ib = 0; ib < IF; ++ib) {
+        P.nx.push_back(open(r, slot_x0(ib)));
+        P.nss.push_back(e->batches[ib].ss0 ? open(r, slot_ss0(ib)) : nullptr);
+        P.npos.push_back(open(r, slot_pos(ib)));
+      }
+    }
+    if (n1 > 1 && e->span == n1 - 1) {  // next tokens back to the first span (it owns the embedding)
+      P.fflags = (uint32_t*)open(0, 0);
+      for (int ib = 0; ib < IF; ++ib) P.fnext.push_back(open(0, slot_next(ib)));
     }
   } else {
-    P.rflags.push_back((uint32_t*)open(0, 0));
-    for (int ib = 0; ib < IF; ++ib) P.bwd.push_back(open(0, 1 + 2 * IF + ib));
+    P.rflags.push_back((uint32_t*)open(e->span, 0));
+    for (int ib = 0; ib < IF; ++ib) P.bwd.push_back(open(e->span, slot_bwd(ib)));
   }
   (void)rank;
   GH_CUDA(cudaMemcpy(dok, &ok, 4, cudaMemcpyHostToDevice));
@@ -1085,7 +1152,7 @@ static gh_status peer_setup(gh_engine* e) {
     P.opened.clear();
     return GH_OK;  // NCCL send/recv transport
   }
-  const int ncs = e->role == 1 ? kp : 1;
+  const int ncs = e->role == 1 ? kp + 1 : 1;
   for (int j = 0; j < ncs; ++j) {
     cudaStream_t c;
     GH_CUDA(cudaStreamCreateWithFlags(&c, cudaStreamNonBlocking));
@@ -1097,12 +1164,21 @@ static gh_status peer_setup(gh_engine* e) {
     P.ev.push_back(v);
   }
   P.seq.assign(IF, 0);
+  P.seqxo.assign(IF, 0);
+  P.seqxi.assign(IF, 0);
+  P.seqt.assign(IF, 0);
   P.on = true;
   return GH_OK;
 }
 
+// flag word offsets (gh_engine::Peer::flags)
+static uint32_t f_bwd(const gh_engine* e, int ib, int j) { return (uint32_t)(ib * e->kp + j); }
+static uint32_t f_fwd(const gh_engine* e, int ib) { return (uint32_t)(e->batches.size() * e->kp + ib); }
+static uint32_t f_x(const gh_engine* e, int ib) { return (uint32_t)(e->batches.size() * (e->kp + 1) + ib); }
+static uint32_t f_tok(const gh_engine* e, int ib) { return (uint32_t)(e->batches.size() * (e->kp + 2) + ib); }
+
 // Tier-1: copy batch ib's fwd message shards (and, at the first layer of a step, its positions)
-// into every Tier-2 rank's buffers, then publish the sequence number in that rank's flag word.
+// into every Tier-2 rank of this span, then publish the sequence number in that rank's flag word.
 static gh_status peer_send_fwd(gh_engine* e, int ib, bool with_pos, cudaStream_t st) {
   auto& P = e->peer;
   auto& b = e->batches[ib];
@@ -1116,53 +1192,123 @@ static gh_status peer_send_fwd(gh_engine* e, int ib, bool with_pos, cudaStream_t
       GH_CUDA(cudaMemcpyAsync(P.pos[j][ib], b.pos + e->shard_off[j], (size_t)e->shard_cnt[j] * 4, cudaMemcpyDeviceToDevice, c));
     GH_CUDA(cudaMemcpyAsync(P.fwd[j][ib], (char*)b.fwd + e->shard_off[j] * fwd_row, e->shard_cnt[j] * fwd_row,
                             cudaMemcpyDeviceToDevice, c));
-    GH_CU(memops().write((CUstream)c, (CUdeviceptr)(P.rflags[j] + ib), sq, CU_STREAM_WRITE_VALUE_DEFAULT));
+    GH_CU(memops().write((CUstream)c, (CUdeviceptr)(P.rflags[j] + f_fwd(e, ib)), sq, CU_STREAM_WRITE_VALUE_DEFAULT));
   }
   return GH_OK;
 }
 
+// Sums-of-squares slices the last W2 epilogue of a span wrote (the next span's first QKV applies
+// its RMSNorm from them, exactly as inside one span); 0 = the unfused path.
+static int handoff_ss_slices(gh_engine* e) {
+  const Shape& s = e->sh;
+  const int B = (int)e->cfg.batch;
+  if (s.db != 2 || B > kFusedNormMaxBatch) return 0;
+  return e->t1->plan(s.D, s.Dh, B).slices();
+}
+
+// Tier-1 span s -> s+1: the activation x (+ its sums of squares and the positions) of batch ib.
+static gh_status peer_send_next_span(gh_engine* e, int ib, cudaStream_t st) {
+  auto& P = e->peer;
+  auto& b = e->batches[ib];
+  const Shape& s = e->sh;
+  const size_t R = e->cfg.batch;
+  const uint32_t sq = ++P.seqxo[ib];
+  cudaStream_t c = P.cs[e->kp];
+  GH_CUDA(cudaEventRecord(P.ev[ib], st));
+  GH_CUDA(cudaStreamWaitEvent(c, P.ev[ib], 0));
+  GH_CUDA(cudaMemcpyAsync(P.nx[ib], b.x(b.cur), R * s.D * s.db, cudaMemcpyDeviceToDevice, c));
+  const int sl = b.ss_slices[b.cur];
+  if (P.nss[ib] && sl > 0)
+    GH_CUDA(cudaMemcpyAsync(P.nss[ib], b.ss(b.cur), (size_t)sl * R * sizeof(float), cudaMemcpyDeviceToDevice, c));
+  GH_CUDA(cudaMemcpyAsync(P.npos[ib], b.pos, R * 4, cudaMemcpyDeviceToDevice, c));
+  GH_CU(memops().write((CUstream)c, (CUdeviceptr)(P.nflags + f_x(e, ib)), sq, CU_STREAM_WRITE_VALUE_DEFAULT));
+  return GH_OK;
+}
+
+// Last span -> first span: the greedy next tokens of batch ib (the first span owns the embedding).
+static gh_status peer_send_tokens(gh_engine* e, int ib, cudaStream_t st) {
+  auto& P = e->peer;
+  auto& b = e->batches[ib];
+  const uint32_t sq = ++P.seqt[ib];
+  cudaStream_t c = P.cs[e->kp];
+  GH_CUDA(cudaEventRecord(P.ev[ib], st));
+  GH_CUDA(cudaStreamWaitEvent(c, P.ev[ib], 0));
+  GH_CUDA(cudaMemcpyAsync(P.fnext[ib], b.next, e->cfg.batch * 4, cudaMemcpyDeviceToDevice, c));
+  GH_CU(memops().write((CUstream)c, (CUdeviceptr)(P.fflags + f_tok(e, ib)), sq, CU_STREAM_WRITE_VALUE_DEFAULT));
+  return GH_OK;
+}
+
+// First span with n1 > 1: the next tokens of the previous step of batch ib have landed in b.next.
+static gh_status peer_wait_tokens(gh_engine* e, int ib, cudaStream_t st) {
+  auto& P = e->peer;
+  if (!P.on || e->n1 == 1 || e->role != 1 || e->span != 0) return GH_OK;
+  if (P.seqt[ib] >= P.seqxo[ib]) return GH_OK;  // already awaited (or no step run yet)
+  P.seqt[ib] = P.seqxo[ib];                     // one hand-back per step this span ran
+  GH_CU(memops().wait((CUstream)st, (CUdeviceptr)(P.flags + f_tok(e, ib)), P.seqt[ib], CU_STREAM_WAIT_VALUE_GEQ));
+  return GH_OK;
+}
+
+// One pipelined step of every in-flight batch over the peer transport.  Per Tier-1 span:
+//   span 0:  embed_b -> F1_b(l0) -> fwd;   span s > 0: wait x_b from span s-1 -> F1_b(l0) -> fwd
+//   for each (layer l, batch b): wait attention of every shard -> F3_b(l) -> F1_b(l+1) -> fwd,
+//   after the span's last layer: classifier (last span, tokens back to span 0) or x -> span s+1.
+// Tier-2 rank: for each (layer, batch): wait fwd -> F2 (+ KV append) -> bwd back.
 static gh_status split_step_peer(gh_engine* e, cudaStream_t st) {
   auto& P = e->peer;
+  const int nb = (int)e->batches.size();
   // diagnostics: GH_SPLIT_NOWAIT=1 drops the flag waits (wrong results; isolates compute time)
   static const bool nowait = getenv("GH_SPLIT_NOWAIT") != nullptr;
-  const int nb = (int)e->batches.size();
-  const int N = e->sh.N;
   if (e->role == 1) {
+    const bool first = e->span == 0, last = e->span == e->n1 - 1;
     for (int ib = 0; ib < nb; ++ib) {
       auto& b = e->batches[ib];
-      GH_TRY(act_embed(e, b, st));
-      GH_TRY(act_pre(e, b, 0, st));
+      if (first) {
+        GH_TRY(act_embed(e, b, st));
+      } else {
+        // the previous span's activation (x, its sums of squares, the positions) has landed
+        ++P.seqxi[ib];
+        if (!nowait)
+          GH_CU(memops().wait((CUstream)st, (CUdeviceptr)(P.flags + f_x(e, ib)), P.seqxi[ib],
+                              CU_STREAM_WAIT_VALUE_GEQ));
+        b.cur = 0;
+        b.ss_slices[0] = handoff_ss_slices(e);
+      }
+      GH_TRY(act_pre(e, b, e->l0, st));
       GH_TRY(peer_send_fwd(e, ib, true, st));
     }
-    for (int l = 0; l < N; ++l)
+    for (int l = e->l0; l < e->l1; ++l)
       for (int ib = 0; ib < nb; ++ib) {
         auto& b = e->batches[ib];
         for (int j = 0; j < e->kp && !nowait; ++j)  // every shard of the attention output has landed
-          GH_CU(memops().wait((CUstream)st, (CUdeviceptr)(P.flags + ib * e->kp + j), P.seq[ib],
+          GH_CU(memops().wait((CUstream)st, (CUdeviceptr)(P.flags + f_bwd(e, ib, j)), P.seq[ib],
                               CU_STREAM_WAIT_VALUE_GEQ));
         GH_TRY(act_post(e, b, l, st));
-        if (l + 1 < N) {
+        if (l + 1 < e->l1) {
           GH_TRY(act_pre(e, b, l + 1, st));
           GH_TRY(peer_send_fwd(e, ib, false, st));
-        } else {
+        } else if (last) {
           GH_TRY(act_classify(e, b, nullptr, st));
+          if (e->n1 > 1) GH_TRY(peer_send_tokens(e, ib, st));
+        } else {
+          GH_TRY(peer_send_next_span(e, ib, st));
         }
       }
   } else {
     const size_t bwd_row = (size_t)e->sh.ld_bwd() * e->sh.db;
-    const int me = e->comm->rank - 1;
-    for (int l = 0; l < N; ++l)
+    const int me = e->shard;
+    for (int l = e->l0; l < e->l1; ++l)
       for (int ib = 0; ib < nb; ++ib) {
         auto& b = e->batches[ib];
         const uint32_t sq = ++P.seq[ib];
-        if (!nowait) GH_CU(memops().wait((CUstream)st, (CUdeviceptr)(P.flags + ib), sq, CU_STREAM_WAIT_VALUE_GEQ));
+        if (!nowait)
+          GH_CU(memops().wait((CUstream)st, (CUdeviceptr)(P.flags + f_fwd(e, ib)), sq, CU_STREAM_WAIT_VALUE_GEQ));
         GH_TRY(gh_tier2_attend(e->t2, l, e->my_cnt, b.slot, b.pos, b.fwd, b.bwd, st));
         GH_CUDA(cudaEventRecord(P.ev[ib], st));
         cudaStream_t c = P.cs[0];
         GH_CUDA(cudaStreamWaitEvent(c, P.ev[ib], 0));
         GH_CUDA(cudaMemcpyAsync((char*)P.bwd[ib] + e->shard_off[me] * bwd_row, b.bwd, e->my_cnt * bwd_row,
                                 cudaMemcpyDeviceToDevice, c));
-        GH_CU(memops().write((CUstream)c, (CUdeviceptr)(P.rflags[0] + ib * e->kp + me), sq,
+        GH_CU(memops().write((CUstream)c, (CUdeviceptr)(P.rflags[0] + f_bwd(e, ib, me)), sq,
                              CU_STREAM_WRITE_VALUE_DEFAULT));
       }
   }
@@ -1171,6 +1317,7 @@ static gh_status split_step_peer(gh_engine* e, cudaStream_t st) {
 
 static gh_status split_step_pipelined(gh_engine* e, cudaStream_t st) {
   if (e->peer.on) return split_step_peer(e, st);
+  if (e->n1 > 1) return fail(GH_EUNSUPPORTED, "Tier-1 pipeline stages need the peer transport");
   const int nb = (int)e->batches.size();
   const int N = e->sh.N;
   ncclComm_t comm = e->comm->comms[0];
@@ -1232,8 +1379,9 @@ gh_status gh_engine_step_all_host(gh_engine* e, const int32_t* tok_host, const i
   cudaStream_t st = (cudaStream_t)stream;
   GH_CUDA(cudaSetDevice(e->cfg.device));
   const size_t R = e->cfg.batch;
-  if (e->role != 2) {
-    if (!tok_host || !pos_host || !next_host) return fail(GH_EINVAL, "host token/pos/next buffers required");
+  if (e->role != 2 && !next_host) return fail(GH_EINVAL, "host next-token buffer required");
+  if (e->role != 2 && e->span == 0) {
+    if (!tok_host || !pos_host) return fail(GH_EINVAL, "host token/pos buffers required");
     for (size_t ib = 0; ib < e->batches.size(); ++ib) {
       GH_CUDA(cudaMemcpyAsync(e->batches[ib].tok, tok_host + ib * R, R * 4, cudaMemcpyHostToDevice, st));
       GH_CUDA(cudaMemcpyAsync(e->batches[ib].pos, pos_host + ib * R, R * 4, cudaMemcpyHostToDevice, st));
@@ -1262,6 +1410,7 @@ gh_status gh_engine_step_host(gh_engine* e, uint32_t ib, const int32_t* tok_host
   if (logits_host && e->role == 0) {
     GH_TRY(engine_layer_loop_colocated(e, b, true, st));
   } else if (logits_host && e->role == 1) {
+    if (e->n1 > 1) return fail(GH_EUNSUPPORTED, "Tier-1 pipeline stages: use gh_engine_step_all / step_all_host");
     ncclComm_t comm = e->comm->comms[0];
     GH_TRY(split_begin(e, b, comm, st));
     for (int l = 0; l < e->sh.N; ++l) GH_TRY(split_layer(e, b, comm, l, st));

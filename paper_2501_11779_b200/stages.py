@@ -153,10 +153,10 @@ class Engine:
 
     def __init__(self, spec: ModelSpec, batch: int, inflight: int = 1, device: int = 0,
                  weight_seed: int = 1234, n_slots: int = 0, use_graph: bool = True,
-                 comm: Comm | None = None, transport: str = "auto"):
+                 comm: Comm | None = None, transport: str = "auto", tier1_ranks: int = 1):
         self.spec, self.batch, self.inflight = spec, batch, inflight
         cfg = L.GhEngineConfig(spec.c(), device, weight_seed, batch, inflight, n_slots, int(use_graph),
-                               self.TRANSPORTS[transport])
+                               self.TRANSPORTS[transport], tier1_ranks)
         h = C.c_void_p()
         L.check(L.lib().gh_engine_create(C.byref(cfg), comm.h if comm else None, C.byref(h)))
         self.h = h

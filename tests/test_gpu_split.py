@@ -158,3 +158,61 @@ def test_pipelined_step_all_matches_colocated(world, IF, transport):
         assert p.exitcode == 0
     ref = run_all(Engine(SPEC, batch=B, inflight=IF, use_graph=False), IF)
     assert np.array_equal(got, ref)
+
+
+def worker_pp(rank, world, port, q, IF, n1):
+    """Tier-1 pipeline stages (n1 spans, each with its own Tier-2 ranks): step_all_host for the
+    first step, then advance + step_all; the last span reports the next tokens."""
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    import torch
+    import torch.distributed as dist
+    from paper_2501_11779_b200.stages import Comm, Engine
+    torch.cuda.set_device(rank)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    obj = [Comm.unique_ids(1) if rank == 0 else None]
+    dist.broadcast_object_list(obj, src=0)
+    comm = Comm(obj[0], world, rank, rank)
+    eng = Engine(SPEC, batch=B, inflight=IF, device=rank, use_graph=False, comm=comm, transport="peer",
+                 tier1_ranks=n1)
+    p = prompts()
+    t1 = eng.role == "tier1"
+    toks = np.stack([np.roll(p[:, 0], ib) for ib in range(IF)]) if t1 else None
+    eng.step_all_host(toks, np.zeros((IF, B), np.int32) if t1 else None)
+    seq = []
+    for _ in range(STEPS):
+        if t1:
+            for ib in range(IF):
+                eng.advance(ib, 1)
+        eng.step_all()
+        if t1:
+            seq.append(np.stack([eng.read_next(ib) for ib in range(IF)]))
+    eng.close()
+    comm.close()
+    if rank == n1 - 1:
+        q.put(np.stack(seq))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.skipif(n_gpus() < 4, reason="needs >= 4 GPUs")
+def test_tier1_pipeline_stages_match_colocated():
+    """SURVEY 8(e) config-5 topology at small scale: 2 Tier-1 spans (layers split by
+    layer_spans), each with a dedicated Tier-2 rank; tokens identical to the colocated engine."""
+    import torch.multiprocessing as mp
+    from paper_2501_11779_b200.stages import Engine
+    world, IF, n1 = 4, 2, 2
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=worker_pp, args=(r, world, port, q, IF, n1)) for r in range(world)]
+    for p in procs:
+        p.start()
+    got = q.get(timeout=600)
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    ref = run_all(Engine(SPEC, batch=B, inflight=IF, use_graph=False), IF)
+    assert np.array_equal(got, ref)
