@@ -105,6 +105,95 @@ def test_tier_split_protocol_matches_colocated(world):
     assert np.array_equal(slg, lg)
 
 
+def worker_pp(rank, world, port, out_q):
+    """Tier-1 pipeline stages (SURVEY 8e, config 5 at toy scale): ranks 0/1 are Tier-1 spans of
+    layer_spans(N, 2), ranks 2/3 each the single Tier-2 rank of span 0/1 (its layers' KV). Span 0
+    embeds, hands [x] (PayloadModel intra-Tier-1 message, netmodel.cpp:22) plus the positions to
+    span 1; span 1 classifies and hands the next tokens back to span 0."""
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from oracle import Oracle
+    n1 = 2
+    spans = gh.layer_spans(SPEC.n_layers, n1)
+    lo = [sum(spans[:s]) for s in range(n1)]
+    prompts = np.random.default_rng(2).integers(0, SPEC.vocab_size, size=(B, 2), dtype=np.int32)
+    D, Dkv = SPEC.d_model, SPEC.d_kv
+    if rank < n1:
+        sp = rank
+        ora = Oracle(SPEC, seed=SEED, n_slots=1)
+        x, fwd, bwd = ora.buffers(B)
+        tok = prompts[:, 0].copy()
+        out = []
+        for t in range(1 + STEPS):
+            if sp == 0:
+                pos = np.full(B, t, np.int32)
+                ora.embed(tok, x)
+            else:
+                pos_t = torch.zeros(B, dtype=torch.int32)
+                dist.recv(pos_t, src=sp - 1)
+                pos = pos_t.numpy().copy()
+                xb = torch.zeros((B, D), dtype=torch.int16)
+                dist.recv(xb, src=sp - 1)
+                x = xb.numpy().view(np.uint16).copy()
+            dist.send(torch.from_numpy(pos.copy()), dst=n1 + sp)      # positions to my Tier-2
+            for layer in range(lo[sp], lo[sp] + spans[sp]):
+                ora.pre(layer, x, pos, fwd)
+                dist.send(torch.from_numpy(fwd.view(np.int16).copy()), dst=n1 + sp)
+                buf = torch.zeros((B, 2 * D), dtype=torch.int16)
+                dist.recv(buf, src=n1 + sp)
+                bwd[:] = buf.numpy().view(np.uint16)
+                x2 = np.zeros_like(x)
+                ora.post(layer, bwd, x2)
+                x = x2
+            if sp + 1 < n1:
+                dist.send(torch.from_numpy(pos.copy()), dst=sp + 1)
+                dist.send(torch.from_numpy(x.view(np.int16).copy()), dst=sp + 1)
+            if sp == n1 - 1:
+                nxt, lg = ora.classify(x)
+                if t >= 1:
+                    out.append((nxt.copy(), lg.copy()))
+                dist.send(torch.from_numpy(nxt.astype(np.int32)), dst=0)
+            if sp == 0:
+                nt = torch.zeros(B, dtype=torch.int32)
+                dist.recv(nt, src=n1 - 1)
+                tok = prompts[:, 1].copy() if t == 0 else nt.numpy().copy()
+        if sp == n1 - 1:
+            out_q.put((np.stack([o[0] for o in out], 1), np.stack([o[1] for o in out], 1)))
+    else:
+        sp = rank - n1
+        ora = Oracle(SPEC, seed=SEED, n_slots=B)        # this span's layers of every prompt
+        slot = np.arange(B, dtype=np.uint32)
+        for t in range(1 + STEPS):
+            pos_t = torch.zeros(B, dtype=torch.int32)
+            dist.recv(pos_t, src=sp)
+            pos = pos_t.numpy()
+            for layer in range(lo[sp], lo[sp] + spans[sp]):
+                buf = torch.zeros((B, 2 * D + 2 * Dkv), dtype=torch.int16)
+                dist.recv(buf, src=sp)
+                fwd = buf.numpy().view(np.uint16).copy()
+                bwd = np.zeros((B, 2 * D), np.uint16)
+                ora.attend(layer, slot, pos, fwd, bwd)
+                dist.send(torch.from_numpy(bwd.view(np.int16).copy()), dst=sp)
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_tier1_pipeline_protocol_matches_colocated():
+    _, gen, lg = reference_tokens()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = free_port()
+    procs = [ctx.Process(target=worker_pp, args=(r, 4, port, q)) for r in range(4)]
+    for p in procs:
+        p.start()
+    sgen, slg = q.get(timeout=240)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    assert np.array_equal(sgen, gen)
+    assert np.array_equal(slg, lg)
+
+
 def test_shard_plan_balanced():
     for batch, kp in ((1024, 7), (7, 3), (170, 1), (1190, 7)):
         off, cnt = gh.shard_plan(batch, kp)
