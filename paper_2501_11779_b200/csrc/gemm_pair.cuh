@@ -276,6 +276,9 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
 #pragma unroll 1
       for (int c0 = 0; c0 < BN; c0 += 32) {
         tx = trace ? globaltimer() : 0;
+        // this chunk's global epilogue inputs first: their latency overlaps the TMEM drain
+        EpiPre<32> pre;
+        if (owner && !skip) epi_prefetch<32, 32>(ep, gs, n0 + rl, b0 + c0 + cb, pre, pos_cached ? pos_smem : nullptr);
         uint32_t r0[16], r1[16];
         tmem_ld16(taddr + c0, r0);
         tmem_ld16(taddr + c0 + 16, r1);
@@ -319,7 +322,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         }
         if (trace) { const unsigned long long n = globaltimer(); tc += n - tx; tx = n; }
         epi_slice<32, 32, 32>(ep, gs, n0 + rl, b0 + c0 + cb, o, 2 * tile_n + rank, inv_smem,
-                              pos_cached ? pos_smem : nullptr);
+                              pos_cached ? pos_smem : nullptr, &pre);
         epi_bar();  // staging is reused by the next chunk
         if (trace) { const unsigned long long n = globaltimer(); td += n - tx; tx = n; }
       }

@@ -112,28 +112,93 @@ GH_DEV void compute_inv_rms(const EpiParams& ep, const GemmShape& gs, float* inv
   }
 }
 
+// Global inputs of a slice epilogue (residual rows, x rows to copy, RoPE table entries), loaded
+// ahead of the epilogue arithmetic so that their latency overlaps the TMEM drain / staging
+// (epi_prefetch); ok == false: the tile edge or alignment needs the direct path in epi_slice.
+template <int En>
+struct EpiPre {
+  uint4 a[En / 8 > 0 ? En / 8 : 1];  // residual (STORE_RESID) or x to copy (QKV_ROPE)
+  float2 cs[En / 2 > 0 ? En / 2 : 1];  // RoPE (cos, sin) of every row pair (QKV_ROPE)
+  bool ok;
+};
+
+template <int En, int RS = 8>
+GH_DEV void epi_prefetch(const EpiParams& ep, const GemmShape& gs, int n, int b, EpiPre<En>& p,
+                         const int* pos_smem = nullptr) {
+  auto off = [](int e) { return (e >> 3) * RS + (e & 7); };
+  p.ok = false;
+  if (En % 8 || b >= gs.Bt || n + off(En - 1) >= gs.N) return;
+  if (ep.kind == EPI_STORE_RESID) {
+    const uint16_t* rp = (const uint16_t*)ep.resid + (long)b * ep.ldr + n;
+    if (((uintptr_t)rp & 15) != 0) return;
+#pragma unroll
+    for (int j = 0; j < En / 8; ++j) p.a[j] = __ldg((const uint4*)(rp + j * RS));
+    p.ok = true;
+  } else if (ep.kind == EPI_QKV_ROPE) {
+    if (ep.xcopy_src && n < ep.xcopy_rows) {
+      const uint16_t* xs = (const uint16_t*)ep.xcopy_src + (long)b * ep.xcopy_ld + n;
+      const uint16_t* xd = (const uint16_t*)ep.out + (long)b * ep.ldo + n - ep.xcopy_rows;
+      if (n + off(En - 1) >= ep.xcopy_rows || ((uintptr_t)xs & 15) || ((uintptr_t)xd & 15)) return;
+#pragma unroll
+      for (int j = 0; j < En / 8; ++j) p.a[j] = __ldg((const uint4*)(xs + j * RS));
+    }
+    if (n < ep.rope_rows) {
+      const float2* cs = ep.rope + (long)(pos_smem ? pos_smem[b] : __ldg(ep.pos + b)) * (ep.d_head >> 1);
+      int hb = 0;
+#pragma unroll
+      for (int e = 0; e < En; e += 2) {
+        if ((e & 7) == 0) hb = ((n + off(e)) % ep.d_head) >> 1;
+        p.cs[e >> 1] = __ldg(cs + hb + ((e & 7) >> 1));
+      }
+    }
+    p.ok = true;
+  }
+}
+
 template <int BN, int En, int RS = 8>
 GH_DEV void epi_slice(const EpiParams& ep, const GemmShape& gs, int n, int b, float (&v)[En], int slice,
-                      const float* inv, const int* pos_smem = nullptr) {
+                      const float* inv, const int* pos_smem = nullptr, const EpiPre<En>* pre = nullptr) {
   // element e of this thread is output row n + off(e)
   auto off = [](int e) { return (e >> 3) * RS + (e & 7); };
   const bool col_ok = b < gs.Bt;
   const bool full = n + off(En - 1) < gs.N;
+  const bool pok = pre && pre->ok;
   if (ep.ss_in && col_ok) {  // fused RMSNorm of the GEMM input
     const float sc = inv[b];
 #pragma unroll
     for (int e = 0; e < En; ++e) v[e] *= sc;
   }
+  bool resid_added = false;
+  if (pok && ep.kind == EPI_STORE_RESID) {  // residual from the prefetched rows
+#pragma unroll
+    for (int j = 0; j < En / 8; ++j) {
+      const uint32_t w[4] = {pre->a[j].x, pre->a[j].y, pre->a[j].z, pre->a[j].w};
+#pragma unroll
+      for (int h = 0; h < 4; ++h) {
+        v[8 * j + 2 * h] += __uint_as_float(w[h] << 16);
+        v[8 * j + 2 * h + 1] += __uint_as_float(w[h] & 0xffff0000u);
+      }
+    }
+    resid_added = true;
+  }
   if (ep.ss_out) {  // sums of squares of the rounded outputs, reduced over the slice's threads
     constexpr int kRuns = 128 / BN;
     float sq = 0.f;
     if (col_ok && ep.kind == EPI_STORE_RESID) {
-      const uint16_t* rp = (const uint16_t*)ep.resid + (long)b * ep.ldr + n;
+      if (resid_added) {
 #pragma unroll
-      for (int e = 0; e < En; ++e) {
-        if (full || n + off(e) < gs.N) {
-          const float y = bf16_to_f32(f32_to_bf16(v[e] + bf16_to_f32(rp[off(e)])));
+        for (int e = 0; e < En; ++e) {
+          const float y = bf16_to_f32(f32_to_bf16(v[e]));
           sq = fmaf(y, y, sq);
+        }
+      } else {
+        const uint16_t* rp = (const uint16_t*)ep.resid + (long)b * ep.ldr + n;
+#pragma unroll
+        for (int e = 0; e < En; ++e) {
+          if (full || n + off(e) < gs.N) {
+            const float y = bf16_to_f32(f32_to_bf16(v[e] + bf16_to_f32(rp[off(e)])));
+            sq = fmaf(y, y, sq);
+          }
         }
       }
     }
@@ -149,7 +214,7 @@ GH_DEV void epi_slice(const EpiParams& ep, const GemmShape& gs, int n, int b, fl
     case EPI_STORE:
     case EPI_STORE_RESID: {
       if (!col_ok) return;
-      if (ep.kind == EPI_STORE_RESID) {
+      if (ep.kind == EPI_STORE_RESID && !resid_added) {
         const uint16_t* rp = (const uint16_t*)ep.resid + (long)b * ep.ldr + n;
         if (full && En % 8 == 0 && ((uintptr_t)rp & 15) == 0) {
           uint4 rr[En / 8 > 0 ? En / 8 : 1];
@@ -179,6 +244,24 @@ GH_DEV void epi_slice(const EpiParams& ep, const GemmShape& gs, int n, int b, fl
     }
     case EPI_QKV_ROPE: {
       if (!col_ok) return;
+      if (pok) {  // prefetched x rows and RoPE entries
+        if (ep.xcopy_src && n < ep.xcopy_rows) {
+          uint16_t* xd = (uint16_t*)ep.out + (long)b * ep.ldo + n - ep.xcopy_rows;
+#pragma unroll
+          for (int j = 0; j < En / 8; ++j) *(uint4*)(xd + j * RS) = pre->a[j];
+        }
+        if (n < ep.rope_rows) {
+#pragma unroll
+          for (int e = 0; e < En; e += 2) {
+            const float2 c = pre->cs[e >> 1];
+            const float a = v[e], o = v[e + 1];
+            v[e] = a * c.x - o * c.y;
+            v[e + 1] = a * c.y + o * c.x;
+          }
+        }
+        store_run_bf16<En, RS>((uint16_t*)ep.out + (long)b * ep.ldo + n, v);
+        return;
+      }
       if (ep.xcopy_src && n < ep.xcopy_rows) {  // x into the message's x slot (fused RMSNorm path)
         const uint16_t* xs = (const uint16_t*)ep.xcopy_src + (long)b * ep.xcopy_ld + n;
         uint16_t* xd = (uint16_t*)ep.out + (long)b * ep.ldo + n - ep.xcopy_rows;
@@ -310,7 +393,7 @@ GH_DEV void push_partial(uint32_t recv_saddr, int rank, int row, const float* v1
 template <int BN, int C>
 GH_DEV void reduce_and_store(const EpiParams& ep, const GemmShape& gs, const float* recv, int r, int n0,
                              int b0, int tile_n, uint32_t consumed_saddr, unsigned long long* tr,
-                             const float* inv) {
+                             const float* inv, uint64_t* ready, uint32_t ready_parity) {
   // thread -> (column b, run of En rows inside this CTA's slice of R = 128/C rows)
   constexpr int R = 128 / C;
   constexpr int En = BN / C;
@@ -318,6 +401,14 @@ GH_DEV void reduce_and_store(const EpiParams& ep, const GemmShape& gs, const flo
   const int t = threadIdx.x - 64;
   const int b = t / kRuns;
   const int rl = (t % kRuns) * En;
+  // the epilogue's global inputs are requested before waiting for the peers' partials (runs of
+  // up to 32 rows: longer runs would not fit the register budget)
+  constexpr int Ep = En <= 32 ? En : 1;
+  EpiPre<Ep> pre;
+  pre.ok = false;
+  if constexpr (En <= 32) epi_prefetch<En>(ep, gs, n0 + r * R + rl, b0 + b, pre);
+  mbar_wait_cluster(ready, ready_parity);  // every peer's push into my buffer is visible
+  if (tr) tr[11] = globaltimer();
   float v[En];
 #pragma unroll
   for (int e = 0; e < En; e += 4) {
@@ -334,7 +425,8 @@ GH_DEV void reduce_and_store(const EpiParams& ep, const GemmShape& gs, const flo
   epi_bar();
   if (threadIdx.x == 64)
     for (int p = 0; p < C; ++p) mbar_arrive_cluster_relaxed(mapa_shared(consumed_saddr, p));
-  epi_slice<BN, En>(ep, gs, n0 + r * R + rl, b0 + b, v, tile_n * C + r, inv);
+  if constexpr (En <= 32) epi_slice<BN, En>(ep, gs, n0 + r * R + rl, b0 + b, v, tile_n * C + r, inv, nullptr, &pre);
+  else epi_slice<BN, En>(ep, gs, n0 + r * R + rl, b0 + b, v, tile_n * C + r, inv);
 }
 
 template <int BN>
@@ -518,20 +610,21 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
           for (int p = 0; p < C; ++p) mbar_arrive_cluster_relaxed(mapa_shared(smem_u32(ready), p));
         }
         if (tr) trace[10] = globaltimer();
-        mbar_wait_cluster(ready, j & 1);  // every peer's push into my buffer is visible
-        if (tr) trace[11] = globaltimer();
         unsigned long long* rt = tr ? trace : nullptr;
+        const uint32_t rp = j & 1;
         if (!skip) {
           switch (C) {
             case 1:
-              if constexpr (BN <= 64) reduce_and_store<BN, 1>(ep, gs, red, rank, n0, b0, tile_n, smem_u32(consumed), rt, inv_smem);
+              if constexpr (BN <= 64) reduce_and_store<BN, 1>(ep, gs, red, rank, n0, b0, tile_n, smem_u32(consumed), rt, inv_smem, ready, rp);
               break;
-            case 2: reduce_and_store<BN, 2>(ep, gs, red, rank, n0, b0, tile_n, smem_u32(consumed), rt, inv_smem); break;
-            case 4: reduce_and_store<BN, 4>(ep, gs, red, rank, n0, b0, tile_n, smem_u32(consumed), rt, inv_smem); break;
+            case 2: reduce_and_store<BN, 2>(ep, gs, red, rank, n0, b0, tile_n, smem_u32(consumed), rt, inv_smem, ready, rp); break;
+            case 4: reduce_and_store<BN, 4>(ep, gs, red, rank, n0, b0, tile_n, smem_u32(consumed), rt, inv_smem, ready, rp); break;
             case 8:
-              if constexpr (BN >= 32) reduce_and_store<BN, 8>(ep, gs, red, rank, n0, b0, tile_n, smem_u32(consumed), rt, inv_smem);
+              if constexpr (BN >= 32) reduce_and_store<BN, 8>(ep, gs, red, rank, n0, b0, tile_n, smem_u32(consumed), rt, inv_smem, ready, rp);
               break;
           }
+        } else {
+          mbar_wait_cluster(ready, rp);
         }
         if (tr) trace[12] = globaltimer();
         if (skip) {

@@ -11,7 +11,9 @@ from paper_2501_11779_b200.stages import Tier2, message_buffers  # noqa: E402
 B = int(sys.argv[1]) if len(sys.argv) > 1 else 64
 ctx = int(sys.argv[2]) if len(sys.argv) > 2 else 512
 layers = 4  # rotate layers so the KV of one launch is never L2-resident from the previous
-spec = gh.LLAMA2_7B.with_(n_layers=layers, max_seq_len=ctx)
+model = sys.argv[3] if len(sys.argv) > 3 else "7b"
+base = {"7b": gh.LLAMA2_7B, "13b": gh.CONFIGS["C4"]["spec"], "70b": gh.CONFIGS["C5"]["spec"]}[model]
+spec = base.with_(n_layers=layers, max_seq_len=ctx)
 t2 = Tier2(spec, n_slots=B)
 t2.fill_synthetic(99, B, ctx - 1)
 x, fwd, bwd = message_buffers(spec, B)
@@ -29,5 +31,5 @@ e1.record()
 torch.cuda.synchronize()
 us = e0.elapsed_time(e1) * 1e3 / reps
 byts = 2 * (2 * spec.d_kv * B * ctx + 2 * B * spec.d_kv + 2 * B * spec.d_model)
-print(f"B={B} ctx={ctx}: {us:.1f} us  {byts / us / 1e3:.0f} GB/s")
+print(f"{model} B={B} ctx={ctx}: {us:.1f} us  {byts / us / 1e3:.0f} GB/s")
 t2.close()
