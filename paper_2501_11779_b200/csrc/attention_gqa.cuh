@@ -1,0 +1,358 @@
+// attention_gqa.cuh — Tier-2 decode attention F2 for grouped-query attention, sm_100a.
+//
+// With G = H / H_kv query heads per KV head (70B: G = 8) the per-query-head kernel of
+// attention.cuh streams every KV block G times.  Here one work unit = (prompt b, KV head g): the
+// K/V tiles of the unit are streamed ONCE and all G query heads are scored against each tile, so
+// the kernel moves the algorithmic bytes of SURVEY.md §8d instead of G times them.
+//
+// Same pipeline as attention.cuh (persistent CTA per SM, 1 TMA producer warp + 8 consumer warps,
+// cp.async.bulk K/V stages of 64 positions, per-unit header carrying q of the G heads, the new
+// k / v and the G residual slices, online softmax in the exp2 domain, fused KV append), with the
+// consumers organised as NG = G / HPW head groups of 8 / NG warps: a warp keeps HPW (= 2) query heads in
+// registers, reads each 16-byte K / V chunk from shared memory once and applies it to its HPW
+// heads, and covers 64 / (8 / NG) positions of every stage.  The last warp to finish a unit merges
+// the 8 partial states (per head: the 8 / NG warps of its group) and writes the G outputs.
+#pragma once
+#include "attention.cuh"
+#include "common.cuh"
+#include "params.hpp"
+
+namespace gh {
+
+template <typename T, int DH, int G>
+struct GqaCfg {
+  static constexpr int HPW = 2;                        // query heads per warp (register budget)
+  static constexpr int NG = G / HPW;                   // head groups
+  static constexpr int WG = 8 / NG;                    // warps per head group
+  static constexpr int kVec = 16 / sizeof(T);
+  static constexpr int kChunks = DH / kVec;
+  static constexpr int kLpp = (kChunks % 8 == 0) ? 8 : (kChunks % 4 == 0) ? 4 : (kChunks % 2 == 0) ? 2 : 1;
+  static constexpr int kCpl = kChunks / kLpp;
+  static constexpr int kPg = 32 / kLpp;                // positions per warp pass
+  static constexpr int kW = 8;                         // consumer warps
+  static constexpr int kTpos = (kW * kPg > 64) ? kW * kPg : 64;  // positions per stage
+  static constexpr int kPasses = kTpos / (WG * kPg);  // position passes of a warp per stage
+  static constexpr int kTileBytes = kTpos * DH * (int)sizeof(T);
+  // header: q of G heads | new k | new v | x slices of G heads | {L, b, g, slot}
+  static constexpr int kHdrBytes = (2 * G + 2) * DH * (int)sizeof(T) + 16;
+  static constexpr int kStageBytes = ((2 * kTileBytes + kHdrBytes + 127) / 128) * 128;
+  static constexpr int kNB = 2;                        // combine buffers (units in flight)
+  static constexpr int kCombPerUnit = kW * HPW * (DH + 2);  // floats
+  static constexpr int kStages = ((227 * 1024 - 2048 - kNB * kCombPerUnit * 4) / kStageBytes) > 5
+                                     ? 5 : ((227 * 1024 - 2048 - kNB * kCombPerUnit * 4) / kStageBytes);
+  static constexpr int kThreads = 32 * (1 + kW);
+  static constexpr int kEl = kCpl * kVec;
+  static constexpr int kCombOffset = kStages * kStageBytes;
+  static constexpr int kCombBytes = kNB * kCombPerUnit * 4;
+  static constexpr int kCtlOffset = kCombOffset + ((kCombBytes + 127) / 128) * 128;
+  static constexpr int kBarOffset = kCtlOffset + 128;
+  static constexpr int kSmem = kBarOffset + 2 * kStages * 8 + 16;
+  static_assert(kStages >= 2, "GQA attention stages");
+  static_assert(G % HPW == 0 && NG <= kW && kW % NG == 0 && kPasses >= 1, "GQA group shape");
+};
+
+// (9 warps per CTA: a sub-partition holds 3 warps' registers, i.e. at most 168 per thread, which
+// is why a warp keeps HPW = 2 query heads)
+template <typename T, int DH, int G>
+__global__ void __launch_bounds__(GqaCfg<T, DH, G>::kThreads, 1)
+    attn_gqa_kernel(const AttnArgs a) {
+  using C = GqaCfg<T, DH, G>;
+  constexpr int HPW = C::HPW, WG = C::WG;
+  extern __shared__ __align__(128) uint8_t smem[];
+  uint64_t* full = (uint64_t*)(smem + C::kBarOffset);
+  uint64_t* empty = full + C::kStages;
+  float* comb = (float*)(smem + C::kCombOffset);
+  int* comb_cnt = (int*)(smem + C::kCtlOffset);
+  volatile int* comb_seq = comb_cnt + C::kNB;
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const int n_units = a.B * a.Hkv;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < C::kStages; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], C::kW); }
+    for (int i = 0; i < C::kNB; ++i) { comb_cnt[i] = 0; comb_seq[i] = 0; }
+    fence_barrier_init();
+  }
+  __syncthreads();
+  griddep_launch_dependents();
+  griddep_wait();
+
+  const T* fwd = (const T*)a.msg_fwd;
+  T* bwd = (T*)a.msg_bwd;
+  T* arena = (T*)a.arena;
+  const long ld_fwd = 2L * a.D + 2L * a.Dkv;
+  const long ld_bwd = 2L * a.D;
+  const uint32_t hdr_bytes = (uint32_t)((2 * G + 2) * DH * sizeof(T));
+
+  if (warp == 0) {
+    // ------------------------------------------------ producer
+    if (elect_one()) {
+      const uint64_t pol = policy_evict_first();
+      uint32_t it = 0;
+      int u = blockIdx.x;
+      int L = 0, sl = 0;
+      if (u < n_units) { L = a.pos[u / a.Hkv]; sl = (int)a.slot[u / a.Hkv]; }
+      for (; u < n_units; u += gridDim.x) {
+        const int b = u / a.Hkv, g = u % a.Hkv;
+        const int un = u + gridDim.x;
+        int Ln = 0, sln = 0;
+        if (un < n_units) { Ln = a.pos[un / a.Hkv]; sln = (int)a.slot[un / a.Hkv]; }
+        const T* kbase = arena + (long)sl * a.slot_stride + (long)g * a.head_stride;
+        const T* vbase = kbase + a.kv_stride;
+        const int nch = L > 0 ? (L + C::kTpos - 1) / C::kTpos : 1;
+        for (int c = 0; c < nch; ++c, ++it) {
+          const int s = it % C::kStages;
+          mbar_wait(&empty[s], ((it / C::kStages) & 1) ^ 1);
+          const int np = max(0, min(C::kTpos, L - c * C::kTpos));
+          const uint32_t bytes = (uint32_t)np * DH * sizeof(T);
+          uint8_t* sk = smem + s * C::kStageBytes;
+          uint8_t* hdr = sk + 2 * C::kTileBytes;
+          if (c == 0) {
+            int* meta = (int*)(hdr + (2 * G + 2) * DH * sizeof(T));
+            meta[0] = L; meta[1] = b; meta[2] = g; meta[3] = sl;
+          }
+          mbar_arrive_expect_tx(&full[s], 2 * bytes + (c == 0 ? hdr_bytes : 0u));
+          if (np > 0) {
+            bulk_g2s(sk, kbase + (long)c * C::kTpos * DH, bytes, &full[s], pol);
+            bulk_g2s(sk + C::kTileBytes, vbase + (long)c * C::kTpos * DH, bytes, &full[s], pol);
+          }
+          if (c == 0) {
+            const T* row = fwd + (long)b * ld_fwd;
+            const uint32_t gq = (uint32_t)(G * DH * sizeof(T));
+            bulk_g2s(hdr, row + a.D + (long)g * G * DH, gq, &full[s], pol);                        // q of the group
+            bulk_g2s(hdr + gq, row + 2L * a.D + (long)g * DH, DH * sizeof(T), &full[s], pol);      // new k
+            bulk_g2s(hdr + gq + DH * sizeof(T), row + 2L * a.D + a.Dkv + (long)g * DH, DH * sizeof(T), &full[s],
+                     pol);                                                                         // new v
+            bulk_g2s(hdr + gq + 2 * DH * sizeof(T), row + (long)g * G * DH, gq, &full[s], pol);    // x slices
+          }
+        }
+        L = Ln;
+        sl = sln;
+      }
+      prefetch_l2_share(a.pf, a.pf_bytes, blockIdx.x, gridDim.x);
+    }
+    return;
+  }
+
+  // -------------------------------------------------- consumers
+  const int cw = warp - 1;
+  const int ng = cw / WG;             // my head group: query heads ng*HPW .. +HPW of the unit
+  const int wi = cw % WG;             // my index inside the group
+  const int grp = lane / C::kLpp;
+  const int sub = lane % C::kLpp;
+  uint32_t it = 0;
+
+  int ui = 0;
+  for (int u = blockIdx.x; u < n_units; u += gridDim.x, ++ui) {
+    const int s0 = it % C::kStages;
+    mbar_wait(&full[s0], (it / C::kStages) & 1);
+    const uint8_t* hdr = smem + s0 * C::kStageBytes + 2 * C::kTileBytes;
+    const T* hq = (const T*)hdr;                  // [G][DH]
+    const T* hk = hq + G * DH;
+    const T* hv = hk + DH;
+    const T* hx = hv + DH;                        // [G][DH]
+    const int* meta = (const int*)(hdr + (2 * G + 2) * DH * sizeof(T));
+    const int L = meta[0], b = meta[1], g = meta[2], slot = meta[3];
+    const int nch = L > 0 ? (L + C::kTpos - 1) / C::kTpos : 1;
+
+    float q[HPW][C::kEl], o[HPW][C::kEl], m[HPW], l[HPW];
+#pragma unroll
+    for (int hh = 0; hh < HPW; ++hh) {
+#pragma unroll
+      for (int j = 0; j < C::kCpl; ++j) {
+        uint4 c = *(const uint4*)(hq + (ng * HPW + hh) * DH + (sub + j * C::kLpp) * C::kVec);
+        chunk_to_f32<T>(c, q[hh] + j * C::kVec);
+      }
+#pragma unroll
+      for (int e = 0; e < C::kEl; ++e) { q[hh][e] *= a.scale_log2; o[hh][e] = 0.f; }
+      m[hh] = -INFINITY;
+      l[hh] = 0.f;
+    }
+
+    if (wi == 0) {
+      // new token: scores of my heads with the new key (group 0 lanes keep the mass); the first
+      // warp also appends k / v to the arena
+      T* kdst = arena + (long)slot * a.slot_stride + (long)g * a.head_stride + (long)L * DH;
+      T* vdst = kdst + a.kv_stride;
+      float vf[C::kEl], kf[C::kEl];
+#pragma unroll
+      for (int j = 0; j < C::kCpl; ++j) {
+        const int off = (sub + j * C::kLpp) * C::kVec;
+        uint4 kc = *(const uint4*)(hk + off);
+        uint4 vc = *(const uint4*)(hv + off);
+        if (cw == 0 && grp == 0) {
+          *(uint4*)(kdst + off) = kc;
+          *(uint4*)(vdst + off) = vc;
+        }
+        chunk_to_f32<T>(kc, kf + j * C::kVec);
+        chunk_to_f32<T>(vc, vf + j * C::kVec);
+      }
+#pragma unroll
+      for (int hh = 0; hh < HPW; ++hh) {
+        float part = 0.f;
+#pragma unroll
+        for (int e = 0; e < C::kEl; ++e) part = fmaf(q[hh][e], kf[e], part);
+#pragma unroll
+        for (int o2 = C::kLpp / 2; o2 > 0; o2 >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o2);
+        m[hh] = part;
+        if (grp == 0) {
+          l[hh] = 1.f;
+#pragma unroll
+          for (int e = 0; e < C::kEl; ++e) o[hh][e] = vf[e];
+        }
+      }
+    }
+
+    if (cw == C::kW - 1) {
+      // residual pass-through of the unit's G slices: bwd.x[(g*G + i)*DH ..] = fwd.x[...]
+      const int n16 = G * C::kChunks;
+      for (int i = lane; i < n16; i += 32)
+        *((uint4*)(bwd + (long)b * ld_bwd + (long)g * G * DH) + i) = ((const uint4*)hx)[i];
+    }
+
+    for (int c = 0; c < nch; ++c, ++it) {
+      const int s = it % C::kStages;
+      const int np = max(0, min(C::kTpos, L - c * C::kTpos));
+      if (c > 0) mbar_wait(&full[s], (it / C::kStages) & 1);
+      const T* sk = (const T*)(smem + s * C::kStageBytes);
+      const T* sv = (const T*)(smem + s * C::kStageBytes + C::kTileBytes);
+
+      float sc[C::kPasses][HPW];
+      float mx[HPW];
+#pragma unroll
+      for (int hh = 0; hh < HPW; ++hh) mx[hh] = -INFINITY;
+#pragma unroll
+      for (int ps = 0; ps < C::kPasses; ++ps) {
+        const int r = ps * WG * C::kPg + wi * C::kPg + grp;
+        float kf[C::kEl];
+        if (r < np) {
+#pragma unroll
+          for (int j = 0; j < C::kCpl; ++j) {
+            uint4 kc = *(const uint4*)(sk + r * DH + (sub + j * C::kLpp) * C::kVec);
+            chunk_to_f32<T>(kc, kf + j * C::kVec);
+          }
+        }
+#pragma unroll
+        for (int hh = 0; hh < HPW; ++hh) {
+          float part = 0.f;
+          if (r < np) {
+            float pp[2] = {0.f, 0.f};
+#pragma unroll
+            for (int e = 0; e < C::kEl; ++e) pp[e & 1] = fmaf(q[hh][e], kf[e], pp[e & 1]);
+            part = pp[0] + pp[1];
+          }
+#pragma unroll
+          for (int o2 = C::kLpp / 2; o2 > 0; o2 >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o2);
+          sc[ps][hh] = (r < np) ? part : -INFINITY;
+          mx[hh] = fmaxf(mx[hh], sc[ps][hh]);
+        }
+      }
+      float mn[HPW];
+#pragma unroll
+      for (int hh = 0; hh < HPW; ++hh) {
+#pragma unroll
+        for (int o2 = C::kLpp; o2 < 32; o2 <<= 1) mx[hh] = fmaxf(mx[hh], __shfl_xor_sync(0xffffffffu, mx[hh], o2));
+        mn[hh] = fmaxf(m[hh], mx[hh]);
+        if (mx[hh] != -INFINITY) {
+          const float corr = (m[hh] == -INFINITY) ? 0.f : exp2f(m[hh] - mn[hh]);
+          l[hh] *= corr;
+#pragma unroll
+          for (int e = 0; e < C::kEl; ++e) o[hh][e] *= corr;
+          m[hh] = mn[hh];
+        }
+      }
+#pragma unroll
+      for (int ps = 0; ps < C::kPasses; ++ps) {
+        const int r = ps * WG * C::kPg + wi * C::kPg + grp;
+        if (r < np) {
+          float vf[C::kEl];
+#pragma unroll
+          for (int j = 0; j < C::kCpl; ++j) {
+            uint4 vc = *(const uint4*)(sv + r * DH + (sub + j * C::kLpp) * C::kVec);
+            chunk_to_f32<T>(vc, vf + j * C::kVec);
+          }
+#pragma unroll
+          for (int hh = 0; hh < HPW; ++hh) {
+            const float p = exp2f(sc[ps][hh] - m[hh]);
+            l[hh] += p;
+#pragma unroll
+            for (int e = 0; e < C::kEl; ++e) o[hh][e] = fmaf(p, vf[e], o[hh][e]);
+          }
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[s]);
+    }
+
+    // merge the lane groups of this warp (m is warp-uniform per head)
+#pragma unroll
+    for (int hh = 0; hh < HPW; ++hh)
+#pragma unroll
+      for (int o2 = C::kLpp; o2 < 32; o2 <<= 1) {
+        l[hh] += __shfl_xor_sync(0xffffffffu, l[hh], o2);
+#pragma unroll
+        for (int e = 0; e < C::kEl; ++e) o[hh][e] += __shfl_xor_sync(0xffffffffu, o[hh][e], o2);
+      }
+    // publish [warp][head][DH + 2] into combine buffer ui % kNB; the last warp merges
+    const int cbi = ui % C::kNB;
+    while (comb_seq[cbi] != ui / C::kNB) { }
+    float* cbuf = comb + cbi * C::kCombPerUnit;
+#pragma unroll
+    for (int hh = 0; hh < HPW; ++hh) {
+      float* cwbuf = cbuf + (cw * HPW + hh) * (DH + 2);
+      if (grp == 0) {
+#pragma unroll
+        for (int j = 0; j < C::kCpl; ++j)
+#pragma unroll
+          for (int e = 0; e < C::kVec; ++e) cwbuf[(sub + j * C::kLpp) * C::kVec + e] = o[hh][j * C::kVec + e];
+      }
+      if (lane == 0) { cwbuf[DH] = m[hh]; cwbuf[DH + 1] = l[hh]; }
+    }
+    __syncwarp();
+    int last = 0;
+    if (lane == 0) {
+      __threadfence_block();
+      last = atomicAdd(&comb_cnt[cbi], 1) == C::kW - 1;
+    }
+    last = __shfl_sync(0xffffffffu, last, 0);
+    if (last) {
+      __threadfence_block();
+      for (int hq = 0; hq < G; ++hq) {  // query head hq of the unit: head group hq / HPW, slot hq % HPW
+        const int gg = hq / HPW, hh = hq % HPW;
+        float M = -INFINITY;
+#pragma unroll
+        for (int k = 0; k < C::kW; ++k)
+          if (k < WG) M = fmaxf(M, cbuf[((gg * WG + k) * HPW + hh) * (DH + 2) + DH]);
+        float den = 0.f;
+        float f[C::kW];
+#pragma unroll
+        for (int k = 0; k < C::kW; ++k) {
+          f[k] = 0.f;
+          if (k < WG) {
+            const float mw = cbuf[((gg * WG + k) * HPW + hh) * (DH + 2) + DH];
+            f[k] = (mw == -INFINITY) ? 0.f : exp2f(mw - M);
+            den += cbuf[((gg * WG + k) * HPW + hh) * (DH + 2) + DH + 1] * f[k];
+          }
+        }
+        const float inv = 1.f / den;
+        T* orow = bwd + (long)b * ld_bwd + a.D + (long)(g * G + hq) * DH;
+        for (int d = lane; d < DH; d += 32) {
+          float acc = 0.f;
+#pragma unroll
+          for (int k = 0; k < C::kW; ++k)
+            if (k < WG) acc += cbuf[((gg * WG + k) * HPW + hh) * (DH + 2) + d] * f[k];
+          St<T>::store(orow, d, acc * inv);
+        }
+      }
+      __syncwarp();
+      if (lane == 0) {
+        comb_cnt[cbi] = 0;
+        __threadfence_block();
+        comb_seq[cbi] = ui / C::kNB + 1;
+      }
+    }
+  }
+}
+
+}  // namespace gh

@@ -15,6 +15,7 @@
 #include <mutex>
 
 #include "attention.cuh"
+#include "attention_gqa.cuh"
 #include "common.cuh"
 #include "gemm_pair.cuh"
 #include "gemm_tc.cuh"
@@ -656,10 +657,22 @@ static cudaError_t configure_attn_w() {
   return cudaFuncSetAttribute(attn_decode_kernel<T, DH, W>, cudaFuncAttributePreferredSharedMemoryCarveout,
                               (int)cudaSharedmemCarveoutMaxShared);
 }
+template <typename T, int DH, int G>
+static cudaError_t configure_attn_gqa() {
+  cudaError_t e = cudaFuncSetAttribute(attn_gqa_kernel<T, DH, G>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       GqaCfg<T, DH, G>::kSmem);
+  if (e != cudaSuccess) return e;
+  return cudaFuncSetAttribute(attn_gqa_kernel<T, DH, G>, cudaFuncAttributePreferredSharedMemoryCarveout,
+                              (int)cudaSharedmemCarveoutMaxShared);
+}
 template <typename T, int DH>
 static cudaError_t configure_attn() {
   cudaError_t e = configure_attn_w<T, DH, 8>();
-  return e != cudaSuccess ? e : configure_attn_w<T, DH, 16>();
+  if (e == cudaSuccess) e = configure_attn_w<T, DH, 16>();
+  if (e == cudaSuccess) e = configure_attn_gqa<T, DH, 2>();
+  if (e == cudaSuccess) e = configure_attn_gqa<T, DH, 4>();
+  if (e == cudaSuccess) e = configure_attn_gqa<T, DH, 8>();
+  return e;
 }
 static int attn_warps() {  // consumer warps per CTA (diagnostics override GH_ATTN_WARPS)
   static const int w = getenv("GH_ATTN_WARPS") ? atoi(getenv("GH_ATTN_WARPS")) : 8;
@@ -673,8 +686,27 @@ static cudaError_t launch_attn_w(const AttnArgs& a, cudaStream_t st) {
   const int grid = std::min(units, kNumSMs);
   return launch_pdl(attn_decode_kernel<T, DH, W>, grid, C::kThreads, C::kSmem, st, a);
 }
+template <typename T, int DH, int G>
+static cudaError_t launch_attn_gqa(const AttnArgs& a, cudaStream_t st) {
+  using C = GqaCfg<T, DH, G>;
+  const int units = a.B * a.Hkv;
+  if (units <= 0) return cudaSuccess;
+  const int grid = std::min(units, kNumSMs);
+  return launch_pdl(attn_gqa_kernel<T, DH, G>, grid, C::kThreads, C::kSmem, st, a);
+}
+// group size handled by the group-shared kernel (one unit per KV head): 2, 4 or 8, else 0
+static int gqa_group(const AttnArgs& a) {
+  static const bool off = getenv("GH_NO_GQA") != nullptr;  // diagnostics: per-query-head kernel
+  const int G = a.Hkv > 0 && a.H % a.Hkv == 0 ? a.H / a.Hkv : 1;
+  return (!off && (G == 2 || G == 4 || G == 8)) ? G : 0;
+}
 template <typename T, int DH>
 static cudaError_t launch_attn_t(const AttnArgs& a, cudaStream_t st) {
+  switch (gqa_group(a)) {
+    case 2: return launch_attn_gqa<T, DH, 2>(a, st);
+    case 4: return launch_attn_gqa<T, DH, 4>(a, st);
+    case 8: return launch_attn_gqa<T, DH, 8>(a, st);
+  }
   return attn_warps() == 16 ? launch_attn_w<T, DH, 16>(a, st) : launch_attn_w<T, DH, 8>(a, st);
 }
 
