@@ -396,10 +396,18 @@ def run_split(args, wl, rank, world):
     nsteps = max(2, args.steps // 2)
     toks = np.tile(tok, (IF, 1))
     poss = np.tile(pos, (IF, 1))
+    n1 = max(1, args.tier1)
     for _ in range(nsteps):
         r = eng.step_all_host(toks if eng.role == "tier1" else None, poss if eng.role == "tier1" else None,
                               stream=stream)
-        if r is not None:
+        if n1 > 1:  # Tier-1 stages: the last stage's next tokens go back to the first stage's host
+            if rank == n1 - 1:
+                dist.send(torch.from_numpy(np.ascontiguousarray(r, dtype=np.int32)), dst=0)
+            elif rank == 0:
+                buf = torch.zeros((IF, wl["batch"]), dtype=torch.int32)
+                dist.recv(buf, src=n1 - 1)
+                toks = buf.numpy()
+        elif r is not None:
             toks = r
     e2e_ms = torch.tensor([(time.perf_counter() - t0) * 1e3 / nsteps], dtype=torch.float64)
     dist.all_reduce(e2e_ms, op=dist.ReduceOp.MAX)
