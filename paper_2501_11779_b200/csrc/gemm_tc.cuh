@@ -429,6 +429,47 @@ GH_DEV void reduce_and_store(const EpiParams& ep, const GemmShape& gs, const flo
   else epi_slice<BN, En>(ep, gs, n0 + r * R + rl, b0 + b, v, tile_n * C + r, inv);
 }
 
+// Wide batch tiles (BN > 128, one batch tile for 129..192 columns): thread t owns whole
+// columns t, t + 128, ... of the CTA's R-row slice (no cross-thread reduction in the epilogue),
+// processed one at a time; the receive buffer is released after the last one.
+template <int BN, int C>
+GH_DEV void reduce_and_store_wide(const EpiParams& ep, const GemmShape& gs, const float* recv, int r, int n0,
+                                  int b0, int tile_n, uint32_t consumed_saddr, const float* inv, uint64_t* ready,
+                                  uint32_t ready_parity) {
+  constexpr int R = 128 / C;
+  constexpr int En = R;
+  constexpr int Ep = En <= 32 ? En : 1;
+  const int t = threadIdx.x - 64;
+#pragma unroll 1
+  for (int k = 0; k < (BN + 127) / 128; ++k) {
+    const int b = t + 128 * k;
+    EpiPre<Ep> pre;
+    pre.ok = false;
+    if constexpr (En <= 32)
+      if (b < BN) epi_prefetch<En>(ep, gs, n0 + r * R, b0 + b, pre);
+    if (k == 0) mbar_wait_cluster(ready, ready_parity);  // every peer's push into my buffer is visible
+    if (b < BN) {
+      float v[En];
+#pragma unroll
+      for (int e = 0; e < En; e += 4) {
+        float4 a = *(const float4*)(recv + recv_index<BN, C>(0, b, e));
+#pragma unroll
+        for (int p = 1; p < C; ++p) {  // rank order: deterministic
+          const float4 q = *(const float4*)(recv + recv_index<BN, C>(p, b, e));
+          a.x += q.x; a.y += q.y; a.z += q.z; a.w += q.w;
+        }
+        v[e] = a.x; v[e + 1] = a.y; v[e + 2] = a.z; v[e + 3] = a.w;
+      }
+      // BN template of epi_slice = 128: one thread per column (no cross-thread reductions)
+      if constexpr (En <= 32) epi_slice<128, En>(ep, gs, n0 + r * R, b0 + b, v, tile_n * C + r, inv, nullptr, &pre);
+      else epi_slice<128, En>(ep, gs, n0 + r * R, b0 + b, v, tile_n * C + r, inv);
+    }
+  }
+  epi_bar();  // my receive buffer is free again: every peer may push its next tile
+  if (threadIdx.x == 64)
+    for (int p = 0; p < C; ++p) mbar_arrive_cluster_relaxed(mapa_shared(consumed_saddr, p));
+}
+
 template <int BN>
 __global__ void __launch_bounds__(kGemmThreads, 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CUtensorMap tmX,
@@ -613,15 +654,23 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         unsigned long long* rt = tr ? trace : nullptr;
         const uint32_t rp = j & 1;
         if (!skip) {
-          switch (C) {
-            case 1:
-              if constexpr (BN <= 64) reduce_and_store<BN, 1>(ep, gs, red, rank, n0, b0, tile_n, smem_u32(consumed), rt, inv_smem, ready, rp);
-              break;
-            case 2: reduce_and_store<BN, 2>(ep, gs, red, rank, n0, b0, tile_n, smem_u32(consumed), rt, inv_smem, ready, rp); break;
-            case 4: reduce_and_store<BN, 4>(ep, gs, red, rank, n0, b0, tile_n, smem_u32(consumed), rt, inv_smem, ready, rp); break;
-            case 8:
-              if constexpr (BN >= 32) reduce_and_store<BN, 8>(ep, gs, red, rank, n0, b0, tile_n, smem_u32(consumed), rt, inv_smem, ready, rp);
-              break;
+          if constexpr (BN > 128) {
+            switch (C) {
+              case 2: reduce_and_store_wide<BN, 2>(ep, gs, red, rank, n0, b0, tile_n, smem_u32(consumed), inv_smem, ready, rp); break;
+              case 4: reduce_and_store_wide<BN, 4>(ep, gs, red, rank, n0, b0, tile_n, smem_u32(consumed), inv_smem, ready, rp); break;
+              default: break;  // the planner never pairs a wide tile with C = 1 or 8
+            }
+          } else {
+            switch (C) {
+              case 1:
+                if constexpr (BN <= 64) reduce_and_store<BN, 1>(ep, gs, red, rank, n0, b0, tile_n, smem_u32(consumed), rt, inv_smem, ready, rp);
+                break;
+              case 2: reduce_and_store<BN, 2>(ep, gs, red, rank, n0, b0, tile_n, smem_u32(consumed), rt, inv_smem, ready, rp); break;
+              case 4: reduce_and_store<BN, 4>(ep, gs, red, rank, n0, b0, tile_n, smem_u32(consumed), rt, inv_smem, ready, rp); break;
+              case 8:
+                if constexpr (BN >= 32) reduce_and_store<BN, 8>(ep, gs, red, rank, n0, b0, tile_n, smem_u32(consumed), rt, inv_smem, ready, rp);
+                break;
+            }
           }
         } else {
           mbar_wait_cluster(ready, rp);

@@ -420,11 +420,13 @@ static int max_clusters_bn(int BN, int C) {
     case 16: return max_clusters<16>(C);
     case 32: return max_clusters<32>(C);
     case 64: return max_clusters<64>(C);
-    default: return max_clusters<128>(C);
+    case 128: return max_clusters<128>(C);
+    default: return max_clusters<192>(C);
   }
 }
 
 static int pair_override = 0;  // diagnostics: 1 = split-K only, 2 = pair whenever possible
+static int wide_override = 0;  // diagnostics: 1 = never BN = 192, 2 = always when 128 < B <= 192
 
 static int pair_stages(int BN) { return std::max(2, PairSmem::max_stages(BN, 227 * 1024)); }
 
@@ -507,14 +509,12 @@ static GemmPlan plan_pair(int N, int K, int Bt, double* cost_out) {
 // Choose the cluster size C minimising the k-blocks on the critical path of one CTA:
 // rounds(C) * (ceil(KB / C) + reduction overhead), rounds = ceil(tiles / co-resident clusters).
 // Batches above 128 columns also consider the pair kernel (always used above 256).
-GemmPlan plan_gemm(int N, int K, int Bt) {
+// split-K plan for batch tile BN (cost in k-blocks on the critical path -> *kb_out)
+static GemmPlan plan_splitk(int N, int KB, int Bt, int BN, double* kb_out) {
   GemmPlan p;
-  const int bt_cap = std::min(Bt, 128);
-  p.BN = 128;
-  for (int bn : kBNs) if (bn >= bt_cap) { p.BN = bn; break; }
+  p.BN = BN;
   p.b_tiles = (Bt + p.BN - 1) / p.BN;
   p.n_tiles = (N + kBlockM - 1) / kBlockM;
-  const int KB = (K + kBlockK - 1) / kBlockK;
   const int tiles = p.n_tiles * p.b_tiles;
   double best = 1e30;
   // C = 8 (clusters of 8 CTAs) is excluded: only ~16 such clusters fit (GPC packing) and it
@@ -528,11 +528,34 @@ GemmPlan plan_gemm(int N, int K, int Bt) {
     const double cost = rounds * ((KB + C - 1) / C + (C > 1 ? 1.0 : 0.0));
     if (cost < best - 1e-9) { best = cost; p.C = C; p.n_clusters = ncl; }
   }
+  *kb_out = best;
+  return p;
+}
+static double splitk_clk(const GemmPlan& p, double kb, int N, int K) {
+  return std::max(kb * kblock_clk(16384.0 + p.BN * 128.0, 2.0 * p.BN), hbm_floor_clk(N, K)) + 5100.0;
+}
+
+GemmPlan plan_gemm(int N, int K, int Bt) {
+  const int KB = (K + kBlockK - 1) / kBlockK;
+  const int bt_cap = std::min(Bt, 128);
+  int bn = 128;
+  for (int b : kBNs) if (b >= bt_cap) { bn = b; break; }
+  double best = 0;
+  GemmPlan p = plan_splitk(N, KB, Bt, bn, &best);
+  // 129..192 columns: one wide batch tile (BN = 192) instead of two 128-column tiles
+  if (Bt > 128 && Bt <= 192 && wide_override != 1) {
+    double kbw = 0;
+    GemmPlan pw = plan_splitk(N, KB, Bt, 192, &kbw);
+    if (kbw < 1e29 && (wide_override == 2 || splitk_clk(pw, kbw, N, K) < splitk_clk(p, best, N, K))) {
+      p = pw;
+      best = kbw;
+    }
+  }
   if ((Bt > 128 && pair_override != 1) || pair_override == 2 || Bt > 256) {
     double pc = 0;
     GemmPlan pp = plan_pair(N, K, Bt, &pc);
     // split-K cluster kernel: critical-path k-blocks, HBM floor, reduction + epilogue tail (~2.6 us)
-    const double sc = std::max(best * kblock_clk(16384.0 + p.BN * 128.0, 2.0 * p.BN), hbm_floor_clk(N, K)) + 5100.0;
+    const double sc = splitk_clk(p, best, N, K);
     if (Bt > 256 || pair_override == 2 || pc < sc) p = pp;
   }
   static const bool verbose = getenv("GH_GEMM_VERBOSE") != nullptr;  // diagnostics
@@ -601,6 +624,7 @@ static cudaError_t launch_pair(const CUtensorMap* tmW, const CUtensorMap* tmX, G
 
 void gemm_debug_cluster(int C) { cluster_override = C; }
 void gemm_debug_pair(int mode) { pair_override = mode; }
+void gemm_debug_wide(int mode) { wide_override = mode; }
 void gemm_debug_set(int stages) { stages_override = stages; }
 
 cudaError_t launch_gemm(const Weight& W, const CUtensorMap* tmW, const void* X, long ldx,
@@ -644,6 +668,7 @@ cudaError_t launch_gemm(const Weight& W, const CUtensorMap* tmW, const void* X, 
     case 32: return launch_tc<32>(tmW, tmX, gs, p, ep, st);
     case 64: return launch_tc<64>(tmW, tmX, gs, p, ep, st);
     case 128: return launch_tc<128>(tmW, tmX, gs, p, ep, st);
+    case 192: return launch_tc<192>(tmW, tmX, gs, p, ep, st);
   }
   return cudaErrorInvalidValue;
 }
@@ -735,6 +760,7 @@ cudaError_t configure_kernels() {
   cudaError_t e = cudaSuccess;
   auto chk = [&](cudaError_t r) { if (e == cudaSuccess) e = r; };
   chk(configure_tc<16>()); chk(configure_tc<32>()); chk(configure_tc<64>()); chk(configure_tc<128>());
+  chk(configure_tc<192>());
   chk(cudaFuncSetAttribute(gemm_pair_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
   chk(configure_attn<bf16_t, 48>()); chk(configure_attn<bf16_t, 64>()); chk(configure_attn<bf16_t, 128>());
   chk(configure_attn<float, 48>()); chk(configure_attn<float, 64>()); chk(configure_attn<float, 128>());

@@ -65,6 +65,7 @@ constexpr size_t kSkWsBytes = (size_t)74 * 256 * 256 * 4;  // co-resident pairs 
 void gemm_debug_set(int stages);  // 0 = production pipeline depth
 void gemm_debug_cluster(int C);   // 0 = production cluster-size choice
 void gemm_debug_pair(int mode);   // 0 = planner's choice, 1 = force split-K (B <= 256), 2 = force pair
+void gemm_debug_wide(int mode);   // 0 = planner's choice, 1 = no 192-column tile, 2 = force it
 
 // Encode a 2-D bf16 tensor map over a row-major [rows, cols] matrix with row stride ld
 // (elements), box {64, box_rows}, 128-byte swizzle.

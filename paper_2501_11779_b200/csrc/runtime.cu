@@ -1446,12 +1446,15 @@ extern "C" gh_status gh_debug_gemm_bench(int N, int K, int B, int flags, int sta
   GH_TRY(dev_alloc(mem, (size_t)B * K * 2, &X));
   GH_TRY(dev_alloc(mem, (size_t)B * N * 2, &Y));
   GH_CUDA(cudaMemset(X, 0, (size_t)B * K * 2));
-  // diagnostics: ks > 0 forces the split-K cluster size, -1 forces split-K, -2 the pair kernel
+  // diagnostics: ks > 0 forces the split-K cluster size, -1 forces split-K, -2 the pair kernel,
+  // -3 split-K with the 192-column tile, -4 split-K without it
   if (ks >= 0) gemm_debug_cluster(ks);
-  else gemm_debug_pair(-ks);
+  else if (ks >= -2) gemm_debug_pair(-ks);
+  else { gemm_debug_pair(1); gemm_debug_wide(ks == -3 ? 2 : 1); }
   GemmPlan p = plan_gemm(N, K, B);
   gemm_debug_cluster(0);
   gemm_debug_pair(0);
+  gemm_debug_wide(0);
   GH_CUDA(make_tmap_bf16(&tmX, X, (uint64_t)B, (uint64_t)K, (uint64_t)K, (uint32_t)p.x_box_rows()));
   GemmScratch sc;
   {

@@ -21,11 +21,11 @@ def bench(N, K, B, flags=0, cluster=0, reps=20):
 
 shapes = {"qkv": (12288, 4096), "o": (4096, 4096), "w13": (22016, 4096), "w2": (4096, 11008), "lm": (32000, 4096)}
 for B in [int(a) for a in sys.argv[1:]] or [192, 448, 1024]:
-    tot = {"prod": 0.0, "split": 0.0, "pair": 0.0}
+    tot = {"prod": 0.0, "split": 0.0, "pair": 0.0, "wide192": 0.0, "split128": 0.0}
     for name, (N, K) in shapes.items():
         flops = 2.0 * N * K * B
         row = [f"B={B:5d} {name:4s}"]
-        for label, cl in [("prod", 0), ("split", -1), ("pair", -2)]:
+        for label, cl in [("prod", 0), ("split", -1), ("pair", -2), ("wide192", -3), ("split128", -4)]:
             try:
                 t = bench(N, K, B, cluster=cl)
                 tot[label] += t if name != "lm" else 0.0
