@@ -481,7 +481,9 @@ static GemmPlan plan_pair(int N, int K, int Bt, double* cost_out) {
     last_bn = BN;
     const int b_tiles = (Bt + BN - 1) / BN;
     const double tkb = kblock_clk(16384.0 + BN * 64.0, 2.0 * BN);
+    static const int force_split = getenv("GH_PAIR_SPLIT") ? atoi(getenv("GH_PAIR_SPLIT")) : -1;  // diagnostics
     for (int split = 0; split < 2; ++split) {
+      if (force_split >= 0 && split != force_split) continue;
       const long tiles = (long)n_tiles * b_tiles, units = tiles * KB;
       double cost;
       int np;
