@@ -356,3 +356,308 @@ __global__ void __launch_bounds__(GqaCfg<T, DH, G>::kThreads, 1)
 }
 
 }  // namespace gh
+
+namespace gh {
+
+// ====================================================================== tensor-core GQA (bf16, d_h 128)
+// The same unit (prompt, KV head) and pipeline, with the group's scores and P·V on the tensor
+// cores (mma.sync m16n8k16 / m16n8k8, bf16 in, fp32 accumulate; the query heads are the M = 16
+// rows, zero-padded above G).  K and V tiles arrive through TMA with the 128-byte swizzle (a 3-D
+// tensor map over the whole KV arena: [rows = (layer, slot, K/V, kv head)][position][d_h], boxes of
+// 64 positions x 64 d_h) so that the ldmatrix fragment loads are bank-conflict free.  Consumer warp
+// w owns positions 8w..8w+7 of every 64-position stage: S (16 x 8) = Q (16 x 128) · K_wᵀ as 8
+// MMAs, an online softmax per query head over its quad of lanes, O (16 x 128) += P (16 x 8) · V_w
+// as 16 MMAs.  The 8 warps' states and the new token's (computed on CUDA cores by warp 0) are
+// merged by the last warp of the unit.
+GH_DEV void ldsm_x4(uint32_t addr, uint32_t& r0, uint32_t& r1, uint32_t& r2, uint32_t& r3) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0, %1, %2, %3}, [%4];"
+               : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3) : "r"(addr));
+}
+GH_DEV void ldsm_x4_t(uint32_t addr, uint32_t& r0, uint32_t& r1, uint32_t& r2, uint32_t& r3) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0, %1, %2, %3}, [%4];"
+               : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3) : "r"(addr));
+}
+GH_DEV void mma_16816(float (&d)[4], uint32_t a0, uint32_t a1, uint32_t a2, uint32_t a3, uint32_t b0, uint32_t b1) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0, %1, %2, %3}, {%4, %5, %6, %7}, {%8, %9}, "
+      "{%0, %1, %2, %3};"
+      : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+      : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
+}
+GH_DEV void mma_1688(float (&d)[4], uint32_t a0, uint32_t a1, uint32_t b0) {
+  asm volatile("mma.sync.aligned.m16n8k8.row.col.f32.bf16.bf16.f32 {%0, %1, %2, %3}, {%4, %5}, {%6}, {%0, %1, %2, %3};"
+               : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+               : "r"(a0), "r"(a1), "r"(b0));
+}
+GH_DEV void tma_load_3d(void* smem_dst, const void* tmap, int c0, int c1, int c2, uint64_t* bar, uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes.L2::cache_hint"
+      " [%0], [%1, {%2, %3, %4}], [%5], %6;\n" ::"r"(smem_u32(smem_dst)),
+      "l"(tmap), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar)), "l"(policy)
+      : "memory");
+}
+
+template <int G>
+struct GqaTcCfg {
+  static constexpr int DH = 128;
+  static constexpr int kW = 8;                     // consumer warps, 8 positions each
+  static constexpr int kTpos = 64;
+  static constexpr int kBox = 64 * 64 * 2;         // one TMA box: 64 positions x 64 d_h (8 KB)
+  static constexpr int kKV = 4 * kBox;             // K (2 boxes) + V (2 boxes)
+  static constexpr int kHdrBytes = (2 * G + 2) * DH * 2 + 16;
+  static constexpr int kStageBytes = kKV + ((kHdrBytes + 1023) / 1024) * 1024;  // boxes stay 1 KB aligned
+  static constexpr int kNB = 2;
+  static constexpr int kCombPerUnit = (kW + 1) * G * (DH + 2);  // + the new token's state
+  static constexpr int kCombBytes = kNB * kCombPerUnit * 4;
+  static constexpr int kStages = ((227 * 1024 - 2048 - kCombBytes - 1024) / kStageBytes) > 6
+                                     ? 6 : ((227 * 1024 - 2048 - kCombBytes - 1024) / kStageBytes);
+  static constexpr int kThreads = 32 * (1 + kW);
+  static constexpr int kCombOffset = kStages * kStageBytes;
+  static constexpr int kCtlOffset = kCombOffset + ((kCombBytes + 127) / 128) * 128;
+  static constexpr int kBarOffset = kCtlOffset + 128;
+  static constexpr int kSmem = kBarOffset + 2 * kStages * 8 + 16 + 1024;  // + alignment slack
+  static_assert(G >= 1 && G <= 8 && kStages >= 2, "tensor-core GQA shape");
+};
+
+template <int G>
+__global__ void __launch_bounds__(GqaTcCfg<G>::kThreads, 1)
+    attn_gqa_tc_kernel(const __grid_constant__ CUtensorMap tmKV, const AttnArgs a) {
+  using C = GqaTcCfg<G>;
+  constexpr int DH = C::DH;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  uint64_t* full = (uint64_t*)(smem + C::kBarOffset);
+  uint64_t* empty = full + C::kStages;
+  float* comb = (float*)(smem + C::kCombOffset);
+  int* comb_cnt = (int*)(smem + C::kCtlOffset);
+  volatile int* comb_seq = comb_cnt + C::kNB;
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const int n_units = a.B * a.Hkv;
+
+  if (threadIdx.x == 0) {
+    prefetch_tmap(&tmKV);
+    for (int s = 0; s < C::kStages; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], C::kW); }
+    for (int i = 0; i < C::kNB; ++i) { comb_cnt[i] = 0; comb_seq[i] = 0; }
+    fence_barrier_init();
+  }
+  __syncthreads();
+  griddep_launch_dependents();
+  griddep_wait();
+
+  const bf16_t* fwd = (const bf16_t*)a.msg_fwd;
+  bf16_t* bwd = (bf16_t*)a.msg_bwd;
+  bf16_t* arena = (bf16_t*)a.arena;
+  const long ld_fwd = 2L * a.D + 2L * a.Dkv;
+  const long ld_bwd = 2L * a.D;
+  constexpr uint32_t hdr_bytes = (uint32_t)((2 * G + 2) * DH * 2);
+
+  if (warp == 0) {
+    // ------------------------------------------------ producer
+    if (elect_one()) {
+      const uint64_t pol = policy_evict_first();
+      uint32_t it = 0;
+      int u = blockIdx.x;
+      int L = 0, sl = 0;
+      if (u < n_units) { L = a.pos[u / a.Hkv]; sl = (int)a.slot[u / a.Hkv]; }
+      for (; u < n_units; u += gridDim.x) {
+        const int b = u / a.Hkv, g = u % a.Hkv;
+        const int un = u + gridDim.x;
+        int Ln = 0, sln = 0;
+        if (un < n_units) { Ln = a.pos[un / a.Hkv]; sln = (int)a.slot[un / a.Hkv]; }
+        const int row_k = ((a.layer_local * a.n_slots + sl) * 2 + 0) * a.Hkv + g;
+        const int row_v = row_k + a.Hkv;
+        const int nch = L > 0 ? (L + C::kTpos - 1) / C::kTpos : 1;
+        for (int c = 0; c < nch; ++c, ++it) {
+          const int s = it % C::kStages;
+          mbar_wait(&empty[s], ((it / C::kStages) & 1) ^ 1);
+          uint8_t* st = smem + s * C::kStageBytes;
+          uint8_t* hdr = st + C::kKV;
+          if (c == 0) {
+            int* meta = (int*)(hdr + hdr_bytes);
+            meta[0] = L; meta[1] = b; meta[2] = g; meta[3] = sl;
+          }
+          const bool any = L > 0;
+          mbar_arrive_expect_tx(&full[s], (any ? (uint32_t)C::kKV : 0u) + (c == 0 ? hdr_bytes : 0u));
+          if (any) {  // full 64-position boxes (rows past L are masked by the consumers)
+            tma_load_3d(st, &tmKV, 0, c * C::kTpos, row_k, &full[s], pol);
+            tma_load_3d(st + C::kBox, &tmKV, 64, c * C::kTpos, row_k, &full[s], pol);
+            tma_load_3d(st + 2 * C::kBox, &tmKV, 0, c * C::kTpos, row_v, &full[s], pol);
+            tma_load_3d(st + 3 * C::kBox, &tmKV, 64, c * C::kTpos, row_v, &full[s], pol);
+          }
+          if (c == 0) {
+            const bf16_t* row = fwd + (long)b * ld_fwd;
+            constexpr uint32_t gq = (uint32_t)(G * DH * 2);
+            bulk_g2s(hdr, row + a.D + (long)g * G * DH, gq, &full[s], pol);                      // q of the group
+            bulk_g2s(hdr + gq, row + 2L * a.D + (long)g * DH, DH * 2, &full[s], pol);            // new k
+            bulk_g2s(hdr + gq + DH * 2, row + 2L * a.D + a.Dkv + (long)g * DH, DH * 2, &full[s], pol);  // new v
+            bulk_g2s(hdr + gq + 2 * DH * 2, row + (long)g * G * DH, gq, &full[s], pol);          // x slices
+          }
+        }
+        L = Ln;
+        sl = sln;
+      }
+      prefetch_l2_share(a.pf, a.pf_bytes, blockIdx.x, gridDim.x);
+    }
+    return;
+  }
+
+  // -------------------------------------------------- consumers
+  const int cw = warp - 1;
+  const int qr = lane >> 2;            // query head (MMA row) of this lane's accumulator entries
+  const int qc = (lane & 3) * 2;       // first of its two columns
+  uint32_t it = 0;
+  int ui = 0;
+  for (int u = blockIdx.x; u < n_units; u += gridDim.x, ++ui) {
+    const int s0 = it % C::kStages;
+    mbar_wait(&full[s0], (it / C::kStages) & 1);
+    const uint8_t* hdr = smem + s0 * C::kStageBytes + C::kKV;
+    const bf16_t* hq = (const bf16_t*)hdr;
+    const bf16_t* hk = hq + G * DH;
+    const bf16_t* hv = hk + DH;
+    const bf16_t* hx = hv + DH;
+    const int* meta = (const int*)(hdr + hdr_bytes);
+    const int L = meta[0], b = meta[1], g = meta[2], slot = meta[3];
+    const int nch = L > 0 ? (L + C::kTpos - 1) / C::kTpos : 1;
+
+    // Q fragments (A operand, rows = query heads; rows >= G and 8..15 are zero)
+    uint32_t qa[8][2];
+#pragma unroll
+    for (int kk = 0; kk < 8; ++kk) {
+      qa[kk][0] = qr < G ? *(const uint32_t*)(hq + qr * DH + kk * 16 + qc) : 0u;
+      qa[kk][1] = qr < G ? *(const uint32_t*)(hq + qr * DH + kk * 16 + 8 + qc) : 0u;
+    }
+    float o[16][4];
+#pragma unroll
+    for (int j = 0; j < 16; ++j) o[j][0] = o[j][1] = o[j][2] = o[j][3] = 0.f;
+    float m = -INFINITY, l = 0.f;  // per query head qr (quad-uniform m; l is this lane's partial)
+
+    const int cb = ui % C::kNB;
+    float* cbuf = comb + cb * C::kCombPerUnit;
+    if (cw == 0) {
+      // new token: its key / value from the header; append them to the arena; its state is merged
+      // as a ninth partial (m = score, l = 1, o = v) by the last warp
+      bf16_t* kdst = arena + (long)slot * a.slot_stride + (long)g * a.head_stride + (long)L * DH;
+      bf16_t* vdst = kdst + a.kv_stride;
+      if (lane < DH / 8) {
+        *((uint4*)kdst + lane) = ((const uint4*)hk)[lane];
+        *((uint4*)vdst + lane) = ((const uint4*)hv)[lane];
+      }
+      while (comb_seq[cb] != ui / C::kNB) { }
+      for (int h = 0; h < G; ++h) {
+        float part = 0.f;
+        for (int d = lane; d < DH; d += 32) part = fmaf(bf16_to_f32(hq[h * DH + d].bits), bf16_to_f32(hk[d].bits), part);
+        part = warp_sum(part) * a.scale_log2;
+        float* nb = cbuf + (C::kW * G + h) * (DH + 2);
+        for (int d = lane; d < DH; d += 32) nb[d] = bf16_to_f32(hv[d].bits);
+        if (lane == 0) { nb[DH] = part; nb[DH + 1] = 1.f; }
+      }
+    }
+    if (cw == C::kW - 1) {
+      for (int i = lane; i < G * DH / 8; i += 32)
+        *((uint4*)(bwd + (long)b * ld_bwd + (long)g * G * DH) + i) = ((const uint4*)hx)[i];
+    }
+
+    for (int c = 0; c < nch; ++c, ++it) {
+      const int s = it % C::kStages;
+      const int np = max(0, min(C::kTpos, L - c * C::kTpos));
+      if (c > 0) mbar_wait(&full[s], (it / C::kStages) & 1);
+      const uint32_t st = smem_u32(smem + s * C::kStageBytes);
+      if (cw * 8 < np) {
+        // ---- S = Q Kᵀ for positions 8cw..8cw+7 (B fragments by ldmatrix from the swizzled boxes)
+        float sacc[4] = {0.f, 0.f, 0.f, 0.f};
+        const int prow = cw * 8 + (lane & 7);          // position row this lane addresses
+#pragma unroll
+        for (int kk = 0; kk < 8; kk += 2) {
+          const int chunk = kk * 2 + (lane >> 3);       // 16-byte d_h chunk 0..15 of block lane/8
+          const uint32_t addr = st + (chunk >> 3) * C::kBox + prow * 128 + (((chunk & 7) ^ (prow & 7)) << 4);
+          uint32_t b0, b1, b2, b3;
+          ldsm_x4(addr, b0, b1, b2, b3);
+          mma_16816(sacc, qa[kk][0], 0u, qa[kk][1], 0u, b0, b1);
+          mma_16816(sacc, qa[kk + 1][0], 0u, qa[kk + 1][1], 0u, b2, b3);
+        }
+        // ---- online softmax per query head (row qr) over this warp's 8 positions
+        const int p0 = cw * 8 + qc;
+        float s0 = (p0 < np) ? sacc[0] * a.scale_log2 : -INFINITY;
+        float s1 = (p0 + 1 < np) ? sacc[1] * a.scale_log2 : -INFINITY;
+        float mx = fmaxf(s0, s1);
+        mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 1));
+        mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 2));
+        const float mn = fmaxf(m, mx);                  // mx is finite: position 8cw < np
+        const float corr = (m == -INFINITY) ? 0.f : exp2f(m - mn);
+        const float e0 = exp2f(s0 - mn), e1 = exp2f(s1 - mn);
+        l = l * corr + e0 + e1;
+        m = mn;
+#pragma unroll
+        for (int j = 0; j < 16; ++j) { o[j][0] *= corr; o[j][1] *= corr; }
+        const uint32_t pa = pack_bf16x2(e0, e1);        // P as the A operand (rows 8..15 zero)
+        // ---- O += P Vw (V fragments by ldmatrix.trans: 4 d_h tiles of 8 per instruction)
+#pragma unroll
+        for (int dg = 0; dg < 4; ++dg) {
+          const int chunk = dg * 4 + (lane >> 3);       // d_h chunk (8 d_h) of tile lane/8
+          const uint32_t addr =
+              st + 2 * C::kBox + (chunk >> 3) * C::kBox + prow * 128 + (((chunk & 7) ^ (prow & 7)) << 4);
+          uint32_t v0, v1, v2, v3;
+          ldsm_x4_t(addr, v0, v1, v2, v3);
+          mma_1688(o[dg * 4 + 0], pa, 0u, v0);
+          mma_1688(o[dg * 4 + 1], pa, 0u, v1);
+          mma_1688(o[dg * 4 + 2], pa, 0u, v2);
+          mma_1688(o[dg * 4 + 3], pa, 0u, v3);
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[s]);
+    }
+
+    // publish this warp's state [warp][head][DH + 2]; the last warp merges 8 + 1 states per head
+    l += __shfl_xor_sync(0xffffffffu, l, 1);
+    l += __shfl_xor_sync(0xffffffffu, l, 2);
+    if (cw != 0) while (comb_seq[cb] != ui / C::kNB) { }
+    if (qr < G) {
+      float* wb = cbuf + (cw * G + qr) * (DH + 2);
+#pragma unroll
+      for (int j = 0; j < 16; ++j) { wb[j * 8 + qc] = o[j][0]; wb[j * 8 + qc + 1] = o[j][1]; }
+      if ((lane & 3) == 0) { wb[DH] = m; wb[DH + 1] = l; }
+    }
+    __syncwarp();
+    int last = 0;
+    if (lane == 0) {
+      __threadfence_block();
+      last = atomicAdd(&comb_cnt[cb], 1) == C::kW - 1;
+    }
+    last = __shfl_sync(0xffffffffu, last, 0);
+    if (last) {
+      __threadfence_block();
+      for (int hq = 0; hq < G; ++hq) {
+        float M = -INFINITY;
+#pragma unroll
+        for (int w = 0; w <= C::kW; ++w) M = fmaxf(M, cbuf[(w * G + hq) * (DH + 2) + DH]);
+        float f[C::kW + 1];
+        float den = 0.f;
+#pragma unroll
+        for (int w = 0; w <= C::kW; ++w) {
+          const float mw = cbuf[(w * G + hq) * (DH + 2) + DH];
+          f[w] = (mw == -INFINITY) ? 0.f : exp2f(mw - M);
+          den += cbuf[(w * G + hq) * (DH + 2) + DH + 1] * f[w];
+        }
+        const float inv = 1.f / den;
+        bf16_t* orow = bwd + (long)b * ld_bwd + a.D + (long)(g * G + hq) * DH;
+        for (int d = lane; d < DH; d += 32) {
+          float acc = 0.f;
+#pragma unroll
+          for (int w = 0; w <= C::kW; ++w) acc += cbuf[(w * G + hq) * (DH + 2) + d] * f[w];
+          St<bf16_t>::store(orow, d, acc * inv);
+        }
+      }
+      __syncwarp();
+      if (lane == 0) {
+        comb_cnt[cb] = 0;
+        __threadfence_block();
+        comb_seq[cb] = ui / C::kNB + 1;
+      }
+    }
+  }
+}
+
+}  // namespace gh

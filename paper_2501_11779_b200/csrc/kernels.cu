@@ -378,6 +378,21 @@ cudaError_t make_tmap_bf16(CUtensorMap* out, const void* base, uint64_t rows, ui
   return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorInvalidValue;
 }
 
+// KV arena [rows][positions][d_h] (bf16, d_h = 128) as a 3-D tensor map with 64 x 64 boxes and the
+// 128-byte swizzle (tensor-core GQA attention)
+cudaError_t make_tmap_kv(CUtensorMap* out, const void* base, uint64_t rows, uint64_t positions, uint64_t dh) {
+  auto enc = get_encode();
+  if (!enc) return cudaErrorNotSupported;
+  cuuint64_t dims[3] = {dh, positions, rows};
+  cuuint64_t strides[2] = {dh * 2, positions * dh * 2};
+  cuuint32_t box[3] = {64, 64, 1};
+  cuuint32_t estr[3] = {1, 1, 1};
+  CUresult r = enc(out, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(base), dims, strides, box, estr,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorInvalidValue;
+}
+
 static const int kBNs[] = {16, 32, 64, 128};  // batches > 128 use several batch tiles
 static int stages_override = 0;  // diagnostics
 static int cluster_override = 0;  // diagnostics
@@ -692,6 +707,10 @@ static cudaError_t configure_attn_gqa() {
   return cudaFuncSetAttribute(attn_gqa_kernel<T, DH, G>, cudaFuncAttributePreferredSharedMemoryCarveout,
                               (int)cudaSharedmemCarveoutMaxShared);
 }
+template <int G>
+static cudaError_t configure_attn_gqa_tc() {
+  return cudaFuncSetAttribute(attn_gqa_tc_kernel<G>, cudaFuncAttributeMaxDynamicSharedMemorySize, GqaTcCfg<G>::kSmem);
+}
 template <typename T, int DH>
 static cudaError_t configure_attn() {
   cudaError_t e = configure_attn_w<T, DH, 8>();
@@ -727,8 +746,24 @@ static int gqa_group(const AttnArgs& a) {
   const int G = a.Hkv > 0 && a.H % a.Hkv == 0 ? a.H / a.Hkv : 1;
   return (!off && (G == 2 || G == 4 || G == 8)) ? G : 0;
 }
+template <int G>
+static cudaError_t launch_attn_gqa_tc(const AttnArgs& a, cudaStream_t st) {
+  using C = GqaTcCfg<G>;
+  const int units = a.B * a.Hkv;
+  if (units <= 0) return cudaSuccess;
+  const int grid = std::min(units, kNumSMs);
+  return launch_pdl(attn_gqa_tc_kernel<G>, grid, C::kThreads, C::kSmem, st, *a.kv_tmap, a);
+}
 template <typename T, int DH>
 static cudaError_t launch_attn_t(const AttnArgs& a, cudaStream_t st) {
+  static const bool no_tc = getenv("GH_NO_GQA_TC") != nullptr;  // diagnostics: CUDA-core GQA kernel
+  if constexpr (sizeof(T) == 2 && DH == 128) {
+    if (a.kv_tmap && !no_tc) switch (gqa_group(a)) {
+        case 2: return launch_attn_gqa_tc<2>(a, st);
+        case 4: return launch_attn_gqa_tc<4>(a, st);
+        case 8: return launch_attn_gqa_tc<8>(a, st);
+      }
+  }
   switch (gqa_group(a)) {
     case 2: return launch_attn_gqa<T, DH, 2>(a, st);
     case 4: return launch_attn_gqa<T, DH, 4>(a, st);
@@ -763,6 +798,7 @@ cudaError_t configure_kernels() {
   auto chk = [&](cudaError_t r) { if (e == cudaSuccess) e = r; };
   chk(configure_tc<16>()); chk(configure_tc<32>()); chk(configure_tc<64>()); chk(configure_tc<128>());
   chk(configure_tc<192>());
+  chk(configure_attn_gqa_tc<2>()); chk(configure_attn_gqa_tc<4>()); chk(configure_attn_gqa_tc<8>());
   chk(cudaFuncSetAttribute(gemm_pair_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
   chk(configure_attn<bf16_t, 48>()); chk(configure_attn<bf16_t, 64>()); chk(configure_attn<bf16_t, 128>());
   chk(configure_attn<float, 48>()); chk(configure_attn<float, 64>()); chk(configure_attn<float, 128>());

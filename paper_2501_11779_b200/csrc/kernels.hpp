@@ -80,6 +80,8 @@ cudaError_t launch_gemm(const Weight& W, const CUtensorMap* tmW, const void* X, 
                         const EpiParams& ep, const GemmScratch& scratch, cudaStream_t st,
                         const void* pf = nullptr, size_t pf_bytes = 0);  // L2 prefetch of the next weights
 
+cudaError_t make_tmap_kv(CUtensorMap* out, const void* base, uint64_t rows, uint64_t positions, uint64_t dh);
+
 cudaError_t launch_rmsnorm(int dtype_bytes, const void* x, long ldx, const void* w, void* y,
                            long ldy, void* copy_out, long ldc, int B, int D, float eps,
                            cudaStream_t st);

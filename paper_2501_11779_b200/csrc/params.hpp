@@ -77,6 +77,9 @@ struct AttnArgs {
   int flags;            // diagnostics: 1 = consumers release stages without computing
   const void* pf;       // L2 prefetch of the next kernel's leading weight bytes (see GemmShape)
   unsigned long long pf_bytes;
+  int layer_local;      // layer index inside the Tier-2's arena (tensor-core GQA path)
+  int n_slots;
+  const CUtensorMap* kv_tmap;  // host-side: 3-D map of the whole arena (nullptr = no TMA path)
 };
 
 }  // namespace gh

@@ -458,6 +458,8 @@ struct gh_tier2 {
   std::vector<std::unique_ptr<DevMem>> mem;
   void* arena = nullptr;
   size_t arena_bytes = 0;
+  bool has_tmap = false;
+  CUtensorMap kv_tmap;  // whole arena, 3-D (tensor-core GQA attention)
   long slot_stride() const { return 2L * sh.Hkv * sh.S * sh.dh; }
   long layer_stride() const { return (long)n_slots * slot_stride(); }
 };
@@ -484,6 +486,13 @@ gh_status gh_tier2_create(const gh_model_spec* spec, int device, uint32_t layer_
     return fail(GH_EINFEASIBLE, "KV arena of " + std::to_string(t->arena_bytes) +
                                     " bytes exceeds free device memory (binding constraint: memory)");
   GH_TRY(dev_alloc(t->mem, t->arena_bytes, &t->arena));
+  // zeroed once: never-written positions are finite (tile loads past a prompt's length are masked,
+  // and 0 x NaN would not be)
+  GH_CUDA(cudaMemset(t->arena, 0, t->arena_bytes));
+  if (sh.db == 2 && sh.dh == 128 && sh.Hkv < sh.H) {
+    const uint64_t rows = (uint64_t)(layer_end - layer_begin) * n_slots * 2 * sh.Hkv;
+    t->has_tmap = make_tmap_kv(&t->kv_tmap, t->arena, rows, (uint64_t)sh.S, 128) == cudaSuccess;
+  }
   *out = t.release();
   return GH_OK;
 }
@@ -536,6 +545,9 @@ static gh_status t2_attend(gh_tier2* t, uint32_t layer, uint32_t B, const uint32
   a.flags = attn_flags;
   a.pf = pf;
   a.pf_bytes = pf ? pf_bytes : 0;
+  a.layer_local = (int)(layer - t->l0);
+  a.n_slots = (int)t->n_slots;
+  a.kv_tmap = t->has_tmap ? &t->kv_tmap : nullptr;
   GH_CUDA(launch_attention(s.db, s.dh, a, (cudaStream_t)stream));
   return GH_OK;
 }

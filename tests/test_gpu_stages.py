@@ -23,9 +23,13 @@ SPECS = {
     "small-bf16": gh.ModelSpec("small-bf16", 2, 512, 512, 1024, 4, 4, 256, 2, 2000),
     "gqa-bf16": gh.ModelSpec("gqa-bf16", 2, 1024, 256, 1536, 16, 4, 256, 2, 1000),
     "dh64-bf16": gh.ModelSpec("dh64-bf16", 2, 512, 512, 768, 8, 8, 192, 2, 777),
+    # d_h 128 with G = 8 and G = 2 query heads per KV head: the tensor-core GQA attention kernel
+    "gqa8-dh128": gh.ModelSpec("gqa8-dh128", 2, 2048, 256, 2048, 16, 2, 320, 2, 900),
+    "gqa2-dh128": gh.ModelSpec("gqa2-dh128", 2, 1024, 512, 1536, 8, 4, 200, 2, 900),
     "7b-2layer": gh.LLAMA2_7B.with_(n_layers=2, max_seq_len=512),
 }
-BATCH = {"tiny-fp32": 4, "small-bf16": 24, "gqa-bf16": 9, "dh64-bf16": 37, "7b-2layer": 64}
+BATCH = {"tiny-fp32": 4, "small-bf16": 24, "gqa-bf16": 9, "dh64-bf16": 37, "7b-2layer": 64, "gqa8-dh128": 11,
+         "gqa2-dh128": 7}
 
 
 def to_torch(a, spec):
