@@ -196,6 +196,8 @@ def workload(args, world):
     c = gh.CONFIGS[cfg]
     spec, ctx = c["spec"], c["ctx"]
     if world == 1:
+        if cfg in ("C4", "C5"):
+            raise SystemExit(f"--config {cfg} is a tier-split configuration (run it with N >= 2 GPUs)")
         return dict(name=cfg, spec=spec, ctx=ctx, batch=c["batch"], requested=c["batch"], inflight=1,
                     shard=c["batch"], kp=0)
     n1 = max(1, args.tier1)
@@ -209,7 +211,7 @@ def workload(args, world):
                     inflight=IF, shard=shard, kp=kp,
                     admitted_slots=gh.two_tier_context_slots(spec, 1, kp, 179 * GiB, ctx))
     mem = 179 * GiB
-    slots = gh.two_tier_context_slots(spec, 1, kp, mem, ctx)  # optimizer.cpp:175-192
+    slots = gh.two_tier_context_slots(spec, n1, kp, mem, ctx)  # optimizer.cpp:175-192
     inflight = 2
     per_gpu = slots // kp
     shard = min(per_gpu // inflight, c["batch"] // (kp * inflight) or 1)
@@ -425,7 +427,7 @@ def main():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", default=None, choices=[None, "C2", "C3"])
+    ap.add_argument("--config", default=None, choices=[None, "C2", "C3", "C4", "C5"])
     ap.add_argument("--cpu-threads", type=int, default=0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--tier1", type=int, default=1,
