@@ -290,7 +290,7 @@ __global__ void __launch_bounds__(AttnCfg<T, DH, W>::kThreads, 1)
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[s]);
     }
-    if (a.flags & 1) continue;
+    if (a.flags & 3) continue;  // diagnostics: 1 = streaming only, 2 = no merge / output
 
     // merge the groups of this warp (m is warp-uniform)
 #pragma unroll

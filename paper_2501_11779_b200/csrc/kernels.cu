@@ -757,12 +757,14 @@ static cudaError_t launch_attn_gqa_tc(const AttnArgs& a, cudaStream_t st) {
 template <typename T, int DH>
 static cudaError_t launch_attn_t(const AttnArgs& a, cudaStream_t st) {
   static const bool no_tc = getenv("GH_NO_GQA_TC") != nullptr;  // diagnostics: CUDA-core GQA kernel
+  static const bool mha_tc = getenv("GH_MHA_TC") != nullptr;     // diagnostics: tensor-core kernel for MHA
   if constexpr (sizeof(T) == 2 && DH == 128) {
     if (a.kv_tmap && !no_tc) switch (gqa_group(a)) {
         case 2: return launch_attn_gqa_tc<2>(a, st);
         case 4: return launch_attn_gqa_tc<4>(a, st);
         case 8: return launch_attn_gqa_tc<8>(a, st);
       }
+    if (a.kv_tmap && mha_tc && a.H == a.Hkv) return launch_attn_gqa_tc<1>(a, st);
   }
   switch (gqa_group(a)) {
     case 2: return launch_attn_gqa<T, DH, 2>(a, st);
@@ -798,7 +800,8 @@ cudaError_t configure_kernels() {
   auto chk = [&](cudaError_t r) { if (e == cudaSuccess) e = r; };
   chk(configure_tc<16>()); chk(configure_tc<32>()); chk(configure_tc<64>()); chk(configure_tc<128>());
   chk(configure_tc<192>());
-  chk(configure_attn_gqa_tc<2>()); chk(configure_attn_gqa_tc<4>()); chk(configure_attn_gqa_tc<8>());
+  chk(configure_attn_gqa_tc<1>()); chk(configure_attn_gqa_tc<2>()); chk(configure_attn_gqa_tc<4>());
+  chk(configure_attn_gqa_tc<8>());
   chk(cudaFuncSetAttribute(gemm_pair_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
   chk(configure_attn<bf16_t, 48>()); chk(configure_attn<bf16_t, 64>()); chk(configure_attn<bf16_t, 128>());
   chk(configure_attn<float, 48>()); chk(configure_attn<float, 64>()); chk(configure_attn<float, 128>());

@@ -489,7 +489,7 @@ gh_status gh_tier2_create(const gh_model_spec* spec, int device, uint32_t layer_
   // zeroed once: never-written positions are finite (tile loads past a prompt's length are masked,
   // and 0 x NaN would not be)
   GH_CUDA(cudaMemset(t->arena, 0, t->arena_bytes));
-  if (sh.db == 2 && sh.dh == 128 && sh.Hkv < sh.H) {
+  if (sh.db == 2 && sh.dh == 128) {
     const uint64_t rows = (uint64_t)(layer_end - layer_begin) * n_slots * 2 * sh.Hkv;
     t->has_tmap = make_tmap_kv(&t->kv_tmap, t->arena, rows, (uint64_t)sh.S, 128) == cudaSuccess;
   }
