@@ -36,7 +36,7 @@ struct AttnCfg {
   static constexpr int kHdrBytes = 4 * DH * (int)sizeof(T) + 16;
   static constexpr int kStageBytes = ((2 * kTileBytes + kHdrBytes + 127) / 128) * 128;
   static constexpr int kStages = (196608 / kStageBytes) > 6 ? 6 : (196608 / kStageBytes);
-  static constexpr int kThreads = 32 * (1 + kW);
+  static constexpr int kThreads = 32 * (2 + kW);       // producer, kW consumers, merge warp
   static constexpr int kEl = kCpl * kVec;              // elements per lane
   static constexpr int kNB = 4;                        // combine buffers (units in flight)
   static constexpr int kCombOffset = kStages * kStageBytes;
@@ -87,6 +87,7 @@ __global__ void __launch_bounds__(AttnCfg<T, DH, W>::kThreads, 1)
   float* comb = (float*)(smem + C::kCombOffset);
   int* comb_cnt = (int*)(smem + C::kCtlOffset);       // [kNB] warps that published unit i
   volatile int* comb_seq = comb_cnt + C::kNB;          // [kNB] units combined from this buffer
+  volatile int* comb_bh = comb_cnt + 2 * C::kNB;       // [kNB][2] (prompt, head) of the unit in the buffer
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -153,6 +154,47 @@ __global__ void __launch_bounds__(AttnCfg<T, DH, W>::kThreads, 1)
         sl = sln;
       }
       prefetch_l2_share(a.pf, a.pf_bytes, blockIdx.x, gridDim.x);
+    }
+    return;
+  }
+
+  if (warp == C::kW + 1) {
+    // -------------------------------------------------- merge warp: combines the kW published
+    // partial states of each unit (in unit order) and writes the output row, so that no consumer
+    // warp falls behind the stage ring while merging
+    if (a.flags & 3) return;
+    int ui = 0;
+    for (int u = blockIdx.x; u < n_units; u += gridDim.x, ++ui) {
+      const int cb = ui % C::kNB;
+      while (*(volatile int*)&comb_cnt[cb] < C::kW) { }
+      __threadfence_block();
+      const float* cbuf = comb + cb * C::kW * (DH + 2);
+      const int b = comb_bh[2 * cb], h = comb_bh[2 * cb + 1];
+      float M = -INFINITY;
+#pragma unroll
+      for (int w = 0; w < C::kW; ++w) M = fmaxf(M, cbuf[w * (DH + 2) + DH]);
+      float den = 0.f;
+      float f[C::kW];
+#pragma unroll
+      for (int w = 0; w < C::kW; ++w) {
+        const float mw = cbuf[w * (DH + 2) + DH];
+        f[w] = (mw == -INFINITY) ? 0.f : exp2f(mw - M);
+        den += cbuf[w * (DH + 2) + DH + 1] * f[w];
+      }
+      const float inv = 1.f / den;
+      T* orow = bwd + (long)b * ld_bwd + a.D + (long)h * DH;
+      for (int d = lane; d < DH; d += 32) {
+        float acc = 0.f;
+#pragma unroll
+        for (int w = 0; w < C::kW; ++w) acc += cbuf[w * (DH + 2) + d] * f[w];
+        St<T>::store(orow, d, acc * inv);
+      }
+      __syncwarp();
+      if (lane == 0) {
+        comb_cnt[cb] = 0;
+        __threadfence_block();
+        comb_seq[cb] = ui / C::kNB + 1;
+      }
     }
     return;
   }
@@ -299,8 +341,8 @@ __global__ void __launch_bounds__(AttnCfg<T, DH, W>::kThreads, 1)
 #pragma unroll
       for (int e = 0; e < C::kEl; ++e) o[e] += __shfl_xor_sync(0xffffffffu, o[e], o2);
     }
-    // publish this warp's state to combine buffer ui % kNB; the last warp to publish merges the
-    // kW states and writes the output (no CTA barrier: the other warps move on to the next unit)
+    // publish this warp's state to combine buffer ui % kNB for the merge warp (no CTA barrier: the
+    // consumer warps move on to the next unit)
     const int cb = ui % C::kNB;
     while (comb_seq[cb] != ui / C::kNB) { }  // the merge of unit ui - kNB has left this buffer
     float* cbuf = comb + cb * C::kW * (DH + 2);
@@ -312,40 +354,11 @@ __global__ void __launch_bounds__(AttnCfg<T, DH, W>::kThreads, 1)
         for (int e = 0; e < C::kVec; ++e) cwbuf[(sub + j * C::kLpp) * C::kVec + e] = o[j * C::kVec + e];
     }
     if (lane == 0) { cwbuf[DH] = m; cwbuf[DH + 1] = l; }
+    if (cw == 0 && lane == 0) { comb_bh[2 * cb] = b; comb_bh[2 * cb + 1] = h; }
     __syncwarp();
-    int last = 0;
     if (lane == 0) {
       __threadfence_block();
-      last = atomicAdd(&comb_cnt[cb], 1) == C::kW - 1;
-    }
-    last = __shfl_sync(0xffffffffu, last, 0);
-    if (last) {
-      __threadfence_block();
-      float M = -INFINITY;
-#pragma unroll
-      for (int w = 0; w < C::kW; ++w) M = fmaxf(M, cbuf[w * (DH + 2) + DH]);
-      float den = 0.f;
-      float f[C::kW];
-#pragma unroll
-      for (int w = 0; w < C::kW; ++w) {
-        const float mw = cbuf[w * (DH + 2) + DH];
-        f[w] = (mw == -INFINITY) ? 0.f : exp2f(mw - M);
-        den += cbuf[w * (DH + 2) + DH + 1] * f[w];
-      }
-      const float inv = 1.f / den;
-      T* orow = bwd + (long)b * ld_bwd + a.D + (long)h * DH;
-      for (int d = lane; d < DH; d += 32) {
-        float acc = 0.f;
-#pragma unroll
-        for (int w = 0; w < C::kW; ++w) acc += cbuf[w * (DH + 2) + d] * f[w];
-        St<T>::store(orow, d, acc * inv);
-      }
-      __syncwarp();
-      if (lane == 0) {
-        comb_cnt[cb] = 0;
-        __threadfence_block();
-        comb_seq[cb] = ui / C::kNB + 1;
-      }
+      atomicAdd(&comb_cnt[cb], 1);
     }
   }
 }

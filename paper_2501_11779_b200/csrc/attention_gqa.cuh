@@ -368,7 +368,7 @@ namespace gh {
 // w owns positions 8w..8w+7 of every 64-position stage: S (16 x 8) = Q (16 x 128) · K_wᵀ as 8
 // MMAs, an online softmax per query head over its quad of lanes, O (16 x 128) += P (16 x 8) · V_w
 // as 16 MMAs.  The 8 warps' states and the new token's (computed on CUDA cores by warp 0) are
-// merged by the last warp of the unit.
+// merged by a dedicated merge warp, so no consumer falls behind the stage ring.
 GH_DEV void ldsm_x4(uint32_t addr, uint32_t& r0, uint32_t& r1, uint32_t& r2, uint32_t& r3) {
   asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0, %1, %2, %3}, [%4];"
                : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3) : "r"(addr));
@@ -411,7 +411,7 @@ struct GqaTcCfg {
   static constexpr int kCombBytes = kNB * kCombPerUnit * 4;
   static constexpr int kStages = ((227 * 1024 - 2048 - kCombBytes - 1024) / kStageBytes) > 6
                                      ? 6 : ((227 * 1024 - 2048 - kCombBytes - 1024) / kStageBytes);
-  static constexpr int kThreads = 32 * (1 + kW);
+  static constexpr int kThreads = 32 * (2 + kW);   // producer, kW consumers, merge warp
   static constexpr int kCombOffset = kStages * kStageBytes;
   static constexpr int kCtlOffset = kCombOffset + ((kCombBytes + 127) / 128) * 128;
   static constexpr int kBarOffset = kCtlOffset + 128;
@@ -431,6 +431,7 @@ __global__ void __launch_bounds__(GqaTcCfg<G>::kThreads, 1)
   float* comb = (float*)(smem + C::kCombOffset);
   int* comb_cnt = (int*)(smem + C::kCtlOffset);
   volatile int* comb_seq = comb_cnt + C::kNB;
+  volatile int* comb_bg = comb_cnt + 2 * C::kNB;  // [kNB][2] (prompt, KV head) of the unit in the buffer
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -499,6 +500,47 @@ __global__ void __launch_bounds__(GqaTcCfg<G>::kThreads, 1)
         sl = sln;
       }
       prefetch_l2_share(a.pf, a.pf_bytes, blockIdx.x, gridDim.x);
+    }
+    return;
+  }
+
+  if (warp == C::kW + 1) {
+    // -------------------------------------------------- merge warp (unit order): combines the kW
+    // consumer states and the new token's state of every query head, writes the G output rows
+    int ui = 0;
+    for (int u = blockIdx.x; u < n_units; u += gridDim.x, ++ui) {
+      const int cb = ui % C::kNB;
+      while (*(volatile int*)&comb_cnt[cb] < C::kW) { }
+      __threadfence_block();
+      const float* cbuf = comb + cb * C::kCombPerUnit;
+      const int b = comb_bg[2 * cb], g = comb_bg[2 * cb + 1];
+      for (int hq = 0; hq < G; ++hq) {
+        float M = -INFINITY;
+#pragma unroll
+        for (int w = 0; w <= C::kW; ++w) M = fmaxf(M, cbuf[(w * G + hq) * (DH + 2) + DH]);
+        float f[C::kW + 1];
+        float den = 0.f;
+#pragma unroll
+        for (int w = 0; w <= C::kW; ++w) {
+          const float mw = cbuf[(w * G + hq) * (DH + 2) + DH];
+          f[w] = (mw == -INFINITY) ? 0.f : exp2f(mw - M);
+          den += cbuf[(w * G + hq) * (DH + 2) + DH + 1] * f[w];
+        }
+        const float inv = 1.f / den;
+        bf16_t* orow = bwd + (long)b * ld_bwd + a.D + (long)(g * G + hq) * DH;
+        for (int d = lane; d < DH; d += 32) {
+          float acc = 0.f;
+#pragma unroll
+          for (int w = 0; w <= C::kW; ++w) acc += cbuf[(w * G + hq) * (DH + 2) + d] * f[w];
+          St<bf16_t>::store(orow, d, acc * inv);
+        }
+      }
+      __syncwarp();
+      if (lane == 0) {
+        comb_cnt[cb] = 0;
+        __threadfence_block();
+        comb_seq[cb] = ui / C::kNB + 1;
+      }
     }
     return;
   }
@@ -620,42 +662,11 @@ __global__ void __launch_bounds__(GqaTcCfg<G>::kThreads, 1)
       for (int j = 0; j < 16; ++j) { wb[j * 8 + qc] = o[j][0]; wb[j * 8 + qc + 1] = o[j][1]; }
       if ((lane & 3) == 0) { wb[DH] = m; wb[DH + 1] = l; }
     }
+    if (cw == 0 && lane == 0) { comb_bg[2 * cb] = b; comb_bg[2 * cb + 1] = g; }
     __syncwarp();
-    int last = 0;
     if (lane == 0) {
       __threadfence_block();
-      last = atomicAdd(&comb_cnt[cb], 1) == C::kW - 1;
-    }
-    last = __shfl_sync(0xffffffffu, last, 0);
-    if (last) {
-      __threadfence_block();
-      for (int hq = 0; hq < G; ++hq) {
-        float M = -INFINITY;
-#pragma unroll
-        for (int w = 0; w <= C::kW; ++w) M = fmaxf(M, cbuf[(w * G + hq) * (DH + 2) + DH]);
-        float f[C::kW + 1];
-        float den = 0.f;
-#pragma unroll
-        for (int w = 0; w <= C::kW; ++w) {
-          const float mw = cbuf[(w * G + hq) * (DH + 2) + DH];
-          f[w] = (mw == -INFINITY) ? 0.f : exp2f(mw - M);
-          den += cbuf[(w * G + hq) * (DH + 2) + DH + 1] * f[w];
-        }
-        const float inv = 1.f / den;
-        bf16_t* orow = bwd + (long)b * ld_bwd + a.D + (long)(g * G + hq) * DH;
-        for (int d = lane; d < DH; d += 32) {
-          float acc = 0.f;
-#pragma unroll
-          for (int w = 0; w <= C::kW; ++w) acc += cbuf[(w * G + hq) * (DH + 2) + d] * f[w];
-          St<bf16_t>::store(orow, d, acc * inv);
-        }
-      }
-      __syncwarp();
-      if (lane == 0) {
-        comb_cnt[cb] = 0;
-        __threadfence_block();
-        comb_seq[cb] = ui / C::kNB + 1;
-      }
+      atomicAdd(&comb_cnt[cb], 1);
     }
   }
 }
