@@ -212,9 +212,13 @@ def workload(args, world):
                     admitted_slots=gh.two_tier_context_slots(spec, 1, kp, 179 * GiB, ctx))
     mem = 179 * GiB
     slots = gh.two_tier_context_slots(spec, n1, kp, mem, ctx)  # optimizer.cpp:175-192
-    inflight = 2
+    inflight = args.inflight or 2
     per_gpu = slots // kp
     shard = min(per_gpu // inflight, c["batch"] // (kp * inflight) or 1)
+    if args.shard:  # e.g. the reference optimizer's choice (oracle.Ref.optimize)
+        shard = args.shard
+        if shard * inflight > per_gpu:
+            raise SystemExit(f"--shard {shard} x IF {inflight} exceeds the {per_gpu} admitted slots per Tier-2 GPU")
     return dict(name=cfg, spec=spec, ctx=ctx, batch=shard * kp, requested=c["batch"], inflight=inflight,
                 shard=shard, kp=kp, admitted_slots=slots)
 

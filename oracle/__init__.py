@@ -239,6 +239,7 @@ def rlib() -> C.CDLL:
             "ref_profile_check": (C.c_int, [C.c_char_p, P(C.c_int)]),
             "ref_profile_latency": (C.c_int, [C.c_char_p, C.c_int, u64, u64, P(C.c_int64)]),
             "ref_cmd_simulate": (C.c_int, [C.c_char_p] * 4 + [u64, u64, u64, u64, u64, C.c_char_p, u64]),
+            "ref_cmd_optimize": (C.c_int, [C.c_char_p] * 4 + [u64, u64, C.c_char_p, u64]),
         }
         for n, (r, a) in sig.items():
             f = getattr(L, n)
@@ -320,6 +321,13 @@ class Ref:
     def profile_latency(path, stage, batch, seq=0):
         o = C.c_int64()
         return rlib().ref_profile_latency(str(path).encode(), stage, batch, seq, C.byref(o)), o.value
+
+    @staticmethod
+    def optimize(model, cluster, t1, t2, seq=0, max_nodes=0):
+        buf = C.create_string_buffer(1 << 20)
+        rc = rlib().ref_cmd_optimize(*(str(p).encode() for p in (model, cluster, t1, t2)), seq, max_nodes,
+                                     buf, 1 << 20)
+        return rc, buf.value.decode()
 
     @staticmethod
     def simulate(model, cluster, t1, t2, k1, k2, batch, seq=0, inflight=0):

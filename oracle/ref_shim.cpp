@@ -133,4 +133,21 @@ int ref_cmd_simulate(const char* model, const char* cluster, const char* t1_prof
   return rc;
 }
 
+// The reference optimizer (commands.hpp:92, optimizer.cpp:515-583) over the given profiles.
+int ref_cmd_optimize(const char* model, const char* cluster, const char* t1_profile, const char* t2_profile,
+                     uint64_t seq, uint64_t max_nodes, char* out, uint64_t cap) {
+  std::ostringstream os, es;
+  OptimizeArgs a;
+  a.model_path = model;
+  a.cluster_path = cluster;
+  a.profile_paths = {t1_profile, t2_profile};
+  if (seq) a.seq_len = seq;
+  if (max_nodes) a.max_nodes = max_nodes;
+  a.threads = 1;
+  int rc = cmd_optimize(a, os, es);
+  std::string s = os.str() + es.str();
+  if (out && cap) { strncpy(out, s.c_str(), cap - 1); out[cap - 1] = 0; }
+  return rc;
+}
+
 }  // extern "C"

@@ -2,6 +2,7 @@
 reference's own parser (profiles.cpp:168-224) with no warnings, and latency queries through the
 reference (profiles.cpp:93-129) return the emitted values."""
 import ctypes as C
+from pathlib import Path
 
 import pytest
 
@@ -63,3 +64,19 @@ def test_reference_parser_rejects_duplicates(tmp_path):
     write_profile(p, "b200", [("attention", 512, 4, 1.0), ("attention", 512, 4, 2.0)])
     rc, _ = Ref.profile_check(p)
     assert rc == 2
+
+
+@needs_ref
+def test_reference_optimizer_on_b200_profiles(tmp_path):
+    """the unmodified reference optimizer (optimizer.cpp:515-583) runs on the
+    committed B200 stage profiles (the Tier-1 file also carries the attention rows, which the
+    optimizer needs for single-tier candidates) and picks a two-tier configuration."""
+    root = Path(__file__).resolve().parents[1]
+    t1 = (root / "profiles/b200_tier1_C2.csv").read_text().splitlines()
+    t2 = (root / "profiles/b200_tier2_C2.csv").read_text().splitlines()
+    comb = tmp_path / "t1all.csv"
+    comb.write_text("\n".join(t1 + [ln.replace("b200-tier2", "b200-tier1") for ln in t2[1:]]) + "\n")
+    rc, rep = Ref.optimize(root / "configs/llama2-7b-ctx512.json", root / "configs/b200x8_cluster.json", comb,
+                           root / "profiles/b200_tier2_C2.csv", 512, 4)
+    assert rc == 0, rep
+    assert "best config: K=1 K'=" in rep and "tok/s" in rep
