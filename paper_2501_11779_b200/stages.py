@@ -249,3 +249,60 @@ class Dispatcher:
                 tok = nxt
         gen = np.stack(out, axis=1) if out else np.zeros((B, 0), np.int32)
         return gen, (np.stack(logits, axis=1) if want_logits else None)
+
+
+class ContinuousDispatcher:
+    """Continuous batching with context-slot reuse: the engine's B rows
+    are decode lanes, each bound to its own context slot; a request occupies a lane from its first
+    prompt token until it has generated `max_new` tokens, and the lane (with its slot) is then
+    handed to the next queued request at position 0.  Every step decodes all busy lanes at their
+    own positions (ragged contexts); idle lanes decode a dummy token at position 0 and are
+    ignored.  Reusing a slot needs no clearing: attention reads only the positions below the
+    request's current one, all of which it wrote itself."""
+
+    def __init__(self, engine: Engine):
+        self.engine = engine
+
+    def run(self, requests, max_new: int):
+        """requests: sequence of 1-D int32 prompt arrays (any lengths >= 1).  Returns the list of
+        generated token arrays (max_new each), in request order, and the number of steps."""
+        B = self.engine.batch
+        queue = list(range(len(requests)))
+        lane_req = [-1] * B           # request index in each lane
+        lane_t = [0] * B              # position of the lane's next input token
+        out = [[] for _ in requests]
+        tok = np.zeros(B, np.int32)
+        pos = np.zeros(B, np.int32)
+
+        def admit(lane):
+            if queue:
+                r = queue.pop(0)
+                lane_req[lane], lane_t[lane] = r, 0
+                tok[lane] = int(requests[r][0])
+            else:
+                lane_req[lane] = -1
+                tok[lane] = 0
+            pos[lane] = 0
+
+        for lane in range(B):
+            admit(lane)
+        steps = 0
+        while any(r >= 0 for r in lane_req):
+            nxt, _ = self.engine.step_host(tok, pos)
+            steps += 1
+            for lane in range(B):
+                r = lane_req[lane]
+                if r < 0:
+                    continue
+                t = lane_t[lane]
+                plen = len(requests[r])
+                if t + 1 < plen:          # still feeding the prompt
+                    tok[lane] = int(requests[r][t + 1])
+                else:
+                    out[r].append(int(nxt[lane]))
+                    tok[lane] = nxt[lane]
+                lane_t[lane] = t + 1
+                pos[lane] = t + 1
+                if len(out[r]) == max_new:
+                    admit(lane)       # the lane's slot goes to the next request
+        return [np.array(o, np.int32) for o in out], steps
