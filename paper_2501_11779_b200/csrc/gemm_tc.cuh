@@ -104,11 +104,36 @@ GH_DEV void compute_inv_rms(const EpiParams& ep, const GemmShape& gs, float* inv
   const float* __restrict__ ssp = ep.ss_in;
   const int ns = ep.ss_in_slices, Bt = gs.Bt;
   const float dim = (float)ep.ss_dim, eps = ep.ss_eps;
-  for (int b = threadIdx.x - 64; b < Bt; b += 128) {
-    float ss = 0.f;
-#pragma unroll 8
-    for (int s = 0; s < ns; ++s) ss += __ldg(ssp + (long)s * Bt + b);  // slice order: deterministic
-    inv[b] = 1.0f / sqrtf(ss / dim + eps);
+  const int t = threadIdx.x - 64;
+  if (Bt <= 128) {  // one column per thread: 16 slices in flight
+    if (t < Bt) {
+      float ss = 0.f;
+#pragma unroll 16
+      for (int s = 0; s < ns; ++s) ss += __ldg(ssp + (long)s * Bt + t);  // slice order: deterministic
+      inv[t] = 1.0f / sqrtf(ss / dim + eps);
+    }
+    return;
+  }
+  // up to 8 columns per thread (Bt <= 1024) summed together, so that 8 x 4 loads are in flight
+  // at once (the sums of a large batch otherwise serialise on load latency); slice order is kept
+  constexpr int kCols = 8;
+  for (int b0 = 0; b0 < Bt; b0 += 128 * kCols) {
+    float acc[kCols];
+#pragma unroll
+    for (int k = 0; k < kCols; ++k) acc[k] = 0.f;
+#pragma unroll 4
+    for (int s = 0; s < ns; ++s) {
+#pragma unroll
+      for (int k = 0; k < kCols; ++k) {
+        const int b = b0 + t + 128 * k;
+        if (b < Bt) acc[k] += __ldg(ssp + (long)s * Bt + b);
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < kCols; ++k) {
+      const int b = b0 + t + 128 * k;
+      if (b < Bt) inv[b] = 1.0f / sqrtf(acc[k] / dim + eps);
+    }
   }
 }
 
