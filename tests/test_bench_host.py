@@ -1,0 +1,43 @@
+"""Host-side logic of bench.py (CPU): the reference-style profile interpolation and the if_gh
+in-flight batch choice read from the committed B200 profiles."""
+import importlib.util
+import sys
+from pathlib import Path
+
+import pytest
+
+ROOT = Path(__file__).resolve().parents[1]
+
+
+@pytest.fixture(scope="module")
+def bench():
+    spec = importlib.util.spec_from_file_location("bench_mod", ROOT / "bench.py")
+    mod = importlib.util.module_from_spec(spec)
+    argv = sys.argv
+    sys.argv = ["bench.py"]
+    try:
+        spec.loader.exec_module(mod)
+    finally:
+        sys.argv = argv
+    return mod
+
+
+def test_profile_latency_interpolation(bench, tmp_path):
+    p = tmp_path / "t.csv"
+    p.write_text("device,stage,seq_len,batch_size,latency_us\n"
+                 "d,nonattention,512,2,10.0\nd,nonattention,512,4,20.0\nd,nonattention,512,8,30.0\n")
+    f = bench._profile_latency
+    assert f(p, "nonattention", 1) == 10.0          # clamp below (profiles.cpp:93-129)
+    assert f(p, "nonattention", 3) == 15.0          # interior interpolation
+    assert f(p, "nonattention", 12) == 40.0         # top-two extrapolation
+
+
+def test_if_gh_from_profiles(bench):
+    import paper_2501_11779_b200 as gh
+    spec = gh.CONFIGS["C2"]["spec"]
+    for kp in (1, 3, 7):
+        IF = bench.if_gh_from_profiles(spec, 64 * kp, 64, 512)
+        assert 2 <= IF <= 8
+    # Tier-1 nonattention grows with the batch while Tier-2 attention per shard is fixed, so the
+    # in-flight batches needed to cover a Tier-2 round trip never grow with K'
+    assert bench.if_gh_from_profiles(spec, 64 * 7, 64, 512) <= bench.if_gh_from_profiles(spec, 64, 64, 512)
