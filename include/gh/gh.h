@@ -158,6 +158,23 @@ gh_status gh_tier2_check(const gh_tier2* t2, uint32_t B, const uint32_t* slot_ho
  * values from `seed` (benchmark pre-fill; content does not change the cost). */
 gh_status gh_tier2_fill_synthetic(gh_tier2* t2, uint64_t seed, uint32_t n_slots_to_fill,
                                   uint32_t n_positions, void* stream);
+/* Paged KV arena (the page-granular form of the slot arena): n_slots logical slots
+ * share a pool of n_pages pages of GH_KV_PAGE_POSITIONS positions (all layers of the span, K and V,
+ * every KV head: n_pages * 2 * dtype * 64 * D_kv * span bytes).  A slot's positions must be mapped
+ * before a step attends them; pages return to the pool on unmap, so prompts of different lengths
+ * share the arena instead of each reserving max_seq_len.  Attention results are bit-identical to
+ * the contiguous arena. */
+#define GH_KV_PAGE_POSITIONS 64
+gh_status gh_tier2_create_paged(const gh_model_spec* spec, int device, uint32_t layer_begin,
+                                uint32_t layer_end, uint32_t n_slots, uint32_t n_pages, gh_tier2** out);
+/* Ensure positions [0, n_positions) of `slot` are backed by pages (grows the slot's mapping; no
+ * partial allocation: GH_EINFEASIBLE when the pool is short).  Synchronises `stream` first, so
+ * the table is updated between steps.  No-op (n_positions <= S checked) on a contiguous arena. */
+gh_status gh_tier2_map(gh_tier2* t2, uint32_t slot, uint32_t n_positions, void* stream);
+/* Return the slot's pages to the pool (after the last step that reads it has been queued on the
+ * stream the next gh_tier2_map synchronises). */
+gh_status gh_tier2_unmap(gh_tier2* t2, uint32_t slot);
+uint32_t gh_tier2_pages_free(const gh_tier2* t2);
 /* Copy one (layer, slot, kv, head) block of positions [0, n) to host (tests). */
 gh_status gh_tier2_read_kv(gh_tier2* t2, uint32_t layer, uint32_t slot, uint32_t kv,
                            uint32_t head, uint32_t n, void* host_out);
@@ -195,6 +212,9 @@ typedef struct gh_engine_config {
                               optimizer.cpp:116-123; embedding on the first, classifier on the
                               last) and ranks T + s*K' + j are the K' Tier-2 ranks dedicated to
                               span s; world = T * (1 + K').  Peer transport only. */
+  uint32_t kv_pages;       /* 0: contiguous slots of max_seq_len positions; > 0: paged KV arena of
+                              kv_pages pages of GH_KV_PAGE_POSITIONS positions shared by the slots
+                              (gh_tier2_create_paged; map with gh_engine_kv_map before a step) */
 } gh_engine_config;
 
 /* Inter-tier message transport of the pipelined tier-split step.
@@ -239,6 +259,10 @@ gh_status gh_engine_advance(gh_engine* e, uint32_t ib, int pos_increment, void* 
 gh_status gh_engine_read_next(gh_engine* e, uint32_t ib, int32_t* next_host);
 gh_tier1* gh_engine_tier1(gh_engine* e);
 gh_tier2* gh_engine_tier2(gh_engine* e);
+/* Paged KV (kv_pages > 0): gh_tier2_map / gh_tier2_unmap of this rank's Tier-2 (slot = ib * batch
+ * + row on a colocated engine, the local slot on a Tier-2 rank); no-ops for contiguous slots. */
+gh_status gh_engine_kv_map(gh_engine* e, uint32_t slot, uint32_t n_positions);
+gh_status gh_engine_kv_unmap(gh_engine* e, uint32_t slot);
 /* Launch count of this library's kernels since the last reset (device work accounting). */
 uint64_t gh_kernel_launches(int reset);
 

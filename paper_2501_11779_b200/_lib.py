@@ -62,7 +62,8 @@ class GhEngineConfig(C.Structure):
                 ("batch", C.c_uint32), ("inflight", C.c_uint32), ("n_slots", C.c_uint32),
                 ("use_graph", C.c_int),
                 ("transport", C.c_int),
-                ("tier1_ranks", C.c_uint32)]
+                ("tier1_ranks", C.c_uint32),
+                ("kv_pages", C.c_uint32)]
 
 
 u64, u32, i32, i64, vp = C.c_uint64, C.c_uint32, C.c_int32, C.c_int64, C.c_void_p
@@ -102,6 +103,10 @@ PROTOTYPES = {
     "gh_tier2_fill_synthetic": (st, [vp, u64, u32, u32, vp]),
     "gh_tier2_read_kv": (st, [vp, u32, u32, u32, u32, u32, vp]),
     "gh_tier2_arena_bytes": (u64, [vp]),
+    "gh_tier2_create_paged": (st, [P(GhSpec), C.c_int, u32, u32, u32, u32, P(vp)]),
+    "gh_tier2_map": (st, [vp, u32, u32, vp]),
+    "gh_tier2_unmap": (st, [vp, u32]),
+    "gh_tier2_pages_free": (u32, [vp]),
     "gh_comm_unique_id": (st, [P(C.c_uint8)]),
     "gh_comm_create": (st, [P(C.c_uint8), C.c_int, C.c_int, C.c_int, P(vp)]),
     "gh_comm_create_n": (st, [P(C.c_uint8), C.c_int, C.c_int, C.c_int, C.c_int, P(vp)]),
@@ -119,6 +124,8 @@ PROTOTYPES = {
     "gh_engine_read_next": (st, [vp, u32, vp]),
     "gh_engine_tier1": (vp, [vp]),
     "gh_engine_tier2": (vp, [vp]),
+    "gh_engine_kv_map": (st, [vp, u32, u32]),
+    "gh_engine_kv_unmap": (st, [vp, u32]),
     "gh_kernel_launches": (u64, [C.c_int]),
     "gh_debug_gemm_bench": (st, [C.c_int] * 7 + [P(C.c_float)]),
     "gh_debug_gemm_trace": (st, [C.c_int] * 5 + [P(C.c_float), P(C.c_uint64), C.c_int]),

@@ -20,6 +20,22 @@
 
 namespace gh {
 
+// K and V of positions [q0, q0 + np) of (slot sl, kv head g) into sk / sv: one bulk copy each for
+// contiguous slots, one per 64-position page segment for the paged arena.
+template <typename T, int DH>
+GH_DEV void load_kv_chunk(const AttnArgs& a, const T* arena, int sl, int g, int q0, int np, uint8_t* sk,
+                          uint8_t* sv, uint64_t* bar, uint64_t pol) {
+  for (int q = 0; q < np;) {
+    const int p = q0 + q;
+    const int n = a.page_table ? min(np - q, kKvPagePositions - p % kKvPagePositions) : np - q;
+    const T* kb = arena + kv_offset(a, sl, g, p, DH);
+    const uint32_t off = (uint32_t)q * DH * sizeof(T), bytes = (uint32_t)n * DH * sizeof(T);
+    bulk_g2s(sk + off, kb, bytes, bar, pol);
+    bulk_g2s(sv + off, kb + a.kv_stride, bytes, bar, pol);
+    q += n;
+  }
+}
+
 template <typename T, int DH, int W = 8>
 struct AttnCfg {
   static constexpr int kVec = 16 / sizeof(T);          // elements per 16-byte chunk
@@ -123,8 +139,6 @@ __global__ void __launch_bounds__(AttnCfg<T, DH, W>::kThreads, 1)
         const int un = u + gridDim.x;
         int Ln = 0, sln = 0;
         if (un < n_units) { Ln = a.pos[un / a.H]; sln = (int)a.slot[un / a.H]; }
-        const T* kbase = arena + (long)sl * a.slot_stride + (long)kvh * a.head_stride;
-        const T* vbase = kbase + a.kv_stride;
         const int nch = L > 0 ? (L + C::kTpos - 1) / C::kTpos : 1;
         for (int c = 0; c < nch; ++c, ++it) {
           const int s = it % C::kStages;
@@ -138,10 +152,7 @@ __global__ void __launch_bounds__(AttnCfg<T, DH, W>::kThreads, 1)
             meta[0] = L; meta[1] = b; meta[2] = h; meta[3] = sl;
           }
           mbar_arrive_expect_tx(&full[s], 2 * bytes + (c == 0 ? 4 * DH * (uint32_t)sizeof(T) : 0u));
-          if (np > 0) {
-            bulk_g2s(sk, kbase + (long)c * C::kTpos * DH, bytes, &full[s], pol);
-            bulk_g2s(sk + C::kTileBytes, vbase + (long)c * C::kTpos * DH, bytes, &full[s], pol);
-          }
+          if (np > 0) load_kv_chunk<T, DH>(a, arena, sl, kvh, c * C::kTpos, np, sk, sk + C::kTileBytes, &full[s], pol);
           if (c == 0) {
             const T* row = fwd + (long)b * ld_fwd;
             bulk_g2s(hdr, row + a.D + (long)h * DH, DH * sizeof(T), &full[s], pol);
@@ -231,7 +242,7 @@ __global__ void __launch_bounds__(AttnCfg<T, DH, W>::kThreads, 1)
 
     if (cw == 0) {
       // new token: score from the header, append k/v to the arena (group 0 lanes)
-      T* kdst = arena + (long)slot * a.slot_stride + (long)kvh * a.head_stride + (long)L * DH;
+      T* kdst = arena + kv_offset(a, slot, kvh, L, DH);
       T* vdst = kdst + a.kv_stride;
       float part = 0.f;
       float vf[C::kEl];

@@ -98,8 +98,6 @@ __global__ void __launch_bounds__(GqaCfg<T, DH, G>::kThreads, 1)
         const int un = u + gridDim.x;
         int Ln = 0, sln = 0;
         if (un < n_units) { Ln = a.pos[un / a.Hkv]; sln = (int)a.slot[un / a.Hkv]; }
-        const T* kbase = arena + (long)sl * a.slot_stride + (long)g * a.head_stride;
-        const T* vbase = kbase + a.kv_stride;
         const int nch = L > 0 ? (L + C::kTpos - 1) / C::kTpos : 1;
         for (int c = 0; c < nch; ++c, ++it) {
           const int s = it % C::kStages;
@@ -113,10 +111,7 @@ __global__ void __launch_bounds__(GqaCfg<T, DH, G>::kThreads, 1)
             meta[0] = L; meta[1] = b; meta[2] = g; meta[3] = sl;
           }
           mbar_arrive_expect_tx(&full[s], 2 * bytes + (c == 0 ? hdr_bytes : 0u));
-          if (np > 0) {
-            bulk_g2s(sk, kbase + (long)c * C::kTpos * DH, bytes, &full[s], pol);
-            bulk_g2s(sk + C::kTileBytes, vbase + (long)c * C::kTpos * DH, bytes, &full[s], pol);
-          }
+          if (np > 0) load_kv_chunk<T, DH>(a, arena, sl, g, c * C::kTpos, np, sk, sk + C::kTileBytes, &full[s], pol);
           if (c == 0) {
             const T* row = fwd + (long)b * ld_fwd;
             const uint32_t gq = (uint32_t)(G * DH * sizeof(T));
@@ -173,7 +168,7 @@ __global__ void __launch_bounds__(GqaCfg<T, DH, G>::kThreads, 1)
     if (wi == 0) {
       // new token: scores of my heads with the new key (group 0 lanes keep the mass); the first
       // warp also appends k / v to the arena
-      T* kdst = arena + (long)slot * a.slot_stride + (long)g * a.head_stride + (long)L * DH;
+      T* kdst = arena + kv_offset(a, slot, g, L, DH);
       T* vdst = kdst + a.kv_stride;
       float vf[C::kEl], kf[C::kEl];
 #pragma unroll
@@ -467,8 +462,8 @@ __global__ void __launch_bounds__(GqaTcCfg<G>::kThreads, 1)
         const int un = u + gridDim.x;
         int Ln = 0, sln = 0;
         if (un < n_units) { Ln = a.pos[un / a.Hkv]; sln = (int)a.slot[un / a.Hkv]; }
-        const int row_k = ((a.layer_local * a.n_slots + sl) * 2 + 0) * a.Hkv + g;
-        const int row_v = row_k + a.Hkv;
+        // tensor-map rows (layer, slot or page, K/V, kv head); paged: one page per stage
+        const int* pt = a.page_table ? a.page_table + (long)sl * a.max_pages : nullptr;
         const int nch = L > 0 ? (L + C::kTpos - 1) / C::kTpos : 1;
         for (int c = 0; c < nch; ++c, ++it) {
           const int s = it % C::kStages;
@@ -482,10 +477,13 @@ __global__ void __launch_bounds__(GqaTcCfg<G>::kThreads, 1)
           const bool any = L > 0;
           mbar_arrive_expect_tx(&full[s], (any ? (uint32_t)C::kKV : 0u) + (c == 0 ? hdr_bytes : 0u));
           if (any) {  // full 64-position boxes (rows past L are masked by the consumers)
-            tma_load_3d(st, &tmKV, 0, c * C::kTpos, row_k, &full[s], pol);
-            tma_load_3d(st + C::kBox, &tmKV, 64, c * C::kTpos, row_k, &full[s], pol);
-            tma_load_3d(st + 2 * C::kBox, &tmKV, 0, c * C::kTpos, row_v, &full[s], pol);
-            tma_load_3d(st + 3 * C::kBox, &tmKV, 64, c * C::kTpos, row_v, &full[s], pol);
+            const int blk = pt ? pt[c] : sl, p0 = pt ? 0 : c * C::kTpos;
+            const int row_k = ((a.layer_local * a.n_slots + blk) * 2 + 0) * a.Hkv + g;
+            const int row_v = row_k + a.Hkv;
+            tma_load_3d(st, &tmKV, 0, p0, row_k, &full[s], pol);
+            tma_load_3d(st + C::kBox, &tmKV, 64, p0, row_k, &full[s], pol);
+            tma_load_3d(st + 2 * C::kBox, &tmKV, 0, p0, row_v, &full[s], pol);
+            tma_load_3d(st + 3 * C::kBox, &tmKV, 64, p0, row_v, &full[s], pol);
           }
           if (c == 0) {
             const bf16_t* row = fwd + (long)b * ld_fwd;
@@ -580,7 +578,7 @@ __global__ void __launch_bounds__(GqaTcCfg<G>::kThreads, 1)
     if (cw == 0) {
       // new token: its key / value from the header; append them to the arena; its state is merged
       // as a ninth partial (m = score, l = 1, o = v) by the last warp
-      bf16_t* kdst = arena + (long)slot * a.slot_stride + (long)g * a.head_stride + (long)L * DH;
+      bf16_t* kdst = arena + kv_offset(a, slot, g, L, DH);
       bf16_t* vdst = kdst + a.kv_stride;
       if (lane < DH / 8) {
         *((uint4*)kdst + lane) = ((const uint4*)hk)[lane];

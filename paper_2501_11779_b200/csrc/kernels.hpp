@@ -105,9 +105,11 @@ RowSegs make_segs(uint64_t seed, int n, const uint64_t* tids, const int* rows, c
 // Generate W (logical [N, K] from `segs`) in W's layout (row-major or tile-contiguous).
 cudaError_t launch_init_weight(const Weight& W, const RowSegs& segs, cudaStream_t st);
 cudaError_t launch_fill_const(int dtype_bytes, void* dst, uint64_t n, float v, cudaStream_t st);
-// Fill positions [0, npos) of K and V blocks of `n_slots` slots for layers [l0, l1).
-cudaError_t launch_fill_kv(int dtype_bytes, void* arena, uint64_t seed, int l0, int l1,
-                           int n_slots, int n_slots_cap, int Hkv, int S, int DH, int npos,
+struct AttnArgs;
+// Fill positions [0, npos) of K and V of slots [0, n_slots) for layers [l0, l1); `lay` holds the
+// arena layout (strides, page table) of one layer, layer_stride the elements per layer.
+cudaError_t launch_fill_kv(int dtype_bytes, void* arena, uint64_t seed, int l0, int l1, int n_slots,
+                           long layer_stride, const AttnArgs& lay, int Hkv, int S, int DH, int npos,
                            cudaStream_t st);
 // Set dynamic shared-memory limits of every kernel instantiation (call before graph capture).
 cudaError_t configure_kernels();

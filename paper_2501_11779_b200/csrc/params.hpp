@@ -80,6 +80,22 @@ struct AttnArgs {
   int layer_local;      // layer index inside the Tier-2's arena (tensor-core GQA path)
   int n_slots;
   const CUtensorMap* kv_tmap;  // host-side: 3-D map of the whole arena (nullptr = no TMA path)
+  // Paged arena (nullptr = contiguous slots): page_table[slot * max_pages + p] is the page holding
+  // positions [64p, 64p + 64) of the slot; slot_stride / kv_stride / head_stride then describe a
+  // page (2 * Hkv * 64 * DH / Hkv * 64 * DH / 64 * DH) and n_slots is the number of pages.
+  const int* page_table;
+  int max_pages;
 };
+// Positions per KV page of the paged arena (one 64-position TMA box / attention stage).
+constexpr int kKvPagePositions = 64;
+
+// Element offset (from the layer base) of position `pos` of (slot, kv head) in either layout.
+__host__ __device__ inline long kv_offset(const AttnArgs& a, int slot, int head, int pos, int DH) {
+  if (a.page_table) {
+    const int pg = a.page_table[(long)slot * a.max_pages + pos / kKvPagePositions];
+    return (long)pg * a.slot_stride + (long)head * a.head_stride + (long)(pos % kKvPagePositions) * DH;
+  }
+  return (long)slot * a.slot_stride + (long)head * a.head_stride + (long)pos * DH;
+}
 
 }  // namespace gh

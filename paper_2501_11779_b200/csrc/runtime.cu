@@ -451,6 +451,8 @@ gh_status gh_tier1_classify(gh_tier1* t, uint32_t B, const void* x, float* logit
 }  // extern "C"
 
 // ================================================================== Tier-2
+static_assert(kKvPagePositions == GH_KV_PAGE_POSITIONS, "page size of the ABI");
+
 struct gh_tier2 {
   Shape sh;
   int device = 0;
@@ -460,14 +462,31 @@ struct gh_tier2 {
   size_t arena_bytes = 0;
   bool has_tmap = false;
   CUtensorMap kv_tmap;  // whole arena, 3-D (tensor-core GQA attention)
-  long slot_stride() const { return 2L * sh.Hkv * sh.S * sh.dh; }
-  long layer_stride() const { return (long)n_slots * slot_stride(); }
+  // paged arena: a pool of n_pages pages of kKvPagePositions positions (all layers of the span use
+  // the same page ids); page_table[slot][p] maps a slot's positions [64p, 64p + 64) to a page
+  bool paged = false;
+  uint32_t n_pages = 0, max_pages = 0;
+  int* d_pt = nullptr;              // device [n_slots][max_pages]
+  std::vector<int> h_pt;            // host mirror
+  std::vector<uint32_t> mapped;     // pages mapped per slot
+  std::vector<int> free_pages;      // LIFO pool
+  long span() const { return paged ? kKvPagePositions : sh.S; }   // positions per block
+  long slot_stride() const { return 2L * sh.Hkv * span() * sh.dh; }  // per slot (contiguous) or page
+  long kv_stride() const { return (long)sh.Hkv * span() * sh.dh; }
+  long head_stride() const { return span() * sh.dh; }
+  long layer_stride() const { return (long)(paged ? n_pages : n_slots) * slot_stride(); }
+  void layout(AttnArgs& a) const {
+    a.slot_stride = slot_stride();
+    a.kv_stride = kv_stride();
+    a.head_stride = head_stride();
+    a.n_slots = (int)(paged ? n_pages : n_slots);
+    a.page_table = paged ? d_pt : nullptr;
+    a.max_pages = (int)max_pages;
+  }
 };
 
-extern "C" {
-
-gh_status gh_tier2_create(const gh_model_spec* spec, int device, uint32_t layer_begin,
-                          uint32_t layer_end, uint32_t n_slots, gh_tier2** out) {
+static gh_status tier2_create(const gh_model_spec* spec, int device, uint32_t layer_begin, uint32_t layer_end,
+                              uint32_t n_slots, uint32_t n_pages, gh_tier2** out) {
   if (!out) return fail(GH_EINVAL, "out is null");
   *out = nullptr;
   Shape sh;
@@ -479,6 +498,9 @@ gh_status gh_tier2_create(const gh_model_spec* spec, int device, uint32_t layer_
   GH_CUDA(configure_kernels());
   auto t = std::make_unique<gh_tier2>();
   t->sh = sh; t->device = device; t->l0 = layer_begin; t->l1 = layer_end; t->n_slots = n_slots;
+  t->paged = n_pages > 0;
+  t->n_pages = n_pages;
+  t->max_pages = (uint32_t)((sh.S + kKvPagePositions - 1) / kKvPagePositions);
   t->arena_bytes = (size_t)(layer_end - layer_begin) * (size_t)t->layer_stride() * sh.db;
   size_t free_b = 0, total_b = 0;
   GH_CUDA(cudaMemGetInfo(&free_b, &total_b));
@@ -489,13 +511,75 @@ gh_status gh_tier2_create(const gh_model_spec* spec, int device, uint32_t layer_
   // zeroed once: never-written positions are finite (tile loads past a prompt's length are masked,
   // and 0 x NaN would not be)
   GH_CUDA(cudaMemset(t->arena, 0, t->arena_bytes));
+  if (t->paged) {
+    void* p;
+    const size_t n = (size_t)n_slots * t->max_pages;
+    GH_TRY(dev_alloc(t->mem, n * sizeof(int), &p));
+    t->d_pt = (int*)p;
+    t->h_pt.assign(n, 0);  // unmapped entries point at page 0 (a valid address; never attended)
+    GH_CUDA(cudaMemcpy(t->d_pt, t->h_pt.data(), n * sizeof(int), cudaMemcpyHostToDevice));
+    t->mapped.assign(n_slots, 0);
+    for (uint32_t i = 0; i < n_pages; ++i) t->free_pages.push_back((int)(n_pages - 1 - i));
+  }
   if (sh.db == 2 && sh.dh == 128) {
-    const uint64_t rows = (uint64_t)(layer_end - layer_begin) * n_slots * 2 * sh.Hkv;
-    t->has_tmap = make_tmap_kv(&t->kv_tmap, t->arena, rows, (uint64_t)sh.S, 128) == cudaSuccess;
+    const uint64_t rows = (uint64_t)(layer_end - layer_begin) * (t->paged ? n_pages : n_slots) * 2 * sh.Hkv;
+    t->has_tmap = make_tmap_kv(&t->kv_tmap, t->arena, rows, (uint64_t)t->span(), 128) == cudaSuccess;
   }
   *out = t.release();
   return GH_OK;
 }
+
+extern "C" {
+
+gh_status gh_tier2_create(const gh_model_spec* spec, int device, uint32_t layer_begin,
+                          uint32_t layer_end, uint32_t n_slots, gh_tier2** out) {
+  return tier2_create(spec, device, layer_begin, layer_end, n_slots, 0, out);
+}
+
+gh_status gh_tier2_create_paged(const gh_model_spec* spec, int device, uint32_t layer_begin, uint32_t layer_end,
+                                uint32_t n_slots, uint32_t n_pages, gh_tier2** out) {
+  if (n_pages == 0) return fail(GH_EINVAL, "n_pages must be >= 1");
+  return tier2_create(spec, device, layer_begin, layer_end, n_slots, n_pages, out);
+}
+
+gh_status gh_tier2_map(gh_tier2* t, uint32_t slot, uint32_t n_positions, void* stream) {
+  if (!t) return fail(GH_EINVAL, "null argument");
+  if (slot >= t->n_slots) return fail(GH_EINVAL, "slot " + std::to_string(slot) + " >= n_slots");
+  if (n_positions > (uint32_t)t->sh.S)
+    return fail(GH_EINFEASIBLE, std::to_string(n_positions) + " positions exceed max_seq_len");
+  if (!t->paged) return GH_OK;  // contiguous slots hold max_seq_len positions
+  const uint32_t need = (n_positions + kKvPagePositions - 1) / kKvPagePositions;
+  const uint32_t have = t->mapped[slot];
+  if (need <= have) return GH_OK;
+  if (need - have > t->free_pages.size())
+    return fail(GH_EINFEASIBLE, "KV page pool exhausted: " + std::to_string(need - have) + " pages needed, " +
+                                    std::to_string(t->free_pages.size()) + " free (binding constraint: memory)");
+  GH_CUDA(cudaSetDevice(t->device));
+  cudaStream_t st = (cudaStream_t)stream;
+  GH_CUDA(cudaStreamSynchronize(st));  // steps already queued on `stream` see the old table
+  int* row = t->h_pt.data() + (size_t)slot * t->max_pages;
+  for (uint32_t p = have; p < need; ++p) {
+    row[p] = t->free_pages.back();
+    t->free_pages.pop_back();
+  }
+  t->mapped[slot] = need;
+  GH_CUDA(cudaMemcpyAsync(t->d_pt + (size_t)slot * t->max_pages + have, row + have, (size_t)(need - have) * sizeof(int),
+                          cudaMemcpyHostToDevice, st));
+  GH_CUDA(cudaStreamSynchronize(st));
+  return GH_OK;
+}
+
+gh_status gh_tier2_unmap(gh_tier2* t, uint32_t slot) {
+  if (!t) return fail(GH_EINVAL, "null argument");
+  if (slot >= t->n_slots) return fail(GH_EINVAL, "slot " + std::to_string(slot) + " >= n_slots");
+  if (!t->paged) return GH_OK;
+  int* row = t->h_pt.data() + (size_t)slot * t->max_pages;
+  for (uint32_t p = t->mapped[slot]; p-- > 0;) t->free_pages.push_back(row[p]);
+  t->mapped[slot] = 0;
+  return GH_OK;
+}
+
+uint32_t gh_tier2_pages_free(const gh_tier2* t) { return t && t->paged ? (uint32_t)t->free_pages.size() : 0; }
 
 gh_status gh_tier2_destroy(gh_tier2* t) {
   if (t) { cudaSetDevice(t->device); cudaDeviceSynchronize(); delete t; }
@@ -512,6 +596,9 @@ gh_status gh_tier2_check(const gh_tier2* t, uint32_t B, const uint32_t* slot, co
                                       " (binding constraint: memory)");
     if (pos[b] < 0 || pos[b] >= t->sh.S)
       return fail(GH_EINFEASIBLE, "position " + std::to_string(pos[b]) + " outside [0, max_seq_len)");
+    if (t->paged && (uint32_t)pos[b] / kKvPagePositions >= t->mapped[slot[b]])
+      return fail(GH_EINFEASIBLE, "position " + std::to_string(pos[b]) + " of slot " + std::to_string(slot[b]) +
+                                      " is not mapped to a KV page (gh_tier2_map)");
   }
   return GH_OK;
 }
@@ -536,9 +623,7 @@ static gh_status t2_attend(gh_tier2* t, uint32_t layer, uint32_t B, const uint32
   a.arena = (char*)t->arena + (size_t)(layer - t->l0) * t->layer_stride() * s.db;
   a.slot = slot;
   a.pos = pos;
-  a.slot_stride = t->slot_stride();
-  a.kv_stride = (long)s.Hkv * s.S * s.dh;
-  a.head_stride = (long)s.S * s.dh;
+  t->layout(a);
   a.B = (int)B; a.H = s.H; a.Hkv = s.Hkv; a.D = s.D; a.Dkv = s.Dkv;
   a.scale_log2 = (float)(1.4426950408889634 / std::sqrt((double)s.dh));
   static const int attn_flags = getenv("GH_ATTN_FLAGS") ? atoi(getenv("GH_ATTN_FLAGS")) : 0;  // diagnostics
@@ -546,7 +631,6 @@ static gh_status t2_attend(gh_tier2* t, uint32_t layer, uint32_t B, const uint32
   a.pf = pf;
   a.pf_bytes = pf ? pf_bytes : 0;
   a.layer_local = (int)(layer - t->l0);
-  a.n_slots = (int)t->n_slots;
   a.kv_tmap = t->has_tmap ? &t->kv_tmap : nullptr;
   GH_CUDA(launch_attention(s.db, s.dh, a, (cudaStream_t)stream));
   return GH_OK;
@@ -557,7 +641,13 @@ extern "C" {
 gh_status gh_tier2_fill_synthetic(gh_tier2* t, uint64_t seed, uint32_t n_fill, uint32_t npos, void* stream) {
   if (!t) return fail(GH_EINVAL, "null argument");
   if (n_fill > t->n_slots || npos > (uint32_t)t->sh.S) return fail(GH_EINVAL, "fill exceeds arena");
-  GH_CUDA(launch_fill_kv(t->sh.db, t->arena, seed, (int)t->l0, (int)t->l1, (int)n_fill, (int)t->n_slots,
+  if (t->paged)
+    for (uint32_t i = 0; i < n_fill; ++i)
+      if (t->mapped[i] * (uint32_t)kKvPagePositions < npos)
+        return fail(GH_EINVAL, "fill: positions of slot " + std::to_string(i) + " are not mapped (gh_tier2_map)");
+  AttnArgs lay{};
+  t->layout(lay);
+  GH_CUDA(launch_fill_kv(t->sh.db, t->arena, seed, (int)t->l0, (int)t->l1, (int)n_fill, t->layer_stride(), lay,
                          t->sh.Hkv, t->sh.S, t->sh.dh, (int)npos, (cudaStream_t)stream));
   return GH_OK;
 }
@@ -568,10 +658,22 @@ gh_status gh_tier2_read_kv(gh_tier2* t, uint32_t layer, uint32_t slot, uint32_t 
   if (layer < t->l0 || layer >= t->l1 || slot >= t->n_slots || kv > 1 || head >= (uint32_t)t->sh.Hkv ||
       n > (uint32_t)t->sh.S)
     return fail(GH_EINVAL, "read_kv out of range");
+  if (t->paged && t->mapped[slot] * (uint32_t)kKvPagePositions < n)
+    return fail(GH_EINVAL, "read_kv: positions are not mapped");
   const Shape& s = t->sh;
-  const size_t off = (size_t)(layer - t->l0) * t->layer_stride() + (size_t)slot * t->slot_stride() +
-                     (size_t)kv * s.Hkv * s.S * s.dh + (size_t)head * s.S * s.dh;
-  GH_CUDA(cudaMemcpy(host_out, (char*)t->arena + off * s.db, (size_t)n * s.dh * s.db, cudaMemcpyDeviceToHost));
+  GH_CUDA(cudaSetDevice(t->device));
+  GH_CUDA(cudaDeviceSynchronize());
+  AttnArgs lay{};
+  t->layout(lay);
+  lay.page_table = t->paged ? t->h_pt.data() : nullptr;  // host mirror for the offsets
+  const size_t lbase = (size_t)(layer - t->l0) * t->layer_stride();
+  for (uint32_t q = 0; q < n;) {  // contiguous runs (one page at most when paged)
+    const uint32_t m = t->paged ? std::min<uint32_t>(n - q, kKvPagePositions - q % kKvPagePositions) : n - q;
+    const size_t off = lbase + kv_offset(lay, (int)slot, (int)head, (int)q, s.dh) + (size_t)kv * t->kv_stride();
+    GH_CUDA(cudaMemcpy((char*)host_out + (size_t)q * s.dh * s.db, (char*)t->arena + off * s.db,
+                       (size_t)m * s.dh * s.db, cudaMemcpyDeviceToHost));
+    q += m;
+  }
   return GH_OK;
 }
 
@@ -828,7 +930,7 @@ gh_status gh_engine_create(const gh_engine_config* cfg, gh_comm* comm, gh_engine
     uint32_t need = (uint32_t)R * cfg->inflight;
     uint32_t n_slots = cfg->n_slots ? cfg->n_slots : need;
     if (n_slots < need) return fail(GH_EINFEASIBLE, "n_slots smaller than batch * inflight (binding constraint: memory)");
-    GH_TRY(gh_tier2_create(&cfg->spec, cfg->device, (uint32_t)e->l0, (uint32_t)e->l1, n_slots, &e->t2));
+    GH_TRY(tier2_create(&cfg->spec, cfg->device, (uint32_t)e->l0, (uint32_t)e->l1, n_slots, cfg->kv_pages, &e->t2));
   }
   GH_CUDA(cudaEventCreateWithFlags(&e->fork, cudaEventDisableTiming));
   e->batches.resize(cfg->inflight);
@@ -899,6 +1001,18 @@ gh_status gh_engine_advance(gh_engine* e, uint32_t ib, int inc, void* stream) {
   return GH_OK;
 }
 gh_tier2* gh_engine_tier2(gh_engine* e) { return e ? e->t2 : nullptr; }
+
+gh_status gh_engine_kv_map(gh_engine* e, uint32_t slot, uint32_t n_positions) {
+  if (!e) return fail(GH_EINVAL, "null engine");
+  if (!e->t2) return fail(GH_EUNSUPPORTED, "this rank holds no KV (Tier-1 role)");
+  return gh_tier2_map(e->t2, slot, n_positions, nullptr);
+}
+
+gh_status gh_engine_kv_unmap(gh_engine* e, uint32_t slot) {
+  if (!e) return fail(GH_EINVAL, "null engine");
+  if (!e->t2) return fail(GH_EUNSUPPORTED, "this rank holds no KV (Tier-1 role)");
+  return gh_tier2_unmap(e->t2, slot);
+}
 
 gh_status gh_engine_io(gh_engine* e, uint32_t ib, int32_t** tok, int32_t** pos, uint32_t** slot, int32_t** next) {
   if (!e || ib >= e->batches.size()) return fail(GH_EINVAL, "bad engine / batch index");
@@ -1416,6 +1530,11 @@ gh_status gh_engine_step_host(gh_engine* e, uint32_t ib, const int32_t* tok_host
   const int R = e->rows();
   if (e->role != 2) {
     if (!tok_host || !pos_host || !next_host) return fail(GH_EINVAL, "host token/pos/next buffers required");
+    if (e->role == 0 && e->t2->paged) {  // paged KV: every attended position must be mapped
+      std::vector<uint32_t> sl(R);
+      for (int i = 0; i < R; ++i) sl[i] = ib * R + i;
+      GH_TRY(gh_tier2_check(e->t2, (uint32_t)R, sl.data(), pos_host));
+    }
     GH_CUDA(cudaMemcpyAsync(b.tok, tok_host, (size_t)R * 4, cudaMemcpyHostToDevice, st));
     GH_CUDA(cudaMemcpyAsync(b.pos, pos_host, (size_t)R * 4, cudaMemcpyHostToDevice, st));
   }

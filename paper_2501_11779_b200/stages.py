@@ -65,17 +65,36 @@ class Tier1:
 
 
 class Tier2:
-    """KV-context stage: n_slots prompt slots for layers [layer_begin, layer_end)."""
+    """KV-context stage: n_slots prompt slots for layers [layer_begin, layer_end).  With
+    n_pages > 0 the arena is a pool of n_pages pages of PAGE_POSITIONS positions shared by the
+    slots (map() before a step attends a position, unmap() returns the pages)."""
+
+    PAGE_POSITIONS = 64  # GH_KV_PAGE_POSITIONS
 
     def __init__(self, spec: ModelSpec, n_slots: int, device: int = 0, layer_begin: int = 0,
-                 layer_end: int | None = None):
+                 layer_end: int | None = None, n_pages: int = 0):
         self.spec = spec
         self.n_slots = n_slots
+        self.n_pages = n_pages
         self.layer_begin, self.layer_end = layer_begin, spec.n_layers if layer_end is None else layer_end
         h = C.c_void_p()
-        L.check(L.lib().gh_tier2_create(C.byref(spec.c()), device, self.layer_begin, self.layer_end,
-                                        n_slots, C.byref(h)))
+        if n_pages:
+            L.check(L.lib().gh_tier2_create_paged(C.byref(spec.c()), device, self.layer_begin, self.layer_end,
+                                                  n_slots, n_pages, C.byref(h)))
+        else:
+            L.check(L.lib().gh_tier2_create(C.byref(spec.c()), device, self.layer_begin, self.layer_end,
+                                            n_slots, C.byref(h)))
         self.h = h
+
+    def map(self, slot: int, n_positions: int, stream=None):
+        L.check(L.lib().gh_tier2_map(self.h, slot, n_positions, _stream(stream)))
+
+    def unmap(self, slot: int):
+        L.check(L.lib().gh_tier2_unmap(self.h, slot))
+
+    @property
+    def pages_free(self) -> int:
+        return L.lib().gh_tier2_pages_free(self.h)
 
     def close(self):
         if getattr(self, "h", None) and L is not None and L.lib is not None:
@@ -153,10 +172,12 @@ class Engine:
 
     def __init__(self, spec: ModelSpec, batch: int, inflight: int = 1, device: int = 0,
                  weight_seed: int = 1234, n_slots: int = 0, use_graph: bool = True,
-                 comm: Comm | None = None, transport: str = "auto", tier1_ranks: int = 1):
+                 comm: Comm | None = None, transport: str = "auto", tier1_ranks: int = 1,
+                 kv_pages: int = 0):
         self.spec, self.batch, self.inflight = spec, batch, inflight
+        self.kv_pages = kv_pages
         cfg = L.GhEngineConfig(spec.c(), device, weight_seed, batch, inflight, n_slots, int(use_graph),
-                               self.TRANSPORTS[transport], tier1_ranks)
+                               self.TRANSPORTS[transport], tier1_ranks, kv_pages)
         h = C.c_void_p()
         L.check(L.lib().gh_engine_create(C.byref(cfg), comm.h if comm else None, C.byref(h)))
         self.h = h
@@ -180,6 +201,13 @@ class Engine:
     @property
     def tier2(self) -> int:
         return L.lib().gh_engine_tier2(self.h)
+
+    def kv_map(self, slot: int, n_positions: int):
+        """Paged KV: back positions [0, n_positions) of a slot with pages (no-op when contiguous)."""
+        L.check(L.lib().gh_engine_kv_map(self.h, slot, n_positions))
+
+    def kv_unmap(self, slot: int):
+        L.check(L.lib().gh_engine_kv_unmap(self.h, slot))
 
     def step_host(self, tok: np.ndarray | None, pos: np.ndarray | None, want_logits=False, ib=0,
                   stream=None):
@@ -258,7 +286,11 @@ class ContinuousDispatcher:
     handed to the next queued request at position 0.  Every step decodes all busy lanes at their
     own positions (ragged contexts); idle lanes decode a dummy token at position 0 and are
     ignored.  Reusing a slot needs no clearing: attention reads only the positions below the
-    request's current one, all of which it wrote itself."""
+    request's current one, all of which it wrote itself.
+
+    With a paged KV arena (Engine(kv_pages=...)) a request maps exactly the positions it will
+    attend (prompt + max_new - 1) when it is admitted and returns its pages when it finishes; a
+    request waits in the queue (its lane idles on one page) until the pool can back it."""
 
     def __init__(self, engine: Engine):
         self.engine = engine
@@ -275,14 +307,22 @@ class ContinuousDispatcher:
         pos = np.zeros(B, np.int32)
 
         def admit(lane):
-            if queue:
-                r = queue.pop(0)
-                lane_req[lane], lane_t[lane] = r, 0
-                tok[lane] = int(requests[r][0])
-            else:
-                lane_req[lane] = -1
-                tok[lane] = 0
+            self.engine.kv_unmap(lane)
+            lane_req[lane] = -1
+            tok[lane] = 0
             pos[lane] = 0
+            if queue:
+                r = queue[0]
+                try:
+                    self.engine.kv_map(lane, len(requests[r]) + max_new - 1)
+                except L.FeasibilityError:  # page pool short: the request waits
+                    pass
+                else:
+                    queue.pop(0)
+                    lane_req[lane], lane_t[lane] = r, 0
+                    tok[lane] = int(requests[r][0])
+            if lane_req[lane] < 0:
+                self.engine.kv_map(lane, 1)  # the idle lane's dummy token
 
         for lane in range(B):
             admit(lane)
@@ -293,6 +333,8 @@ class ContinuousDispatcher:
             for lane in range(B):
                 r = lane_req[lane]
                 if r < 0:
+                    if queue:
+                        admit(lane)   # retry: pages may have been returned by now
                     continue
                 t = lane_t[lane]
                 plen = len(requests[r])
@@ -305,4 +347,11 @@ class ContinuousDispatcher:
                 pos[lane] = t + 1
                 if len(out[r]) == max_new:
                     admit(lane)       # the lane's slot goes to the next request
+            if queue and all(r < 0 for r in lane_req):
+                for lane in range(B):  # every lane idle: offer the whole pool
+                    self.engine.kv_unmap(lane)
+                for lane in range(B):
+                    admit(lane)
+        if queue:
+            raise L.FeasibilityError(L.GH_EINFEASIBLE, f"request {queue[0]} needs more KV pages than the pool holds")
         return [np.array(o, np.int32) for o in out], steps

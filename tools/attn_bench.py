@@ -1,4 +1,7 @@
-"""Time the Tier-2 attention kernel alone (CUDA events, KV >> L2) at a batch / context."""
+"""Time the Tier-2 attention kernel alone (CUDA events, KV >> L2) at a batch / context.
+
+  python tools/attn_bench.py [B] [ctx] [7b|13b|70b] [paged]   (paged: shuffled 64-position pages)
+"""
 import sys
 from pathlib import Path
 
@@ -14,7 +17,13 @@ layers = 4  # rotate layers so the KV of one launch is never L2-resident from th
 model = sys.argv[3] if len(sys.argv) > 3 else "7b"
 base = {"7b": gh.LLAMA2_7B, "13b": gh.CONFIGS["C4"]["spec"], "70b": gh.CONFIGS["C5"]["spec"]}[model]
 spec = base.with_(n_layers=layers, max_seq_len=ctx)
-t2 = Tier2(spec, n_slots=B)
+paged = len(sys.argv) > 4 and sys.argv[4] == "paged"
+per = -(-ctx // 64)
+t2 = Tier2(spec, n_slots=B, n_pages=B * per if paged else 0)
+if paged:  # round-robin mapping: consecutive pages of a slot are B pages apart
+    for r in range(per):
+        for s in range(B):
+            t2.map(s, min((r + 1) * 64, ctx))
 t2.fill_synthetic(99, B, ctx - 1)
 x, fwd, bwd = message_buffers(spec, B)
 fwd.normal_()
@@ -31,5 +40,5 @@ e1.record()
 torch.cuda.synchronize()
 us = e0.elapsed_time(e1) * 1e3 / reps
 byts = 2 * (2 * spec.d_kv * B * ctx + 2 * B * spec.d_kv + 2 * B * spec.d_model)
-print(f"{model} B={B} ctx={ctx}: {us:.1f} us  {byts / us / 1e3:.0f} GB/s")
+print(f"{model}{' paged' if paged else ''} B={B} ctx={ctx}: {us:.1f} us  {byts / us / 1e3:.0f} GB/s")
 t2.close()
