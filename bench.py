@@ -68,7 +68,7 @@ class Clocks:
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
-                 "-lms", "20"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+                 "-lms", os.environ.get("GH_CLOCKS_MS", "20")], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.thread = threading.Thread(target=self._reader, daemon=True)
             self.thread.start()
             deadline = time.perf_counter() + 10
@@ -386,6 +386,8 @@ def run_split(args, wl, rank, world):
             if eng.role == "tier1":
                 for ib in range(IF):
                     eng.advance(ib, 0, stream=stream)
+            if os.environ.get("GH_BENCH_STEP_SYNC"):  # diagnostics: drain the pipeline every step
+                stream.synchronize()
         e1.record(stream)
         torch.cuda.synchronize()
         dist.barrier()
@@ -416,6 +418,8 @@ def run_split(args, wl, rank, world):
         elif r is not None:
             toks = r
     e2e_ms = torch.tensor([(time.perf_counter() - t0) * 1e3 / nsteps], dtype=torch.float64)
+    print(f"rank {rank} ({eng.role}): device {ms_local:.3f} ms/step, e2e {float(e2e_ms.item()):.3f} ms/step",
+          file=sys.stderr)
     dist.all_reduce(e2e_ms, op=dist.ReduceOp.MAX)
     eng.close()
     comm.close()
