@@ -154,8 +154,9 @@ gh_status gh_tier2_attend(gh_tier2* t2, uint32_t layer, uint32_t B, const uint32
 /* Host-side admission check of a batch (slot < n_slots, 0 <= pos < S). */
 gh_status gh_tier2_check(const gh_tier2* t2, uint32_t B, const uint32_t* slot_host,
                          const int32_t* pos_host);
-/* Fill positions [0, n_positions) of the given slots (all layers) with synthetic N(0,1)-like
- * values from `seed` (benchmark pre-fill; content does not change the cost). */
+/* Fill positions [0, n_positions) of slots [0, n_slots_to_fill) (all layers) with synthetic
+ * N(0,1)-like values from `seed` (benchmark pre-fill; content does not change the cost).  Paged
+ * arena: each slot is filled up to min(n_positions, its mapped positions). */
 gh_status gh_tier2_fill_synthetic(gh_tier2* t2, uint64_t seed, uint32_t n_slots_to_fill,
                                   uint32_t n_positions, void* stream);
 /* Paged KV arena (the page-granular form of the slot arena): n_slots logical slots

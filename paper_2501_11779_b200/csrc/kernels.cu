@@ -89,7 +89,7 @@ __global__ void fill_const_kernel(T* dst, uint64_t n, float v) {
 // slots or pages, kv_offset) and the value depends only on the logical (layer, slot, kv, h, p, d).
 template <typename T>
 __global__ void fill_kv_kernel(T* arena, uint64_t seed, int l0, int n_layers, int n_slots, long layer_stride,
-                               const AttnArgs lay, int Hkv, int S, int DH, int npos, float k) {
+                               const AttnArgs lay, const int* limit, int Hkv, int S, int DH, int npos, float k) {
   const uint64_t per_block = (uint64_t)Hkv * npos * DH;  // one (layer, slot, kv)
   const uint64_t total = (uint64_t)n_layers * n_slots * 2 * per_block;
   for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < total;
@@ -101,6 +101,7 @@ __global__ void fill_kv_kernel(T* arena, uint64_t seed, int l0, int n_layers, in
     const int h = (int)(r / ((uint64_t)npos * DH));
     const int p = (int)((r / DH) % npos);
     const int d = (int)(r % DH);
+    if (limit && p >= limit[slot]) continue;  // paged: positions past the slot's mapping
     const uint64_t base = tensor_base(seed, tid_kv((uint64_t)(l0 + l), (uint64_t)slot, (uint64_t)kv));
     const uint64_t logical = ((uint64_t)h * S + p) * DH + d;
     const uint64_t phys = (uint64_t)l * layer_stride + kv_offset(lay, slot, h, p, DH) + kv * lay.kv_stride + d;
@@ -144,16 +145,16 @@ cudaError_t launch_fill_const(int db, void* dst, uint64_t n, float v, cudaStream
 }
 
 cudaError_t launch_fill_kv(int db, void* arena, uint64_t seed, int l0, int l1, int n_slots, long layer_stride,
-                           const AttnArgs& lay, int Hkv, int S, int DH, int npos, cudaStream_t st) {
+                           const AttnArgs& lay, const int* limit, int Hkv, int S, int DH, int npos, cudaStream_t st) {
   if (npos <= 0 || n_slots <= 0 || l1 <= l0) return cudaSuccess;
   const uint64_t total = (uint64_t)(l1 - l0) * n_slots * 2 * Hkv * npos * DH;
   GH_COUNT_LAUNCH();
   if (db == 4)
     fill_kv_kernel<float><<<grid_for(total), 256, 0, st>>>((float*)arena, seed, l0, l1 - l0, n_slots, layer_stride,
-                                                           lay, Hkv, S, DH, npos, ih_k(1.0));
+                                                           lay, limit, Hkv, S, DH, npos, ih_k(1.0));
   else
     fill_kv_kernel<bf16_t><<<grid_for(total), 256, 0, st>>>((bf16_t*)arena, seed, l0, l1 - l0, n_slots,
-                                                            layer_stride, lay, Hkv, S, DH, npos, ih_k(1.0));
+                                                            layer_stride, lay, limit, Hkv, S, DH, npos, ih_k(1.0));
   return cudaGetLastError();
 }
 

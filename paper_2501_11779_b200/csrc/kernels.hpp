@@ -107,10 +107,11 @@ cudaError_t launch_init_weight(const Weight& W, const RowSegs& segs, cudaStream_
 cudaError_t launch_fill_const(int dtype_bytes, void* dst, uint64_t n, float v, cudaStream_t st);
 struct AttnArgs;
 // Fill positions [0, npos) of K and V of slots [0, n_slots) for layers [l0, l1); `lay` holds the
-// arena layout (strides, page table) of one layer, layer_stride the elements per layer.
+// arena layout (strides, page table) of one layer, layer_stride the elements per layer; `limit`
+// (device [n_slots], may be null) caps each slot's filled positions.
 cudaError_t launch_fill_kv(int dtype_bytes, void* arena, uint64_t seed, int l0, int l1, int n_slots,
-                           long layer_stride, const AttnArgs& lay, int Hkv, int S, int DH, int npos,
-                           cudaStream_t st);
+                           long layer_stride, const AttnArgs& lay, const int* limit, int Hkv, int S, int DH,
+                           int npos, cudaStream_t st);
 // Set dynamic shared-memory limits of every kernel instantiation (call before graph capture).
 cudaError_t configure_kernels();
 

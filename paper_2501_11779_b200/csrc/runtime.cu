@@ -467,6 +467,7 @@ struct gh_tier2 {
   bool paged = false;
   uint32_t n_pages = 0, max_pages = 0;
   int* d_pt = nullptr;              // device [n_slots][max_pages]
+  int* d_limit = nullptr;           // device [n_slots] (synthetic fill of ragged contexts)
   std::vector<int> h_pt;            // host mirror
   std::vector<uint32_t> mapped;     // pages mapped per slot
   std::vector<int> free_pages;      // LIFO pool
@@ -516,6 +517,8 @@ static gh_status tier2_create(const gh_model_spec* spec, int device, uint32_t la
     const size_t n = (size_t)n_slots * t->max_pages;
     GH_TRY(dev_alloc(t->mem, n * sizeof(int), &p));
     t->d_pt = (int*)p;
+    GH_TRY(dev_alloc(t->mem, (size_t)n_slots * sizeof(int), &p));
+    t->d_limit = (int*)p;
     t->h_pt.assign(n, 0);  // unmapped entries point at page 0 (a valid address; never attended)
     GH_CUDA(cudaMemcpy(t->d_pt, t->h_pt.data(), n * sizeof(int), cudaMemcpyHostToDevice));
     t->mapped.assign(n_slots, 0);
@@ -641,14 +644,24 @@ extern "C" {
 gh_status gh_tier2_fill_synthetic(gh_tier2* t, uint64_t seed, uint32_t n_fill, uint32_t npos, void* stream) {
   if (!t) return fail(GH_EINVAL, "null argument");
   if (n_fill > t->n_slots || npos > (uint32_t)t->sh.S) return fail(GH_EINVAL, "fill exceeds arena");
-  if (t->paged)
-    for (uint32_t i = 0; i < n_fill; ++i)
-      if (t->mapped[i] * (uint32_t)kKvPagePositions < npos)
-        return fail(GH_EINVAL, "fill: positions of slot " + std::to_string(i) + " are not mapped (gh_tier2_map)");
+  const int* limit = nullptr;
+  if (t->paged) {  // each slot is filled up to its mapping (ragged contexts), at least one page
+    std::vector<int> lim(n_fill);
+    for (uint32_t i = 0; i < n_fill; ++i) {
+      if (t->mapped[i] == 0)
+        return fail(GH_EINVAL, "fill: slot " + std::to_string(i) + " has no KV pages (gh_tier2_map)");
+      lim[i] = (int)std::min<uint32_t>(npos, t->mapped[i] * (uint32_t)kKvPagePositions);
+    }
+    if (n_fill) {
+      GH_CUDA(cudaStreamSynchronize((cudaStream_t)stream));
+      GH_CUDA(cudaMemcpy(t->d_limit, lim.data(), n_fill * sizeof(int), cudaMemcpyHostToDevice));
+    }
+    limit = t->d_limit;
+  }
   AttnArgs lay{};
   t->layout(lay);
   GH_CUDA(launch_fill_kv(t->sh.db, t->arena, seed, (int)t->l0, (int)t->l1, (int)n_fill, t->layer_stride(), lay,
-                         t->sh.Hkv, t->sh.S, t->sh.dh, (int)npos, (cudaStream_t)stream));
+                         limit, t->sh.Hkv, t->sh.S, t->sh.dh, (int)npos, (cudaStream_t)stream));
   return GH_OK;
 }
 

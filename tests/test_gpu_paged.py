@@ -101,7 +101,7 @@ def test_paged_map_errors(need_gpu):
     with pytest.raises(L.FeasibilityError):       # slot 1 has no pages
         t2.check(np.array([1], np.uint32), np.array([0], np.int32))
     t2.check(np.array([0], np.uint32), np.array([191], np.int32))
-    with pytest.raises(L.ValidationError):        # fill needs mapped positions
+    with pytest.raises(L.ValidationError):        # fill needs every slot backed by a page
         t2.fill_synthetic(1, 2, 10)
     t2.unmap(0)
     assert t2.pages_free == 5
@@ -139,3 +139,24 @@ def test_paged_engine_continuous_batching(need_gpu):
     with pytest.raises(L.FeasibilityError):
         ContinuousDispatcher(eng).run([reqs[4]], max_new)
     eng.close()
+
+
+def test_paged_ragged_fill(need_gpu):
+    """The synthetic fill of a paged arena stops at each slot's mapping and writes the same logical
+    values as the contiguous fill."""
+    from paper_2501_11779_b200.stages import Tier2
+    spec = SPECS["small-bf16"]
+    S = spec.max_seq_len
+    lens = [1, 64, 65, 200, S]
+    contig = Tier2(spec, n_slots=len(lens))
+    paged = Tier2(spec, n_slots=len(lens), n_pages=sum(-(-n // PAGE) for n in lens))
+    for s, n in enumerate(lens):
+        paged.map(s, n)
+    assert paged.pages_free == 0
+    contig.fill_synthetic(4, len(lens), S)
+    paged.fill_synthetic(4, len(lens), S)
+    for s, n in enumerate(lens):
+        for kv in (0, 1):
+            assert np.array_equal(contig.read_kv(1, s, kv, 2, n), paged.read_kv(1, s, kv, 2, n))
+    contig.close()
+    paged.close()
