@@ -36,6 +36,20 @@ GH_DEV void load_kv_chunk(const AttnArgs& a, const T* arena, int sl, int g, int 
   }
 }
 
+// Persistent unit schedule: a CTA's first unit is blockIdx.x; later ones come from the launch's
+// work counter (ragged contexts balance across CTAs) or, without one, stride gridDim.x.
+GH_DEV int next_unit(const AttnArgs& a, int u) {
+  return a.work ? (int)atomicAdd(a.work, 1u) + (int)gridDim.x : u + (int)gridDim.x;
+}
+// Producer after its last fetch: the last CTA to get here resets the counter for the next launch
+// (no CTA fetches any more once every producer has counted itself out).
+GH_DEV void units_done(const AttnArgs& a) {
+  if (a.work && atomicAdd(a.work + 1, 1u) == gridDim.x - 1) {
+    atomicExch(a.work, 0u);
+    atomicExch(a.work + 1, 0u);
+  }
+}
+
 template <typename T, int DH, int W = 8>
 struct AttnCfg {
   static constexpr int kVec = 16 / sizeof(T);          // elements per 16-byte chunk
@@ -133,10 +147,10 @@ __global__ void __launch_bounds__(AttnCfg<T, DH, W>::kThreads, 1)
       int u = blockIdx.x;
       int L = 0, sl = 0;
       if (u < n_units) { L = a.pos[u / a.H]; sl = (int)a.slot[u / a.H]; }
-      for (; u < n_units; u += gridDim.x) {
+      while (u < n_units) {
         const int b = u / a.H, h = u % a.H, kvh = h / group;
         // next unit's position / slot, one unit ahead (hides the dependent global loads)
-        const int un = u + gridDim.x;
+        const int un = next_unit(a, u);
         int Ln = 0, sln = 0;
         if (un < n_units) { Ln = a.pos[un / a.H]; sln = (int)a.slot[un / a.H]; }
         const int nch = L > 0 ? (L + C::kTpos - 1) / C::kTpos : 1;
@@ -161,8 +175,16 @@ __global__ void __launch_bounds__(AttnCfg<T, DH, W>::kThreads, 1)
             bulk_g2s(hdr + 3 * DH * sizeof(T), row + (long)h * DH, DH * sizeof(T), &full[s], pol);
           }
         }
+        u = un;
         L = Ln;
         sl = sln;
+      }
+      units_done(a);
+      {  // end of this CTA's units: a header-only stage with L = -1
+        const int s = it % C::kStages;
+        mbar_wait(&empty[s], ((it / C::kStages) & 1) ^ 1);
+        *(int*)(smem + s * C::kStageBytes + 2 * C::kTileBytes + 4 * DH * sizeof(T)) = -1;
+        mbar_arrive(&full[s]);
       }
       prefetch_l2_share(a.pf, a.pf_bytes, blockIdx.x, gridDim.x);
     }
@@ -174,13 +196,13 @@ __global__ void __launch_bounds__(AttnCfg<T, DH, W>::kThreads, 1)
     // partial states of each unit (in unit order) and writes the output row, so that no consumer
     // warp falls behind the stage ring while merging
     if (a.flags & 3) return;
-    int ui = 0;
-    for (int u = blockIdx.x; u < n_units; u += gridDim.x, ++ui) {
+    for (int ui = 0;; ++ui) {
       const int cb = ui % C::kNB;
       while (*(volatile int*)&comb_cnt[cb] < C::kW) { }
       __threadfence_block();
       const float* cbuf = comb + cb * C::kW * (DH + 2);
       const int b = comb_bh[2 * cb], h = comb_bh[2 * cb + 1];
+      if (b < 0) return;  // the consumers saw the end of the CTA's units
       float M = -INFINITY;
 #pragma unroll
       for (int w = 0; w < C::kW; ++w) M = fmaxf(M, cbuf[w * (DH + 2) + DH]);
@@ -216,8 +238,7 @@ __global__ void __launch_bounds__(AttnCfg<T, DH, W>::kThreads, 1)
   const int sub = lane % C::kLpp;
   uint32_t it = 0;
 
-  int ui = 0;
-  for (int u = blockIdx.x; u < n_units; u += gridDim.x, ++ui) {
+  for (int ui = 0;; ++ui) {
     // unit header (first stage of the unit)
     const int s0 = it % C::kStages;
     mbar_wait(&full[s0], (it / C::kStages) & 1);
@@ -226,7 +247,21 @@ __global__ void __launch_bounds__(AttnCfg<T, DH, W>::kThreads, 1)
     const T* hk = hq + DH;
     const T* hv = hk + DH;
     const int* meta = (const int*)(hdr + 4 * DH * sizeof(T));
-    const int L = meta[0], b = meta[1], h = meta[2], kvh = h / group, slot = meta[3];
+    const int L = meta[0];
+    if (L < 0) {  // end of units: pass the end marker to the merge warp through the next buffer
+      if (!(a.flags & 3)) {
+        const int cb = ui % C::kNB;
+        while (comb_seq[cb] != ui / C::kNB) { }
+        if (cw == 0 && lane == 0) comb_bh[2 * cb] = -1;
+        __syncwarp();
+        if (lane == 0) {
+          __threadfence_block();
+          atomicAdd(&comb_cnt[cb], 1);
+        }
+      }
+      return;
+    }
+    const int b = meta[1], h = meta[2], kvh = h / group, slot = meta[3];
     const int nch = L > 0 ? (L + C::kTpos - 1) / C::kTpos : 1;
 
     float q[C::kEl], o[C::kEl];

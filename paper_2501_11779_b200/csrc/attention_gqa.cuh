@@ -93,9 +93,9 @@ __global__ void __launch_bounds__(GqaCfg<T, DH, G>::kThreads, 1)
       int u = blockIdx.x;
       int L = 0, sl = 0;
       if (u < n_units) { L = a.pos[u / a.Hkv]; sl = (int)a.slot[u / a.Hkv]; }
-      for (; u < n_units; u += gridDim.x) {
+      while (u < n_units) {
         const int b = u / a.Hkv, g = u % a.Hkv;
-        const int un = u + gridDim.x;
+        const int un = next_unit(a, u);
         int Ln = 0, sln = 0;
         if (un < n_units) { Ln = a.pos[un / a.Hkv]; sln = (int)a.slot[un / a.Hkv]; }
         const int nch = L > 0 ? (L + C::kTpos - 1) / C::kTpos : 1;
@@ -122,8 +122,16 @@ __global__ void __launch_bounds__(GqaCfg<T, DH, G>::kThreads, 1)
             bulk_g2s(hdr + gq + 2 * DH * sizeof(T), row + (long)g * G * DH, gq, &full[s], pol);    // x slices
           }
         }
+        u = un;
         L = Ln;
         sl = sln;
+      }
+      units_done(a);
+      {  // end of this CTA's units: a header-only stage with L = -1
+        const int s = it % C::kStages;
+        mbar_wait(&empty[s], ((it / C::kStages) & 1) ^ 1);
+        *(int*)(smem + s * C::kStageBytes + 2 * C::kTileBytes + hdr_bytes) = -1;
+        mbar_arrive(&full[s]);
       }
       prefetch_l2_share(a.pf, a.pf_bytes, blockIdx.x, gridDim.x);
     }
@@ -138,8 +146,7 @@ __global__ void __launch_bounds__(GqaCfg<T, DH, G>::kThreads, 1)
   const int sub = lane % C::kLpp;
   uint32_t it = 0;
 
-  int ui = 0;
-  for (int u = blockIdx.x; u < n_units; u += gridDim.x, ++ui) {
+  for (int ui = 0;; ++ui) {
     const int s0 = it % C::kStages;
     mbar_wait(&full[s0], (it / C::kStages) & 1);
     const uint8_t* hdr = smem + s0 * C::kStageBytes + 2 * C::kTileBytes;
@@ -148,7 +155,9 @@ __global__ void __launch_bounds__(GqaCfg<T, DH, G>::kThreads, 1)
     const T* hv = hk + DH;
     const T* hx = hv + DH;                        // [G][DH]
     const int* meta = (const int*)(hdr + (2 * G + 2) * DH * sizeof(T));
-    const int L = meta[0], b = meta[1], g = meta[2], slot = meta[3];
+    const int L = meta[0];
+    if (L < 0) return;  // end of the CTA's units
+    const int b = meta[1], g = meta[2], slot = meta[3];
     const int nch = L > 0 ? (L + C::kTpos - 1) / C::kTpos : 1;
 
     float q[HPW][C::kEl], o[HPW][C::kEl], m[HPW], l[HPW];
@@ -457,9 +466,9 @@ __global__ void __launch_bounds__(GqaTcCfg<G>::kThreads, 1)
       int u = blockIdx.x;
       int L = 0, sl = 0;
       if (u < n_units) { L = a.pos[u / a.Hkv]; sl = (int)a.slot[u / a.Hkv]; }
-      for (; u < n_units; u += gridDim.x) {
+      while (u < n_units) {
         const int b = u / a.Hkv, g = u % a.Hkv;
-        const int un = u + gridDim.x;
+        const int un = next_unit(a, u);
         int Ln = 0, sln = 0;
         if (un < n_units) { Ln = a.pos[un / a.Hkv]; sln = (int)a.slot[un / a.Hkv]; }
         // tensor-map rows (layer, slot or page, K/V, kv head); paged: one page per stage
@@ -494,8 +503,16 @@ __global__ void __launch_bounds__(GqaTcCfg<G>::kThreads, 1)
             bulk_g2s(hdr + gq + 2 * DH * 2, row + (long)g * G * DH, gq, &full[s], pol);          // x slices
           }
         }
+        u = un;
         L = Ln;
         sl = sln;
+      }
+      units_done(a);
+      {  // end of this CTA's units: a header-only stage with L = -1
+        const int s = it % C::kStages;
+        mbar_wait(&empty[s], ((it / C::kStages) & 1) ^ 1);
+        *(int*)(smem + s * C::kStageBytes + C::kKV + hdr_bytes) = -1;
+        mbar_arrive(&full[s]);
       }
       prefetch_l2_share(a.pf, a.pf_bytes, blockIdx.x, gridDim.x);
     }
@@ -505,13 +522,13 @@ __global__ void __launch_bounds__(GqaTcCfg<G>::kThreads, 1)
   if (warp == C::kW + 1) {
     // -------------------------------------------------- merge warp (unit order): combines the kW
     // consumer states and the new token's state of every query head, writes the G output rows
-    int ui = 0;
-    for (int u = blockIdx.x; u < n_units; u += gridDim.x, ++ui) {
+    for (int ui = 0;; ++ui) {
       const int cb = ui % C::kNB;
       while (*(volatile int*)&comb_cnt[cb] < C::kW) { }
       __threadfence_block();
       const float* cbuf = comb + cb * C::kCombPerUnit;
       const int b = comb_bg[2 * cb], g = comb_bg[2 * cb + 1];
+      if (b < 0) return;  // the consumers saw the end of the CTA's units
       for (int hq = 0; hq < G; ++hq) {
         float M = -INFINITY;
 #pragma unroll
@@ -548,8 +565,7 @@ __global__ void __launch_bounds__(GqaTcCfg<G>::kThreads, 1)
   const int qr = lane >> 2;            // query head (MMA row) of this lane's accumulator entries
   const int qc = (lane & 3) * 2;       // first of its two columns
   uint32_t it = 0;
-  int ui = 0;
-  for (int u = blockIdx.x; u < n_units; u += gridDim.x, ++ui) {
+  for (int ui = 0;; ++ui) {
     const int s0 = it % C::kStages;
     mbar_wait(&full[s0], (it / C::kStages) & 1);
     const uint8_t* hdr = smem + s0 * C::kStageBytes + C::kKV;
@@ -558,7 +574,19 @@ __global__ void __launch_bounds__(GqaTcCfg<G>::kThreads, 1)
     const bf16_t* hv = hk + DH;
     const bf16_t* hx = hv + DH;
     const int* meta = (const int*)(hdr + hdr_bytes);
-    const int L = meta[0], b = meta[1], g = meta[2], slot = meta[3];
+    const int L = meta[0];
+    if (L < 0) {  // end of units: pass the end marker to the merge warp through the next buffer
+      const int cb = ui % C::kNB;
+      while (comb_seq[cb] != ui / C::kNB) { }
+      if (cw == 0 && lane == 0) comb_bg[2 * cb] = -1;
+      __syncwarp();
+      if (lane == 0) {
+        __threadfence_block();
+        atomicAdd(&comb_cnt[cb], 1);
+      }
+      return;
+    }
+    const int b = meta[1], g = meta[2], slot = meta[3];
     const int nch = L > 0 ? (L + C::kTpos - 1) / C::kTpos : 1;
 
     // Q fragments (A operand, rows = query heads; rows >= G and 8..15 are zero)

@@ -85,6 +85,9 @@ struct AttnArgs {
   // page (2 * Hkv * 64 * DH / Hkv * 64 * DH / 64 * DH) and n_slots is the number of pages.
   const int* page_table;
   int max_pages;
+  // Dynamic unit schedule (nullptr = static stride gridDim.x): work[0] hands out units after each
+  // CTA's first, work[1] counts finished producers; the last one zeroes both for the next launch.
+  unsigned int* work;
 };
 // Positions per KV page of the paged arena (one 64-position TMA box / attention stage).
 constexpr int kKvPagePositions = 64;

@@ -468,6 +468,11 @@ struct gh_tier2 {
   uint32_t n_pages = 0, max_pages = 0;
   int* d_pt = nullptr;              // device [n_slots][max_pages]
   int* d_limit = nullptr;           // device [n_slots] (synthetic fill of ragged contexts)
+  // attention work counters (dynamic unit schedule), one pair per launch from a ring so that
+  // launches in flight at the same time (in-flight batches) never share one
+  static constexpr int kWorkRing = 64;
+  unsigned int* work = nullptr;
+  int work_next = 0;
   std::vector<int> h_pt;            // host mirror
   std::vector<uint32_t> mapped;     // pages mapped per slot
   std::vector<int> free_pages;      // LIFO pool
@@ -512,6 +517,12 @@ static gh_status tier2_create(const gh_model_spec* spec, int device, uint32_t la
   // zeroed once: never-written positions are finite (tile loads past a prompt's length are masked,
   // and 0 x NaN would not be)
   GH_CUDA(cudaMemset(t->arena, 0, t->arena_bytes));
+  {
+    void* p;
+    GH_TRY(dev_alloc(t->mem, gh_tier2::kWorkRing * 2 * sizeof(unsigned int), &p));
+    GH_CUDA(cudaMemset(p, 0, gh_tier2::kWorkRing * 2 * sizeof(unsigned int)));
+    t->work = (unsigned int*)p;
+  }
   if (t->paged) {
     void* p;
     const size_t n = (size_t)n_slots * t->max_pages;
@@ -634,6 +645,8 @@ static gh_status t2_attend(gh_tier2* t, uint32_t layer, uint32_t B, const uint32
   a.pf = pf;
   a.pf_bytes = pf ? pf_bytes : 0;
   a.layer_local = (int)(layer - t->l0);
+  static const bool static_units = getenv("GH_ATTN_STATIC") != nullptr;  // diagnostics
+  a.work = static_units ? nullptr : t->work + 2 * (t->work_next++ % gh_tier2::kWorkRing);
   a.kv_tmap = t->has_tmap ? &t->kv_tmap : nullptr;
   GH_CUDA(launch_attention(s.db, s.dh, a, (cudaStream_t)stream));
   return GH_OK;
