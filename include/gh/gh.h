@@ -151,6 +151,11 @@ gh_status gh_tier2_destroy(gh_tier2* t2);
  * host only when check_host != 0 via gh_tier2_check) for slot >= n_slots or pos >= S. */
 gh_status gh_tier2_attend(gh_tier2* t2, uint32_t layer, uint32_t B, const uint32_t* slot,
                           const int32_t* pos, const void* msg_fwd, void* msg_bwd, void* stream);
+/* KV append of every row of msg_fwd at (slot[b], pos[b]) without attention: run before
+ * gh_tier2_attend when rows of one step share a slot (chunked prefill), so that every row sees
+ * the keys of the rows before it.  gh_tier2_attend's own append rewrites the same values. */
+gh_status gh_tier2_append(gh_tier2* t2, uint32_t layer, uint32_t B, const uint32_t* slot,
+                          const int32_t* pos, const void* msg_fwd, void* stream);
 /* Host-side admission check of a batch (slot < n_slots, 0 <= pos < S). */
 gh_status gh_tier2_check(const gh_tier2* t2, uint32_t B, const uint32_t* slot_host,
                          const int32_t* pos_host);
@@ -213,6 +218,9 @@ typedef struct gh_engine_config {
                               optimizer.cpp:116-123; embedding on the first, classifier on the
                               last) and ranks T + s*K' + j are the K' Tier-2 ranks dedicated to
                               span s; world = T * (1 + K').  Peer transport only. */
+  int prefill;             /* colocated: rows of one step may share a slot at consecutive positions
+                              (chunked prefill mixed with decode rows); every row's key / value is
+                              appended before attention (gh_tier2_append) */
   uint32_t kv_pages;       /* 0: contiguous slots of max_seq_len positions; > 0: paged KV arena of
                               kv_pages pages of GH_KV_PAGE_POSITIONS positions shared by the slots
                               (gh_tier2_create_paged; map with gh_engine_kv_map before a step) */
@@ -264,6 +272,10 @@ gh_tier2* gh_engine_tier2(gh_engine* e);
  * + row on a colocated engine, the local slot on a Tier-2 rank); no-ops for contiguous slots. */
 gh_status gh_engine_kv_map(gh_engine* e, uint32_t slot, uint32_t n_positions);
 gh_status gh_engine_kv_unmap(gh_engine* e, uint32_t slot);
+/* Per-row context slots of in-flight batch ib (colocated engine; default ib * batch + row).
+ * With prefill != 0 several rows may name the same slot (consecutive positions of one prompt).
+ * Synchronises the device. */
+gh_status gh_engine_set_slots(gh_engine* e, uint32_t ib, const uint32_t* slot_host);
 /* Launch count of this library's kernels since the last reset (device work accounting). */
 uint64_t gh_kernel_launches(int reset);
 

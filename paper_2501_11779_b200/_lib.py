@@ -63,6 +63,7 @@ class GhEngineConfig(C.Structure):
                 ("use_graph", C.c_int),
                 ("transport", C.c_int),
                 ("tier1_ranks", C.c_uint32),
+                ("prefill", C.c_int),
                 ("kv_pages", C.c_uint32)]
 
 
@@ -106,6 +107,7 @@ PROTOTYPES = {
     "gh_tier2_create_paged": (st, [P(GhSpec), C.c_int, u32, u32, u32, u32, P(vp)]),
     "gh_tier2_map": (st, [vp, u32, u32, vp]),
     "gh_tier2_unmap": (st, [vp, u32]),
+    "gh_tier2_append": (st, [vp, u32, u32, vp, vp, vp, vp]),
     "gh_tier2_pages_free": (u32, [vp]),
     "gh_comm_unique_id": (st, [P(C.c_uint8)]),
     "gh_comm_create": (st, [P(C.c_uint8), C.c_int, C.c_int, C.c_int, P(vp)]),
@@ -126,6 +128,7 @@ PROTOTYPES = {
     "gh_engine_tier2": (vp, [vp]),
     "gh_engine_kv_map": (st, [vp, u32, u32]),
     "gh_engine_kv_unmap": (st, [vp, u32]),
+    "gh_engine_set_slots": (st, [vp, u32, P(u32)]),
     "gh_kernel_launches": (u64, [C.c_int]),
     "gh_debug_gemm_bench": (st, [C.c_int] * 7 + [P(C.c_float)]),
     "gh_debug_gemm_trace": (st, [C.c_int] * 5 + [P(C.c_float), P(C.c_uint64), C.c_int]),

@@ -109,6 +109,27 @@ __global__ void fill_kv_kernel(T* arena, uint64_t seed, int l0, int n_layers, in
   }
 }
 
+// Append the key / value of every row of the fwd message to the arena at (slot[b], pos[b]) ahead of
+// the attention kernel, for steps in which several rows of one prompt (chunked prefill) attend
+// each other's positions.  16 bytes per thread; either arena layout (kv_offset).
+template <typename T>
+__global__ void append_kv_kernel(const AttnArgs a, int DH) {
+  constexpr int kVec = 16 / sizeof(T);
+  griddep_launch_dependents();
+  griddep_wait();  // the fwd message comes from the QKV GEMM
+  const int per_row = 2 * a.Dkv / kVec;
+  const long total = (long)a.B * per_row;
+  const T* fwd = (const T*)a.msg_fwd;
+  T* arena = (T*)a.arena;
+  const long ld_fwd = 2L * a.D + 2L * a.Dkv;
+  for (long i = blockIdx.x * (long)blockDim.x + threadIdx.x; i < total; i += (long)gridDim.x * blockDim.x) {
+    const int b = (int)(i / per_row), r = (int)(i % per_row) * kVec;
+    const int kv = r / a.Dkv, e = r % a.Dkv, h = e / DH, d = e % DH;
+    const uint4 v = *(const uint4*)(fwd + b * ld_fwd + 2L * a.D + r);
+    *(uint4*)(arena + kv_offset(a, (int)a.slot[b], h, a.pos[b], DH) + kv * a.kv_stride + d) = v;
+  }
+}
+
 static int grid_for(uint64_t n) {
   uint64_t g = (n + 255) / 256;
   return (int)std::min<uint64_t>(g, (uint64_t)kNumSMs * 32);
@@ -777,6 +798,14 @@ static cudaError_t launch_attn_t(const AttnArgs& a, cudaStream_t st) {
 
 bool attention_supported(int db, int dh) {
   return (db == 2 || db == 4) && (dh == 48 || dh == 64 || dh == 128);
+}
+
+cudaError_t launch_append_kv(int db, int dh, const AttnArgs& a, cudaStream_t st) {
+  const long chunks = (long)a.B * 2 * a.Dkv * db / 16;
+  const int grid = (int)std::min<long>((chunks + 255) / 256, (long)kNumSMs * 8);
+  if (chunks == 0) return cudaSuccess;
+  if (db == 4) return launch_pdl(append_kv_kernel<float>, grid, 256, 0, st, a, dh);
+  return launch_pdl(append_kv_kernel<bf16_t>, grid, 256, 0, st, a, dh);
 }
 
 cudaError_t launch_attention(int db, int dh, const AttnArgs& a, cudaStream_t st) {

@@ -95,6 +95,8 @@ cudaError_t launch_argmax_rows(const float* logits, int B, int V, int32_t* next_
 struct AttnArgs;
 cudaError_t launch_attention(int dtype_bytes, int d_head, const AttnArgs& a, cudaStream_t st);
 bool attention_supported(int dtype_bytes, int d_head);
+// Write every row's key / value (fwd message) into the arena at (slot[b], pos[b]).
+cudaError_t launch_append_kv(int dtype_bytes, int d_head, const AttnArgs& a, cudaStream_t st);
 
 // Synthetic initialisation (deterministic, see common.cuh / DESIGN.md)
 // Logical matrix [rows, cols] of tensor `tid` with std `std_`; `row_map` selects which logical

@@ -652,7 +652,29 @@ static gh_status t2_attend(gh_tier2* t, uint32_t layer, uint32_t B, const uint32
   return GH_OK;
 }
 
+static gh_status t2_append(gh_tier2* t, uint32_t layer, uint32_t B, const uint32_t* slot, const int32_t* pos,
+                           const void* msg_fwd, void* stream) {
+  if (!t || !slot || !pos || !msg_fwd) return fail(GH_EINVAL, "null argument");
+  if (layer < t->l0 || layer >= t->l1) return fail(GH_EINVAL, "layer not owned by this Tier-2");
+  if (B == 0) return GH_OK;
+  const Shape& s = t->sh;
+  AttnArgs a{};
+  a.msg_fwd = msg_fwd;
+  a.arena = (char*)t->arena + (size_t)(layer - t->l0) * t->layer_stride() * s.db;
+  a.slot = slot;
+  a.pos = pos;
+  t->layout(a);
+  a.B = (int)B; a.H = s.H; a.Hkv = s.Hkv; a.D = s.D; a.Dkv = s.Dkv;
+  GH_CUDA(launch_append_kv(s.db, s.dh, a, (cudaStream_t)stream));
+  return GH_OK;
+}
+
 extern "C" {
+
+gh_status gh_tier2_append(gh_tier2* t, uint32_t layer, uint32_t B, const uint32_t* slot, const int32_t* pos,
+                          const void* msg_fwd, void* stream) {
+  return t2_append(t, layer, B, slot, pos, msg_fwd, stream);
+}
 
 gh_status gh_tier2_fill_synthetic(gh_tier2* t, uint64_t seed, uint32_t n_fill, uint32_t npos, void* stream) {
   if (!t) return fail(GH_EINVAL, "null argument");
@@ -811,6 +833,7 @@ struct gh_engine {
   struct Batch {
     int32_t *tok = nullptr, *pos = nullptr, *next = nullptr;
     uint32_t* slot = nullptr;
+    std::vector<uint32_t> slot_host;       // host copy of `slot` (admission checks)
     void *x0 = nullptr, *x1 = nullptr, *fwd = nullptr, *bwd = nullptr;
     float *ss0 = nullptr, *ss1 = nullptr;  // per-slice sums of squares of x0 / x1 (fused RMSNorm)
     int ss_slices[2] = {0, 0};
@@ -899,6 +922,7 @@ static gh_status engine_layer_loop_colocated(gh_engine* e, gh_engine::Batch& b, 
   for (int l = 0; l < s.N; ++l) {
     GH_TRY(act_pre(e, b, l, st));
     const Weight& wo = e->t1->layers[l].o;
+    if (e->cfg.prefill) GH_TRY(t2_append(e->t2, l, B, b.slot, b.pos, b.fwd, st));  // rows may share a prompt
     GH_TRY(t2_attend(e->t2, l, B, b.slot, b.pos, b.fwd, b.bwd, st, wo.ptr, gh_tier1::prefetch_bytes(&wo)));
     GH_TRY(act_post(e, b, l, st));
   }
@@ -931,6 +955,7 @@ gh_status gh_engine_create(const gh_engine_config* cfg, gh_comm* comm, gh_engine
     if (e->n1 > s.N) return fail(GH_EINVAL, "more Tier-1 spans than layers");
     if (e->n1 > 1 && cfg->transport == GH_TRANSPORT_NCCL)
       return fail(GH_EUNSUPPORTED, "Tier-1 pipeline stages need the peer transport");
+    if (cfg->prefill) return fail(GH_EUNSUPPORTED, "chunked prefill rows: colocated engine only");
     e->kp = (world - e->n1) / e->n1;
     e->role = rank < e->n1 ? 1 : 2;
     e->span = rank < e->n1 ? rank : (rank - e->n1) / e->kp;
@@ -980,6 +1005,7 @@ gh_status gh_engine_create(const gh_engine_config* cfg, gh_comm* comm, gh_engine
     std::vector<uint32_t> slots(R);
     for (int i = 0; i < R; ++i) slots[i] = ib * R + i;
     GH_CUDA(cudaMemcpy(b.slot, slots.data(), R * 4, cudaMemcpyHostToDevice));
+    b.slot_host = slots;
     GH_CUDA(cudaMemset(b.tok, 0, R * 4));
     GH_CUDA(cudaMemset(b.pos, 0, R * 4));
     GH_CUDA(cudaMemset(b.next, 0, R * 4));
@@ -1032,6 +1058,21 @@ gh_status gh_engine_kv_map(gh_engine* e, uint32_t slot, uint32_t n_positions) {
   if (!e) return fail(GH_EINVAL, "null engine");
   if (!e->t2) return fail(GH_EUNSUPPORTED, "this rank holds no KV (Tier-1 role)");
   return gh_tier2_map(e->t2, slot, n_positions, nullptr);
+}
+
+gh_status gh_engine_set_slots(gh_engine* e, uint32_t ib, const uint32_t* slot_host) {
+  if (!e || !slot_host || ib >= e->batches.size()) return fail(GH_EINVAL, "bad engine / batch index / slots");
+  if (e->role != 0) return fail(GH_EUNSUPPORTED, "per-row slots: colocated engine only");
+  auto& b = e->batches[ib];
+  const int R = e->rows();
+  for (int i = 0; i < R; ++i)
+    if (slot_host[i] >= e->t2->n_slots)
+      return fail(GH_EINVAL, "slot " + std::to_string(slot_host[i]) + " >= n_slots " + std::to_string(e->t2->n_slots));
+  GH_CUDA(cudaSetDevice(e->cfg.device));
+  GH_CUDA(cudaDeviceSynchronize());  // no step in flight reads the old slots
+  GH_CUDA(cudaMemcpy(b.slot, slot_host, (size_t)R * 4, cudaMemcpyHostToDevice));
+  b.slot_host.assign(slot_host, slot_host + R);
+  return GH_OK;
 }
 
 gh_status gh_engine_kv_unmap(gh_engine* e, uint32_t slot) {
@@ -1556,11 +1597,8 @@ gh_status gh_engine_step_host(gh_engine* e, uint32_t ib, const int32_t* tok_host
   const int R = e->rows();
   if (e->role != 2) {
     if (!tok_host || !pos_host || !next_host) return fail(GH_EINVAL, "host token/pos/next buffers required");
-    if (e->role == 0 && e->t2->paged) {  // paged KV: every attended position must be mapped
-      std::vector<uint32_t> sl(R);
-      for (int i = 0; i < R; ++i) sl[i] = ib * R + i;
-      GH_TRY(gh_tier2_check(e->t2, (uint32_t)R, sl.data(), pos_host));
-    }
+    if (e->role == 0 && e->t2->paged)  // paged KV: every attended position must be mapped
+      GH_TRY(gh_tier2_check(e->t2, (uint32_t)R, b.slot_host.data(), pos_host));
     GH_CUDA(cudaMemcpyAsync(b.tok, tok_host, (size_t)R * 4, cudaMemcpyHostToDevice, st));
     GH_CUDA(cudaMemcpyAsync(b.pos, pos_host, (size_t)R * 4, cudaMemcpyHostToDevice, st));
   }

@@ -118,6 +118,11 @@ class Tier2:
         L.check(L.lib().gh_tier2_attend(self.h, layer, msg_fwd.shape[0], L.ptr(slot), L.ptr(pos),
                                         L.ptr(msg_fwd), L.ptr(msg_bwd), _stream(stream)))
 
+    def append(self, layer: int, slot, pos, msg_fwd, stream=None):
+        """KV append of every row without attention (rows of one prompt in one step)."""
+        L.check(L.lib().gh_tier2_append(self.h, layer, msg_fwd.shape[0], L.ptr(slot), L.ptr(pos),
+                                        L.ptr(msg_fwd), _stream(stream)))
+
     def fill_synthetic(self, seed: int, n_slots: int, n_positions: int, stream=None):
         L.check(L.lib().gh_tier2_fill_synthetic(self.h, seed, n_slots, n_positions, _stream(stream)))
 
@@ -173,11 +178,13 @@ class Engine:
     def __init__(self, spec: ModelSpec, batch: int, inflight: int = 1, device: int = 0,
                  weight_seed: int = 1234, n_slots: int = 0, use_graph: bool = True,
                  comm: Comm | None = None, transport: str = "auto", tier1_ranks: int = 1,
-                 kv_pages: int = 0):
+                 kv_pages: int = 0, prefill: bool = False):
         self.spec, self.batch, self.inflight = spec, batch, inflight
         self.kv_pages = kv_pages
+        self.prefill = prefill
+        self.n_slots = n_slots or batch * inflight
         cfg = L.GhEngineConfig(spec.c(), device, weight_seed, batch, inflight, n_slots, int(use_graph),
-                               self.TRANSPORTS[transport], tier1_ranks, kv_pages)
+                               self.TRANSPORTS[transport], tier1_ranks, int(prefill), kv_pages)
         h = C.c_void_p()
         L.check(L.lib().gh_engine_create(C.byref(cfg), comm.h if comm else None, C.byref(h)))
         self.h = h
@@ -208,6 +215,11 @@ class Engine:
 
     def kv_unmap(self, slot: int):
         L.check(L.lib().gh_engine_kv_unmap(self.h, slot))
+
+    def set_slots(self, slots, ib=0):
+        """Context slot of every row of in-flight batch ib (colocated)."""
+        s = np.ascontiguousarray(slots, dtype=np.uint32)
+        L.check(L.lib().gh_engine_set_slots(self.h, ib, s.ctypes.data_as(C.POINTER(C.c_uint32))))
 
     def step_host(self, tok: np.ndarray | None, pos: np.ndarray | None, want_logits=False, ib=0,
                   stream=None):
@@ -354,4 +366,88 @@ class ContinuousDispatcher:
                     admit(lane)
         if queue:
             raise L.FeasibilityError(L.GH_EINFEASIBLE, f"request {queue[0]} needs more KV pages than the pool holds")
+        return [np.array(o, np.int32) for o in out], steps
+
+
+class MixedDispatcher:
+    """Mixed prefill + decode batches: the engine's B rows are a pool, not
+    lanes.  Every step, each admitted request in its decode phase takes one row (its last token);
+    a request still reading its prompt takes up to `chunk` rows, one per prompt token at
+    consecutive positions of its slot (chunked prefill), so a prompt of n tokens needs
+    ceil(n / chunk) steps instead of n.  The engine runs with prefill=True: every row's key and
+    value are appended before attention, so the rows of one prompt see each other's keys exactly
+    as they would one token per step -- each request's tokens equal decoding it alone.  The
+    row of a request's last prompt token yields its first generated token.  Rows left over hold
+    a dummy token in a reserved scratch slot (the engine's last slot).  With a paged arena a
+    request maps prompt + max_new - 1 positions on admission and returns them when done."""
+
+    def __init__(self, engine: Engine, chunk: int = 16):
+        if not engine.prefill:
+            raise L.ValidationError(L.GH_EINVAL, "MixedDispatcher needs Engine(prefill=True)")
+        if engine.n_slots < 2:
+            raise L.ValidationError(L.GH_EINVAL, "MixedDispatcher needs n_slots >= 2 (one scratch slot)")
+        self.engine, self.chunk = engine, chunk
+
+    def run(self, requests, max_new: int):
+        """Returns (generated token arrays in request order, steps)."""
+        eng, B = self.engine, self.engine.batch
+        scratch = eng.n_slots - 1
+        free_slots = list(range(eng.n_slots - 1))
+        queue = list(range(len(requests)))
+        active = []                       # [request, slot, fed]
+        out = [[] for _ in requests]
+        eng.kv_map(scratch, 1)
+        last_slots = None
+        steps = 0
+        while queue or active:
+            # admission (FIFO) while a slot and, when paged, the pages are available
+            while queue and free_slots:
+                r = queue[0]
+                s = free_slots[0]
+                try:
+                    eng.kv_map(s, len(requests[r]) + max_new - 1)
+                except L.FeasibilityError:
+                    if not active:
+                        raise
+                    break
+                queue.pop(0)
+                free_slots.pop(0)
+                active.append([r, s, 0])
+            tok = np.zeros(B, np.int32)
+            pos = np.zeros(B, np.int32)
+            slots = np.full(B, scratch, np.uint32)
+            emit = []                      # (row, request) pairs whose next token is generated
+            row = 0
+            for a in active:
+                r, s, fed = a
+                p = requests[r]
+                if row >= B:
+                    break
+                if fed < len(p):           # prefill rows
+                    n = min(self.chunk, len(p) - fed, B - row)
+                    tok[row:row + n] = p[fed:fed + n]
+                    pos[row:row + n] = np.arange(fed, fed + n)
+                    slots[row:row + n] = s
+                    if fed + n == len(p):
+                        emit.append((row + n - 1, a))
+                    a[2] = fed + n
+                    row += n
+                else:                      # decode row: the last generated token
+                    tok[row] = out[r][-1]
+                    pos[row] = len(p) + len(out[r]) - 1
+                    slots[row] = s
+                    emit.append((row, a))
+                    row += 1
+            if last_slots is None or not np.array_equal(slots, last_slots):
+                eng.set_slots(slots)
+                last_slots = slots
+            nxt, _ = eng.step_host(tok, pos)
+            steps += 1
+            for rw, a in emit:
+                r = a[0]
+                out[r].append(int(nxt[rw]))
+                if len(out[r]) == max_new:
+                    active.remove(a)
+                    eng.kv_unmap(a[1])
+                    free_slots.append(a[1])
         return [np.array(o, np.int32) for o in out], steps
