@@ -980,7 +980,8 @@ gh_status gh_engine_create(const gh_engine_config* cfg, gh_comm* comm, gh_engine
   if (e->role != 1) {
     uint32_t need = (uint32_t)R * cfg->inflight;
     uint32_t n_slots = cfg->n_slots ? cfg->n_slots : need;
-    if (n_slots < need) return fail(GH_EINFEASIBLE, "n_slots smaller than batch * inflight (binding constraint: memory)");
+    if (n_slots < need && !cfg->prefill)  // prefill rows share slots: any n_slots >= 1
+      return fail(GH_EINFEASIBLE, "n_slots smaller than batch * inflight (binding constraint: memory)");
     GH_TRY(tier2_create(&cfg->spec, cfg->device, (uint32_t)e->l0, (uint32_t)e->l1, n_slots, cfg->kv_pages, &e->t2));
   }
   GH_CUDA(cudaEventCreateWithFlags(&e->fork, cudaEventDisableTiming));
@@ -1003,7 +1004,7 @@ gh_status gh_engine_create(const gh_engine_config* cfg, gh_comm* comm, gh_engine
     }
     if (e->role != 2) { GH_TRY(dev_alloc(e->mem, (size_t)R * s.V * 4, &p)); b.logits = (float*)p; }
     std::vector<uint32_t> slots(R);
-    for (int i = 0; i < R; ++i) slots[i] = ib * R + i;
+    for (int i = 0; i < R; ++i) slots[i] = e->t2 ? (ib * R + i) % e->t2->n_slots : ib * R + i;
     GH_CUDA(cudaMemcpy(b.slot, slots.data(), R * 4, cudaMemcpyHostToDevice));
     b.slot_host = slots;
     GH_CUDA(cudaMemset(b.tok, 0, R * 4));
