@@ -195,6 +195,8 @@ def workload(args, world):
     cfg = args.config or "C2"
     c = gh.CONFIGS[cfg]
     spec, ctx = c["spec"], c["ctx"]
+    if args.paged and (world == 1 or cfg == "C2"):
+        raise SystemExit("--paged is a tier-split option of C3 / C4 / C5 (tools/paged_bench.py covers one GPU)")
     if world == 1:
         if cfg in ("C4", "C5"):
             raise SystemExit(f"--config {cfg} is a tier-split configuration (run it with N >= 2 GPUs)")
@@ -219,8 +221,46 @@ def workload(args, world):
         shard = args.shard
         if shard * inflight > per_gpu:
             raise SystemExit(f"--shard {shard} x IF {inflight} exceeds the {per_gpu} admitted slots per Tier-2 GPU")
+    if args.paged:
+        return paged_workload(cfg, spec, ctx, c["batch"], kp, inflight, per_gpu, n1)
     return dict(name=cfg, spec=spec, ctx=ctx, batch=shard * kp, requested=c["batch"], inflight=inflight,
                 shard=shard, kp=kp, admitted_slots=slots)
+
+
+PAGE = 64  # GH_KV_PAGE_POSITIONS
+
+
+def paged_workload(cfg, spec, ctx, requested, kp, inflight, per_gpu, n1):
+    """Tier split on a paged KV arena: each Tier-2 GPU gets the pages of its
+    per_gpu full-context slots; every prompt has its own context drawn uniformly from [1, ctx)
+    (seed 4321), and the shard is the largest that fits every Tier-2 GPU's pages (up to the
+    requested batch).  Prompt g = ib * batch + j * shard + r lives on Tier-2 rank j, local slot
+    ib * shard + r."""
+    if n1 != 1:
+        raise SystemExit("--paged: one Tier-1 rank")
+    pages = per_gpu * (ctx // PAGE)
+    cap = max(1, requested // (kp * inflight))
+    rng = np.random.default_rng(4321)
+    ctxs_all = rng.integers(1, ctx, size=cap * kp * inflight).astype(np.int32)
+
+    def fits(shard):
+        batch = shard * kp
+        for j in range(kp):
+            used = 0
+            for ib in range(inflight):
+                c = ctxs_all[:batch * inflight].reshape(inflight, batch)[ib, j * shard:(j + 1) * shard]
+                used += int(np.sum((c + 1 + PAGE - 1) // PAGE))
+            if used > pages:
+                return False
+        return True
+
+    shard = 1
+    while shard < cap and fits(shard + 1):
+        shard += 1
+    batch = shard * kp
+    ctxs = ctxs_all[:batch * inflight].reshape(inflight, batch)
+    return dict(name=cfg + "-paged", spec=spec, ctx=ctx, batch=batch, requested=requested, inflight=inflight,
+                shard=shard, kp=kp, admitted_slots=per_gpu * kp, kv_pages=pages, ctxs=ctxs)
 
 
 def ncu_traffic(kernel_prefix):
@@ -354,18 +394,25 @@ def run_split(args, wl, rank, world):
     dist.broadcast_object_list(obj, src=0)
     comm = Comm(obj[0], world, rank, dev)
     eng = Engine(spec, batch=wl["batch"], inflight=IF, device=dev, use_graph=False, comm=comm,
-                 transport=args.transport, tier1_ranks=max(1, args.tier1))
+                 transport=args.transport, tier1_ranks=max(1, args.tier1), kv_pages=wl.get("kv_pages", 0))
     transport = eng.transport
     lib = gh.lib()
     stream = torch.cuda.Stream()
+    ctxs = wl.get("ctxs")  # paged: per-prompt contexts [IF, batch]
     if eng.role == "tier2":
+        if ctxs is not None:  # back each local slot with the pages of its own context
+            j, sh = rank - 1, wl["shard"]
+            for ib in range(IF):
+                for r in range(sh):
+                    eng.kv_map(ib * sh + r, int(ctxs[ib, j * sh + r]) + 1)
         L.check(lib.gh_tier2_fill_synthetic(eng.tier2, 99, wl["shard"] * IF, ctx - 1, None))
     rng = np.random.default_rng(5678)
     tok = rng.integers(0, spec.vocab_size, size=wl["batch"]).astype(np.int32)
     pos = np.full(wl["batch"], ctx - 1, np.int32)
     torch.cuda.synchronize()
     t1 = eng.role == "tier1"
-    eng.step_all_host(np.tile(tok, (IF, 1)) if t1 else None, np.tile(pos, (IF, 1)) if t1 else None, stream=stream)
+    pos_all = ctxs if ctxs is not None else np.tile(pos, (IF, 1))
+    eng.step_all_host(np.tile(tok, (IF, 1)) if t1 else None, pos_all if t1 else None, stream=stream)
     dist.barrier()
     n0 = lib.gh_kernel_launches(0)
     for _ in range(args.warmup):
@@ -403,7 +450,7 @@ def run_split(args, wl, rank, world):
     t0 = time.perf_counter()
     nsteps = max(2, args.steps // 2)
     toks = np.tile(tok, (IF, 1))
-    poss = np.tile(pos, (IF, 1))
+    poss = pos_all
     n1 = max(1, args.tier1)
     for _ in range(nsteps):
         r = eng.step_all_host(toks if eng.role == "tier1" else None, poss if eng.role == "tier1" else None,
@@ -444,6 +491,8 @@ def main():
                     help="C2 tier split: prompts per Tier-2 GPU per in-flight batch (default 64, the N=1 batch)")
     ap.add_argument("--inflight", type=int, default=0,
                     help="tier split: in-flight batches (0 = if_gh from the stage profiles)")
+    ap.add_argument("--paged", action="store_true",
+                    help="tier split (C3/C4/C5): paged KV arena, per-prompt contexts uniform in [1, ctx)")
     ap.add_argument("--transport", default="auto", choices=["auto", "nccl", "peer"],
                     help="tier-split message transport (peer: copy engines + IPC flags; nccl: send/recv)")
     args = ap.parse_args()
@@ -465,6 +514,10 @@ def main():
            "inflight": wl["inflight"], "dtype_storage": "bf16", "l2": "inputs larger than L2 (no flush)"}
     if "admitted_slots" in wl:
         cfg["admitted_slots"] = wl["admitted_slots"]
+    if "ctxs" in wl:
+        cfg["contexts"] = (f"paged KV ({wl['kv_pages']} pages of {PAGE} positions per Tier-2 GPU = its "
+                           f"{wl['admitted_slots'] // wl['kp']} full-context slots); per-prompt context uniform "
+                           f"in [1, {wl['ctx']}), mean {float(np.mean(wl['ctxs'])):.0f}")
 
     if args.impl == "reference":
         if world > 1 and rank != 0:

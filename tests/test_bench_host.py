@@ -41,3 +41,21 @@ def test_if_gh_from_profiles(bench):
     # Tier-1 nonattention grows with the batch while Tier-2 attention per shard is fixed, so the
     # in-flight batches needed to cover a Tier-2 round trip never grow with K'
     assert bench.if_gh_from_profiles(spec, 64 * 7, 64, 512) <= bench.if_gh_from_profiles(spec, 64, 64, 512)
+
+
+def test_paged_workload_fits_every_tier2_gpu():
+    """bench.py --paged: the chosen shard's pages fit each Tier-2 GPU's budget, one more prompt
+    per shard would not (or the requested batch is reached), and it admits more prompts than
+    the contiguous slots."""
+    import numpy as np
+    import bench
+    import paper_2501_11779_b200 as gh
+    spec = gh.CONFIGS["C3"]["spec"]
+    wl = bench.paged_workload("C3", spec, 2048, 1024, 3, 2, 170, 1)
+    pages, sh, kp = wl["kv_pages"], wl["shard"], wl["kp"]
+    assert pages == 170 * 32 and wl["ctxs"].shape == (2, sh * kp)
+    for j in range(kp):
+        used = sum(int(np.sum((wl["ctxs"][ib, j * sh:(j + 1) * sh] + 64) // 64)) for ib in range(2))
+        assert used <= pages
+    assert sh * kp * 2 > 510            # more than the 510 contiguous C3 slots at K' = 3
+    assert sh * kp * 2 <= 1024
