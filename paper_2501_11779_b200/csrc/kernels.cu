@@ -416,7 +416,7 @@ cudaError_t make_tmap_kv(CUtensorMap* out, const void* base, uint64_t rows, uint
 }
 
 static const int kBNs[] = {16, 32, 64, 128};  // batches > 128 use several batch tiles
-static int stages_override = 0;  // diagnostics
+static int stages_override = getenv("GH_GEMM_STAGES") ? atoi(getenv("GH_GEMM_STAGES")) : 0;  // diagnostics
 static int cluster_override = 0;  // diagnostics
 
 template <int BN>
@@ -448,6 +448,7 @@ static int max_clusters(int C) {
     cudaGetLastError();
     n = kNumSMs / C;
   }
+  n = std::min(n, kNumSMs / C);  // persistent grid: at most one CTA of this kernel per SM
   cache[C] = n;
   return n;
 }
