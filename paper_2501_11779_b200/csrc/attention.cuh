@@ -131,7 +131,8 @@ __global__ void __launch_bounds__(AttnCfg<T, DH, W>::kThreads, 1)
   }
   __syncthreads();
   griddep_launch_dependents();
-  griddep_wait();  // the fwd message (and the arena of the previous step) are now visible
+  // griddepcontrol.wait (the fwd message, and the arena when a.kv_early == 0, are visible after
+  // it) is taken per role below: the producer may stream the first unit's cached keys first
 
   const T* fwd = (const T*)a.msg_fwd;
   T* bwd = (T*)a.msg_bwd;
@@ -147,6 +148,22 @@ __global__ void __launch_bounds__(AttnCfg<T, DH, W>::kThreads, 1)
       int u = blockIdx.x;
       int L = 0, sl = 0;
       if (u < n_units) { L = a.pos[u / a.H]; sl = (int)a.slot[u / a.H]; }
+      // early start: the first unit's cached K / V (independent of the predecessor) fill the
+      // free stages before griddepcontrol.wait; stage 0's arrive (with the header) comes after it
+      int pre = 0;
+      if (a.kv_early && u < n_units) {
+        const int kvh = (u % a.H) / group;
+        pre = min(L > 0 ? (L + C::kTpos - 1) / C::kTpos : 1, C::kStages);
+        for (int c = 0; c < pre; ++c) {
+          const int np = max(0, min(C::kTpos, L - c * C::kTpos));
+          const uint32_t bytes = (uint32_t)np * DH * sizeof(T);
+          uint8_t* sk = smem + c * C::kStageBytes;
+          if (c == 0) mbar_expect_tx(&full[0], 2 * bytes);
+          else mbar_arrive_expect_tx(&full[c], 2 * bytes);
+          if (np > 0) load_kv_chunk<T, DH>(a, arena, sl, kvh, c * C::kTpos, np, sk, sk + C::kTileBytes, &full[c], pol);
+        }
+      }
+      griddep_wait();
       while (u < n_units) {
         const int b = u / a.H, h = u % a.H, kvh = h / group;
         // next unit's position / slot, one unit ahead (hides the dependent global loads)
@@ -156,9 +173,11 @@ __global__ void __launch_bounds__(AttnCfg<T, DH, W>::kThreads, 1)
         const int nch = L > 0 ? (L + C::kTpos - 1) / C::kTpos : 1;
         for (int c = 0; c < nch; ++c, ++it) {
           const int s = it % C::kStages;
+          const bool issued = (int)it < pre;  // K / V already requested before the wait
+          if (issued && c > 0) continue;
           mbar_wait(&empty[s], ((it / C::kStages) & 1) ^ 1);
           const int np = max(0, min(C::kTpos, L - c * C::kTpos));
-          const uint32_t bytes = (uint32_t)np * DH * sizeof(T);
+          const uint32_t bytes = issued ? 0u : (uint32_t)np * DH * sizeof(T);
           uint8_t* sk = smem + s * C::kStageBytes;
           uint8_t* hdr = sk + 2 * C::kTileBytes;
           if (c == 0) {  // unit header: metadata (plain store, released by the arrive) + q/k/v/x copies
@@ -166,7 +185,8 @@ __global__ void __launch_bounds__(AttnCfg<T, DH, W>::kThreads, 1)
             meta[0] = L; meta[1] = b; meta[2] = h; meta[3] = sl;
           }
           mbar_arrive_expect_tx(&full[s], 2 * bytes + (c == 0 ? 4 * DH * (uint32_t)sizeof(T) : 0u));
-          if (np > 0) load_kv_chunk<T, DH>(a, arena, sl, kvh, c * C::kTpos, np, sk, sk + C::kTileBytes, &full[s], pol);
+          if (np > 0 && !issued)
+            load_kv_chunk<T, DH>(a, arena, sl, kvh, c * C::kTpos, np, sk, sk + C::kTileBytes, &full[s], pol);
           if (c == 0) {
             const T* row = fwd + (long)b * ld_fwd;
             bulk_g2s(hdr, row + a.D + (long)h * DH, DH * sizeof(T), &full[s], pol);
@@ -196,6 +216,7 @@ __global__ void __launch_bounds__(AttnCfg<T, DH, W>::kThreads, 1)
     // partial states of each unit (in unit order) and writes the output row, so that no consumer
     // warp falls behind the stage ring while merging
     if (a.flags & 3) return;
+    griddep_wait();
     for (int ui = 0;; ++ui) {
       const int cb = ui % C::kNB;
       while (*(volatile int*)&comb_cnt[cb] < C::kW) { }
@@ -233,6 +254,7 @@ __global__ void __launch_bounds__(AttnCfg<T, DH, W>::kThreads, 1)
   }
 
   // -------------------------------------------------- consumers
+  griddep_wait();  // they write the arena and the bwd message
   const int cw = warp - 1;
   const int grp = lane / C::kLpp;
   const int sub = lane % C::kLpp;

@@ -88,6 +88,9 @@ struct AttnArgs {
   // Dynamic unit schedule (nullptr = static stride gridDim.x): work[0] hands out units after each
   // CTA's first, work[1] counts finished producers; the last one zeroes both for the next launch.
   unsigned int* work;
+  // 1: the kernel's predecessor writes neither the arena nor pos / slot (the QKV GEMM or a stream
+  // wait), so the first unit's cached keys / values may be requested before griddepcontrol.wait
+  int kv_early;
 };
 // Positions per KV page of the paged arena (one 64-position TMA box / attention stage).
 constexpr int kKvPagePositions = 64;

@@ -311,7 +311,8 @@ gh_status gh_tier1_destroy(gh_tier1* t) {
 }  // extern "C"
 
 static gh_status t2_attend(gh_tier2* t, uint32_t layer, uint32_t B, const uint32_t* slot, const int32_t* pos,
-                           const void* msg_fwd, void* msg_bwd, void* stream, const void* pf, size_t pf_bytes);
+                           const void* msg_fwd, void* msg_bwd, void* stream, const void* pf, size_t pf_bytes,
+                           int kv_early = 0);
 
 // ---- Tier-1 stage implementations.  `SsRef` describes per-slice sums of squares of an
 // activation buffer emitted by its producer (embedding / W2 epilogue) so that the consumer GEMM
@@ -625,8 +626,10 @@ gh_status gh_tier2_attend(gh_tier2* t, uint32_t layer, uint32_t B, const uint32_
 
 // `pf`: leading bytes of the weight Tier-1 streams next on this GPU (colocated engine), prefetched
 // into L2 during the attention kernel's tail
+// `kv_early`: the caller guarantees the kernel's predecessor writes neither the arena nor pos / slot
 static gh_status t2_attend(gh_tier2* t, uint32_t layer, uint32_t B, const uint32_t* slot, const int32_t* pos,
-                           const void* msg_fwd, void* msg_bwd, void* stream, const void* pf, size_t pf_bytes) {
+                           const void* msg_fwd, void* msg_bwd, void* stream, const void* pf, size_t pf_bytes,
+                           int kv_early) {
   if (!t || !slot || !pos || !msg_fwd || !msg_bwd) return fail(GH_EINVAL, "null argument");
   if (layer < t->l0 || layer >= t->l1) return fail(GH_EINVAL, "layer not owned by this Tier-2");
   if (B == 0) return GH_OK;
@@ -648,6 +651,8 @@ static gh_status t2_attend(gh_tier2* t, uint32_t layer, uint32_t B, const uint32
   static const bool static_units = getenv("GH_ATTN_STATIC") != nullptr;  // diagnostics
   a.work = static_units ? nullptr : t->work + 2 * (t->work_next++ % gh_tier2::kWorkRing);
   a.kv_tmap = t->has_tmap ? &t->kv_tmap : nullptr;
+  static const bool no_early = getenv("GH_ATTN_NO_EARLY") != nullptr;  // diagnostics
+  a.kv_early = kv_early && !no_early;
   GH_CUDA(launch_attention(s.db, s.dh, a, (cudaStream_t)stream));
   return GH_OK;
 }
@@ -923,7 +928,9 @@ static gh_status engine_layer_loop_colocated(gh_engine* e, gh_engine::Batch& b, 
     GH_TRY(act_pre(e, b, l, st));
     const Weight& wo = e->t1->layers[l].o;
     if (e->cfg.prefill) GH_TRY(t2_append(e->t2, l, B, b.slot, b.pos, b.fwd, st));  // rows may share a prompt
-    GH_TRY(t2_attend(e->t2, l, B, b.slot, b.pos, b.fwd, b.bwd, st, wo.ptr, gh_tier1::prefetch_bytes(&wo)));
+    // predecessor: the QKV GEMM (or the append kernel with prefill rows, which writes the arena)
+    GH_TRY(t2_attend(e->t2, l, B, b.slot, b.pos, b.fwd, b.bwd, st, wo.ptr, gh_tier1::prefetch_bytes(&wo),
+                     e->cfg.prefill ? 0 : 1));
     GH_TRY(act_post(e, b, l, st));
   }
   return act_classify(e, b, want_logits ? b.logits : nullptr, st);
