@@ -276,6 +276,10 @@ gh_status gh_engine_kv_unmap(gh_engine* e, uint32_t slot);
  * With prefill != 0 several rows may name the same slot (consecutive positions of one prompt).
  * Synchronises the device. */
 gh_status gh_engine_set_slots(gh_engine* e, uint32_t ib, const uint32_t* slot_host);
+/* This rank's rows of every in-flight batch: a Tier-2 rank holds the KV of rows [off, off + cnt)
+ * (shard `index` of kp, gh_shard_plan) in its local slots ib * cnt + (row - off); other roles
+ * report index -1 and the whole batch.  kp = Tier-2 ranks per Tier-1 span (0 colocated). */
+gh_status gh_engine_shard(const gh_engine* e, int* index, uint32_t* off, uint32_t* cnt, uint32_t* kp);
 /* Launch count of this library's kernels since the last reset (device work accounting). */
 uint64_t gh_kernel_launches(int reset);
 

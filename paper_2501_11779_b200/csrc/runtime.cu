@@ -1068,6 +1068,16 @@ gh_status gh_engine_kv_map(gh_engine* e, uint32_t slot, uint32_t n_positions) {
   return gh_tier2_map(e->t2, slot, n_positions, nullptr);
 }
 
+gh_status gh_engine_shard(const gh_engine* e, int* index, uint32_t* off, uint32_t* cnt, uint32_t* kp) {
+  if (!e) return fail(GH_EINVAL, "null engine");
+  const bool t2 = e->role == 2;
+  if (index) *index = t2 ? e->shard : -1;
+  if (off) *off = t2 ? (uint32_t)e->shard_off[e->shard] : 0u;
+  if (cnt) *cnt = t2 ? (uint32_t)e->my_cnt : e->cfg.batch;
+  if (kp) *kp = (uint32_t)e->kp;
+  return GH_OK;
+}
+
 gh_status gh_engine_set_slots(gh_engine* e, uint32_t ib, const uint32_t* slot_host) {
   if (!e || !slot_host || ib >= e->batches.size()) return fail(GH_EINVAL, "bad engine / batch index / slots");
   if (e->role != 0) return fail(GH_EUNSUPPORTED, "per-row slots: colocated engine only");

@@ -216,6 +216,13 @@ class Engine:
     def kv_unmap(self, slot: int):
         L.check(L.lib().gh_engine_kv_unmap(self.h, slot))
 
+    def shard(self):
+        """(index, row offset, row count, K'): the rows whose KV this rank holds (Tier-2), or
+        (-1, 0, batch, K') for Tier-1 / colocated ranks."""
+        i, o, c, k = C.c_int(), C.c_uint32(), C.c_uint32(), C.c_uint32()
+        L.check(L.lib().gh_engine_shard(self.h, C.byref(i), C.byref(o), C.byref(c), C.byref(k)))
+        return i.value, o.value, c.value, k.value
+
     def set_slots(self, slots, ib=0):
         """Context slot of every row of in-flight batch ib (colocated)."""
         s = np.ascontiguousarray(slots, dtype=np.uint32)
@@ -302,15 +309,57 @@ class ContinuousDispatcher:
 
     With a paged KV arena (Engine(kv_pages=...)) a request maps exactly the positions it will
     attend (prompt + max_new - 1) when it is admitted and returns its pages when it finishes; a
-    request waits in the queue (its lane idles on one page) until the pool can back it."""
+    request waits in the queue (its lane idles on one page) until its lane's pool can back it.
+
+    Tier split: every rank runs the same dispatcher over the same requests (SPMD).  Admission
+    depends only on prompt lengths, max_new and the page accounting (kept here for every Tier-2
+    shard), never on token values, so all ranks take identical decisions; a Tier-2 rank maps the
+    pages of the lanes in its shard and steps with no host tokens, and only Tier-1 sees tokens."""
+
+    PAGE = 64  # GH_KV_PAGE_POSITIONS
 
     def __init__(self, engine: Engine):
         self.engine = engine
 
     def run(self, requests, max_new: int):
         """requests: sequence of 1-D int32 prompt arrays (any lengths >= 1).  Returns the list of
-        generated token arrays (max_new each), in request order, and the number of steps."""
-        B = self.engine.batch
+        generated token arrays (max_new each, in request order; zeros on Tier-2 ranks) and the
+        number of steps."""
+        eng = self.engine
+        B = eng.batch
+        role = eng.role
+        index, off, cnt, kp = eng.shard()
+        # lane -> shard (the rows of each Tier-2 rank, analytic.cpp:119) and per-shard page pools
+        if kp:
+            from .spec import shard_plan
+            offs, cnts = shard_plan(B, kp)
+            lane_shard = np.repeat(np.arange(kp), cnts)
+        else:
+            lane_shard = np.zeros(B, np.int64)
+        paged = eng.kv_pages > 0
+        free = [eng.kv_pages] * max(1, kp)
+        mapped = [0] * B                  # pages held by each lane
+
+        def pages(n):
+            return -(-n // self.PAGE)
+
+        def kv_unmap(lane):
+            free[lane_shard[lane]] += mapped[lane]
+            mapped[lane] = 0
+            if role != "tier1" and off <= lane < off + cnt:
+                eng.kv_unmap(lane - off)
+
+        def kv_map(lane, n):              # False when the lane's pool cannot back n positions
+            need = pages(n) - mapped[lane] if paged else 0
+            if need > free[lane_shard[lane]]:
+                return False
+            if role != "tier1" and off <= lane < off + cnt:
+                eng.kv_map(lane - off, n)
+            if need > 0:
+                free[lane_shard[lane]] -= need
+                mapped[lane] += need
+            return True
+
         queue = list(range(len(requests)))
         lane_req = [-1] * B           # request index in each lane
         lane_t = [0] * B              # position of the lane's next input token
@@ -319,28 +368,26 @@ class ContinuousDispatcher:
         pos = np.zeros(B, np.int32)
 
         def admit(lane):
-            self.engine.kv_unmap(lane)
+            kv_unmap(lane)
             lane_req[lane] = -1
             tok[lane] = 0
             pos[lane] = 0
-            if queue:
-                r = queue[0]
-                try:
-                    self.engine.kv_map(lane, len(requests[r]) + max_new - 1)
-                except L.FeasibilityError:  # page pool short: the request waits
-                    pass
-                else:
-                    queue.pop(0)
-                    lane_req[lane], lane_t[lane] = r, 0
-                    tok[lane] = int(requests[r][0])
-            if lane_req[lane] < 0:
-                self.engine.kv_map(lane, 1)  # the idle lane's dummy token
+            if queue and kv_map(lane, len(requests[queue[0]]) + max_new - 1):
+                r = queue.pop(0)
+                lane_req[lane], lane_t[lane] = r, 0
+                tok[lane] = int(requests[r][0])
+            if lane_req[lane] < 0 and not kv_map(lane, 1):  # the idle lane's dummy token
+                raise L.FeasibilityError(L.GH_EINFEASIBLE, "KV page pool smaller than one page per lane")
 
         for lane in range(B):
             admit(lane)
         steps = 0
         while any(r >= 0 for r in lane_req):
-            nxt, _ = self.engine.step_host(tok, pos)
+            if role == "tier2":
+                eng.step_host(None, None)
+                nxt = np.zeros(B, np.int32)
+            else:
+                nxt, _ = eng.step_host(tok, pos)
             steps += 1
             for lane in range(B):
                 r = lane_req[lane]
@@ -361,7 +408,7 @@ class ContinuousDispatcher:
                     admit(lane)       # the lane's slot goes to the next request
             if queue and all(r < 0 for r in lane_req):
                 for lane in range(B):  # every lane idle: offer the whole pool
-                    self.engine.kv_unmap(lane)
+                    kv_unmap(lane)
                 for lane in range(B):
                     admit(lane)
         if queue:
@@ -384,6 +431,8 @@ class MixedDispatcher:
     def __init__(self, engine: Engine, chunk: int = 16):
         if not engine.prefill:
             raise L.ValidationError(L.GH_EINVAL, "MixedDispatcher needs Engine(prefill=True)")
+        if engine.role != "colocated":
+            raise L.UnsupportedError(L.GH_EUNSUPPORTED, "MixedDispatcher: colocated engine only")
         if engine.n_slots < 2:
             raise L.ValidationError(L.GH_EINVAL, "MixedDispatcher needs n_slots >= 2 (one scratch slot)")
         self.engine, self.chunk = engine, chunk

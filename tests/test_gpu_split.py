@@ -216,3 +216,67 @@ def test_tier1_pipeline_stages_match_colocated():
         assert p.exitcode == 0
     ref = run_all(Engine(SPEC, batch=B, inflight=IF, use_graph=False), IF)
     assert np.array_equal(got, ref)
+
+
+PSPEC = gh.ModelSpec("split-paged", 2, 512, 512, 1024, 4, 4, 256, 2, 1500)
+PLENS = [3, 70, 1, 33, 129, 12, 64, 65, 8, 20, 100, 2]
+PNEW = 5
+PB = 6
+
+
+def paged_requests():
+    rng = np.random.default_rng(17)
+    return [rng.integers(0, PSPEC.vocab_size, size=n, dtype=np.int32) for n in PLENS]
+
+
+def worker_paged(rank, world, port, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    import torch
+    import torch.distributed as dist
+    from paper_2501_11779_b200.stages import Comm, ContinuousDispatcher, Engine
+    torch.cuda.set_device(rank)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    obj = [Comm.unique_ids(1) if rank == 0 else None]
+    dist.broadcast_object_list(obj, src=0)
+    comm = Comm(obj[0], world, rank, rank)
+    eng = Engine(PSPEC, batch=PB, device=rank, use_graph=False, comm=comm, kv_pages=7)
+    out, steps = ContinuousDispatcher(eng).run(paged_requests(), PNEW)
+    eng.close()
+    comm.close()
+    if rank == 0:
+        q.put((out, steps))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.skipif(n_gpus() < 2, reason="needs >= 2 GPUs")
+@pytest.mark.parametrize("world", [2, 3])
+def test_continuous_batching_paged_tier_split(world):
+    """Continuous batching on paged Tier-2 ranks (SURVEY 8f-2 in the tier split): every rank
+    runs the dispatcher SPMD; each Tier-2 rank maps its own shard's lanes from a pool smaller
+    than its lanes x max_seq_len, so requests wait for pages.  Tokens identical to the colocated
+    engine with contiguous slots."""
+    if n_gpus() < world:
+        pytest.skip(f"needs {world} GPUs")
+    import torch.multiprocessing as mp
+    from paper_2501_11779_b200.stages import ContinuousDispatcher, Engine
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=worker_paged, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    got, steps = q.get(timeout=600)
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    ref = Engine(PSPEC, batch=PB, use_graph=False)
+    want, ref_steps = ContinuousDispatcher(ref).run(paged_requests(), PNEW)
+    ref.close()
+    for w, g in zip(want, got):
+        assert np.array_equal(w, g)
+    if world == 2:
+        assert steps > ref_steps  # one Tier-2 pool of 7 pages for 6 lanes: requests waited
