@@ -351,7 +351,10 @@ class ContinuousDispatcher:
 
         def kv_map(lane, n):              # False when the lane's pool cannot back n positions
             need = pages(n) - mapped[lane] if paged else 0
-            if need > free[lane_shard[lane]]:
+            sh = lane_shard[lane]
+            # keep one page for every other lane of the shard that holds none (its dummy token)
+            empty = sum(1 for o in range(B) if o != lane and lane_shard[o] == sh and mapped[o] == 0) if paged else 0
+            if need > free[sh] - empty:
                 return False
             if role != "tier1" and off <= lane < off + cnt:
                 eng.kv_map(lane - off, n)

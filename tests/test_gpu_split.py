@@ -239,8 +239,11 @@ def worker_paged(rank, world, port, q):
     obj = [Comm.unique_ids(1) if rank == 0 else None]
     dist.broadcast_object_list(obj, src=0)
     comm = Comm(obj[0], world, rank, rank)
-    eng = Engine(PSPEC, batch=PB, device=rank, use_graph=False, comm=comm, kv_pages=7)
-    out, steps = ContinuousDispatcher(eng).run(paged_requests(), PNEW)
+    eng = Engine(PSPEC, batch=PB, device=rank, use_graph=False, comm=comm, kv_pages=8)
+    try:
+        out, steps = ContinuousDispatcher(eng).run(paged_requests(), PNEW)
+    except Exception as e:  # every rank takes the same decisions: report instead of hanging
+        out, steps = repr(e), -1
     eng.close()
     comm.close()
     if rank == 0:
@@ -269,14 +272,15 @@ def test_continuous_batching_paged_tier_split(world):
     procs = [ctx.Process(target=worker_paged, args=(r, world, port, q)) for r in range(world)]
     for p in procs:
         p.start()
-    got, steps = q.get(timeout=600)
+    got, steps = q.get(timeout=300)
     for p in procs:
         p.join(timeout=120)
         assert p.exitcode == 0
+    assert steps >= 0, got
     ref = Engine(PSPEC, batch=PB, use_graph=False)
     want, ref_steps = ContinuousDispatcher(ref).run(paged_requests(), PNEW)
     ref.close()
     for w, g in zip(want, got):
         assert np.array_equal(w, g)
     if world == 2:
-        assert steps > ref_steps  # one Tier-2 pool of 7 pages for 6 lanes: requests waited
+        assert steps > ref_steps  # one Tier-2 pool of 8 pages for 6 lanes: requests waited
