@@ -219,7 +219,8 @@ __global__ void __launch_bounds__(AttnCfg<T, DH, W>::kThreads, 1)
     griddep_wait();
     for (int ui = 0;; ++ui) {
       const int cb = ui % C::kNB;
-      while (*(volatile int*)&comb_cnt[cb] < C::kW) { }
+      while (*(volatile int*)&comb_cnt[cb] < C::kW)
+        if (!(a.flags & 8)) __nanosleep(32);  // idle most of the time: back off (8: diagnostics, spin)
       __threadfence_block();
       const float* cbuf = comb + cb * C::kW * (DH + 2);
       const int b = comb_bh[2 * cb], h = comb_bh[2 * cb + 1];

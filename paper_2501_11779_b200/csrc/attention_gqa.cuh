@@ -524,7 +524,8 @@ __global__ void __launch_bounds__(GqaTcCfg<G>::kThreads, 1)
     // consumer states and the new token's state of every query head, writes the G output rows
     for (int ui = 0;; ++ui) {
       const int cb = ui % C::kNB;
-      while (*(volatile int*)&comb_cnt[cb] < C::kW) { }
+      while (*(volatile int*)&comb_cnt[cb] < C::kW)
+        if (!(a.flags & 8)) __nanosleep(32);  // idle most of the time: back off (8: diagnostics, spin)
       __threadfence_block();
       const float* cbuf = comb + cb * C::kCombPerUnit;
       const int b = comb_bg[2 * cb], g = comb_bg[2 * cb + 1];

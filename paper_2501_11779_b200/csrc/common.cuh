@@ -198,9 +198,11 @@ GH_DEV void cluster_sync_all() {
 // spin (acquire, gpu scope) until *flag >= target
 GH_DEV void flag_wait(const unsigned int* flag, unsigned int target) {
   unsigned int v;
-  do {
+  for (;;) {
     asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(flag) : "memory");
-  } while (v < target);
+    if (v >= target) break;
+    __nanosleep(64);  // polls go to L2: back off
+  }
 }
 
 // ------------------------------------------------------------------ bulk / tensor copies (TMA)
