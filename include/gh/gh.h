@@ -138,6 +138,11 @@ gh_status gh_tier1_post(gh_tier1* t1, uint32_t layer, uint32_t B, const void* ms
  * logits (optional, device fp32 [B, V]); next_tok device int32 [B]. */
 gh_status gh_tier1_classify(gh_tier1* t1, uint32_t B, const void* x, float* logits,
                             int32_t* next_tok, void* stream);
+/* Classifier with temperature sampling: inv_temperature [B] device fp32 (1/T, 0 = greedy row),
+ * seed [B] device uint32, pos [B] device int32 (the position of the token being decoded). */
+gh_status gh_tier1_classify_sample(gh_tier1* t1, uint32_t B, const void* x, const int32_t* pos,
+                                   const float* inv_temperature, const uint32_t* seed, float* logits,
+                                   int32_t* next_tok, void* stream);
 
 /* ------------------------------------------------------------------ Tier-2 (KV context; F2)
  * KV arena for layers [layer_begin, layer_end) and n_slots prompts at max_seq_len:
@@ -276,6 +281,12 @@ gh_status gh_engine_kv_unmap(gh_engine* e, uint32_t slot);
  * With prefill != 0 several rows may name the same slot (consecutive positions of one prompt).
  * Synchronises the device. */
 gh_status gh_engine_set_slots(gh_engine* e, uint32_t ib, const uint32_t* slot_host);
+/* Per-row sampling of in-flight batch ib (batch state "temperature"): temperature 0 =
+ * greedy (the default), > 0 = sample from softmax(logits / T) by the Gumbel-max rule with noise
+ * from (seed, position, token id) -- deterministic and reproducible on the host
+ * (oracle/sampling.py).  Synchronises the device; Tier-2 ranks ignore it. */
+gh_status gh_engine_set_sampling(gh_engine* e, uint32_t ib, const float* temperature_host,
+                                 const uint32_t* seed_host);
 /* This rank's rows of every in-flight batch: a Tier-2 rank holds the KV of rows [off, off + cnt)
  * (shard `index` of kp, gh_shard_plan) in its local slots ib * cnt + (row - off); other roles
  * report index -1 and the whole batch.  kp = Tier-2 ranks per Tier-1 span (0 colocated). */

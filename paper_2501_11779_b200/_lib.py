@@ -130,6 +130,8 @@ PROTOTYPES = {
     "gh_engine_kv_unmap": (st, [vp, u32]),
     "gh_engine_set_slots": (st, [vp, u32, P(u32)]),
     "gh_engine_shard": (st, [vp, P(C.c_int), P(u32), P(u32), P(u32)]),
+    "gh_engine_set_sampling": (st, [vp, u32, P(C.c_float), P(u32)]),
+    "gh_tier1_classify_sample": (st, [vp, u32, vp, vp, vp, vp, vp, vp, vp]),
     "gh_kernel_launches": (u64, [C.c_int]),
     "gh_debug_gemm_bench": (st, [C.c_int] * 7 + [P(C.c_float)]),
     "gh_debug_gemm_trace": (st, [C.c_int] * 5 + [P(C.c_float), P(C.c_uint64), C.c_int]),

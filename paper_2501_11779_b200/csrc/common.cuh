@@ -17,6 +17,26 @@ constexpr int kNumSMs = 148;
 // fp32 storage (C1 tiny model) or bf16 storage (7B/13B/70B shapes).  Compute is fp32.
 struct bf16_t { uint16_t bits; };
 
+// ---- temperature sampling (Gumbel-max): token = argmax_r(logit_r / T + g_r), g_r = -log(-log(u_r))
+// with u_r a counter-based uniform of (seed, position, r); T = 0 rows stay greedy.  The scores
+// use separately rounded fp32 multiply / add and the noise is computed in double and rounded
+// once, so a numpy restatement (oracle/sampling.py) reproduces every decision bit for bit.
+GH_HD uint64_t splitmix64(uint64_t x) {
+  x += 0x9E3779B97F4A7C15ull;
+  x = (x ^ (x >> 30)) * 0xBF58476D1CE4E5B9ull;
+  x = (x ^ (x >> 27)) * 0x94D049BB133111EBull;
+  return x ^ (x >> 31);
+}
+GH_HD uint64_t sample_key(uint32_t seed, int pos) { return splitmix64(((uint64_t)seed << 32) | (uint32_t)pos); }
+GH_DEV float gumbel_noise(uint64_t key, int r) {
+  const uint64_t h = splitmix64(key + (uint64_t)r);
+  const double u = ((double)(h >> 11) + 0.5) * 0x1p-53;
+  return (float)(-log(-log(u)));
+}
+GH_DEV float sample_score(float logit, float inv_t, uint64_t key, int r) {
+  return __fadd_rn(__fmul_rn(logit, inv_t), gumbel_noise(key, r));
+}
+
 GH_HD float bf16_to_f32(uint16_t b) {
   union { uint32_t u; float f; } v; v.u = (uint32_t)b << 16; return v.f;
 }

@@ -304,13 +304,20 @@ __global__ void argmax_final_kernel(const float2* part, int n_tiles, int B, int3
     next[b] = idx;
   }
 }
-__global__ void argmax_rows_kernel(const float* logits, int V, int32_t* next) {
+__global__ void argmax_rows_kernel(const float* logits, int V, int32_t* next, const float* inv_temp,
+                                   const uint32_t* seed, const int* pos) {
   const int b = blockIdx.x;
   griddep_launch_dependents();
   griddep_wait();
   const float* r = logits + (long)b * V;
   float v = -INFINITY; int idx = 0x7fffffff;
-  for (int i = threadIdx.x; i < V; i += blockDim.x) argmax_merge(v, idx, r[i], i);
+  const float it = inv_temp ? inv_temp[b] : 0.f;
+  if (it > 0.f) {  // temperature sampling (common.cuh)
+    const uint64_t key = sample_key(seed[b], pos[b]);
+    for (int i = threadIdx.x; i < V; i += blockDim.x) argmax_merge(v, idx, sample_score(r[i], it, key, i), i);
+  } else {
+    for (int i = threadIdx.x; i < V; i += blockDim.x) argmax_merge(v, idx, r[i], i);
+  }
   __shared__ float sv[32]; __shared__ int si[32];
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1)
@@ -325,8 +332,9 @@ __global__ void argmax_rows_kernel(const float* logits, int V, int32_t* next) {
 cudaError_t launch_argmax_final(const float2* part, int n_tiles, int B, int32_t* next, cudaStream_t st) {
   return launch_pdl(argmax_final_kernel, B, 256, 0, st, part, n_tiles, B, next);
 }
-cudaError_t launch_argmax_rows(const float* logits, int B, int V, int32_t* next, cudaStream_t st) {
-  return launch_pdl(argmax_rows_kernel, B, 256, 0, st, logits, V, next);
+cudaError_t launch_argmax_rows(const float* logits, int B, int V, int32_t* next, cudaStream_t st,
+                               const float* inv_temp, const uint32_t* seed, const int* pos) {
+  return launch_pdl(argmax_rows_kernel, B, 256, 0, st, logits, V, next, inv_temp, seed, pos);
 }
 
 // ====================================================================== batch state

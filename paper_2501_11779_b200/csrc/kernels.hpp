@@ -89,8 +89,10 @@ cudaError_t launch_embed(int dtype_bytes, const void* table, const int32_t* tok,
                          int D, int V, float* ss, cudaStream_t st);
 cudaError_t launch_argmax_final(const float2* part, int n_tiles, int B, int32_t* next_tok,
                                 cudaStream_t st);
+// (inv_temp / seed / pos: temperature sampling per row, common.cuh; nullptr = greedy)
 cudaError_t launch_argmax_rows(const float* logits, int B, int V, int32_t* next_tok,
-                               cudaStream_t st);
+                               cudaStream_t st, const float* inv_temp = nullptr,
+                               const uint32_t* seed = nullptr, const int* pos = nullptr);
 
 struct AttnArgs;
 cudaError_t launch_attention(int dtype_bytes, int d_head, const AttnArgs& a, cudaStream_t st);

@@ -404,8 +404,11 @@ static gh_status t1_post(gh_tier1* t, uint32_t layer, uint32_t B, const void* ms
   return t->gemm(L.w2, &L.tm_2, t->g, s.Dh, (int)B, ep, st, next);
 }
 
+// Sampling (all three may be null = greedy): inv_temp [B] (0 = greedy row), seed [B], pos [B].
 static gh_status t1_classify(gh_tier1* t, uint32_t B, const void* x, SsRef ss, float* logits, int32_t* next,
-                             cudaStream_t st) {
+                             cudaStream_t st, const float* inv_temp = nullptr, const uint32_t* seed = nullptr,
+                             const int32_t* pos = nullptr) {
+  if (inv_temp && (!seed || !pos)) return fail(GH_EINVAL, "sampling needs seed and pos");
   if (!t || !x || !next) return fail(GH_EINVAL, "null argument");
   if (!t->has_cls) return fail(GH_EINVAL, "this Tier-1 span does not own the classifier");
   if (B > t->max_batch) return fail(GH_EINVAL, "B exceeds max_batch");
@@ -415,6 +418,7 @@ static gh_status t1_classify(gh_tier1* t, uint32_t B, const void* x, SsRef ss, f
   ep.kind = EPI_LOGITS_ARGMAX;
   ep.logits = logits; ep.ldl = s.V;
   ep.part = t->part;
+  ep.inv_temp = inv_temp; ep.seed = seed; ep.pos = pos;
   const void* in = x;
   if (s.db == 2 && ss.ss && B <= (uint32_t)kFusedNormMaxBatch) {
     ep.ss_in = ss.ss; ep.ss_in_slices = ss.slices; ep.ss_dim = s.D; ep.ss_eps = s.s.norm_eps;
@@ -426,12 +430,18 @@ static gh_status t1_classify(gh_tier1* t, uint32_t B, const void* x, SsRef ss, f
   if (s.db == 2) {
     GH_CUDA(launch_argmax_final(t->part, t->plan(s.V, s.D, (int)B).slices(), (int)B, next, st));
   } else {
-    GH_CUDA(launch_argmax_rows(logits ? logits : t->gsc.stage, (int)B, s.V, next, st));
+    GH_CUDA(launch_argmax_rows(logits ? logits : t->gsc.stage, (int)B, s.V, next, st, inv_temp, seed, pos));
   }
   return GH_OK;
 }
 
 extern "C" {
+
+gh_status gh_tier1_classify_sample(gh_tier1* t, uint32_t B, const void* x, const int32_t* pos,
+                                   const float* inv_temperature, const uint32_t* seed, float* logits,
+                                   int32_t* next_tok, void* stream) {
+  return t1_classify(t, B, x, SsRef{}, logits, next_tok, (cudaStream_t)stream, inv_temperature, seed, pos);
+}
 
 gh_status gh_tier1_embed(gh_tier1* t, uint32_t B, const int32_t* tok, void* x, void* stream) {
   return t1_embed(t, B, tok, x, nullptr, (cudaStream_t)stream);
@@ -839,6 +849,8 @@ struct gh_engine {
     int32_t *tok = nullptr, *pos = nullptr, *next = nullptr;
     uint32_t* slot = nullptr;
     std::vector<uint32_t> slot_host;       // host copy of `slot` (admission checks)
+    float* inv_temp = nullptr;             // [R] 1 / temperature per row (0 = greedy), sampling
+    uint32_t* seed = nullptr;              // [R] sampling seed per row
     void *x0 = nullptr, *x1 = nullptr, *fwd = nullptr, *bwd = nullptr;
     float *ss0 = nullptr, *ss1 = nullptr;  // per-slice sums of squares of x0 / x1 (fused RMSNorm)
     int ss_slices[2] = {0, 0};
@@ -912,7 +924,8 @@ static gh_status act_post(gh_engine* e, gh_engine::Batch& b, int l, cudaStream_t
   return GH_OK;
 }
 static gh_status act_classify(gh_engine* e, gh_engine::Batch& b, float* logits, cudaStream_t st) {
-  return t1_classify(e->t1, e->cfg.batch, b.x(b.cur), SsRef{b.ss(b.cur), b.ss_slices[b.cur]}, logits, b.next, st);
+  return t1_classify(e->t1, e->cfg.batch, b.x(b.cur), SsRef{b.ss(b.cur), b.ss_slices[b.cur]}, logits, b.next, st,
+                     b.inv_temp, b.seed, b.pos);
 }
 
 extern "C" {
@@ -1000,6 +1013,10 @@ gh_status gh_engine_create(const gh_engine_config* cfg, gh_comm* comm, gh_engine
     GH_TRY(dev_alloc(e->mem, (size_t)R * 4, &p)); b.pos = (int32_t*)p;
     GH_TRY(dev_alloc(e->mem, (size_t)R * 4, &p)); b.next = (int32_t*)p;
     GH_TRY(dev_alloc(e->mem, (size_t)R * 4, &p)); b.slot = (uint32_t*)p;
+    GH_TRY(dev_alloc(e->mem, (size_t)R * 4, &p)); b.inv_temp = (float*)p;
+    GH_CUDA(cudaMemset(p, 0, (size_t)R * 4));  // greedy until gh_engine_set_sampling
+    GH_TRY(dev_alloc(e->mem, (size_t)R * 4, &p)); b.seed = (uint32_t*)p;
+    GH_CUDA(cudaMemset(p, 0, (size_t)R * 4));
     GH_TRY(dev_alloc(e->mem, (size_t)R * s.D * s.db, &b.x0));
     GH_TRY(dev_alloc(e->mem, (size_t)R * s.D * s.db, &b.x1));
     GH_TRY(dev_alloc(e->mem, (size_t)R * s.ld_fwd() * s.db, &b.fwd));
@@ -1066,6 +1083,24 @@ gh_status gh_engine_kv_map(gh_engine* e, uint32_t slot, uint32_t n_positions) {
   if (!e) return fail(GH_EINVAL, "null engine");
   if (!e->t2) return fail(GH_EUNSUPPORTED, "this rank holds no KV (Tier-1 role)");
   return gh_tier2_map(e->t2, slot, n_positions, nullptr);
+}
+
+gh_status gh_engine_set_sampling(gh_engine* e, uint32_t ib, const float* temperature_host, const uint32_t* seed_host) {
+  if (!e || ib >= e->batches.size()) return fail(GH_EINVAL, "bad engine / batch index");
+  if (e->role == 2) return GH_OK;  // Tier-2 ranks do not classify
+  if (!temperature_host || !seed_host) return fail(GH_EINVAL, "null temperature / seed");
+  auto& b = e->batches[ib];
+  const int R = e->rows();
+  std::vector<float> inv(R);
+  for (int i = 0; i < R; ++i) {
+    if (!(temperature_host[i] >= 0.f)) return fail(GH_EINVAL, "temperature must be >= 0");
+    inv[i] = temperature_host[i] > 0.f ? 1.0f / temperature_host[i] : 0.f;
+  }
+  GH_CUDA(cudaSetDevice(e->cfg.device));
+  GH_CUDA(cudaDeviceSynchronize());  // no step in flight reads the old values
+  GH_CUDA(cudaMemcpy(b.inv_temp, inv.data(), (size_t)R * 4, cudaMemcpyHostToDevice));
+  GH_CUDA(cudaMemcpy(b.seed, seed_host, (size_t)R * 4, cudaMemcpyHostToDevice));
+  return GH_OK;
 }
 
 gh_status gh_engine_shard(const gh_engine* e, int* index, uint32_t* off, uint32_t* cnt, uint32_t* kp) {

@@ -216,6 +216,13 @@ class Engine:
     def kv_unmap(self, slot: int):
         L.check(L.lib().gh_engine_kv_unmap(self.h, slot))
 
+    def set_sampling(self, temperature, seed, ib=0):
+        """Per-row temperature (0 = greedy) and seed of in-flight batch ib."""
+        t = np.ascontiguousarray(temperature, dtype=np.float32)
+        sd = np.ascontiguousarray(seed, dtype=np.uint32)
+        L.check(L.lib().gh_engine_set_sampling(self.h, ib, t.ctypes.data_as(C.POINTER(C.c_float)),
+                                               sd.ctypes.data_as(C.POINTER(C.c_uint32))))
+
     def shard(self):
         """(index, row offset, row count, K'): the rows whose KV this rank holds (Tier-2), or
         (-1, 0, batch, K') for Tier-1 / colocated ranks."""
