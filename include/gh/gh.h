@@ -139,7 +139,8 @@ gh_status gh_tier1_post(gh_tier1* t1, uint32_t layer, uint32_t B, const void* ms
 gh_status gh_tier1_classify(gh_tier1* t1, uint32_t B, const void* x, float* logits,
                             int32_t* next_tok, void* stream);
 /* Classifier with temperature sampling: inv_temperature [B] device fp32 (1/T, 0 = greedy row),
- * seed [B] device uint32, pos [B] device int32 (the position of the token being decoded). */
+ * seed [B] device uint32, pos [B] device int32 (the position of the token being decoded);
+ * logits (required, device fp32 [B, V]) receive the logits the sampler reads. */
 gh_status gh_tier1_classify_sample(gh_tier1* t1, uint32_t B, const void* x, const int32_t* pos,
                                    const float* inv_temperature, const uint32_t* seed, float* logits,
                                    int32_t* next_tok, void* stream);

@@ -17,7 +17,8 @@ constexpr int kNumSMs = 148;
 // fp32 storage (C1 tiny model) or bf16 storage (7B/13B/70B shapes).  Compute is fp32.
 struct bf16_t { uint16_t bits; };
 
-// ---- temperature sampling (Gumbel-max): token = argmax_r(logit_r / T + g_r), g_r = -log(-log(u_r))
+// ---- temperature sampling (Gumbel-max, argmax_rows_kernel over the written logits):
+// token = argmax_r(logit_r / T + g_r), g_r = -log(-log(u_r))
 // with u_r a counter-based uniform of (seed, position, r); T = 0 rows stay greedy.  The scores
 // use separately rounded fp32 multiply / add and the noise is computed in double and rounded
 // once, so a numpy restatement (oracle/sampling.py) reproduces every decision bit for bit.

@@ -346,21 +346,10 @@ GH_DEV void epi_slice(const EpiParams& ep, const GemmShape& gs, int n, int b, fl
       // EPI_LOGITS_ARGMAX: logits (optional) and (max, argmax) over the slice per column b
       float best = -INFINITY;
       int bi = 0x7fffffff;
-      const float it = (ep.inv_temp && col_ok) ? ep.inv_temp[b] : 0.f;
-      if (it > 0.f) {  // temperature sampling: argmax of the Gumbel-perturbed scores
-        const uint64_t key = sample_key(ep.seed[b], ep.pos[b]);
 #pragma unroll
-        for (int e = 0; e < En; ++e) {
-          const int r = n + off(e);
-          const float sc = sample_score(v[e], it, key, r);
-          if (r < gs.N && (sc > best || (sc == best && r < bi))) { best = sc; bi = r; }
-        }
-      } else {
-#pragma unroll
-        for (int e = 0; e < En; ++e) {
-          const int r = n + off(e);
-          if (r < gs.N && (v[e] > best || (v[e] == best && r < bi))) { best = v[e]; bi = r; }
-        }
+      for (int e = 0; e < En; ++e) {
+        const int r = n + off(e);
+        if (r < gs.N && (v[e] > best || (v[e] == best && r < bi))) { best = v[e]; bi = r; }
       }
       if (ep.logits && col_ok) {
         float* lp = ep.logits + (long)b * ep.ldl + n;

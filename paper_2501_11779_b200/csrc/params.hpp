@@ -26,10 +26,6 @@ struct EpiParams {
   float* logits;        // [B][ldl] fp32 (optional)
   long ldl;
   float2* part;         // [n_tiles * C][Bt] (max value, argmax index as float bits); C = cluster size
-  // LOGITS_ARGMAX sampling (nullptr = greedy): per column 1/T (0 = greedy) and seed; the
-  // position comes from `pos`
-  const float* inv_temp;
-  const uint32_t* seed;
   // fused RMSNorm (bf16 tcgen05 path): the GEMM input X is the raw activation; column b of the
   // accumulator is scaled by 1/sqrt(sum_s ss_in[s][b] / ss_dim + ss_eps) (norm weight folded
   // into W).  ss_in holds per-slice sums of squares written by the producer of X.

@@ -408,7 +408,7 @@ static gh_status t1_post(gh_tier1* t, uint32_t layer, uint32_t B, const void* ms
 static gh_status t1_classify(gh_tier1* t, uint32_t B, const void* x, SsRef ss, float* logits, int32_t* next,
                              cudaStream_t st, const float* inv_temp = nullptr, const uint32_t* seed = nullptr,
                              const int32_t* pos = nullptr) {
-  if (inv_temp && (!seed || !pos)) return fail(GH_EINVAL, "sampling needs seed and pos");
+  if (inv_temp && (!seed || !pos || !logits)) return fail(GH_EINVAL, "sampling needs seed, pos and a logits buffer");
   if (!t || !x || !next) return fail(GH_EINVAL, "null argument");
   if (!t->has_cls) return fail(GH_EINVAL, "this Tier-1 span does not own the classifier");
   if (B > t->max_batch) return fail(GH_EINVAL, "B exceeds max_batch");
@@ -418,7 +418,6 @@ static gh_status t1_classify(gh_tier1* t, uint32_t B, const void* x, SsRef ss, f
   ep.kind = EPI_LOGITS_ARGMAX;
   ep.logits = logits; ep.ldl = s.V;
   ep.part = t->part;
-  ep.inv_temp = inv_temp; ep.seed = seed; ep.pos = pos;
   const void* in = x;
   if (s.db == 2 && ss.ss && B <= (uint32_t)kFusedNormMaxBatch) {
     ep.ss_in = ss.ss; ep.ss_in_slices = ss.slices; ep.ss_dim = s.D; ep.ss_eps = s.s.norm_eps;
@@ -427,7 +426,9 @@ static gh_status t1_classify(gh_tier1* t, uint32_t B, const void* x, SsRef ss, f
     in = t->xn;
   }
   GH_TRY(t->gemm(t->cls, &t->tm_cls, in, s.D, (int)B, ep, st, t->l1 > t->l0 ? &t->layers[0].qkv : nullptr));
-  if (s.db == 2) {
+  if (inv_temp) {  // temperature sampling over the written logits (keeps the GEMM epilogue lean)
+    GH_CUDA(launch_argmax_rows(logits, (int)B, s.V, next, st, inv_temp, seed, pos));
+  } else if (s.db == 2) {
     GH_CUDA(launch_argmax_final(t->part, t->plan(s.V, s.D, (int)B).slices(), (int)B, next, st));
   } else {
     GH_CUDA(launch_argmax_rows(logits ? logits : t->gsc.stage, (int)B, s.V, next, st, inv_temp, seed, pos));
@@ -851,6 +852,7 @@ struct gh_engine {
     std::vector<uint32_t> slot_host;       // host copy of `slot` (admission checks)
     float* inv_temp = nullptr;             // [R] 1 / temperature per row (0 = greedy), sampling
     uint32_t* seed = nullptr;              // [R] sampling seed per row
+    bool sampling = false;                 // some row has T > 0 (classifier path; graph recaptured on change)
     void *x0 = nullptr, *x1 = nullptr, *fwd = nullptr, *bwd = nullptr;
     float *ss0 = nullptr, *ss1 = nullptr;  // per-slice sums of squares of x0 / x1 (fused RMSNorm)
     int ss_slices[2] = {0, 0};
@@ -924,8 +926,10 @@ static gh_status act_post(gh_engine* e, gh_engine::Batch& b, int l, cudaStream_t
   return GH_OK;
 }
 static gh_status act_classify(gh_engine* e, gh_engine::Batch& b, float* logits, cudaStream_t st) {
-  return t1_classify(e->t1, e->cfg.batch, b.x(b.cur), SsRef{b.ss(b.cur), b.ss_slices[b.cur]}, logits, b.next, st,
-                     b.inv_temp, b.seed, b.pos);
+  if (b.sampling)  // logits are always written (the sampler reads them)
+    return t1_classify(e->t1, e->cfg.batch, b.x(b.cur), SsRef{b.ss(b.cur), b.ss_slices[b.cur]},
+                       logits ? logits : b.logits, b.next, st, b.inv_temp, b.seed, b.pos);
+  return t1_classify(e->t1, e->cfg.batch, b.x(b.cur), SsRef{b.ss(b.cur), b.ss_slices[b.cur]}, logits, b.next, st);
 }
 
 extern "C" {
@@ -1100,6 +1104,12 @@ gh_status gh_engine_set_sampling(gh_engine* e, uint32_t ib, const float* tempera
   GH_CUDA(cudaDeviceSynchronize());  // no step in flight reads the old values
   GH_CUDA(cudaMemcpy(b.inv_temp, inv.data(), (size_t)R * 4, cudaMemcpyHostToDevice));
   GH_CUDA(cudaMemcpy(b.seed, seed_host, (size_t)R * 4, cudaMemcpyHostToDevice));
+  bool any = false;
+  for (float v : inv) any = any || v > 0.f;
+  if (any != b.sampling) {
+    b.sampling = any;
+    if (b.graph) { cudaGraphExecDestroy(b.graph); b.graph = nullptr; }  // recaptured on the next step
+  }
   return GH_OK;
 }
 
