@@ -328,10 +328,11 @@ class ContinuousDispatcher:
     def __init__(self, engine: Engine):
         self.engine = engine
 
-    def run(self, requests, max_new: int):
-        """requests: sequence of 1-D int32 prompt arrays (any lengths >= 1).  Returns the list of
-        generated token arrays (max_new each, in request order; zeros on Tier-2 ranks) and the
-        number of steps."""
+    def run(self, requests, max_new: int, sampling=None):
+        """requests: sequence of 1-D int32 prompt arrays (any lengths >= 1); sampling: optional
+        per-request (temperature, seed) pairs (temperature 0 = greedy, the default).  Returns the
+        list of generated token arrays (max_new each, in request order; zeros on Tier-2 ranks)
+        and the number of steps."""
         eng = self.engine
         B = eng.batch
         role = eng.role
@@ -376,16 +377,25 @@ class ContinuousDispatcher:
         out = [[] for _ in requests]
         tok = np.zeros(B, np.int32)
         pos = np.zeros(B, np.int32)
+        temp = np.zeros(B, np.float32)    # per-lane sampling state (batch-state temperature)
+        seed = np.zeros(B, np.uint32)
+        dirty = [sampling is not None]
 
         def admit(lane):
             kv_unmap(lane)
             lane_req[lane] = -1
             tok[lane] = 0
             pos[lane] = 0
+            if sampling is not None and temp[lane] != 0:
+                temp[lane] = 0
+                dirty[0] = True
             if queue and kv_map(lane, len(requests[queue[0]]) + max_new - 1):
                 r = queue.pop(0)
                 lane_req[lane], lane_t[lane] = r, 0
                 tok[lane] = int(requests[r][0])
+                if sampling is not None:
+                    temp[lane], seed[lane] = sampling[r]
+                    dirty[0] = True
             if lane_req[lane] < 0 and not kv_map(lane, 1):  # the idle lane's dummy token
                 raise L.FeasibilityError(L.GH_EINFEASIBLE, "KV page pool smaller than one page per lane")
 
@@ -393,6 +403,9 @@ class ContinuousDispatcher:
             admit(lane)
         steps = 0
         while any(r >= 0 for r in lane_req):
+            if dirty[0] and role != "tier2":
+                eng.set_sampling(temp, seed)
+                dirty[0] = False
             if role == "tier2":
                 eng.step_host(None, None)
                 nxt = np.zeros(B, np.int32)

@@ -60,3 +60,32 @@ def test_sampling_validation(need_gpu):
     with pytest.raises(L.ValidationError):
         eng.set_sampling(np.array([1.0, -0.5], np.float32), np.zeros(2, np.uint32))
     eng.close()
+
+
+def test_continuous_batching_with_sampling_matches_oracle(need_gpu):
+    """Per-request temperature through the dispatcher: every request's tokens equal decoding it
+    alone with the fp32 oracle's logits and the numpy sampler (same seed, same positions)."""
+    from oracle import Oracle
+    from paper_2501_11779_b200.stages import ContinuousDispatcher, Engine
+    spec = gh.TINY.with_(n_layers=2, max_seq_len=64)
+    rng = np.random.default_rng(12)
+    reqs = [rng.integers(0, spec.vocab_size, size=int(n), dtype=np.int32) for n in rng.integers(1, 6, size=7)]
+    smp = [(float(t), int(sd)) for t, sd in zip([0.0, 0.7, 1.3, 0.0, 2.0, 0.4, 1.0], rng.integers(0, 2**31, 7))]
+    max_new = 6
+    eng = Engine(spec, batch=3, use_graph=False)
+    got, _ = ContinuousDispatcher(eng).run(reqs, max_new, sampling=smp)
+    eng.close()
+    ora = Oracle(spec, n_slots=1)
+    for r, (T, sd), g in zip(reqs, smp, got):
+        tok = np.array([r[0]], np.int32)
+        out = []
+        for t in range(len(r) - 1 + max_new):
+            _, lg = ora.step(tok, np.array([t], np.int32), np.zeros(1, np.uint32))
+            nxt = sampling.sample(lg, [T], [sd], [t])
+            if t + 1 < len(r):
+                tok = np.array([r[t + 1]], np.int32)
+            else:
+                out.append(int(nxt[0]))
+                tok = nxt.astype(np.int32)
+        assert np.array_equal(g, np.array(out, np.int32)), (T, g, out)
+    ora.close()
