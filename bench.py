@@ -151,6 +151,51 @@ def cpu_sample(spec, B, ctx, threads=0):
     return B / t_step, sample, cores, t_step
 
 
+def cpu_stage_profiles(spec, ctx, batches, threads, out_dir, name):
+    """SURVEY §8(d) CPU baseline for configurations whose KV does not fit host RAM whole (C3-C5):
+    per-layer nonattention (F1+F3), attention (F2 at context ctx) and classifier latencies of
+    the oracle on the host cores at each batch, written as reference-format profile CSVs
+    (cpu_tier1_<name>.csv, cpu_tier2_<name>.csv, device "cpu-tier1" / "cpu-tier2").  Returns the
+    rows."""
+    from oracle import Oracle
+    from paper_2501_11779_b200.profiles import write_profile
+    one = spec.with_(n_layers=1, max_seq_len=max(spec.max_seq_len, ctx))
+    maxb = max(batches)
+    ora = Oracle(one, n_slots=maxb, threads=threads)
+    ora.fill_synthetic(99, maxb, ctx - 1)
+    rng = np.random.default_rng(5678)
+    rows = []
+
+    def best(fn, reps=2):
+        t = []
+        for _ in range(reps):
+            t0 = time.perf_counter()
+            fn()
+            t.append(time.perf_counter() - t0)
+        return min(t) * 1e6
+
+    for B in batches:
+        x, fwd, bwd = ora.buffers(B)
+        x[...] = rng.standard_normal(x.shape).astype(x.dtype)
+        x2 = np.zeros_like(x)
+        pos = np.full(B, ctx - 1, np.int32)
+        slot = np.arange(B, dtype=np.uint32)
+        ora.pre(0, x, pos, fwd)
+        ora.attend(0, slot, pos, fwd, bwd)
+        non = best(lambda: (ora.pre(0, x, pos, fwd), ora.post(0, bwd, x2)))
+        att = best(lambda: ora.attend(0, slot, pos, fwd, bwd))
+        cls = best(lambda: ora.classify(x, want_logits=False))
+        rows += [("nonattention", ctx, B, non), ("attention", ctx, B, att), ("classifier", ctx, B, cls)]
+        print(f"cpu B={B}: nonattention {non / 1e3:.1f} ms, attention {att / 1e3:.1f} ms, classifier "
+              f"{cls / 1e3:.1f} ms per layer", file=sys.stderr, flush=True)
+    ora.close()
+    out = Path(out_dir)
+    out.mkdir(parents=True, exist_ok=True)
+    write_profile(out / f"cpu_tier1_{name}.csv", "cpu-tier1", [r for r in rows if r[0] != "attention"])
+    write_profile(out / f"cpu_tier2_{name}.csv", "cpu-tier2", [r for r in rows if r[0] == "attention"])
+    return rows
+
+
 # ------------------------------------------------------------------ configs
 def _profile_latency(path: Path, stage: str, batch: int) -> float:
     """Per-layer latency (us) at `batch` from a reference-format profile CSV: linear interpolation
@@ -491,6 +536,9 @@ def main():
                     help="C2 tier split: prompts per Tier-2 GPU per in-flight batch (default 64, the N=1 batch)")
     ap.add_argument("--inflight", type=int, default=0,
                     help="tier split: in-flight batches (0 = if_gh from the stage profiles)")
+    ap.add_argument("--cpu-profiles", default="",
+                    help="with --impl reference: write the oracle's per-layer CPU stage profiles (cpu_tier{1,2}_<config>.csv) here")
+    ap.add_argument("--cpu-batches", default="1,8,32,64,128")
     ap.add_argument("--paged", action="store_true",
                     help="tier split (C3/C4/C5): paged KV arena, per-prompt contexts uniform in [1, ctx)")
     ap.add_argument("--transport", default="auto", choices=["auto", "nccl", "peer"],
@@ -519,6 +567,14 @@ def main():
                            f"{wl['admitted_slots'] // wl['kp']} full-context slots); per-prompt context uniform "
                            f"in [1, {wl['ctx']}), mean {float(np.mean(wl['ctxs'])):.0f}")
 
+    if args.impl == "reference" and args.cpu_profiles:  # CPU stage profiles
+        from oracle import olib
+        name = args.config or "C2"
+        batches = [int(b) for b in args.cpu_batches.split(",")]
+        rows = cpu_stage_profiles(spec, wl["ctx"], batches, args.cpu_threads, args.cpu_profiles, name)
+        print(json.dumps({"impl": "reference", "cpu_profiles": args.cpu_profiles, "config": name, "ctx": wl["ctx"],
+                          "cores": olib().or_max_threads(), "rows": rows}))
+        return
     if args.impl == "reference":
         if world > 1 and rank != 0:
             return
