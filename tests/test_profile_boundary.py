@@ -80,3 +80,23 @@ def test_reference_optimizer_on_b200_profiles(tmp_path):
                            root / "profiles/b200_tier2_C2.csv", 512, 4)
     assert rc == 0, rep
     assert "best config: K=1 K'=" in rep and "tok/s" in rep
+
+
+@pytest.mark.skipif(not ref_available(), reason="reference library not built")
+def test_reference_planner_on_cpu_profiles():
+    """the host-CPU stage profiles of the C3 shape (bench.py --impl reference
+    --cpu-profiles, measured on the B200 box's host) load in the unmodified planner. CPU-only
+    two-tier, B200 Tier-1 + CPU Tier-2 (the paper's prototype split) and all-B200
+    deployments come out in increasing order."""
+    import re
+    root = Path(__file__).resolve().parents[1]
+    model = root / "configs/llama2-7b-ctx2048.json"
+    tput = {}
+    for name, cl, t1, t2 in [("cpu", "cpu_host_cluster.json", "cpu_tier1_C3.csv", "cpu_tier2_C3.csv"),
+                             ("b200+cpu", "b200_cpu_cluster.json", "b200_tier1_C3.csv", "cpu_tier2_C3.csv"),
+                             ("b200", "b200x8_cluster.json", "b200_tier1_C3.csv", "b200_tier2_C3.csv")]:
+        rc, rep = Ref.simulate(model, root / "configs" / cl, root / "profiles" / t1, root / "profiles" / t2,
+                               1, 3, 64, 2048, inflight=2)
+        assert rc == 0, rep
+        tput[name] = float(re.search(r"throughput: ([0-9.e+]+) tok/s", rep).group(1))
+    assert 0 < tput["cpu"] < tput["b200+cpu"] < tput["b200"]
