@@ -240,6 +240,9 @@ def workload(args, world):
     cfg = args.config or "C2"
     c = gh.CONFIGS[cfg]
     spec, ctx = c["spec"], c["ctx"]
+    if getattr(args, "cpu_profiles", ""):  # CPU stage profiles: the shape and context only
+        return dict(name=cfg, spec=spec, ctx=ctx, batch=c["batch"], requested=c["batch"], inflight=1,
+                    shard=c["batch"], kp=0)
     if args.paged and (world == 1 or cfg == "C2"):
         raise SystemExit("--paged is a tier-split option of C3 / C4 / C5 (tools/paged_bench.py covers one GPU)")
     if world == 1:

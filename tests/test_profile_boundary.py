@@ -100,3 +100,17 @@ def test_reference_planner_on_cpu_profiles():
         assert rc == 0, rep
         tput[name] = float(re.search(r"throughput: ([0-9.e+]+) tok/s", rep).group(1))
     assert 0 < tput["cpu"] < tput["b200+cpu"] < tput["b200"]
+
+
+@pytest.mark.skipif(not ref_available(), reason="reference library not built")
+@pytest.mark.parametrize("cfg,model,ctx,batch", [("C4", "llama2-13b-ctx4096.json", 4096, 16),
+                                                 ("C5", "llama2-70b-ctx8192.json", 8192, 32)])
+def test_reference_planner_on_cpu_profiles_c4_c5(cfg, model, ctx, batch):
+    """The C4 / C5 host-CPU stage profiles load in the unmodified planner (CPU two-tier)."""
+    import re
+    root = Path(__file__).resolve().parents[1]
+    rc, rep = Ref.simulate(root / "configs" / model, root / "configs/cpu_host_cluster.json",
+                           root / f"profiles/cpu_tier1_{cfg}.csv", root / f"profiles/cpu_tier2_{cfg}.csv",
+                           1, 3, batch, ctx, inflight=2)
+    assert rc == 0, rep
+    assert float(re.search(r"throughput: ([0-9.e+]+) tok/s", rep).group(1)) > 0
