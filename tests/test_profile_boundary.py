@@ -113,4 +113,12 @@ def test_reference_planner_on_cpu_profiles_c4_c5(cfg, model, ctx, batch):
                            root / f"profiles/cpu_tier1_{cfg}.csv", root / f"profiles/cpu_tier2_{cfg}.csv",
                            1, 3, batch, ctx, inflight=2)
     assert rc == 0, rep
-    assert float(re.search(r"throughput: ([0-9.e+]+) tok/s", rep).group(1)) > 0
+    cpu = float(re.search(r"throughput: ([0-9.e+]+) tok/s", rep).group(1))
+    # the B200 stage profiles of the same shape (tools/emit_profile.py) at the measured N = 4 split
+    shard = {"C4": 27, "C5": 34}[cfg]
+    rc, rep = Ref.simulate(root / "configs" / model, root / "configs/b200x8_cluster.json",
+                           root / f"profiles/b200_tier1_{cfg}.csv", root / f"profiles/b200_tier2_{cfg}.csv",
+                           1, 3, shard, ctx, inflight=2)
+    assert rc == 0, rep
+    b200 = float(re.search(r"throughput: ([0-9.e+]+) tok/s", rep).group(1))
+    assert 0 < cpu < b200
