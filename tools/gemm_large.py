@@ -20,7 +20,12 @@ def bench(N, K, B, flags=0, cluster=0, reps=20):
 
 
 shapes = {"qkv": (12288, 4096), "o": (4096, 4096), "w13": (22016, 4096), "w2": (4096, 11008), "lm": (32000, 4096)}
-for B in [int(a) for a in sys.argv[1:]] or [192, 448, 1024]:
+args = [a for a in sys.argv[1:] if a.isdigit()]
+if "70b" in sys.argv:
+    shapes = {"qkv": (10240, 8192), "o": (8192, 8192), "w13": (57344, 8192), "w2": (8192, 28672), "lm": (32000, 8192)}
+elif "13b" in sys.argv:
+    shapes = {"qkv": (15360, 5120), "o": (5120, 5120), "w13": (27648, 5120), "w2": (5120, 13824), "lm": (32000, 5120)}
+for B in [int(a) for a in args] or [192, 448, 1024]:
     tot = {"prod": 0.0, "split": 0.0, "pair": 0.0, "wide192": 0.0, "split128": 0.0}
     for name, (N, K) in shapes.items():
         flops = 2.0 * N * K * B
