@@ -224,7 +224,7 @@ typedef struct gh_engine_config {
                               optimizer.cpp:116-123; embedding on the first, classifier on the
                               last) and ranks T + s*K' + j are the K' Tier-2 ranks dedicated to
                               span s; world = T * (1 + K').  Peer transport only. */
-  int prefill;             /* colocated: rows of one step may share a slot at consecutive positions
+  int prefill;             /* rows of one step may share a slot at consecutive positions
                               (chunked prefill mixed with decode rows); every row's key / value is
                               appended before attention (gh_tier2_append) */
   uint32_t kv_pages;       /* 0: contiguous slots of max_seq_len positions; > 0: paged KV arena of
@@ -278,9 +278,10 @@ gh_tier2* gh_engine_tier2(gh_engine* e);
  * + row on a colocated engine, the local slot on a Tier-2 rank); no-ops for contiguous slots. */
 gh_status gh_engine_kv_map(gh_engine* e, uint32_t slot, uint32_t n_positions);
 gh_status gh_engine_kv_unmap(gh_engine* e, uint32_t slot);
-/* Per-row context slots of in-flight batch ib (colocated engine; default ib * batch + row).
- * With prefill != 0 several rows may name the same slot (consecutive positions of one prompt).
- * Synchronises the device. */
+/* Per-row context slots of in-flight batch ib (default ib * rows + row).  Colocated: one slot per
+ * row of the batch; Tier-2 rank: the local slots of its shard's rows (gh_engine_shard); Tier-1:
+ * no-op.  With prefill != 0 several rows may name the same slot (consecutive positions of one
+ * prompt).  Synchronises the device. */
 gh_status gh_engine_set_slots(gh_engine* e, uint32_t ib, const uint32_t* slot_host);
 /* Per-row sampling of in-flight batch ib (batch state "temperature"): temperature 0 =
  * greedy (the default), > 0 = sample from softmax(logits / T) by the Gumbel-max rule with noise

@@ -979,7 +979,8 @@ gh_status gh_engine_create(const gh_engine_config* cfg, gh_comm* comm, gh_engine
     if (e->n1 > s.N) return fail(GH_EINVAL, "more Tier-1 spans than layers");
     if (e->n1 > 1 && cfg->transport == GH_TRANSPORT_NCCL)
       return fail(GH_EUNSUPPORTED, "Tier-1 pipeline stages need the peer transport");
-    if (cfg->prefill) return fail(GH_EUNSUPPORTED, "chunked prefill rows: colocated engine only");
+    if (cfg->prefill && cfg->tier1_ranks > 1)
+      return fail(GH_EUNSUPPORTED, "chunked prefill rows: one Tier-1 rank");
     e->kp = (world - e->n1) / e->n1;
     e->role = rank < e->n1 ? 1 : 2;
     e->span = rank < e->n1 ? rank : (rank - e->n1) / e->kp;
@@ -1125,9 +1126,9 @@ gh_status gh_engine_shard(const gh_engine* e, int* index, uint32_t* off, uint32_
 
 gh_status gh_engine_set_slots(gh_engine* e, uint32_t ib, const uint32_t* slot_host) {
   if (!e || !slot_host || ib >= e->batches.size()) return fail(GH_EINVAL, "bad engine / batch index / slots");
-  if (e->role != 0) return fail(GH_EUNSUPPORTED, "per-row slots: colocated engine only");
+  if (e->role == 1) return GH_OK;  // Tier-1 holds no KV: the Tier-2 ranks take their rows' slots
   auto& b = e->batches[ib];
-  const int R = e->rows();
+  const int R = e->rows();          // Tier-2: the rows of this rank's shard (gh_engine_shard)
   for (int i = 0; i < R; ++i)
     if (slot_host[i] >= e->t2->n_slots)
       return fail(GH_EINVAL, "slot " + std::to_string(slot_host[i]) + " >= n_slots " + std::to_string(e->t2->n_slots));
@@ -1189,6 +1190,7 @@ static gh_status split_layer(gh_engine* e, gh_engine::Batch& b, ncclComm_t comm,
     GH_TRY(act_post(e, b, l, st));
   } else {
     GH_NCCL(api.Recv(b.fwd, e->my_cnt * fwd_row, ncclUint8, 0, comm, st));
+    if (e->cfg.prefill) GH_TRY(t2_append(e->t2, l, e->my_cnt, b.slot, b.pos, b.fwd, st));
     GH_TRY(gh_tier2_attend(e->t2, l, e->my_cnt, b.slot, b.pos, b.fwd, b.bwd, st));
     GH_NCCL(api.Send(b.bwd, e->my_cnt * bwd_row, ncclUint8, 0, comm, st));
   }
@@ -1558,7 +1560,8 @@ static gh_status split_step_peer(gh_engine* e, cudaStream_t st) {
         const uint32_t sq = ++P.seq[ib];
         if (!nowait)
           GH_CU(memops().wait((CUstream)st, (CUdeviceptr)(P.flags + f_fwd(e, ib)), sq, CU_STREAM_WAIT_VALUE_GEQ));
-        GH_TRY(gh_tier2_attend(e->t2, l, e->my_cnt, b.slot, b.pos, b.fwd, b.bwd, st));
+        if (e->cfg.prefill) GH_TRY(t2_append(e->t2, l, e->my_cnt, b.slot, b.pos, b.fwd, st));
+    GH_TRY(gh_tier2_attend(e->t2, l, e->my_cnt, b.slot, b.pos, b.fwd, b.bwd, st));
         GH_CUDA(cudaEventRecord(P.ev[ib], st));
         cudaStream_t c = P.cs[0];
         GH_CUDA(cudaStreamWaitEvent(c, P.ev[ib], 0));
@@ -1609,7 +1612,8 @@ static gh_status split_step_pipelined(gh_engine* e, cudaStream_t st) {
     for (int l = 0; l < N; ++l)
       for (int ib = 0; ib < nb; ++ib) {
         auto& b = e->batches[ib];
-        GH_TRY(gh_tier2_attend(e->t2, l, e->my_cnt, b.slot, b.pos, b.fwd, b.bwd, st));
+        if (e->cfg.prefill) GH_TRY(t2_append(e->t2, l, e->my_cnt, b.slot, b.pos, b.fwd, st));
+    GH_TRY(gh_tier2_attend(e->t2, l, e->my_cnt, b.slot, b.pos, b.fwd, b.bwd, st));
         const bool last = (l == N - 1 && ib == nb - 1);
         GH_TRY(t2_group(e, comm, st, ib, last ? -1 : (ib + 1) % nb, false));
       }

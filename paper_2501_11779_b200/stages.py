@@ -448,78 +448,106 @@ class MixedDispatcher:
     value are appended before attention, so the rows of one prompt see each other's keys exactly
     as they would one token per step -- each request's tokens equal decoding it alone.  The
     row of a request's last prompt token yields its first generated token.  Rows left over hold
-    a dummy token in a reserved scratch slot (the engine's last slot).  With a paged arena a
-    request maps prompt + max_new - 1 positions on admission and returns them when done."""
+    a dummy token in a reserved scratch slot (the last slot).  With a paged arena (colocated) a
+    request maps prompt + max_new - 1 positions on admission and returns them when done.
+
+    Tier split: every rank runs the dispatcher SPMD (admission depends only on lengths).  A
+    request lives on one Tier-2 shard (its slot is a local slot of that rank) and only takes rows
+    of that shard's row range; each Tier-2 rank installs the slots of its own rows."""
 
     def __init__(self, engine: Engine, chunk: int = 16):
         if not engine.prefill:
             raise L.ValidationError(L.GH_EINVAL, "MixedDispatcher needs Engine(prefill=True)")
-        if engine.role != "colocated":
-            raise L.UnsupportedError(L.GH_EUNSUPPORTED, "MixedDispatcher: colocated engine only")
         if engine.n_slots < 2:
             raise L.ValidationError(L.GH_EINVAL, "MixedDispatcher needs n_slots >= 2 (one scratch slot)")
+        if engine.role != "colocated" and engine.kv_pages:
+            raise L.UnsupportedError(L.GH_EUNSUPPORTED, "MixedDispatcher: paged KV in the tier split")
         self.engine, self.chunk = engine, chunk
 
     def run(self, requests, max_new: int):
-        """Returns (generated token arrays in request order, steps)."""
+        """Returns (generated token arrays in request order (zeros on Tier-2 ranks), steps)."""
         eng, B = self.engine, self.engine.batch
-        scratch = eng.n_slots - 1
-        free_slots = list(range(eng.n_slots - 1))
+        role = eng.role
+        _, off, cnt, kp = eng.shard()
+        if kp:
+            from .spec import shard_plan
+            offs, cnts = shard_plan(B, kp)
+        else:
+            offs, cnts = [0], [B]
+        nsh = len(offs)
+        scratch = eng.n_slots - 1         # a local slot of every shard
+        free_slots = [list(range(eng.n_slots - 1)) for _ in range(nsh)]
         queue = list(range(len(requests)))
-        active = []                       # [request, slot, fed]
+        active = [[] for _ in range(nsh)]  # per shard: [request, local slot, fed]
         out = [[] for _ in requests]
-        eng.kv_map(scratch, 1)
+        colocated = role == "colocated"
+        if colocated:
+            eng.kv_map(scratch, 1)
         last_slots = None
         steps = 0
-        while queue or active:
-            # admission (FIFO) while a slot and, when paged, the pages are available
-            while queue and free_slots:
-                r = queue[0]
-                s = free_slots[0]
-                try:
-                    eng.kv_map(s, len(requests[r]) + max_new - 1)
-                except L.FeasibilityError:
-                    if not active:
-                        raise
+        while queue or any(active):
+            # admission (FIFO): the shard with a free slot and the fewest active requests
+            while queue:
+                cand = [j for j in range(nsh) if free_slots[j]]
+                if not cand:
                     break
+                j = min(cand, key=lambda k: (len(active[k]), k))
+                r = queue[0]
+                s = free_slots[j][0]
+                if colocated:
+                    try:
+                        eng.kv_map(s, len(requests[r]) + max_new - 1)
+                    except L.FeasibilityError:
+                        if not any(active):
+                            raise
+                        break
                 queue.pop(0)
-                free_slots.pop(0)
-                active.append([r, s, 0])
+                free_slots[j].pop(0)
+                active[j].append([r, s, 0])
             tok = np.zeros(B, np.int32)
             pos = np.zeros(B, np.int32)
             slots = np.full(B, scratch, np.uint32)
-            emit = []                      # (row, request) pairs whose next token is generated
-            row = 0
-            for a in active:
-                r, s, fed = a
-                p = requests[r]
-                if row >= B:
-                    break
-                if fed < len(p):           # prefill rows
-                    n = min(self.chunk, len(p) - fed, B - row)
-                    tok[row:row + n] = p[fed:fed + n]
-                    pos[row:row + n] = np.arange(fed, fed + n)
-                    slots[row:row + n] = s
-                    if fed + n == len(p):
-                        emit.append((row + n - 1, a))
-                    a[2] = fed + n
-                    row += n
-                else:                      # decode row: the last generated token
-                    tok[row] = out[r][-1]
-                    pos[row] = len(p) + len(out[r]) - 1
-                    slots[row] = s
-                    emit.append((row, a))
-                    row += 1
+            emit = []                      # (row, entry) pairs whose next token is generated
+            for j in range(nsh):
+                row, end = offs[j], offs[j] + cnts[j]
+                for a in active[j]:
+                    r, s, fed = a
+                    p = requests[r]
+                    if row >= end:
+                        break
+                    if fed < len(p):       # prefill rows
+                        n = min(self.chunk, len(p) - fed, end - row)
+                        tok[row:row + n] = p[fed:fed + n]
+                        pos[row:row + n] = np.arange(fed, fed + n)
+                        slots[row:row + n] = s
+                        if fed + n == len(p):
+                            emit.append((row + n - 1, j, a))
+                        a[2] = fed + n
+                        row += n
+                    else:                  # decode row: the last generated token
+                        tok[row] = out[r][-1] if out[r] else 0
+                        pos[row] = len(p) + len(out[r]) - 1
+                        slots[row] = s
+                        emit.append((row, j, a))
+                        row += 1
             if last_slots is None or not np.array_equal(slots, last_slots):
-                eng.set_slots(slots)
+                if role == "tier2":
+                    eng.set_slots(slots[off:off + cnt])
+                elif colocated:
+                    eng.set_slots(slots)
                 last_slots = slots
-            nxt, _ = eng.step_host(tok, pos)
+            if role == "tier2":
+                eng.step_host(None, None)
+                nxt = np.zeros(B, np.int32)
+            else:
+                nxt, _ = eng.step_host(tok, pos)
             steps += 1
-            for rw, a in emit:
+            for rw, j, a in emit:
                 r = a[0]
                 out[r].append(int(nxt[rw]))
                 if len(out[r]) == max_new:
-                    active.remove(a)
-                    eng.kv_unmap(a[1])
-                    free_slots.append(a[1])
+                    active[j].remove(a)
+                    if colocated:
+                        eng.kv_unmap(a[1])
+                    free_slots[j].append(a[1])
         return [np.array(o, np.int32) for o in out], steps

@@ -284,3 +284,58 @@ def test_continuous_batching_paged_tier_split(world):
         assert np.array_equal(w, g)
     if world == 2:
         assert steps > ref_steps  # one Tier-2 pool of 8 pages for 6 lanes: requests waited
+
+
+def worker_mixed(rank, world, port, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    import torch
+    import torch.distributed as dist
+    from paper_2501_11779_b200.stages import Comm, Engine, MixedDispatcher
+    torch.cuda.set_device(rank)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    obj = [Comm.unique_ids(1) if rank == 0 else None]
+    dist.broadcast_object_list(obj, src=0)
+    comm = Comm(obj[0], world, rank, rank)
+    eng = Engine(PSPEC, batch=12, n_slots=5, device=rank, use_graph=False, comm=comm, prefill=True)
+    try:
+        out, steps = MixedDispatcher(eng, chunk=8).run(paged_requests(), PNEW)
+    except Exception as e:  # every rank takes the same decisions: report instead of hanging
+        out, steps = repr(e), -1
+    eng.close()
+    comm.close()
+    if rank == 0:
+        q.put((out, steps))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.skipif(n_gpus() < 2, reason="needs >= 2 GPUs")
+@pytest.mark.parametrize("world", [2, 3])
+def test_mixed_prefill_tier_split(world):
+    """Chunked prefill in the tier split: requests live on one Tier-2 shard and take
+    rows of that shard only; Tier-2 ranks append every row's key / value before attention.
+    Tokens identical to the colocated engine at the same row count."""
+    if n_gpus() < world:
+        pytest.skip(f"needs {world} GPUs")
+    import torch.multiprocessing as mp
+    from paper_2501_11779_b200.stages import ContinuousDispatcher, Engine
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=worker_mixed, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    got, steps = q.get(timeout=300)
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    assert steps >= 0, got
+    ref = Engine(PSPEC, batch=12, use_graph=False)
+    want, ref_steps = ContinuousDispatcher(ref).run(paged_requests(), PNEW)
+    ref.close()
+    for w, g in zip(want, got):
+        assert np.array_equal(w, g)
+    assert steps < ref_steps
