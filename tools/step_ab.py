@@ -1,9 +1,18 @@
-import sys, time
-sys.path.insert(0, "/root/repo")
-import numpy as np, torch
-import paper_2501_11779_b200 as gh
-from paper_2501_11779_b200 import _lib as L
-from paper_2501_11779_b200.stages import Engine
+"""Colocated C2 step timed four ways (diagnostics): back-to-back graph replays with / without the
+advance kernel, each step synchronised, and the end-to-end host path (wall clock).
+
+  python tools/step_ab.py
+"""
+import sys
+import time
+from pathlib import Path
+
+sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+import paper_2501_11779_b200 as gh  # noqa: E402
+from paper_2501_11779_b200 import _lib as L  # noqa: E402
+from paper_2501_11779_b200.stages import Engine  # noqa: E402
 spec = gh.CONFIGS["C2"]["spec"]; B = 64; ctx = 512
 eng = Engine(spec, batch=B, use_graph=True)
 L.check(gh.lib().gh_tier2_fill_synthetic(eng.tier2, 99, B, ctx - 1, None))
