@@ -478,7 +478,7 @@ def run_split(args, wl, rank, world):
         e0.record(stream)
         for _ in range(args.steps):
             eng.step_all(stream=stream)
-            if eng.role == "tier1":
+            if eng.role == "tier1" and not os.environ.get("GH_BENCH_NO_ADVANCE"):  # (diagnostics)
                 for ib in range(IF):
                     eng.advance(ib, 0, stream=stream)
             if os.environ.get("GH_BENCH_STEP_SYNC"):  # diagnostics: drain the pipeline every step
