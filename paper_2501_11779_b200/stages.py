@@ -448,8 +448,9 @@ class MixedDispatcher:
     value are appended before attention, so the rows of one prompt see each other's keys exactly
     as they would one token per step -- each request's tokens equal decoding it alone.  The
     row of a request's last prompt token yields its first generated token.  Rows left over hold
-    a dummy token in a reserved scratch slot (the last slot).  With a paged arena (colocated) a
-    request maps prompt + max_new - 1 positions on admission and returns them when done.
+    a dummy token in a reserved scratch slot (the last slot).  With a paged arena a request maps
+    prompt + max_new - 1 positions on admission (page accounting per Tier-2 shard, kept on every
+    rank) and returns them when done; a request waits while no shard can back it.
 
     Tier split: every rank runs the dispatcher SPMD (admission depends only on lengths).  A
     request lives on one Tier-2 shard (its slot is a local slot of that rank) and only takes rows
@@ -460,8 +461,6 @@ class MixedDispatcher:
             raise L.ValidationError(L.GH_EINVAL, "MixedDispatcher needs Engine(prefill=True)")
         if engine.n_slots < 2:
             raise L.ValidationError(L.GH_EINVAL, "MixedDispatcher needs n_slots >= 2 (one scratch slot)")
-        if engine.role != "colocated" and engine.kv_pages:
-            raise L.UnsupportedError(L.GH_EUNSUPPORTED, "MixedDispatcher: paged KV in the tier split")
         self.engine, self.chunk = engine, chunk
 
     def run(self, requests, max_new: int):
@@ -480,8 +479,19 @@ class MixedDispatcher:
         queue = list(range(len(requests)))
         active = [[] for _ in range(nsh)]  # per shard: [request, local slot, fed]
         out = [[] for _ in requests]
-        colocated = role == "colocated"
-        if colocated:
+        holds_kv = role != "tier1"
+        my_shard = next((j for j in range(nsh) if offs[j] == off), 0) if role == "tier2" else 0
+        # page accounting per shard (kept on every rank so that all take the same decisions)
+        paged = eng.kv_pages > 0
+        pages_free = [eng.kv_pages - 1] * nsh if paged else [0] * nsh  # minus the scratch page
+
+        def pages(n):
+            return -(-n // ContinuousDispatcher.PAGE)
+
+        def mine(j):                      # this rank holds shard j's KV
+            return holds_kv and (role == "colocated" or j == my_shard)
+
+        if holds_kv:
             eng.kv_map(scratch, 1)
         last_slots = None
         steps = 0
@@ -491,16 +501,19 @@ class MixedDispatcher:
                 cand = [j for j in range(nsh) if free_slots[j]]
                 if not cand:
                     break
-                j = min(cand, key=lambda k: (len(active[k]), k))
                 r = queue[0]
+                need = pages(len(requests[r]) + max_new - 1) if paged else 0
+                cand = [k for k in cand if need <= pages_free[k]]
+                if not cand:
+                    if not any(active):
+                        raise L.FeasibilityError(L.GH_EINFEASIBLE,
+                                                 f"request {r} needs more KV pages than a Tier-2 pool holds")
+                    break
+                j = min(cand, key=lambda k: (len(active[k]), k))
                 s = free_slots[j][0]
-                if colocated:
-                    try:
-                        eng.kv_map(s, len(requests[r]) + max_new - 1)
-                    except L.FeasibilityError:
-                        if not any(active):
-                            raise
-                        break
+                if mine(j):
+                    eng.kv_map(s, len(requests[r]) + max_new - 1)
+                pages_free[j] -= need
                 queue.pop(0)
                 free_slots[j].pop(0)
                 active[j].append([r, s, 0])
@@ -533,7 +546,7 @@ class MixedDispatcher:
             if last_slots is None or not np.array_equal(slots, last_slots):
                 if role == "tier2":
                     eng.set_slots(slots[off:off + cnt])
-                elif colocated:
+                elif role == "colocated":
                     eng.set_slots(slots)
                 last_slots = slots
             if role == "tier2":
@@ -547,7 +560,9 @@ class MixedDispatcher:
                 out[r].append(int(nxt[rw]))
                 if len(out[r]) == max_new:
                     active[j].remove(a)
-                    if colocated:
+                    if mine(j):
                         eng.kv_unmap(a[1])
+                    if paged:
+                        pages_free[j] += pages(len(requests[r]) + max_new - 1)
                     free_slots[j].append(a[1])
         return [np.array(o, np.int32) for o in out], steps

@@ -286,7 +286,7 @@ def test_continuous_batching_paged_tier_split(world):
         assert steps > ref_steps  # one Tier-2 pool of 8 pages for 6 lanes: requests waited
 
 
-def worker_mixed(rank, world, port, q):
+def worker_mixed(rank, world, port, q, kv_pages=0):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     import torch
     import torch.distributed as dist
@@ -296,7 +296,8 @@ def worker_mixed(rank, world, port, q):
     obj = [Comm.unique_ids(1) if rank == 0 else None]
     dist.broadcast_object_list(obj, src=0)
     comm = Comm(obj[0], world, rank, rank)
-    eng = Engine(PSPEC, batch=12, n_slots=5, device=rank, use_graph=False, comm=comm, prefill=True)
+    eng = Engine(PSPEC, batch=12, n_slots=5, device=rank, use_graph=False, comm=comm, prefill=True,
+                 kv_pages=kv_pages)
     try:
         out, steps = MixedDispatcher(eng, chunk=8).run(paged_requests(), PNEW)
     except Exception as e:  # every rank takes the same decisions: report instead of hanging
@@ -310,8 +311,8 @@ def worker_mixed(rank, world, port, q):
 
 
 @pytest.mark.skipif(n_gpus() < 2, reason="needs >= 2 GPUs")
-@pytest.mark.parametrize("world", [2, 3])
-def test_mixed_prefill_tier_split(world):
+@pytest.mark.parametrize("world,kv_pages", [(2, 0), (3, 0), (2, 7), (3, 6)])
+def test_mixed_prefill_tier_split(world, kv_pages):
     """Chunked prefill in the tier split: requests live on one Tier-2 shard and take
     rows of that shard only; Tier-2 ranks append every row's key / value before attention.
     Tokens identical to the colocated engine at the same row count."""
@@ -325,7 +326,7 @@ def test_mixed_prefill_tier_split(world):
     s.close()
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
-    procs = [ctx.Process(target=worker_mixed, args=(r, world, port, q)) for r in range(world)]
+    procs = [ctx.Process(target=worker_mixed, args=(r, world, port, q, kv_pages)) for r in range(world)]
     for p in procs:
         p.start()
     got, steps = q.get(timeout=300)
@@ -338,4 +339,5 @@ def test_mixed_prefill_tier_split(world):
     ref.close()
     for w, g in zip(want, got):
         assert np.array_equal(w, g)
-    assert steps < ref_steps
+    if not kv_pages:
+        assert steps < ref_steps
