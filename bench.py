@@ -622,9 +622,9 @@ def main():
     if world == 1:
         ab = attention_bytes(spec, wl["batch"], wl["ctx"])
         ach = ab / (res["attn_ms"] / 1e3) / 1e9
-        out["roofline"] = {"bound": "hbm", "kernel": "attn_decode_kernel (Tier-2 F2, one layer)",
+        out["roofline"] = {"bound": "hbm", "kernel": "attn_gqa_tc_kernel<1> (Tier-2 F2, one layer)",
                            "achieved": ach, "peak": hbm, "unit": "GB/s", "frac": ach / hbm,
-                           "peak_kind": peak_kind, "traffic": ncu_traffic("attn_decode_kernel"),
+                           "peak_kind": peak_kind, "traffic": ncu_traffic("attn_gqa_tc_kernel"),
                            "traffic_source": "profiles/*_ncu_full_metrics.csv (dram read+write per launch)",
                            "algorithmic_bytes": ab,
                            "duration_us": res["attn_ms"] * 1e3, "frac_of_8TBs": ach / 8000.0}

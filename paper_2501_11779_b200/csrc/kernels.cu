@@ -788,14 +788,17 @@ static cudaError_t launch_attn_gqa_tc(const AttnArgs& a, cudaStream_t st) {
 template <typename T, int DH>
 static cudaError_t launch_attn_t(const AttnArgs& a, cudaStream_t st) {
   static const bool no_tc = getenv("GH_NO_GQA_TC") != nullptr;  // diagnostics: CUDA-core GQA kernel
-  static const bool mha_tc = getenv("GH_MHA_TC") != nullptr;     // diagnostics: tensor-core kernel for MHA
+  // MHA on the tensor-core kernel too (G = 1): at the same HBM traffic it spends less energy per
+  // byte than the CUDA-core dot products, which holds the bandwidth under the 1000 W cap
+  // (sustained 6.96 vs 6.53 TB/s at 7B, B 85, ctx 2048)
+  static const bool mha_cc = getenv("GH_MHA_CUDA_CORE") != nullptr;  // diagnostics: CUDA-core MHA kernel
   if constexpr (sizeof(T) == 2 && DH == 128) {
     if (a.kv_tmap && !no_tc) switch (gqa_group(a)) {
         case 2: return launch_attn_gqa_tc<2>(a, st);
         case 4: return launch_attn_gqa_tc<4>(a, st);
         case 8: return launch_attn_gqa_tc<8>(a, st);
       }
-    if (a.kv_tmap && mha_tc && a.H == a.Hkv) return launch_attn_gqa_tc<1>(a, st);
+    if (a.kv_tmap && !no_tc && !mha_cc && a.H == a.Hkv) return launch_attn_gqa_tc<1>(a, st);
   }
   switch (gqa_group(a)) {
     case 2: return launch_attn_gqa<T, DH, 2>(a, st);

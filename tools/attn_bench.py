@@ -2,6 +2,7 @@
 
   python tools/attn_bench.py [B] [ctx] [7b|13b|70b] [paged]   (paged: shuffled 64-position pages)
 """
+import os
 import sys
 from pathlib import Path
 
@@ -32,7 +33,7 @@ slot = torch.arange(B, dtype=torch.int32, device="cuda")
 for i in range(8):
     t2.attend(i % layers, slot, pos, fwd, bwd)
 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-reps = 40
+reps = int(os.environ.get("GH_REPS", "40"))
 e0.record()
 for i in range(reps):
     t2.attend(i % layers, slot, pos, fwd, bwd)
