@@ -7,3 +7,4 @@ timeout 400 python bench.py --impl reference > $O/ref.json 2> $O/ref.err; echo "
 timeout 400 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 --master-addr 127.0.0.1 --master-port 29511 bench.py --gpus 2 > $O/n2.json 2> $O/n2.err; echo "n2 rc=$?"; cat $O/n2.json
 timeout 400 python -m torch.distributed.run --nnodes=1 --nproc-per-node 4 --master-addr 127.0.0.1 --master-port 29512 bench.py --gpus 4 > $O/n4.json 2> $O/n4.err; echo "n4 rc=$?"; cat $O/n4.json
 timeout 400 python -m torch.distributed.run --nnodes=1 --nproc-per-node 4 --master-addr 127.0.0.1 --master-port 29513 bench.py --gpus 4 --config C3 > $O/n4c3.json 2> $O/n4c3.err; echo "n4c3 rc=$?"; cat $O/n4c3.json
+timeout 500 python -m torch.distributed.run --nnodes=1 --nproc-per-node 4 --master-addr 127.0.0.1 --master-port 29514 bench.py --gpus 4 --config C3 --paged > $O/n4c3_paged.json 2> $O/n4c3_paged.err; echo "n4c3p rc=$?"; cat $O/n4c3_paged.json
