@@ -449,7 +449,9 @@ __global__ void __launch_bounds__(GqaTcCfg<G>::kThreads, 1)
   }
   __syncthreads();
   griddep_launch_dependents();
-  griddep_wait();
+  // the producer may request its first unit's cached K / V before griddepcontrol.wait
+  // (a.kv_early, see attention.cuh); every other warp waits here
+  if (warp != 0) griddep_wait();
 
   const bf16_t* fwd = (const bf16_t*)a.msg_fwd;
   bf16_t* bwd = (bf16_t*)a.msg_bwd;
@@ -466,6 +468,25 @@ __global__ void __launch_bounds__(GqaTcCfg<G>::kThreads, 1)
       int u = blockIdx.x;
       int L = 0, sl = 0;
       if (u < n_units) { L = a.pos[u / a.Hkv]; sl = (int)a.slot[u / a.Hkv]; }
+      int pre = 0;  // stages of the first unit whose K / V were requested before the wait
+      if (a.kv_early && u < n_units && L > 0) {
+        const int g = u % a.Hkv;
+        const int* pt = a.page_table ? a.page_table + (long)sl * a.max_pages : nullptr;
+        pre = min((L + C::kTpos - 1) / C::kTpos, C::kStages);
+        for (int c = 0; c < pre; ++c) {
+          uint8_t* st = smem + c * C::kStageBytes;
+          if (c == 0) mbar_expect_tx(&full[0], (uint32_t)C::kKV);
+          else mbar_arrive_expect_tx(&full[c], (uint32_t)C::kKV);
+          const int blk = pt ? pt[c] : sl, p0 = pt ? 0 : c * C::kTpos;
+          const int row_k = ((a.layer_local * a.n_slots + blk) * 2 + 0) * a.Hkv + g;
+          const int row_v = row_k + a.Hkv;
+          tma_load_3d(st, &tmKV, 0, p0, row_k, &full[c], pol);
+          tma_load_3d(st + C::kBox, &tmKV, 64, p0, row_k, &full[c], pol);
+          tma_load_3d(st + 2 * C::kBox, &tmKV, 0, p0, row_v, &full[c], pol);
+          tma_load_3d(st + 3 * C::kBox, &tmKV, 64, p0, row_v, &full[c], pol);
+        }
+      }
+      griddep_wait();
       while (u < n_units) {
         const int b = u / a.Hkv, g = u % a.Hkv;
         const int un = next_unit(a, u);
@@ -476,6 +497,8 @@ __global__ void __launch_bounds__(GqaTcCfg<G>::kThreads, 1)
         const int nch = L > 0 ? (L + C::kTpos - 1) / C::kTpos : 1;
         for (int c = 0; c < nch; ++c, ++it) {
           const int s = it % C::kStages;
+          const bool issued = (int)it < pre;
+          if (issued && c > 0) continue;
           mbar_wait(&empty[s], ((it / C::kStages) & 1) ^ 1);
           uint8_t* st = smem + s * C::kStageBytes;
           uint8_t* hdr = st + C::kKV;
@@ -483,7 +506,7 @@ __global__ void __launch_bounds__(GqaTcCfg<G>::kThreads, 1)
             int* meta = (int*)(hdr + hdr_bytes);
             meta[0] = L; meta[1] = b; meta[2] = g; meta[3] = sl;
           }
-          const bool any = L > 0;
+          const bool any = L > 0 && !issued;
           mbar_arrive_expect_tx(&full[s], (any ? (uint32_t)C::kKV : 0u) + (c == 0 ? hdr_bytes : 0u));
           if (any) {  // full 64-position boxes (rows past L are masked by the consumers)
             const int blk = pt ? pt[c] : sl, p0 = pt ? 0 : c * C::kTpos;
