@@ -340,7 +340,9 @@ cudaError_t launch_argmax_rows(const float* logits, int B, int V, int32_t* next,
 // ====================================================================== batch state
 __global__ void advance_kernel(int32_t* tok, const int32_t* next, int32_t* pos, int n, int inc) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  griddep_launch_dependents();
+  // no early griddepcontrol.launch_dependents: the next step's kernels start only after this one
+  // completes, so the attention kernel's pre-wait reads (pos / slot and the cached K / V,
+  // a.kv_early) see this step's positions and arena even through a chain of early triggers
   griddep_wait();
   if (i < n) { tok[i] = next[i]; pos[i] += inc; }
 }

@@ -318,6 +318,14 @@ class ContinuousDispatcher:
     attend (prompt + max_new - 1) when it is admitted and returns its pages when it finishes; a
     request waits in the queue (its lane idles on one page) until its lane's pool can back it.
 
+    On-demand paging (``on_demand=True``, paged arena only): admission maps only the
+    request's prompt, and a lane maps one more page when its next position crosses a page
+    boundary.  When its shard's pool is dry, the most recently admitted request of that shard is
+    preempted: its pages return to the pool and it goes back to the head of the queue with the
+    tokens it has generated appended to its prompt, so re-admission recomputes its context
+    (positions, weights and row results are unchanged, hence so are its tokens).  The oldest
+    request of a shard always advances, so the loop terminates.  ``self.preemptions`` counts them.
+
     Tier split: every rank runs the same dispatcher over the same requests (SPMD).  Admission
     depends only on prompt lengths, max_new and the page accounting (kept here for every Tier-2
     shard), never on token values, so all ranks take identical decisions; a Tier-2 rank maps the
@@ -325,8 +333,10 @@ class ContinuousDispatcher:
 
     PAGE = 64  # GH_KV_PAGE_POSITIONS
 
-    def __init__(self, engine: Engine):
+    def __init__(self, engine: Engine, on_demand: bool = False):
         self.engine = engine
+        self.on_demand = on_demand
+        self.preemptions = 0
 
     def run(self, requests, max_new: int, sampling=None):
         """requests: sequence of 1-D int32 prompt arrays (any lengths >= 1); sampling: optional
@@ -371,8 +381,21 @@ class ContinuousDispatcher:
                 mapped[lane] += need
             return True
 
+        on_demand = self.on_demand and paged
+        self.preemptions = 0
+        prompt = [np.asarray(q) for q in requests]  # grows by the generated tokens on preemption
+        if on_demand:
+            # a request must fit its shard's pool beside one dummy page per other lane, else
+            # growth would preempt it forever
+            lanes = int(np.bincount(lane_shard).max())
+            for i, q in enumerate(requests):
+                if pages(len(q) + max_new - 1) > eng.kv_pages - (lanes - 1):
+                    raise L.FeasibilityError(L.GH_EINFEASIBLE,
+                                             f"request {i} needs more KV pages than the pool holds")
         queue = list(range(len(requests)))
         lane_req = [-1] * B           # request index in each lane
+        lane_seq = [0] * B            # admission order (preemption victims: the latest)
+        n_admit = [0]
         lane_t = [0] * B              # position of the lane's next input token
         out = [[] for _ in requests]
         tok = np.zeros(B, np.int32)
@@ -381,7 +404,12 @@ class ContinuousDispatcher:
         seed = np.zeros(B, np.uint32)
         dirty = [sampling is not None]
 
-        def admit(lane):
+        def need_at_admission(r):
+            if on_demand:
+                return len(prompt[r])
+            return len(requests[r]) + max_new - 1
+
+        def release(lane):
             kv_unmap(lane)
             lane_req[lane] = -1
             tok[lane] = 0
@@ -389,20 +417,49 @@ class ContinuousDispatcher:
             if sampling is not None and temp[lane] != 0:
                 temp[lane] = 0
                 dirty[0] = True
-            if queue and kv_map(lane, len(requests[queue[0]]) + max_new - 1):
+
+        def admit(lane):
+            release(lane)
+            if queue and kv_map(lane, need_at_admission(queue[0])):
                 r = queue.pop(0)
                 lane_req[lane], lane_t[lane] = r, 0
-                tok[lane] = int(requests[r][0])
+                n_admit[0] += 1
+                lane_seq[lane] = n_admit[0]
+                tok[lane] = int(prompt[r][0])
                 if sampling is not None:
                     temp[lane], seed[lane] = sampling[r]
                     dirty[0] = True
             if lane_req[lane] < 0 and not kv_map(lane, 1):  # the idle lane's dummy token
                 raise L.FeasibilityError(L.GH_EINFEASIBLE, "KV page pool smaller than one page per lane")
 
+        def preempt(lane):
+            r = lane_req[lane]
+            prompt[r] = np.concatenate([np.asarray(requests[r]), np.asarray(out[r], dtype=np.asarray(requests[r]).dtype)])
+            queue.insert(0, r)
+            release(lane)
+            self.preemptions += 1
+            if not kv_map(lane, 1):   # the idle lane's dummy token (its own pages just came back)
+                raise L.FeasibilityError(L.GH_EINFEASIBLE, "KV page pool smaller than one page per lane")
+
+        def grow():
+            # oldest first: a page goes to the longest-running request of the shard
+            for lane in sorted((x for x in range(B) if lane_req[x] >= 0), key=lambda x: lane_seq[x]):
+                if lane_req[lane] < 0 or pages(int(pos[lane]) + 1) <= mapped[lane]:
+                    continue
+                while not kv_map(lane, int(pos[lane]) + 1):
+                    sh = lane_shard[lane]
+                    victim = max((x for x in range(B) if lane_req[x] >= 0 and lane_shard[x] == sh),
+                                 key=lambda x: lane_seq[x])
+                    preempt(victim)
+                    if victim == lane:
+                        break
+
         for lane in range(B):
             admit(lane)
         steps = 0
         while any(r >= 0 for r in lane_req):
+            if on_demand:
+                grow()
             if dirty[0] and role != "tier2":
                 eng.set_sampling(temp, seed)
                 dirty[0] = False
@@ -419,9 +476,9 @@ class ContinuousDispatcher:
                         admit(lane)   # retry: pages may have been returned by now
                     continue
                 t = lane_t[lane]
-                plen = len(requests[r])
+                plen = len(prompt[r])
                 if t + 1 < plen:          # still feeding the prompt
-                    tok[lane] = int(requests[r][t + 1])
+                    tok[lane] = int(prompt[r][t + 1])
                 else:
                     out[r].append(int(nxt[lane]))
                     tok[lane] = nxt[lane]

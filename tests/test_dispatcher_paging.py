@@ -1,0 +1,99 @@
+"""Host logic of ContinuousDispatcher's paged admission (CPU, no GPU): on-demand page growth with
+recompute preemption against a fake engine whose next token is a hash of the lane's whole
+context, so a token is right only when every position below it was written by the same request
+in order (what the real KV arena requires).  Checks the page accounting never exceeds the pool,
+every attended position is mapped, and each request's tokens equal decoding it alone."""
+import hashlib
+
+import numpy as np
+import pytest
+
+from paper_2501_11779_b200 import _lib as L
+from paper_2501_11779_b200.stages import ContinuousDispatcher
+
+PAGE = ContinuousDispatcher.PAGE
+
+
+def _next(ctx):
+    return int.from_bytes(hashlib.blake2b(np.asarray(ctx, np.int64).tobytes(), digest_size=4).digest(), "little") % 1000
+
+
+class FakeEngine:
+    role = "colocated"
+
+    def __init__(self, batch, kv_pages):
+        self.batch, self.kv_pages = batch, kv_pages
+        self.pages = [0] * batch
+        self.hist = [dict() for _ in range(batch)]
+        self.peak = 0
+
+    def shard(self):
+        return -1, 0, self.batch, 0
+
+    def kv_map(self, slot, n):
+        self.pages[slot] = max(self.pages[slot], -(-n // PAGE))
+        assert sum(self.pages) <= self.kv_pages, "pool over-committed"
+        self.peak = max(self.peak, sum(self.pages))
+
+    def kv_unmap(self, slot):
+        self.pages[slot] = 0
+
+    def set_sampling(self, t, s):
+        pass
+
+    def step_host(self, tok, pos):
+        nxt = np.zeros(self.batch, np.int32)
+        for b in range(self.batch):
+            p = int(pos[b])
+            assert self.pages[b] * PAGE >= p + 1, "attended position not mapped"
+            self.hist[b][p] = int(tok[b])
+            nxt[b] = _next([self.hist[b][i] for i in range(p + 1)])
+        return nxt, None
+
+
+def _alone(req, max_new):
+    ctx, out = list(req), []
+    for _ in range(max_new):
+        out.append(_next(ctx))
+        ctx.append(out[-1])
+    return out
+
+
+def _requests(n, seed=3):
+    rng = np.random.default_rng(seed)
+    return [rng.integers(0, 1000, int(rng.integers(1, 150))).astype(np.int32) for _ in range(n)]
+
+
+@pytest.mark.parametrize("on_demand", [False, True])
+def test_paged_admission_matches_alone(on_demand):
+    reqs, max_new, B = _requests(10), 90, 4
+    eng = FakeEngine(B, kv_pages=9)
+    d = ContinuousDispatcher(eng, on_demand=on_demand)
+    got, steps = d.run(reqs, max_new)
+    for r, g in zip(reqs, got):
+        assert g.tolist() == _alone(r.tolist(), max_new)
+    if on_demand:
+        assert d.preemptions > 0      # this pool is too small for 4 concurrent full requests
+    else:
+        assert d.preemptions == 0
+
+
+def test_on_demand_admits_more_than_up_front():
+    """With a pool that backs every lane's prompt but not every lane's full length, on-demand
+    paging runs more requests at once than mapping the full length at admission."""
+    reqs, max_new, B = _requests(8, seed=5), 64, 4
+    res = {}
+    for od in (False, True):
+        eng = FakeEngine(B, kv_pages=12)
+        d = ContinuousDispatcher(eng, on_demand=od)
+        got, steps = d.run(reqs, max_new)
+        for r, g in zip(reqs, got):
+            assert g.tolist() == _alone(r.tolist(), max_new)
+        res[od] = steps
+    assert res[True] <= res[False]
+
+
+def test_on_demand_rejects_request_larger_than_pool():
+    eng = FakeEngine(2, kv_pages=3)
+    with pytest.raises(L.FeasibilityError):
+        ContinuousDispatcher(eng, on_demand=True).run([np.arange(150, dtype=np.int32)], 40)

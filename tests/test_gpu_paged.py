@@ -141,6 +141,28 @@ def test_paged_engine_continuous_batching(need_gpu):
     eng.close()
 
 
+def test_paged_engine_on_demand_preemption(need_gpu):
+    """On-demand paging: admission maps the prompt only, lanes grow a page at a time, and a dry
+    pool preempts the latest request, which recomputes its context on re-admission.  The tokens
+    equal the contiguous-arena engine's, with preemptions taken on a 6-page pool."""
+    from paper_2501_11779_b200.stages import ContinuousDispatcher, Engine
+    spec = gh.TINY.with_(n_layers=2, max_seq_len=256)
+    rng = np.random.default_rng(9)
+    lens = [60, 100, 3, 70, 40, 64, 65, 9]
+    reqs = [rng.integers(0, spec.vocab_size, size=n, dtype=np.int32) for n in lens]
+    max_new = 70
+    ref_eng = Engine(spec, batch=3, use_graph=False)
+    want, _ = ContinuousDispatcher(ref_eng).run(reqs, max_new)
+    ref_eng.close()
+    eng = Engine(spec, batch=3, use_graph=False, kv_pages=6)
+    d = ContinuousDispatcher(eng, on_demand=True)
+    got, steps = d.run(reqs, max_new)
+    eng.close()
+    assert d.preemptions > 0
+    for w, g in zip(want, got):
+        assert np.array_equal(w, g)
+
+
 def test_paged_ragged_fill(need_gpu):
     """The synthetic fill of a paged arena stops at each slot's mapping and writes the same logical
     values as the contiguous fill."""
