@@ -191,6 +191,13 @@ uint32_t gh_tier2_pages_free(const gh_tier2* t2);
 gh_status gh_tier2_read_kv(gh_tier2* t2, uint32_t layer, uint32_t slot, uint32_t kv,
                            uint32_t head, uint32_t n, void* host_out);
 uint64_t gh_tier2_arena_bytes(const gh_tier2* t2);
+/* Swap a slot's context out to / back from host memory (preemption by swap instead of
+ * recompute, P:471-479 batch state).  The host buffer holds positions [0, n) of every owned
+ * layer in a library-defined layout of gh_tier2_kv_swap_bytes(t2, n) bytes; restore may target
+ * a different slot (and different pages) mapped for n positions.  Synchronous on `stream`. */
+uint64_t gh_tier2_kv_swap_bytes(const gh_tier2* t2, uint32_t n_positions);
+gh_status gh_tier2_kv_swap(gh_tier2* t2, uint32_t slot, uint32_t n_positions, void* host,
+                           int to_host, void* stream);
 
 /* ------------------------------------------------------------------ NCCL transport
  * One communicator per process (one process per GPU).  `unique_id` is the 128-byte
@@ -278,6 +285,9 @@ gh_tier2* gh_engine_tier2(gh_engine* e);
  * + row on a colocated engine, the local slot on a Tier-2 rank); no-ops for contiguous slots. */
 gh_status gh_engine_kv_map(gh_engine* e, uint32_t slot, uint32_t n_positions);
 gh_status gh_engine_kv_unmap(gh_engine* e, uint32_t slot);
+/* gh_tier2_kv_swap on the engine's Tier-2 context (after the engine's queued steps finish). */
+gh_status gh_engine_kv_swap(gh_engine* e, uint32_t slot, uint32_t n_positions, void* host, int to_host);
+uint64_t gh_engine_kv_swap_bytes(const gh_engine* e, uint32_t n_positions);
 /* Per-row context slots of in-flight batch ib (default ib * rows + row).  Colocated: one slot per
  * row of the batch; Tier-2 rank: the local slots of its shard's rows (gh_engine_shard); Tier-1:
  * no-op.  With prefill != 0 several rows may name the same slot (consecutive positions of one

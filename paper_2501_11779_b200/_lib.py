@@ -128,6 +128,10 @@ PROTOTYPES = {
     "gh_engine_tier2": (vp, [vp]),
     "gh_engine_kv_map": (st, [vp, u32, u32]),
     "gh_engine_kv_unmap": (st, [vp, u32]),
+    "gh_engine_kv_swap": (st, [vp, u32, u32, vp, C.c_int]),
+    "gh_engine_kv_swap_bytes": (C.c_uint64, [vp, u32]),
+    "gh_tier2_kv_swap": (st, [vp, u32, u32, vp, C.c_int, vp]),
+    "gh_tier2_kv_swap_bytes": (C.c_uint64, [vp, u32]),
     "gh_engine_set_slots": (st, [vp, u32, P(u32)]),
     "gh_engine_shard": (st, [vp, P(C.c_int), P(u32), P(u32), P(u32)]),
     "gh_engine_set_sampling": (st, [vp, u32, P(C.c_float), P(u32)]),

@@ -716,6 +716,48 @@ gh_status gh_tier2_fill_synthetic(gh_tier2* t, uint64_t seed, uint32_t n_fill, u
   return GH_OK;
 }
 
+// host layout: paged [layer][page][2][Hkv][64][dh] (whole pages); contiguous [layer][2 Hkv][n][dh]
+uint64_t gh_tier2_kv_swap_bytes(const gh_tier2* t, uint32_t n) {
+  if (!t) return 0;
+  const uint64_t P = t->paged ? (uint64_t)((n + kKvPagePositions - 1) / kKvPagePositions) * kKvPagePositions : n;
+  return (uint64_t)(t->l1 - t->l0) * 2 * t->sh.Hkv * P * t->sh.dh * t->sh.db;
+}
+
+gh_status gh_tier2_kv_swap(gh_tier2* t, uint32_t slot, uint32_t n, void* host, int to_host, void* stream) {
+  if (!t || !host) return fail(GH_EINVAL, "null argument");
+  if (slot >= t->n_slots || n > (uint32_t)t->sh.S) return fail(GH_EINVAL, "kv_swap out of range");
+  if (t->paged && t->mapped[slot] * (uint32_t)kKvPagePositions < n)
+    return fail(GH_EINVAL, "kv_swap: positions are not mapped");
+  if (n == 0) return GH_OK;
+  const Shape& s = t->sh;
+  GH_CUDA(cudaSetDevice(t->device));
+  cudaStream_t st = (cudaStream_t)stream;
+  const cudaMemcpyKind kind = to_host ? cudaMemcpyDeviceToHost : cudaMemcpyHostToDevice;
+  char* h = (char*)host;
+  char* arena = (char*)t->arena;
+  for (int l = 0; l < (int)(t->l1 - t->l0); ++l) {
+    const size_t lbase = (size_t)l * t->layer_stride() * s.db;
+    if (t->paged) {  // one block of 2 x Hkv x 64 positions per page
+      const uint32_t np = (n + kKvPagePositions - 1) / kKvPagePositions;
+      const size_t blk = (size_t)t->slot_stride() * s.db;
+      for (uint32_t p = 0; p < np; ++p) {
+        char* d = arena + lbase + (size_t)t->h_pt[(size_t)slot * t->max_pages + p] * blk;
+        if (to_host) GH_CUDA(cudaMemcpyAsync(h, d, blk, kind, st));
+        else GH_CUDA(cudaMemcpyAsync(d, h, blk, kind, st));
+        h += blk;
+      }
+    } else {  // 2 x Hkv rows of n positions at a pitch of max_seq_len positions
+      const size_t row = (size_t)n * s.dh * s.db, pitch = (size_t)t->span() * s.dh * s.db;
+      char* d = arena + lbase + (size_t)slot * t->slot_stride() * s.db;
+      if (to_host) GH_CUDA(cudaMemcpy2DAsync(h, row, d, pitch, row, 2 * s.Hkv, kind, st));
+      else GH_CUDA(cudaMemcpy2DAsync(d, pitch, h, row, row, 2 * s.Hkv, kind, st));
+      h += row * 2 * s.Hkv;
+    }
+  }
+  GH_CUDA(cudaStreamSynchronize(st));
+  return GH_OK;
+}
+
 gh_status gh_tier2_read_kv(gh_tier2* t, uint32_t layer, uint32_t slot, uint32_t kv, uint32_t head,
                            uint32_t n, void* host_out) {
   if (!t || !host_out) return fail(GH_EINVAL, "null argument");
@@ -1088,6 +1130,18 @@ gh_status gh_engine_kv_map(gh_engine* e, uint32_t slot, uint32_t n_positions) {
   if (!e) return fail(GH_EINVAL, "null engine");
   if (!e->t2) return fail(GH_EUNSUPPORTED, "this rank holds no KV (Tier-1 role)");
   return gh_tier2_map(e->t2, slot, n_positions, nullptr);
+}
+
+gh_status gh_engine_kv_swap(gh_engine* e, uint32_t slot, uint32_t n_positions, void* host, int to_host) {
+  if (!e) return fail(GH_EINVAL, "null engine");
+  if (!e->t2) return fail(GH_EUNSUPPORTED, "this rank holds no KV (Tier-1 role)");
+  GH_CUDA(cudaSetDevice(e->t2->device));
+  GH_CUDA(cudaDeviceSynchronize());  // the engine's queued steps read / write the arena
+  return gh_tier2_kv_swap(e->t2, slot, n_positions, host, to_host, nullptr);
+}
+
+uint64_t gh_engine_kv_swap_bytes(const gh_engine* e, uint32_t n_positions) {
+  return e && e->t2 ? gh_tier2_kv_swap_bytes(e->t2, n_positions) : 0;
 }
 
 gh_status gh_engine_set_sampling(gh_engine* e, uint32_t ib, const float* temperature_host, const uint32_t* seed_host) {

@@ -216,6 +216,26 @@ class Engine:
     def kv_unmap(self, slot: int):
         L.check(L.lib().gh_engine_kv_unmap(self.h, slot))
 
+    def kv_swap_out(self, slot: int, n_positions: int):
+        """Copy positions [0, n) of a slot's context (every owned layer) to a pinned host buffer
+        (page-locked, so the copies run at PCIe speed; buffers are recycled by kv_swap_in)."""
+        import torch
+        nbytes = L.lib().gh_engine_kv_swap_bytes(self.h, n_positions)
+        pool = self.__dict__.setdefault("_swap_pool", [])
+        fit = [i for i, b in enumerate(pool) if b.numel() >= nbytes]
+        if fit:
+            buf = pool.pop(min(fit, key=lambda i: pool[i].numel()))
+        else:
+            buf = torch.empty(max(nbytes, 1), dtype=torch.uint8, pin_memory=True)
+        L.check(L.lib().gh_engine_kv_swap(self.h, slot, n_positions, buf.data_ptr(), 1))
+        return buf
+
+    def kv_swap_in(self, slot: int, n_positions: int, buf):
+        """Restore a kv_swap_out buffer into a slot mapped for n positions."""
+        assert buf.numel() >= L.lib().gh_engine_kv_swap_bytes(self.h, n_positions)
+        L.check(L.lib().gh_engine_kv_swap(self.h, slot, n_positions, buf.data_ptr(), 0))
+        self.__dict__.setdefault("_swap_pool", []).append(buf)
+
     def set_sampling(self, temperature, seed, ib=0):
         """Per-row temperature (0 = greedy) and seed of in-flight batch ib."""
         t = np.ascontiguousarray(temperature, dtype=np.float32)
@@ -325,6 +345,9 @@ class ContinuousDispatcher:
     tokens it has generated appended to its prompt, so re-admission recomputes its context
     (positions, weights and row results are unchanged, hence so are its tokens).  The oldest
     request of a shard always advances, so the loop terminates.  ``self.preemptions`` counts them.
+    With ``preempt="swap"`` the preempted request's context is copied to host memory instead
+    (gh_engine_kv_swap) and restored into whichever lane re-admits it, which resumes at the saved
+    position without recomputing.
 
     Tier split: every rank runs the same dispatcher over the same requests (SPMD).  Admission
     depends only on prompt lengths, max_new and the page accounting (kept here for every Tier-2
@@ -333,9 +356,12 @@ class ContinuousDispatcher:
 
     PAGE = 64  # GH_KV_PAGE_POSITIONS
 
-    def __init__(self, engine: Engine, on_demand: bool = False):
+    def __init__(self, engine: Engine, on_demand: bool = False, preempt: str = "recompute"):
+        if preempt not in ("recompute", "swap"):
+            raise ValueError(f"preempt must be 'recompute' or 'swap', not {preempt!r}")
         self.engine = engine
         self.on_demand = on_demand
+        self.preempt = preempt
         self.preemptions = 0
 
     def run(self, requests, max_new: int, sampling=None):
@@ -404,7 +430,14 @@ class ContinuousDispatcher:
         seed = np.zeros(B, np.uint32)
         dirty = [sampling is not None]
 
+        swapped = {}                  # request -> (positions saved, next input token, host buffer)
+
+        def holds(lane):              # this rank holds the lane's KV
+            return role != "tier1" and off <= lane < off + cnt
+
         def need_at_admission(r):
+            if r in swapped:
+                return swapped[r][0]
             if on_demand:
                 return len(prompt[r])
             return len(requests[r]) + max_new - 1
@@ -426,6 +459,11 @@ class ContinuousDispatcher:
                 n_admit[0] += 1
                 lane_seq[lane] = n_admit[0]
                 tok[lane] = int(prompt[r][0])
+                if r in swapped:      # resume at the saved position
+                    t, tk, buf = swapped.pop(r)
+                    if holds(lane):
+                        eng.kv_swap_in(lane - off, t, buf)
+                    lane_t[lane], pos[lane], tok[lane] = t, t, tk
                 if sampling is not None:
                     temp[lane], seed[lane] = sampling[r]
                     dirty[0] = True
@@ -434,7 +472,12 @@ class ContinuousDispatcher:
 
         def preempt(lane):
             r = lane_req[lane]
-            prompt[r] = np.concatenate([np.asarray(requests[r]), np.asarray(out[r], dtype=np.asarray(requests[r]).dtype)])
+            t = lane_t[lane]
+            if self.preempt == "swap" and t > 0:
+                swapped[r] = (t, int(tok[lane]), eng.kv_swap_out(lane - off, t) if holds(lane) else None)
+            else:
+                prompt[r] = np.concatenate([np.asarray(requests[r]),
+                                            np.asarray(out[r], dtype=np.asarray(requests[r]).dtype)])
             queue.insert(0, r)
             release(lane)
             self.preemptions += 1

@@ -26,6 +26,7 @@ class FakeEngine:
         self.pages = [0] * batch
         self.hist = [dict() for _ in range(batch)]
         self.peak = 0
+        self.swaps = 0
 
     def shard(self):
         return -1, 0, self.batch, 0
@@ -40,6 +41,15 @@ class FakeEngine:
 
     def set_sampling(self, t, s):
         pass
+
+    def kv_swap_out(self, slot, n):
+        assert self.pages[slot] * PAGE >= n
+        self.swaps += 1
+        return [self.hist[slot][i] for i in range(n)]
+
+    def kv_swap_in(self, slot, n, buf):
+        assert self.pages[slot] * PAGE >= n and len(buf) == n
+        self.hist[slot] = dict(enumerate(buf))
 
     def step_host(self, tok, pos):
         nxt = np.zeros(self.batch, np.int32)
@@ -64,18 +74,33 @@ def _requests(n, seed=3):
     return [rng.integers(0, 1000, int(rng.integers(1, 150))).astype(np.int32) for _ in range(n)]
 
 
-@pytest.mark.parametrize("on_demand", [False, True])
-def test_paged_admission_matches_alone(on_demand):
+@pytest.mark.parametrize("on_demand,preempt", [(False, "recompute"), (True, "recompute"), (True, "swap")])
+def test_paged_admission_matches_alone(on_demand, preempt):
     reqs, max_new, B = _requests(10), 90, 4
     eng = FakeEngine(B, kv_pages=9)
-    d = ContinuousDispatcher(eng, on_demand=on_demand)
+    d = ContinuousDispatcher(eng, on_demand=on_demand, preempt=preempt)
     got, steps = d.run(reqs, max_new)
     for r, g in zip(reqs, got):
         assert g.tolist() == _alone(r.tolist(), max_new)
     if on_demand:
         assert d.preemptions > 0      # this pool is too small for 4 concurrent full requests
+        assert (eng.swaps > 0) == (preempt == "swap")
     else:
         assert d.preemptions == 0
+
+
+def test_swap_takes_fewer_steps_than_recompute():
+    reqs, max_new, B = _requests(10), 90, 4
+    steps = {}
+    for preempt in ("recompute", "swap"):
+        d = ContinuousDispatcher(FakeEngine(B, kv_pages=9), on_demand=True, preempt=preempt)
+        _, steps[preempt] = d.run(reqs, max_new)
+    assert steps["swap"] < steps["recompute"]
+
+
+def test_bad_preempt_policy():
+    with pytest.raises(ValueError):
+        ContinuousDispatcher(FakeEngine(2, 4), preempt="drop")
 
 
 def test_on_demand_admits_more_than_up_front():

@@ -141,7 +141,37 @@ def test_paged_engine_continuous_batching(need_gpu):
     eng.close()
 
 
-def test_paged_engine_on_demand_preemption(need_gpu):
+@pytest.mark.parametrize("paged", [False, True])
+def test_kv_swap_round_trip(paged, need_gpu):
+    """gh_tier2_kv_swap: a slot's context saved to host and restored into another slot (other
+    pages) reads back bit-identical for every layer, K / V and head."""
+    from paper_2501_11779_b200.stages import Tier2
+    spec = gh.LLAMA2_70B.with_(n_layers=2, max_seq_len=512)
+    n = 200
+    t2 = Tier2(spec, n_slots=3, n_pages=12) if paged else Tier2(spec, n_slots=3)
+    try:
+        if paged:
+            t2.map(2, 64)     # slot 2 holds a page first, so slot 0 and slot 1 get other pages
+            t2.map(0, n)
+        t2.fill_synthetic(7, 1, n)
+        size = L.lib().gh_tier2_kv_swap_bytes(t2.h, n)
+        buf = np.zeros(size, np.uint8)
+        L.check(L.lib().gh_tier2_kv_swap(t2.h, 0, n, buf.ctypes.data, 1, None))
+        if paged:
+            t2.map(1, n)
+        L.check(L.lib().gh_tier2_kv_swap(t2.h, 1, n, buf.ctypes.data, 0, None))
+        for layer in range(2):
+            for kv in range(2):
+                for head in range(spec.n_kv_heads):
+                    assert np.array_equal(t2.read_kv(layer, 0, kv, head, n), t2.read_kv(layer, 1, kv, head, n))
+        with pytest.raises(L.GhError):
+            L.check(L.lib().gh_tier2_kv_swap(t2.h, 0, 513, buf.ctypes.data, 1, None))
+    finally:
+        t2.close()
+
+
+@pytest.mark.parametrize("preempt", ["recompute", "swap"])
+def test_paged_engine_on_demand_preemption(preempt, need_gpu):
     """On-demand paging: admission maps the prompt only, lanes grow a page at a time, and a dry
     pool preempts the latest request, which recomputes its context on re-admission.  The tokens
     equal the contiguous-arena engine's, with preemptions taken on a 6-page pool."""
@@ -155,7 +185,7 @@ def test_paged_engine_on_demand_preemption(need_gpu):
     want, _ = ContinuousDispatcher(ref_eng).run(reqs, max_new)
     ref_eng.close()
     eng = Engine(spec, batch=3, use_graph=False, kv_pages=6)
-    d = ContinuousDispatcher(eng, on_demand=True)
+    d = ContinuousDispatcher(eng, on_demand=True, preempt=preempt)
     got, steps = d.run(reqs, max_new)
     eng.close()
     assert d.preemptions > 0

@@ -229,7 +229,7 @@ def paged_requests():
     return [rng.integers(0, PSPEC.vocab_size, size=n, dtype=np.int32) for n in PLENS]
 
 
-def worker_paged(rank, world, port, q, on_demand=False):
+def worker_paged(rank, world, port, q, on_demand=False, preempt="recompute"):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     import torch
     import torch.distributed as dist
@@ -241,7 +241,7 @@ def worker_paged(rank, world, port, q, on_demand=False):
     comm = Comm(obj[0], world, rank, rank)
     eng = Engine(PSPEC, batch=PB, device=rank, use_graph=False, comm=comm, kv_pages=8)
     try:
-        out, steps = ContinuousDispatcher(eng, on_demand=on_demand).run(paged_requests(), PNEW)
+        out, steps = ContinuousDispatcher(eng, on_demand=on_demand, preempt=preempt).run(paged_requests(), PNEW)
     except Exception as e:  # every rank takes the same decisions: report instead of hanging
         out, steps = repr(e), -1
     eng.close()
@@ -254,8 +254,8 @@ def worker_paged(rank, world, port, q, on_demand=False):
 
 @pytest.mark.skipif(n_gpus() < 2, reason="needs >= 2 GPUs")
 @pytest.mark.parametrize("world", [2, 3])
-@pytest.mark.parametrize("on_demand", [False, True])
-def test_continuous_batching_paged_tier_split(world, on_demand):
+@pytest.mark.parametrize("on_demand,preempt", [(False, "recompute"), (True, "recompute"), (True, "swap")])
+def test_continuous_batching_paged_tier_split(world, on_demand, preempt):
     """Continuous batching on paged Tier-2 ranks (SURVEY 8f-2 in the tier split): every rank
     runs the dispatcher SPMD; each Tier-2 rank maps its own shard's lanes from a pool smaller
     than its lanes x max_seq_len, so requests wait for pages (or, on demand, grow page by page and
@@ -271,7 +271,7 @@ def test_continuous_batching_paged_tier_split(world, on_demand):
     s.close()
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
-    procs = [ctx.Process(target=worker_paged, args=(r, world, port, q, on_demand)) for r in range(world)]
+    procs = [ctx.Process(target=worker_paged, args=(r, world, port, q, on_demand, preempt)) for r in range(world)]
     for p in procs:
         p.start()
     got, steps = q.get(timeout=300)
