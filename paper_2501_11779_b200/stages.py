@@ -345,6 +345,8 @@ class ContinuousDispatcher:
     tokens it has generated appended to its prompt, so re-admission recomputes its context
     (positions, weights and row results are unchanged, hence so are its tokens).  The oldest
     request of a shard always advances, so the loop terminates.  ``self.preemptions`` counts them.
+    ``order="shortest"`` admits the shortest prompts first (max_new is common to all requests, so
+    this is shortest-job-first); a preempted request still re-enters at the queue head.
     With ``preempt="swap"`` the preempted request's context is copied to host memory instead
     (gh_engine_kv_swap) and restored into whichever lane re-admits it, which resumes at the saved
     position without recomputing.
@@ -356,9 +358,13 @@ class ContinuousDispatcher:
 
     PAGE = 64  # GH_KV_PAGE_POSITIONS
 
-    def __init__(self, engine: Engine, on_demand: bool = False, preempt: str = "recompute"):
+    def __init__(self, engine: Engine, on_demand: bool = False, preempt: str = "recompute",
+                 order: str = "fifo"):
         if preempt not in ("recompute", "swap"):
             raise ValueError(f"preempt must be 'recompute' or 'swap', not {preempt!r}")
+        if order not in ("fifo", "shortest"):
+            raise ValueError(f"order must be 'fifo' or 'shortest', not {order!r}")
+        self.order = order
         self.engine = engine
         self.on_demand = on_demand
         self.preempt = preempt
@@ -419,6 +425,8 @@ class ContinuousDispatcher:
                     raise L.FeasibilityError(L.GH_EINFEASIBLE,
                                              f"request {i} needs more KV pages than the pool holds")
         queue = list(range(len(requests)))
+        if self.order == "shortest":  # shortest prompt first (stable: ties keep request order)
+            queue.sort(key=lambda r: len(requests[r]))
         lane_req = [-1] * B           # request index in each lane
         lane_seq = [0] * B            # admission order (preemption victims: the latest)
         n_admit = [0]

@@ -122,3 +122,25 @@ def test_on_demand_rejects_request_larger_than_pool():
     eng = FakeEngine(2, kv_pages=3)
     with pytest.raises(L.FeasibilityError):
         ContinuousDispatcher(eng, on_demand=True).run([np.arange(150, dtype=np.int32)], 40)
+
+
+def test_shortest_first_order():
+    """order="shortest": requests are admitted by prompt length (ties in request order); tokens
+    are unchanged, and with one lane the admission order is exactly the sorted order."""
+    reqs, max_new = _requests(7, seed=9), 20
+    eng = FakeEngine(1, kv_pages=8)
+    seen = []
+    step = eng.step_host
+
+    def spy(tok, pos):
+        if int(pos[0]) == 0:
+            seen.append(int(tok[0]))
+        return step(tok, pos)
+    eng.step_host = spy
+    got, _ = ContinuousDispatcher(eng, order="shortest").run(reqs, max_new)
+    for r, g in zip(reqs, got):
+        assert g.tolist() == _alone(r.tolist(), max_new)
+    want = [int(reqs[i][0]) for i in sorted(range(len(reqs)), key=lambda i: len(reqs[i]))]
+    assert seen == want
+    with pytest.raises(ValueError):
+        ContinuousDispatcher(eng, order="random")
