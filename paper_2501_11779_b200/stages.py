@@ -191,6 +191,7 @@ class Engine:
         self.comm = comm
         self.role = self.ROLES[L.lib().gh_engine_role(h)]
         self._pinned = {}
+        self._swap_pool = []              # pinned host buffers recycled by kv_swap_out / kv_swap_in
 
     def close(self):
         if getattr(self, "h", None) and L is not None and L.lib is not None:
@@ -221,7 +222,7 @@ class Engine:
         (page-locked, so the copies run at PCIe speed; buffers are recycled by kv_swap_in)."""
         import torch
         nbytes = L.lib().gh_engine_kv_swap_bytes(self.h, n_positions)
-        pool = self.__dict__.setdefault("_swap_pool", [])
+        pool = self._swap_pool
         fit = [i for i, b in enumerate(pool) if b.numel() >= nbytes]
         if fit:
             buf = pool.pop(min(fit, key=lambda i: pool[i].numel()))
@@ -234,7 +235,7 @@ class Engine:
         """Restore a kv_swap_out buffer into a slot mapped for n positions."""
         assert buf.numel() >= L.lib().gh_engine_kv_swap_bytes(self.h, n_positions)
         L.check(L.lib().gh_engine_kv_swap(self.h, slot, n_positions, buf.data_ptr(), 0))
-        self.__dict__.setdefault("_swap_pool", []).append(buf)
+        self._swap_pool.append(buf)
 
     def set_sampling(self, temperature, seed, ib=0):
         """Per-row temperature (0 = greedy) and seed of in-flight batch ib."""
