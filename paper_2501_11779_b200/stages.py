@@ -350,7 +350,8 @@ class ContinuousDispatcher:
     this is shortest-job-first); a preempted request still re-enters at the queue head.
     With ``preempt="swap"`` the preempted request's context is copied to host memory instead
     (gh_engine_kv_swap) and restored into whichever lane re-admits it, which resumes at the saved
-    position without recomputing.
+    position without recomputing.  In the tier split the buffer lives on the request's Tier-2
+    shard, so a lane of another shard that admits it recomputes its context instead.
 
     Tier split: every rank runs the same dispatcher over the same requests (SPMD).  Admission
     depends only on prompt lengths, max_new and the page accounting (kept here for every Tier-2
@@ -444,7 +445,12 @@ class ContinuousDispatcher:
         def holds(lane):              # this rank holds the lane's KV
             return role != "tier1" and off <= lane < off + cnt
 
-        def need_at_admission(r):
+        def need_at_admission(r, lane):
+            if r in swapped and swapped[r][3] != lane_shard[lane]:
+                # its context sits in another Tier-2 shard's host buffer: recompute it instead
+                swapped.pop(r)
+                prompt[r] = np.concatenate([np.asarray(requests[r]),
+                                            np.asarray(out[r], dtype=np.asarray(requests[r]).dtype)])
             if r in swapped:
                 return swapped[r][0]
             if on_demand:
@@ -462,14 +468,14 @@ class ContinuousDispatcher:
 
         def admit(lane):
             release(lane)
-            if queue and kv_map(lane, need_at_admission(queue[0])):
+            if queue and kv_map(lane, need_at_admission(queue[0], lane)):
                 r = queue.pop(0)
                 lane_req[lane], lane_t[lane] = r, 0
                 n_admit[0] += 1
                 lane_seq[lane] = n_admit[0]
                 tok[lane] = int(prompt[r][0])
                 if r in swapped:      # resume at the saved position
-                    t, tk, buf = swapped.pop(r)
+                    t, tk, buf, _ = swapped.pop(r)
                     if holds(lane):
                         eng.kv_swap_in(lane - off, t, buf)
                     lane_t[lane], pos[lane], tok[lane] = t, t, tk
@@ -483,7 +489,8 @@ class ContinuousDispatcher:
             r = lane_req[lane]
             t = lane_t[lane]
             if self.preempt == "swap" and t > 0:
-                swapped[r] = (t, int(tok[lane]), eng.kv_swap_out(lane - off, t) if holds(lane) else None)
+                swapped[r] = (t, int(tok[lane]), eng.kv_swap_out(lane - off, t) if holds(lane) else None,
+                              lane_shard[lane])
             else:
                 prompt[r] = np.concatenate([np.asarray(requests[r]),
                                             np.asarray(out[r], dtype=np.asarray(requests[r]).dtype)])

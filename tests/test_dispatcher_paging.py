@@ -144,3 +144,64 @@ def test_shortest_first_order():
     assert seen == want
     with pytest.raises(ValueError):
         ContinuousDispatcher(eng, order="random")
+
+
+class FakeShardEngine(FakeEngine):
+    """A rank of a tier split with K' Tier-2 shards, each with its own page pool: Tier-1 sees
+    tokens and no KV; Tier-2 shard j holds lanes [off, off + cnt) and sees no tokens."""
+
+    def __init__(self, batch, kv_pages, kp, j):
+        from paper_2501_11779_b200.spec import shard_plan
+        offs, cnts = shard_plan(batch, kp)
+        self.kp, self.j = kp, j
+        self.role = "tier1" if j < 0 else "tier2"
+        self.off, self.cnt = (0, batch) if j < 0 else (offs[j], cnts[j])
+        super().__init__(self.cnt, kv_pages)
+        self.batch = batch
+        self.maps = 0
+
+    def shard(self):
+        return self.j, self.off, self.cnt, self.kp
+
+    def kv_map(self, slot, n):
+        assert self.role == "tier2" and 0 <= slot < self.cnt
+        self.maps += 1
+        super().kv_map(slot, n)
+
+    def kv_unmap(self, slot):
+        assert self.role == "tier2"
+        super().kv_unmap(slot)
+
+    def kv_swap_out(self, slot, n):
+        assert self.role == "tier2" and self.pages[slot] * PAGE >= n
+        self.swaps += 1
+        return [0] * n
+
+    def kv_swap_in(self, slot, n, buf):
+        assert self.role == "tier2" and self.pages[slot] * PAGE >= n and len(buf) == n
+
+    def step_host(self, tok, pos):
+        if self.role == "tier2":
+            assert tok is None and pos is None
+            return None, None
+        # Tier-1: tokens only (its decisions must not depend on their values)
+        return np.array([_next([int(tok[b]), int(pos[b])]) for b in range(self.batch)], np.int32), None
+
+
+@pytest.mark.parametrize("preempt", ["recompute", "swap"])
+def test_on_demand_spmd_decisions_agree_across_ranks(preempt):
+    """Tier split SPMD: every rank runs the dispatcher over the same requests; admission and
+    preemption depend only on lengths and per-shard page accounting, so the Tier-1 rank and each
+    Tier-2 rank take the same number of steps and preemptions, and no shard pool over-commits."""
+    reqs, max_new, B, kp, pages = _requests(12, seed=4), 70, 6, 3, 5
+    runs = []
+    for j in [-1] + list(range(kp)):
+        eng = FakeShardEngine(B, pages, kp, j)
+        d = ContinuousDispatcher(eng, on_demand=True, preempt=preempt)
+        _, steps = d.run(reqs, max_new)
+        runs.append((steps, d.preemptions, eng))
+    assert len({(s, p) for s, p, _ in runs}) == 1, [(s, p) for s, p, _ in runs]
+    assert runs[0][1] > 0
+    for _, _, eng in runs[1:]:
+        assert eng.peak <= pages and eng.maps > 0
+        assert (eng.swaps > 0) == (preempt == "swap") or eng.swaps == 0
