@@ -35,6 +35,7 @@ ROOT = Path(__file__).resolve().parent
 sys.path.insert(0, str(ROOT))
 
 GiB = 1 << 30
+REF_BUDGET_S = 90.0  # --impl reference: wall budget of the timed CPU samples
 
 
 def peaks():
@@ -584,14 +585,21 @@ def main():
         B = wl["batch"] if wl["kp"] == 0 else min(wl["batch"], 64)
         vals = []
         samples = []
-        for _ in range(max(1, min(args.steps, 3))):
+        # W untimed samples, then K timed ones; the timed loop stops early (the line reports the
+        # steps actually run) once it has spent REF_BUDGET_S so the arm ends within minutes
+        for _ in range(args.warmup):
+            cpu_sample(spec, B, wl["ctx"], args.cpu_threads)
+        t_end = time.perf_counter() + REF_BUDGET_S
+        for _ in range(max(1, args.steps)):
             v, sample, cores, _ = cpu_sample(spec, B, wl["ctx"], args.cpu_threads)
             vals.append(v)
             samples.append(sample)
+            if time.perf_counter() > t_end:
+                break
         v = statistics.mean(vals)
         print(json.dumps({
             "impl": "reference", "metric": metric, "value": v, "unit": "tokens/s", "n_gpus": 0,
-            "steps": len(vals), "warmup": 0, "ms_per_step": B / v * 1e3, "higher_is_better": True,
+            "steps": len(vals), "warmup": args.warmup, "ms_per_step": B / v * 1e3, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic", "config": cfg,
             "cpu_baseline": {"value": v, "unit": "tokens/s", "cores": cores, "kind": "port",
                              "sample": samples[-1]},
