@@ -440,7 +440,11 @@ class ContinuousDispatcher:
         seed = np.zeros(B, np.uint32)
         dirty = [sampling is not None]
 
-        swapped = {}                  # request -> (positions saved, next input token, host buffer)
+        swapped = {}                  # request -> (positions saved, next input token, host buffer, shard)
+
+        def recompute(r):             # re-admission feeds the prompt and the tokens generated so far
+            prompt[r] = np.concatenate([np.asarray(requests[r]),
+                                        np.asarray(out[r], dtype=np.asarray(requests[r]).dtype)])
 
         def holds(lane):              # this rank holds the lane's KV
             return role != "tier1" and off <= lane < off + cnt
@@ -449,8 +453,7 @@ class ContinuousDispatcher:
             if r in swapped and swapped[r][3] != lane_shard[lane]:
                 # its context sits in another Tier-2 shard's host buffer: recompute it instead
                 swapped.pop(r)
-                prompt[r] = np.concatenate([np.asarray(requests[r]),
-                                            np.asarray(out[r], dtype=np.asarray(requests[r]).dtype)])
+                recompute(r)
             if r in swapped:
                 return swapped[r][0]
             if on_demand:
@@ -492,8 +495,7 @@ class ContinuousDispatcher:
                 swapped[r] = (t, int(tok[lane]), eng.kv_swap_out(lane - off, t) if holds(lane) else None,
                               lane_shard[lane])
             else:
-                prompt[r] = np.concatenate([np.asarray(requests[r]),
-                                            np.asarray(out[r], dtype=np.asarray(requests[r]).dtype)])
+                recompute(r)
             queue.insert(0, r)
             release(lane)
             self.preemptions += 1
