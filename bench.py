@@ -35,7 +35,6 @@ ROOT = Path(__file__).resolve().parent
 sys.path.insert(0, str(ROOT))
 
 GiB = 1 << 30
-REF_BUDGET_S = 90.0  # --impl reference: wall budget of the timed CPU samples
 
 
 def peaks():
@@ -114,42 +113,60 @@ class Clocks:
 
 
 # ------------------------------------------------------------------ CPU baseline (oracle)
-def cpu_sample(spec, B, ctx, threads=0):
-    """Time the oracle on a bounded sample: embed + 2 layers + classifier of the same shape at
-    batch B and context ctx; extrapolate to all layers.  Returns (tokens/s, sample text, cores)."""
+def _mem_available() -> int:
+    try:
+        for ln in open("/proc/meminfo"):
+            if ln.startswith("MemAvailable:"):
+                return int(ln.split()[1]) * 1024
+    except OSError:
+        pass
+    return 0
+
+
+def cpu_batch(spec, B, ctx):
+    """Largest batch <= B whose oracle state (weights in the storage dtype + the KV of B prompts at
+    max_seq_len) fits in 70 % of the host's available memory."""
+    import paper_2501_11779_b200 as gh
+    w = gh.weights_bytes(spec)
+    kv = gh.kv_bytes_per_prompt(spec, spec.max_seq_len)
+    avail = _mem_available()
+    if not avail:
+        return B
+    return max(1, min(B, int((0.7 * avail - w) // kv)))
+
+
+def cpu_steps(spec, B, ctx, warmup, steps, threads=0):
+    """The CPU reference run of the workload: the oracle (oracle.c, fp32 compute, bf16 storage,
+    OpenMP over all host threads) decodes FULL steps -- embedding, all n_layers layers (F1, F2 over
+    the ctx-position context, F3) and the classifier + greedy argmax -- for B prompts at a fixed
+    context (every step appends at position ctx-1, the GPU bench's steady state), with each step's
+    next tokens fed back.  `warmup` untimed steps, then `steps` timed ones (>= 4
+    steady-state steps; des.hpp:20-21 discards warm-up passes).  Returns (tokens/s, sample text,
+    cores, per-step seconds)."""
     from oracle import Oracle, olib
-    sub = spec.with_(n_layers=2)
-    t_setup = time.time()
-    ora = Oracle(sub, n_slots=B, threads=threads)
+    t0 = time.perf_counter()
+    ora = Oracle(spec, n_slots=B, threads=threads)
     ora.fill_synthetic(99, B, ctx - 1)
-    setup_s = time.time() - t_setup
+    setup_s = time.perf_counter() - t0
     rng = np.random.default_rng(5678)
     tok = rng.integers(0, spec.vocab_size, size=B).astype(np.int32)
     pos = np.full(B, ctx - 1, np.int32)
     slot = np.arange(B, dtype=np.uint32)
-    x, fwd, bwd = ora.buffers(B)
-    x2 = np.zeros_like(x)
-    t0 = time.perf_counter()
-    ora.embed(tok, x)
-    t_emb = time.perf_counter() - t0
-    t_layers = []
-    for layer in range(2):
+    for _ in range(warmup):
+        tok, _ = ora.step(tok, pos, slot, want_logits=False)
+    times = []
+    for _ in range(steps):
         t0 = time.perf_counter()
-        ora.pre(layer, x, pos, fwd)
-        ora.attend(layer, slot, pos, fwd, bwd)
-        ora.post(layer, bwd, x2)
-        t_layers.append(time.perf_counter() - t0)
-        x, x2 = x2, x
-    t0 = time.perf_counter()
-    ora.classify(x, want_logits=False)
-    t_cls = time.perf_counter() - t0
+        tok, _ = ora.step(tok, pos, slot, want_logits=False)
+        times.append(time.perf_counter() - t0)
     ora.close()
-    t_step = t_emb + spec.n_layers * statistics.mean(t_layers) + t_cls
     cores = olib().or_max_threads()
-    sample = (f"oracle.c fp32 on {cores} threads: embed + 2 of {spec.n_layers} layers + classifier at batch {B}, "
-              f"ctx {ctx}; per-layer {statistics.mean(t_layers) * 1e3:.1f} ms x {spec.n_layers} + classifier "
-              f"{t_cls * 1e3:.1f} ms = {t_step:.2f} s/step (setup {setup_s:.1f} s untimed)")
-    return B / t_step, sample, cores, t_step
+    t_step = statistics.mean(times)
+    sample = (f"oracle.c fp32 compute / bf16 storage on {cores} threads: {steps} timed full decode steps "
+              f"(after {warmup} untimed) of batch {B}, context {ctx}: embed + {spec.n_layers} layers + "
+              f"classifier/argmax, {t_step:.2f} s/step (min {min(times):.2f}, max {max(times):.2f}); "
+              f"weights + KV pre-fill {setup_s:.1f} s untimed")
+    return B / t_step, sample, cores, times
 
 
 def cpu_stage_profiles(spec, ctx, batches, threads, out_dir, name):
@@ -582,27 +599,15 @@ def main():
     if args.impl == "reference":
         if world > 1 and rank != 0:
             return
-        B = wl["batch"] if wl["kp"] == 0 else min(wl["batch"], 64)
-        vals = []
-        samples = []
-        # W untimed samples, then K timed ones; the timed loop stops early (the line reports the
-        # steps actually run) once it has spent REF_BUDGET_S so the arm ends within minutes
-        for _ in range(args.warmup):
-            cpu_sample(spec, B, wl["ctx"], args.cpu_threads)
-        t_end = time.perf_counter() + REF_BUDGET_S
-        for _ in range(max(1, args.steps)):
-            v, sample, cores, _ = cpu_sample(spec, B, wl["ctx"], args.cpu_threads)
-            vals.append(v)
-            samples.append(sample)
-            if time.perf_counter() > t_end:
-                break
-        v = statistics.mean(vals)
+        B = cpu_batch(spec, wl["batch"] if wl["kp"] == 0 else min(wl["batch"], 64), wl["ctx"])
+        # exactly W untimed + K timed full decode steps of the workload (no extrapolation)
+        v, sample, cores, times = cpu_steps(spec, B, wl["ctx"], args.warmup, max(1, args.steps), args.cpu_threads)
         print(json.dumps({
             "impl": "reference", "metric": metric, "value": v, "unit": "tokens/s", "n_gpus": 0,
-            "steps": len(vals), "warmup": args.warmup, "ms_per_step": B / v * 1e3, "higher_is_better": True,
+            "steps": len(times), "warmup": args.warmup, "ms_per_step": B / v * 1e3, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic", "config": cfg,
             "cpu_baseline": {"value": v, "unit": "tokens/s", "cores": cores, "kind": "port",
-                             "sample": samples[-1]},
+                             "sample": sample, "batch": B},
             "e2e": {"value": v, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
             "note": "reference has no decode implementation (SURVEY.md §0.2); the CPU arm is the oracle port "
                     "of the paper's CPU Tier-2 path (P:514, OpenMP)"}))
@@ -646,9 +651,12 @@ def main():
         out["step_roofline"] = {"bytes_per_step": step_bytes, "ideal_ms": step_bytes / (hbm * 1e9) * 1e3,
                                 "frac": step_bytes / (hbm * 1e9) / (res["ms"] / 1e3)}
     if not args.no_cpu_baseline and world == 1:  # the CPU baseline is an N = 1 figure (rank 0 only)
-        B = wl["batch"] if wl["kp"] == 0 else min(wl["batch"], 64)
-        v, sample, cores, _ = cpu_sample(spec, B, wl["ctx"], args.cpu_threads)
-        out["cpu_baseline"] = {"value": v, "unit": "tokens/s", "cores": cores, "kind": "port", "sample": sample}
+        B = cpu_batch(spec, wl["batch"] if wl["kp"] == 0 else min(wl["batch"], 64), wl["ctx"])
+        # bounded sample (~10-30 s of CPU work): 1 untimed + 4 timed full steps, the same procedure
+        # as the reference arm
+        v, sample, cores, _ = cpu_steps(spec, B, wl["ctx"], 1, 4, args.cpu_threads)
+        out["cpu_baseline"] = {"value": v, "unit": "tokens/s", "cores": cores, "kind": "port", "sample": sample,
+                               "batch": B}
     print(json.dumps(out))
     if world > 1:
         import torch.distributed as dist

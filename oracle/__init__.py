@@ -68,6 +68,7 @@ def olib() -> C.CDLL:
             "or_classify": (i32, [vp, i32, vp, vp, vp]),
             "or_decode_step": (i32, [vp, vp, i32, vp, vp, vp, vp, vp]),
             "or_set_threads": (None, [i32]),
+            "or_set_sum_order": (None, [i32]),
             "or_max_threads": (i32, []),
             "or_randn": (None, [u64, u64, u64, u64, C.c_double, vp]),
         }
@@ -181,6 +182,12 @@ class Oracle:
     def _rc(rc):
         if rc != 0:
             raise RuntimeError(f"oracle call failed with code {rc}")
+
+
+def set_sum_order(order: int) -> None:
+    """0 = the restatement's summation order; 1 = every fp32 reduction reversed (noise-floor
+    calibration of bf16 parity tolerances, see oracle.c)."""
+    olib().or_set_sum_order(order)
 
 
 def randn(seed, tid, start, n, std):

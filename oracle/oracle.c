@@ -172,6 +172,14 @@ float or_model_weight(const or_model* m, uint32_t layer, int which, uint64_t idx
 }
 
 /* ------------------------------------------------------------------ kernels (fp32 compute) */
+/* Summation order (test calibration only).  0 = the restatement's order.  1 = every fp32 reduction
+ * (GEMM dot products, attention scores, the softmax denominator and P.V, RMSNorm sums of squares)
+ * runs in the reverse order: an equally valid P:514 implementation whose stored bf16 values differ
+ * from order 0 only where a differently ordered fp32 sum rounds across a bf16 boundary.  Order 0 vs
+ * order 1 measures the bf16-storage noise floor the GPU's (split-K / tensor-core) order is held to. */
+static int g_order = 0;
+void or_set_sum_order(int order) { g_order = order; }
+
 /* Y[b][n] = sum_k X[b][k] W[n][k]; X fp32 [B][K] (already storage-rounded), W native dtype */
 static void gemm(const float* X, int B, const void* W, int db, int N, int K, float* Y) {
 #pragma omp parallel
@@ -183,11 +191,20 @@ static void gemm(const float* X, int B, const void* W, int db, int N, int K, flo
       for (int b = 0; b < B; ++b) {
         const float* x = X + (size_t)b * K;
         float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-        int k = 0;
-        for (; k + 8 <= K; k += 8)
-          for (int j = 0; j < 8; ++j) acc[j] += wrow[k + j] * x[k + j];
-        float s = ((acc[0] + acc[1]) + (acc[2] + acc[3])) + ((acc[4] + acc[5]) + (acc[6] + acc[7]));
-        for (; k < K; ++k) s += wrow[k] * x[k];
+        float s;
+        if (g_order == 0) {
+          int k = 0;
+          for (; k + 8 <= K; k += 8)
+            for (int j = 0; j < 8; ++j) acc[j] += wrow[k + j] * x[k + j];
+          s = ((acc[0] + acc[1]) + (acc[2] + acc[3])) + ((acc[4] + acc[5]) + (acc[6] + acc[7]));
+          for (; k < K; ++k) s += wrow[k] * x[k];
+        } else {
+          int k = K;
+          for (; k >= 8; k -= 8)
+            for (int j = 0; j < 8; ++j) acc[j] += wrow[k - 1 - j] * x[k - 1 - j];
+          s = ((acc[7] + acc[6]) + (acc[5] + acc[4])) + ((acc[3] + acc[2]) + (acc[1] + acc[0]));
+          for (; k > 0; --k) s += wrow[k - 1] * x[k - 1];
+        }
         Y[(size_t)b * N + n] = s;
       }
     }
@@ -198,7 +215,10 @@ static void gemm(const float* X, int B, const void* W, int db, int N, int K, flo
 /* y = x * 1/sqrt(mean(x^2)+eps) * g  (g = 1, norms are unit-initialised) */
 static void rmsnorm_row(const float* x, int D, float eps, float* y, int db) {
   float ss = 0.f;
-  for (int i = 0; i < D; ++i) ss += x[i] * x[i];
+  if (g_order == 0)
+    for (int i = 0; i < D; ++i) ss += x[i] * x[i];
+  else
+    for (int i = D - 1; i >= 0; --i) ss += x[i] * x[i];
   const float inv = 1.0f / sqrtf(ss / (float)D + eps);
   for (int i = 0; i < D; ++i) y[i] = rnd(db, x[i] * inv);
 }
@@ -328,13 +348,18 @@ int or_attend(or_kv* c, uint32_t layer, int B, const uint32_t* slot, const int32
       for (int p = 0; p < n; ++p) {
         const size_t kb = kv_index(c, layer, slot[b], 0, kvh, p);
         float s = 0.f;
-        for (int d = 0; d < dh; ++d) s += q[d] * ld(c->arena, db, kb + d);
+        if (g_order == 0)
+          for (int d = 0; d < dh; ++d) s += q[d] * ld(c->arena, db, kb + d);
+        else
+          for (int d = dh - 1; d >= 0; --d) s += q[d] * ld(c->arena, db, kb + d);
         sc[p] = s * scale;
         if (sc[p] > mx) mx = sc[p];
       }
       float den = 0.f;
-      for (int p = 0; p < n; ++p) { sc[p] = expf(sc[p] - mx); den += sc[p]; }
-      for (int p = 0; p < n; ++p) {
+      for (int p = 0; p < n; ++p) sc[p] = expf(sc[p] - mx);
+      for (int i = 0; i < n; ++i) {
+        const int p = g_order == 0 ? i : n - 1 - i;
+        den += sc[p];
         const size_t vb = kv_index(c, layer, slot[b], 1, kvh, p);
         for (int d = 0; d < dh; ++d) o[d] += sc[p] * ld(c->arena, db, vb + d);
       }

@@ -147,7 +147,9 @@ __global__ void __launch_bounds__(AttnCfg<T, DH, W>::kThreads, 1)
       uint32_t it = 0;
       int u = blockIdx.x;
       int L = 0, sl = 0;
-      if (u < n_units) { L = a.pos[u / a.H]; sl = (int)a.slot[u / a.H]; }
+      // positions / slots are read before griddepcontrol.wait only by kv_early callers (whose
+      // predecessor writes neither them nor the arena)
+      if (a.kv_early && u < n_units) { L = a.pos[u / a.H]; sl = (int)a.slot[u / a.H]; }
       // early start: the first unit's cached K / V (independent of the predecessor) fill the
       // free stages before griddepcontrol.wait; stage 0's arrive (with the header) comes after it
       int pre = 0;
@@ -164,6 +166,7 @@ __global__ void __launch_bounds__(AttnCfg<T, DH, W>::kThreads, 1)
         }
       }
       griddep_wait();
+      if (!a.kv_early && u < n_units) { L = a.pos[u / a.H]; sl = (int)a.slot[u / a.H]; }
       while (u < n_units) {
         const int b = u / a.H, h = u % a.H, kvh = h / group;
         // next unit's position / slot, one unit ahead (hides the dependent global loads)

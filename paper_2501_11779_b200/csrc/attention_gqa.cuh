@@ -467,7 +467,9 @@ __global__ void __launch_bounds__(GqaTcCfg<G>::kThreads, 1)
       uint32_t it = 0;
       int u = blockIdx.x;
       int L = 0, sl = 0;
-      if (u < n_units) { L = a.pos[u / a.Hkv]; sl = (int)a.slot[u / a.Hkv]; }
+      // positions / slots are read before griddepcontrol.wait only by kv_early callers, which
+      // promise that the preceding kernel writes neither them nor the arena
+      if (a.kv_early && u < n_units) { L = a.pos[u / a.Hkv]; sl = (int)a.slot[u / a.Hkv]; }
       int pre = 0;  // stages of the first unit whose K / V were requested before the wait
       if (a.kv_early && u < n_units && L > 0) {
         const int g = u % a.Hkv;
@@ -487,6 +489,7 @@ __global__ void __launch_bounds__(GqaTcCfg<G>::kThreads, 1)
         }
       }
       griddep_wait();
+      if (!a.kv_early && u < n_units) { L = a.pos[u / a.Hkv]; sl = (int)a.slot[u / a.Hkv]; }
       while (u < n_units) {
         const int b = u / a.Hkv, g = u % a.Hkv;
         const int un = next_unit(a, u);
@@ -682,8 +685,13 @@ __global__ void __launch_bounds__(GqaTcCfg<G>::kThreads, 1)
         l = l * corr + e0 + e1;
         m = mn;
 #pragma unroll
-        for (int j = 0; j < 16; ++j) { o[j][0] *= corr; o[j][1] *= corr; }
-        const uint32_t pa = pack_bf16x2(e0, e1);        // P as the A operand (rows 8..15 zero)
+        for (int j = 0; j < 16; ++j) { o[j][0] *= corr; o[j][1] *= corr; o[j][2] *= corr; o[j][3] *= corr; }
+        // P as the A operand: rows 0..7 = bf16(P); rows 8..15 (no query head lives there) = the
+        // rounding residual bf16(P - bf16(P)).  Accumulator rows r and r + 8 of one lane then sum
+        // to (bf16(P) + residual) V, i.e. P V with P exact to ~2^-17 relative at no extra MMA:
+        // the fp32-compute rule of P:514, consistent with l, which sums the same unrounded P.
+        const uint32_t pa = pack_bf16x2(e0, e1);
+        const uint32_t pl = pack_bf16x2(e0 - __uint_as_float(pa << 16), e1 - __uint_as_float(pa & 0xffff0000u));
         // ---- O += P Vw (V fragments by ldmatrix.trans: 4 d_h tiles of 8 per instruction)
 #pragma unroll
         for (int dg = 0; dg < 4; ++dg) {
@@ -692,10 +700,10 @@ __global__ void __launch_bounds__(GqaTcCfg<G>::kThreads, 1)
               st + 2 * C::kBox + (chunk >> 3) * C::kBox + prow * 128 + (((chunk & 7) ^ (prow & 7)) << 4);
           uint32_t v0, v1, v2, v3;
           ldsm_x4_t(addr, v0, v1, v2, v3);
-          mma_1688(o[dg * 4 + 0], pa, 0u, v0);
-          mma_1688(o[dg * 4 + 1], pa, 0u, v1);
-          mma_1688(o[dg * 4 + 2], pa, 0u, v2);
-          mma_1688(o[dg * 4 + 3], pa, 0u, v3);
+          mma_1688(o[dg * 4 + 0], pa, pl, v0);
+          mma_1688(o[dg * 4 + 1], pa, pl, v1);
+          mma_1688(o[dg * 4 + 2], pa, pl, v2);
+          mma_1688(o[dg * 4 + 3], pa, pl, v3);
         }
       }
       __syncwarp();
@@ -709,7 +717,7 @@ __global__ void __launch_bounds__(GqaTcCfg<G>::kThreads, 1)
     if (qr < G) {
       float* wb = cbuf + (cw * G + qr) * (DH + 2);
 #pragma unroll
-      for (int j = 0; j < 16; ++j) { wb[j * 8 + qc] = o[j][0]; wb[j * 8 + qc + 1] = o[j][1]; }
+      for (int j = 0; j < 16; ++j) { wb[j * 8 + qc] = o[j][0] + o[j][2]; wb[j * 8 + qc + 1] = o[j][1] + o[j][3]; }
       if ((lane & 3) == 0) { wb[DH] = m; wb[DH + 1] = l; }
     }
     if (cw == 0 && lane == 0) { comb_bg[2 * cb] = b; comb_bg[2 * cb + 1] = g; }

@@ -59,3 +59,23 @@ def test_paged_workload_fits_every_tier2_gpu():
         assert used <= pages
     assert sh * kp * 2 > 510            # more than the 510 contiguous C3 slots at K' = 3
     assert sh * kp * 2 <= 1024
+
+
+def test_cpu_steps_runs_exact_full_steps(bench):
+    """The CPU reference arm times exactly K full decode steps (all layers + classifier) after W
+    untimed ones: no per-layer extrapolation."""
+    import paper_2501_11779_b200 as gh
+    spec = gh.TINY.with_(n_layers=2, max_seq_len=32)
+    v, sample, cores, times = bench.cpu_steps(spec, 4, 16, 1, 3, threads=2)
+    assert len(times) == 3 and all(t > 0 for t in times)
+    assert abs(v - 4 / (sum(times) / 3)) < 1e-9 * v
+    assert "3 timed full decode steps" in sample and "2 layers" in sample
+
+
+def test_cpu_batch_respects_host_memory(bench, monkeypatch):
+    import paper_2501_11779_b200 as gh
+    spec = gh.CONFIGS["C3"]["spec"]          # 1 GiB of KV per prompt at 2048 positions
+    monkeypatch.setattr(bench, "_mem_available", lambda: 64 << 30)
+    B = bench.cpu_batch(spec, 64, 2048)
+    assert 1 <= B < 64
+    assert gh.weights_bytes(spec) + B * gh.kv_bytes_per_prompt(spec, 2048) <= 0.7 * (64 << 30)
