@@ -269,9 +269,17 @@ def workload(args, world):
         return dict(name=cfg, spec=spec, ctx=ctx, batch=c["batch"], requested=c["batch"], inflight=1,
                     shard=c["batch"], kp=0)
     n1 = max(1, args.tier1)
-    if (world - n1) % n1 or world <= n1:
-        raise SystemExit(f"--tier1 {n1}: world size {world} must be tier1 * (1 + K')")
-    kp = (world - n1) // n1  # Tier-2 GPUs per Tier-1 span
+    tp = max(1, args.tier1_tp)
+    if tp > 1:  # Tier-1 tensor parallelism: ranks 0..tp-1 share every layer, the rest are Tier-2
+        if n1 > 1:
+            raise SystemExit("--tier1-tp and --tier1 (pipeline spans) are exclusive")
+        if world <= tp:
+            raise SystemExit(f"--tier1-tp {tp}: world size {world} must be > {tp}")
+        kp = world - tp
+    else:
+        if (world - n1) % n1 or world <= n1:
+            raise SystemExit(f"--tier1 {n1}: world size {world} must be tier1 * (1 + K')")
+        kp = (world - n1) // n1  # Tier-2 GPUs per Tier-1 span
     if cfg == "C2":  # weak scaling of the N=1 workload: 64 prompts per Tier-2 GPU per in-flight batch
         shard = args.shard or c["batch"]
         IF = args.inflight or if_gh_from_profiles(spec, shard * kp, shard, ctx)
@@ -460,14 +468,15 @@ def run_split(args, wl, rank, world):
     dist.broadcast_object_list(obj, src=0)
     comm = Comm(obj[0], world, rank, dev)
     eng = Engine(spec, batch=wl["batch"], inflight=IF, device=dev, use_graph=False, comm=comm,
-                 transport=args.transport, tier1_ranks=max(1, args.tier1), kv_pages=wl.get("kv_pages", 0))
+                 transport=args.transport, tier1_ranks=max(1, args.tier1), kv_pages=wl.get("kv_pages", 0),
+                 tier1_tp=max(1, args.tier1_tp))
     transport = eng.transport
     lib = gh.lib()
     stream = torch.cuda.Stream()
     ctxs = wl.get("ctxs")  # paged: per-prompt contexts [IF, batch]
     if eng.role == "tier2":
         if ctxs is not None:  # back each local slot with the pages of its own context
-            j, sh = rank - 1, wl["shard"]
+            j, sh = rank - max(1, args.tier1_tp), wl["shard"]
             for ib in range(IF):
                 for r in range(sh):
                     eng.kv_map(ib * sh + r, int(ctxs[ib, j * sh + r]) + 1)
@@ -553,6 +562,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--tier1", type=int, default=1,
                     help="tier split: Tier-1 pipeline stages (layer spans, each with its own Tier-2 GPUs)")
+    ap.add_argument("--tier1-tp", type=int, default=1,
+                    help="tier split: Tier-1 tensor parallelism over this many GPUs (SURVEY 8f-3); the rest are Tier-2")
     ap.add_argument("--shard", type=int, default=0,
                     help="C2 tier split: prompts per Tier-2 GPU per in-flight batch (default 64, the N=1 batch)")
     ap.add_argument("--inflight", type=int, default=0,
@@ -575,7 +586,10 @@ def main():
     metric = "decode tokens/s (Llama-2-7B shape, 2-tier split)"
     cfg = {"workload": f"{wl['name']}: {spec.name} shape random-init, context {wl['ctx']}, "
                        + ("both tiers colocated on 1 GPU" if wl["kp"] == 0 else
-                          (f"Tier-1 on 1 GPU + Tier-2 KV sharded by prompt over {wl['kp']} GPUs, IF={wl['inflight']}"
+                          (f"Tier-1 tensor-parallel over {args.tier1_tp} GPUs (W_o / W_2 all-reduced in the GEMM "
+                           f"epilogue over NVLink) + Tier-2 KV sharded by prompt over {wl['kp']} GPUs, IF={wl['inflight']}"
+                           if args.tier1_tp > 1 else
+                           f"Tier-1 on 1 GPU + Tier-2 KV sharded by prompt over {wl['kp']} GPUs, IF={wl['inflight']}"
                            if args.tier1 <= 1 else
                            f"Tier-1 pipelined over {args.tier1} GPUs (layer spans), each span with "
                            f"{wl['kp']} Tier-2 GPUs holding its layers' KV, IF={wl['inflight']}")),

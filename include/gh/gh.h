@@ -105,6 +105,22 @@ gh_status gh_batch_grid(uint64_t max_batch, uint64_t* out, uint64_t cap, uint64_
 /* Tier split of a Tier-1 batch over K' Tier-2 ranks: balanced shards differing by at most one
  * prompt (analytic.cpp:119), lower ranks first; off/cnt arrays of length kp. */
 gh_status gh_shard_plan(uint64_t batch, uint64_t kp, uint64_t* off, uint64_t* cnt);
+/* Rank layout of the engine's tier split (host only; gh_engine_create uses exactly this):
+ * world = T + n1 * K' ranks.  Tier-1 ranks come first -- n1 = tier1_ranks pipeline spans
+ * (layer_spans, optimizer.cpp:116-123) or T = tier1_tp tensor-parallel ranks sharing every layer
+ * -- then K' Tier-2 ranks per span, rank T + s*K' + j holding prompt shard j
+ * (gh_shard_plan, analytic.cpp:119) of span s's layers.  world 1 = colocated. */
+typedef struct gh_rank_layout {
+  int role;                 /* 0 colocated, 1 Tier-1, 2 Tier-2 */
+  int span;                 /* Tier-1 pipeline span served */
+  int tp_rank;              /* Tier-1 tensor-parallel slice (0 without TP) */
+  int shard;                /* Tier-2: shard index within its span; -1 otherwise */
+  uint32_t kp;              /* Tier-2 ranks per span (K'); 0 colocated */
+  uint32_t layer_begin, layer_end;
+  uint32_t row_off, row_cnt;  /* rows of each in-flight batch whose KV this rank holds (Tier-2) */
+} gh_rank_layout;
+gh_status gh_engine_layout(uint32_t world, uint32_t rank, uint32_t tier1_ranks, uint32_t tier1_tp,
+                           uint64_t n_layers, uint32_t batch, gh_rank_layout* out);
 /* Throughput identity B_total*IF/mean(TBT) (des.cpp:298-310); gen_ts in ns. */
 gh_status gh_throughput_from(const int64_t* gen_ts_ns, uint64_t n, uint64_t batch_total,
                              uint64_t inflight, double* tokens_per_s);
@@ -237,6 +253,17 @@ typedef struct gh_engine_config {
   uint32_t kv_pages;       /* 0: contiguous slots of max_seq_len positions; > 0: paged KV arena of
                               kv_pages pages of GH_KV_PAGE_POSITIONS positions shared by the slots
                               (gh_tier2_create_paged; map with gh_engine_kv_map before a step) */
+  uint32_t tier1_tp;       /* tier split: Tier-1 tensor parallelism (0/1 = none; SURVEY 8f-3,
+                              if_tp analytic.cpp:22-29).  Ranks 0..T-1 each hold a head slice of
+                              W_q/W_k/W_v and the matching input columns of W_o, and a hidden-unit
+                              slice of W_1/W_3 and the matching input columns of W_2, for every
+                              layer; W_o and W_2 are all-reduced inside their GEMM epilogue over
+                              NVLink peer stores with per-slice flags (no NCCL).  Ranks T.. are the
+                              K' = world - T Tier-2 ranks; the inter-tier messages are the
+                              PayloadModel rows cut into T head blocks ([x_r|q_r|k_r|v_r] from
+                              rank r, [x_r|attn_r] back to it).  bf16, head dim 128, peer
+                              transport, gh_engine_step_all / step_all_host only; every Tier-1 rank
+                              decodes the same tokens (feed them the same host tokens). */
 } gh_engine_config;
 
 /* Inter-tier message transport of the pipelined tier-split step.
@@ -279,6 +306,11 @@ gh_status gh_engine_io(gh_engine* e, uint32_t ib, int32_t** tok, int32_t** pos,
 gh_status gh_engine_advance(gh_engine* e, uint32_t ib, int pos_increment, void* stream);
 /* Copy the next tokens of in-flight batch ib to host (synchronous; Tier-1 / colocated only). */
 gh_status gh_engine_read_next(gh_engine* e, uint32_t ib, int32_t* next_host);
+/* keep != 0: every classifier run of the engine also writes the fp32 logits [B, V] of its batch
+ * (off by default: the argmax epilogue then stores no logits); gh_engine_read_logits copies the
+ * last ones of batch ib to host (synchronous; Tier-1 ranks that own the classifier). */
+gh_status gh_engine_keep_logits(gh_engine* e, int keep);
+gh_status gh_engine_read_logits(gh_engine* e, uint32_t ib, float* logits_host);
 gh_tier1* gh_engine_tier1(gh_engine* e);
 gh_tier2* gh_engine_tier2(gh_engine* e);
 /* Paged KV (kv_pages > 0): gh_tier2_map / gh_tier2_unmap of this rank's Tier-2 (slot = ib * batch

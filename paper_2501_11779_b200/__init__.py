@@ -6,12 +6,12 @@ the C ABI in include/gh/gh.h (libgh.so, built in-tree); this package is the Pyth
 from ._lib import (CudaError, FeasibilityError, GhError, NcclError, UnsupportedError, ValidationError,
                    lib)
 from .spec import (CONFIGS, LLAMA2_7B, LLAMA2_13B, LLAMA2_70B, TINY, ModelSpec, attention_footprint,
-                   batch_grid, kv_bytes_per_prompt, layer_spans, node_weight_bytes, nonattention_footprint,
+                   batch_grid, engine_layout, kv_bytes_per_prompt, layer_spans, node_weight_bytes, nonattention_footprint,
                    payload, shard_plan, throughput_from, two_tier_context_slots, weights_bytes)
 
 __all__ = [
     "CONFIGS", "LLAMA2_7B", "LLAMA2_13B", "LLAMA2_70B", "TINY", "ModelSpec", "attention_footprint",
-    "batch_grid", "kv_bytes_per_prompt", "layer_spans", "node_weight_bytes", "nonattention_footprint",
+    "batch_grid", "engine_layout", "kv_bytes_per_prompt", "layer_spans", "node_weight_bytes", "nonattention_footprint",
     "payload", "shard_plan", "throughput_from", "two_tier_context_slots", "weights_bytes", "GhError", "ValidationError",
     "FeasibilityError", "CudaError", "NcclError", "UnsupportedError", "lib",
 ]

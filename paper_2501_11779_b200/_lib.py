@@ -64,7 +64,14 @@ class GhEngineConfig(C.Structure):
                 ("transport", C.c_int),
                 ("tier1_ranks", C.c_uint32),
                 ("prefill", C.c_int),
-                ("kv_pages", C.c_uint32)]
+                ("kv_pages", C.c_uint32),
+                ("tier1_tp", C.c_uint32)]
+
+
+class GhRankLayout(C.Structure):
+    _fields_ = [("role", C.c_int), ("span", C.c_int), ("tp_rank", C.c_int), ("shard", C.c_int),
+                ("kp", C.c_uint32), ("layer_begin", C.c_uint32), ("layer_end", C.c_uint32),
+                ("row_off", C.c_uint32), ("row_cnt", C.c_uint32)]
 
 
 u64, u32, i32, i64, vp = C.c_uint64, C.c_uint32, C.c_int32, C.c_int64, C.c_void_p
@@ -124,6 +131,9 @@ PROTOTYPES = {
     "gh_engine_io": (st, [vp, u32, P(vp), P(vp), P(vp), P(vp)]),
     "gh_engine_advance": (st, [vp, u32, C.c_int, vp]),
     "gh_engine_read_next": (st, [vp, u32, vp]),
+    "gh_engine_layout": (st, [u32, u32, u32, u32, u64, u32, P(GhRankLayout)]),
+    "gh_engine_keep_logits": (st, [vp, C.c_int]),
+    "gh_engine_read_logits": (st, [vp, u32, vp]),
     "gh_engine_tier1": (vp, [vp]),
     "gh_engine_tier2": (vp, [vp]),
     "gh_engine_kv_map": (st, [vp, u32, u32]),

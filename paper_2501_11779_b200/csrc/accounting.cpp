@@ -154,6 +154,55 @@ gh_status gh_shard_plan(uint64_t batch, uint64_t kp, uint64_t* off, uint64_t* cn
   return GH_OK;
 }
 
+// Rank layout of a tier split (the engine's decomposition, host only): Tier-1 pipeline spans
+// (layer_spans, optimizer.cpp:116-123) or Tier-1 tensor-parallel ranks, then K'
+// Tier-2 ranks per span holding balanced prompt shards (analytic.cpp:119).
+gh_status gh_engine_layout(uint32_t world, uint32_t rank, uint32_t tier1_ranks, uint32_t tier1_tp,
+                           uint64_t n_layers, uint32_t batch, gh_rank_layout* out) {
+  if (!out) return fail(GH_EINVAL, "null argument");
+  if (world == 0 || rank >= world) return fail(GH_EINVAL, "rank outside the world");
+  gh_rank_layout L{};
+  const uint32_t n1 = tier1_ranks > 1 ? tier1_ranks : 1, tp = tier1_tp > 1 ? tier1_tp : 1;
+  L.tp_rank = 0;
+  L.shard = -1;
+  L.layer_begin = 0;
+  L.layer_end = (uint32_t)n_layers;
+  L.row_off = 0;
+  L.row_cnt = batch;
+  if (world == 1) {
+    if (tp > 1 || n1 > 1) return fail(GH_EINVAL, "Tier-1 spans / tensor parallelism need a tier split");
+    L.role = 0;
+    L.span = 0;
+    L.kp = 0;
+    *out = L;
+    return GH_OK;
+  }
+  if (tp > 1 && n1 > 1) return fail(GH_EUNSUPPORTED, "tier1_tp and tier1_ranks (pipeline spans) together");
+  const uint32_t t1 = tp > 1 ? tp : n1;  // Tier-1 ranks
+  if (world <= t1 || (world - t1) % n1) return fail(GH_EINVAL, "world size must be T + n1 * K' with K' >= 1");
+  if (n1 > n_layers) return fail(GH_EINVAL, "more Tier-1 spans than layers");
+  L.kp = (world - t1) / n1;
+  if (batch < L.kp) return fail(GH_EINVAL, "batch smaller than the number of Tier-2 ranks");
+  L.role = rank < t1 ? 1 : 2;
+  L.span = rank < t1 ? (tp > 1 ? 0 : (int)rank) : (int)((rank - t1) / L.kp);
+  if (tp > 1 && rank < t1) L.tp_rank = (int)rank;
+  std::vector<uint64_t> spans(n1);
+  GH_TRY(gh_layer_spans(n_layers, n1, spans.data()));
+  uint64_t l0 = 0;
+  for (int s = 0; s < L.span; ++s) l0 += spans[s];
+  L.layer_begin = (uint32_t)l0;
+  L.layer_end = (uint32_t)(l0 + spans[L.span]);
+  if (L.role == 2) {
+    L.shard = (int)((rank - t1) % L.kp);
+    std::vector<uint64_t> off(L.kp), cnt(L.kp);
+    GH_TRY(gh_shard_plan(batch, L.kp, off.data(), cnt.data()));
+    L.row_off = (uint32_t)off[L.shard];
+    L.row_cnt = (uint32_t)cnt[L.shard];
+  }
+  *out = L;
+  return GH_OK;
+}
+
 // throughput_from (des.cpp:298-310)
 gh_status gh_throughput_from(const int64_t* ts, uint64_t n, uint64_t batch_total,
                              uint64_t inflight, double* tps) {

@@ -456,8 +456,13 @@ __global__ void __launch_bounds__(GqaTcCfg<G>::kThreads, 1)
   const bf16_t* fwd = (const bf16_t*)a.msg_fwd;
   bf16_t* bwd = (bf16_t*)a.msg_bwd;
   bf16_t* arena = (bf16_t*)a.arena;
-  const long ld_fwd = 2L * a.D + 2L * a.Dkv;
-  const long ld_bwd = 2L * a.D;
+  // message rows: tp head blocks (AttnArgs::tp); tp = 1 is the plain PayloadModel row
+  const int tp = a.tp > 1 ? a.tp : 1;
+  const int gpb = a.Hkv / tp;                 // KV heads per block
+  const long wf = (2L * a.D + 2L * a.Dkv) / tp, wb = 2L * a.D / tp;
+  const long Dt = a.D / tp, Dkvt = a.Dkv / tp;
+  auto frow = [&](int b, int g) { return fwd + ((long)(g / gpb) * a.B + b) * wf; };
+  auto brow = [&](int b, int g) { return bwd + ((long)(g / gpb) * a.B + b) * wb; };
   constexpr uint32_t hdr_bytes = (uint32_t)((2 * G + 2) * DH * 2);
 
   if (warp == 0) {
@@ -521,12 +526,13 @@ __global__ void __launch_bounds__(GqaTcCfg<G>::kThreads, 1)
             tma_load_3d(st + 3 * C::kBox, &tmKV, 64, p0, row_v, &full[s], pol);
           }
           if (c == 0) {
-            const bf16_t* row = fwd + (long)b * ld_fwd;
+            const bf16_t* row = frow(b, g);
+            const long gl = g % gpb;
             constexpr uint32_t gq = (uint32_t)(G * DH * 2);
-            bulk_g2s(hdr, row + a.D + (long)g * G * DH, gq, &full[s], pol);                      // q of the group
-            bulk_g2s(hdr + gq, row + 2L * a.D + (long)g * DH, DH * 2, &full[s], pol);            // new k
-            bulk_g2s(hdr + gq + DH * 2, row + 2L * a.D + a.Dkv + (long)g * DH, DH * 2, &full[s], pol);  // new v
-            bulk_g2s(hdr + gq + 2 * DH * 2, row + (long)g * G * DH, gq, &full[s], pol);          // x slices
+            bulk_g2s(hdr, row + Dt + gl * G * DH, gq, &full[s], pol);                     // q of the group
+            bulk_g2s(hdr + gq, row + 2 * Dt + gl * DH, DH * 2, &full[s], pol);            // new k
+            bulk_g2s(hdr + gq + DH * 2, row + 2 * Dt + Dkvt + gl * DH, DH * 2, &full[s], pol);  // new v
+            bulk_g2s(hdr + gq + 2 * DH * 2, row + gl * G * DH, gq, &full[s], pol);        // x slices
           }
         }
         u = un;
@@ -569,7 +575,7 @@ __global__ void __launch_bounds__(GqaTcCfg<G>::kThreads, 1)
           den += cbuf[(w * G + hq) * (DH + 2) + DH + 1] * f[w];
         }
         const float inv = 1.f / den;
-        bf16_t* orow = bwd + (long)b * ld_bwd + a.D + (long)(g * G + hq) * DH;
+        bf16_t* orow = brow(b, g) + Dt + (long)((g % gpb) * G + hq) * DH;
         for (int d = lane; d < DH; d += 32) {
           float acc = 0.f;
 #pragma unroll
@@ -651,7 +657,7 @@ __global__ void __launch_bounds__(GqaTcCfg<G>::kThreads, 1)
     }
     if (cw == C::kW - 1) {
       for (int i = lane; i < G * DH / 8; i += 32)
-        *((uint4*)(bwd + (long)b * ld_bwd + (long)g * G * DH) + i) = ((const uint4*)hx)[i];
+        *((uint4*)(brow(b, g) + (long)(g % gpb) * G * DH) + i) = ((const uint4*)hx)[i];
     }
 
     for (int c = 0; c < nch; ++c, ++it) {

@@ -226,6 +226,20 @@ GH_DEV void flag_wait(const unsigned int* flag, unsigned int target) {
   }
 }
 
+// System-scope flags between GPUs (NVLink peer mappings): release store into a peer's flag word,
+// acquire spin on a local flag word that peers write.
+GH_DEV void flag_store_release_sys(unsigned int* flag, unsigned int v) {
+  asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(flag), "r"(v) : "memory");
+}
+GH_DEV void flag_wait_sys(const unsigned int* flag, unsigned int target) {
+  unsigned int v;
+  for (;;) {
+    asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(flag) : "memory");
+    if ((int)(v - target) >= 0) break;  // sequence numbers (wrap-safe)
+    __nanosleep(32);
+  }
+}
+
 // ------------------------------------------------------------------ bulk / tensor copies (TMA)
 // 1-D bulk copy global -> shared, completion signalled on an mbarrier (SASS: UBLKCP).
 GH_DEV void bulk_g2s(void* smem_dst, const void* gmem_src, uint32_t bytes, uint64_t* bar,

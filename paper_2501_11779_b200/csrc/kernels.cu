@@ -72,7 +72,8 @@ __global__ void init_weight_kernel(T* dst, uint64_t n_phys, int N, int K, int KB
         seg = 0; r = n;
         while (seg + 1 < sg.n && r >= sg.rows[seg]) { r -= sg.rows[seg]; ++seg; }
       }
-      v = randn_scaled(sg.base[seg], (uint64_t)r * K + k, sg.k[seg]);
+      const uint64_t ldk = sg.ldk ? (uint64_t)sg.ldk : (uint64_t)K;
+      v = randn_scaled(sg.base[seg], (uint64_t)(sg.row0[seg] + r) * ldk + (uint64_t)(sg.k0 + k), sg.k[seg]);
     }
     St<T>::store(dst, i, v);
   }
@@ -616,6 +617,20 @@ GemmPlan plan_gemm(int N, int K, int Bt) {
   return p;
 }
 
+GemmPlan plan_gemm_tp(int N, int K, int Bt) {
+  const int KB = (K + kBlockK - 1) / kBlockK;
+  const int bt_cap = std::min(Bt, 128);
+  int bn = 128;
+  for (int b : kBNs) if (b >= bt_cap) { bn = b; break; }
+  double best = 0;
+  GemmPlan p = plan_splitk(N, KB, Bt, bn, &best);
+  static const bool verbose = getenv("GH_GEMM_VERBOSE") != nullptr;  // diagnostics
+  if (verbose)
+    fprintf(stderr, "[gh] gemm (tp all-reduce) N=%d K=%d B=%d: split-K BN=%d b_tiles=%d n_tiles=%d C=%d clusters=%d\n",
+            N, K, Bt, p.BN, p.b_tiles, p.n_tiles, p.C, p.n_clusters);
+  return p;
+}
+
 template <int BN>
 static cudaError_t configure_tc() {
   return cudaFuncSetAttribute(gemm_tc_kernel<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
@@ -794,14 +809,16 @@ static cudaError_t launch_attn_t(const AttnArgs& a, cudaStream_t st) {
   // byte than the CUDA-core dot products, which holds the bandwidth under the 1000 W cap
   // (sustained 6.96 vs 6.53 TB/s at 7B, B 85, ctx 2048)
   static const bool mha_cc = getenv("GH_MHA_CUDA_CORE") != nullptr;  // diagnostics: CUDA-core MHA kernel
+  const bool head_blocks = a.tp > 1;  // tensor-parallel message layout: the tensor-core kernel only
   if constexpr (sizeof(T) == 2 && DH == 128) {
-    if (a.kv_tmap && !no_tc) switch (gqa_group(a)) {
+    if (a.kv_tmap && (!no_tc || head_blocks)) switch (gqa_group(a)) {
         case 2: return launch_attn_gqa_tc<2>(a, st);
         case 4: return launch_attn_gqa_tc<4>(a, st);
         case 8: return launch_attn_gqa_tc<8>(a, st);
       }
-    if (a.kv_tmap && !no_tc && !mha_cc && a.H == a.Hkv) return launch_attn_gqa_tc<1>(a, st);
+    if (a.kv_tmap && (head_blocks || (!no_tc && !mha_cc)) && a.H == a.Hkv) return launch_attn_gqa_tc<1>(a, st);
   }
+  if (head_blocks) return cudaErrorNotSupported;
   switch (gqa_group(a)) {
     case 2: return launch_attn_gqa<T, DH, 2>(a, st);
     case 4: return launch_attn_gqa<T, DH, 4>(a, st);

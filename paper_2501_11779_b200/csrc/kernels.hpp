@@ -32,6 +32,11 @@ struct RowSegs {
   float k[3];         // sqrt(3) * std / 2^24 per segment
   int n = 1;
   int interleave2 = 0;
+  // Tensor-parallel slice of the logical tensors: physical (r, k) of segment s is logical
+  // (row0[s] + r, k0 + k) of a matrix with ldk logical columns (0 = K, no slicing).
+  int row0[3] = {0, 0, 0};
+  int k0 = 0;
+  int ldk = 0;
 };
 
 // Per-GEMM launch plan chosen on the host: batch tile and persistent cluster split-K grid.
@@ -52,6 +57,10 @@ struct GemmPlan {
 // uses the pair kernel, whose scale table holds 1024 columns, for every batch above 256).
 constexpr int kFusedNormMaxBatch = 1024;
 GemmPlan plan_gemm(int N, int K, int Bt);
+// Plan of a GEMM whose epilogue all-reduces across tensor-parallel ranks: the cluster split-K
+// kernel with batch tiles of at most 128 columns (every rank runs the identical plan, so the
+// slices the ranks exchange coincide)
+GemmPlan plan_gemm_tp(int N, int K, int Bt);
 
 // Scratch shared by every GEMM of a tier (SIMT staging, diagnostics).
 struct GemmScratch {

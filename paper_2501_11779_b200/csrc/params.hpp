@@ -40,7 +40,20 @@ struct EpiParams {
   const void* xcopy_src;
   long xcopy_ld;
   int xcopy_rows;
+  // Tier-1 tensor parallelism: all-reduce of the tp_n ranks' fp32 partial outputs
+  // inside the epilogue (W_o and W_2, STORE_RESID).  The owner of each output slice stores its
+  // partial into every rank's receive buffer tp_dst[p] ([tp_n][Bt][N] fp32; p == tp_rank is the
+  // local one) over NVLink peer mappings, releases a per-slice flag tp_flag_dst[p][slice][tp_rank]
+  // = tp_seq, acquires the peers' flags in its own tp_flags, and sums the tp_n partials in rank
+  // order (identical on every rank), then adds the residual.  tp_n <= 1: no exchange.
+  int tp_n;
+  int tp_rank;
+  unsigned int tp_seq;
+  float* tp_dst[4];
+  unsigned int* tp_flag_dst[4];
+  const unsigned int* tp_flags;
 };
+constexpr int kMaxTp = 4;
 
 struct GemmShape {
   int N, K, Bt;         // weight rows, reduction length, batch
@@ -91,6 +104,11 @@ struct AttnArgs {
   // 1: the kernel's predecessor writes neither the arena nor pos / slot (the QKV GEMM or a stream
   // wait), so the first unit's cached keys / values may be requested before griddepcontrol.wait
   int kv_early;
+  // Tier-1 tensor parallelism over tp ranks (1 = none): the messages are the PayloadModel rows cut
+  // into tp head blocks, block r = the columns of Tier-1 rank r:
+  //   fwd [tp][B][(2D + 2Dkv)/tp] = [x_r | q_r | k_r | v_r],   bwd [tp][B][2D/tp] = [x_r | attn_r]
+  // (tp = 1: the plain [x|q|k|v] / [x|attn] rows).  Same bytes per token.
+  int tp;
 };
 // Positions per KV page of the paged arena (one 64-position TMA box / attention stage).
 constexpr int kKvPagePositions = 64;

@@ -102,6 +102,20 @@ struct gh_tier1 {
   Shape sh;
   int device = 0;
   uint32_t l0 = 0, l1 = 0, max_batch = 0;
+  // Tier-1 tensor parallelism: this object holds rank tp_rank's slice of every layer
+  // (heads [r H/T, (r+1) H/T) of W_q / W_k / W_v and the matching input columns of W_o; hidden
+  // units [r Dh/T, (r+1) Dh/T) of W_1 / W_3 and the matching input columns of W_2), the embedding
+  // and classifier whole.  W_o and W_2 are all-reduced inside their GEMM epilogue (tp_allreduce).
+  int tp = 1, tp_rank = 0;
+  struct TpCtx {
+    float* buf[2] = {nullptr, nullptr};  // receive buffers [tp][max_batch][D] fp32 (reduce parity)
+    unsigned int* flags = nullptr;       // [kTpFlagSlices][kMaxTp] sequence numbers written by peers
+    float* peer_buf[2][kMaxTp] = {};     // rank p's receive buffers (p == tp_rank: local)
+    unsigned int* peer_flags[kMaxTp] = {};
+    unsigned int seq = 0;                // all-reduces issued (identical on every rank)
+    bool ready = false;                  // peer mappings in place (engine peer setup)
+  } tpc;
+  static constexpr int kTpFlagSlices = 1 << 14;
   std::vector<std::unique_ptr<DevMem>> mem;
   struct Layer {
     Weight qkv, o, w13, w2;
@@ -120,12 +134,13 @@ struct gh_tier1 {
   float2* part = nullptr;
   GemmScratch gsc;
   TmapCache tmaps;
-  std::map<std::tuple<int, int, int>, GemmPlan> plans;
+  std::map<std::tuple<int, int, int, bool>, GemmPlan> plans;
 
-  const GemmPlan& plan(int N, int K, int B) {
-    auto key = std::make_tuple(N, K, B);
+  // tp: a GEMM whose epilogue all-reduces across the TP ranks (plan_gemm_tp)
+  const GemmPlan& plan(int N, int K, int B, bool tp_reduce = false) {
+    auto key = std::make_tuple(N, K, B, tp_reduce);
     auto it = plans.find(key);
-    if (it == plans.end()) it = plans.emplace(key, plan_gemm(N, K, B)).first;
+    if (it == plans.end()) it = plans.emplace(key, tp_reduce ? plan_gemm_tp(N, K, B) : plan_gemm(N, K, B)).first;
     return it->second;
   }
   // X: [B, K] with row stride ldx
@@ -133,7 +148,8 @@ struct gh_tier1 {
   // L2 during this GEMM's tail (gemm_tc.cuh, GemmShape::pf)
   gh_status gemm(const Weight& W, const CUtensorMap* tmW, const void* X, long ldx, int B,
                  const EpiParams& ep, cudaStream_t st, const Weight* next = nullptr) {
-    const GemmPlan& p = plan(W.N, W.K, B);
+    const GemmPlan& p = plan(W.N, W.K, B, ep.tp_n > 1);
+    if (ep.tp_n > 1 && (p.pair || p.BN > 128)) return fail(GH_EINTERNAL, "tp all-reduce needs the split-K plan");
     CUtensorMap* tmX = nullptr;
     if (sh.db == 2) GH_TRY(tmaps.get(X, (uint64_t)B, (uint64_t)W.K, (uint64_t)ldx, (uint32_t)p.x_box_rows(), &tmX));
     GH_CUDA(launch_gemm(W, tmW, X, ldx, tmX, B, p, ep, gsc, st, next ? next->ptr : nullptr, prefetch_bytes(next)));
@@ -150,6 +166,25 @@ static EpiParams epi_default() {
   EpiParams e;
   memset(&e, 0, sizeof(e));
   return e;
+}
+
+// Tensor-parallel all-reduce parameters of the next reducing GEMM (W_o or W_2) of a TP Tier-1:
+// a fresh sequence number, the receive buffers of its parity, the flag words of every rank.
+static gh_status epi_tp(gh_tier1* t, int B, EpiParams& ep) {
+  if (t->tp <= 1) return GH_OK;
+  auto& c = t->tpc;
+  if (!c.ready) return fail(GH_EINVAL, "tensor-parallel Tier-1 used before its peers were mapped (engine only)");
+  if ((uint32_t)B > t->max_batch) return fail(GH_EINVAL, "B exceeds max_batch");
+  const unsigned int seq = ++c.seq;
+  ep.tp_n = t->tp;
+  ep.tp_rank = t->tp_rank;
+  ep.tp_seq = seq;
+  for (int p = 0; p < t->tp; ++p) {
+    ep.tp_dst[p] = c.peer_buf[seq & 1][p];
+    ep.tp_flag_dst[p] = c.peer_flags[p];
+  }
+  ep.tp_flags = c.flags;
+  return GH_OK;
 }
 
 // tm != nullptr: a tcgen05 GEMM operand -> tile-contiguous layout for bf16 (kernels.hpp Weight)
@@ -193,8 +228,11 @@ uint64_t gh_kernel_launches(int reset) {
   return v;
 }
 
-gh_status gh_tier1_create(const gh_model_spec* spec, int device, uint32_t layer_begin,
-                          uint32_t layer_end, uint64_t seed, uint32_t max_batch, gh_tier1** out) {
+}  // extern "C"
+
+// tp > 1: tensor-parallel slice tp_rank of every layer (gh_tier1::tp); tp = 1: whole layers.
+static gh_status tier1_create(const gh_model_spec* spec, int device, uint32_t layer_begin, uint32_t layer_end,
+                              uint64_t seed, uint32_t max_batch, int tp, int tp_rank, gh_tier1** out) {
   if (!out) return fail(GH_EINVAL, "out is null");
   *out = nullptr;
   Shape sh;
@@ -202,36 +240,54 @@ gh_status gh_tier1_create(const gh_model_spec* spec, int device, uint32_t layer_
   if (layer_begin >= layer_end || layer_end > (uint32_t)sh.N) return fail(GH_EINVAL, "bad layer range");
   if (max_batch == 0) return fail(GH_EINVAL, "max_batch must be >= 1");
   if (sh.V == 0) return fail(GH_EINVAL, "vocab_size required for Tier-1");
+  if (tp < 1 || tp > kMaxTp || tp_rank < 0 || tp_rank >= tp) return fail(GH_EINVAL, "bad tensor-parallel rank");
+  if (tp > 1) {
+    if (sh.db != 2) return fail(GH_EUNSUPPORTED, "tensor parallelism: bf16 storage (tcgen05 path) only");
+    if (sh.H % tp || sh.Hkv % tp) return fail(GH_EINVAL, "tensor parallelism: heads and kv heads must divide by tp");
+    if ((sh.D / tp) % 64 || (sh.Dh / tp) % 64 || (sh.Dkv / tp) % 64)
+      return fail(GH_EUNSUPPORTED, "tensor parallelism: D/tp, D_kv/tp and D_h/tp must be multiples of 64");
+    if (max_batch > (uint32_t)kFusedNormMaxBatch) return fail(GH_EUNSUPPORTED, "tensor parallelism: batch <= 1024");
+  }
   if (gh_device_count() <= device) return fail(GH_ECUDA, "no CUDA device " + std::to_string(device));
   GH_CUDA(cudaSetDevice(device));
   GH_CUDA(configure_kernels());
   auto t = std::make_unique<gh_tier1>();
   t->sh = sh; t->device = device; t->l0 = layer_begin; t->l1 = layer_end; t->max_batch = max_batch;
+  t->tp = tp; t->tp_rank = tp_rank;
   const int D = sh.D, Dkv = sh.Dkv, Dh = sh.Dh, V = sh.V, db = sh.db;
+  const int Dt = D / tp, Dkvt = Dkv / tp, Dht = Dh / tp;  // this rank's heads / hidden units
   cudaStream_t st = 0;
   t->layers.resize(layer_end - layer_begin);
   for (uint32_t l = layer_begin; l < layer_end; ++l) {
     auto& L = t->layers[l - layer_begin];
     const double sD = 1.0 / std::sqrt((double)D), sH = 1.0 / std::sqrt((double)Dh);
-    {
+    {  // rows [q_r | k_r | v_r]
       const uint64_t tq[3] = {tid_layer(l, kWq), tid_layer(l, kWk), tid_layer(l, kWv)};
-      const int rq[3] = {D, Dkv, Dkv};
+      const int rq[3] = {Dt, Dkvt, Dkvt};
       const double sq[3] = {sD, sD, sD};
-      GH_TRY(init_weight(t.get(), &L.qkv, D + 2 * Dkv, D, &L.tm_qkv, make_segs(seed, 3, tq, rq, sq, false)));
+      RowSegs sg = make_segs(seed, 3, tq, rq, sq, false);
+      sg.row0[0] = tp_rank * Dt; sg.row0[1] = sg.row0[2] = tp_rank * Dkvt;
+      GH_TRY(init_weight(t.get(), &L.qkv, Dt + 2 * Dkvt, D, &L.tm_qkv, sg));
     }
-    {
+    {  // all D output rows, input columns of this rank's heads
       const uint64_t to = tid_layer(l, kWo); const int ro = D; const double so = sD;
-      GH_TRY(init_weight(t.get(), &L.o, D, D, &L.tm_o, make_segs(seed, 1, &to, &ro, &so, false)));
+      RowSegs sg = make_segs(seed, 1, &to, &ro, &so, false);
+      sg.k0 = tp_rank * Dt; sg.ldk = D;
+      GH_TRY(init_weight(t.get(), &L.o, D, Dt, &L.tm_o, sg));
     }
-    {
+    {  // hidden units [r Dh/T, (r+1) Dh/T), gate / up interleaved
       const uint64_t t13[2] = {tid_layer(l, kW1), tid_layer(l, kW3)};
-      const int r13[2] = {Dh, Dh};
+      const int r13[2] = {Dht, Dht};
       const double s13[2] = {sD, sD};
-      GH_TRY(init_weight(t.get(), &L.w13, 2 * Dh, D, &L.tm_13, make_segs(seed, 2, t13, r13, s13, true)));
+      RowSegs sg = make_segs(seed, 2, t13, r13, s13, true);
+      sg.row0[0] = sg.row0[1] = tp_rank * Dht;
+      GH_TRY(init_weight(t.get(), &L.w13, 2 * Dht, D, &L.tm_13, sg));
     }
-    {
+    {  // all D output rows, input columns of this rank's hidden units
       const uint64_t t2 = tid_layer(l, kW2); const int r2 = D; const double s2 = sH;
-      GH_TRY(init_weight(t.get(), &L.w2, D, Dh, &L.tm_2, make_segs(seed, 1, &t2, &r2, &s2, false)));
+      RowSegs sg = make_segs(seed, 1, &t2, &r2, &s2, false);
+      sg.k0 = tp_rank * Dht; sg.ldk = Dh;
+      GH_TRY(init_weight(t.get(), &L.w2, D, Dht, &L.tm_2, sg));
     }
     GH_TRY(dev_alloc(t->mem, (size_t)D * db, &L.attn_norm));
     GH_TRY(dev_alloc(t->mem, (size_t)D * db, &L.ffn_norm));
@@ -298,9 +354,26 @@ gh_status gh_tier1_create(const gh_model_spec* spec, int device, uint32_t layer_
     t->gsc.stage = (float*)p;
     t->gsc.stage_floats = n;
   }
+  if (tp > 1) {  // all-reduce receive buffers and flags (mapped by the peers in the engine's setup)
+    void* p;
+    for (int par = 0; par < 2; ++par) {
+      GH_TRY(dev_alloc(t->mem, (size_t)tp * B * D * sizeof(float), &p));
+      t->tpc.buf[par] = (float*)p;
+    }
+    GH_TRY(dev_alloc(t->mem, (size_t)gh_tier1::kTpFlagSlices * kMaxTp * sizeof(unsigned int), &p));
+    GH_CUDA(cudaMemset(p, 0, (size_t)gh_tier1::kTpFlagSlices * kMaxTp * sizeof(unsigned int)));
+    t->tpc.flags = (unsigned int*)p;
+  }
   GH_CUDA(cudaDeviceSynchronize());
   *out = t.release();
   return GH_OK;
+}
+
+extern "C" {
+
+gh_status gh_tier1_create(const gh_model_spec* spec, int device, uint32_t layer_begin,
+                          uint32_t layer_end, uint64_t seed, uint32_t max_batch, gh_tier1** out) {
+  return tier1_create(spec, device, layer_begin, layer_end, seed, max_batch, 1, 0, out);
 }
 
 gh_status gh_tier1_destroy(gh_tier1* t) {
@@ -312,7 +385,7 @@ gh_status gh_tier1_destroy(gh_tier1* t) {
 
 static gh_status t2_attend(gh_tier2* t, uint32_t layer, uint32_t B, const uint32_t* slot, const int32_t* pos,
                            const void* msg_fwd, void* msg_bwd, void* stream, const void* pf, size_t pf_bytes,
-                           int kv_early = 0);
+                           int kv_early = 0, int tp = 1);
 
 // ---- Tier-1 stage implementations.  `SsRef` describes per-slice sums of squares of an
 // activation buffer emitted by its producer (embedding / W2 epilogue) so that the consumer GEMM
@@ -350,6 +423,18 @@ static gh_status t1_pre(gh_tier1* t, uint32_t layer, uint32_t B, const void* x, 
   ep.pos = pos;
   ep.d_head = s.dh;
   ep.rope_rows = s.D + s.Dkv;
+  if (t->tp > 1) {
+    // this rank's head block of the message, [x_r | q_r | k_r | v_r] (AttnArgs::tp layout)
+    const int Dt = s.D / t->tp;
+    if (!(ss.ss && B <= (uint32_t)kFusedNormMaxBatch))
+      return fail(GH_EINVAL, "tensor-parallel F1 needs the fused RMSNorm statistics (engine path)");
+    ep.out = (char*)msg_fwd + (size_t)Dt * s.db;
+    ep.ldo = s.ld_fwd() / t->tp;
+    ep.rope_rows = (s.D + s.Dkv) / t->tp;
+    ep.ss_in = ss.ss; ep.ss_in_slices = ss.slices; ep.ss_dim = s.D; ep.ss_eps = s.s.norm_eps;
+    ep.xcopy_src = (const char*)x + (size_t)t->tp_rank * Dt * s.db; ep.xcopy_ld = s.D; ep.xcopy_rows = Dt;
+    return t->gemm(L.qkv, &L.tm_qkv, x, s.D, (int)B, ep, st);
+  }
   if (s.db == 2 && ss.ss && B <= (uint32_t)kFusedNormMaxBatch) {
     // fused: QKV on the raw x, RMSNorm scale in the epilogue, x copied into the message there
     ep.ss_in = ss.ss; ep.ss_in_slices = ss.slices; ep.ss_dim = s.D; ep.ss_eps = s.s.norm_eps;
@@ -362,12 +447,49 @@ static gh_status t1_pre(gh_tier1* t, uint32_t layer, uint32_t B, const void* x, 
   return t->gemm(L.qkv, &L.tm_qkv, t->xn, s.D, (int)B, ep, st);
 }
 
+// x_resid: the layer's input activation [B][D] (tensor-parallel Tier-1: the residual is the local
+// replica of x, the message block carries only this rank's columns); nullptr = the bwd message's x.
+static gh_status t1_post_tp(gh_tier1* t, uint32_t layer, uint32_t B, const void* msg_bwd, const void* x_resid,
+                            void* x_next, float* ss_next, int* ss_next_slices, cudaStream_t st) {
+  const Shape& s = t->sh;
+  auto& L = t->layers[layer - t->l0];
+  const int Dt = s.D / t->tp, Dht = s.Dh / t->tp;
+  if (!x_resid || !ss_next) return fail(GH_EINVAL, "tensor-parallel F3 runs in the engine (residual + statistics)");
+  // h = x + sum_r attn_r Wo_r^T   (all-reduced in the epilogue; + sums of squares of h)
+  EpiParams ep = epi_default();
+  ep.kind = EPI_STORE_RESID;
+  ep.out = t->h; ep.ldo = s.D;
+  ep.resid = x_resid; ep.ldr = s.D;
+  ep.ss_out = t->ss_h;
+  GH_TRY(epi_tp(t, (int)B, ep));
+  GH_TRY(t->gemm(L.o, &L.tm_o, (const char*)msg_bwd + (size_t)Dt * s.db, s.ld_bwd() / t->tp, (int)B, ep, st,
+                 &L.w13));
+  // g_r = silu(rms(h) W1_r^T) * (rms(h) W3_r^T): this rank's hidden units
+  ep = epi_default();
+  ep.kind = EPI_SWIGLU;
+  ep.out = t->g; ep.ldo = Dht;
+  ep.ss_in = t->ss_h; ep.ss_in_slices = t->plan(s.D, Dt, (int)B, true).slices(); ep.ss_dim = s.D;
+  ep.ss_eps = s.s.norm_eps;
+  GH_TRY(t->gemm(L.w13, &L.tm_13, t->h, s.D, (int)B, ep, st, &L.w2));
+  // x_next = h + sum_r g_r W2_r^T   (all-reduced; + sums of squares of x_next)
+  ep = epi_default();
+  ep.kind = EPI_STORE_RESID;
+  ep.out = x_next; ep.ldo = s.D;
+  ep.resid = t->h; ep.ldr = s.D;
+  ep.ss_out = ss_next;
+  if (ss_next_slices) *ss_next_slices = t->plan(s.D, Dht, (int)B, true).slices();
+  GH_TRY(epi_tp(t, (int)B, ep));
+  const Weight* next = layer + 1 < t->l1 ? &t->layers[layer + 1 - t->l0].qkv : (t->has_cls ? &t->cls : nullptr);
+  return t->gemm(L.w2, &L.tm_2, t->g, Dht, (int)B, ep, st, next);
+}
+
 static gh_status t1_post(gh_tier1* t, uint32_t layer, uint32_t B, const void* msg_bwd, void* x_next, float* ss_next,
-                         int* ss_next_slices, cudaStream_t st) {
+                         int* ss_next_slices, cudaStream_t st, const void* x_resid = nullptr) {
   if (!t || !msg_bwd || !x_next) return fail(GH_EINVAL, "null argument");
   if (layer < t->l0 || layer >= t->l1) return fail(GH_EINVAL, "layer not owned by this Tier-1");
   if (B > t->max_batch) return fail(GH_EINVAL, "B exceeds max_batch");
   if (B == 0) return GH_OK;
+  if (t->tp > 1) return t1_post_tp(t, layer, B, msg_bwd, x_resid, x_next, ss_next, ss_next_slices, st);
   const Shape& s = t->sh;
   auto& L = t->layers[layer - t->l0];
   const bool fused = s.db == 2 && B <= (uint32_t)kFusedNormMaxBatch;
@@ -640,12 +762,15 @@ gh_status gh_tier2_attend(gh_tier2* t, uint32_t layer, uint32_t B, const uint32_
 // `kv_early`: the caller guarantees the kernel's predecessor writes neither the arena nor pos / slot
 static gh_status t2_attend(gh_tier2* t, uint32_t layer, uint32_t B, const uint32_t* slot, const int32_t* pos,
                            const void* msg_fwd, void* msg_bwd, void* stream, const void* pf, size_t pf_bytes,
-                           int kv_early) {
+                           int kv_early, int tp) {
   if (!t || !slot || !pos || !msg_fwd || !msg_bwd) return fail(GH_EINVAL, "null argument");
   if (layer < t->l0 || layer >= t->l1) return fail(GH_EINVAL, "layer not owned by this Tier-2");
   if (B == 0) return GH_OK;
   const Shape& s = t->sh;
+  if (tp > 1 && !(t->has_tmap && s.Hkv % tp == 0))
+    return fail(GH_EUNSUPPORTED, "head-blocked (tensor-parallel) messages need the tensor-core attention kernel");
   AttnArgs a;
+  a.tp = tp;
   a.msg_fwd = msg_fwd;
   a.msg_bwd = msg_bwd;
   a.arena = (char*)t->arena + (size_t)(layer - t->l0) * t->layer_stride() * s.db;
@@ -884,7 +1009,12 @@ struct gh_engine {
   int span = 0;  // this rank's span (tier1 / tier2)
   int shard = 0; // tier2: this rank's prompt shard within its span
   int l0 = 0, l1 = 0;  // this rank's layers
-  int t2_rank(int sp, int j) const { return n1 + sp * kp + j; }
+  int tp = 1;    // Tier-1 tensor-parallel ranks: ranks 0..tp-1 share every layer
+  int t1n() const { return tp > 1 ? tp : n1; }  // Tier-1 ranks (TP ranks or pipeline spans)
+  int t2_rank(int sp, int j) const { return t1n() + sp * kp + j; }
+  // message rows of this rank: a TP Tier-1 rank holds its head block [x_r|q_r|k_r|v_r] / [x_r|attn_r]
+  long fwd_w() const { return sh.ld_fwd() / (role == 1 ? tp : 1); }
+  long bwd_w() const { return sh.ld_bwd() / (role == 1 ? tp : 1); }
   gh_tier1* t1 = nullptr;
   gh_tier2* t2 = nullptr;
   std::vector<std::unique_ptr<DevMem>> mem;
@@ -907,6 +1037,7 @@ struct gh_engine {
     cudaGraphExec_t graph = nullptr;
   };
   std::vector<Batch> batches;
+  bool keep_logits = false;               // classifier runs also store the logits (gh_engine_keep_logits)
   std::vector<int> shard_off, shard_cnt;  // split mode: per Tier-2 rank
   int my_cnt = 0;                         // tier2: prompts of my shard per batch
   cudaEvent_t fork = nullptr;
@@ -922,8 +1053,8 @@ struct gh_engine {
     // arrived (tier1, span > 0), [IF*(K'+2) + ib] next tokens from the last span arrived (span 0)
     uint32_t* flags = nullptr;
     std::vector<std::vector<void*>> fwd, pos; // tier1: [j][ib] its Tier-2 rank j's fwd / pos buffers
-    std::vector<uint32_t*> rflags;            // tier1: [j] its Tier-2 rank j's flags; tier2: [0] its Tier-1's
-    std::vector<void*> bwd;                   // tier2: [ib] its Tier-1's bwd buffers
+    std::vector<uint32_t*> rflags;            // tier1: [j] its Tier-2 rank j's flags; tier2: [r] Tier-1 rank r's
+    std::vector<std::vector<void*>> bwd;      // tier2: [r][ib] Tier-1 rank r's bwd buffers (r < tp)
     uint32_t* nflags = nullptr;               // tier1 span s < n1-1: span s+1's flags
     std::vector<void*> nx, nss, npos;         // [ib] span s+1's x0 / ss0 / pos buffers
     uint32_t* fflags = nullptr;               // last span (n1 > 1): span 0's flags
@@ -949,6 +1080,10 @@ struct gh_engine {
     gh_tier2_destroy(t2);
   }
   int rows() const { return role == 2 ? my_cnt : (int)cfg.batch; }
+  bool use_graph_any() const {
+    for (auto& b : batches) if (b.graph) return true;
+    return false;
+  }
 };
 
 // Tier-1 stage calls on an in-flight batch's activation ping-pong (x0 / x1) with the sums of
@@ -963,11 +1098,12 @@ static gh_status act_pre(gh_engine* e, gh_engine::Batch& b, int l, cudaStream_t 
 }
 static gh_status act_post(gh_engine* e, gh_engine::Batch& b, int l, cudaStream_t st) {
   const int nx = b.cur ^ 1;
-  GH_TRY(t1_post(e->t1, l, e->cfg.batch, b.bwd, b.x(nx), b.ss(nx), &b.ss_slices[nx], st));
+  GH_TRY(t1_post(e->t1, l, e->cfg.batch, b.bwd, b.x(nx), b.ss(nx), &b.ss_slices[nx], st, b.x(b.cur)));
   b.cur = nx;
   return GH_OK;
 }
 static gh_status act_classify(gh_engine* e, gh_engine::Batch& b, float* logits, cudaStream_t st) {
+  if (!logits && e->keep_logits) logits = b.logits;
   if (b.sampling)  // logits are always written (the sampler reads them)
     return t1_classify(e->t1, e->cfg.batch, b.x(b.cur), SsRef{b.ss(b.cur), b.ss_slices[b.cur]},
                        logits ? logits : b.logits, b.next, st, b.inv_temp, b.seed, b.pos);
@@ -1012,8 +1148,31 @@ gh_status gh_engine_create(const gh_engine_config* cfg, gh_comm* comm, gh_engine
   const int rank = comm ? comm->rank : 0;
   e->l0 = 0;
   e->l1 = s.N;
+  e->tp = cfg->tier1_tp > 1 ? (int)cfg->tier1_tp : 1;
   if (world == 1) {
+    if (e->tp > 1) return fail(GH_EINVAL, "tier1_tp > 1 needs a tier split (world >= tier1_tp + 1)");
     e->role = 0;
+  } else if (e->tp > 1) {
+    // Tier-1 tensor parallelism: ranks 0..tp-1 hold a head / hidden-unit slice of every layer,
+    // ranks tp.. are the K' Tier-2 ranks (each holds all heads of its prompt shard)
+    if (cfg->tier1_ranks > 1) return fail(GH_EUNSUPPORTED, "tier1_tp and tier1_ranks (pipeline spans) together");
+    if (world <= e->tp) return fail(GH_EINVAL, "world size must be tier1_tp + K' with K' >= 1");
+    if (cfg->transport == GH_TRANSPORT_NCCL) return fail(GH_EUNSUPPORTED, "tensor parallelism needs the peer transport");
+    if (cfg->prefill) return fail(GH_EUNSUPPORTED, "chunked prefill rows: no tensor parallelism");
+    if (e->tp > kMaxTp) return fail(GH_EUNSUPPORTED, "tier1_tp <= 4");
+    if (s.db != 2 || s.dh != 128 || s.Hkv % e->tp)
+      return fail(GH_EUNSUPPORTED, "tensor parallelism: bf16, head dim 128, kv heads divisible by tier1_tp");
+    e->kp = world - e->tp;
+    e->role = rank < e->tp ? 1 : 2;
+    e->shard = rank < e->tp ? 0 : rank - e->tp;
+    if ((int)cfg->batch < e->kp) return fail(GH_EINVAL, "batch smaller than the number of Tier-2 ranks");
+    std::vector<uint64_t> off(e->kp), cnt(e->kp);  // balanced shards (analytic.cpp:119)
+    GH_TRY(gh_shard_plan(cfg->batch, e->kp, off.data(), cnt.data()));
+    for (int j = 0; j < e->kp; ++j) {
+      e->shard_off.push_back((int)off[j]);
+      e->shard_cnt.push_back((int)cnt[j]);
+    }
+    if (e->role == 2) e->my_cnt = e->shard_cnt[e->shard];
   } else {
     e->n1 = cfg->tier1_ranks > 1 ? (int)cfg->tier1_ranks : 1;
     if (world <= e->n1 || (world - e->n1) % e->n1)
@@ -1040,10 +1199,20 @@ gh_status gh_engine_create(const gh_engine_config* cfg, gh_comm* comm, gh_engine
     }
     if (e->role == 2) e->my_cnt = e->shard_cnt[e->shard];
   }
+  {  // the decomposition is exactly the host-side gh_engine_layout (tested on CPU at world 8)
+    gh_rank_layout lay;
+    GH_TRY(gh_engine_layout((uint32_t)world, (uint32_t)rank, cfg->tier1_ranks, cfg->tier1_tp, (uint64_t)s.N,
+                            cfg->batch, &lay));
+    const bool same = lay.role == e->role && (e->role == 0 || (lay.span == e->span && (int)lay.kp == e->kp &&
+                      (int)lay.layer_begin == e->l0 && (int)lay.layer_end == e->l1 &&
+                      (e->role != 2 || (lay.shard == e->shard && (int)lay.row_off == e->shard_off[e->shard] &&
+                                        (int)lay.row_cnt == e->my_cnt))));
+    if (!same) return fail(GH_EINTERNAL, "engine layout disagrees with gh_engine_layout");
+  }
   const int R = e->rows();
   if (e->role != 2)
-    GH_TRY(gh_tier1_create(&cfg->spec, cfg->device, (uint32_t)e->l0, (uint32_t)e->l1, cfg->weight_seed, cfg->batch,
-                           &e->t1));
+    GH_TRY(tier1_create(&cfg->spec, cfg->device, (uint32_t)e->l0, (uint32_t)e->l1, cfg->weight_seed, cfg->batch,
+                        e->tp, e->tp > 1 ? rank : 0, &e->t1));
   if (e->role != 1) {
     uint32_t need = (uint32_t)R * cfg->inflight;
     uint32_t n_slots = cfg->n_slots ? cfg->n_slots : need;
@@ -1066,8 +1235,8 @@ gh_status gh_engine_create(const gh_engine_config* cfg, gh_comm* comm, gh_engine
     GH_CUDA(cudaMemset(p, 0, (size_t)R * 4));
     GH_TRY(dev_alloc(e->mem, (size_t)R * s.D * s.db, &b.x0));
     GH_TRY(dev_alloc(e->mem, (size_t)R * s.D * s.db, &b.x1));
-    GH_TRY(dev_alloc(e->mem, (size_t)R * s.ld_fwd() * s.db, &b.fwd));
-    GH_TRY(dev_alloc(e->mem, (size_t)R * s.ld_bwd() * s.db, &b.bwd));
+    GH_TRY(dev_alloc(e->mem, (size_t)R * e->fwd_w() * s.db, &b.fwd));
+    GH_TRY(dev_alloc(e->mem, (size_t)R * e->bwd_w() * s.db, &b.bwd));
     {
       const size_t nss = (size_t)(s.D + 127) / 128 * 8 * R;  // W2 output tiles x max cluster size
       GH_TRY(dev_alloc(e->mem, nss * sizeof(float), &p)); b.ss0 = (float*)p;
@@ -1086,7 +1255,7 @@ gh_status gh_engine_create(const gh_engine_config* cfg, gh_comm* comm, gh_engine
   }
   GH_CUDA(cudaDeviceSynchronize());
   if (e->role != 0 && cfg->transport != GH_TRANSPORT_NCCL) GH_TRY(peer_setup(e.get()));
-  if ((cfg->transport == GH_TRANSPORT_PEER || e->n1 > 1) && e->role != 0 && !e->peer.on)
+  if ((cfg->transport == GH_TRANSPORT_PEER || e->n1 > 1 || e->tp > 1) && e->role != 0 && !e->peer.on)
     return fail(GH_EUNSUPPORTED, "peer transport requested but not available on every rank");
   *out = e.release();
   return GH_OK;
@@ -1111,6 +1280,23 @@ gh_status gh_engine_read_next(gh_engine* e, uint32_t ib, int32_t* next_host) {
   GH_CUDA(cudaSetDevice(e->cfg.device));
   GH_CUDA(cudaDeviceSynchronize());
   GH_CUDA(cudaMemcpy(next_host, e->batches[ib].next, (size_t)e->cfg.batch * 4, cudaMemcpyDeviceToHost));
+  return GH_OK;
+}
+
+gh_status gh_engine_keep_logits(gh_engine* e, int keep) {
+  if (!e) return fail(GH_EINVAL, "null engine");
+  if (e->role == 2) return fail(GH_EINVAL, "Tier-2 ranks run no classifier");
+  if (e->use_graph_any()) return fail(GH_EUNSUPPORTED, "set before the first step (the CUDA graph is captured then)");
+  e->keep_logits = keep != 0;
+  return GH_OK;
+}
+
+gh_status gh_engine_read_logits(gh_engine* e, uint32_t ib, float* logits_host) {
+  if (!e || ib >= e->batches.size() || !logits_host) return fail(GH_EINVAL, "bad argument");
+  if (e->role == 2 || !e->batches[ib].logits) return fail(GH_EINVAL, "this rank holds no logits");
+  GH_CUDA(cudaSetDevice(e->cfg.device));
+  GH_CUDA(cudaDeviceSynchronize());
+  GH_CUDA(cudaMemcpy(logits_host, e->batches[ib].logits, (size_t)e->cfg.batch * e->sh.V * 4, cudaMemcpyDeviceToHost));
   return GH_OK;
 }
 
@@ -1277,7 +1463,8 @@ gh_status gh_engine_step_device(gh_engine* e, uint32_t ib, void* stream) {
     }
     return engine_layer_loop_colocated(e, b, false, st);
   }
-  if (e->n1 > 1) return fail(GH_EUNSUPPORTED, "Tier-1 pipeline stages: use gh_engine_step_all / step_all_host");
+  if (e->n1 > 1 || e->tp > 1)
+    return fail(GH_EUNSUPPORTED, "Tier-1 pipeline stages / tensor parallelism: use gh_engine_step_all / step_all_host");
   ncclComm_t comm = e->comm->comms[0];
   GH_TRY(split_begin(e, b, comm, st));
   for (int l = 0; l < e->sh.N; ++l) GH_TRY(split_layer(e, b, comm, l, st));
@@ -1373,17 +1560,18 @@ static gh_status peer_setup(gh_engine* e) {
   auto& api = nccl();
   auto& P = e->peer;
   const int IF = (int)e->batches.size(), kp = e->kp, world = e->comm->nranks, rank = e->comm->rank;
-  const int n1 = e->n1;
-  const int nslot = 1 + 6 * IF;
+  const int n1 = e->n1, tp = e->tp;
+  const int nslot = 4 + 6 * IF;
   auto slot_fwd = [&](int ib) { return 1 + ib; };
   auto slot_pos = [&](int ib) { return 1 + IF + ib; };
   auto slot_bwd = [&](int ib) { return 1 + 2 * IF + ib; };
   auto slot_x0 = [&](int ib) { return 1 + 3 * IF + ib; };
   auto slot_ss0 = [&](int ib) { return 1 + 4 * IF + ib; };
   auto slot_next = [&](int ib) { return 1 + 5 * IF + ib; };
+  const int slot_tpf = 1 + 6 * IF, slot_tpb = 2 + 6 * IF;  // TP all-reduce flags, buffers (2 parities)
   ncclComm_t comm = e->comm->comms[0];
   void* p;
-  const size_t nflags = (size_t)IF * (kp + 3);
+  const size_t nflags = (size_t)IF * (kp + tp + 2);
   GH_TRY(dev_alloc(e->mem, nflags * 4, &p));
   P.flags = (uint32_t*)p;
   GH_CUDA(cudaMemset(P.flags, 0, nflags * 4));
@@ -1404,6 +1592,11 @@ static gh_status peer_setup(gh_engine* e) {
       if (b.ss0) get(slot_ss0(ib), b.ss0);
       get(slot_next(ib), b.next);
     }
+  }
+  if (e->role == 1 && tp > 1) {
+    get(slot_tpf, e->t1->tpc.flags);
+    get(slot_tpb, e->t1->tpc.buf[0]);
+    get(slot_tpb + 1, e->t1->tpc.buf[1]);
   }
   const size_t rec = nslot * sizeof(cudaIpcMemHandle_t);
   void *dmine, *dall, *dok;
@@ -1449,9 +1642,30 @@ static gh_status peer_setup(gh_engine* e) {
       P.fflags = (uint32_t*)open(0, 0);
       for (int ib = 0; ib < IF; ++ib) P.fnext.push_back(open(0, slot_next(ib)));
     }
+    if (tp > 1) {  // the other TP ranks' all-reduce receive buffers and flag words
+      auto& c = e->t1->tpc;
+      for (int q = 0; q < tp; ++q) {
+        if (q == rank) {
+          c.peer_flags[q] = c.flags;
+          c.peer_buf[0][q] = c.buf[0];
+          c.peer_buf[1][q] = c.buf[1];
+        } else {
+          c.peer_flags[q] = (unsigned int*)open(q, slot_tpf);
+          c.peer_buf[0][q] = (float*)open(q, slot_tpb);
+          c.peer_buf[1][q] = (float*)open(q, slot_tpb + 1);
+        }
+      }
+    }
+  } else if (tp > 1) {  // every TP Tier-1 rank receives its head block of the attention output
+    P.bwd.assign(tp, std::vector<void*>(IF, nullptr));
+    for (int r = 0; r < tp; ++r) {
+      P.rflags.push_back((uint32_t*)open(r, 0));
+      for (int ib = 0; ib < IF; ++ib) P.bwd[r][ib] = open(r, slot_bwd(ib));
+    }
   } else {
     P.rflags.push_back((uint32_t*)open(e->span, 0));
-    for (int ib = 0; ib < IF; ++ib) P.bwd.push_back(open(e->span, slot_bwd(ib)));
+    P.bwd.assign(1, std::vector<void*>());
+    for (int ib = 0; ib < IF; ++ib) P.bwd[0].push_back(open(e->span, slot_bwd(ib)));
   }
   (void)rank;
   GH_CUDA(cudaMemcpy(dok, &ok, 4, cudaMemcpyHostToDevice));
@@ -1464,7 +1678,7 @@ static gh_status peer_setup(gh_engine* e) {
     P.opened.clear();
     return GH_OK;  // NCCL send/recv transport
   }
-  const int ncs = e->role == 1 ? kp + 1 : 1;
+  const int ncs = e->role == 1 ? kp + 1 : std::max(1, tp);
   for (int j = 0; j < ncs; ++j) {
     cudaStream_t c;
     GH_CUDA(cudaStreamCreateWithFlags(&c, cudaStreamNonBlocking));
@@ -1480,31 +1694,41 @@ static gh_status peer_setup(gh_engine* e) {
   P.seqxi.assign(IF, 0);
   P.seqt.assign(IF, 0);
   P.on = true;
+  if (e->role == 1 && tp > 1) e->t1->tpc.ready = true;
   return GH_OK;
 }
 
 // flag word offsets (gh_engine::Peer::flags)
+//   [ib*K' + j]                   tier1: the attention output of Tier-2 shard j arrived
+//   [IF*K' + ib*tp + r]           tier2: the fwd head block of Tier-1 rank r arrived (tp = 1: r = 0)
+//   [IF*(K'+tp) + ib]             tier1 span > 0: the previous span's activation arrived
+//   [IF*(K'+tp+1) + ib]           tier1 span 0: the last span's next tokens arrived
 static uint32_t f_bwd(const gh_engine* e, int ib, int j) { return (uint32_t)(ib * e->kp + j); }
-static uint32_t f_fwd(const gh_engine* e, int ib) { return (uint32_t)(e->batches.size() * e->kp + ib); }
-static uint32_t f_x(const gh_engine* e, int ib) { return (uint32_t)(e->batches.size() * (e->kp + 1) + ib); }
-static uint32_t f_tok(const gh_engine* e, int ib) { return (uint32_t)(e->batches.size() * (e->kp + 2) + ib); }
+static uint32_t f_fwd(const gh_engine* e, int ib, int r) {
+  return (uint32_t)(e->batches.size() * e->kp + ib * e->tp + r);
+}
+static uint32_t f_x(const gh_engine* e, int ib) { return (uint32_t)(e->batches.size() * (e->kp + e->tp) + ib); }
+static uint32_t f_tok(const gh_engine* e, int ib) { return (uint32_t)(e->batches.size() * (e->kp + e->tp + 1) + ib); }
 
 // Tier-1: copy batch ib's fwd message shards (and, at the first layer of a step, its positions)
 // into every Tier-2 rank of this span, then publish the sequence number in that rank's flag word.
 static gh_status peer_send_fwd(gh_engine* e, int ib, bool with_pos, cudaStream_t st) {
   auto& P = e->peer;
   auto& b = e->batches[ib];
-  const size_t fwd_row = (size_t)e->sh.ld_fwd() * e->sh.db;
+  const size_t fwd_row = (size_t)e->fwd_w() * e->sh.db;  // this rank's (head block of the) row
+  const int me = e->tp > 1 ? e->comm->rank : 0;           // TP rank: block index at the Tier-2
   const uint32_t sq = ++P.seq[ib];
   GH_CUDA(cudaEventRecord(P.ev[ib], st));
   for (int j = 0; j < e->kp; ++j) {
     cudaStream_t c = P.cs[j];
     GH_CUDA(cudaStreamWaitEvent(c, P.ev[ib], 0));
-    if (with_pos)
+    if (with_pos && me == 0)
       GH_CUDA(cudaMemcpyAsync(P.pos[j][ib], b.pos + e->shard_off[j], (size_t)e->shard_cnt[j] * 4, cudaMemcpyDeviceToDevice, c));
-    GH_CUDA(cudaMemcpyAsync(P.fwd[j][ib], (char*)b.fwd + e->shard_off[j] * fwd_row, e->shard_cnt[j] * fwd_row,
+    // head block `me` of the Tier-2's [tp][cnt][row/tp] buffer (tp = 1: the plain rows)
+    GH_CUDA(cudaMemcpyAsync((char*)P.fwd[j][ib] + (size_t)me * e->shard_cnt[j] * fwd_row,
+                            (char*)b.fwd + e->shard_off[j] * fwd_row, e->shard_cnt[j] * fwd_row,
                             cudaMemcpyDeviceToDevice, c));
-    GH_CU(memops().write((CUstream)c, (CUdeviceptr)(P.rflags[j] + f_fwd(e, ib)), sq, CU_STREAM_WRITE_VALUE_DEFAULT));
+    GH_CU(memops().write((CUstream)c, (CUdeviceptr)(P.rflags[j] + f_fwd(e, ib, me)), sq, CU_STREAM_WRITE_VALUE_DEFAULT));
   }
   return GH_OK;
 }
@@ -1606,23 +1830,27 @@ static gh_status split_step_peer(gh_engine* e, cudaStream_t st) {
         }
       }
   } else {
-    const size_t bwd_row = (size_t)e->sh.ld_bwd() * e->sh.db;
+    const int tp = e->tp;
+    const size_t bwd_row = (size_t)e->sh.ld_bwd() / tp * e->sh.db;  // one head block of a row
     const int me = e->shard;
     for (int l = e->l0; l < e->l1; ++l)
       for (int ib = 0; ib < nb; ++ib) {
         auto& b = e->batches[ib];
         const uint32_t sq = ++P.seq[ib];
-        if (!nowait)
-          GH_CU(memops().wait((CUstream)st, (CUdeviceptr)(P.flags + f_fwd(e, ib)), sq, CU_STREAM_WAIT_VALUE_GEQ));
+        for (int r = 0; r < tp && !nowait; ++r)  // every Tier-1 rank's head block has landed
+          GH_CU(memops().wait((CUstream)st, (CUdeviceptr)(P.flags + f_fwd(e, ib, r)), sq, CU_STREAM_WAIT_VALUE_GEQ));
         if (e->cfg.prefill) GH_TRY(t2_append(e->t2, l, e->my_cnt, b.slot, b.pos, b.fwd, st));
-    GH_TRY(gh_tier2_attend(e->t2, l, e->my_cnt, b.slot, b.pos, b.fwd, b.bwd, st));
+        GH_TRY(t2_attend(e->t2, l, e->my_cnt, b.slot, b.pos, b.fwd, b.bwd, st, nullptr, 0, 0, tp));
         GH_CUDA(cudaEventRecord(P.ev[ib], st));
-        cudaStream_t c = P.cs[0];
-        GH_CUDA(cudaStreamWaitEvent(c, P.ev[ib], 0));
-        GH_CUDA(cudaMemcpyAsync((char*)P.bwd[ib] + e->shard_off[me] * bwd_row, b.bwd, e->my_cnt * bwd_row,
-                                cudaMemcpyDeviceToDevice, c));
-        GH_CU(memops().write((CUstream)c, (CUdeviceptr)(P.rflags[0] + f_bwd(e, ib, me)), sq,
-                             CU_STREAM_WRITE_VALUE_DEFAULT));
+        for (int r = 0; r < tp; ++r) {  // head block r of every row to Tier-1 rank r
+          cudaStream_t c = P.cs[r];
+          GH_CUDA(cudaStreamWaitEvent(c, P.ev[ib], 0));
+          GH_CUDA(cudaMemcpyAsync((char*)P.bwd[r][ib] + e->shard_off[me] * bwd_row,
+                                  (char*)b.bwd + (size_t)r * e->my_cnt * bwd_row, e->my_cnt * bwd_row,
+                                  cudaMemcpyDeviceToDevice, c));
+          GH_CU(memops().write((CUstream)c, (CUdeviceptr)(P.rflags[r] + f_bwd(e, ib, me)), sq,
+                               CU_STREAM_WRITE_VALUE_DEFAULT));
+        }
       }
   }
   return GH_OK;
@@ -1630,7 +1858,7 @@ static gh_status split_step_peer(gh_engine* e, cudaStream_t st) {
 
 static gh_status split_step_pipelined(gh_engine* e, cudaStream_t st) {
   if (e->peer.on) return split_step_peer(e, st);
-  if (e->n1 > 1) return fail(GH_EUNSUPPORTED, "Tier-1 pipeline stages need the peer transport");
+  if (e->n1 > 1 || e->tp > 1) return fail(GH_EUNSUPPORTED, "Tier-1 pipeline stages / tensor parallelism need the peer transport");
   const int nb = (int)e->batches.size();
   const int N = e->sh.N;
   ncclComm_t comm = e->comm->comms[0];
@@ -1726,7 +1954,8 @@ gh_status gh_engine_step_host(gh_engine* e, uint32_t ib, const int32_t* tok_host
   if (logits_host && e->role == 0) {
     GH_TRY(engine_layer_loop_colocated(e, b, true, st));
   } else if (logits_host && e->role == 1) {
-    if (e->n1 > 1) return fail(GH_EUNSUPPORTED, "Tier-1 pipeline stages: use gh_engine_step_all / step_all_host");
+    if (e->n1 > 1 || e->tp > 1)
+      return fail(GH_EUNSUPPORTED, "Tier-1 pipeline stages / tensor parallelism: use gh_engine_step_all / step_all_host");
     ncclComm_t comm = e->comm->comms[0];
     GH_TRY(split_begin(e, b, comm, st));
     for (int l = 0; l < e->sh.N; ++l) GH_TRY(split_layer(e, b, comm, l, st));

@@ -174,3 +174,13 @@ def shard_plan(batch: int, kp: int):
     cnt = (C.c_uint64 * max(kp, 1))()
     L.check(L.lib().gh_shard_plan(batch, kp, off, cnt))
     return list(off), list(cnt)
+
+
+def engine_layout(world: int, rank: int, batch: int, n_layers: int, tier1_ranks: int = 1, tier1_tp: int = 1) -> dict:
+    """The engine's rank layout of a tier split (gh_engine_layout): role ("colocated" / "tier1" /
+    "tier2"), span, tp_rank, shard, kp, layer range and the rows of each in-flight batch whose KV
+    a Tier-2 rank holds."""
+    out = L.GhRankLayout()
+    L.check(L.lib().gh_engine_layout(world, rank, tier1_ranks, tier1_tp, n_layers, batch, C.byref(out)))
+    return dict(role={0: "colocated", 1: "tier1", 2: "tier2"}[out.role], span=out.span, tp_rank=out.tp_rank,
+                shard=out.shard, kp=out.kp, layers=(out.layer_begin, out.layer_end), rows=(out.row_off, out.row_cnt))

@@ -178,13 +178,13 @@ class Engine:
     def __init__(self, spec: ModelSpec, batch: int, inflight: int = 1, device: int = 0,
                  weight_seed: int = 1234, n_slots: int = 0, use_graph: bool = True,
                  comm: Comm | None = None, transport: str = "auto", tier1_ranks: int = 1,
-                 kv_pages: int = 0, prefill: bool = False):
+                 kv_pages: int = 0, prefill: bool = False, tier1_tp: int = 1):
         self.spec, self.batch, self.inflight = spec, batch, inflight
         self.kv_pages = kv_pages
         self.prefill = prefill
         self.n_slots = n_slots or batch * inflight
         cfg = L.GhEngineConfig(spec.c(), device, weight_seed, batch, inflight, n_slots, int(use_graph),
-                               self.TRANSPORTS[transport], tier1_ranks, int(prefill), kv_pages)
+                               self.TRANSPORTS[transport], tier1_ranks, int(prefill), kv_pages, tier1_tp)
         h = C.c_void_p()
         L.check(L.lib().gh_engine_create(C.byref(cfg), comm.h if comm else None, C.byref(h)))
         self.h = h
@@ -292,6 +292,15 @@ class Engine:
     def read_next(self, ib=0) -> np.ndarray:
         out = np.empty(self.batch, dtype=np.int32)
         L.check(L.lib().gh_engine_read_next(self.h, ib, out.ctypes.data))
+        return out
+
+    def keep_logits(self, keep: bool = True):
+        """Every classifier run also writes its fp32 logits (read them with read_logits)."""
+        L.check(L.lib().gh_engine_keep_logits(self.h, int(keep)))
+
+    def read_logits(self, ib=0) -> np.ndarray:
+        out = np.empty((self.batch, self.spec.vocab_size), dtype=np.float32)
+        L.check(L.lib().gh_engine_read_logits(self.h, ib, out.ctypes.data))
         return out
 
     def advance(self, ib=0, pos_increment=0, stream=None):
