@@ -338,6 +338,67 @@ gh_status gh_engine_shard(const gh_engine* e, int* index, uint32_t* off, uint32_
 /* Launch count of this library's kernels since the last reset (device work accounting). */
 uint64_t gh_kernel_launches(int reset);
 
+/* ------------------------------------------------------------------ batch-state dispatcher
+ * Glinthawk's dispatcher: batch-state objects for the IF in-flight batches, refilled
+ * from the request queue as prompts finish.  Lanes = IF x B rows, each bound to its context slot;
+ * per-Tier-2-shard page accounting on a paged arena (admission maps a request's positions, or,
+ * with on_demand, its prompt and then a page at a time, preempting the shard's most recently
+ * admitted request by recompute or by swap when a pool runs dry -- the oversubscription the
+ * planner assumes, optimizer.cpp:42-45, 194-207).  Decisions depend only on lengths, max_new and
+ * page counts, so in a tier split every rank runs the same dispatcher over the same requests
+ * (SPMD; Tier-2 ranks apply the KV actions of their shard, Tier-1 ranks feed tokens).  The
+ * engine step is gh_engine_step_all (pipelined IF >= 2 split, or the colocated CUDA graphs);
+ * lane inputs, page tables and sampling state are updated stream-ordered (no host
+ * synchronisation per change), and a step's tokens are read one step later. */
+typedef struct gh_dispatcher gh_dispatcher;
+typedef struct gh_dispatch_config {
+  uint32_t max_new;      /* tokens generated per request */
+  int on_demand;         /* paged arena: map the prompt, grow a page at a time, preempt when dry */
+  int preempt_swap;      /* preempt by swapping the context to host memory (else recompute) */
+  int order_shortest;    /* admit the shortest prompt first (else FIFO) */
+} gh_dispatch_config;
+typedef struct gh_dispatch_stats {
+  uint64_t steps, admitted, finished, tokens, preemptions, swaps;
+  uint32_t peak_pages;   /* most pages of one shard's pool in use at once */
+} gh_dispatch_stats;
+/* Not for engines with Tier-1 pipeline spans (tier1_ranks > 1) or prefill rows. */
+gh_status gh_dispatcher_create(gh_engine* e, const gh_dispatch_config* cfg, gh_dispatcher** out);
+gh_status gh_dispatcher_destroy(gh_dispatcher* d);
+/* Queue a request (GH_EINFEASIBLE when it can never fit a slot / a shard's page pool). */
+gh_status gh_dispatcher_submit(gh_dispatcher* d, const int32_t* prompt, uint32_t len, float temperature,
+                               uint32_t seed, uint64_t* id);
+/* One engine step over every in-flight batch; *busy = 0 once every request has finished. */
+gh_status gh_dispatcher_step(gh_dispatcher* d, int* busy);
+/* Steps until every submitted request has finished and its tokens are on the host. */
+gh_status gh_dispatcher_run(gh_dispatcher* d, uint64_t* steps);
+/* Generated tokens of a finished request (max_new; zeros on Tier-2 ranks). */
+gh_status gh_dispatcher_result(const gh_dispatcher* d, uint64_t id, int32_t* tokens, uint32_t cap, uint32_t* n);
+gh_status gh_dispatcher_stats(const gh_dispatcher* d, gh_dispatch_stats* out);
+
+/* The dispatcher's decision logic alone (host only, no GPU): plan -> the caller runs the step ->
+ * commit -> resolve (the tokens of the oldest committed step, any lag).  Lane inputs: src 0 idle
+ * (a dummy token at position 0), 1 host token, 2 the token the lane's previous step generated.
+ * KV actions (op 0 map [0, n), 1 unmap, 2 swap out [0, n) to buffer `buf`, 3 swap in) apply to
+ * the lane's slot before the step. */
+typedef struct gh_sched gh_sched;
+typedef struct gh_sched_config {
+  uint32_t batch, inflight, kp, pages, max_seq, max_new;
+  int on_demand, preempt_swap, order_shortest;
+} gh_sched_config;
+typedef struct gh_lane_input { int32_t src, tok, pos; } gh_lane_input;
+typedef struct gh_kv_action { int32_t op; uint32_t lane; uint32_t n; uint64_t buf; } gh_kv_action;
+gh_status gh_sched_create(const gh_sched_config* cfg, gh_sched** out);
+gh_status gh_sched_destroy(gh_sched* s);
+gh_status gh_sched_submit(gh_sched* s, const int32_t* prompt, uint32_t len, float temperature, uint32_t seed,
+                          uint64_t* id);
+gh_status gh_sched_plan(gh_sched* s, gh_lane_input* inputs, gh_kv_action* actions, uint32_t cap, uint32_t* n_actions);
+gh_status gh_sched_commit(gh_sched* s);
+gh_status gh_sched_resolve(gh_sched* s, const int32_t* next_tokens);
+int gh_sched_done(const gh_sched* s);
+uint32_t gh_sched_unresolved(const gh_sched* s);
+gh_status gh_sched_result(const gh_sched* s, uint64_t id, int32_t* tokens, uint32_t cap, uint32_t* n);
+gh_status gh_sched_stats(const gh_sched* s, gh_dispatch_stats* out);
+
 /* ------------------------------------------------------------------ diagnostics
  * Microbenchmark of the Tier-1 tcgen05 GEMM on device 0: Y[B,N] = X[B,K] W[N,K]^T (bf16) with
  * the plain-store epilogue.  flags = GEMM_DBG_* bits (1 no MMA, 2 no activation loads, 4 no L2

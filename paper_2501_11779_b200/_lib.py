@@ -74,6 +74,29 @@ class GhRankLayout(C.Structure):
                 ("row_off", C.c_uint32), ("row_cnt", C.c_uint32)]
 
 
+class GhDispatchConfig(C.Structure):
+    _fields_ = [("max_new", C.c_uint32), ("on_demand", C.c_int), ("preempt_swap", C.c_int),
+                ("order_shortest", C.c_int)]
+
+
+class GhDispatchStats(C.Structure):
+    _fields_ = [(n, C.c_uint64) for n in ("steps", "admitted", "finished", "tokens", "preemptions", "swaps")]
+    _fields_ += [("peak_pages", C.c_uint32)]
+
+
+class GhSchedConfig(C.Structure):
+    _fields_ = [(n, C.c_uint32) for n in ("batch", "inflight", "kp", "pages", "max_seq", "max_new")]
+    _fields_ += [(n, C.c_int) for n in ("on_demand", "preempt_swap", "order_shortest")]
+
+
+class GhLaneInput(C.Structure):
+    _fields_ = [("src", C.c_int32), ("tok", C.c_int32), ("pos", C.c_int32)]
+
+
+class GhKvAction(C.Structure):
+    _fields_ = [("op", C.c_int32), ("lane", C.c_uint32), ("n", C.c_uint32), ("buf", C.c_uint64)]
+
+
 u64, u32, i32, i64, vp = C.c_uint64, C.c_uint32, C.c_int32, C.c_int64, C.c_void_p
 P = C.POINTER
 st = C.c_int  # gh_status
@@ -132,6 +155,23 @@ PROTOTYPES = {
     "gh_engine_advance": (st, [vp, u32, C.c_int, vp]),
     "gh_engine_read_next": (st, [vp, u32, vp]),
     "gh_engine_layout": (st, [u32, u32, u32, u32, u64, u32, P(GhRankLayout)]),
+    "gh_dispatcher_create": (st, [vp, P(GhDispatchConfig), P(vp)]),
+    "gh_dispatcher_destroy": (st, [vp]),
+    "gh_dispatcher_submit": (st, [vp, vp, u32, C.c_float, u32, P(u64)]),
+    "gh_dispatcher_step": (st, [vp, P(C.c_int)]),
+    "gh_dispatcher_run": (st, [vp, P(u64)]),
+    "gh_dispatcher_result": (st, [vp, u64, vp, u32, P(u32)]),
+    "gh_dispatcher_stats": (st, [vp, P(GhDispatchStats)]),
+    "gh_sched_create": (st, [P(GhSchedConfig), P(vp)]),
+    "gh_sched_destroy": (st, [vp]),
+    "gh_sched_submit": (st, [vp, vp, u32, C.c_float, u32, P(u64)]),
+    "gh_sched_plan": (st, [vp, P(GhLaneInput), P(GhKvAction), u32, P(u32)]),
+    "gh_sched_commit": (st, [vp]),
+    "gh_sched_resolve": (st, [vp, vp]),
+    "gh_sched_done": (C.c_int, [vp]),
+    "gh_sched_unresolved": (u32, [vp]),
+    "gh_sched_result": (st, [vp, u64, vp, u32, P(u32)]),
+    "gh_sched_stats": (st, [vp, P(GhDispatchStats)]),
     "gh_engine_keep_logits": (st, [vp, C.c_int]),
     "gh_engine_read_logits": (st, [vp, u32, vp]),
     "gh_engine_tier1": (vp, [vp]),

@@ -352,6 +352,23 @@ cudaError_t launch_advance(int32_t* tok, const int32_t* next, int32_t* pos, int 
   return launch_pdl(advance_kernel, (n + 255) / 256, 256, 0, st, tok, next, pos, n, inc);
 }
 
+// Dispatcher inputs of one in-flight batch (sched.hpp): in = [src | tok | pos] x n rows; a row
+// whose src is 2 (device feedback) takes the token its previous step generated.
+__global__ void dispatch_inputs_kernel(int32_t* tok, const int32_t* next, int32_t* pos, const int32_t* in, int n) {
+  griddep_wait();
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) {
+    tok[i] = in[i] == 2 ? next[i] : in[n + i];
+    pos[i] = in[2 * n + i];
+  }
+}
+cudaError_t launch_dispatch_inputs(int32_t* tok, const int32_t* next, int32_t* pos, const int32_t* in, int n,
+                                   cudaStream_t st) {
+  if (n <= 0) return cudaSuccess;
+  // like the advance kernel, the batch-state writer never triggers its dependents early
+  return launch_pdl(dispatch_inputs_kernel, (n + 255) / 256, 256, 0, st, tok, next, pos, in, n);
+}
+
 // ====================================================================== SIMT GEMM (fp32 storage)
 // One warp per weight row n, 4 batch columns per warp; lanes stride K (coalesced on W and X).
 template <typename T>

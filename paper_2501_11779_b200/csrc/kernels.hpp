@@ -130,6 +130,9 @@ cudaError_t configure_kernels();
 
 cudaError_t launch_advance(int32_t* tok, const int32_t* next, int32_t* pos, int n, int inc,
                            cudaStream_t st);
+// dispatcher inputs: in = [src (0 idle, 1 host, 2 device feedback) | tok | pos] x n
+cudaError_t launch_dispatch_inputs(int32_t* tok, const int32_t* next, int32_t* pos, const int32_t* in, int n,
+                                   cudaStream_t st);
 
 uint64_t& launch_counter();
 

@@ -28,6 +28,7 @@
 #include "gh/gh.h"
 #include "internal.hpp"
 #include "kernels.hpp"
+#include "sched.hpp"
 
 namespace gh {
 
@@ -610,6 +611,18 @@ struct gh_tier2 {
   std::vector<int> h_pt;            // host mirror
   std::vector<uint32_t> mapped;     // pages mapped per slot
   std::vector<int> free_pages;      // LIFO pool
+  // stream-ordered page-table updates (the dispatcher maps without synchronising): pinned
+  // mirrors of the table, one per step of a small ring, each guarded by the event of its copies
+  static constexpr int kPtRing = 4;
+  int* pt_stage[kPtRing] = {};
+  cudaEvent_t pt_ev[kPtRing] = {};
+  int pt_cur = -1;
+  ~gh_tier2() {
+    for (int i = 0; i < kPtRing; ++i) {
+      if (pt_stage[i]) cudaFreeHost(pt_stage[i]);
+      if (pt_ev[i]) cudaEventDestroy(pt_ev[i]);
+    }
+  }
   long span() const { return paged ? kKvPagePositions : sh.S; }   // positions per block
   long slot_stride() const { return 2L * sh.Hkv * span() * sh.dh; }  // per slot (contiguous) or page
   long kv_stride() const { return (long)sh.Hkv * span() * sh.dh; }
@@ -716,6 +729,53 @@ gh_status gh_tier2_map(gh_tier2* t, uint32_t slot, uint32_t n_positions, void* s
   GH_CUDA(cudaStreamSynchronize(st));
   return GH_OK;
 }
+
+}  // extern "C"
+
+// ---- stream-ordered page-table updates (dispatcher).  Steps already queued on the stream keep
+// reading the old entries; the copy lands before the next step, so no host synchronisation.
+static gh_status t2_updates_begin(gh_tier2* t) {
+  if (!t->paged) return GH_OK;
+  t->pt_cur = (t->pt_cur + 1) % gh_tier2::kPtRing;
+  const int c = t->pt_cur;
+  const size_t n = (size_t)t->n_slots * t->max_pages;
+  if (!t->pt_stage[c]) {
+    GH_CUDA(cudaMallocHost((void**)&t->pt_stage[c], n * sizeof(int)));
+    GH_CUDA(cudaEventCreateWithFlags(&t->pt_ev[c], cudaEventDisableTiming));
+  } else {
+    GH_CUDA(cudaEventSynchronize(t->pt_ev[c]));  // its copies of kPtRing steps ago are done
+  }
+  return GH_OK;
+}
+static gh_status t2_map_async(gh_tier2* t, uint32_t slot, uint32_t n_positions, cudaStream_t st) {
+  if (slot >= t->n_slots) return fail(GH_EINVAL, "slot " + std::to_string(slot) + " >= n_slots");
+  if (n_positions > (uint32_t)t->sh.S)
+    return fail(GH_EINFEASIBLE, std::to_string(n_positions) + " positions exceed max_seq_len");
+  if (!t->paged) return GH_OK;
+  const uint32_t need = (n_positions + kKvPagePositions - 1) / kKvPagePositions;
+  const uint32_t have = t->mapped[slot];
+  if (need <= have) return GH_OK;
+  if (need - have > t->free_pages.size())
+    return fail(GH_EINFEASIBLE, "KV page pool exhausted (binding constraint: memory)");
+  const size_t base = (size_t)slot * t->max_pages;
+  int* row = t->h_pt.data() + base;
+  int* stage = t->pt_stage[t->pt_cur] + base;
+  for (uint32_t p = have; p < need; ++p) {
+    row[p] = t->free_pages.back();
+    t->free_pages.pop_back();
+    stage[p] = row[p];
+  }
+  t->mapped[slot] = need;
+  GH_CUDA(cudaMemcpyAsync(t->d_pt + base + have, stage + have, (size_t)(need - have) * sizeof(int),
+                          cudaMemcpyHostToDevice, st));
+  return GH_OK;
+}
+static gh_status t2_updates_end(gh_tier2* t, cudaStream_t st) {
+  if (t->paged) GH_CUDA(cudaEventRecord(t->pt_ev[t->pt_cur], st));
+  return GH_OK;
+}
+
+extern "C" {
 
 gh_status gh_tier2_unmap(gh_tier2* t, uint32_t slot) {
   if (!t) return fail(GH_EINVAL, "null argument");
@@ -1969,6 +2029,317 @@ gh_status gh_engine_step_host(gh_engine* e, uint32_t ib, const int32_t* tok_host
       GH_CUDA(cudaMemcpyAsync(logits_host, b.logits, (size_t)R * e->sh.V * 4, cudaMemcpyDeviceToHost, st));
   }
   GH_CUDA(cudaStreamSynchronize(st));
+  return GH_OK;
+}
+
+}  // extern "C"
+
+// ================================================================== batch-state dispatcher
+// The host scheduler (sched.hpp) driving the engine: IF in-flight batches x B lanes, each lane
+// bound to its context slot (colocated: ib * B + row; Tier-2 rank: ib * cnt + row - off, the
+// engine's default slots), continuous refill from the queue, per-shard page accounting.  Every
+// step: KV actions of the lanes this rank holds (stream-ordered page-table updates, no host
+// synchronisation), the lane inputs uploaded from a pinned ring and selected on the device
+// (prompt token from the host or the lane's own previous token), the engine step over all
+// in-flight batches (gh_engine_step_all: pipelined tier split, or the colocated CUDA graphs),
+// and the next tokens copied back into the ring; the host reads a step's tokens one step later,
+// so it never waits for the step it just queued.  Every rank of a tier split runs the same
+// dispatcher over the same requests (decisions never depend on token values).
+struct gh_sched {
+  Sched s;
+};
+
+struct gh_dispatcher {
+  gh_engine* e = nullptr;
+  Sched s;
+  static constexpr int kRing = 4;
+  int32_t* h_in = nullptr;     // pinned [kRing][IF][3][B] lane inputs
+  int32_t* h_next = nullptr;   // pinned [kRing][IF][B] next tokens
+  float* h_temp = nullptr;     // pinned [kRing][IF][B] 1 / temperature
+  uint32_t* h_seed = nullptr;  // pinned [kRing][IF][B]
+  int32_t* d_in = nullptr;     // device [IF][3][B]
+  cudaEvent_t ev[kRing] = {};
+  bool ev_used[kRing] = {};
+  std::map<uint64_t, void*> swapbuf;  // swap id -> pinned host buffer
+  std::unique_ptr<DevMem> din_mem;
+  cudaStream_t st = nullptr;
+  ~gh_dispatcher() {
+    if (st) cudaStreamSynchronize(st);
+    for (auto& kv : swapbuf) cudaFreeHost(kv.second);
+    if (h_in) cudaFreeHost(h_in);
+    if (h_next) cudaFreeHost(h_next);
+    if (h_temp) cudaFreeHost(h_temp);
+    if (h_seed) cudaFreeHost(h_seed);
+    for (auto v : ev) if (v) cudaEventDestroy(v);
+    if (st) cudaStreamDestroy(st);
+  }
+  uint32_t B() const { return e->cfg.batch; }
+  uint32_t IF() const { return (uint32_t)e->batches.size(); }
+  bool tokens_here() const { return e->role != 2; }  // Tier-1 (every TP rank) / colocated
+  // the local slot of a lane when this rank holds its KV, else -1
+  int64_t holder_slot(uint32_t lane) const {
+    const uint32_t ib = lane / B(), row = lane % B();
+    if (e->role == 0) return (int64_t)ib * B() + row;
+    if (e->role == 2) {
+      const int off = e->shard_off[e->shard];
+      if ((int)row >= off && (int)row < off + e->my_cnt) return (int64_t)ib * e->my_cnt + (row - off);
+    }
+    return -1;
+  }
+};
+
+static SchedConfig sched_config(const gh_dispatch_config* c, uint32_t batch, uint32_t inflight, uint32_t kp,
+                                uint32_t pages, uint32_t max_seq) {
+  SchedConfig sc;
+  sc.batch = batch; sc.inflight = inflight; sc.kp = kp; sc.pages = pages; sc.max_seq = max_seq;
+  sc.max_new = c->max_new; sc.on_demand = c->on_demand != 0; sc.swap = c->preempt_swap != 0;
+  sc.shortest = c->order_shortest != 0;
+  return sc;
+}
+
+static gh_status disp_apply(gh_dispatcher* d, const std::vector<KvAction>& acts) {
+  gh_engine* e = d->e;
+  gh_tier2* t = e->t2;
+  if (!t) return GH_OK;  // Tier-1 holds no KV
+  GH_TRY(t2_updates_begin(t));
+  for (const KvAction& a : acts) {
+    const int64_t slot = d->holder_slot(a.lane);
+    if (slot < 0) continue;
+    switch (a.op) {
+      case kMap: GH_TRY(t2_map_async(t, (uint32_t)slot, a.n, d->st)); break;
+      case kUnmap: GH_TRY(gh_tier2_unmap(t, (uint32_t)slot)); break;
+      case kSwapOut: {  // synchronous: waits for the steps that wrote the positions
+        const uint64_t bytes = gh_tier2_kv_swap_bytes(t, a.n);
+        void* h = nullptr;
+        GH_CUDA(cudaMallocHost(&h, std::max<uint64_t>(bytes, 1)));
+        d->swapbuf[a.buf] = h;
+        GH_TRY(gh_tier2_kv_swap(t, (uint32_t)slot, a.n, h, 1, d->st));
+        break;
+      }
+      case kSwapIn: {
+        auto it = d->swapbuf.find(a.buf);
+        if (it == d->swapbuf.end()) return fail(GH_EINTERNAL, "swap buffer missing on its shard");
+        GH_TRY(gh_tier2_kv_swap(t, (uint32_t)slot, a.n, it->second, 0, d->st));
+        cudaFreeHost(it->second);
+        d->swapbuf.erase(it);
+        break;
+      }
+    }
+  }
+  return t2_updates_end(t, d->st);
+}
+
+// one step: plan, KV actions, inputs, engine step, next tokens back (resolved one step later)
+static gh_status disp_step(gh_dispatcher* d, bool* idle) {
+  gh_engine* e = d->e;
+  std::vector<LaneInput> in;
+  std::vector<KvAction> acts;
+  std::string err = d->s.plan(in, acts);
+  if (!err.empty()) return fail(GH_EINFEASIBLE, err);
+  bool busy = false;
+  for (auto& x : in) busy |= x.src != kIdle;
+  GH_TRY(disp_apply(d, acts));
+  *idle = !busy;
+  if (!busy) return GH_OK;  // nothing to decode: the caller drains the unresolved steps
+  const uint32_t B = d->B(), IF = d->IF();
+  const int k = (int)(d->s.steps % gh_dispatcher::kRing);
+  if (d->ev_used[k]) GH_CUDA(cudaEventSynchronize(d->ev[k]));  // ring slot k's copies are done
+  if (d->tokens_here()) {
+    int32_t* hin = d->h_in + (size_t)k * IF * 3 * B;
+    for (uint32_t l = 0; l < IF * B; ++l) {
+      const uint32_t ib = l / B, r = l % B;
+      int32_t* b3 = hin + (size_t)ib * 3 * B;
+      b3[r] = in[l].src;
+      b3[B + r] = in[l].tok;
+      b3[2 * B + r] = in[l].pos;
+    }
+    GH_CUDA(cudaMemcpyAsync(d->d_in, hin, (size_t)IF * 3 * B * 4, cudaMemcpyHostToDevice, d->st));
+    std::vector<float> it;
+    std::vector<uint32_t> sd;
+    if (d->s.sampling(it, sd)) {  // per-row batch-state temperature
+      float* ht = d->h_temp + (size_t)k * IF * B;
+      uint32_t* hs = d->h_seed + (size_t)k * IF * B;
+      std::copy(it.begin(), it.end(), ht);
+      std::copy(sd.begin(), sd.end(), hs);
+      for (uint32_t ib = 0; ib < IF; ++ib) {
+        auto& b = e->batches[ib];
+        GH_CUDA(cudaMemcpyAsync(b.inv_temp, ht + (size_t)ib * B, B * 4, cudaMemcpyHostToDevice, d->st));
+        GH_CUDA(cudaMemcpyAsync(b.seed, hs + (size_t)ib * B, B * 4, cudaMemcpyHostToDevice, d->st));
+        bool any = false;
+        for (uint32_t r = 0; r < B; ++r) any |= ht[(size_t)ib * B + r] != 0.f;
+        if (any != b.sampling) {
+          b.sampling = any;
+          if (b.graph) {  // the classifier path changes: recapture the colocated step
+            GH_CUDA(cudaStreamSynchronize(d->st));
+            cudaGraphExecDestroy(b.graph);
+            b.graph = nullptr;
+          }
+        }
+      }
+    }
+    for (uint32_t ib = 0; ib < IF; ++ib) {
+      auto& b = e->batches[ib];
+      GH_CUDA(launch_dispatch_inputs(b.tok, b.next, b.pos, d->d_in + (size_t)ib * 3 * B, (int)B, d->st));
+    }
+  }
+  GH_TRY(gh_engine_step_all(e, d->st));
+  if (d->tokens_here()) {
+    int32_t* hn = d->h_next + (size_t)k * IF * B;
+    for (uint32_t ib = 0; ib < IF; ++ib)
+      GH_CUDA(cudaMemcpyAsync(hn + (size_t)ib * B, e->batches[ib].next, B * 4, cudaMemcpyDeviceToHost, d->st));
+  }
+  GH_CUDA(cudaEventRecord(d->ev[k], d->st));
+  d->ev_used[k] = true;
+  d->s.commit();
+  return GH_OK;
+}
+
+// tokens of the oldest unresolved step (its ring slot's copies are complete once its event is)
+static gh_status disp_resolve_one(gh_dispatcher* d) {
+  const uint64_t step = d->s.steps - d->s.unresolved();  // index of the oldest unresolved step
+  const int k = (int)(step % gh_dispatcher::kRing);
+  if (d->tokens_here()) {
+    GH_CUDA(cudaEventSynchronize(d->ev[k]));
+    d->s.resolve(d->h_next + (size_t)k * d->IF() * d->B());
+  } else {
+    d->s.resolve(nullptr);  // Tier-2 ranks: values are irrelevant, the resolution point is not
+  }
+  return GH_OK;
+}
+
+extern "C" {
+
+gh_status gh_sched_create(const gh_sched_config* c, gh_sched** out) {
+  if (!c || !out) return fail(GH_EINVAL, "null argument");
+  *out = nullptr;
+  gh_dispatch_config dc{c->max_new, c->on_demand, c->preempt_swap, c->order_shortest};
+  auto g = std::make_unique<gh_sched>();
+  std::string err = g->s.init(sched_config(&dc, c->batch, c->inflight, c->kp, c->pages, c->max_seq));
+  if (!err.empty()) return fail(GH_EINVAL, err);
+  *out = g.release();
+  return GH_OK;
+}
+gh_status gh_sched_destroy(gh_sched* g) { delete g; return GH_OK; }
+gh_status gh_sched_submit(gh_sched* g, const int32_t* prompt, uint32_t len, float temperature, uint32_t seed,
+                          uint64_t* id) {
+  if (!g || !prompt || !id) return fail(GH_EINVAL, "null argument");
+  std::string err = g->s.submit(prompt, len, temperature, seed, id);
+  return err.empty() ? GH_OK : fail(GH_EINFEASIBLE, err);
+}
+gh_status gh_sched_plan(gh_sched* g, gh_lane_input* in, gh_kv_action* acts, uint32_t cap, uint32_t* n_acts) {
+  if (!g || !in || !n_acts) return fail(GH_EINVAL, "null argument");
+  std::vector<LaneInput> li;
+  std::vector<KvAction> ka;
+  std::string err = g->s.plan(li, ka);
+  if (!err.empty()) return fail(GH_EINFEASIBLE, err);
+  for (size_t i = 0; i < li.size(); ++i) in[i] = {li[i].src, li[i].tok, li[i].pos};
+  *n_acts = (uint32_t)ka.size();
+  if (ka.size() > cap) return fail(GH_EINVAL, "action buffer too small");
+  for (size_t i = 0; i < ka.size(); ++i) acts[i] = {ka[i].op, ka[i].lane, ka[i].n, ka[i].buf};
+  return GH_OK;
+}
+gh_status gh_sched_commit(gh_sched* g) {
+  if (!g) return fail(GH_EINVAL, "null argument");
+  g->s.commit();
+  return GH_OK;
+}
+gh_status gh_sched_resolve(gh_sched* g, const int32_t* next) {
+  if (!g) return fail(GH_EINVAL, "null argument");
+  if (!g->s.unresolved()) return fail(GH_EINVAL, "no unresolved step");
+  g->s.resolve(next);
+  return GH_OK;
+}
+int gh_sched_done(const gh_sched* g) { return g && g->s.done() ? 1 : 0; }
+uint32_t gh_sched_unresolved(const gh_sched* g) { return g ? g->s.unresolved() : 0; }
+static gh_status sched_result(const Sched& s, uint64_t id, int32_t* tokens, uint32_t cap, uint32_t* n) {
+  const std::vector<int32_t>* r = s.result(id);
+  if (!r) return fail(GH_EINVAL, "request " + std::to_string(id) + " is not finished (or not resolved)");
+  *n = (uint32_t)r->size();
+  if (tokens) std::copy(r->begin(), r->begin() + std::min<size_t>(cap, r->size()), tokens);
+  return GH_OK;
+}
+static void sched_stats(const Sched& s, gh_dispatch_stats* o) {
+  o->steps = s.steps; o->admitted = s.admitted; o->finished = s.finished; o->tokens = s.tokens;
+  o->preemptions = s.preemptions; o->swaps = s.swaps; o->peak_pages = s.peak_pages;
+}
+gh_status gh_sched_result(const gh_sched* g, uint64_t id, int32_t* tokens, uint32_t cap, uint32_t* n) {
+  if (!g || !n) return fail(GH_EINVAL, "null argument");
+  return sched_result(g->s, id, tokens, cap, n);
+}
+gh_status gh_sched_stats(const gh_sched* g, gh_dispatch_stats* out) {
+  if (!g || !out) return fail(GH_EINVAL, "null argument");
+  sched_stats(g->s, out);
+  return GH_OK;
+}
+
+gh_status gh_dispatcher_create(gh_engine* e, const gh_dispatch_config* cfg, gh_dispatcher** out) {
+  if (!e || !cfg || !out) return fail(GH_EINVAL, "null argument");
+  *out = nullptr;
+  if (e->n1 > 1) return fail(GH_EUNSUPPORTED, "the dispatcher drives one Tier-1 span (or TP ranks), not pipeline spans");
+  if (e->cfg.prefill) return fail(GH_EUNSUPPORTED, "prefill-row engines are driven by the mixed dispatcher");
+  GH_CUDA(cudaSetDevice(e->cfg.device));
+  auto d = std::make_unique<gh_dispatcher>();
+  d->e = e;
+  const uint32_t kp = e->role == 0 ? 0 : (uint32_t)e->kp;
+  const uint32_t pages = e->cfg.kv_pages;
+  std::string err = d->s.init(sched_config(cfg, e->cfg.batch, (uint32_t)e->batches.size(), kp, pages, (uint32_t)e->sh.S));
+  if (!err.empty()) return fail(GH_EINVAL, err);
+  const size_t n = (size_t)d->IF() * d->B();
+  GH_CUDA(cudaStreamCreateWithFlags(&d->st, cudaStreamNonBlocking));
+  GH_CUDA(cudaMallocHost((void**)&d->h_in, gh_dispatcher::kRing * n * 3 * 4));
+  GH_CUDA(cudaMallocHost((void**)&d->h_next, gh_dispatcher::kRing * n * 4));
+  GH_CUDA(cudaMallocHost((void**)&d->h_temp, gh_dispatcher::kRing * n * 4));
+  GH_CUDA(cudaMallocHost((void**)&d->h_seed, gh_dispatcher::kRing * n * 4));
+  d->din_mem = std::make_unique<DevMem>();
+  GH_CUDA(cudaMalloc(&d->din_mem->p, n * 3 * 4));
+  d->d_in = (int32_t*)d->din_mem->p;
+  for (auto& v : d->ev) GH_CUDA(cudaEventCreateWithFlags(&v, cudaEventDisableTiming));
+  *out = d.release();
+  return GH_OK;
+}
+gh_status gh_dispatcher_destroy(gh_dispatcher* d) {
+  if (d) {
+    cudaSetDevice(d->e->cfg.device);
+    delete d;
+  }
+  return GH_OK;
+}
+gh_status gh_dispatcher_submit(gh_dispatcher* d, const int32_t* prompt, uint32_t len, float temperature,
+                               uint32_t seed, uint64_t* id) {
+  if (!d || !prompt || !id) return fail(GH_EINVAL, "null argument");
+  if (temperature < 0.f) return fail(GH_EINVAL, "temperature must be >= 0");
+  std::string err = d->s.submit(prompt, len, temperature, seed, id);
+  return err.empty() ? GH_OK : fail(GH_EINFEASIBLE, err);
+}
+gh_status gh_dispatcher_step(gh_dispatcher* d, int* busy) {
+  if (!d) return fail(GH_EINVAL, "null argument");
+  GH_CUDA(cudaSetDevice(d->e->cfg.device));
+  bool idle = false;
+  GH_TRY(disp_step(d, &idle));
+  if (idle) {  // nothing to decode until every step's tokens are known (preempted requests wait)
+    while (d->s.unresolved()) GH_TRY(disp_resolve_one(d));
+  } else if (d->s.unresolved() > 1) {
+    GH_TRY(disp_resolve_one(d));  // the step before the one just queued
+  }
+  if (busy) *busy = d->s.done() ? 0 : 1;
+  return GH_OK;
+}
+gh_status gh_dispatcher_run(gh_dispatcher* d, uint64_t* steps) {
+  if (!d) return fail(GH_EINVAL, "null argument");
+  GH_CUDA(cudaSetDevice(d->e->cfg.device));
+  while (!d->s.done()) GH_TRY(gh_dispatcher_step(d, nullptr));
+  while (d->s.unresolved()) GH_TRY(disp_resolve_one(d));
+  GH_CUDA(cudaStreamSynchronize(d->st));
+  if (steps) *steps = d->s.steps;
+  return GH_OK;
+}
+gh_status gh_dispatcher_result(const gh_dispatcher* d, uint64_t id, int32_t* tokens, uint32_t cap, uint32_t* n) {
+  if (!d || !n) return fail(GH_EINVAL, "null argument");
+  return sched_result(d->s, id, tokens, cap, n);
+}
+gh_status gh_dispatcher_stats(const gh_dispatcher* d, gh_dispatch_stats* out) {
+  if (!d || !out) return fail(GH_EINVAL, "null argument");
+  sched_stats(d->s, out);
   return GH_OK;
 }
 

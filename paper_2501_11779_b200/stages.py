@@ -335,235 +335,192 @@ class Dispatcher:
         return gen, (np.stack(logits, axis=1) if want_logits else None)
 
 
+class Scheduler:
+    """The dispatcher's decision logic (C++ gh_sched, host only): batch-state objects of IF
+    in-flight batches x B lanes with per-shard page accounting (sched.hpp).
+    plan() -> (inputs [lanes] of (src, tok, pos), KV actions); the caller runs the step, then
+    commit(), and resolve(next tokens) for the oldest committed step (any lag)."""
+
+    SRC_IDLE, SRC_HOST, SRC_DEVICE = 0, 1, 2
+    MAP, UNMAP, SWAP_OUT, SWAP_IN = 0, 1, 2, 3
+
+    def __init__(self, batch: int, max_new: int, inflight: int = 1, kp: int = 0, pages: int = 0, max_seq: int = 0,
+                 on_demand: bool = False, preempt: str = "recompute", order: str = "fifo"):
+        cfg = L.GhSchedConfig(batch, inflight, kp, pages, max_seq, max_new, int(on_demand), int(preempt == "swap"),
+                              int(order == "shortest"))
+        h = C.c_void_p()
+        L.check(L.lib().gh_sched_create(C.byref(cfg), C.byref(h)))
+        self.h = h
+        self.lanes = batch * inflight
+        self._in = (L.GhLaneInput * self.lanes)()
+        self._acts = (L.GhKvAction * (8 * self.lanes + 16))()
+
+    def close(self):
+        if getattr(self, "h", None) and L is not None and L.lib is not None:
+            L.lib().gh_sched_destroy(self.h)
+            self.h = None
+
+    __del__ = close
+
+    def submit(self, prompt, temperature: float = 0.0, seed: int = 0) -> int:
+        p = np.ascontiguousarray(prompt, dtype=np.int32)
+        i = C.c_uint64()
+        L.check(L.lib().gh_sched_submit(self.h, p.ctypes.data, len(p), temperature, seed, C.byref(i)))
+        return i.value
+
+    def plan(self):
+        n = C.c_uint32()
+        L.check(L.lib().gh_sched_plan(self.h, self._in, self._acts, len(self._acts), C.byref(n)))
+        ins = np.array([(x.src, x.tok, x.pos) for x in self._in], np.int32).reshape(self.lanes, 3)
+        return ins, [(a.op, a.lane, a.n, a.buf) for a in self._acts[:n.value]]
+
+    def commit(self):
+        L.check(L.lib().gh_sched_commit(self.h))
+
+    def resolve(self, next_tokens=None):
+        p = None if next_tokens is None else np.ascontiguousarray(next_tokens, dtype=np.int32)
+        L.check(L.lib().gh_sched_resolve(self.h, None if p is None else p.ctypes.data))
+
+    @property
+    def done(self) -> bool:
+        return bool(L.lib().gh_sched_done(self.h))
+
+    @property
+    def unresolved(self) -> int:
+        return L.lib().gh_sched_unresolved(self.h)
+
+    def result(self, i: int) -> np.ndarray:
+        return _result(L.lib().gh_sched_result, self.h, i)
+
+    def stats(self) -> dict:
+        o = L.GhDispatchStats()
+        L.check(L.lib().gh_sched_stats(self.h, C.byref(o)))
+        return {f: getattr(o, f) for f, _ in o._fields_}
+
+
+def _result(fn, h, i):
+    n = C.c_uint32()
+    L.check(fn(h, i, None, 0, C.byref(n)))
+    out = np.empty(n.value, np.int32)
+    L.check(fn(h, i, out.ctypes.data, n.value, C.byref(n)))
+    return out
+
+
 class ContinuousDispatcher:
-    """Continuous batching with context-slot reuse: the engine's B rows
-    are decode lanes, each bound to its own context slot; a request occupies a lane from its first
-    prompt token until it has generated `max_new` tokens, and the lane (with its slot) is then
-    handed to the next queued request at position 0.  Every step decodes all busy lanes at their
-    own positions (ragged contexts); idle lanes decode a dummy token at position 0 and are
-    ignored.  Reusing a slot needs no clearing: attention reads only the positions below the
-    request's current one, all of which it wrote itself.
+    """Continuous batching with context-slot reuse -- a thin wrapper over
+    the native batch-state dispatcher (gh_dispatcher_*, C++ sched.hpp / runtime.cu).
+
+    The engine's IF x B rows are decode lanes, each bound to its own context slot; a request
+    occupies a lane from its first prompt token until it has generated `max_new` tokens, and the
+    lane (with its slot) then goes to the next queued request at position 0.  Every step decodes
+    all busy lanes of every in-flight batch at their own positions through gh_engine_step_all
+    (the pipelined tier split, or the colocated CUDA graphs); lane inputs, page tables and the
+    sampling state are updated stream-ordered, and a step's tokens are read one step later.
 
     With a paged KV arena (Engine(kv_pages=...)) a request maps exactly the positions it will
     attend (prompt + max_new - 1) when it is admitted and returns its pages when it finishes; a
-    request waits in the queue (its lane idles on one page) until its lane's pool can back it.
+    request waits in the queue while its shard's pool cannot back it.  ``on_demand=True`` maps
+    only the prompt and grows a page at a time; when a shard's pool is dry its most recently
+    admitted request is preempted -- recomputed (``preempt="recompute"``: it re-enters the queue
+    head and re-reads its prompt plus the tokens it generated) or swapped to host memory
+    (``preempt="swap"``: restored into a lane of the same Tier-2 shard, resuming at its saved
+    position).  ``order="shortest"`` admits the shortest prompts first.
 
-    On-demand paging (``on_demand=True``, paged arena only): admission maps only the
-    request's prompt, and a lane maps one more page when its next position crosses a page
-    boundary.  When its shard's pool is dry, the most recently admitted request of that shard is
-    preempted: its pages return to the pool and it goes back to the head of the queue with the
-    tokens it has generated appended to its prompt, so re-admission recomputes its context
-    (positions, weights and row results are unchanged, hence so are its tokens).  The oldest
-    request of a shard always advances, so the loop terminates.  ``self.preemptions`` counts them.
-    ``order="shortest"`` admits the shortest prompts first (max_new is common to all requests, so
-    this is shortest-job-first); a preempted request still re-enters at the queue head.
-    With ``preempt="swap"`` the preempted request's context is copied to host memory instead
-    (gh_engine_kv_swap) and restored into whichever lane re-admits it, which resumes at the saved
-    position without recomputing.  In the tier split the buffer lives on the request's Tier-2
-    shard, so a lane of another shard that admits it recomputes its context instead.
-
-    Tier split: every rank runs the same dispatcher over the same requests (SPMD).  Admission
-    depends only on prompt lengths, max_new and the page accounting (kept here for every Tier-2
-    shard), never on token values, so all ranks take identical decisions; a Tier-2 rank maps the
-    pages of the lanes in its shard and steps with no host tokens, and only Tier-1 sees tokens."""
+    Tier split: every rank runs the same dispatcher over the same requests (SPMD); decisions depend
+    only on lengths, max_new and page counts.  Tier-2 ranks apply their shard's KV actions;
+    Tier-1 ranks (every tensor-parallel one) feed tokens.  Engines that are not an ``Engine`` (test
+    doubles with kv_map / kv_unmap / kv_swap_out / kv_swap_in / set_sampling / step_host / shard)
+    are driven by the same native decision logic (gh_sched) from Python."""
 
     PAGE = 64  # GH_KV_PAGE_POSITIONS
 
-    def __init__(self, engine: Engine, on_demand: bool = False, preempt: str = "recompute",
-                 order: str = "fifo"):
+    def __init__(self, engine, on_demand: bool = False, preempt: str = "recompute", order: str = "fifo"):
         if preempt not in ("recompute", "swap"):
             raise ValueError(f"preempt must be 'recompute' or 'swap', not {preempt!r}")
         if order not in ("fifo", "shortest"):
             raise ValueError(f"order must be 'fifo' or 'shortest', not {order!r}")
-        self.order = order
-        self.engine = engine
-        self.on_demand = on_demand
-        self.preempt = preempt
+        self.engine, self.on_demand, self.preempt, self.order = engine, on_demand, preempt, order
         self.preemptions = 0
+        self.stats = {}
 
     def run(self, requests, max_new: int, sampling=None):
-        """requests: sequence of 1-D int32 prompt arrays (any lengths >= 1); sampling: optional
-        per-request (temperature, seed) pairs (temperature 0 = greedy, the default).  Returns the
-        list of generated token arrays (max_new each, in request order; zeros on Tier-2 ranks)
-        and the number of steps."""
+        """requests: sequence of 1-D int32 prompts (any lengths >= 1); sampling: optional
+        per-request (temperature, seed) pairs (temperature 0 = greedy).  Returns (generated token
+        arrays, max_new each, in request order -- zeros on Tier-2 ranks -- and the step count)."""
+        eng = self.engine
+        on_demand = self.on_demand and eng.kv_pages > 0
+        if not isinstance(eng, Engine):
+            return self._run_host(requests, max_new, sampling, on_demand)
+        cfg = L.GhDispatchConfig(max_new, int(on_demand), int(self.preempt == "swap"), int(self.order == "shortest"))
+        h = C.c_void_p()
+        L.check(L.lib().gh_dispatcher_create(eng.h, C.byref(cfg), C.byref(h)))
+        try:
+            ids = []
+            for i, q in enumerate(requests):
+                t, sd = sampling[i] if sampling is not None else (0.0, 0)
+                p = np.ascontiguousarray(q, dtype=np.int32)
+                rid = C.c_uint64()
+                L.check(L.lib().gh_dispatcher_submit(h, p.ctypes.data, len(p), float(t), int(sd), C.byref(rid)))
+                ids.append(rid.value)
+            steps = C.c_uint64()
+            L.check(L.lib().gh_dispatcher_run(h, C.byref(steps)))
+            out = [_result(L.lib().gh_dispatcher_result, h, i) for i in ids]
+            o = L.GhDispatchStats()
+            L.check(L.lib().gh_dispatcher_stats(h, C.byref(o)))
+            self.stats = {f: getattr(o, f) for f, _ in o._fields_}
+        finally:
+            L.lib().gh_dispatcher_destroy(h)
+        self.preemptions = self.stats["preemptions"]
+        return out, int(steps.value)
+
+    def _run_host(self, requests, max_new, sampling, on_demand):
+        """The native decision logic driving a duck-typed engine from Python, one step of lag."""
+        from collections import deque
         eng = self.engine
         B = eng.batch
-        role = eng.role
-        index, off, cnt, kp = eng.shard()
-        # lane -> shard (the rows of each Tier-2 rank, analytic.cpp:119) and per-shard page pools
-        if kp:
-            from .spec import shard_plan
-            offs, cnts = shard_plan(B, kp)
-            lane_shard = np.repeat(np.arange(kp), cnts)
-        else:
-            lane_shard = np.zeros(B, np.int64)
-        paged = eng.kv_pages > 0
-        free = [eng.kv_pages] * max(1, kp)
-        mapped = [0] * B                  # pages held by each lane
-
-        def pages(n):
-            return -(-n // self.PAGE)
-
-        def kv_unmap(lane):
-            free[lane_shard[lane]] += mapped[lane]
-            mapped[lane] = 0
-            if role != "tier1" and off <= lane < off + cnt:
-                eng.kv_unmap(lane - off)
-
-        def kv_map(lane, n):              # False when the lane's pool cannot back n positions
-            need = pages(n) - mapped[lane] if paged else 0
-            sh = lane_shard[lane]
-            # keep one page for every other lane of the shard that holds none (its dummy token)
-            empty = sum(1 for o in range(B) if o != lane and lane_shard[o] == sh and mapped[o] == 0) if paged else 0
-            if need > free[sh] - empty:
-                return False
-            if role != "tier1" and off <= lane < off + cnt:
-                eng.kv_map(lane - off, n)
-            if need > 0:
-                free[lane_shard[lane]] -= need
-                mapped[lane] += need
-            return True
-
-        on_demand = self.on_demand and paged
-        self.preemptions = 0
-        prompt = [np.asarray(q) for q in requests]  # grows by the generated tokens on preemption
-        if on_demand:
-            # a request must fit its shard's pool beside one dummy page per other lane, else
-            # growth would preempt it forever
-            lanes = int(np.bincount(lane_shard).max())
-            for i, q in enumerate(requests):
-                if pages(len(q) + max_new - 1) > eng.kv_pages - (lanes - 1):
-                    raise L.FeasibilityError(L.GH_EINFEASIBLE,
-                                             f"request {i} needs more KV pages than the pool holds")
-        queue = list(range(len(requests)))
-        if self.order == "shortest":  # shortest prompt first (stable: ties keep request order)
-            queue.sort(key=lambda r: len(requests[r]))
-        lane_req = [-1] * B           # request index in each lane
-        lane_seq = [0] * B            # admission order (preemption victims: the latest)
-        n_admit = [0]
-        lane_t = [0] * B              # position of the lane's next input token
-        out = [[] for _ in requests]
-        tok = np.zeros(B, np.int32)
-        pos = np.zeros(B, np.int32)
-        temp = np.zeros(B, np.float32)    # per-lane sampling state (batch-state temperature)
-        seed = np.zeros(B, np.uint32)
-        dirty = [sampling is not None]
-
-        swapped = {}                  # request -> (positions saved, next input token, host buffer, shard)
-
-        def recompute(r):             # re-admission feeds the prompt and the tokens generated so far
-            prompt[r] = np.concatenate([np.asarray(requests[r]),
-                                        np.asarray(out[r], dtype=np.asarray(requests[r]).dtype)])
-
-        def holds(lane):              # this rank holds the lane's KV
-            return role != "tier1" and off <= lane < off + cnt
-
-        def need_at_admission(r, lane):
-            if r in swapped and swapped[r][3] != lane_shard[lane]:
-                # its context sits in another Tier-2 shard's host buffer: recompute it instead
-                swapped.pop(r)
-                recompute(r)
-            if r in swapped:
-                return swapped[r][0]
-            if on_demand:
-                return len(prompt[r])
-            return len(requests[r]) + max_new - 1
-
-        def release(lane):
-            kv_unmap(lane)
-            lane_req[lane] = -1
-            tok[lane] = 0
-            pos[lane] = 0
-            if sampling is not None and temp[lane] != 0:
-                temp[lane] = 0
-                dirty[0] = True
-
-        def admit(lane):
-            release(lane)
-            if queue and kv_map(lane, need_at_admission(queue[0], lane)):
-                r = queue.pop(0)
-                lane_req[lane], lane_t[lane] = r, 0
-                n_admit[0] += 1
-                lane_seq[lane] = n_admit[0]
-                tok[lane] = int(prompt[r][0])
-                if r in swapped:      # resume at the saved position
-                    t, tk, buf, _ = swapped.pop(r)
-                    if holds(lane):
-                        eng.kv_swap_in(lane - off, t, buf)
-                    lane_t[lane], pos[lane], tok[lane] = t, t, tk
-                if sampling is not None:
-                    temp[lane], seed[lane] = sampling[r]
-                    dirty[0] = True
-            if lane_req[lane] < 0 and not kv_map(lane, 1):  # the idle lane's dummy token
-                raise L.FeasibilityError(L.GH_EINFEASIBLE, "KV page pool smaller than one page per lane")
-
-        def preempt(lane):
-            r = lane_req[lane]
-            t = lane_t[lane]
-            if self.preempt == "swap" and t > 0:
-                swapped[r] = (t, int(tok[lane]), eng.kv_swap_out(lane - off, t) if holds(lane) else None,
-                              lane_shard[lane])
-            else:
-                recompute(r)
-            queue.insert(0, r)
-            release(lane)
-            self.preemptions += 1
-            if not kv_map(lane, 1):   # the idle lane's dummy token (its own pages just came back)
-                raise L.FeasibilityError(L.GH_EINFEASIBLE, "KV page pool smaller than one page per lane")
-
-        def grow():
-            # oldest first: a page goes to the longest-running request of the shard
-            for lane in sorted((x for x in range(B) if lane_req[x] >= 0), key=lambda x: lane_seq[x]):
-                if lane_req[lane] < 0 or pages(int(pos[lane]) + 1) <= mapped[lane]:
+        _, off, cnt, kp = eng.shard()
+        sch = Scheduler(B, max_new, 1, kp, eng.kv_pages, getattr(getattr(eng, "spec", None), "max_seq_len", 0),
+                        on_demand, self.preempt, self.order)
+        ids = [sch.submit(q, *(sampling[i] if sampling is not None else (0.0, 0))) for i, q in enumerate(requests)]
+        holds = lambda lane: eng.role != "tier1" and off <= lane < off + cnt  # noqa: E731
+        bufs, hist = {}, deque()
+        last = np.zeros(B, np.int32)
+        while not sch.done:
+            ins, acts = sch.plan()
+            for op, lane, n, buf in acts:
+                if not holds(lane):
                     continue
-                while not kv_map(lane, int(pos[lane]) + 1):
-                    sh = lane_shard[lane]
-                    victim = max((x for x in range(B) if lane_req[x] >= 0 and lane_shard[x] == sh),
-                                 key=lambda x: lane_seq[x])
-                    preempt(victim)
-                    if victim == lane:
-                        break
-
-        for lane in range(B):
-            admit(lane)
-        steps = 0
-        while any(r >= 0 for r in lane_req):
-            if on_demand:
-                grow()
-            if dirty[0] and role != "tier2":
-                eng.set_sampling(temp, seed)
-                dirty[0] = False
-            if role == "tier2":
+                if op == Scheduler.MAP:
+                    eng.kv_map(lane - off, n)
+                elif op == Scheduler.UNMAP:
+                    eng.kv_unmap(lane - off)
+                elif op == Scheduler.SWAP_OUT:
+                    bufs[buf] = eng.kv_swap_out(lane - off, n)
+                else:
+                    eng.kv_swap_in(lane - off, n, bufs.pop(buf))
+            if not (ins[:, 0] != Scheduler.SRC_IDLE).any():
+                while sch.unresolved:
+                    sch.resolve(hist.popleft())
+                continue
+            tok = np.where(ins[:, 0] == Scheduler.SRC_DEVICE, last, ins[:, 1]).astype(np.int32)
+            if eng.role == "tier2":
                 eng.step_host(None, None)
                 nxt = np.zeros(B, np.int32)
             else:
-                nxt, _ = eng.step_host(tok, pos)
-            steps += 1
-            for lane in range(B):
-                r = lane_req[lane]
-                if r < 0:
-                    if queue:
-                        admit(lane)   # retry: pages may have been returned by now
-                    continue
-                t = lane_t[lane]
-                plen = len(prompt[r])
-                if t + 1 < plen:          # still feeding the prompt
-                    tok[lane] = int(prompt[r][t + 1])
-                else:
-                    out[r].append(int(nxt[lane]))
-                    tok[lane] = nxt[lane]
-                lane_t[lane] = t + 1
-                pos[lane] = t + 1
-                if len(out[r]) == max_new:
-                    admit(lane)       # the lane's slot goes to the next request
-            if queue and all(r < 0 for r in lane_req):
-                for lane in range(B):  # every lane idle: offer the whole pool
-                    kv_unmap(lane)
-                for lane in range(B):
-                    admit(lane)
-        if queue:
-            raise L.FeasibilityError(L.GH_EINFEASIBLE, f"request {queue[0]} needs more KV pages than the pool holds")
-        return [np.array(o, np.int32) for o in out], steps
+                nxt, _ = eng.step_host(tok, ins[:, 2].copy())
+            last = np.asarray(nxt, np.int32)
+            sch.commit()
+            hist.append(last.copy())
+            if sch.unresolved > 1:
+                sch.resolve(hist.popleft())
+        while sch.unresolved:
+            sch.resolve(hist.popleft())
+        self.stats = sch.stats()
+        self.preemptions = self.stats["preemptions"]
+        out = [sch.result(i) for i in ids]
+        steps = self.stats["steps"]
+        sch.close()
+        return out, steps
 
 
 class MixedDispatcher:

@@ -229,7 +229,7 @@ def paged_requests():
     return [rng.integers(0, PSPEC.vocab_size, size=n, dtype=np.int32) for n in PLENS]
 
 
-def worker_paged(rank, world, port, q, on_demand=False, preempt="recompute"):
+def worker_paged(rank, world, port, q, on_demand=False, preempt="recompute", IF=1):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     import torch
     import torch.distributed as dist
@@ -239,7 +239,7 @@ def worker_paged(rank, world, port, q, on_demand=False, preempt="recompute"):
     obj = [Comm.unique_ids(1) if rank == 0 else None]
     dist.broadcast_object_list(obj, src=0)
     comm = Comm(obj[0], world, rank, rank)
-    eng = Engine(PSPEC, batch=PB, device=rank, use_graph=False, comm=comm, kv_pages=8)
+    eng = Engine(PSPEC, batch=PB, inflight=IF, device=rank, use_graph=False, comm=comm, kv_pages=8 * IF)
     try:
         out, steps = ContinuousDispatcher(eng, on_demand=on_demand, preempt=preempt).run(paged_requests(), PNEW)
     except Exception as e:  # every rank takes the same decisions: report instead of hanging
@@ -253,14 +253,16 @@ def worker_paged(rank, world, port, q, on_demand=False, preempt="recompute"):
 
 
 @pytest.mark.skipif(n_gpus() < 2, reason="needs >= 2 GPUs")
+@pytest.mark.parametrize("IF", [1, 2])
 @pytest.mark.parametrize("world", [2, 3])
 @pytest.mark.parametrize("on_demand,preempt", [(False, "recompute"), (True, "recompute"), (True, "swap")])
-def test_continuous_batching_paged_tier_split(world, on_demand, preempt):
-    """Continuous batching on paged Tier-2 ranks (SURVEY 8f-2 in the tier split): every rank
-    runs the dispatcher SPMD; each Tier-2 rank maps its own shard's lanes from a pool smaller
-    than its lanes x max_seq_len, so requests wait for pages (or, on demand, grow page by page and
-    preempt the latest request of the shard).  Tokens identical to the colocated engine with
-    contiguous slots."""
+def test_continuous_batching_paged_tier_split(world, on_demand, preempt, IF):
+    """Continuous batching on paged Tier-2 ranks (SURVEY 8f-2 in the tier split) through the
+    native batch-state dispatcher driving the pipelined step (IF in-flight batches, peer
+    transport): every rank runs the dispatcher SPMD; each Tier-2 rank maps its own shard's lanes
+    from a pool smaller than its lanes x max_seq_len, so requests wait for pages (or, on demand,
+    grow page by page and preempt the latest request of the shard).  Tokens identical to the
+    colocated engine with contiguous slots."""
     if n_gpus() < world:
         pytest.skip(f"needs {world} GPUs")
     import torch.multiprocessing as mp
@@ -271,7 +273,7 @@ def test_continuous_batching_paged_tier_split(world, on_demand, preempt):
     s.close()
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
-    procs = [ctx.Process(target=worker_paged, args=(r, world, port, q, on_demand, preempt)) for r in range(world)]
+    procs = [ctx.Process(target=worker_paged, args=(r, world, port, q, on_demand, preempt, IF)) for r in range(world)]
     for p in procs:
         p.start()
     got, steps = q.get(timeout=300)
@@ -284,7 +286,7 @@ def test_continuous_batching_paged_tier_split(world, on_demand, preempt):
     ref.close()
     for w, g in zip(want, got):
         assert np.array_equal(w, g)
-    if world == 2 and not on_demand:
+    if world == 2 and not on_demand and IF == 1:
         assert steps > ref_steps  # one Tier-2 pool of 8 pages for 6 lanes: requests waited
 
 
