@@ -1,13 +1,12 @@
 """NCCL tier split on real GPUs (needs >= 2 GPUs; skipped otherwise): rank 0 = Tier-1, ranks
 1.. = Tier-2 holding the KV of their prompt shard.  Tokens and logits must be identical to the
 colocated engine (same kernels, same batch -> same arithmetic)."""
-import os
-import socket
 
 import numpy as np
 import pytest
 
 import paper_2501_11779_b200 as gh
+from _ranks import collect, init_rank, spawn
 
 pytestmark = pytest.mark.gpu
 
@@ -47,12 +46,11 @@ def run_engine(eng, ib_count=1):
 
 
 def worker(rank, world, port, q):
-    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     import torch
     import torch.distributed as dist
     from paper_2501_11779_b200.stages import Comm, Engine
     torch.cuda.set_device(rank)
-    dist.init_process_group("gloo", rank=rank, world_size=world)
+    init_rank(rank, world, port)
     obj = [Comm.unique_ids(1) if rank == 0 else None]
     dist.broadcast_object_list(obj, src=0)
     comm = Comm(obj[0], world, rank, rank)
@@ -71,21 +69,9 @@ def worker(rank, world, port, q):
 def test_nccl_tier_split_matches_colocated(world):
     if n_gpus() < world:
         pytest.skip(f"needs {world} GPUs")
-    import torch.multiprocessing as mp
     from paper_2501_11779_b200.stages import Engine
-    s = socket.socket()
-    s.bind(("127.0.0.1", 0))
-    port = s.getsockname()[1]
-    s.close()
-    ctx = mp.get_context("spawn")
-    q = ctx.Queue()
-    procs = [ctx.Process(target=worker, args=(r, world, port, q)) for r in range(world)]
-    for p in procs:
-        p.start()
-    toks, lg = q.get(timeout=600)
-    for p in procs:
-        p.join(timeout=120)
-        assert p.exitcode == 0
+    procs, q = spawn(worker, world, ())
+    toks, lg = collect(procs, q, 1, 600)[0]
     ref = Engine(SPEC, batch=B, use_graph=False)
     rtoks, rlg = run_engine(ref)
     ref.close()
@@ -95,12 +81,11 @@ def test_nccl_tier_split_matches_colocated(world):
 
 def worker_all(rank, world, port, q, IF, transport="auto"):
     """step_all (pipelined, all in-flight batches) + advance for STEPS steps."""
-    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     import torch
     import torch.distributed as dist
     from paper_2501_11779_b200.stages import Comm, Engine
     torch.cuda.set_device(rank)
-    dist.init_process_group("gloo", rank=rank, world_size=world)
+    init_rank(rank, world, port)
     comm = None
     if world > 1:
         obj = [Comm.unique_ids(1) if rank == 0 else None]
@@ -140,22 +125,10 @@ def test_pipelined_step_all_matches_colocated(world, IF, transport):
     copy engines + stream-ordered flags): tokens identical to the colocated engine."""
     if n_gpus() < world:
         pytest.skip(f"needs {world} GPUs")
-    import torch.multiprocessing as mp
     from paper_2501_11779_b200.stages import Engine
-    s = socket.socket()
-    s.bind(("127.0.0.1", 0))
-    port = s.getsockname()[1]
-    s.close()
-    ctx = mp.get_context("spawn")
-    q = ctx.Queue()
-    procs = [ctx.Process(target=worker_all, args=(r, world, port, q, IF, transport)) for r in range(world)]
-    for p in procs:
-        p.start()
-    got, used = q.get(timeout=600)
+    procs, q = spawn(worker_all, world, (IF, transport))
+    got, used = collect(procs, q, 1, 600)[0]
     assert used == transport
-    for p in procs:
-        p.join(timeout=120)
-        assert p.exitcode == 0
     ref = run_all(Engine(SPEC, batch=B, inflight=IF, use_graph=False), IF)
     assert np.array_equal(got, ref)
 
@@ -163,12 +136,11 @@ def test_pipelined_step_all_matches_colocated(world, IF, transport):
 def worker_pp(rank, world, port, q, IF, n1):
     """Tier-1 pipeline stages (n1 spans, each with its own Tier-2 ranks): step_all_host for the
     first step, then advance + step_all; the last span reports the next tokens."""
-    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     import torch
     import torch.distributed as dist
     from paper_2501_11779_b200.stages import Comm, Engine
     torch.cuda.set_device(rank)
-    dist.init_process_group("gloo", rank=rank, world_size=world)
+    init_rank(rank, world, port)
     obj = [Comm.unique_ids(1) if rank == 0 else None]
     dist.broadcast_object_list(obj, src=0)
     comm = Comm(obj[0], world, rank, rank)
@@ -198,22 +170,10 @@ def worker_pp(rank, world, port, q, IF, n1):
 def test_tier1_pipeline_stages_match_colocated():
     """SURVEY 8(e) config-5 topology at small scale: 2 Tier-1 spans (layers split by
     layer_spans), each with a dedicated Tier-2 rank; tokens identical to the colocated engine."""
-    import torch.multiprocessing as mp
     from paper_2501_11779_b200.stages import Engine
     world, IF, n1 = 4, 2, 2
-    s = socket.socket()
-    s.bind(("127.0.0.1", 0))
-    port = s.getsockname()[1]
-    s.close()
-    ctx = mp.get_context("spawn")
-    q = ctx.Queue()
-    procs = [ctx.Process(target=worker_pp, args=(r, world, port, q, IF, n1)) for r in range(world)]
-    for p in procs:
-        p.start()
-    got = q.get(timeout=600)
-    for p in procs:
-        p.join(timeout=120)
-        assert p.exitcode == 0
+    procs, q = spawn(worker_pp, world, (IF, n1))
+    got = collect(procs, q, 1, 600)[0]
     ref = run_all(Engine(SPEC, batch=B, inflight=IF, use_graph=False), IF)
     assert np.array_equal(got, ref)
 
@@ -230,12 +190,11 @@ def paged_requests():
 
 
 def worker_paged(rank, world, port, q, on_demand=False, preempt="recompute", IF=1):
-    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     import torch
     import torch.distributed as dist
     from paper_2501_11779_b200.stages import Comm, ContinuousDispatcher, Engine
     torch.cuda.set_device(rank)
-    dist.init_process_group("gloo", rank=rank, world_size=world)
+    init_rank(rank, world, port)
     obj = [Comm.unique_ids(1) if rank == 0 else None]
     dist.broadcast_object_list(obj, src=0)
     comm = Comm(obj[0], world, rank, rank)
@@ -265,21 +224,9 @@ def test_continuous_batching_paged_tier_split(world, on_demand, preempt, IF):
     colocated engine with contiguous slots."""
     if n_gpus() < world:
         pytest.skip(f"needs {world} GPUs")
-    import torch.multiprocessing as mp
     from paper_2501_11779_b200.stages import ContinuousDispatcher, Engine
-    s = socket.socket()
-    s.bind(("127.0.0.1", 0))
-    port = s.getsockname()[1]
-    s.close()
-    ctx = mp.get_context("spawn")
-    q = ctx.Queue()
-    procs = [ctx.Process(target=worker_paged, args=(r, world, port, q, on_demand, preempt, IF)) for r in range(world)]
-    for p in procs:
-        p.start()
-    got, steps = q.get(timeout=300)
-    for p in procs:
-        p.join(timeout=120)
-        assert p.exitcode == 0
+    procs, q = spawn(worker_paged, world, (on_demand, preempt, IF))
+    got, steps = collect(procs, q, 1, 300)[0]
     assert steps >= 0, got
     ref = Engine(PSPEC, batch=PB, use_graph=False)
     want, ref_steps = ContinuousDispatcher(ref).run(paged_requests(), PNEW)
@@ -291,12 +238,11 @@ def test_continuous_batching_paged_tier_split(world, on_demand, preempt, IF):
 
 
 def worker_mixed(rank, world, port, q, kv_pages=0):
-    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     import torch
     import torch.distributed as dist
     from paper_2501_11779_b200.stages import Comm, Engine, MixedDispatcher
     torch.cuda.set_device(rank)
-    dist.init_process_group("gloo", rank=rank, world_size=world)
+    init_rank(rank, world, port)
     obj = [Comm.unique_ids(1) if rank == 0 else None]
     dist.broadcast_object_list(obj, src=0)
     comm = Comm(obj[0], world, rank, rank)
@@ -322,21 +268,9 @@ def test_mixed_prefill_tier_split(world, kv_pages):
     Tokens identical to the colocated engine at the same row count."""
     if n_gpus() < world:
         pytest.skip(f"needs {world} GPUs")
-    import torch.multiprocessing as mp
     from paper_2501_11779_b200.stages import ContinuousDispatcher, Engine
-    s = socket.socket()
-    s.bind(("127.0.0.1", 0))
-    port = s.getsockname()[1]
-    s.close()
-    ctx = mp.get_context("spawn")
-    q = ctx.Queue()
-    procs = [ctx.Process(target=worker_mixed, args=(r, world, port, q, kv_pages)) for r in range(world)]
-    for p in procs:
-        p.start()
-    got, steps = q.get(timeout=300)
-    for p in procs:
-        p.join(timeout=120)
-        assert p.exitcode == 0
+    procs, q = spawn(worker_mixed, world, (kv_pages,))
+    got, steps = collect(procs, q, 1, 300)[0]
     assert steps >= 0, got
     ref = Engine(PSPEC, batch=12, use_graph=False)
     want, ref_steps = ContinuousDispatcher(ref).run(paged_requests(), PNEW)

@@ -10,13 +10,12 @@ relative RMS <= 1e-2 per step (2-3 layers; the single-GPU engine shows ~5e-3 at 
 argmax equal wherever the oracle's top-2 margin exceeds twice the step's largest logit error.
 Every TP rank must decode bit-identical tokens (the all-reduce sums the partials in rank order on
 every rank, so the replicated activations never drift apart)."""
-import os
-import socket
 
 import numpy as np
 import pytest
 
 import paper_2501_11779_b200 as gh
+from _ranks import collect, init_rank, spawn
 
 pytestmark = pytest.mark.gpu
 
@@ -53,12 +52,11 @@ def oracle_run(spec, B):
 
 
 def worker(rank, world, port, q, name, tp, B, fed):
-    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     import torch
     import torch.distributed as dist
     from paper_2501_11779_b200.stages import Comm, Engine
     torch.cuda.set_device(rank)
-    dist.init_process_group("gloo", rank=rank, world_size=world)
+    init_rank(rank, world, port)
     obj = [Comm.unique_ids(1) if rank == 0 else None]
     dist.broadcast_object_list(obj, src=0)
     comm = Comm(obj[0], world, rank, rank)
@@ -84,20 +82,8 @@ def worker(rank, world, port, q, name, tp, B, fed):
 
 
 def run_split(name, world, tp, B, fed):
-    import torch.multiprocessing as mp
-    s = socket.socket()
-    s.bind(("127.0.0.1", 0))
-    port = s.getsockname()[1]
-    s.close()
-    ctx = mp.get_context("spawn")
-    q = ctx.Queue()
-    procs = [ctx.Process(target=worker, args=(r, world, port, q, name, tp, B, fed)) for r in range(world)]
-    for p in procs:
-        p.start()
-    got = dict((r, (t, lg)) for r, t, lg in (q.get(timeout=900) for _ in range(tp)))
-    for p in procs:
-        p.join(timeout=120)
-        assert p.exitcode == 0
+    procs, q = spawn(worker, world, (name, tp, B, fed))
+    got = dict((r, (t, lg)) for r, t, lg in collect(procs, q, tp, 900))
     return got
 
 

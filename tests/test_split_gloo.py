@@ -4,26 +4,18 @@ engine sends over NCCL (fwd [x|q|k|v] per shard, bwd [x|attn] per shard, plus th
 the start of a step), with the oracle as the stage implementation.  The result must equal the
 colocated oracle bit for bit (same arithmetic, same message bytes)."""
 import os
-import socket
 
 import numpy as np
 import pytest
 import torch
 import torch.distributed as dist
-import torch.multiprocessing as mp
 
 import paper_2501_11779_b200 as gh
+from _ranks import collect, init_rank, spawn
 
 SPEC = gh.ModelSpec("split-cpu", 2, 128, 64, 192, 4, 2, 32, 2, 97)
 B, STEPS, SEED = 7, 5, 1234
 
-
-def free_port():
-    s = socket.socket()
-    s.bind(("127.0.0.1", 0))
-    p = s.getsockname()[1]
-    s.close()
-    return p
 
 
 def reference_tokens(B=B, spec=SPEC):
@@ -35,8 +27,7 @@ def reference_tokens(B=B, spec=SPEC):
 
 
 def worker(rank, world, port, out_q, B=B):
-    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
-    dist.init_process_group("gloo", rank=rank, world_size=world)
+    init_rank(rank, world, port)
     from oracle import Oracle
     kp = world - 1
     off, cnt = gh.shard_plan(B, kp)
@@ -92,16 +83,8 @@ def worker(rank, world, port, out_q, B=B):
 def test_tier_split_protocol_matches_colocated(world, B):
     """world 8 = BASELINE C3's largest layout: one Tier-1 + K' = 7 Tier-2 ranks (shards 3,2,...,2)."""
     _, gen, lg = reference_tokens(B)
-    ctx = mp.get_context("spawn")
-    q = ctx.Queue()
-    port = free_port()
-    procs = [ctx.Process(target=worker, args=(r, world, port, q, B)) for r in range(world)]
-    for p in procs:
-        p.start()
-    sgen, slg = q.get(timeout=240)
-    for p in procs:
-        p.join(timeout=60)
-        assert p.exitcode == 0
+    procs, q = spawn(worker, world, (B,))
+    sgen, slg = collect(procs, q, 1, 240)[0]
     assert np.array_equal(sgen, gen)
     assert np.array_equal(slg, lg)
 
@@ -112,8 +95,7 @@ def worker_pp(rank, world, port, out_q, B=B):
     prompt shard j).  Span 0 embeds, hands [x] (PayloadModel intra-Tier-1 message,
     netmodel.cpp:22) plus the positions to span 1; span 1 classifies and hands the next tokens
     back to span 0.  The layout is the engine's (gh_engine_layout)."""
-    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
-    dist.init_process_group("gloo", rank=rank, world_size=world)
+    init_rank(rank, world, port)
     from oracle import Oracle
     n1 = 2
     kp = (world - n1) // n1
@@ -195,16 +177,8 @@ def worker_pp(rank, world, port, out_q, B=B):
 def test_tier1_pipeline_protocol_matches_colocated(world, B):
     """world 8 = BASELINE C5 as pipeline spans: T = 2 Tier-1 spans, K' = 3 Tier-2 ranks each."""
     _, gen, lg = reference_tokens(B)
-    ctx = mp.get_context("spawn")
-    q = ctx.Queue()
-    port = free_port()
-    procs = [ctx.Process(target=worker_pp, args=(r, world, port, q, B)) for r in range(world)]
-    for p in procs:
-        p.start()
-    sgen, slg = q.get(timeout=240)
-    for p in procs:
-        p.join(timeout=60)
-        assert p.exitcode == 0
+    procs, q = spawn(worker_pp, world, (B,))
+    sgen, slg = collect(procs, q, 1, 240)[0]
     assert np.array_equal(sgen, gen)
     assert np.array_equal(slg, lg)
 
@@ -255,8 +229,7 @@ def worker_tp(rank, world, port, out_q, B):
     Tier-2 rank assembles the PayloadModel row from the T blocks, attends, and returns block r of
     [x | attn] to rank r.  W_o and W_2 partials are all-reduced across the T ranks (gathered and
     summed in rank order, as the GEMM epilogue does), so every TP rank holds the same x."""
-    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
-    dist.init_process_group("gloo", rank=rank, world_size=world)
+    init_rank(rank, world, port)
     from oracle import Oracle
     spec, T = TP_SPEC, 2
     tp_group = dist.new_group(list(range(T)))
@@ -354,16 +327,8 @@ def test_tier1_tensor_parallel_protocol(world, B):
     logits within 1e-4 relative of the colocated oracle (only the summation order differs), tokens
     equal wherever the margin is clear, and both TP ranks decode identical tokens."""
     _, gen, lg = reference_tokens(B, TP_SPEC)
-    ctx = mp.get_context("spawn")
-    q = ctx.Queue()
-    port = free_port()
-    procs = [ctx.Process(target=worker_tp, args=(r, world, port, q, B)) for r in range(world)]
-    for p in procs:
-        p.start()
-    res = dict((r, (g, l)) for r, g, l in (q.get(timeout=240) for _ in range(2)))
-    for p in procs:
-        p.join(timeout=60)
-        assert p.exitcode == 0
+    procs, q = spawn(worker_tp, world, (B,))
+    res = dict((r, (g, l)) for r, g, l in collect(procs, q, 2, 240))
     sgen, slg = res[0]
     assert np.array_equal(res[1][0], sgen) and np.array_equal(res[1][1], slg)
     err = np.abs(slg - lg).max()
