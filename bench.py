@@ -38,10 +38,13 @@ GiB = 1 << 30
 
 
 def peaks():
+    """(HBM GB/s, bf16 TFLOP/s sustained, kind) -- the driver-measured copy bandwidth and the
+    sustained (back-to-back, under the power cap) dense bf16 rate: the Tier-1 GEMMs run inside a
+    long step, so the sustained figure is their ceiling."""
     p = ROOT / "MEASURED_PEAKS.json"
     if p.exists():
         d = json.loads(p.read_text())
-        return d["hbm_gbs"], d["bf16_tflops"], "measured"
+        return d["hbm_gbs"], d.get("bf16_tflops_sustained", d["bf16_tflops"]), "measured"
     return 6650.0, 1590.0, "fallback"
 
 
@@ -337,6 +340,28 @@ def paged_workload(cfg, spec, ctx, requested, kp, inflight, per_gpu, n1):
                 shard=shard, kp=kp, admitted_slots=per_gpu * kp, kv_pages=pages, ctxs=ctxs)
 
 
+def ncu_tensor_pipe(kernel_prefix):
+    """Time-weighted sm__pipe_tensor_cycles_active (% of peak) of a kernel family from the committed
+    ncu --set full capture (profiles/*_ncu_full_metrics.csv, newest round first), or None."""
+    import csv
+    for p in sorted((ROOT / "profiles").glob("r*_ncu_full_metrics.csv"), reverse=True):
+        num = den = 0.0
+        with open(p) as f:
+            for row in csv.DictReader(f):
+                if kernel_prefix not in row.get("Kernel Name", ""):
+                    continue
+                t = next((v for k, v in row.items() if k.startswith("gpu__time_duration.sum")), None)
+                pct = next((v for k, v in row.items() if k.startswith("sm__pipe_tensor_cycles_active")), None)
+                try:
+                    num += float(t) * float(pct)
+                    den += float(t)
+                except (TypeError, ValueError):
+                    continue
+        if den > 0:
+            return num / den
+    return None
+
+
 def ncu_traffic(kernel_prefix):
     """DRAM bytes per launch (read + write) of a kernel from the committed ncu --set full capture
     (profiles/*_ncu_full_metrics.csv, newest round first), or None."""
@@ -405,13 +430,24 @@ def run_colocated(args, wl):
     ms = e0.elapsed_time(e1) / args.steps
     value = B / (ms / 1e3)
 
-    # e2e through the public API: host tokens/pos in, next tokens out, every step
+    # e2e through the public API (gh_engine_step_host): every step copies the host tokens and
+    # positions in, replays the step and copies the next tokens out, synchronously -- the same K
+    # steps as the device-timed region, timed by the host clock around them
     nxt = tok
+    stream.synchronize()
     t0 = time.perf_counter()
-    for _ in range(max(2, args.steps // 2)):
+    for _ in range(args.steps):
         nxt, _ = eng.step_host(nxt, pos, stream=stream)
-    e2e_ms = (time.perf_counter() - t0) * 1e3 / max(2, args.steps // 2)
+    e2e_ms = (time.perf_counter() - t0) * 1e3 / args.steps
 
+    if os.environ.get("GH_PROFILE_GEMMS"):  # diagnostics: per-GEMM times of one eager step (serialised)
+        import ctypes
+        lib.gh_debug_gemm_profile(1)
+        eng.step_host(tok, pos, want_logits=True, stream=stream)
+        lib.gh_debug_gemm_profile(0)
+        buf = ctypes.create_string_buffer(1 << 16)
+        lib.gh_debug_gemm_profile_dump(buf, 1 << 16)
+        print(f"GEMM profile:\n{buf.value.decode()}", file=sys.stderr)
     # dominant kernel: attention of one layer, timed alone with CUDA events on its stream
     eng.close()
     del eng
@@ -540,6 +576,15 @@ def run_split(args, wl, rank, world):
         elif r is not None:
             toks = r
     e2e_ms = torch.tensor([(time.perf_counter() - t0) * 1e3 / nsteps], dtype=torch.float64)
+    if os.environ.get("GH_PROFILE_GEMMS"):  # diagnostics: per-GEMM times of one more step (serialised)
+        import ctypes
+        lib.gh_debug_gemm_profile(1)
+        eng.step_all(stream=stream)
+        stream.synchronize()
+        lib.gh_debug_gemm_profile(0)
+        buf = ctypes.create_string_buffer(1 << 16)
+        lib.gh_debug_gemm_profile_dump(buf, 1 << 16)
+        print(f"rank {rank} GEMM profile:\n{buf.value.decode()}", file=sys.stderr)
     print(f"rank {rank} ({eng.role}): device {ms_local:.3f} ms/step, e2e {float(e2e_ms.item()):.3f} ms/step",
           file=sys.stderr)
     dist.all_reduce(e2e_ms, op=dist.ReduceOp.MAX)
@@ -661,6 +706,15 @@ def main():
                                         "tcgen05 GEMMs)", "achieved": gach, "peak": hbm, "unit": "GB/s",
                                         "frac": gach / hbm, "duration_us": res["na_ms"] * 1e3,
                                         "algorithmic_bytes": gb}
+        # tensor roofline of the same Tier-1 GEMMs: FLOPs 2*B*D*(2D + 3D_h + 2D_kv) (model.cpp:54, MACs x 2)
+        fl = 2 * wl["batch"] * spec.d_model * (2 * spec.d_model + 3 * spec.d_hidden + 2 * spec.d_kv)
+        tach = fl / (res["na_ms"] / 1e3) / 1e12
+        out["roofline_tensor"] = {"bound": "tensor", "kernels": "Tier-1 F1+F3 GEMMs of one layer (tcgen05)",
+                                  "achieved": tach, "peak": tf, "unit": "TFLOP/s", "frac": tach / tf,
+                                  "peak_kind": "measured sustained", "flops": fl,
+                                  "tensor_pipe_active_pct": ncu_tensor_pipe("gemm_tc_kernel"),
+                                  "note": f"B = {wl['batch']}: {fl / gb:.0f} FLOP per weight byte, far below the "
+                                          "~220 FLOP/B ridge, so the HBM roofline (roofline_nonattention) binds"}
         step_bytes = spec.n_layers * (ab + gb) + spec.dtype_bytes * 2 * spec.vocab_size * spec.d_model // 2
         out["step_roofline"] = {"bytes_per_step": step_bytes, "ideal_ms": step_bytes / (hbm * 1e9) * 1e3,
                                 "frac": step_bytes / (hbm * 1e9) / (res["ms"] / 1e3)}

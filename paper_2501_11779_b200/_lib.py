@@ -188,6 +188,8 @@ PROTOTYPES = {
     "gh_tier1_classify_sample": (st, [vp, u32, vp, vp, vp, vp, vp, vp, vp]),
     "gh_kernel_launches": (u64, [C.c_int]),
     "gh_debug_gemm_bench": (st, [C.c_int] * 7 + [P(C.c_float)]),
+    "gh_debug_gemm_profile": (st, [C.c_int]),
+    "gh_debug_gemm_profile_dump": (st, [C.c_char_p, u64]),
     "gh_debug_gemm_trace": (st, [C.c_int] * 5 + [P(C.c_float), P(C.c_uint64), C.c_int]),
 }
 

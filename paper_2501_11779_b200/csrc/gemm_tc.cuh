@@ -417,54 +417,45 @@ GH_DEV void push_partial(uint32_t recv_saddr, int rank, int row, const float* v1
 
 // Tier-1 tensor parallelism: all-reduce of this thread's fully K-reduced fp32 values v (output
 // rows n .. n+En-1 of batch column b) across the ep.tp_n ranks, inside the epilogue.  The 128
-// epilogue threads of the slice (index fi) store their partials into every rank's receive buffer
-// (the peers' over NVLink), fence at system scope, and one thread releases the slice's flag in
-// every peer and then acquires the peers' flags for the same slice; every rank then sums the
-// tp_n partials in rank order, so the result (and everything computed from it) is bit-identical
-// on all ranks.  Every rank runs the same plan (plan_gemm_tp) and visits its tiles in the same
-// order, and every CTA of the persistent grid is resident, so the waits cannot deadlock.
-template <int En>
-GH_DEV void tp_allreduce(const EpiParams& ep, const GemmShape& gs, int n, int b, float (&v)[En], int fi) {
+// epilogue threads of the slice store its partial into every rank's receive buffer (the peers'
+// over NVLink), fence at system scope, and one thread releases the slice's flag in every peer
+// and then acquires the peers' flags for the same slice; every rank then sums the tp_n partials
+// in rank order, so the result (and everything computed from it) is bit-identical on all ranks.
+// Every rank runs the same plan (plan_gemm_tp) and visits its tiles in the same order, and every
+// CTA of the persistent grid is resident, so the waits cannot deadlock.
+// Receive buffer of rank p: [src rank][slice fi][row in slice][BN columns] fp32.  A slice is one
+// contiguous R x BN block and consecutive threads hold consecutive columns, so each store
+// instruction of a warp writes contiguous runs of the row (128 B when a thread owns a whole
+// column run), which is what NVLink carries efficiently; columns past the batch are not sent.
+template <int BN, int C, int En>
+GH_DEV void tp_allreduce(const EpiParams& ep, const GemmShape& gs, int rl, int b, float (&v)[En], int fi) {
+  constexpr int R = 128 / C;
   const bool ok = b < gs.Bt;
-  const long blk = (long)gs.Bt * gs.N;
-  const long at = (long)b * gs.N + n;
-  if (ok) {
+  const long blk = (long)gs.b_tiles * gs.n_tiles * 128 * BN;  // one source rank's partials
+  const long at = (long)fi * R * BN + (long)rl * BN + (b % BN);
+  if (ok && !(ep.tp_dbg & 2)) {
     for (int p = 0; p < ep.tp_n; ++p) {
       float* dst = ep.tp_dst[p] + ep.tp_rank * blk + at;
 #pragma unroll
-      for (int e = 0; e < En; e += 4)
-        if (n + e + 3 < gs.N) *(float4*)(dst + e) = make_float4(v[e], v[e + 1], v[e + 2], v[e + 3]);
-        else
-          for (int q = 0; q < 4 && n + e + q < gs.N; ++q) dst[e + q] = v[e + q];
+      for (int e = 0; e < En; ++e) dst[(long)e * BN] = v[e];
     }
   }
-  __threadfence_system();
+  if (!(ep.tp_dbg & 2)) __threadfence_system();
   epi_bar();
   if (threadIdx.x == 64) {
     for (int p = 0; p < ep.tp_n; ++p)
       if (p != ep.tp_rank) flag_store_release_sys(ep.tp_flag_dst[p] + (long)fi * kMaxTp + ep.tp_rank, ep.tp_seq);
-    for (int p = 0; p < ep.tp_n; ++p)
+    for (int p = 0; p < ep.tp_n && !(ep.tp_dbg & 1); ++p)
       if (p != ep.tp_rank) flag_wait_sys(ep.tp_flags + (long)fi * kMaxTp + p, ep.tp_seq);
   }
   epi_bar();
   if (ok) {
     const float* src = ep.tp_dst[ep.tp_rank] + at;  // the local receive buffer
 #pragma unroll
-    for (int e = 0; e < En; e += 4) {
-      if (n + e + 3 < gs.N) {
-        float4 a = __ldcg((const float4*)(src + e));
-        for (int p = 1; p < ep.tp_n; ++p) {  // rank order: identical sums on every rank
-          const float4 q = __ldcg((const float4*)(src + p * blk + e));
-          a.x += q.x; a.y += q.y; a.z += q.z; a.w += q.w;
-        }
-        v[e] = a.x; v[e + 1] = a.y; v[e + 2] = a.z; v[e + 3] = a.w;
-      } else {
-        for (int q = 0; q < 4 && n + e + q < gs.N; ++q) {
-          float a = __ldcg(src + e + q);
-          for (int p = 1; p < ep.tp_n; ++p) a += __ldcg(src + p * blk + e + q);
-          v[e + q] = a;
-        }
-      }
+    for (int e = 0; e < En; ++e) {
+      float a = __ldcg(src + (long)e * BN);
+      for (int p = 1; p < ep.tp_n; ++p) a += __ldcg(src + p * blk + (long)e * BN);  // rank order
+      v[e] = a;
     }
   }
 }
@@ -505,7 +496,7 @@ GH_DEV void reduce_and_store(const EpiParams& ep, const GemmShape& gs, const flo
   if (threadIdx.x == 64)
     for (int p = 0; p < C; ++p) mbar_arrive_cluster_relaxed(mapa_shared(consumed_saddr, p));
   if (ep.tp_n > 1)
-    tp_allreduce<En>(ep, gs, n0 + r * R + rl, b0 + b, v, (b0 / BN) * gs.n_tiles * C + tile_n * C + r);
+    tp_allreduce<BN, C, En>(ep, gs, rl, b0 + b, v, (b0 / BN) * gs.n_tiles * C + tile_n * C + r);
   if constexpr (En <= 32) epi_slice<BN, En>(ep, gs, n0 + r * R + rl, b0 + b, v, tile_n * C + r, inv, nullptr, &pre);
   else epi_slice<BN, En>(ep, gs, n0 + r * R + rl, b0 + b, v, tile_n * C + r, inv);
 }

@@ -491,7 +491,8 @@ static int max_clusters_bn(int BN, int C) {
   }
 }
 
-static int pair_override = 0;  // diagnostics: 1 = split-K only, 2 = pair whenever possible
+// diagnostics: 1 = split-K only, 2 = pair whenever possible (GH_GEMM_PAIR or gemm_debug_pair)
+static int pair_override = getenv("GH_GEMM_PAIR") ? atoi(getenv("GH_GEMM_PAIR")) : 0;
 static int wide_override = 0;  // diagnostics: 1 = never BN = 192, 2 = always when 128 < B <= 192
 
 static int pair_stages(int BN) { return std::max(2, PairSmem::max_stages(BN, 227 * 1024)); }

@@ -98,6 +98,19 @@ struct TmapCache {
 
 using namespace gh;
 
+// ================================================================== GEMM profiler (diagnostics)
+// gh_debug_gemm_profile(1): every Tier-1 GEMM launch of this process is bracketed by CUDA events
+// (which serialises it against its neighbours: no PDL overlap), and gh_debug_gemm_profile_dump
+// reports the mean time per (N, K, B, all-reduce) shape.  Off by default.
+namespace gh {
+struct GemmProfiler {
+  bool on = false;
+  struct Rec { int N, K, B; bool tp; cudaEvent_t a, b; };
+  std::vector<Rec> recs;
+  std::mutex mu;
+} g_prof;
+}  // namespace gh
+
 // ================================================================== Tier-1
 struct gh_tier1 {
   Shape sh;
@@ -109,7 +122,7 @@ struct gh_tier1 {
   // and classifier whole.  W_o and W_2 are all-reduced inside their GEMM epilogue (tp_allreduce).
   int tp = 1, tp_rank = 0;
   struct TpCtx {
-    float* buf[2] = {nullptr, nullptr};  // receive buffers [tp][max_batch][D] fp32 (reduce parity)
+    float* buf[2] = {nullptr, nullptr};  // receive buffers [tp][slice][row][BN] fp32 (reduce parity)
     unsigned int* flags = nullptr;       // [kTpFlagSlices][kMaxTp] sequence numbers written by peers
     float* peer_buf[2][kMaxTp] = {};     // rank p's receive buffers (p == tp_rank: local)
     unsigned int* peer_flags[kMaxTp] = {};
@@ -153,7 +166,19 @@ struct gh_tier1 {
     if (ep.tp_n > 1 && (p.pair || p.BN > 128)) return fail(GH_EINTERNAL, "tp all-reduce needs the split-K plan");
     CUtensorMap* tmX = nullptr;
     if (sh.db == 2) GH_TRY(tmaps.get(X, (uint64_t)B, (uint64_t)W.K, (uint64_t)ldx, (uint32_t)p.x_box_rows(), &tmX));
+    GemmProfiler::Rec rec{};
+    if (g_prof.on) {
+      rec = {W.N, W.K, B, ep.tp_n > 1, nullptr, nullptr};
+      GH_CUDA(cudaEventCreate(&rec.a));
+      GH_CUDA(cudaEventCreate(&rec.b));
+      GH_CUDA(cudaEventRecord(rec.a, st));
+    }
     GH_CUDA(launch_gemm(W, tmW, X, ldx, tmX, B, p, ep, gsc, st, next ? next->ptr : nullptr, prefetch_bytes(next)));
+    if (g_prof.on) {
+      GH_CUDA(cudaEventRecord(rec.b, st));
+      std::lock_guard<std::mutex> lk(g_prof.mu);
+      g_prof.recs.push_back(rec);
+    }
     return GH_OK;
   }
   static size_t prefetch_bytes(const Weight* w) {
@@ -185,6 +210,8 @@ static gh_status epi_tp(gh_tier1* t, int B, EpiParams& ep) {
     ep.tp_flag_dst[p] = c.peer_flags[p];
   }
   ep.tp_flags = c.flags;
+  static const int dbg = getenv("GH_TP_DBG") ? atoi(getenv("GH_TP_DBG")) : 0;  // diagnostics (wrong results)
+  ep.tp_dbg = dbg;
   return GH_OK;
 }
 
@@ -340,7 +367,7 @@ static gh_status tier1_create(const gh_model_spec* spec, int device, uint32_t la
     t->part = (float2*)p;
   }
   if (getenv("GH_GEMM_DBG")) t->gsc.debug_flags = atoi(getenv("GH_GEMM_DBG"));  // diagnostics (wrong results)
-  if (db == 2 && B > 128) {  // batches the planner may give to the CTA-pair kernel (stream-K)
+  if (db == 2) {  // the CTA-pair kernel's stream-K workspace (batches > 128, or GH_GEMM_PAIR=2)
     void* p;
     GH_TRY(dev_alloc(t->mem, kSkWsBytes, &p));
     t->gsc.sk_ws = (float*)p;
@@ -357,8 +384,8 @@ static gh_status tier1_create(const gh_model_spec* spec, int device, uint32_t la
   }
   if (tp > 1) {  // all-reduce receive buffers and flags (mapped by the peers in the engine's setup)
     void* p;
-    for (int par = 0; par < 2; ++par) {
-      GH_TRY(dev_alloc(t->mem, (size_t)tp * B * D * sizeof(float), &p));
+    for (int par = 0; par < 2; ++par) {  // [tp][slices][rows][BN]: batch and rows padded to tiles
+      GH_TRY(dev_alloc(t->mem, (size_t)tp * ((B + 127) / 128 * 128) * ((D + 127) / 128 * 128) * sizeof(float), &p));
       t->tpc.buf[par] = (float*)p;
     }
     GH_TRY(dev_alloc(t->mem, (size_t)gh_tier1::kTpFlagSlices * kMaxTp * sizeof(unsigned int), &p));
@@ -2344,6 +2371,41 @@ gh_status gh_dispatcher_stats(const gh_dispatcher* d, gh_dispatch_stats* out) {
 }
 
 }  // extern "C"
+
+extern "C" gh_status gh_debug_gemm_profile(int on) {
+  std::lock_guard<std::mutex> lk(g_prof.mu);
+  g_prof.on = on != 0;
+  return GH_OK;
+}
+
+extern "C" gh_status gh_debug_gemm_profile_dump(char* buf, uint64_t cap) {
+  if (!buf || cap == 0) return fail(GH_EINVAL, "null argument");
+  std::lock_guard<std::mutex> lk(g_prof.mu);
+  std::map<std::tuple<int, int, int, bool>, std::pair<int, double>> agg;
+  for (auto& r : g_prof.recs) {
+    float ms = 0.f;
+    if (cudaEventSynchronize(r.b) == cudaSuccess && cudaEventElapsedTime(&ms, r.a, r.b) == cudaSuccess) {
+      auto& a = agg[std::make_tuple(r.N, r.K, r.B, r.tp)];
+      a.first += 1;
+      a.second += ms * 1e3;
+    }
+    cudaEventDestroy(r.a);
+    cudaEventDestroy(r.b);
+  }
+  g_prof.recs.clear();
+  std::string out;
+  for (auto& kv : agg) {
+    const auto& k = kv.first;
+    const double us = kv.second.second / kv.second.first;
+    const double mb = (double)std::get<0>(k) * std::get<1>(k) * 2 / 1e6;
+    out += "N=" + std::to_string(std::get<0>(k)) + " K=" + std::to_string(std::get<1>(k)) + " B=" +
+           std::to_string(std::get<2>(k)) + (std::get<3>(k) ? " tp-allreduce" : "") + " n=" +
+           std::to_string(kv.second.first) + " mean_us=" + std::to_string(us) + " weight_MB=" + std::to_string(mb) +
+           " TB/s=" + std::to_string(mb / us) + "\n";
+  }
+  snprintf(buf, cap, "%s", out.c_str());
+  return GH_OK;
+}
 
 extern "C" gh_status gh_debug_gemm_bench(int N, int K, int B, int flags, int stages, int ks, int reps, float* us) {
   if (!us || N <= 0 || K <= 0 || B <= 0 || reps <= 0) return fail(GH_EINVAL, "bad argument");

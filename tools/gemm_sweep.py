@@ -17,6 +17,10 @@ def bench(N, K, B, flags=0, stages=0, cluster=0, reps=20):
 
 
 shapes = {"qkv": (12288, 4096), "o": (4096, 4096), "w13": (22016, 4096), "w2": (4096, 11008), "lm": (32000, 4096)}
+if "tp70b" in sys.argv:  # the 70B shapes of one of two tensor-parallel Tier-1 ranks
+    shapes = {"qkv": (5120, 8192), "o": (8192, 4096), "w13": (28672, 8192), "w2": (8192, 14336)}
+elif "70b" in sys.argv:
+    shapes = {"qkv": (10240, 8192), "o": (8192, 8192), "w13": (57344, 8192), "w2": (8192, 28672)}
 B = int(sys.argv[1]) if len(sys.argv) > 1 else 64
 for name, (N, K) in shapes.items():
     wb = N * K * 2
