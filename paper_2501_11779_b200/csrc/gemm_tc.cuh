@@ -416,47 +416,87 @@ GH_DEV void push_partial(uint32_t recv_saddr, int rank, int row, const float* v1
 }
 
 // Tier-1 tensor parallelism: all-reduce of this thread's fully K-reduced fp32 values v (output
-// rows n .. n+En-1 of batch column b) across the ep.tp_n ranks, inside the epilogue.  The 128
-// epilogue threads of the slice store its partial into every rank's receive buffer (the peers'
-// over NVLink), fence at system scope, and one thread releases the slice's flag in every peer
-// and then acquires the peers' flags for the same slice; every rank then sums the tp_n partials
-// in rank order, so the result (and everything computed from it) is bit-identical on all ranks.
-// Every rank runs the same plan (plan_gemm_tp) and visits its tiles in the same order, and every
-// CTA of the persistent grid is resident, so the waits cannot deadlock.
-// Receive buffer of rank p: [src rank][slice fi][row in slice][BN columns] fp32.  A slice is one
-// contiguous R x BN block and consecutive threads hold consecutive columns, so each store
-// instruction of a warp writes contiguous runs of the row (128 B when a thread owns a whole
-// column run), which is what NVLink carries efficiently; columns past the batch are not sent.
+// rows rl .. rl+En-1 of the slice, batch column b) across the ep.tp_n ranks, inside the epilogue,
+// with no fence and no separate flag: every value travels to each peer as one 8-byte word
+// {value, sequence number} (a single NVLink write, so the pair is seen whole or not at all), and a
+// peer's partial is known to have arrived when its words carry this all-reduce's sequence number
+// (the low-latency scheme of NCCL's LL protocol).  Every rank then sums the tp_n partials in rank
+// order, so the result (and everything computed from it) is bit-identical on all ranks.  All ranks
+// run the same plan (plan_gemm_tp) and visit their tiles in the same order, and every CTA of the
+// persistent grid is resident, so the waits cannot deadlock; receive buffers alternate between
+// two parities, so a word can only be overwritten after its reader has consumed it.
+// Receive buffer of rank p: [src rank][slice fi][row in slice][BN columns] of {value, seq}.  A slice
+// is one contiguous block and consecutive threads hold consecutive columns, so each store of a warp
+// writes a contiguous run (256 B when a thread owns a whole column run); columns past the batch are
+// not sent.
+GH_DEV void st_sys_u2(uint2* p, uint32_t a, uint32_t b, bool weak) {
+  if (weak) asm volatile("st.global.cg.v2.u32 [%0], {%1, %2};" ::"l"(p), "r"(a), "r"(b));
+  else asm volatile("st.relaxed.sys.global.v2.u32 [%0], {%1, %2};" ::"l"(p), "r"(a), "r"(b) : "memory");
+}
+GH_DEV uint2 ld_sys_u2(const uint2* p, bool weak) {
+  uint2 r;
+  if (weak) asm volatile("ld.global.cg.v2.u32 {%0, %1}, [%2];" : "=r"(r.x), "=r"(r.y) : "l"(p));
+  else asm volatile("ld.relaxed.sys.global.v2.u32 {%0, %1}, [%2];" : "=r"(r.x), "=r"(r.y) : "l"(p) : "memory");
+  return r;
+}
 template <int BN, int C, int En>
 GH_DEV void tp_allreduce(const EpiParams& ep, const GemmShape& gs, int rl, int b, float (&v)[En], int fi) {
   constexpr int R = 128 / C;
-  const bool ok = b < gs.Bt;
-  const long blk = (long)gs.b_tiles * gs.n_tiles * 128 * BN;  // one source rank's partials
+  if (b >= gs.Bt || (ep.tp_dbg & 4)) return;  // columns past the batch: nothing to exchange
+  const long blk = (long)gs.b_tiles * gs.n_tiles * 128 * BN;  // one source rank's words
   const long at = (long)fi * R * BN + (long)rl * BN + (b % BN);
-  if (ok && !(ep.tp_dbg & 2)) {
-    for (int p = 0; p < ep.tp_n; ++p) {
-      float* dst = ep.tp_dst[p] + ep.tp_rank * blk + at;
+  const uint32_t seq = ep.tp_seq;
+  // (rank loops are unrolled over kMaxTp so that tp_dst[] is indexed by constants)
+  if (!(ep.tp_dbg & 2)) {
 #pragma unroll
-      for (int e = 0; e < En; ++e) dst[(long)e * BN] = v[e];
+    for (int p = 0; p < kMaxTp; ++p) {
+      if (p >= ep.tp_n || p == ep.tp_rank) continue;
+      uint2* dst = (uint2*)ep.tp_dst[p] + ep.tp_rank * blk + at;
+#pragma unroll
+      for (int e = 0; e < En; ++e) st_sys_u2(dst + (long)e * BN, __float_as_uint(v[e]), seq, ep.tp_dbg & 16);
     }
   }
-  if (!(ep.tp_dbg & 2)) __threadfence_system();
-  epi_bar();
-  if (threadIdx.x == 64) {
-    for (int p = 0; p < ep.tp_n; ++p)
-      if (p != ep.tp_rank) flag_store_release_sys(ep.tp_flag_dst[p] + (long)fi * kMaxTp + ep.tp_rank, ep.tp_seq);
-    for (int p = 0; p < ep.tp_n && !(ep.tp_dbg & 1); ++p)
-      if (p != ep.tp_rank) flag_wait_sys(ep.tp_flags + (long)fi * kMaxTp + p, ep.tp_seq);
-  }
-  epi_bar();
-  if (ok) {
-    const float* src = ep.tp_dst[ep.tp_rank] + at;  // the local receive buffer
+  const uint2* src = (const uint2*)(ep.tp_rank == 0 ? ep.tp_dst[0] : ep.tp_rank == 1 ? ep.tp_dst[1]
+                                    : ep.tp_rank == 2 ? ep.tp_dst[2] : ep.tp_dst[3]) + at;  // local buffer
+  const bool wait = !(ep.tp_dbg & 1), weak = ep.tp_dbg & 8;
+  constexpr int kC = En < 4 ? En : (BN == 64 ? 4 : (En < 16 ? En : 16));  // words in flight per poll (register budget)
 #pragma unroll
-    for (int e = 0; e < En; ++e) {
-      float a = __ldcg(src + (long)e * BN);
-      for (int p = 1; p < ep.tp_n; ++p) a += __ldcg(src + p * blk + (long)e * BN);  // rank order
-      v[e] = a;
+  for (int c = 0; c < En; c += kC) {
+    float a[kC];
+#pragma unroll
+    for (int p = 0; p < kMaxTp; ++p) {  // rank order: identical sums on every rank
+      if (p >= ep.tp_n) break;
+      float x[kC];
+      if (p == ep.tp_rank) {
+#pragma unroll
+        for (int e = 0; e < kC; ++e) x[e] = v[c + e];
+      } else {
+        // the chunk's words requested at once (a poll per word would serialise the loads behind
+        // their branches), then only the stale ones polled again
+        const uint2* w_at = src + p * blk + (long)c * BN;
+        uint2 w[kC];
+#pragma unroll
+        for (int e = 0; e < kC; ++e) w[e] = ld_sys_u2(w_at + (long)e * BN, weak);
+        bool stale = false;
+#pragma unroll
+        for (int e = 0; e < kC; ++e) stale |= w[e].y != seq;
+        while (wait && stale) {
+          stale = false;
+#pragma unroll
+          for (int e = 0; e < kC; ++e)
+            if (w[e].y != seq) {
+              w[e] = ld_sys_u2(w_at + (long)e * BN, weak);
+              stale |= w[e].y != seq;
+            }
+        }
+#pragma unroll
+        for (int e = 0; e < kC; ++e) x[e] = __uint_as_float(w[e].x);
+      }
+#pragma unroll
+      for (int e = 0; e < kC; ++e) a[e] = p == 0 ? x[e] : a[e] + x[e];
     }
+#pragma unroll
+    for (int e = 0; e < kC; ++e) v[c + e] = a[e];
   }
 }
 
@@ -495,8 +535,14 @@ GH_DEV void reduce_and_store(const EpiParams& ep, const GemmShape& gs, const flo
   epi_bar();
   if (threadIdx.x == 64)
     for (int p = 0; p < C; ++p) mbar_arrive_cluster_relaxed(mapa_shared(consumed_saddr, p));
-  if (ep.tp_n > 1)
-    tp_allreduce<BN, C, En>(ep, gs, rl, b0 + b, v, (b0 / BN) * gs.n_tiles * C + tile_n * C + r);
+  if constexpr (En <= 32) {  // plan_gemm_tp keeps runs <= 32 rows (register budget)
+    if (ep.tp_n > 1) {
+      tp_allreduce<BN, C, En>(ep, gs, rl, b0 + b, v, (b0 / BN) * gs.n_tiles * C + tile_n * C + r);
+      if (tr) tr[13] = globaltimer();  // (diagnostics) all-reduce done
+    }
+  } else {
+    if (ep.tp_n > 1) __trap();
+  }
   if constexpr (En <= 32) epi_slice<BN, En>(ep, gs, n0 + r * R + rl, b0 + b, v, tile_n * C + r, inv, nullptr, &pre);
   else epi_slice<BN, En>(ep, gs, n0 + r * R + rl, b0 + b, v, tile_n * C + r, inv);
 }
@@ -753,7 +799,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
           if (threadIdx.x == 64)
             for (int p = 0; p < C; ++p) mbar_arrive_cluster_relaxed(mapa_shared(smem_u32(consumed), p));
         }
-        if (tr) trace[13] = globaltimer();
+        if (tr && ep.tp_n <= 1) trace[13] = globaltimer();
       }
     }
     if (my_tiles > 0) mbar_wait_cluster(consumed, (my_tiles - 1) & 1);  // peers done with my smem

@@ -445,7 +445,7 @@ cudaError_t make_tmap_kv(CUtensorMap* out, const void* base, uint64_t rows, uint
 
 static const int kBNs[] = {16, 32, 64, 128};  // batches > 128 use several batch tiles
 static int stages_override = getenv("GH_GEMM_STAGES") ? atoi(getenv("GH_GEMM_STAGES")) : 0;  // diagnostics
-static int cluster_override = 0;  // diagnostics
+static int cluster_override = getenv("GH_GEMM_CLUSTER") ? atoi(getenv("GH_GEMM_CLUSTER")) : 0;  // diagnostics
 
 template <int BN>
 static int tc_stages() {
@@ -579,7 +579,7 @@ static GemmPlan plan_pair(int N, int K, int Bt, double* cost_out) {
 // rounds(C) * (ceil(KB / C) + reduction overhead), rounds = ceil(tiles / co-resident clusters).
 // Batches above 128 columns also consider the pair kernel (always used above 256).
 // split-K plan for batch tile BN (cost in k-blocks on the critical path -> *kb_out)
-static GemmPlan plan_splitk(int N, int KB, int Bt, int BN, double* kb_out) {
+static GemmPlan plan_splitk(int N, int KB, int Bt, int BN, double* kb_out, int min_c = 1) {
   GemmPlan p;
   p.BN = BN;
   p.b_tiles = (Bt + p.BN - 1) / p.BN;
@@ -589,6 +589,7 @@ static GemmPlan plan_splitk(int N, int KB, int Bt, int BN, double* kb_out) {
   // C = 8 (clusters of 8 CTAs) is excluded: only ~16 such clusters fit (GPC packing) and it
   // measured 2-3x slower than C <= 4 for every decode shape (tools/gemm_sweep.py).
   for (int C : {1, 2, 4}) {
+    if (C < min_c) continue;
     if (C == 1 && p.BN > 64) continue;  // the reduction keeps BN/C <= 64 rows per thread
     if (C > 1 && (p.BN / C < 4 || C > KB)) continue;
     if (cluster_override && C != cluster_override) continue;
@@ -641,7 +642,8 @@ GemmPlan plan_gemm_tp(int N, int K, int Bt) {
   int bn = 128;
   for (int b : kBNs) if (b >= bt_cap) { bn = b; break; }
   double best = 0;
-  GemmPlan p = plan_splitk(N, KB, Bt, bn, &best);
+  // the all-reducing epilogue holds at most 32 rows per thread (BN / C <= 32)
+  GemmPlan p = plan_splitk(N, KB, Bt, bn, &best, std::max(1, bn / 32));
   static const bool verbose = getenv("GH_GEMM_VERBOSE") != nullptr;  // diagnostics
   if (verbose)
     fprintf(stderr, "[gh] gemm (tp all-reduce) N=%d K=%d B=%d: split-K BN=%d b_tiles=%d n_tiles=%d C=%d clusters=%d\n",

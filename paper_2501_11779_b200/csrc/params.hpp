@@ -42,17 +42,16 @@ struct EpiParams {
   int xcopy_rows;
   // Tier-1 tensor parallelism: all-reduce of the tp_n ranks' fp32 partial outputs
   // inside the epilogue (W_o and W_2, STORE_RESID).  The owner of each output slice stores its
-  // partial into every rank's receive buffer tp_dst[p] ([tp_n][slice][row][BN] fp32; p == tp_rank is the
-  // local one) over NVLink peer mappings, releases a per-slice flag tp_flag_dst[p][slice][tp_rank]
-  // = tp_seq, acquires the peers' flags in its own tp_flags, and sums the tp_n partials in rank
-  // order (identical on every rank), then adds the residual.  tp_n <= 1: no exchange.
+  // partial as {value, tp_seq} words into every peer's receive buffer tp_dst[p]
+  // ([tp_n][slice][row][BN] uint2; p == tp_rank is the local one, which the peers write), polls the
+  // peers' words of the same slice until they carry tp_seq, and sums the tp_n partials in rank
+  // order, then adds the residual.  tp_n <= 1: no exchange.
   int tp_n;
   int tp_rank;
   unsigned int tp_seq;
   float* tp_dst[4];
-  unsigned int* tp_flag_dst[4];
-  const unsigned int* tp_flags;
-  int tp_dbg;           // diagnostics (wrong results): 1 = no flag wait, 2 = no peer stores / fence
+  int tp_dbg;           // diagnostics (wrong results): 1 = no waiting for the peers, 2 = no peer stores,
+                        // 4 = no all-reduce at all
 };
 constexpr int kMaxTp = 4;
 

@@ -108,6 +108,10 @@ struct GemmProfiler {
   struct Rec { int N, K, B; bool tp; cudaEvent_t a, b; };
   std::vector<Rec> recs;
   std::mutex mu;
+  // GH_GEMM_TRACE=NxK: per-CTA timelines of the profiled GEMMs of that shape (gemm_tc.cuh trace
+  // stamps), summarised as medians over CTAs and launches
+  int trace_n = 0, trace_k = 0;
+  std::vector<std::vector<double>> phases;  // per launch: median per phase
 } g_prof;
 }  // namespace gh
 
@@ -122,14 +126,12 @@ struct gh_tier1 {
   // and classifier whole.  W_o and W_2 are all-reduced inside their GEMM epilogue (tp_allreduce).
   int tp = 1, tp_rank = 0;
   struct TpCtx {
-    float* buf[2] = {nullptr, nullptr};  // receive buffers [tp][slice][row][BN] fp32 (reduce parity)
-    unsigned int* flags = nullptr;       // [kTpFlagSlices][kMaxTp] sequence numbers written by peers
+    // receive buffers [tp][slice][row][BN] of {fp32 value, sequence number} (two parities)
+    float* buf[2] = {nullptr, nullptr};
     float* peer_buf[2][kMaxTp] = {};     // rank p's receive buffers (p == tp_rank: local)
-    unsigned int* peer_flags[kMaxTp] = {};
     unsigned int seq = 0;                // all-reduces issued (identical on every rank)
     bool ready = false;                  // peer mappings in place (engine peer setup)
   } tpc;
-  static constexpr int kTpFlagSlices = 1 << 14;
   std::vector<std::unique_ptr<DevMem>> mem;
   struct Layer {
     Weight qkv, o, w13, w2;
@@ -147,6 +149,7 @@ struct gh_tier1 {
   float* ss_h = nullptr;  // per-slice sums of squares of h (fused FFN RMSNorm)
   float2* part = nullptr;
   GemmScratch gsc;
+  unsigned long long* trace_buf = nullptr;  // GEMM profiler timelines (diagnostics)
   TmapCache tmaps;
   std::map<std::tuple<int, int, int, bool>, GemmPlan> plans;
 
@@ -167,15 +170,42 @@ struct gh_tier1 {
     CUtensorMap* tmX = nullptr;
     if (sh.db == 2) GH_TRY(tmaps.get(X, (uint64_t)B, (uint64_t)W.K, (uint64_t)ldx, (uint32_t)p.x_box_rows(), &tmX));
     GemmProfiler::Rec rec{};
+    GemmScratch sc = gsc;
+    const bool traced = g_prof.on && W.N == g_prof.trace_n && W.K == g_prof.trace_k && !p.pair;
     if (g_prof.on) {
       rec = {W.N, W.K, B, ep.tp_n > 1, nullptr, nullptr};
       GH_CUDA(cudaEventCreate(&rec.a));
       GH_CUDA(cudaEventCreate(&rec.b));
       GH_CUDA(cudaEventRecord(rec.a, st));
+      if (traced) {
+        if (!trace_buf) {
+          void* q;
+          GH_TRY(dev_alloc(mem, (size_t)kNumSMs * 16 * 8, &q));
+          trace_buf = (unsigned long long*)q;
+        }
+        GH_CUDA(cudaMemsetAsync(trace_buf, 0, (size_t)kNumSMs * 16 * 8, st));
+        sc.trace = trace_buf;
+      }
     }
-    GH_CUDA(launch_gemm(W, tmW, X, ldx, tmX, B, p, ep, gsc, st, next ? next->ptr : nullptr, prefetch_bytes(next)));
+    GH_CUDA(launch_gemm(W, tmW, X, ldx, tmX, B, p, ep, sc, st, next ? next->ptr : nullptr, prefetch_bytes(next)));
     if (g_prof.on) {
       GH_CUDA(cudaEventRecord(rec.b, st));
+      if (traced) {  // phases relative to the earliest CTA start: median over CTAs of the last tile
+        std::vector<unsigned long long> h((size_t)kNumSMs * 16);
+        GH_CUDA(cudaMemcpyAsync(h.data(), trace_buf, h.size() * 8, cudaMemcpyDeviceToHost, st));
+        GH_CUDA(cudaStreamSynchronize(st));
+        unsigned long long t0 = ~0ull;
+        for (int c = 0; c < kNumSMs; ++c) if (h[c * 16 + 6]) t0 = std::min(t0, h[c * 16]);
+        std::vector<double> med(16, 0.0);
+        for (int i = 0; i < 16; ++i) {
+          std::vector<double> v;
+          for (int c = 0; c < kNumSMs; ++c)
+            if (h[c * 16 + 6] && h[c * 16 + i]) v.push_back((double)(h[c * 16 + i] - t0) / 1e3);
+          if (!v.empty()) { std::nth_element(v.begin(), v.begin() + v.size() / 2, v.end()); med[i] = v[v.size() / 2]; }
+        }
+        std::lock_guard<std::mutex> lk(g_prof.mu);
+        g_prof.phases.push_back(med);
+      }
       std::lock_guard<std::mutex> lk(g_prof.mu);
       g_prof.recs.push_back(rec);
     }
@@ -207,9 +237,7 @@ static gh_status epi_tp(gh_tier1* t, int B, EpiParams& ep) {
   ep.tp_seq = seq;
   for (int p = 0; p < t->tp; ++p) {
     ep.tp_dst[p] = c.peer_buf[seq & 1][p];
-    ep.tp_flag_dst[p] = c.peer_flags[p];
   }
-  ep.tp_flags = c.flags;
   static const int dbg = getenv("GH_TP_DBG") ? atoi(getenv("GH_TP_DBG")) : 0;  // diagnostics (wrong results)
   ep.tp_dbg = dbg;
   return GH_OK;
@@ -382,15 +410,14 @@ static gh_status tier1_create(const gh_model_spec* spec, int device, uint32_t la
     t->gsc.stage = (float*)p;
     t->gsc.stage_floats = n;
   }
-  if (tp > 1) {  // all-reduce receive buffers and flags (mapped by the peers in the engine's setup)
+  if (tp > 1) {  // all-reduce receive buffers (mapped by the peers in the engine's setup)
     void* p;
-    for (int par = 0; par < 2; ++par) {  // [tp][slices][rows][BN]: batch and rows padded to tiles
-      GH_TRY(dev_alloc(t->mem, (size_t)tp * ((B + 127) / 128 * 128) * ((D + 127) / 128 * 128) * sizeof(float), &p));
+    for (int par = 0; par < 2; ++par) {  // [tp][slices][rows][BN] x 8 B: batch and rows padded to tiles
+      const size_t bytes = (size_t)tp * ((B + 127) / 128 * 128) * ((D + 127) / 128 * 128) * 8;
+      GH_TRY(dev_alloc(t->mem, bytes, &p));
+      GH_CUDA(cudaMemset(p, 0, bytes));  // sequence numbers start at 1
       t->tpc.buf[par] = (float*)p;
     }
-    GH_TRY(dev_alloc(t->mem, (size_t)gh_tier1::kTpFlagSlices * kMaxTp * sizeof(unsigned int), &p));
-    GH_CUDA(cudaMemset(p, 0, (size_t)gh_tier1::kTpFlagSlices * kMaxTp * sizeof(unsigned int)));
-    t->tpc.flags = (unsigned int*)p;
   }
   GH_CUDA(cudaDeviceSynchronize());
   *out = t.release();
@@ -1648,14 +1675,14 @@ static gh_status peer_setup(gh_engine* e) {
   auto& P = e->peer;
   const int IF = (int)e->batches.size(), kp = e->kp, world = e->comm->nranks, rank = e->comm->rank;
   const int n1 = e->n1, tp = e->tp;
-  const int nslot = 4 + 6 * IF;
+  const int nslot = 3 + 6 * IF;
   auto slot_fwd = [&](int ib) { return 1 + ib; };
   auto slot_pos = [&](int ib) { return 1 + IF + ib; };
   auto slot_bwd = [&](int ib) { return 1 + 2 * IF + ib; };
   auto slot_x0 = [&](int ib) { return 1 + 3 * IF + ib; };
   auto slot_ss0 = [&](int ib) { return 1 + 4 * IF + ib; };
   auto slot_next = [&](int ib) { return 1 + 5 * IF + ib; };
-  const int slot_tpf = 1 + 6 * IF, slot_tpb = 2 + 6 * IF;  // TP all-reduce flags, buffers (2 parities)
+  const int slot_tpb = 1 + 6 * IF;  // TP all-reduce receive buffers (2 parities)
   ncclComm_t comm = e->comm->comms[0];
   void* p;
   const size_t nflags = (size_t)IF * (kp + tp + 2);
@@ -1681,7 +1708,6 @@ static gh_status peer_setup(gh_engine* e) {
     }
   }
   if (e->role == 1 && tp > 1) {
-    get(slot_tpf, e->t1->tpc.flags);
     get(slot_tpb, e->t1->tpc.buf[0]);
     get(slot_tpb + 1, e->t1->tpc.buf[1]);
   }
@@ -1729,15 +1755,13 @@ static gh_status peer_setup(gh_engine* e) {
       P.fflags = (uint32_t*)open(0, 0);
       for (int ib = 0; ib < IF; ++ib) P.fnext.push_back(open(0, slot_next(ib)));
     }
-    if (tp > 1) {  // the other TP ranks' all-reduce receive buffers and flag words
+    if (tp > 1) {  // the other TP ranks' all-reduce receive buffers
       auto& c = e->t1->tpc;
       for (int q = 0; q < tp; ++q) {
         if (q == rank) {
-          c.peer_flags[q] = c.flags;
           c.peer_buf[0][q] = c.buf[0];
           c.peer_buf[1][q] = c.buf[1];
         } else {
-          c.peer_flags[q] = (unsigned int*)open(q, slot_tpf);
           c.peer_buf[0][q] = (float*)open(q, slot_tpb);
           c.peer_buf[1][q] = (float*)open(q, slot_tpb + 1);
         }
@@ -2375,6 +2399,7 @@ gh_status gh_dispatcher_stats(const gh_dispatcher* d, gh_dispatch_stats* out) {
 extern "C" gh_status gh_debug_gemm_profile(int on) {
   std::lock_guard<std::mutex> lk(g_prof.mu);
   g_prof.on = on != 0;
+  if (const char* t = getenv("GH_GEMM_TRACE")) sscanf(t, "%dx%d", &g_prof.trace_n, &g_prof.trace_k);
   return GH_OK;
 }
 
@@ -2402,6 +2427,20 @@ extern "C" gh_status gh_debug_gemm_profile_dump(char* buf, uint64_t cap) {
            std::to_string(std::get<2>(k)) + (std::get<3>(k) ? " tp-allreduce" : "") + " n=" +
            std::to_string(kv.second.first) + " mean_us=" + std::to_string(us) + " weight_MB=" + std::to_string(mb) +
            " TB/s=" + std::to_string(mb / us) + "\n";
+  }
+  if (!g_prof.phases.empty()) {  // mean over launches of the per-launch medians (us from the first CTA start)
+    static const char* names[16] = {"start", "w_prefetched", "griddep_wait", "first_stage", "last_mma", "epi_done",
+                                    "exit", "tfull", "drain", "consumed", "published", "ready", "epi_slice_done",
+                                    "allreduce_done", "last", "reduced"};
+    out += "trace " + std::to_string(g_prof.trace_n) + "x" + std::to_string(g_prof.trace_k) + " (" +
+           std::to_string(g_prof.phases.size()) + " launches):";
+    for (int i = 0; i < 16; ++i) {
+      double m = 0;
+      for (auto& ph : g_prof.phases) m += ph[i];
+      out += std::string(" ") + names[i] + "=" + std::to_string(m / g_prof.phases.size());
+    }
+    out += "\n";
+    g_prof.phases.clear();
   }
   snprintf(buf, cap, "%s", out.c_str());
   return GH_OK;
