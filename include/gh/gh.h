@@ -364,9 +364,10 @@ typedef struct gh_dispatch_stats {
 /* Not for engines with Tier-1 pipeline spans (tier1_ranks > 1) or prefill rows. */
 gh_status gh_dispatcher_create(gh_engine* e, const gh_dispatch_config* cfg, gh_dispatcher** out);
 gh_status gh_dispatcher_destroy(gh_dispatcher* d);
-/* Queue a request (GH_EINFEASIBLE when it can never fit a slot / a shard's page pool). */
+/* Queue a request generating max_new tokens (0 = the configured max_new); GH_EINFEASIBLE when it
+ * can never fit a slot / a shard's page pool. */
 gh_status gh_dispatcher_submit(gh_dispatcher* d, const int32_t* prompt, uint32_t len, float temperature,
-                               uint32_t seed, uint64_t* id);
+                               uint32_t seed, uint32_t max_new, uint64_t* id);
 /* One engine step over every in-flight batch; *busy = 0 once every request has finished. */
 gh_status gh_dispatcher_step(gh_dispatcher* d, int* busy);
 /* Steps until every submitted request has finished and its tokens are on the host. */
@@ -390,7 +391,7 @@ typedef struct gh_kv_action { int32_t op; uint32_t lane; uint32_t n; uint64_t bu
 gh_status gh_sched_create(const gh_sched_config* cfg, gh_sched** out);
 gh_status gh_sched_destroy(gh_sched* s);
 gh_status gh_sched_submit(gh_sched* s, const int32_t* prompt, uint32_t len, float temperature, uint32_t seed,
-                          uint64_t* id);
+                          uint32_t max_new, uint64_t* id);
 gh_status gh_sched_plan(gh_sched* s, gh_lane_input* inputs, gh_kv_action* actions, uint32_t cap, uint32_t* n_actions);
 gh_status gh_sched_commit(gh_sched* s);
 gh_status gh_sched_resolve(gh_sched* s, const int32_t* next_tokens);

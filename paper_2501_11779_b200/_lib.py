@@ -157,14 +157,14 @@ PROTOTYPES = {
     "gh_engine_layout": (st, [u32, u32, u32, u32, u64, u32, P(GhRankLayout)]),
     "gh_dispatcher_create": (st, [vp, P(GhDispatchConfig), P(vp)]),
     "gh_dispatcher_destroy": (st, [vp]),
-    "gh_dispatcher_submit": (st, [vp, vp, u32, C.c_float, u32, P(u64)]),
+    "gh_dispatcher_submit": (st, [vp, vp, u32, C.c_float, u32, u32, P(u64)]),
     "gh_dispatcher_step": (st, [vp, P(C.c_int)]),
     "gh_dispatcher_run": (st, [vp, P(u64)]),
     "gh_dispatcher_result": (st, [vp, u64, vp, u32, P(u32)]),
     "gh_dispatcher_stats": (st, [vp, P(GhDispatchStats)]),
     "gh_sched_create": (st, [P(GhSchedConfig), P(vp)]),
     "gh_sched_destroy": (st, [vp]),
-    "gh_sched_submit": (st, [vp, vp, u32, C.c_float, u32, P(u64)]),
+    "gh_sched_submit": (st, [vp, vp, u32, C.c_float, u32, u32, P(u64)]),
     "gh_sched_plan": (st, [vp, P(GhLaneInput), P(GhKvAction), u32, P(u32)]),
     "gh_sched_commit": (st, [vp]),
     "gh_sched_resolve": (st, [vp, vp]),

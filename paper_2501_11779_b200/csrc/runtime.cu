@@ -2272,9 +2272,9 @@ gh_status gh_sched_create(const gh_sched_config* c, gh_sched** out) {
 }
 gh_status gh_sched_destroy(gh_sched* g) { delete g; return GH_OK; }
 gh_status gh_sched_submit(gh_sched* g, const int32_t* prompt, uint32_t len, float temperature, uint32_t seed,
-                          uint64_t* id) {
+                          uint32_t max_new, uint64_t* id) {
   if (!g || !prompt || !id) return fail(GH_EINVAL, "null argument");
-  std::string err = g->s.submit(prompt, len, temperature, seed, id);
+  std::string err = g->s.submit(prompt, len, temperature, seed, id, max_new);
   return err.empty() ? GH_OK : fail(GH_EINFEASIBLE, err);
 }
 gh_status gh_sched_plan(gh_sched* g, gh_lane_input* in, gh_kv_action* acts, uint32_t cap, uint32_t* n_acts) {
@@ -2356,10 +2356,10 @@ gh_status gh_dispatcher_destroy(gh_dispatcher* d) {
   return GH_OK;
 }
 gh_status gh_dispatcher_submit(gh_dispatcher* d, const int32_t* prompt, uint32_t len, float temperature,
-                               uint32_t seed, uint64_t* id) {
+                               uint32_t seed, uint32_t max_new, uint64_t* id) {
   if (!d || !prompt || !id) return fail(GH_EINVAL, "null argument");
   if (temperature < 0.f) return fail(GH_EINVAL, "temperature must be >= 0");
-  std::string err = d->s.submit(prompt, len, temperature, seed, id);
+  std::string err = d->s.submit(prompt, len, temperature, seed, id, max_new);
   return err.empty() ? GH_OK : fail(GH_EINFEASIBLE, err);
 }
 gh_status gh_dispatcher_step(gh_dispatcher* d, int* busy) {

@@ -28,9 +28,11 @@ std::string Sched::init(const SchedConfig& c) {
   return "";
 }
 
-std::string Sched::submit(const int32_t* prompt, uint32_t len, float temperature, uint32_t seed, uint64_t* id_out) {
+std::string Sched::submit(const int32_t* prompt, uint32_t len, float temperature, uint32_t seed, uint64_t* id_out,
+                          uint32_t max_new) {
   if (len == 0) return "empty prompt";
-  const uint32_t positions = len + c_.max_new - 1;  // every position the request ever attends
+  if (max_new == 0) max_new = c_.max_new;
+  const uint32_t positions = len + max_new - 1;  // every position the request ever attends
   if (c_.max_seq && positions > c_.max_seq)
     return "request needs " + std::to_string(positions) + " positions, max_seq_len is " + std::to_string(c_.max_seq);
   if (paged()) {  // it must fit its shard's pool beside one dummy page per other lane
@@ -44,6 +46,7 @@ std::string Sched::submit(const int32_t* prompt, uint32_t len, float temperature
   Req r;
   r.prompt.assign(prompt, prompt + len);
   r.orig_len = len;
+  r.max_new = max_new;
   r.temp = temperature;
   r.seed = seed;
   reqs_.push_back(std::move(r));
@@ -107,7 +110,7 @@ bool Sched::admissible(const Req& r, uint32_t lane) const {
 uint32_t Sched::admit_need(const Req& r) const {
   if (r.swapped) return r.swap_t + 1;  // the saved context plus the position it decodes next
   if (c_.on_demand) return r.orig_len + r.n_out;  // the prompt (+ the outputs it re-reads)
-  return r.orig_len + c_.max_new - 1;
+  return r.orig_len + r.max_new - 1;
 }
 
 void Sched::admit(uint32_t lane, std::vector<KvAction>& acts) {
@@ -240,7 +243,7 @@ void Sched::commit() {
       L.fed_back = false;
     }
     ++L.t;
-    if (r.n_out == c_.max_new) {  // done: the lane (and its slot) goes to the next request
+    if (r.n_out == r.max_new) {  // done: the lane (and its slot) goes to the next request
       r.done = true;
       ++finished;
       if (r.temp != 0.f) sampling_dirty_ = true;

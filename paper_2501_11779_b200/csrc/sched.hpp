@@ -35,7 +35,7 @@ struct SchedConfig {
   uint32_t kp = 0;           // Tier-2 shards per batch (0: colocated, one pool)
   uint32_t pages = 0;        // KV pages per shard pool (0: contiguous slots of max_seq_len)
   uint32_t max_seq = 0;      // positions per slot (max_seq_len)
-  uint32_t max_new = 1;      // tokens generated per request
+  uint32_t max_new = 1;      // tokens generated per request (default; submit may override)
   bool on_demand = false;    // paged: map the prompt only, grow a page at a time
   bool swap = false;         // preemption by swap (else recompute)
   bool shortest = false;     // admission order: shortest prompt first (else FIFO)
@@ -61,7 +61,8 @@ class Sched {
   // returns "" or the validation error
   std::string init(const SchedConfig& c);
   // "" or the reason the request can never be served (longer than a slot / a page pool)
-  std::string submit(const int32_t* prompt, uint32_t len, float temperature, uint32_t seed, uint64_t* id);
+  std::string submit(const int32_t* prompt, uint32_t len, float temperature, uint32_t seed, uint64_t* id,
+                     uint32_t max_new = 0);  // max_new 0: the configured one
   // the next step: inputs of every lane (IF * B) and the KV actions to apply first.  Returns an
   // error string (infeasible request) or "".
   std::string plan(std::vector<LaneInput>& in, std::vector<KvAction>& acts);
@@ -81,6 +82,7 @@ class Sched {
   struct Req {
     std::vector<int32_t> prompt;       // grows by the generated tokens on recompute preemption
     uint32_t orig_len = 0;             // the submitted prompt's length (output k sits at orig_len + k)
+    uint32_t max_new = 0;              // tokens to generate
     bool recompute = false;            // preempted by recompute: re-read prompt + outputs on admission
     std::vector<int32_t> out;          // generated tokens (values resolved a step late)
     uint32_t n_out = 0;                // generated so far (resolved or not)

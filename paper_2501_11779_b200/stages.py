@@ -362,10 +362,10 @@ class Scheduler:
 
     __del__ = close
 
-    def submit(self, prompt, temperature: float = 0.0, seed: int = 0) -> int:
+    def submit(self, prompt, temperature: float = 0.0, seed: int = 0, max_new: int = 0) -> int:
         p = np.ascontiguousarray(prompt, dtype=np.int32)
         i = C.c_uint64()
-        L.check(L.lib().gh_sched_submit(self.h, p.ctypes.data, len(p), temperature, seed, C.byref(i)))
+        L.check(L.lib().gh_sched_submit(self.h, p.ctypes.data, len(p), temperature, seed, max_new, C.byref(i)))
         return i.value
 
     def plan(self):
@@ -443,14 +443,17 @@ class ContinuousDispatcher:
         self.preemptions = 0
         self.stats = {}
 
-    def run(self, requests, max_new: int, sampling=None):
-        """requests: sequence of 1-D int32 prompts (any lengths >= 1); sampling: optional
-        per-request (temperature, seed) pairs (temperature 0 = greedy).  Returns (generated token
-        arrays, max_new each, in request order -- zeros on Tier-2 ranks -- and the step count)."""
+    def run(self, requests, max_new, sampling=None):
+        """requests: sequence of 1-D int32 prompts (any lengths >= 1); max_new: tokens to generate,
+        one int for all requests or one per request; sampling: optional per-request (temperature,
+        seed) pairs (temperature 0 = greedy).  Returns (generated token arrays in request order --
+        zeros on Tier-2 ranks -- and the step count)."""
+        per = np.broadcast_to(np.asarray(max_new, dtype=np.int64), (len(requests),))
+        max_new = int(per.max()) if len(requests) else 1
         eng = self.engine
         on_demand = self.on_demand and eng.kv_pages > 0
         if not isinstance(eng, Engine):
-            return self._run_host(requests, max_new, sampling, on_demand)
+            return self._run_host(requests, max_new, sampling, on_demand, per)
         cfg = L.GhDispatchConfig(max_new, int(on_demand), int(self.preempt == "swap"), int(self.order == "shortest"))
         h = C.c_void_p()
         L.check(L.lib().gh_dispatcher_create(eng.h, C.byref(cfg), C.byref(h)))
@@ -460,7 +463,8 @@ class ContinuousDispatcher:
                 t, sd = sampling[i] if sampling is not None else (0.0, 0)
                 p = np.ascontiguousarray(q, dtype=np.int32)
                 rid = C.c_uint64()
-                L.check(L.lib().gh_dispatcher_submit(h, p.ctypes.data, len(p), float(t), int(sd), C.byref(rid)))
+                L.check(L.lib().gh_dispatcher_submit(h, p.ctypes.data, len(p), float(t), int(sd), int(per[i]),
+                                                     C.byref(rid)))
                 ids.append(rid.value)
             steps = C.c_uint64()
             L.check(L.lib().gh_dispatcher_run(h, C.byref(steps)))
@@ -473,7 +477,7 @@ class ContinuousDispatcher:
         self.preemptions = self.stats["preemptions"]
         return out, int(steps.value)
 
-    def _run_host(self, requests, max_new, sampling, on_demand):
+    def _run_host(self, requests, max_new, sampling, on_demand, per):
         """The native decision logic driving a duck-typed engine from Python, one step of lag."""
         from collections import deque
         eng = self.engine
@@ -481,7 +485,8 @@ class ContinuousDispatcher:
         _, off, cnt, kp = eng.shard()
         sch = Scheduler(B, max_new, 1, kp, eng.kv_pages, getattr(getattr(eng, "spec", None), "max_seq_len", 0),
                         on_demand, self.preempt, self.order)
-        ids = [sch.submit(q, *(sampling[i] if sampling is not None else (0.0, 0))) for i, q in enumerate(requests)]
+        ids = [sch.submit(q, *(sampling[i] if sampling is not None else (0.0, 0)), max_new=int(per[i]))
+               for i, q in enumerate(requests)]
         holds = lambda lane: eng.role != "tier1" and off <= lane < off + cnt  # noqa: E731
         bufs, hist = {}, deque()
         last = np.zeros(B, np.int32)

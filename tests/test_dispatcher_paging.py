@@ -269,3 +269,14 @@ def test_scheduler_inflight_shards_lagged_tokens(on_demand, preempt, lag):
     assert st["finished"] == len(reqs) and st["tokens"] >= len(reqs) * max_new
     if on_demand:
         assert st["preemptions"] > 0 and (st["swaps"] > 0) == (preempt == "swap")
+
+
+@pytest.mark.parametrize("on_demand", [False, True])
+def test_per_request_max_new(on_demand):
+    """max_new per request: each request generates its own count and equals decoding it alone."""
+    reqs = _requests(9, seed=21)
+    per = [int(n) for n in np.random.default_rng(3).integers(1, 80, len(reqs))]
+    eng = FakeEngine(3, kv_pages=9)
+    got, _ = ContinuousDispatcher(eng, on_demand=on_demand).run(reqs, per)
+    for r, n, g in zip(reqs, per, got):
+        assert g.tolist() == _alone(r.tolist(), n)
