@@ -360,6 +360,8 @@ typedef struct gh_dispatch_config {
 typedef struct gh_dispatch_stats {
   uint64_t steps, admitted, finished, tokens, preemptions, swaps;
   uint32_t peak_pages;   /* most pages of one shard's pool in use at once */
+  uint64_t lane_steps;   /* busy lanes summed over steps: tokens processed (prompt, generated, recomputed) */
+  uint64_t context_sum;  /* positions attended summed over busy lane-steps (mean context = / lane_steps) */
 } gh_dispatch_stats;
 /* Not for engines with Tier-1 pipeline spans (tier1_ranks > 1) or prefill rows. */
 gh_status gh_dispatcher_create(gh_engine* e, const gh_dispatch_config* cfg, gh_dispatcher** out);

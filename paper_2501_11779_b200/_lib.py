@@ -81,7 +81,7 @@ class GhDispatchConfig(C.Structure):
 
 class GhDispatchStats(C.Structure):
     _fields_ = [(n, C.c_uint64) for n in ("steps", "admitted", "finished", "tokens", "preemptions", "swaps")]
-    _fields_ += [("peak_pages", C.c_uint32)]
+    _fields_ += [("peak_pages", C.c_uint32), ("lane_steps", C.c_uint64), ("context_sum", C.c_uint64)]
 
 
 class GhSchedConfig(C.Structure):

@@ -2312,6 +2312,7 @@ static gh_status sched_result(const Sched& s, uint64_t id, int32_t* tokens, uint
 static void sched_stats(const Sched& s, gh_dispatch_stats* o) {
   o->steps = s.steps; o->admitted = s.admitted; o->finished = s.finished; o->tokens = s.tokens;
   o->preemptions = s.preemptions; o->swaps = s.swaps; o->peak_pages = s.peak_pages;
+  o->lane_steps = s.lane_steps; o->context_sum = s.context_sum;
 }
 gh_status gh_sched_result(const gh_sched* g, uint64_t id, int32_t* tokens, uint32_t cap, uint32_t* n) {
   if (!g || !n) return fail(GH_EINVAL, "null argument");

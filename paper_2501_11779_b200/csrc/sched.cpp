@@ -233,6 +233,8 @@ void Sched::commit() {
     if (L.req < 0) continue;
     Req& r = reqs_[L.req];
     const uint32_t plen = (uint32_t)r.prompt.size();
+    ++lane_steps;
+    context_sum += L.t + 1;
     if (L.t + 1 >= plen) {  // this step's output is the request's next token
       cur_.push_back({(uint64_t)L.req, r.n_out, l});
       ++r.n_out;

@@ -74,6 +74,8 @@ class Sched {
   bool sampling(std::vector<float>& inv_temp, std::vector<uint32_t>& seed);
   const std::vector<int32_t>* result(uint64_t id) const;
   uint64_t steps = 0, preemptions = 0, swaps = 0, admitted = 0, finished = 0, tokens = 0;
+  uint64_t lane_steps = 0;             // busy lanes summed over steps (tokens processed, prompt or generated)
+  uint64_t context_sum = 0;            // positions attended, summed over busy lane-steps
   uint32_t lane_shard(uint32_t lane) const { return shard_of_[lane % c_.batch]; }
   uint32_t lanes() const { return c_.batch * c_.inflight; }
   uint32_t peak_pages = 0;             // the largest number of pages of one pool in use (tests)
