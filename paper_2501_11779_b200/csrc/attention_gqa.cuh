@@ -411,6 +411,10 @@ struct GqaTcCfg {
   static constexpr int kHdrBytes = (2 * G + 2) * DH * 2 + 16;
   static constexpr int kStageBytes = kKV + ((kHdrBytes + 1023) / 1024) * 1024;  // boxes stay 1 KB aligned
   static constexpr int kNB = 2;
+  // G >= 4: the consumer warps merge the unit themselves, warp h combining query head h, after a
+  // named barrier -- one merge warp combining G heads serially was the bottleneck at short
+  // contexts (70B, ctx 512: 4.1 TB/s); G < 4 keeps the dedicated merge warp
+  static constexpr bool kSplitMerge = G >= 4;
   static constexpr int kCombPerUnit = (kW + 1) * G * (DH + 2);  // + the new token's state
   static constexpr int kCombBytes = kNB * kCombPerUnit * 4;
   static constexpr int kStages = ((227 * 1024 - 2048 - kCombBytes - 1024) / kStageBytes) > 6
@@ -497,9 +501,6 @@ __global__ void __launch_bounds__(GqaTcCfg<G>::kThreads, 1)
       if (!a.kv_early && u < n_units) { L = a.pos[u / a.Hkv]; sl = (int)a.slot[u / a.Hkv]; }
       while (u < n_units) {
         const int b = u / a.Hkv, g = u % a.Hkv;
-        const int un = next_unit(a, u);
-        int Ln = 0, sln = 0;
-        if (un < n_units) { Ln = a.pos[un / a.Hkv]; sln = (int)a.slot[un / a.Hkv]; }
         // tensor-map rows (layer, slot or page, K/V, kv head); paged: one page per stage
         const int* pt = a.page_table ? a.page_table + (long)sl * a.max_pages : nullptr;
         const int nch = L > 0 ? (L + C::kTpos - 1) / C::kTpos : 1;
@@ -535,9 +536,14 @@ __global__ void __launch_bounds__(GqaTcCfg<G>::kThreads, 1)
             bulk_g2s(hdr + gq + 2 * DH * 2, row + gl * G * DH, gq, &full[s], pol);        // x slices
           }
         }
+        // the next unit is fetched only now, once this unit's stages are all requested: the
+        // work-counter atomic and the dependent position / slot loads (~2 round trips) then
+        // overlap the consumers draining the ring instead of delaying this unit's first loads
+        const int un = next_unit(a, u);
         u = un;
-        L = Ln;
-        sl = sln;
+        L = 0;
+        sl = 0;
+        if (un < n_units) { L = a.pos[un / a.Hkv]; sl = (int)a.slot[un / a.Hkv]; }
       }
       units_done(a);
       {  // end of this CTA's units: a header-only stage with L = -1
@@ -554,6 +560,7 @@ __global__ void __launch_bounds__(GqaTcCfg<G>::kThreads, 1)
   if (warp == C::kW + 1) {
     // -------------------------------------------------- merge warp (unit order): combines the kW
     // consumer states and the new token's state of every query head, writes the G output rows
+    if constexpr (C::kSplitMerge) return;  // the consumers merge (see GqaTcCfg::kSplitMerge)
     for (int ui = 0;; ++ui) {
       const int cb = ui % C::kNB;
       while (*(volatile int*)&comb_cnt[cb] < C::kW)
@@ -609,6 +616,7 @@ __global__ void __launch_bounds__(GqaTcCfg<G>::kThreads, 1)
     const int* meta = (const int*)(hdr + hdr_bytes);
     const int L = meta[0];
     if (L < 0) {  // end of units: pass the end marker to the merge warp through the next buffer
+      if constexpr (C::kSplitMerge) return;
       const int cb = ui % C::kNB;
       while (comb_seq[cb] != ui / C::kNB) { }
       if (cw == 0 && lane == 0) comb_bg[2 * cb] = -1;
@@ -636,6 +644,21 @@ __global__ void __launch_bounds__(GqaTcCfg<G>::kThreads, 1)
 
     const int cb = ui % C::kNB;
     float* cbuf = comb + cb * C::kCombPerUnit;
+    // split merge: warp cw < G keeps the new token's score for query head cw and its value
+    // (d = lane + 32 i) in registers -- the header's stage is released before the merge
+    float nsc = 0.f, nv[DH / 32];
+    if constexpr (C::kSplitMerge) {
+      if (cw < G) {
+        float part = 0.f;
+#pragma unroll
+        for (int i = 0; i < DH / 32; ++i) {
+          const int d = lane + 32 * i;
+          part = fmaf(bf16_to_f32(hq[cw * DH + d].bits), bf16_to_f32(hk[d].bits), part);
+          nv[i] = bf16_to_f32(hv[d].bits);
+        }
+        nsc = warp_sum(part) * a.scale_log2;
+      }
+    }
     if (cw == 0) {
       // new token: its key / value from the header; append them to the arena; its state is merged
       // as a ninth partial (m = score, l = 1, o = v) by the last warp
@@ -645,6 +668,8 @@ __global__ void __launch_bounds__(GqaTcCfg<G>::kThreads, 1)
         *((uint4*)kdst + lane) = ((const uint4*)hk)[lane];
         *((uint4*)vdst + lane) = ((const uint4*)hv)[lane];
       }
+    }
+    if (cw == 0 && !C::kSplitMerge) {
       while (comb_seq[cb] != ui / C::kNB) { }
       for (int h = 0; h < G; ++h) {
         float part = 0.f;
@@ -719,12 +744,46 @@ __global__ void __launch_bounds__(GqaTcCfg<G>::kThreads, 1)
     // publish this warp's state [warp][head][DH + 2]; the last warp merges 8 + 1 states per head
     l += __shfl_xor_sync(0xffffffffu, l, 1);
     l += __shfl_xor_sync(0xffffffffu, l, 2);
-    if (cw != 0) while (comb_seq[cb] != ui / C::kNB) { }
+    if (cw != 0 && !C::kSplitMerge) while (comb_seq[cb] != ui / C::kNB) { }
     if (qr < G) {
       float* wb = cbuf + (cw * G + qr) * (DH + 2);
 #pragma unroll
       for (int j = 0; j < 16; ++j) { wb[j * 8 + qc] = o[j][0] + o[j][2]; wb[j * 8 + qc + 1] = o[j][1] + o[j][3]; }
       if ((lane & 3) == 0) { wb[DH] = m; wb[DH + 1] = l; }
+    }
+    if constexpr (C::kSplitMerge) {
+      // every consumer warp's state of this unit is in the buffer; warp h merges query head h.
+      // Buffer ui % 2 is written again only at unit ui + 2, after the barrier of unit ui + 1,
+      // which every warp passes only once it has merged unit ui.
+      asm volatile("bar.sync 3, %0;" ::"n"(C::kW * 32) : "memory");
+      if (cw < G) {
+        const float* hb = cbuf + cw * (DH + 2);  // warp w's state of head cw at hb + w * G * (DH + 2)
+        float M = nsc;
+#pragma unroll
+        for (int w = 0; w < C::kW; ++w) M = fmaxf(M, hb[w * G * (DH + 2) + DH]);
+        float f[C::kW];
+        float den = 0.f;
+#pragma unroll
+        for (int w = 0; w < C::kW; ++w) {
+          const float mw = hb[w * G * (DH + 2) + DH];
+          f[w] = (mw == -INFINITY) ? 0.f : exp2f(mw - M);
+          den += hb[w * G * (DH + 2) + DH + 1] * f[w];
+        }
+        const float fn = exp2f(nsc - M);  // the new token (l = 1) as the last partial
+        den += fn;
+        const float inv = 1.f / den;
+        bf16_t* orow = brow(b, g) + Dt + (long)((g % gpb) * G + cw) * DH;
+#pragma unroll
+        for (int i = 0; i < DH / 32; ++i) {
+          const int d = lane + 32 * i;
+          float acc = 0.f;
+#pragma unroll
+          for (int w = 0; w < C::kW; ++w) acc += hb[w * G * (DH + 2) + d] * f[w];
+          acc += nv[i] * fn;
+          St<bf16_t>::store(orow, d, acc * inv);
+        }
+      }
+      continue;
     }
     if (cw == 0 && lane == 0) { comb_bg[2 * cb] = b; comb_bg[2 * cb + 1] = g; }
     __syncwarp();
