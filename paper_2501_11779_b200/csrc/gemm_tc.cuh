@@ -774,9 +774,8 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         if (!skip) {
           if constexpr (BN > 128) {
             switch (C) {
-              case 2: reduce_and_store_wide<BN, 2>(ep, gs, red, rank, n0, b0, tile_n, smem_u32(consumed), inv_smem, ready, rp); break;
               case 4: reduce_and_store_wide<BN, 4>(ep, gs, red, rank, n0, b0, tile_n, smem_u32(consumed), inv_smem, ready, rp); break;
-              default: break;  // the planner never pairs a wide tile with C = 1 or 8
+              default: break;  // the planner pairs a wide tile only with C = 4 (64-row runs spill)
             }
           } else {
             switch (C) {

@@ -615,7 +615,7 @@ GemmPlan plan_gemm(int N, int K, int Bt) {
   // 129..192 columns: one wide batch tile (BN = 192) instead of two 128-column tiles
   if (Bt > 128 && Bt <= 192 && wide_override != 1) {
     double kbw = 0;
-    GemmPlan pw = plan_splitk(N, KB, Bt, 192, &kbw);
+    GemmPlan pw = plan_splitk(N, KB, Bt, 192, &kbw, 4);  // C = 4: 32-row runs (C = 2 spills registers)
     if (kbw < 1e29 && (wide_override == 2 || splitk_clk(pw, kbw, N, K) < splitk_clk(p, best, N, K))) {
       p = pw;
       best = kbw;
