@@ -459,7 +459,9 @@ GH_DEV void tp_allreduce(const EpiParams& ep, const GemmShape& gs, int rl, int b
   const uint2* src = (const uint2*)(ep.tp_rank == 0 ? ep.tp_dst[0] : ep.tp_rank == 1 ? ep.tp_dst[1]
                                     : ep.tp_rank == 2 ? ep.tp_dst[2] : ep.tp_dst[3]) + at;  // local buffer
   const bool wait = !(ep.tp_dbg & 1), weak = ep.tp_dbg & 8;
-  constexpr int kC = En < 4 ? En : (BN == 64 ? 4 : 8);  // words in flight per poll (register budget)
+  // words in flight per poll (register budget); never more than the thread's run
+  constexpr int kC = En < 8 ? En : (BN == 64 ? 4 : 8);
+  static_assert(kC <= En && En % kC == 0, "chunks tile the run");
 #pragma unroll
   for (int c = 0; c < En; c += kC) {
     float a[kC];

@@ -86,7 +86,7 @@ def test_planner_prediction_matches_measured_split(tmp_path):
     assert rc == 0, rep
     predicted = float(re.search(r"throughput: ([0-9.e+]+) tok/s", rep).group(1))
     procs, q = spawn(worker, 2)
-    ms = collect(procs, q, 1, 900)[0]
+    ms = collect(procs, q, 1, 300)[0]
     measured = B * IF / (ms / 1e3)
     ratio = measured / predicted
     print(f"planner {predicted:.0f} tok/s, measured {measured:.0f} tok/s ({ms:.2f} ms/step): ratio {ratio:.3f}")

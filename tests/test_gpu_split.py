@@ -71,7 +71,7 @@ def test_nccl_tier_split_matches_colocated(world):
         pytest.skip(f"needs {world} GPUs")
     from paper_2501_11779_b200.stages import Engine
     procs, q = spawn(worker, world, ())
-    toks, lg = collect(procs, q, 1, 600)[0]
+    toks, lg = collect(procs, q, 1, 300)[0]
     ref = Engine(SPEC, batch=B, use_graph=False)
     rtoks, rlg = run_engine(ref)
     ref.close()
@@ -127,7 +127,7 @@ def test_pipelined_step_all_matches_colocated(world, IF, transport):
         pytest.skip(f"needs {world} GPUs")
     from paper_2501_11779_b200.stages import Engine
     procs, q = spawn(worker_all, world, (IF, transport))
-    got, used = collect(procs, q, 1, 600)[0]
+    got, used = collect(procs, q, 1, 300)[0]
     assert used == transport
     ref = run_all(Engine(SPEC, batch=B, inflight=IF, use_graph=False), IF)
     assert np.array_equal(got, ref)
@@ -173,7 +173,7 @@ def test_tier1_pipeline_stages_match_colocated():
     from paper_2501_11779_b200.stages import Engine
     world, IF, n1 = 4, 2, 2
     procs, q = spawn(worker_pp, world, (IF, n1))
-    got = collect(procs, q, 1, 600)[0]
+    got = collect(procs, q, 1, 300)[0]
     ref = run_all(Engine(SPEC, batch=B, inflight=IF, use_graph=False), IF)
     assert np.array_equal(got, ref)
 

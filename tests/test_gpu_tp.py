@@ -83,7 +83,7 @@ def worker(rank, world, port, q, name, tp, B, fed):
 
 def run_split(name, world, tp, B, fed):
     procs, q = spawn(worker, world, (name, tp, B, fed))
-    got = dict((r, (t, lg)) for r, t, lg in collect(procs, q, tp, 900))
+    got = dict((r, (t, lg)) for r, t, lg in collect(procs, q, tp, 300))
     return got
 
 
