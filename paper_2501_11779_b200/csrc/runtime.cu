@@ -962,7 +962,11 @@ uint64_t gh_tier2_kv_swap_bytes(const gh_tier2* t, uint32_t n) {
   return (uint64_t)(t->l1 - t->l0) * 2 * t->sh.Hkv * P * t->sh.dh * t->sh.db;
 }
 
-gh_status gh_tier2_kv_swap(gh_tier2* t, uint32_t slot, uint32_t n, void* host, int to_host, void* stream) {
+}  // extern "C"
+
+// The swap copies of one slot, queued on `stream` (ordered after the steps already queued there,
+// before the ones queued later); gh_tier2_kv_swap waits for them, the dispatcher does not.
+static gh_status t2_kv_swap_async(gh_tier2* t, uint32_t slot, uint32_t n, void* host, int to_host, cudaStream_t st) {
   if (!t || !host) return fail(GH_EINVAL, "null argument");
   if (slot >= t->n_slots || n > (uint32_t)t->sh.S) return fail(GH_EINVAL, "kv_swap out of range");
   if (t->paged && t->mapped[slot] * (uint32_t)kKvPagePositions < n)
@@ -970,7 +974,6 @@ gh_status gh_tier2_kv_swap(gh_tier2* t, uint32_t slot, uint32_t n, void* host, i
   if (n == 0) return GH_OK;
   const Shape& s = t->sh;
   GH_CUDA(cudaSetDevice(t->device));
-  cudaStream_t st = (cudaStream_t)stream;
   const cudaMemcpyKind kind = to_host ? cudaMemcpyDeviceToHost : cudaMemcpyHostToDevice;
   char* h = (char*)host;
   char* arena = (char*)t->arena;
@@ -993,7 +996,14 @@ gh_status gh_tier2_kv_swap(gh_tier2* t, uint32_t slot, uint32_t n, void* host, i
       h += row * 2 * s.Hkv;
     }
   }
-  GH_CUDA(cudaStreamSynchronize(st));
+  return GH_OK;
+}
+
+extern "C" {
+
+gh_status gh_tier2_kv_swap(gh_tier2* t, uint32_t slot, uint32_t n, void* host, int to_host, void* stream) {
+  GH_TRY(t2_kv_swap_async(t, slot, n, host, to_host, (cudaStream_t)stream));
+  if (t && host && n) GH_CUDA(cudaStreamSynchronize((cudaStream_t)stream));
   return GH_OK;
 }
 
@@ -2111,12 +2121,18 @@ struct gh_dispatcher {
   int32_t* d_in = nullptr;     // device [IF][3][B]
   cudaEvent_t ev[kRing] = {};
   bool ev_used[kRing] = {};
-  std::map<uint64_t, void*> swapbuf;  // swap id -> pinned host buffer
+  std::map<uint64_t, std::pair<size_t, void*>> swapbuf;  // swap id -> pinned host buffer (bytes, ptr)
+  // pinned buffers whose swap-in copies were queued: back to the pool once their event has passed
+  struct Retired { cudaEvent_t ev; size_t bytes; void* p; };
+  std::vector<Retired> retired;
+  std::vector<std::pair<size_t, void*>> pool;  // free pinned buffers (cudaFreeHost would synchronise)
   std::unique_ptr<DevMem> din_mem;
   cudaStream_t st = nullptr;
   ~gh_dispatcher() {
     if (st) cudaStreamSynchronize(st);
-    for (auto& kv : swapbuf) cudaFreeHost(kv.second);
+    for (auto& kv : swapbuf) cudaFreeHost(kv.second.second);
+    for (auto& r : retired) { cudaEventDestroy(r.ev); cudaFreeHost(r.p); }
+    for (auto& b : pool) cudaFreeHost(b.second);
     if (h_in) cudaFreeHost(h_in);
     if (h_next) cudaFreeHost(h_next);
     if (h_temp) cudaFreeHost(h_temp);
@@ -2151,6 +2167,17 @@ static SchedConfig sched_config(const gh_dispatch_config* c, uint32_t batch, uin
 static gh_status disp_apply(gh_dispatcher* d, const std::vector<KvAction>& acts) {
   gh_engine* e = d->e;
   gh_tier2* t = e->t2;
+  for (size_t i = 0; i < d->retired.size();) {  // restored buffers whose copies have completed
+    if (cudaEventQuery(d->retired[i].ev) == cudaSuccess) {
+      cudaEventDestroy(d->retired[i].ev);
+      d->pool.push_back({d->retired[i].bytes, d->retired[i].p});
+      d->retired[i] = d->retired.back();
+      d->retired.pop_back();
+    } else {
+      cudaGetLastError();  // cudaErrorNotReady
+      ++i;
+    }
+  }
   if (!t) return GH_OK;  // Tier-1 holds no KV
   GH_TRY(t2_updates_begin(t));
   for (const KvAction& a : acts) {
@@ -2159,19 +2186,36 @@ static gh_status disp_apply(gh_dispatcher* d, const std::vector<KvAction>& acts)
     switch (a.op) {
       case kMap: GH_TRY(t2_map_async(t, (uint32_t)slot, a.n, d->st)); break;
       case kUnmap: GH_TRY(gh_tier2_unmap(t, (uint32_t)slot)); break;
-      case kSwapOut: {  // synchronous: waits for the steps that wrote the positions
-        const uint64_t bytes = gh_tier2_kv_swap_bytes(t, a.n);
+      case kSwapOut: {
+        // stream-ordered: after the steps that wrote the positions, before any step that reuses
+        // the pages (the copies and the steps share the dispatcher's stream) -- no host wait
+        const size_t bytes = std::max<uint64_t>(gh_tier2_kv_swap_bytes(t, a.n), 1);
         void* h = nullptr;
-        GH_CUDA(cudaMallocHost(&h, std::max<uint64_t>(bytes, 1)));
-        d->swapbuf[a.buf] = h;
-        GH_TRY(gh_tier2_kv_swap(t, (uint32_t)slot, a.n, h, 1, d->st));
+        size_t have = 0;
+        int best = -1;  // smallest pooled buffer that fits
+        for (int i = 0; i < (int)d->pool.size(); ++i)
+          if (d->pool[i].first >= bytes && (best < 0 || d->pool[i].first < d->pool[best].first)) best = i;
+        if (best >= 0) {
+          have = d->pool[best].first;
+          h = d->pool[best].second;
+          d->pool[best] = d->pool.back();
+          d->pool.pop_back();
+        } else {
+          GH_CUDA(cudaMallocHost(&h, bytes));
+          have = bytes;
+        }
+        d->swapbuf[a.buf] = {have, h};
+        GH_TRY(t2_kv_swap_async(t, (uint32_t)slot, a.n, h, 1, d->st));
         break;
       }
-      case kSwapIn: {
+      case kSwapIn: {  // queued before the step that resumes the request
         auto it = d->swapbuf.find(a.buf);
         if (it == d->swapbuf.end()) return fail(GH_EINTERNAL, "swap buffer missing on its shard");
-        GH_TRY(gh_tier2_kv_swap(t, (uint32_t)slot, a.n, it->second, 0, d->st));
-        cudaFreeHost(it->second);
+        GH_TRY(t2_kv_swap_async(t, (uint32_t)slot, a.n, it->second.second, 0, d->st));
+        cudaEvent_t done;
+        GH_CUDA(cudaEventCreateWithFlags(&done, cudaEventDisableTiming));
+        GH_CUDA(cudaEventRecord(done, d->st));
+        d->retired.push_back({done, it->second.first, it->second.second});
         d->swapbuf.erase(it);
         break;
       }
