@@ -279,3 +279,49 @@ def test_mixed_prefill_tier_split(world, kv_pages):
         assert np.array_equal(w, g)
     if not kv_pages:
         assert steps < ref_steps
+
+
+SPEC7B = gh.LLAMA2_7B.with_(n_layers=2, max_seq_len=128)  # the C2 kernels' full width, two layers
+
+
+def seven_b_requests():
+    rng = np.random.default_rng(23)
+    return [rng.integers(0, SPEC7B.vocab_size, size=int(n), dtype=np.int32) for n in rng.integers(1, 40, 12)]
+
+
+def worker_7b(rank, world, port, q):
+    import torch
+    import torch.distributed as dist
+    from paper_2501_11779_b200.stages import Comm, ContinuousDispatcher, Engine
+    torch.cuda.set_device(rank)
+    init_rank(rank, world, port)
+    obj = [Comm.unique_ids(1) if rank == 0 else None]
+    dist.broadcast_object_list(obj, src=0)
+    comm = Comm(obj[0], world, rank, rank)
+    eng = Engine(SPEC7B, batch=8, inflight=2, device=rank, use_graph=False, comm=comm, transport="peer")
+    out, steps = ContinuousDispatcher(eng).run(seven_b_requests(), 6)
+    eng.close()
+    comm.close()
+    if rank == 0:
+        q.put((out, steps))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.skipif(n_gpus() < 2, reason="needs >= 2 GPUs")
+@pytest.mark.parametrize("world", [2, 3])
+def test_7b_shape_split_dispatcher_matches_colocated(world):
+    """The Llama-2-7B widths (D 4096, 32 heads, FFN 11008; two layers) through the native
+    dispatcher on the pipelined split (IF 2, peer transport): every request's tokens identical to
+    the colocated engine's (same batch per in-flight batch, hence the same GEMM plans)."""
+    if n_gpus() < world:
+        pytest.skip(f"needs {world} GPUs")
+    from paper_2501_11779_b200.stages import ContinuousDispatcher, Engine
+    procs, q = spawn(worker_7b, world)
+    got, steps = collect(procs, q, 1, 300)[0]
+    ref = Engine(SPEC7B, batch=8, inflight=2, use_graph=False)
+    want, ref_steps = ContinuousDispatcher(ref).run(seven_b_requests(), 6)
+    ref.close()
+    assert steps == ref_steps
+    for w, g in zip(want, got):
+        assert np.array_equal(w, g)
