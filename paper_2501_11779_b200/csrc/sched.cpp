@@ -19,6 +19,8 @@ std::string Sched::init(const SchedConfig& c) {
   }
   free_.assign(ns, c.pages);
   lanes_.assign((size_t)c.batch * c.inflight, Lane{});
+  unmapped_.assign(ns, 0);
+  for (uint32_t l = 0; l < lanes(); ++l) ++unmapped_[lane_shard(l)];
   if (paged()) {
     std::vector<uint32_t> per(ns, 0);
     for (uint32_t l = 0; l < lanes(); ++l) ++per[lane_shard(l)];
@@ -69,12 +71,11 @@ bool Sched::try_map(uint32_t lane, uint32_t n, std::vector<KvAction>& acts) {
   const uint32_t need = pages_for(n) > L.mapped ? pages_for(n) - L.mapped : 0;
   const uint32_t sh = lane_shard(lane);
   // keep one page for every other lane of the shard that holds none (its dummy token)
-  uint32_t empty = 0;
-  for (uint32_t o = 0; o < lanes(); ++o)
-    if (o != lane && lane_shard(o) == sh && lanes_[o].mapped == 0) ++empty;
+  const uint32_t empty = unmapped_[sh] - (L.mapped == 0 ? 1 : 0);
   if (need + empty > free_[sh]) return false;
   if (need) {
     free_[sh] -= need;
+    if (L.mapped == 0) --unmapped_[sh];
     L.mapped += need;
     acts.push_back({kMap, lane, n, 0});
     peak_pages = std::max(peak_pages, c_.pages - free_[sh]);
@@ -86,6 +87,7 @@ void Sched::unmap(uint32_t lane, std::vector<KvAction>& acts) {
   Lane& L = lanes_[lane];
   if (paged() && L.mapped) {
     free_[lane_shard(lane)] += L.mapped;
+    ++unmapped_[lane_shard(lane)];
     L.mapped = 0;
     acts.push_back({kUnmap, lane, 0, 0});
   }

@@ -119,6 +119,7 @@ class Sched {
   SchedConfig c_;
   std::vector<uint32_t> shard_of_;     // row -> shard
   std::vector<uint32_t> free_;         // per shard: free pages
+  std::vector<uint32_t> unmapped_;     // per shard: lanes holding no page
   std::vector<Req> reqs_;
   std::deque<uint64_t> queue_;
   std::vector<Lane> lanes_;
