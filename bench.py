@@ -550,6 +550,13 @@ def run_split(args, wl, rank, world):
         torch.cuda.synchronize()
         dist.barrier()
     ms_local = e0.elapsed_time(e1) / args.steps
+    if os.environ.get("GH_BENCH_HOST_TIMING"):  # diagnostics: host enqueue time of one step (GPU idle)
+        h0 = time.perf_counter()
+        eng.step_all(stream=stream)
+        h1 = time.perf_counter()
+        stream.synchronize()
+        print(f"rank {rank}: host enqueue {1e3 * (h1 - h0):.3f} ms/step", file=sys.stderr)
+        dist.barrier()
     t = torch.tensor([ms_local], dtype=torch.float64)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms = float(t.item())
@@ -578,12 +585,12 @@ def run_split(args, wl, rank, world):
     e2e_ms = torch.tensor([(time.perf_counter() - t0) * 1e3 / nsteps], dtype=torch.float64)
     if os.environ.get("GH_PROFILE_GEMMS"):  # diagnostics: per-GEMM times of one more step (serialised)
         import ctypes
-        lib.gh_debug_gemm_profile(1)
+        lib.gh_debug_gemm_profile(int(os.environ["GH_PROFILE_GEMMS"]))  # 2: per-launch timeline
         eng.step_all(stream=stream)
         stream.synchronize()
         lib.gh_debug_gemm_profile(0)
-        buf = ctypes.create_string_buffer(1 << 16)
-        lib.gh_debug_gemm_profile_dump(buf, 1 << 16)
+        buf = ctypes.create_string_buffer(1 << 20)
+        lib.gh_debug_gemm_profile_dump(buf, 1 << 20)
         print(f"rank {rank} GEMM profile:\n{buf.value.decode()}", file=sys.stderr)
     print(f"rank {rank} ({eng.role}): device {ms_local:.3f} ms/step, e2e {float(e2e_ms.item()):.3f} ms/step",
           file=sys.stderr)

@@ -415,9 +415,11 @@ gh_status gh_debug_gemm_bench(int N, int K, int B, int flags, int stages, int cl
  * 4 last MMA issued, 5 epilogue done, 6 exit, 7.. epilogue phases of the last tile). */
 gh_status gh_debug_gemm_trace(int N, int K, int B, int copies, int reps, float* us,
                               unsigned long long* trace, int trace_cap);
-/* on != 0: bracket every Tier-1 GEMM launch of this process with CUDA events (serialising it:
+/* on == 1: bracket every Tier-1 GEMM launch of this process with CUDA events (serialising it:
  * no PDL overlap); _dump writes one line per (N, K, B, all-reduce) shape with the mean time and
- * weight-stream rate, then clears the records. */
+ * weight-stream rate, then clears the records.  on == 2: timeline mode -- no events; every GEMM
+ * launch (up to 2048) records per-CTA globaltimer stamps and _dump writes one line per launch
+ * (first CTA start, median griddepcontrol.wait return, last CTA exit, in us). */
 gh_status gh_debug_gemm_profile(int on);
 gh_status gh_debug_gemm_profile_dump(char* buf, uint64_t cap);
 

@@ -161,6 +161,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
             if (i == S - 1) {
               if (trace) trace[1] = globaltimer();
               griddep_wait();
+              wait_peer_rows(gs);
               if (trace) trace[2] = globaltimer();
               for (int k = 0; k < S; ++k)
                 tma_load_2d_pair(smem + k * kStage + L::kABytes, &tmX, pre_kb[k] * kBlockK, pre_tile[k],
@@ -175,6 +176,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       if (!pre_done) {  // fewer than S k-blocks in this pair's range
         if (trace) trace[1] = globaltimer();
         griddep_wait();
+        wait_peer_rows(gs);
         if (trace) trace[2] = globaltimer();
         for (int k = 0; k < i; ++k)
           tma_load_2d_pair(smem + k * kStage + L::kABytes, &tmX, pre_kb[k] * kBlockK, pre_tile[k], full0 + k * 8,
@@ -234,6 +236,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     const int n_slots = min(L::kFixSlots, S * kStage / 16384);
     uint32_t pphase = 0;  // parity bits of the fixup barriers (one per slot)
     griddep_wait();  // residual / positions / norm statistics belong to earlier kernels
+    wait_peer_rows(gs);
     // positions of every batch column once (the RoPE table lookups then need no dependent load)
     const bool pos_cached = ep.kind == EPI_QKV_ROPE && gs.Bt <= kPairMaxInvCols;
     if (pos_cached)

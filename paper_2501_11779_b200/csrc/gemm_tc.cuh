@@ -590,6 +590,14 @@ GH_DEV void reduce_and_store_wide(const EpiParams& ep, const GemmShape& gs, cons
     for (int p = 0; p < C; ++p) mbar_arrive_cluster_relaxed(mapa_shared(consumed_saddr, p));
 }
 
+// Rows delivered by the peer transport (GemmShape::xwait): spin on every shard's flag word, then
+// order the async-proxy (TMA) reads that follow after the acquiring loads.
+GH_DEV void wait_peer_rows(const GemmShape& gs) {
+  if (!gs.xwait) return;
+  for (int j = 0; j < gs.xwait_n; ++j) flag_wait_sys(gs.xwait + j, gs.xwait_val);
+  asm volatile("fence.proxy.async.global;" ::: "memory");
+}
+
 template <int BN>
 __global__ void __launch_bounds__(kGemmThreads, 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CUtensorMap tmX,
@@ -657,6 +665,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       }
       if (trace) trace[1] = globaltimer();
       griddep_wait();
+      wait_peer_rows(gs);
       if (trace) trace[2] = globaltimer();
       for (int i = 0; i < pre && load_x; ++i) {
         const int tile = cid + (i / nkb) * ncl, kb = kbA + i % nkb;
@@ -726,6 +735,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     const int row = q * 32 + (threadIdx.x & 31);
     const bool skip = gs.flags & GEMM_DBG_NO_EPI;
     griddep_wait();          // residual / positions belong to earlier kernels
+    wait_peer_rows(gs);
     if (ep.ss_in) {          // overlaps the mainloop: the epilogue warps are idle until tile 0
       compute_inv_rms(ep, gs, inv_smem);
       epi_bar();

@@ -743,6 +743,9 @@ cudaError_t launch_gemm(const Weight& W, const CUtensorMap* tmW, const void* X, 
   gs.sk_ws = sc.sk_ws;
   gs.sk_flags = sc.sk_flags;
   gs.sk_split = p.split ? 1 : 0;
+  gs.xwait = sc.xwait;
+  gs.xwait_n = sc.xwait_n;
+  gs.xwait_val = sc.xwait_val;
   if (p.pair) {
     if (!sc.sk_ws || !sc.sk_flags) return cudaErrorInvalidValue;
     return launch_pair(tmW, tmX, gs, p, ep, st);

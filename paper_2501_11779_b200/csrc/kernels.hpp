@@ -69,6 +69,9 @@ struct GemmScratch {
   unsigned long long* trace = nullptr;                // per-CTA timestamps (diagnostics only)
   float* sk_ws = nullptr;                             // pair kernel stream-K partials (kSkWsBytes)
   unsigned int* sk_flags = nullptr;                   // [kNumSMs] zero-initialised
+  const unsigned int* xwait = nullptr;                // GemmShape::xwait (peer-delivered rows)
+  int xwait_n = 0;
+  unsigned int xwait_val = 0;
 };
 constexpr size_t kSkWsBytes = (size_t)74 * 256 * 256 * 4;  // co-resident pairs x 256 columns x 256 rows fp32
 void gemm_debug_set(int stages);  // 0 = production pipeline depth

@@ -72,6 +72,12 @@ struct GemmShape {
   float* sk_ws;
   unsigned int* sk_flags;
   int sk_split;         // 1: stream-K k-block ranges; 0: contiguous whole-tile ranges
+  // Tier-1 of the split over the peer transport: the activation rows (and the residual) arrive
+  // from xwait_n Tier-2 GPUs, each publishing sequence number xwait_val in its flag word
+  // xwait[j] after its copy (nullptr: the rows belong to earlier kernels only)
+  const unsigned int* xwait;
+  int xwait_n;
+  unsigned int xwait_val;
 };
 enum GemmDbg : int { GEMM_DBG_NO_MMA = 1, GEMM_DBG_NO_X = 2, GEMM_DBG_NO_HINT = 4, GEMM_DBG_NO_EPI = 8, GEMM_DBG_SK_TILES = 16,
                      GEMM_DBG_NO_STORE = 32 };

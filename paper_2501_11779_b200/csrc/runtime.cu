@@ -112,10 +112,26 @@ struct GemmProfiler {
   // stamps), summarised as medians over CTAs and launches
   int trace_n = 0, trace_k = 0;
   std::vector<std::vector<double>> phases;  // per launch: median per phase
+  // gh_debug_gemm_profile(2): timeline mode -- no events (PDL overlap kept); every GEMM launch gets
+  // its own slice of trace stamps, summarised per launch by the dump (first CTA start, median
+  // griddepcontrol.wait return, last CTA exit)
+  bool timeline = false;
+  unsigned long long* tl_buf = nullptr;
+  int tl_cap = 0, tl_next = 0, tl_dev = -1;
+  struct TlRec { int N, K, B; bool pair; };
+  std::vector<TlRec> tl_recs;
 } g_prof;
 }  // namespace gh
 
 // ================================================================== Tier-1
+// Rows of a GEMM's activation operand delivered by peer copies: flag words [n] that reach
+// sequence number v once their copy has landed (GemmShape::xwait; the split's F3 input)
+struct PeerWait {
+  const unsigned int* f;
+  int n;
+  unsigned int v;
+};
+
 struct gh_tier1 {
   Shape sh;
   int device = 0;
@@ -164,13 +180,14 @@ struct gh_tier1 {
   // `next`: the weight the following Tier-1 kernel streams; its leading bytes are prefetched into
   // L2 during this GEMM's tail (gemm_tc.cuh, GemmShape::pf)
   gh_status gemm(const Weight& W, const CUtensorMap* tmW, const void* X, long ldx, int B,
-                 const EpiParams& ep, cudaStream_t st, const Weight* next = nullptr) {
+                 const EpiParams& ep, cudaStream_t st, const Weight* next = nullptr, const PeerWait* pw = nullptr) {
     const GemmPlan& p = plan(W.N, W.K, B, ep.tp_n > 1);
     if (ep.tp_n > 1 && (p.pair || p.BN > 128)) return fail(GH_EINTERNAL, "tp all-reduce needs the split-K plan");
     CUtensorMap* tmX = nullptr;
     if (sh.db == 2) GH_TRY(tmaps.get(X, (uint64_t)B, (uint64_t)W.K, (uint64_t)ldx, (uint32_t)p.x_box_rows(), &tmX));
     GemmProfiler::Rec rec{};
     GemmScratch sc = gsc;
+    if (pw) { sc.xwait = pw->f; sc.xwait_n = pw->n; sc.xwait_val = pw->v; }
     const bool traced = g_prof.on && W.N == g_prof.trace_n && W.K == g_prof.trace_k && !p.pair;
     if (g_prof.on) {
       rec = {W.N, W.K, B, ep.tp_n > 1, nullptr, nullptr};
@@ -186,6 +203,11 @@ struct gh_tier1 {
         GH_CUDA(cudaMemsetAsync(trace_buf, 0, (size_t)kNumSMs * 16 * 8, st));
         sc.trace = trace_buf;
       }
+    }
+    if (g_prof.timeline && g_prof.tl_next < g_prof.tl_cap) {
+      std::lock_guard<std::mutex> lk(g_prof.mu);
+      sc.trace = g_prof.tl_buf + (size_t)g_prof.tl_next++ * kNumSMs * 16;
+      g_prof.tl_recs.push_back({W.N, W.K, B, p.pair});
     }
     GH_CUDA(launch_gemm(W, tmW, X, ldx, tmX, B, p, ep, sc, st, next ? next->ptr : nullptr, prefetch_bytes(next)));
     if (g_prof.on) {
@@ -505,7 +527,8 @@ static gh_status t1_pre(gh_tier1* t, uint32_t layer, uint32_t B, const void* x, 
 // x_resid: the layer's input activation [B][D] (tensor-parallel Tier-1: the residual is the local
 // replica of x, the message block carries only this rank's columns); nullptr = the bwd message's x.
 static gh_status t1_post_tp(gh_tier1* t, uint32_t layer, uint32_t B, const void* msg_bwd, const void* x_resid,
-                            void* x_next, float* ss_next, int* ss_next_slices, cudaStream_t st) {
+                            void* x_next, float* ss_next, int* ss_next_slices, cudaStream_t st,
+                            const PeerWait* pw) {
   const Shape& s = t->sh;
   auto& L = t->layers[layer - t->l0];
   const int Dt = s.D / t->tp, Dht = s.Dh / t->tp;
@@ -518,7 +541,7 @@ static gh_status t1_post_tp(gh_tier1* t, uint32_t layer, uint32_t B, const void*
   ep.ss_out = t->ss_h;
   GH_TRY(epi_tp(t, (int)B, ep));
   GH_TRY(t->gemm(L.o, &L.tm_o, (const char*)msg_bwd + (size_t)Dt * s.db, s.ld_bwd() / t->tp, (int)B, ep, st,
-                 &L.w13));
+                 &L.w13, pw));
   // g_r = silu(rms(h) W1_r^T) * (rms(h) W3_r^T): this rank's hidden units
   ep = epi_default();
   ep.kind = EPI_SWIGLU;
@@ -539,12 +562,13 @@ static gh_status t1_post_tp(gh_tier1* t, uint32_t layer, uint32_t B, const void*
 }
 
 static gh_status t1_post(gh_tier1* t, uint32_t layer, uint32_t B, const void* msg_bwd, void* x_next, float* ss_next,
-                         int* ss_next_slices, cudaStream_t st, const void* x_resid = nullptr) {
+                         int* ss_next_slices, cudaStream_t st, const void* x_resid = nullptr,
+                         const PeerWait* pw = nullptr) {
   if (!t || !msg_bwd || !x_next) return fail(GH_EINVAL, "null argument");
   if (layer < t->l0 || layer >= t->l1) return fail(GH_EINVAL, "layer not owned by this Tier-1");
   if (B > t->max_batch) return fail(GH_EINVAL, "B exceeds max_batch");
   if (B == 0) return GH_OK;
-  if (t->tp > 1) return t1_post_tp(t, layer, B, msg_bwd, x_resid, x_next, ss_next, ss_next_slices, st);
+  if (t->tp > 1) return t1_post_tp(t, layer, B, msg_bwd, x_resid, x_next, ss_next, ss_next_slices, st, pw);
   const Shape& s = t->sh;
   auto& L = t->layers[layer - t->l0];
   const bool fused = s.db == 2 && B <= (uint32_t)kFusedNormMaxBatch;
@@ -554,7 +578,7 @@ static gh_status t1_post(gh_tier1* t, uint32_t layer, uint32_t B, const void* ms
   ep.out = t->h; ep.ldo = s.D;
   ep.resid = msg_bwd; ep.ldr = s.ld_bwd();
   if (fused) ep.ss_out = t->ss_h;
-  GH_TRY(t->gemm(L.o, &L.tm_o, (const char*)msg_bwd + (size_t)s.D * s.db, s.ld_bwd(), (int)B, ep, st, &L.w13));
+  GH_TRY(t->gemm(L.o, &L.tm_o, (const char*)msg_bwd + (size_t)s.D * s.db, s.ld_bwd(), (int)B, ep, st, &L.w13, pw));
   // g = silu(rms(h) W1^T) * (rms(h) W3^T)
   const void* ffn_in = t->h;
   ep = epi_default();
@@ -1220,9 +1244,9 @@ static gh_status act_embed(gh_engine* e, gh_engine::Batch& b, cudaStream_t st) {
 static gh_status act_pre(gh_engine* e, gh_engine::Batch& b, int l, cudaStream_t st) {
   return t1_pre(e->t1, l, e->cfg.batch, b.x(b.cur), SsRef{b.ss(b.cur), b.ss_slices[b.cur]}, b.pos, b.fwd, st);
 }
-static gh_status act_post(gh_engine* e, gh_engine::Batch& b, int l, cudaStream_t st) {
+static gh_status act_post(gh_engine* e, gh_engine::Batch& b, int l, cudaStream_t st, const PeerWait* pw = nullptr) {
   const int nx = b.cur ^ 1;
-  GH_TRY(t1_post(e->t1, l, e->cfg.batch, b.bwd, b.x(nx), b.ss(nx), &b.ss_slices[nx], st, b.x(b.cur)));
+  GH_TRY(t1_post(e->t1, l, e->cfg.batch, b.bwd, b.x(nx), b.ss(nx), &b.ss_slices[nx], st, b.x(b.cur), pw));
   b.cur = nx;
   return GH_OK;
 }
@@ -1915,6 +1939,8 @@ static gh_status split_step_peer(gh_engine* e, cudaStream_t st) {
   const int nb = (int)e->batches.size();
   // diagnostics: GH_SPLIT_NOWAIT=1 drops the flag waits (wrong results; isolates compute time)
   static const bool nowait = getenv("GH_SPLIT_NOWAIT") != nullptr;
+  static const bool nosend = nowait && getenv("GH_SPLIT_NOSEND") != nullptr;  // + no fwd copies
+  static const bool memop_wait = getenv("GH_SPLIT_MEMOP_WAIT") != nullptr;
   if (e->role == 1) {
     const bool first = e->span == 0, last = e->span == e->n1 - 1;
     for (int ib = 0; ib < nb; ++ib) {
@@ -1936,13 +1962,17 @@ static gh_status split_step_peer(gh_engine* e, cudaStream_t st) {
     for (int l = e->l0; l < e->l1; ++l)
       for (int ib = 0; ib < nb; ++ib) {
         auto& b = e->batches[ib];
-        for (int j = 0; j < e->kp && !nowait; ++j)  // every shard of the attention output has landed
+        // every shard of the attention output has landed: the W_o GEMM's producers poll the flag
+        // words themselves (weights stream meanwhile, and the launch keeps its programmatic overlap
+        // with the previous kernel); GH_SPLIT_MEMOP_WAIT=1 waits in the stream instead (diagnostics)
+        const PeerWait pw{P.flags + f_bwd(e, ib, 0), e->kp, P.seq[ib]};
+        for (int j = 0; j < e->kp && !nowait && memop_wait; ++j)
           GH_CU(memops().wait((CUstream)st, (CUdeviceptr)(P.flags + f_bwd(e, ib, j)), P.seq[ib],
                               CU_STREAM_WAIT_VALUE_GEQ));
-        GH_TRY(act_post(e, b, l, st));
+        GH_TRY(act_post(e, b, l, st, nowait || memop_wait ? nullptr : &pw));
         if (l + 1 < e->l1) {
           GH_TRY(act_pre(e, b, l + 1, st));
-          GH_TRY(peer_send_fwd(e, ib, false, st));
+          if (!nosend) GH_TRY(peer_send_fwd(e, ib, false, st));
         } else if (last) {
           GH_TRY(act_classify(e, b, nullptr, st));
           if (e->n1 > 1) GH_TRY(peer_send_tokens(e, ib, st));
@@ -2443,6 +2473,21 @@ gh_status gh_dispatcher_stats(const gh_dispatcher* d, gh_dispatch_stats* out) {
 
 extern "C" gh_status gh_debug_gemm_profile(int on) {
   std::lock_guard<std::mutex> lk(g_prof.mu);
+  if (on == 2) {  // timeline mode (see GemmProfiler)
+    int dev = 0;
+    GH_CUDA(cudaGetDevice(&dev));
+    if (!g_prof.tl_buf || g_prof.tl_dev != dev) {
+      g_prof.tl_cap = 2048;
+      GH_CUDA(cudaMalloc(&g_prof.tl_buf, (size_t)g_prof.tl_cap * kNumSMs * 16 * 8));
+      g_prof.tl_dev = dev;
+    }
+    GH_CUDA(cudaMemset(g_prof.tl_buf, 0, (size_t)g_prof.tl_cap * kNumSMs * 16 * 8));
+    g_prof.tl_next = 0;
+    g_prof.tl_recs.clear();
+    g_prof.timeline = true;
+    return GH_OK;
+  }
+  g_prof.timeline = false;
   g_prof.on = on != 0;
   if (const char* t = getenv("GH_GEMM_TRACE")) sscanf(t, "%dx%d", &g_prof.trace_n, &g_prof.trace_k);
   return GH_OK;
@@ -2464,6 +2509,38 @@ extern "C" gh_status gh_debug_gemm_profile_dump(char* buf, uint64_t cap) {
   }
   g_prof.recs.clear();
   std::string out;
+  if (!g_prof.tl_recs.empty()) {  // timeline: one line per launch, us from the first launch's first CTA
+    GH_CUDA(cudaDeviceSynchronize());
+    const size_t per = (size_t)kNumSMs * 16;
+    std::vector<unsigned long long> h(per * g_prof.tl_recs.size());
+    GH_CUDA(cudaMemcpy(h.data(), g_prof.tl_buf, h.size() * 8, cudaMemcpyDeviceToHost));
+    unsigned long long t0 = ~0ull;
+    for (size_t i = 0; i < per; ++i) if (h[i]) t0 = std::min(t0, h[(i / 16) * 16]);
+    char line[256];
+    for (size_t l = 0; l < g_prof.tl_recs.size(); ++l) {
+      const auto& r = g_prof.tl_recs[l];
+      const unsigned long long* t = h.data() + l * per;
+      const int ex = r.pair ? 10 : 6;
+      unsigned long long first = ~0ull, last = 0;
+      std::vector<unsigned long long> w;
+      int ctas = 0;
+      for (int c = 0; c < kNumSMs; ++c) {
+        if (!t[c * 16]) continue;
+        ++ctas;
+        first = std::min(first, t[c * 16]);
+        last = std::max(last, t[c * 16 + ex]);
+        if (t[c * 16 + 2]) w.push_back(t[c * 16 + 2]);
+      }
+      if (!ctas) continue;
+      std::sort(w.begin(), w.end());
+      const double wm = w.empty() ? 0.0 : (double)(w[w.size() / 2] - t0) / 1e3;
+      snprintf(line, sizeof(line), "tl %zu N=%d K=%d B=%d %s ctas=%d start=%.2f wait=%.2f exit=%.2f\n", l, r.N, r.K,
+               r.B, r.pair ? "pair" : "splitk", ctas, (double)(first - t0) / 1e3, wm, (double)(last - t0) / 1e3);
+      out += line;
+    }
+    g_prof.tl_recs.clear();
+    g_prof.timeline = false;
+  }
   for (auto& kv : agg) {
     const auto& k = kv.first;
     const double us = kv.second.second / kv.second.first;

@@ -39,4 +39,12 @@ e1.record(s)
 torch.cuda.synchronize()
 ms = e0.elapsed_time(e1) / a.steps
 print(f"B={B} ctx={a.ctx} layers={a.layers}: {ms:.3f} ms/step, {B / ms * 1e3:.0f} tok/s")
+if os.environ.get("GH_PROFILE_GEMMS") == "2":  # per-launch GEMM timeline of one more step (--graph 0)
+    import ctypes
+    gh.lib().gh_debug_gemm_profile(2)
+    eng.step_device(stream=s)
+    torch.cuda.synchronize()
+    buf = ctypes.create_string_buffer(1 << 20)
+    gh.lib().gh_debug_gemm_profile_dump(buf, 1 << 20)
+    print(buf.value.decode())
 eng.close()
