@@ -349,13 +349,18 @@ uint64_t gh_kernel_launches(int reset);
  * (SPMD; Tier-2 ranks apply the KV actions of their shard, Tier-1 ranks feed tokens).  The
  * engine step is gh_engine_step_all (pipelined IF >= 2 split, or the colocated CUDA graphs);
  * lane inputs, page tables and sampling state are updated stream-ordered (no host
- * synchronisation per change), and a step's tokens are read one step later. */
+ * synchronisation per change), and a step's tokens are read one step later.
+ * Chunked prefill (prefill_chunk > 1; needs gh_engine_config.prefill): the idle lanes of
+ * an in-flight batch's shard carry further prompt tokens of that shard's lanes still reading
+ * their prompts (up to prefill_chunk tokens of one request per step, at consecutive positions of
+ * the request's own slot). */
 typedef struct gh_dispatcher gh_dispatcher;
 typedef struct gh_dispatch_config {
   uint32_t max_new;      /* tokens generated per request */
   int on_demand;         /* paged arena: map the prompt, grow a page at a time, preempt when dry */
   int preempt_swap;      /* preempt by swapping the context to host memory (else recompute) */
   int order_shortest;    /* admit the shortest prompt first (else FIFO) */
+  uint32_t prefill_chunk; /* prompt tokens of one request per step (0 / 1: one; > 1: chunked prefill) */
 } gh_dispatch_config;
 typedef struct gh_dispatch_stats {
   uint64_t steps, admitted, finished, tokens, preemptions, swaps;
@@ -363,7 +368,7 @@ typedef struct gh_dispatch_stats {
   uint64_t lane_steps;   /* busy lanes summed over steps: tokens processed (prompt, generated, recomputed) */
   uint64_t context_sum;  /* positions attended summed over busy lane-steps (mean context = / lane_steps) */
 } gh_dispatch_stats;
-/* Not for engines with Tier-1 pipeline spans (tier1_ranks > 1) or prefill rows. */
+/* Not for engines with Tier-1 pipeline spans (tier1_ranks > 1). */
 gh_status gh_dispatcher_create(gh_engine* e, const gh_dispatch_config* cfg, gh_dispatcher** out);
 gh_status gh_dispatcher_destroy(gh_dispatcher* d);
 /* Queue a request generating max_new tokens (0 = the configured max_new); GH_EINFEASIBLE when it
@@ -387,8 +392,12 @@ typedef struct gh_sched gh_sched;
 typedef struct gh_sched_config {
   uint32_t batch, inflight, kp, pages, max_seq, max_new;
   int on_demand, preempt_swap, order_shortest;
+  uint32_t prefill_chunk;
 } gh_sched_config;
-typedef struct gh_lane_input { int32_t src, tok, pos; } gh_lane_input;
+/* src 0 idle (dummy token at position 0), 1 host token `tok`, 2 the token the lane's previous step
+ * generated; home = the lane whose slot the row appends to and attends over (itself, or with
+ * chunked prefill the lane whose prompt token it carries). */
+typedef struct gh_lane_input { int32_t src, tok, pos; uint32_t home; } gh_lane_input;
 typedef struct gh_kv_action { int32_t op; uint32_t lane; uint32_t n; uint64_t buf; } gh_kv_action;
 gh_status gh_sched_create(const gh_sched_config* cfg, gh_sched** out);
 gh_status gh_sched_destroy(gh_sched* s);

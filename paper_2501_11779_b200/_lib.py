@@ -76,7 +76,7 @@ class GhRankLayout(C.Structure):
 
 class GhDispatchConfig(C.Structure):
     _fields_ = [("max_new", C.c_uint32), ("on_demand", C.c_int), ("preempt_swap", C.c_int),
-                ("order_shortest", C.c_int)]
+                ("order_shortest", C.c_int), ("prefill_chunk", C.c_uint32)]
 
 
 class GhDispatchStats(C.Structure):
@@ -87,10 +87,11 @@ class GhDispatchStats(C.Structure):
 class GhSchedConfig(C.Structure):
     _fields_ = [(n, C.c_uint32) for n in ("batch", "inflight", "kp", "pages", "max_seq", "max_new")]
     _fields_ += [(n, C.c_int) for n in ("on_demand", "preempt_swap", "order_shortest")]
+    _fields_ += [("prefill_chunk", C.c_uint32)]
 
 
 class GhLaneInput(C.Structure):
-    _fields_ = [("src", C.c_int32), ("tok", C.c_int32), ("pos", C.c_int32)]
+    _fields_ = [("src", C.c_int32), ("tok", C.c_int32), ("pos", C.c_int32), ("home", C.c_uint32)]
 
 
 class GhKvAction(C.Structure):

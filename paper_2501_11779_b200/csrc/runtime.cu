@@ -2149,6 +2149,8 @@ struct gh_dispatcher {
   float* h_temp = nullptr;     // pinned [kRing][IF][B] 1 / temperature
   uint32_t* h_seed = nullptr;  // pinned [kRing][IF][B]
   int32_t* d_in = nullptr;     // device [IF][3][B]
+  uint32_t* h_slot = nullptr;  // pinned [kRing][IF][rows] this rank's rows' slots
+  std::vector<uint32_t> last_slots;  // the slot tables last installed
   cudaEvent_t ev[kRing] = {};
   bool ev_used[kRing] = {};
   std::map<uint64_t, std::pair<size_t, void*>> swapbuf;  // swap id -> pinned host buffer (bytes, ptr)
@@ -2167,6 +2169,7 @@ struct gh_dispatcher {
     if (h_next) cudaFreeHost(h_next);
     if (h_temp) cudaFreeHost(h_temp);
     if (h_seed) cudaFreeHost(h_seed);
+    if (h_slot) cudaFreeHost(h_slot);
     for (auto v : ev) if (v) cudaEventDestroy(v);
     if (st) cudaStreamDestroy(st);
   }
@@ -2191,6 +2194,7 @@ static SchedConfig sched_config(const gh_dispatch_config* c, uint32_t batch, uin
   sc.batch = batch; sc.inflight = inflight; sc.kp = kp; sc.pages = pages; sc.max_seq = max_seq;
   sc.max_new = c->max_new; sc.on_demand = c->on_demand != 0; sc.swap = c->preempt_swap != 0;
   sc.shortest = c->order_shortest != 0;
+  sc.chunk = std::max(1u, c->prefill_chunk);
   return sc;
 }
 
@@ -2254,6 +2258,34 @@ static gh_status disp_apply(gh_dispatcher* d, const std::vector<KvAction>& acts)
   return t2_updates_end(t, d->st);
 }
 
+// The slot tables of this rank's rows: every lane's own slot, except that with chunked prefill a
+// row carrying another lane's prompt token reads and appends that lane's slot.  Installed on the
+// dispatcher's stream (pinned ring slot k) whenever they differ from the last installed ones (the
+// first step installs them: the engine's tables may have been changed by an earlier caller).
+static gh_status disp_slots(gh_dispatcher* d, const std::vector<LaneInput>& in, int k) {
+  gh_engine* e = d->e;
+  const uint32_t B = d->B(), IF = d->IF();
+  const int R = e->rows();
+  const int off = e->role == 2 ? e->shard_off[e->shard] : 0;
+  std::vector<uint32_t> tab((size_t)IF * R);
+  for (uint32_t ib = 0; ib < IF; ++ib)
+    for (int i = 0; i < R; ++i) {
+      const int64_t s = d->holder_slot(in[(size_t)ib * B + off + i].home);
+      if (s < 0) return fail(GH_EINTERNAL, "chunked prefill row borrowed across shards");
+      tab[(size_t)ib * R + i] = (uint32_t)s;
+    }
+  if (tab == d->last_slots) return GH_OK;
+  uint32_t* hs = d->h_slot + (size_t)k * IF * B;
+  std::copy(tab.begin(), tab.end(), hs);
+  for (uint32_t ib = 0; ib < IF; ++ib) {
+    auto& b = e->batches[ib];
+    GH_CUDA(cudaMemcpyAsync(b.slot, hs + (size_t)ib * R, (size_t)R * 4, cudaMemcpyHostToDevice, d->st));
+    b.slot_host.assign(hs + (size_t)ib * R, hs + (size_t)(ib + 1) * R);
+  }
+  d->last_slots.swap(tab);
+  return GH_OK;
+}
+
 // one step: plan, KV actions, inputs, engine step, next tokens back (resolved one step later)
 static gh_status disp_step(gh_dispatcher* d, bool* idle) {
   gh_engine* e = d->e;
@@ -2307,6 +2339,7 @@ static gh_status disp_step(gh_dispatcher* d, bool* idle) {
       GH_CUDA(launch_dispatch_inputs(b.tok, b.next, b.pos, d->d_in + (size_t)ib * 3 * B, (int)B, d->st));
     }
   }
+  if (e->t2) GH_TRY(disp_slots(d, in, k));
   GH_TRY(gh_engine_step_all(e, d->st));
   if (d->tokens_here()) {
     int32_t* hn = d->h_next + (size_t)k * IF * B;
@@ -2337,7 +2370,7 @@ extern "C" {
 gh_status gh_sched_create(const gh_sched_config* c, gh_sched** out) {
   if (!c || !out) return fail(GH_EINVAL, "null argument");
   *out = nullptr;
-  gh_dispatch_config dc{c->max_new, c->on_demand, c->preempt_swap, c->order_shortest};
+  gh_dispatch_config dc{c->max_new, c->on_demand, c->preempt_swap, c->order_shortest, c->prefill_chunk};
   auto g = std::make_unique<gh_sched>();
   std::string err = g->s.init(sched_config(&dc, c->batch, c->inflight, c->kp, c->pages, c->max_seq));
   if (!err.empty()) return fail(GH_EINVAL, err);
@@ -2357,7 +2390,7 @@ gh_status gh_sched_plan(gh_sched* g, gh_lane_input* in, gh_kv_action* acts, uint
   std::vector<KvAction> ka;
   std::string err = g->s.plan(li, ka);
   if (!err.empty()) return fail(GH_EINFEASIBLE, err);
-  for (size_t i = 0; i < li.size(); ++i) in[i] = {li[i].src, li[i].tok, li[i].pos};
+  for (size_t i = 0; i < li.size(); ++i) in[i] = {li[i].src, li[i].tok, li[i].pos, li[i].home};
   *n_acts = (uint32_t)ka.size();
   if (ka.size() > cap) return fail(GH_EINVAL, "action buffer too small");
   for (size_t i = 0; i < ka.size(); ++i) acts[i] = {ka[i].op, ka[i].lane, ka[i].n, ka[i].buf};
@@ -2402,7 +2435,8 @@ gh_status gh_dispatcher_create(gh_engine* e, const gh_dispatch_config* cfg, gh_d
   if (!e || !cfg || !out) return fail(GH_EINVAL, "null argument");
   *out = nullptr;
   if (e->n1 > 1) return fail(GH_EUNSUPPORTED, "the dispatcher drives one Tier-1 span (or TP ranks), not pipeline spans");
-  if (e->cfg.prefill) return fail(GH_EUNSUPPORTED, "prefill-row engines are driven by the mixed dispatcher");
+  if (cfg->prefill_chunk > 1 && !e->cfg.prefill)
+    return fail(GH_EINVAL, "chunked prefill needs a prefill-row engine (gh_engine_config.prefill)");
   GH_CUDA(cudaSetDevice(e->cfg.device));
   auto d = std::make_unique<gh_dispatcher>();
   d->e = e;
@@ -2416,6 +2450,7 @@ gh_status gh_dispatcher_create(gh_engine* e, const gh_dispatch_config* cfg, gh_d
   GH_CUDA(cudaMallocHost((void**)&d->h_next, gh_dispatcher::kRing * n * 4));
   GH_CUDA(cudaMallocHost((void**)&d->h_temp, gh_dispatcher::kRing * n * 4));
   GH_CUDA(cudaMallocHost((void**)&d->h_seed, gh_dispatcher::kRing * n * 4));
+  GH_CUDA(cudaMallocHost((void**)&d->h_slot, gh_dispatcher::kRing * n * 4));
   d->din_mem = std::make_unique<DevMem>();
   GH_CUDA(cudaMalloc(&d->din_mem->p, n * 3 * 4));
   d->d_in = (int32_t*)d->din_mem->p;

@@ -11,6 +11,7 @@ std::string Sched::init(const SchedConfig& c) {
   if (c.max_new == 0) return "max_new must be >= 1";
   if (c.on_demand && c.pages == 0) return "on-demand paging needs a paged KV arena";
   c_ = c;
+  if (c_.chunk == 0) c_.chunk = 1;
   const uint32_t ns = std::max(1u, c.kp);
   shard_of_.assign(c.batch, 0);
   for (uint32_t j = 0, row = 0; j < ns; ++j) {  // balanced shards, low shards first (analytic.cpp:119)
@@ -21,6 +22,13 @@ std::string Sched::init(const SchedConfig& c) {
   lanes_.assign((size_t)c.batch * c.inflight, Lane{});
   unmapped_.assign(ns, 0);
   for (uint32_t l = 0; l < lanes(); ++l) ++unmapped_[lane_shard(l)];
+  std::vector<uint32_t> first(ns + 1, 0);  // first row of each shard
+  for (uint32_t row = 0; row < c.batch; ++row) first[shard_of_[row] + 1] = row + 1;
+  admit_order_.clear();
+  for (uint32_t k = 0; k < c.batch; ++k)
+    for (uint32_t ib = 0; ib < c.inflight; ++ib)
+      for (uint32_t j = 0; j < ns; ++j)
+        if (first[j] + k < first[j + 1]) admit_order_.push_back(ib * c.batch + first[j] + k);
   if (paged()) {
     std::vector<uint32_t> per(ns, 0);
     for (uint32_t l = 0; l < lanes(); ++l) ++per[lane_shard(l)];
@@ -192,8 +200,8 @@ std::string Sched::grow(std::vector<KvAction>& acts) {
 
 std::string Sched::plan(std::vector<LaneInput>& in, std::vector<KvAction>& acts) {
   acts.clear();
-  // finished requests gave their lanes back at commit; admissions first (lane order)
-  for (uint32_t l = 0; l < lanes(); ++l)
+  // finished requests gave their lanes back at commit; admissions first (spread order)
+  for (uint32_t l : admit_order_)
     if (lanes_[l].req < 0) {
       if (lanes_[l].freed) {  // its request finished at the last commit
         unmap(l, acts);
@@ -212,31 +220,69 @@ std::string Sched::plan(std::vector<LaneInput>& in, std::vector<KvAction>& acts)
     return "request " + std::to_string(queue_.front()) + " needs " + std::to_string(admit_need(r)) +
            " positions, more than a KV page pool can back";
   }
-  in.assign(lanes(), LaneInput{kIdle, 0, 0});
+  in.resize(lanes());
   cur_.clear();
   for (uint32_t l = 0; l < lanes(); ++l) {
-    const Lane& L = lanes_[l];
+    Lane& L = lanes_[l];
+    L.fed = 1;
+    in[l] = {kIdle, 0, 0, l};
     if (L.req < 0) continue;
     const Req& r = reqs_[L.req];
     const uint32_t plen = (uint32_t)r.prompt.size();
-    if (L.t < plen) in[l] = {kHost, r.prompt[L.t], (int32_t)L.t};
-    else if (L.fed_back) in[l] = {kDevice, 0, (int32_t)L.t};
-    else in[l] = {kHost, r.out[L.t - r.orig_len], (int32_t)L.t};
+    if (L.t < plen) in[l] = {kHost, r.prompt[L.t], (int32_t)L.t, l};
+    else if (L.fed_back) in[l] = {kDevice, 0, (int32_t)L.t, l};
+    else in[l] = {kHost, r.out[L.t - r.orig_len], (int32_t)L.t, l};
   }
-  last_in_ = in;
+  if (c_.chunk > 1) chunk_prefill(in, acts);
   return "";
+}
+
+void Sched::chunk_prefill(std::vector<LaneInput>& in, std::vector<KvAction>& acts) {
+  const uint32_t B = c_.batch, ns = std::max(1u, c_.kp);
+  std::vector<uint32_t> idle, reading;
+  for (uint32_t ib = 0; ib < c_.inflight; ++ib)
+    for (uint32_t j = 0; j < ns; ++j) {
+      idle.clear();
+      reading.clear();
+      for (uint32_t row = 0; row < B; ++row) {
+        if (shard_of_[row] != j) continue;
+        const uint32_t l = ib * B + row;
+        const Lane& L = lanes_[l];
+        if (L.req < 0) idle.push_back(l);
+        else if (L.t + 1 < reqs_[L.req].prompt.size()) reading.push_back(l);  // >= 2 prompt tokens left
+      }
+      if (idle.empty() || reading.empty()) continue;
+      std::sort(reading.begin(), reading.end(), [&](uint32_t a, uint32_t b) { return lanes_[a].seq < lanes_[b].seq; });
+      size_t next_idle = 0;
+      for (uint32_t l : reading) {  // oldest admission first
+        Lane& L = lanes_[l];
+        const Req& r = reqs_[L.req];
+        uint32_t extra = std::min<uint32_t>({c_.chunk - 1, (uint32_t)r.prompt.size() - L.t - 1,
+                                             (uint32_t)(idle.size() - next_idle)});
+        // on-demand paging: the chunk's positions must be backed (the whole request is otherwise)
+        while (extra && c_.on_demand && !try_map(l, L.t + extra + 1, acts)) --extra;
+        if (!extra) continue;
+        for (uint32_t k = 0; k < extra; ++k)  // borrowed rows: the chunk's leading tokens
+          in[idle[next_idle++]] = {kHost, r.prompt[L.t + k], (int32_t)(L.t + k), l};
+        in[l] = {kHost, r.prompt[L.t + extra], (int32_t)(L.t + extra), l};  // its own row: the last
+        L.fed = extra + 1;
+        if (next_idle == idle.size()) break;
+      }
+    }
 }
 
 void Sched::commit() {
   ++steps;
-  std::vector<KvAction> none;
   for (uint32_t l = 0; l < lanes(); ++l) {
     Lane& L = lanes_[l];
     if (L.req < 0) continue;
     Req& r = reqs_[L.req];
     const uint32_t plen = (uint32_t)r.prompt.size();
-    ++lane_steps;
-    context_sum += L.t + 1;
+    const uint32_t n = L.fed;  // tokens fed at positions [t, t + n); the lane's own row held the last
+    lane_steps += n;
+    context_sum += (uint64_t)n * L.t + (uint64_t)n * (n + 1) / 2;
+    L.t += n - 1;
+    L.fed = 1;
     if (L.t + 1 >= plen) {  // this step's output is the request's next token
       cur_.push_back({(uint64_t)L.req, r.n_out, l});
       ++r.n_out;

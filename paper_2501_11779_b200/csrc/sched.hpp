@@ -14,6 +14,13 @@
 //    context goes to host memory and comes back into a lane of the same shard)
 //  * every step each lane gets an input: an idle lane a dummy token at position 0, a busy lane its
 //    prompt token (host) or the token its previous step generated (device feedback)
+//  * chunked prefill (chunk > 1, "the Dispatcher decides which tokens are placed in empty
+//    slots of batches"): the idle lanes of an in-flight batch's shard carry further prompt tokens
+//    of that shard's busy lanes still reading their prompts -- up to chunk tokens of one request
+//    per step, at consecutive positions of the request's own slot (a prefill-row engine appends
+//    every row's key and value before attention, so the rows see each other exactly as one token
+//    per step would); the request's own lane takes the chunk's last token, so its output and the
+//    device feedback stay on its own row
 //
 // Decisions depend only on prompt lengths, max_new, the page accounting and the step count,
 // never on token values, so every rank of a tier split runs the same scheduler and takes the same
@@ -39,12 +46,15 @@ struct SchedConfig {
   bool on_demand = false;    // paged: map the prompt only, grow a page at a time
   bool swap = false;         // preemption by swap (else recompute)
   bool shortest = false;     // admission order: shortest prompt first (else FIFO)
+  uint32_t chunk = 1;        // prompt tokens of one request per step (> 1: chunked prefill into idle lanes)
 };
 
 // input of one lane for the next step
 enum LaneSrc : int32_t { kIdle = 0, kHost = 1, kDevice = 2 };
 struct LaneInput {
   int32_t src, tok, pos;
+  uint32_t home;    // the lane whose slot this row appends to and attends over (itself, or the
+                    // lane whose prompt chunk it carries)
 };
 // KV action on a lane's slot, applied (before the step) by the rank holding the lane's shard
 enum KvOp : int32_t { kMap = 0, kUnmap = 1, kSwapOut = 2, kSwapIn = 3 };
@@ -104,6 +114,7 @@ class Sched {
     uint32_t mapped = 0;               // pages held
     bool fed_back = false;             // the previous step of this lane produced its next input
     bool freed = false;                // its request finished at the last commit: return the pages
+    uint32_t fed = 1;                  // prompt / output tokens fed by the planned step (chunked prefill)
   };
   uint32_t pages_for(uint32_t n) const { return (n + kPage - 1) / kPage; }
   bool paged() const { return c_.pages > 0; }
@@ -120,6 +131,10 @@ class Sched {
   std::vector<uint32_t> shard_of_;     // row -> shard
   std::vector<uint32_t> free_;         // per shard: free pages
   std::vector<uint32_t> unmapped_;     // per shard: lanes holding no page
+  // admission order: the k-th lane of every (in-flight batch, shard) group before any group's
+  // (k+1)-th, so a partly filled pool spreads its requests over the batches and Tier-2 shards
+  // (equal Tier-2 load) and leaves idle lanes beside each for chunked prefill
+  std::vector<uint32_t> admit_order_;
   std::vector<Req> reqs_;
   std::deque<uint64_t> queue_;
   std::vector<Lane> lanes_;
@@ -129,7 +144,7 @@ class Sched {
   struct Emit { uint64_t req; uint32_t idx; uint32_t lane; };
   std::deque<std::vector<Emit>> pending_;
   std::vector<Emit> cur_;              // outputs of the planned (not yet committed) step
-  std::vector<LaneInput> last_in_;
+  void chunk_prefill(std::vector<LaneInput>& in, std::vector<KvAction>& acts);
 };
 
 }  // namespace gh

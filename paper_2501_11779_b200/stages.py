@@ -338,16 +338,18 @@ class Dispatcher:
 class Scheduler:
     """The dispatcher's decision logic (C++ gh_sched, host only): batch-state objects of IF
     in-flight batches x B lanes with per-shard page accounting (sched.hpp).
-    plan() -> (inputs [lanes] of (src, tok, pos), KV actions); the caller runs the step, then
-    commit(), and resolve(next tokens) for the oldest committed step (any lag)."""
+    plan() -> (inputs [lanes] of (src, tok, pos, home), KV actions); the caller runs the step, then
+    commit(), and resolve(next tokens) for the oldest committed step (any lag).  `home` is the lane
+    whose slot the row appends to and attends over: the row's own lane, or with chunked prefill
+    (chunk > 1) the lane whose prompt token an otherwise idle row carries."""
 
     SRC_IDLE, SRC_HOST, SRC_DEVICE = 0, 1, 2
     MAP, UNMAP, SWAP_OUT, SWAP_IN = 0, 1, 2, 3
 
     def __init__(self, batch: int, max_new: int, inflight: int = 1, kp: int = 0, pages: int = 0, max_seq: int = 0,
-                 on_demand: bool = False, preempt: str = "recompute", order: str = "fifo"):
+                 on_demand: bool = False, preempt: str = "recompute", order: str = "fifo", chunk: int = 1):
         cfg = L.GhSchedConfig(batch, inflight, kp, pages, max_seq, max_new, int(on_demand), int(preempt == "swap"),
-                              int(order == "shortest"))
+                              int(order == "shortest"), chunk)
         h = C.c_void_p()
         L.check(L.lib().gh_sched_create(C.byref(cfg), C.byref(h)))
         self.h = h
@@ -371,7 +373,7 @@ class Scheduler:
     def plan(self):
         n = C.c_uint32()
         L.check(L.lib().gh_sched_plan(self.h, self._in, self._acts, len(self._acts), C.byref(n)))
-        ins = np.array([(x.src, x.tok, x.pos) for x in self._in], np.int32).reshape(self.lanes, 3)
+        ins = np.array([(x.src, x.tok, x.pos, x.home) for x in self._in], np.int32).reshape(self.lanes, 4)
         return ins, [(a.op, a.lane, a.n, a.buf) for a in self._acts[:n.value]]
 
     def commit(self):
@@ -424,7 +426,11 @@ class ContinuousDispatcher:
     admitted request is preempted -- recomputed (``preempt="recompute"``: it re-enters the queue
     head and re-reads its prompt plus the tokens it generated) or swapped to host memory
     (``preempt="swap"``: restored into a lane of the same Tier-2 shard, resuming at its saved
-    position).  ``order="shortest"`` admits the shortest prompts first.
+    position).  ``order="shortest"`` admits the shortest prompts first.  ``chunk > 1`` (an
+    Engine(prefill=True)) is chunked prefill: the idle lanes of a batch's shard carry up
+    to chunk - 1 further prompt tokens of a request still reading its prompt, at consecutive
+    positions of that request's slot, so a prompt of n tokens needs as few as ceil(n / chunk)
+    steps when lanes are free.
 
     Tier split: every rank runs the same dispatcher over the same requests (SPMD); decisions depend
     only on lengths, max_new and page counts.  Tier-2 ranks apply their shard's KV actions;
@@ -434,12 +440,16 @@ class ContinuousDispatcher:
 
     PAGE = 64  # GH_KV_PAGE_POSITIONS
 
-    def __init__(self, engine, on_demand: bool = False, preempt: str = "recompute", order: str = "fifo"):
+    def __init__(self, engine, on_demand: bool = False, preempt: str = "recompute", order: str = "fifo",
+                 chunk: int = 1):
+        if chunk > 1 and not (isinstance(engine, Engine) and engine.prefill):
+            raise L.ValidationError(L.GH_EINVAL, "chunked prefill needs an Engine(prefill=True)")
         if preempt not in ("recompute", "swap"):
             raise ValueError(f"preempt must be 'recompute' or 'swap', not {preempt!r}")
         if order not in ("fifo", "shortest"):
             raise ValueError(f"order must be 'fifo' or 'shortest', not {order!r}")
         self.engine, self.on_demand, self.preempt, self.order = engine, on_demand, preempt, order
+        self.chunk = max(1, int(chunk))
         self.preemptions = 0
         self.stats = {}
 
@@ -454,7 +464,8 @@ class ContinuousDispatcher:
         on_demand = self.on_demand and eng.kv_pages > 0
         if not isinstance(eng, Engine):
             return self._run_host(requests, max_new, sampling, on_demand, per)
-        cfg = L.GhDispatchConfig(max_new, int(on_demand), int(self.preempt == "swap"), int(self.order == "shortest"))
+        cfg = L.GhDispatchConfig(max_new, int(on_demand), int(self.preempt == "swap"), int(self.order == "shortest"),
+                                 self.chunk)
         h = C.c_void_p()
         L.check(L.lib().gh_dispatcher_create(eng.h, C.byref(cfg), C.byref(h)))
         try:

@@ -208,9 +208,10 @@ def test_on_demand_spmd_decisions_agree_across_ranks(preempt):
     assert swaps > 0 if preempt == "swap" else swaps == 0
 
 
+@pytest.mark.parametrize("chunk", [1, 4])
 @pytest.mark.parametrize("lag", [1, 3])
 @pytest.mark.parametrize("on_demand,preempt", [(False, "recompute"), (True, "recompute"), (True, "swap")])
-def test_scheduler_inflight_shards_lagged_tokens(on_demand, preempt, lag):
+def test_scheduler_inflight_shards_lagged_tokens(on_demand, preempt, lag, chunk):
     """The native scheduler (gh_sched) over IF = 2 in-flight batches x B = 5 lanes split into K' = 2
     Tier-2 shards with their own page pools, its tokens resolved `lag` steps late: every request's
     tokens equal decoding it alone, every attended position is mapped on the lane's own shard,
@@ -218,7 +219,7 @@ def test_scheduler_inflight_shards_lagged_tokens(on_demand, preempt, lag):
     from paper_2501_11779_b200.stages import Scheduler
     IF, B, kp, pages, max_new = 2, 5, 2, 9, 70
     reqs = _requests(14, seed=11)
-    sch = Scheduler(B, max_new, IF, kp, pages, 0, on_demand, preempt)
+    sch = Scheduler(B, max_new, IF, kp, pages, 0, on_demand, preempt, chunk=chunk)
     ids = [sch.submit(r) for r in reqs]
     lanes = IF * B
     shard = lambda lane: 0 if lane % B < 3 else 1  # noqa: E731  (shard_plan(5, 2) = 3 + 2 rows)
@@ -249,13 +250,20 @@ def test_scheduler_inflight_shards_lagged_tokens(on_demand, preempt, lag):
                 sch.resolve(pending.pop(0))
             continue
         nxt = np.zeros(lanes, np.int32)
+        rows = []
         for lane in range(lanes):
-            src, tok, p = (int(v) for v in ins[lane])
+            src, tok, p, home = (int(v) for v in ins[lane])
+            # a row carries only a prompt token of a lane of its own in-flight batch and shard
+            assert home // B == lane // B and shard(home) == shard(lane)
+            if home != lane:
+                assert chunk > 1 and src == Scheduler.SRC_HOST and ins[home][0] == Scheduler.SRC_HOST
             if src == Scheduler.SRC_DEVICE:
                 tok = int(last[lane])
-            assert mapped[lane] * PAGE >= p + 1, "attended position not mapped"
-            hist[lane][p] = tok
-            nxt[lane] = _next([hist[lane][i] for i in range(p + 1)])
+            assert mapped[home] * PAGE >= p + 1, "attended position not mapped"
+            hist[home][p] = tok
+            rows.append((lane, home, p))
+        for lane, home, p in rows:  # a prefill-row engine appends every row before attention
+            nxt[lane] = _next([hist[home][i] for i in range(p + 1)])
         last = nxt
         sch.commit()
         pending.append(nxt.copy())
@@ -280,3 +288,40 @@ def test_per_request_max_new(on_demand):
     got, _ = ContinuousDispatcher(eng, on_demand=on_demand).run(reqs, per)
     for r, n, g in zip(reqs, per, got):
         assert g.tolist() == _alone(r.tolist(), n)
+
+
+def test_chunked_prefill_fills_idle_lanes():
+    """Chunked prefill: with fewer requests than lanes, idle lanes carry further prompt
+    tokens of the requests still reading their prompts, so the run takes fewer steps; tokens are
+    unchanged (checked against decoding alone, as above)."""
+    from paper_2501_11779_b200.stages import Scheduler
+    rng = np.random.default_rng(3)
+    reqs = [rng.integers(0, 1000, n).astype(np.int32) for n in (40, 33, 9, 64)]
+    B, IF, kp, max_new = 8, 2, 2, 6
+    steps = {}
+    for chunk in (1, 8):
+        sch = Scheduler(B, max_new, IF, kp, chunk=chunk)
+        ids = [sch.submit(r) for r in reqs]
+        hist = [dict() for _ in range(IF * B)]
+        widest = 0
+        while not sch.done:
+            ins, _ = sch.plan()
+            nxt = np.zeros(IF * B, np.int32)
+            for lane in range(IF * B):
+                src, tok, p, home = (int(v) for v in ins[lane])
+                if src == Scheduler.SRC_DEVICE:
+                    tok = int(last[lane])
+                hist[home][p] = tok
+            for lane in range(IF * B):
+                p, home = int(ins[lane][2]), int(ins[lane][3])
+                nxt[lane] = _next([hist[home][i] for i in range(p + 1)])
+            widest = max(widest, max(int(np.sum(ins[:, 3] == h)) for h in range(IF * B)))
+            last = nxt
+            sch.commit()
+            sch.resolve(nxt)
+        for r, i in zip(reqs, ids):
+            assert sch.result(i).tolist() == _alone(r.tolist(), max_new)
+        steps[chunk] = sch.stats()["steps"]
+        assert widest == (1 if chunk == 1 else 4)  # 4 lanes per (batch, shard): 1 request + 3 idle
+        sch.close()
+    assert steps[8] < steps[1] / 2, steps

@@ -189,7 +189,7 @@ def paged_requests():
     return [rng.integers(0, PSPEC.vocab_size, size=n, dtype=np.int32) for n in PLENS]
 
 
-def worker_paged(rank, world, port, q, on_demand=False, preempt="recompute", IF=1):
+def worker_paged(rank, world, port, q, on_demand=False, preempt="recompute", IF=1, chunk=1):
     import torch
     import torch.distributed as dist
     from paper_2501_11779_b200.stages import Comm, ContinuousDispatcher, Engine
@@ -198,9 +198,11 @@ def worker_paged(rank, world, port, q, on_demand=False, preempt="recompute", IF=
     obj = [Comm.unique_ids(1) if rank == 0 else None]
     dist.broadcast_object_list(obj, src=0)
     comm = Comm(obj[0], world, rank, rank)
-    eng = Engine(PSPEC, batch=PB, inflight=IF, device=rank, use_graph=False, comm=comm, kv_pages=8 * IF)
+    eng = Engine(PSPEC, batch=PB, inflight=IF, device=rank, use_graph=False, comm=comm, kv_pages=8 * IF,
+                 prefill=chunk > 1)
     try:
-        out, steps = ContinuousDispatcher(eng, on_demand=on_demand, preempt=preempt).run(paged_requests(), PNEW)
+        out, steps = ContinuousDispatcher(eng, on_demand=on_demand, preempt=preempt, chunk=chunk).run(
+            paged_requests(), PNEW)
     except Exception as e:  # every rank takes the same decisions: report instead of hanging
         out, steps = repr(e), -1
     eng.close()
@@ -235,6 +237,29 @@ def test_continuous_batching_paged_tier_split(world, on_demand, preempt, IF):
         assert np.array_equal(w, g)
     if world == 2 and not on_demand and IF == 1:
         assert steps > ref_steps  # one Tier-2 pool of 8 pages for 6 lanes: requests waited
+
+
+@pytest.mark.skipif(n_gpus() < 2, reason="needs >= 2 GPUs")
+@pytest.mark.parametrize("world,on_demand", [(2, False), (3, True)])
+def test_native_chunked_prefill_tier_split(world, on_demand):
+    """Chunked prefill through the native dispatcher on the pipelined split (IF 2, peer
+    transport, paged Tier-2 pools): an idle row takes further prompt tokens of a request of its
+    own batch and shard, each Tier-2 rank installs its rows' slot tables stream-ordered.  Tokens
+    identical to the colocated engine; fewer steps than one prompt token per step."""
+    if n_gpus() < world:
+        pytest.skip(f"needs {world} GPUs")
+    from paper_2501_11779_b200.stages import ContinuousDispatcher, Engine
+    procs, q = spawn(worker_paged, world, (on_demand, "recompute", 2, 8))
+    got, steps = collect(procs, q, 1, 300)[0]
+    assert steps >= 0, got
+    procs, q = spawn(worker_paged, world, (on_demand, "recompute", 2, 1))
+    _, steps_lane = collect(procs, q, 1, 300)[0]
+    ref = Engine(PSPEC, batch=PB, use_graph=False)
+    want, _ = ContinuousDispatcher(ref).run(paged_requests(), PNEW)
+    ref.close()
+    for w, g in zip(want, got):
+        assert np.array_equal(w, g)
+    assert steps < steps_lane, (steps, steps_lane)
 
 
 def worker_mixed(rank, world, port, q, kv_pages=0):

@@ -1,5 +1,7 @@
 """Chunked prefill mixed with decode vs one token per lane per step, 7B shape, one
-B200, colocated, through the public dispatchers (host tokens in / out every step, wall clock).
+B200, colocated, through the public dispatchers (wall clock): one token per lane per step
+(ContinuousDispatcher, native), the Python pool-model MixedDispatcher (host tokens in / out every
+step), and the native dispatcher's chunked prefill into idle lanes.
 
   python tools/prefill_bench.py [--requests 64] [--prompt 256 512] [--new 32] [--rows 256] [--chunk 64]
 
@@ -51,6 +53,11 @@ eng = Engine(spec, batch=a.requests)
 lane = run("one_token_per_lane", eng, ContinuousDispatcher(eng))
 eng = Engine(spec, batch=a.rows, n_slots=a.requests + 1, prefill=True)
 mixed = run(f"mixed_rows{a.rows}_chunk{a.chunk}", eng, MixedDispatcher(eng, chunk=a.chunk))
+# the native dispatcher's chunked prefill: rows = lanes (a paged arena: an idle lane holds one page),
+# idle lanes carry prompt tokens of requests still reading their prompts, stream-ordered inputs
+pages = a.requests * -(-(a.prompt[1] + a.new - 1) // 64) + a.rows
+eng = Engine(spec, batch=a.rows, prefill=True, kv_pages=pages)
+native = run(f"native_lanes{a.rows}_chunk{a.chunk}", eng, ContinuousDispatcher(eng, chunk=a.chunk))
 # (token parity at equal row counts is tests/test_gpu_prefill.py; here the row counts differ, so
 # the bf16 GEMM plans and roundings differ and greedy continuations of random weights may too)
 print(json.dumps(res))
