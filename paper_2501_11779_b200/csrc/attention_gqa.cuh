@@ -690,7 +690,7 @@ __global__ void __launch_bounds__(GqaTcCfg<G>::kThreads, 1)
       const int np = max(0, min(C::kTpos, L - c * C::kTpos));
       if (c > 0) mbar_wait(&full[s], (it / C::kStages) & 1);
       const uint32_t st = smem_u32(smem + s * C::kStageBytes);
-      if (cw * 8 < np) {
+      if (cw * 8 < np && !(a.flags & 1)) {  // (flags & 1: diagnostics, K / V streaming only)
         // ---- S = Q Kᵀ for positions 8cw..8cw+7 (B fragments by ldmatrix from the swizzled boxes)
         float sacc[4] = {0.f, 0.f, 0.f, 0.f};
         const int prow = cw * 8 + (lane & 7);          // position row this lane addresses
