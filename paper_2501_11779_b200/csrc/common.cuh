@@ -116,16 +116,9 @@ GH_DEV unsigned long long globaltimer() {
   return t;
 }
 GH_DEV uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
-GH_DEV int lane_id() { return threadIdx.x & 31; }
-GH_DEV int warp_id() { return threadIdx.x >> 5; }
 GH_DEV float warp_sum(float v) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-  return v;
-}
-GH_DEV float warp_max(float v) {
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
   return v;
 }
 GH_DEV bool elect_one() {
@@ -188,16 +181,6 @@ GH_DEV uint32_t mapa_shared(uint32_t saddr, uint32_t rank) {
 }
 // (volatile keeps it after the preceding mbarrier wait; no memory clobber so that a batch of
 // these loads can be issued back to back before their results are consumed)
-GH_DEV float4 ld_dsmem_f4(uint32_t caddr) {
-  float4 v;
-  asm volatile("ld.shared::cluster.v4.f32 {%0, %1, %2, %3}, [%4];"
-               : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(caddr));
-  return v;
-}
-// arrive (release, cluster scope) on an mbarrier that lives in another CTA of the cluster
-GH_DEV void mbar_arrive_cluster(uint32_t caddr) {
-  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(caddr) : "memory");
-}
 GH_DEV void mbar_wait_cluster(uint64_t* bar, uint32_t parity) {
   uint32_t addr = smem_u32(bar);
   asm volatile(
@@ -226,11 +209,8 @@ GH_DEV void flag_wait(const unsigned int* flag, unsigned int target) {
   }
 }
 
-// System-scope flags between GPUs (NVLink peer mappings): release store into a peer's flag word,
-// acquire spin on a local flag word that peers write.
-GH_DEV void flag_store_release_sys(unsigned int* flag, unsigned int v) {
-  asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(flag), "r"(v) : "memory");
-}
+// System-scope flag between GPUs: acquire spin on a local flag word that a peer's copy engine
+// (cuStreamWriteValue32 after its copy) advances to a sequence number.
 GH_DEV void flag_wait_sys(const unsigned int* flag, unsigned int target) {
   unsigned int v;
   for (;;) {
