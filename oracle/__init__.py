@@ -4,8 +4,9 @@ Only tests/, __graft_entry__.smoke() and bench.py (cpu_baseline leg and --impl r
 import this package, and only as the checker / the CPU baseline, never as the measured product.
 
 * ``Oracle`` wraps liboracle.so (oracle.c): the CPU fp32 restatement of the decode step.
-  Parity with upstream decode code is UNPINNED (the reference has none; see oracle.c header);
-  the restatement is pinned on the reference accounting goldens and on tests/golden/.
+  The reference has no decode code to pin against (see oracle.c header); the restatement is
+  pinned on the reference accounting goldens, on transformers' LlamaForCausalLM holding the same
+  weights (hf_llama.py: identical C1 greedy tokens), and on tests/golden/.
 * ``Ref`` wraps _ref/libtierplan_ref.so: the unmodified reference library compiled from
   /root/reference/proj/src by oracle/Makefile, plus the extern "C" shim ref_shim.cpp.
 """

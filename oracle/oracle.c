@@ -5,10 +5,12 @@
  * cpu_baseline / --impl reference legs as the checker; never part of the product path.
  *
  * Parity status: the reference repository (/root/reference/proj, "tierplan") contains no
- * decode arithmetic, so logits/tokens are "parity unpinned" against
- * upstream code: this file restates the paper's operations and is pinned (a) on the reference's
- * accounting goldens through oracle/ref_shim.cpp + the compiled reference sources and (b) on
- * committed golden vectors (tests/golden/) that it generated itself.
+ * decode arithmetic, so there is no upstream decode code to pin against.
+ * This file restates the paper's operations and is pinned (a) on the reference's accounting
+ * goldens through oracle/ref_shim.cpp + the compiled reference sources, (b) on Hugging Face
+ * transformers' LlamaForCausalLM (transformers 5.5.0, fp32) holding the same weights
+ * (oracle/hf_llama.py, tests/test_oracle_hf.py, tests/golden/hf_llama_c1.npz: the 512 C1 greedy
+ * tokens are identical), and (c) on committed golden vectors (tests/golden/).
  *
  * What it restates (P = /root/reference/PAPER.md):
  *   F1 (Table 8 rows P:875-877): RMSNorm -> x*[W_q|W_k|W_v] -> RoPE            or_pre

@@ -43,6 +43,16 @@ def test_c1_greedy_tokens_bit_exact(c1_run):
     assert r["gen"].shape == (4, 128)
 
 
+def test_c1_tokens_equal_transformers_llama(c1_run):
+    """The same 512 tokens from Hugging Face transformers' LlamaForCausalLM holding these weights
+    (tests/golden/hf_llama_c1.npz, tests/test_oracle_hf.py): an implementation independent of
+    the oracle."""
+    from pathlib import Path
+    hf = np.load(Path(__file__).resolve().parent / "golden" / "hf_llama_c1.npz")
+    assert np.array_equal(hf["prompts"], c1_run["prompts"])
+    assert np.array_equal(c1_run["gen"], hf["tokens"])
+
+
 def test_c1_logits_within_tolerance(c1_run):
     r = c1_run
     err = np.abs(r["lg"] - r["rlg"]).max()
