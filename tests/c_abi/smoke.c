@@ -5,6 +5,8 @@
  *   smoke cpu <csv_path>       accounting calls (model.cpp:40-77, netmodel.cpp:18-24,
  *                              optimizer.cpp:116-192) and the profile CSV producer
  *                              (profiles.hpp:66-69); prints one JSON line.  No GPU needed.
+ *   smoke sched                the dispatcher's decision logic (gh_sched_*) with chunked prefill
+ *                              against a toy context-hash model; prints one JSON line.  No GPU.
  *   smoke gpu <prompts.txt>    the INTEGRATION.md per-layer call sequence (gh_tier1_embed ->
  *                              {gh_tier1_pre -> gh_tier2_attend -> gh_tier1_post} x N ->
  *                              gh_tier1_classify) for BASELINE configs[0] (C1: tiny 288x6 fp32,
@@ -137,9 +139,81 @@ static int run_gpu(const char* prompts_path) {
   return 0;
 }
 
+/* The dispatcher's decision logic (gh_sched_*, P:471-479 / P:1117) driven from C against a toy
+ * model whose next token hashes the whole context of the row's slot: IF 2 x B 6 lanes, 2 Tier-2
+ * shards, 9 requests, with and without chunked prefill.  Every request's tokens must equal
+ * decoding it alone; prints {"steps": [chunk 1, chunk 4], "equal": 0/1}. */
+enum { SB = 6, SIF = 2, SLANES = SB * SIF, SMAXPOS = 256, SNEW = 7, SREQ = 9 };
+static int32_t toy_next(const int32_t* ctx, int n) {
+  uint32_t h = 2166136261u;
+  for (int i = 0; i < n; ++i) h = (h ^ (uint32_t)ctx[i]) * 16777619u;
+  return (int32_t)(h % 1000u);
+}
+static int sched_run(uint32_t chunk, const int32_t prompts[SREQ][40], const int lens[SREQ], uint64_t* steps,
+                     int32_t out[SREQ][SNEW]) {
+  gh_sched_config c = {SB, SIF, 2, 0, SMAXPOS, SNEW, 0, 0, 0, chunk};
+  gh_sched* s = NULL;
+  CK(gh_sched_create(&c, &s));
+  uint64_t id[SREQ];
+  for (int r = 0; r < SREQ; ++r) CK(gh_sched_submit(s, prompts[r], (uint32_t)lens[r], 0.f, 0, 0, &id[r]));
+  static int32_t hist[SLANES][SMAXPOS];
+  int32_t last[SLANES] = {0}, next[SLANES];
+  gh_lane_input in[SLANES];
+  gh_kv_action acts[64];
+  uint32_t nacts = 0;
+  while (!gh_sched_done(s)) {
+    CK(gh_sched_plan(s, in, acts, 64, &nacts));
+    for (int l = 0; l < SLANES; ++l) {  /* a prefill-row engine appends every row before attention */
+      const int32_t tok = in[l].src == 2 ? last[l] : in[l].tok;
+      hist[in[l].home][in[l].pos] = tok;
+    }
+    for (int l = 0; l < SLANES; ++l) next[l] = toy_next(hist[in[l].home], in[l].pos + 1);
+    memcpy(last, next, sizeof last);
+    CK(gh_sched_commit(s));
+    CK(gh_sched_resolve(s, next));
+  }
+  gh_dispatch_stats st;
+  CK(gh_sched_stats(s, &st));
+  *steps = st.steps;
+  for (int r = 0; r < SREQ; ++r) {
+    uint32_t n = 0;
+    CK(gh_sched_result(s, id[r], out[r], SNEW, &n));
+    if (n != SNEW) return 1;
+  }
+  CK(gh_sched_destroy(s));
+  return 0;
+}
+static int run_sched(void) {
+  int32_t prompts[SREQ][40];
+  int lens[SREQ];
+  uint32_t x = 12345u;
+  for (int r = 0; r < SREQ; ++r) {
+    lens[r] = 1 + (r * 7) % 37;
+    for (int i = 0; i < lens[r]; ++i) prompts[r][i] = (int32_t)((x = x * 1103515245u + 12345u) >> 16) % 1000;
+  }
+  int equal = 1;
+  uint64_t steps[2];
+  const uint32_t chunks[2] = {1, 4};
+  for (int k = 0; k < 2; ++k) {
+    int32_t out[SREQ][SNEW];
+    if (sched_run(chunks[k], prompts, lens, &steps[k], out)) return 3;
+    for (int r = 0; r < SREQ; ++r) {  /* decoding the request alone */
+      int32_t ctx[40 + SNEW];
+      memcpy(ctx, prompts[r], sizeof(int32_t) * (size_t)lens[r]);
+      for (int i = 0; i < SNEW; ++i) {
+        ctx[lens[r] + i] = toy_next(ctx, lens[r] + i);
+        equal &= ctx[lens[r] + i] == out[r][i];
+      }
+    }
+  }
+  printf("{\"steps\": [%llu, %llu], \"equal\": %d}\n", (unsigned long long)steps[0], (unsigned long long)steps[1], equal);
+  return 0;
+}
+
 int main(int argc, char** argv) {
+  if (argc == 2 && strcmp(argv[1], "sched") == 0) return run_sched();
   if (argc == 3 && strcmp(argv[1], "cpu") == 0) return run_cpu(argv[2]);
   if (argc == 3 && strcmp(argv[1], "gpu") == 0) return run_gpu(argv[2]);
-  fprintf(stderr, "usage: %s cpu <csv> | gpu <prompts.txt>\n", argv[0]);
+  fprintf(stderr, "usage: %s cpu <csv> | gpu <prompts.txt> | sched\n", argv[0]);
   return 1;
 }

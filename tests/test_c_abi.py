@@ -54,6 +54,15 @@ def test_c_consumer_accounting_and_csv(smoke_bin, tmp_path):
     assert len(lines) == 7 and lines[1].startswith("b200,nonattention,512,1,")
 
 
+def test_c_consumer_sched_chunked_prefill(smoke_bin):
+    """gh_sched_* from C: every request equals decoding it alone, with and without chunked
+    prefill, and chunking takes fewer steps when lanes are idle."""
+    r = subprocess.run([str(smoke_bin), "sched"], capture_output=True, text=True, check=True)
+    d = json.loads(r.stdout)
+    assert d["equal"] == 1
+    assert d["steps"][1] < d["steps"][0], d
+
+
 @pytest.mark.gpu
 def test_c_consumer_c1_tokens_bit_exact(smoke_bin, tmp_path, need_gpu):
     g = np.load(ROOT / "tests" / "golden" / "oracle_c1.npz")
