@@ -256,6 +256,17 @@ def if_gh_from_profiles(spec, t1_batch: int, shard: int, ctx: int) -> int:
     return max(2, 1 + math.ceil((t_att + t_rt) / t_noatt))
 
 
+def auto_tier1(args, world: int) -> int:
+    """Tier-1 pipeline spans of the default C2 split: one Tier-1 GPU up to 4 GPUs; from 8 GPUs on,
+    two layer spans, each with (N - 2) / 2 Tier-2 GPUs (the reference's config-5 topology, P:455,
+    optimizer.cpp:116-123).  One Tier-1 GPU for 7 Tier-2 GPUs would stream the weights for a batch
+    of 448 prompts, where the GEMMs run at 233 us per layer (profiles/r02_gemm_timelines.txt); two
+    spans at 192 prompts each share the layers (measured at 4 GPUs, r02_bench_n4_spans.json)."""
+    if (args.config or "C2") != "C2" or args.tier1_tp > 1 or world < 8 or (world - 2) % 2:
+        return 1
+    return 2
+
+
 def workload(args, world):
     import paper_2501_11779_b200 as gh
     cfg = args.config or "C2"
@@ -286,6 +297,8 @@ def workload(args, world):
     if cfg == "C2":  # weak scaling of the N=1 workload: 64 prompts per Tier-2 GPU per in-flight batch
         shard = args.shard or c["batch"]
         IF = args.inflight or if_gh_from_profiles(spec, shard * kp, shard, ctx)
+        if n1 > 1 and not args.inflight:  # one group of batches per span in flight (split_step_peer)
+            IF = n1 * max(3, IF)
         return dict(name="C2-split", spec=spec, ctx=ctx, batch=shard * kp, requested=shard * kp * IF,
                     inflight=IF, shard=shard, kp=kp,
                     admitted_slots=gh.two_tier_context_slots(spec, 1, kp, 179 * GiB, ctx))
@@ -612,8 +625,9 @@ def main():
     ap.add_argument("--config", default=None, choices=[None, "C2", "C3", "C4", "C5"])
     ap.add_argument("--cpu-threads", type=int, default=0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--tier1", type=int, default=1,
-                    help="tier split: Tier-1 pipeline stages (layer spans, each with its own Tier-2 GPUs)")
+    ap.add_argument("--tier1", type=int, default=0,
+                    help="tier split: Tier-1 pipeline stages (layer spans, each with its own Tier-2 GPUs); "
+                         "0 = auto (C2: 2 spans from 8 GPUs on, else 1)")
     ap.add_argument("--tier1-tp", type=int, default=1,
                     help="tier split: Tier-1 tensor parallelism over this many GPUs (SURVEY 8f-3); the rest are Tier-2")
     ap.add_argument("--shard", type=int, default=0,
@@ -631,6 +645,7 @@ def main():
     args.warmup = max(args.warmup, 3)
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
+    args.tier1 = args.tier1 or auto_tier1(args, max(world, args.gpus if world == 1 else world))
     rank = int(os.environ.get("RANK", "0"))
     wl = workload(args, max(world, args.gpus if world == 1 else world))
     spec = wl["spec"]

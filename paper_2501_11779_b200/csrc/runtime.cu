@@ -1183,6 +1183,10 @@ struct gh_engine {
     cudaStream_t stream = nullptr;
     cudaEvent_t done = nullptr;
     cudaGraphExec_t graph = nullptr;
+    // first span of Tier-1 pipeline spans: gh_engine_advance is applied when the batch's next step
+    // starts (after its tokens came back from the last span), not at the end of this step
+    bool adv_pending = false;
+    int adv_inc = 0;
   };
   std::vector<Batch> batches;
   bool keep_logits = false;               // classifier runs also store the logits (gh_engine_keep_logits)
@@ -1453,6 +1457,11 @@ gh_status gh_engine_advance(gh_engine* e, uint32_t ib, int inc, void* stream) {
   if (e->role == 2) return fail(GH_EINVAL, "Tier-2 ranks hold no token state");
   auto& b = e->batches[ib];
   if (e->role == 1 && e->span > 0) return GH_OK;  // later spans take tokens / positions from the hand-off
+  if (e->role == 1 && e->n1 > 1 && e->peer.on) {  // deferred to the batch's next step (split_step_peer)
+    b.adv_pending = true;
+    b.adv_inc += inc;
+    return GH_OK;
+  }
   GH_CUDA(cudaSetDevice(e->cfg.device));
   GH_TRY(peer_wait_tokens(e, (int)ib, (cudaStream_t)stream));  // first span: the last span's next tokens
   GH_CUDA(launch_advance(b.tok, b.next, b.pos, (int)e->cfg.batch, inc, (cudaStream_t)stream));
@@ -1941,10 +1950,24 @@ static gh_status split_step_peer(gh_engine* e, cudaStream_t st) {
   static const bool nowait = getenv("GH_SPLIT_NOWAIT") != nullptr;
   static const bool nosend = nowait && getenv("GH_SPLIT_NOSEND") != nullptr;  // + no fwd copies
   static const bool memop_wait = getenv("GH_SPLIT_MEMOP_WAIT") != nullptr;
+  // Tier-1 pipeline spans: the in-flight batches are cut into min(IF, spans) groups processed one
+  // after another (each group's batches interleaved per layer, so the Tier-2 round trips overlap),
+  // so that span s works on group g while span s+1 works on group g-1 -- with every batch's
+  // layers interleaved across all IF batches, span s+1 could only start at the end of span s's
+  // step and the spans would run one at a time.  One span: a single group (unchanged order).
+  const int ng = e->n1 > 1 ? std::min(nb, e->n1) : 1;
   if (e->role == 1) {
     const bool first = e->span == 0, last = e->span == e->n1 - 1;
-    for (int ib = 0; ib < nb; ++ib) {
+    for (int gi = 0; gi < ng; ++gi) {
+    const int gb0 = gi * nb / ng, gb1 = (gi + 1) * nb / ng;
+    for (int ib = gb0; ib < gb1; ++ib) {
       auto& b = e->batches[ib];
+      if (first && b.adv_pending) {  // the tokens of this batch's previous step (gh_engine_advance)
+        GH_TRY(peer_wait_tokens(e, ib, st));
+        GH_CUDA(launch_advance(b.tok, b.next, b.pos, (int)e->cfg.batch, b.adv_inc, st));
+        b.adv_pending = false;
+        b.adv_inc = 0;
+      }
       if (first) {
         GH_TRY(act_embed(e, b, st));
       } else {
@@ -1960,7 +1983,7 @@ static gh_status split_step_peer(gh_engine* e, cudaStream_t st) {
       GH_TRY(peer_send_fwd(e, ib, true, st));
     }
     for (int l = e->l0; l < e->l1; ++l)
-      for (int ib = 0; ib < nb; ++ib) {
+      for (int ib = gb0; ib < gb1; ++ib) {
         auto& b = e->batches[ib];
         // every shard of the attention output has landed: the W_o GEMM's producers poll the flag
         // words themselves (weights stream meanwhile, and the launch keeps its programmatic overlap
@@ -1980,12 +2003,14 @@ static gh_status split_step_peer(gh_engine* e, cudaStream_t st) {
           GH_TRY(peer_send_next_span(e, ib, st));
         }
       }
+    }
   } else {
     const int tp = e->tp;
     const size_t bwd_row = (size_t)e->sh.ld_bwd() / tp * e->sh.db;  // one head block of a row
     const int me = e->shard;
+    for (int gi = 0; gi < ng; ++gi)
     for (int l = e->l0; l < e->l1; ++l)
-      for (int ib = 0; ib < nb; ++ib) {
+      for (int ib = gi * nb / ng; ib < (gi + 1) * nb / ng; ++ib) {
         auto& b = e->batches[ib];
         const uint32_t sq = ++P.seq[ib];
         for (int r = 0; r < tp && !nowait; ++r)  // every Tier-1 rank's head block has landed
@@ -2076,6 +2101,8 @@ gh_status gh_engine_step_all_host(gh_engine* e, const int32_t* tok_host, const i
   if (e->role != 2 && e->span == 0) {
     if (!tok_host || !pos_host) return fail(GH_EINVAL, "host token/pos buffers required");
     for (size_t ib = 0; ib < e->batches.size(); ++ib) {
+      e->batches[ib].adv_pending = false;  // host inputs replace a deferred advance
+      e->batches[ib].adv_inc = 0;
       GH_CUDA(cudaMemcpyAsync(e->batches[ib].tok, tok_host + ib * R, R * 4, cudaMemcpyHostToDevice, st));
       GH_CUDA(cudaMemcpyAsync(e->batches[ib].pos, pos_host + ib * R, R * 4, cudaMemcpyHostToDevice, st));
     }

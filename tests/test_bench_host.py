@@ -79,3 +79,21 @@ def test_cpu_batch_respects_host_memory(bench, monkeypatch):
     B = bench.cpu_batch(spec, 64, 2048)
     assert 1 <= B < 64
     assert gh.weights_bytes(spec) + B * gh.kv_bytes_per_prompt(spec, 2048) <= 0.7 * (64 << 30)
+
+
+def test_auto_tier1_spans():
+    """The default C2 split uses two Tier-1 layer spans from 8 GPUs on (config-5 topology), one
+    Tier-1 GPU below that and for the other configs / tensor parallelism; the span count divides
+    the GPUs, and with spans the in-flight batches form one group per span."""
+    import argparse
+    import bench
+    def a(config=None, tp=1):
+        return argparse.Namespace(config=config, paged=False, tier1=0, tier1_tp=tp, shard=0, inflight=0,
+                                  cpu_profiles="")
+    assert [bench.auto_tier1(a(), w) for w in (1, 2, 4, 8)] == [1, 1, 1, 2]
+    assert bench.auto_tier1(a("C3"), 8) == 1 and bench.auto_tier1(a(tp=2), 8) == 1
+    args = a()
+    args.tier1 = bench.auto_tier1(args, 8)
+    wl = bench.workload(args, 8)
+    assert (wl["kp"], wl["batch"], wl["shard"]) == (3, 192, 64)
+    assert wl["inflight"] % 2 == 0 and wl["inflight"] >= 6

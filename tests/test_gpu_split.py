@@ -167,11 +167,14 @@ def worker_pp(rank, world, port, q, IF, n1):
 
 
 @pytest.mark.skipif(n_gpus() < 4, reason="needs >= 4 GPUs")
-def test_tier1_pipeline_stages_match_colocated():
+@pytest.mark.parametrize("IF", [2, 3, 4])
+def test_tier1_pipeline_stages_match_colocated(IF):
     """SURVEY 8(e) config-5 topology at small scale: 2 Tier-1 spans (layers split by
-    layer_spans), each with a dedicated Tier-2 rank; tokens identical to the colocated engine."""
+    layer_spans), each with a dedicated Tier-2 rank; the in-flight batches run as min(IF, spans)
+    groups so the spans work on different groups at once, and the first span applies
+    gh_engine_advance when a batch's next step starts.  Tokens identical to the colocated engine."""
     from paper_2501_11779_b200.stages import Engine
-    world, IF, n1 = 4, 2, 2
+    world, n1 = 4, 2
     procs, q = spawn(worker_pp, world, (IF, n1))
     got = collect(procs, q, 1, 300)[0]
     ref = run_all(Engine(SPEC, batch=B, inflight=IF, use_graph=False), IF)
