@@ -302,7 +302,9 @@ gh_status gh_engine_step_all_host(gh_engine* e, const int32_t* tok_host, const i
 gh_status gh_engine_io(gh_engine* e, uint32_t ib, int32_t** tok, int32_t** pos,
                        uint32_t** slot, int32_t** next);
 /* Device-side batch-state update for batch ib: tok <- next, pos += pos_increment (pos_increment
- * 0 keeps the context length fixed, the steady-state benchmark mode). Tier-1 / colocated only. */
+ * 0 keeps the context length fixed, the steady-state benchmark mode). Tier-1 / colocated only.
+ * On the first of several Tier-1 pipeline spans it is applied when the batch's next step starts
+ * (its tokens come back from the last span); host inputs of gh_engine_step_all_host replace it. */
 gh_status gh_engine_advance(gh_engine* e, uint32_t ib, int pos_increment, void* stream);
 /* Copy the next tokens of in-flight batch ib to host (synchronous; Tier-1 / colocated only). */
 gh_status gh_engine_read_next(gh_engine* e, uint32_t ib, int32_t* next_host);
