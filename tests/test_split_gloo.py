@@ -183,6 +183,120 @@ def test_tier1_pipeline_protocol_matches_colocated(world, B):
     assert np.array_equal(slg, lg)
 
 
+def worker_pp_groups(rank, world, port, out_q, B, IF):
+    """Tier-1 pipeline spans with IF in-flight batches in the engine's order (split_step_peer):
+    the batches form min(IF, spans) groups processed one after another on every rank, each
+    group's batches interleaved per layer; a span hands a batch on after its last layer, the
+    last span returns the batch's next tokens, and the first span takes them when that batch's
+    next step starts (the deferred gh_engine_advance).  Sends are non-blocking, like the copy
+    engines of the peer transport; every receive blocks, so an ordering that could deadlock
+    the GPU engine's flag waits hangs here."""
+    init_rank(rank, world, port)
+    from oracle import Oracle
+    n1 = 2
+    kp = (world - n1) // n1
+    ng = min(IF, n1)
+    groups = [range(g * IF // ng, (g + 1) * IF // ng) for g in range(ng)]
+    off, cnt = gh.shard_plan(B, kp)
+    spans = gh.layer_spans(SPEC.n_layers, n1)
+    lo = [sum(spans[:s]) for s in range(n1)]
+    prompts = np.random.default_rng(2).integers(0, SPEC.vocab_size, size=(IF * B, 2), dtype=np.int32)
+    D, Dkv = SPEC.d_model, SPEC.d_kv
+    pending = []
+
+    def isend(a, dst):
+        t = torch.from_numpy(np.ascontiguousarray(a))
+        pending.append((dist.isend(t, dst=dst), t))  # the tensor stays alive until the send is done
+
+    def recv(shape, dtype, src):
+        t = torch.zeros(shape, dtype=dtype)
+        dist.recv(t, src=src)
+        return t.numpy()
+
+    if rank < n1:
+        sp = rank
+        ora = Oracle(SPEC, seed=SEED, n_slots=1)
+        bufs = [ora.buffers(B) for _ in range(IF)]
+        tok = [prompts[ib * B:(ib + 1) * B, 0].copy() for ib in range(IF)]
+        pos = [None] * IF
+        out = [[] for _ in range(IF)]
+        for t in range(1 + STEPS):
+            for grp in groups:
+                for ib in grp:
+                    x, fwd, _ = bufs[ib]
+                    if sp == 0:
+                        if t >= 1:  # this batch's tokens of step t - 1 from the last span
+                            nt = recv(B, torch.int32, n1 - 1)
+                            tok[ib] = prompts[ib * B:(ib + 1) * B, 1].copy() if t == 1 else nt.copy()
+                        pos[ib] = np.full(B, t, np.int32)
+                        ora.embed(tok[ib], x)
+                    else:
+                        pos[ib] = recv(B, torch.int32, sp - 1).copy()
+                        x[:] = recv((B, D), torch.int16, sp - 1).view(np.uint16)
+                    ora.pre(lo[sp], x, pos[ib], fwd)
+                    for j in range(kp):  # positions + the first fwd of this batch to my shards
+                        isend(pos[ib][off[j]:off[j] + cnt[j]], n1 + sp * kp + j)
+                        isend(fwd[off[j]:off[j] + cnt[j]].view(np.int16), n1 + sp * kp + j)
+                for layer in range(lo[sp], lo[sp] + spans[sp]):
+                    for ib in grp:
+                        x, fwd, bwd = bufs[ib]
+                        for j in range(kp):
+                            bwd[off[j]:off[j] + cnt[j]] = recv((cnt[j], 2 * D), torch.int16, n1 + sp * kp + j).view(np.uint16)
+                        x2 = np.zeros_like(x)
+                        ora.post(layer, bwd, x2)
+                        x[:] = x2
+                        if layer + 1 < lo[sp] + spans[sp]:
+                            ora.pre(layer + 1, x, pos[ib], fwd)
+                            for j in range(kp):
+                                isend(fwd[off[j]:off[j] + cnt[j]].view(np.int16), n1 + sp * kp + j)
+                        elif sp + 1 < n1:
+                            isend(pos[ib], sp + 1)
+                            isend(x.view(np.int16), sp + 1)
+                        else:
+                            nxt, lg = ora.classify(x)
+                            if t >= 1:
+                                out[ib].append((nxt.copy(), lg.copy()))
+                            isend(nxt.astype(np.int32), 0)
+        if sp == 0:  # the last step's tokens (the next step would take them)
+            for grp in groups:
+                for ib in grp:
+                    recv(B, torch.int32, n1 - 1)
+        if sp == n1 - 1:
+            out_q.put([(np.stack([o[0] for o in out[ib]], 1), np.stack([o[1] for o in out[ib]], 1))
+                       for ib in range(IF)])
+    else:
+        sp, j = (rank - n1) // kp, (rank - n1) % kp
+        n = cnt[j]
+        ora = Oracle(SPEC, seed=SEED, n_slots=n * IF)  # slots ib * n + i: batch ib's prompts of my shard
+        pos = [None] * IF
+        for t in range(1 + STEPS):
+            for grp in groups:
+                for layer in range(lo[sp], lo[sp] + spans[sp]):
+                    for ib in grp:
+                        if layer == lo[sp]:
+                            pos[ib] = recv(n, torch.int32, sp).copy()
+                        fwd = recv((n, 2 * D + 2 * Dkv), torch.int16, sp).view(np.uint16).copy()
+                        bwd = np.zeros((n, 2 * D), np.uint16)
+                        ora.attend(layer, np.arange(ib * n, (ib + 1) * n, dtype=np.uint32), pos[ib], fwd, bwd)
+                        isend(bwd.view(np.int16), sp)
+    for r, _ in pending:
+        r.wait()
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,B,IF", [(4, B, 4), (8, 13, 6), (8, 13, 3)])
+def test_tier1_pipeline_groups_protocol(world, B, IF):
+    """The 8-GPU bench default (two Tier-1 spans, K' = 3 each, IF 6 in two groups) and uneven
+    groups (IF 3): every batch's tokens and logits equal the colocated oracle's."""
+    _, gen, lg = reference_tokens(IF * B)
+    procs, q = spawn(worker_pp_groups, world, (B, IF))
+    res = collect(procs, q, 1, 240)[0]
+    for ib in range(IF):
+        assert np.array_equal(res[ib][0], gen[ib * B:(ib + 1) * B])
+        assert np.array_equal(res[ib][1], lg[ib * B:(ib + 1) * B])
+
+
 def test_shard_plan_balanced():
     for batch, kp in ((1024, 7), (7, 3), (170, 1), (1190, 7)):
         off, cnt = gh.shard_plan(batch, kp)
